@@ -1,0 +1,890 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * Plain single-threaded fp64 CPU oracle of the SALE per-cycle update
+ * (arXiv 2209.01983; the scheme as written down in SURVEY.md §8(c), because
+ * the paper itself names the steps -- P:133 "SALE", "ideal gas EoS",
+ * P:181 "Lagrangian rezoning / Eulerian rezoning / Advection"
+ * "Calculate_density" -- but prints no discrete equation).  Each function
+ * below cites the §8(c) item it follows.  Loops are whole-mesh, one step at a
+ * time, in the order c.3 / c.4 lists them; no blocking or fusion.
+ *
+ * Parity status of each part: see DESIGN.md §4 (pins) -- "parity unpinned"
+ * items are listed there (absolute discretisation error beyond the Sedov
+ * radius/symmetry checks; long-time C1 behaviour without hourglass control).
+ *
+ * Compile: gcc -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------- */
+/* context                                                                    */
+/* ------------------------------------------------------------------------- */
+struct oracle_ctx {
+    oracle_params p;
+    int64_t nx, ny, nz;          /* cells */
+    int64_t NX, NY, NZ;          /* nodes = cells + 1 */
+    int64_t ncell, nnode;
+    /* state (c.1): node position and velocity, cell mass and specific energy */
+    double *x[3], *u[3];
+    double *m, *e;
+    /* target (initial) mesh x^T, node-wise (c.1, c.4 step 5) */
+    double *xT[3];
+    /* cycle scratch */
+    double *sig;                 /* sigma_K (c.3 step 3)              */
+    double *x1[3], *u1[3];       /* x', u' (c.3 step 6)               */
+    double *e1, *V1;             /* e', V' (c.3 step 7)               */
+    double *dm, *dE, *dP[3], *m2; /* Delta m, Delta E, Delta P, m'' (c.4 step 3) */
+    /* clock (c.3 step 8, c.5) */
+    double t, dt_prev;
+    int64_t cycle;
+    int32_t finished, poisoned;
+    int64_t err_cell;
+    char err[256];
+};
+
+static inline int64_t nid(const oracle_ctx* c, int64_t i, int64_t j, int64_t k)
+{
+    return i + c->NX * (j + c->NY * k);
+}
+static inline int64_t cid(const oracle_ctx* c, int64_t i, int64_t j, int64_t k)
+{
+    return i + c->nx * (j + c->ny * k);
+}
+
+/* ------------------------------------------------------------------------- */
+/* c.2 geometry primitives                                                    */
+/* ------------------------------------------------------------------------- */
+typedef struct { double A[3], Xb[3], s; } face_t;
+
+/* c.2: d1 = P2-P0, d2 = P3-P1; A = 0.5*(d1 x d2); Xbar = 0.25*(((P0+P1)+P2)+P3);
+ * s = (Xbx*Ax + Xby*Ay) + Xbz*Az. */
+static void face_geom(const double P0[3], const double P1[3], const double P2[3],
+                      const double P3[3], face_t* f)
+{
+    double d1[3], d2[3];
+    for (int a = 0; a < 3; ++a) {
+        d1[a] = P2[a] - P0[a];
+        d2[a] = P3[a] - P1[a];
+    }
+    f->A[0] = 0.5 * (d1[1] * d2[2] - d1[2] * d2[1]);
+    f->A[1] = 0.5 * (d1[2] * d2[0] - d1[0] * d2[2]);
+    f->A[2] = 0.5 * (d1[0] * d2[1] - d1[1] * d2[0]);
+    for (int a = 0; a < 3; ++a)
+        f->Xb[a] = 0.25 * (((P0[a] + P1[a]) + P2[a]) + P3[a]);
+    f->s = (f->Xb[0] * f->A[0] + f->Xb[1] * f->A[1]) + f->Xb[2] * f->A[2];
+}
+
+/* Hex-local node (a,b,c) has index (c*2+b)*2+a.  Faces in the order
+ * X0, X1, Y0, Y1, Z0, Z1, each with its canonical P0..P3 (c.2):
+ *   X(a): (a,0,0) (a,1,0) (a,1,1) (a,0,1)
+ *   Y(b): (0,b,0) (0,b,1) (1,b,1) (1,b,0)
+ *   Z(c): (0,0,c) (1,0,c) (1,1,c) (0,1,c)                                    */
+static const int FACE_NODES[6][4] = {
+    {0, 2, 6, 4}, {1, 3, 7, 5},   /* X0, X1 */
+    {0, 4, 5, 1}, {2, 6, 7, 3},   /* Y0, Y1 */
+    {0, 1, 3, 2}, {4, 5, 7, 6},   /* Z0, Z1 */
+};
+
+static void hex_faces(const double N[8][3], face_t F[6])
+{
+    for (int f = 0; f < 6; ++f)
+        face_geom(N[FACE_NODES[f][0]], N[FACE_NODES[f][1]], N[FACE_NODES[f][2]],
+                  N[FACE_NODES[f][3]], &F[f]);
+}
+
+/* c.2: V = (((((s(F+x) - s(F-x)) + s(F+y)) - s(F-y)) + s(F+z)) - s(F-z)) / 3.0 */
+static double hex_volume_from_faces(const face_t F[6])
+{
+    return (((((F[1].s - F[0].s) + F[3].s) - F[2].s) + F[5].s) - F[4].s) / 3.0;
+}
+
+/* c.2: corner vector of hex corner (a,b,c): C = ((A_x(a) + A_y(b)) + A_z(c)),
+ * A_x(1) = A(F+x), A_x(0) = -A(F-x), likewise y, z. */
+static void corner_vector(const face_t F[6], int a, int b, int c, double C[3])
+{
+    for (int q = 0; q < 3; ++q) {
+        double ax = a ? F[1].A[q] : -F[0].A[q];
+        double ay = b ? F[3].A[q] : -F[2].A[q];
+        double az = c ? F[5].A[q] : -F[4].A[q];
+        C[q] = (ax + ay) + az;
+    }
+}
+
+/* gather the 8 node positions of cell (i,j,k) from arrays X[3] */
+static void cell_nodes(const oracle_ctx* c, double* const X[3], int64_t i, int64_t j,
+                       int64_t k, double N[8][3])
+{
+    for (int cc = 0; cc < 2; ++cc)
+        for (int b = 0; b < 2; ++b)
+            for (int a = 0; a < 2; ++a) {
+                int64_t n = nid(c, i + a, j + b, k + cc);
+                int h = (cc * 2 + b) * 2 + a;
+                for (int q = 0; q < 3; ++q) N[h][q] = X[q][n];
+            }
+}
+
+/* ------------------------------------------------------------------------- */
+/* c.3 step 1: EoS                                                            */
+/* ------------------------------------------------------------------------- */
+static void eos(double gamma, double rho, double e, double* p, double* pf, double* cs)
+{
+    *p = ((gamma - 1.0) * rho) * e;
+    *pf = (*p > 0.0) ? *p : 0.0;
+    *cs = sqrt((gamma * *pf) / rho);
+}
+
+/* c.3 step 2, last line */
+static double q_of_du(double rho, double cs, double du, double c1, double c2)
+{
+    return (du < 0.0) ? rho * ((c2 * (du * du)) + ((c1 * cs) * (-du))) : 0.0;
+}
+
+static inline double dmin(double a, double b) { return (b < a) ? b : a; }
+static inline double dmax(double a, double b) { return (b > a) ? b : a; }
+
+/* c.3 step 2: per logical axis, face-centroid separation d, face-average
+ * velocity jump w, delta_a = (w . d)/|d|; du = min over axes; q. */
+static double cell_q(const face_t F[6], const double U[8][3], double rho, double cs,
+                     double c1, double c2)
+{
+    double delta[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        const face_t* fm = &F[2 * ax];
+        const face_t* fp = &F[2 * ax + 1];
+        const int* nm = FACE_NODES[2 * ax];
+        const int* np = FACE_NODES[2 * ax + 1];
+        double d[3], w[3];
+        for (int q = 0; q < 3; ++q) {
+            double Um = 0.25 * (((U[nm[0]][q] + U[nm[1]][q]) + U[nm[2]][q]) + U[nm[3]][q]);
+            double Up = 0.25 * (((U[np[0]][q] + U[np[1]][q]) + U[np[2]][q]) + U[np[3]][q]);
+            d[q] = fp->Xb[q] - fm->Xb[q];
+            w[q] = Up - Um;
+        }
+        double L = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+        delta[ax] = ((w[0] * d[0] + w[1] * d[1]) + w[2] * d[2]) / L;
+    }
+    double du = dmin(dmin(delta[0], delta[1]), delta[2]);
+    return q_of_du(rho, cs, du, c1, c2);
+}
+
+/* c.5: dt_K = (cfl*sqrt(l2)) / ((c + sqrt(v2)) + 1e-30) */
+static double dt_cell(double cfl, double l2, double v2, double cs)
+{
+    return (cfl * sqrt(l2)) / ((cs + sqrt(v2)) + 1e-30);
+}
+
+/* the 12 edges of a hex as pairs of hex-local node indices */
+static const int EDGES[12][2] = {
+    {0, 1}, {2, 3}, {4, 5}, {6, 7},   /* along a */
+    {0, 2}, {1, 3}, {4, 6}, {5, 7},   /* along b */
+    {0, 4}, {1, 5}, {2, 6}, {3, 7},   /* along c */
+};
+
+/* ------------------------------------------------------------------------- */
+/* errors                                                                     */
+/* ------------------------------------------------------------------------- */
+static const char* code_name(int32_t code)
+{
+    switch (code) {
+    case ORACLE_OK: return "OK";
+    case ORACLE_EINVAL: return "EINVAL";
+    case ORACLE_ENOMEM: return "ENOMEM";
+    case ORACLE_ETANGLED: return "ETANGLED";
+    case ORACLE_EDTCOLLAPSE: return "EDTCOLLAPSE";
+    case ORACLE_ENEGMASS: return "ENEGMASS";
+    case ORACLE_EPOISONED: return "EPOISONED";
+    default: return "E?";
+    }
+}
+
+static int32_t fail(oracle_ctx* c, int32_t code, int64_t cell)
+{
+    c->poisoned = 1;
+    c->err_cell = cell;
+    if (cell >= 0) {
+        int64_t i = cell % c->nx, j = (cell / c->nx) % c->ny, k = cell / (c->nx * c->ny);
+        snprintf(c->err, sizeof c->err, "%s cycle=%lld cell=%lld,%lld,%lld", code_name(code),
+                 (long long)c->cycle, (long long)i, (long long)j, (long long)k);
+    } else {
+        snprintf(c->err, sizeof c->err, "%s cycle=%lld", code_name(code), (long long)c->cycle);
+    }
+    return code;
+}
+
+/* ------------------------------------------------------------------------- */
+/* c.1 mesh, c.6 Sedov init                                                   */
+/* ------------------------------------------------------------------------- */
+static int params_valid(const oracle_params* p)
+{
+    if (!p || p->abi_version != ORACLE_ABI_VERSION) return 0;
+    if (p->nx < 1 || p->ny < 1 || p->nz < 1) return 0;
+    if (!(p->lx > 0.0) || !(p->ly > 0.0) || !(p->lz > 0.0)) return 0;
+    if (!(p->gamma > 1.0) || !(p->cfl > 0.0) || !(p->dt_growth > 0.0)) return 0;
+    if (!(p->q_lin >= 0.0) || !(p->q_quad >= 0.0)) return 0;
+    if (p->rezone != 0 && p->rezone != 1) return 0;
+    if (p->reflect_mask > 0x3Fu) return 0;
+    if (!(p->rho0 > 0.0)) return 0;
+    return 1;
+}
+
+static double* alloc_d(int64_t n, int* ok)
+{
+    double* v = (double*)calloc((size_t)n, sizeof(double));
+    if (!v) *ok = 0;
+    return v;
+}
+
+int32_t oracle_create(const oracle_params* p, oracle_ctx** out)
+{
+    if (!out) return ORACLE_EINVAL;
+    *out = NULL;
+    if (!params_valid(p)) return ORACLE_EINVAL;
+    oracle_ctx* c = (oracle_ctx*)calloc(1, sizeof *c);
+    if (!c) return ORACLE_ENOMEM;
+    c->p = *p;
+    c->nx = p->nx; c->ny = p->ny; c->nz = p->nz;
+    c->NX = c->nx + 1; c->NY = c->ny + 1; c->NZ = c->nz + 1;
+    c->ncell = c->nx * c->ny * c->nz;
+    c->nnode = c->NX * c->NY * c->NZ;
+    int ok = 1;
+    for (int q = 0; q < 3; ++q) {
+        c->x[q] = alloc_d(c->nnode, &ok);
+        c->u[q] = alloc_d(c->nnode, &ok);
+        c->xT[q] = alloc_d(c->nnode, &ok);
+        c->x1[q] = alloc_d(c->nnode, &ok);
+        c->u1[q] = alloc_d(c->nnode, &ok);
+        c->dP[q] = alloc_d(c->ncell, &ok);
+    }
+    c->m = alloc_d(c->ncell, &ok);
+    c->e = alloc_d(c->ncell, &ok);
+    c->sig = alloc_d(c->ncell, &ok);
+    c->e1 = alloc_d(c->ncell, &ok);
+    c->V1 = alloc_d(c->ncell, &ok);
+    c->dm = alloc_d(c->ncell, &ok);
+    c->dE = alloc_d(c->ncell, &ok);
+    c->m2 = alloc_d(c->ncell, &ok);
+    if (!ok) {
+        oracle_destroy(c);
+        return ORACLE_ENOMEM;
+    }
+    /* c.1: X_i = (lx*i)/nx, Y_j = (ly*j)/ny, Z_k = (lz*k)/nz */
+    for (int64_t k = 0; k < c->NZ; ++k)
+        for (int64_t j = 0; j < c->NY; ++j)
+            for (int64_t i = 0; i < c->NX; ++i) {
+                int64_t n = nid(c, i, j, k);
+                c->xT[0][n] = (p->lx * (double)i) / (double)p->nx;
+                c->xT[1][n] = (p->ly * (double)j) / (double)p->ny;
+                c->xT[2][n] = (p->lz * (double)k) / (double)p->nz;
+                for (int q = 0; q < 3; ++q) {
+                    c->x[q][n] = c->xT[q][n];
+                    c->u[q][n] = 0.0;
+                }
+            }
+    /* c.6: m_K = rho0 * V_K(x^T); e = e_bg except e_000 = E0 / m_000 */
+    for (int64_t k = 0; k < c->nz; ++k)
+        for (int64_t j = 0; j < c->ny; ++j)
+            for (int64_t i = 0; i < c->nx; ++i) {
+                double N[8][3];
+                face_t F[6];
+                cell_nodes(c, c->x, i, j, k, N);
+                hex_faces(N, F);
+                int64_t K = cid(c, i, j, k);
+                c->m[K] = p->rho0 * hex_volume_from_faces(F);
+                c->e[K] = p->e_background;
+            }
+    c->e[0] = p->e_deposit / c->m[0];
+    c->t = 0.0;
+    c->dt_prev = -1.0;
+    c->cycle = 0;
+    c->err_cell = -1;
+    snprintf(c->err, sizeof c->err, "OK");
+    *out = c;
+    return ORACLE_OK;
+}
+
+void oracle_destroy(oracle_ctx* c)
+{
+    if (!c) return;
+    for (int q = 0; q < 3; ++q) {
+        free(c->x[q]); free(c->u[q]); free(c->xT[q]);
+        free(c->x1[q]); free(c->u1[q]); free(c->dP[q]);
+    }
+    free(c->m); free(c->e); free(c->sig); free(c->e1); free(c->V1);
+    free(c->dm); free(c->dE); free(c->m2);
+    free(c);
+}
+
+/* ------------------------------------------------------------------------- */
+/* c.5 time step                                                              */
+/* ------------------------------------------------------------------------- */
+/* dt_cfl = min over cells of dt_K, from the state (x, u, m, e) */
+static double dt_cfl_of_state(oracle_ctx* c)
+{
+    const oracle_params* p = &c->p;
+    double best = 0.0;
+    int have = 0;
+    for (int64_t k = 0; k < c->nz; ++k)
+        for (int64_t j = 0; j < c->ny; ++j)
+            for (int64_t i = 0; i < c->nx; ++i) {
+                double N[8][3], U[8][3];
+                face_t F[6];
+                cell_nodes(c, c->x, i, j, k, N);
+                cell_nodes(c, c->u, i, j, k, U);
+                hex_faces(N, F);
+                int64_t K = cid(c, i, j, k);
+                double V = hex_volume_from_faces(F);
+                double rho = c->m[K] / V, pr, pf, cs;
+                eos(p->gamma, rho, c->e[K], &pr, &pf, &cs);
+                double l2 = 0.0;
+                for (int ed = 0; ed < 12; ++ed) {
+                    const double* A = N[EDGES[ed][0]];
+                    const double* B = N[EDGES[ed][1]];
+                    double d0 = B[0] - A[0], d1 = B[1] - A[1], d2 = B[2] - A[2];
+                    double len2 = (d0 * d0 + d1 * d1) + d2 * d2;
+                    l2 = (ed == 0) ? len2 : dmin(l2, len2);
+                }
+                double v2 = 0.0;
+                for (int h = 0; h < 8; ++h) {
+                    double s2 = (U[h][0] * U[h][0] + U[h][1] * U[h][1]) + U[h][2] * U[h][2];
+                    v2 = (h == 0) ? s2 : dmax(v2, s2);
+                }
+                double dtK = dt_cell(p->cfl, l2, v2, cs);
+                if (!have) { best = dtK; have = 1; }
+                else best = dmin(best, dtK);
+            }
+    return best;
+}
+
+/* c.5: returns 0 and *dt, or an error code. */
+static int32_t next_dt(oracle_ctx* c, double* dt)
+{
+    const oracle_params* p = &c->p;
+    double dt_cfl = dt_cfl_of_state(c);
+    double dt_u = (c->dt_prev < 0.0) ? dt_cfl : dmin(dt_cfl, p->dt_growth * c->dt_prev);
+    if (!(dt_u > 0.0) || (p->t_end > 0.0 && dt_u < 1e-14 * p->t_end))
+        return ORACLE_EDTCOLLAPSE;
+    double d = dt_u;
+    if (p->t_end > 0.0) d = dmin(dt_u, p->t_end - c->t);
+    *dt = d;
+    return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* c.3 Lagrangian phase                                                       */
+/* ------------------------------------------------------------------------- */
+static void reflect(const oracle_ctx* c, int64_t i, int64_t j, int64_t k, double v[3])
+{
+    uint32_t r = c->p.reflect_mask;
+    if (((r & 1u) && i == 0) || ((r & 2u) && i == c->nx)) v[0] = 0.0;
+    if (((r & 4u) && j == 0) || ((r & 8u) && j == c->ny)) v[1] = 0.0;
+    if (((r & 16u) && k == 0) || ((r & 32u) && k == c->nz)) v[2] = 0.0;
+}
+
+static int cell_exists(const oracle_ctx* c, int64_t i, int64_t j, int64_t k)
+{
+    return i >= 0 && i < c->nx && j >= 0 && j < c->ny && k >= 0 && k < c->nz;
+}
+
+/* Steps 1-3: per cell rho, p, pf, c, q, sigma = 0.25*(pf+q) */
+static void lagrange_sigma(oracle_ctx* c)
+{
+    const oracle_params* p = &c->p;
+    for (int64_t k = 0; k < c->nz; ++k)
+        for (int64_t j = 0; j < c->ny; ++j)
+            for (int64_t i = 0; i < c->nx; ++i) {
+                double N[8][3], U[8][3];
+                face_t F[6];
+                cell_nodes(c, c->x, i, j, k, N);
+                cell_nodes(c, c->u, i, j, k, U);
+                hex_faces(N, F);
+                int64_t K = cid(c, i, j, k);
+                double V = hex_volume_from_faces(F);
+                double rho = c->m[K] / V, pr, pf, cs;
+                eos(p->gamma, rho, c->e[K], &pr, &pf, &cs);
+                double q = cell_q(F, U, rho, cs, p->q_lin, p->q_quad);
+                c->sig[K] = 0.25 * (pf + q);
+            }
+}
+
+/* Steps 4-6: nodal force and mass by gather, kinematics, BC, move */
+static void lagrange_nodes(oracle_ctx* c, double dt)
+{
+    for (int64_t k = 0; k < c->NZ; ++k)
+        for (int64_t j = 0; j < c->NY; ++j)
+            for (int64_t i = 0; i < c->NX; ++i) {
+                double F[3] = {0.0, 0.0, 0.0}, M = 0.0;
+                int first = 1;
+                /* gather order: cells (i-1+a', j-1+b', k-1+c'), a' fastest */
+                for (int cp = 0; cp < 2; ++cp)
+                    for (int bp = 0; bp < 2; ++bp)
+                        for (int ap = 0; ap < 2; ++ap) {
+                            int64_t ci = i - 1 + ap, cj = j - 1 + bp, ck = k - 1 + cp;
+                            if (!cell_exists(c, ci, cj, ck)) continue;
+                            double N[8][3], C[3];
+                            face_t Fc[6];
+                            cell_nodes(c, c->x, ci, cj, ck, N);
+                            hex_faces(N, Fc);
+                            corner_vector(Fc, 1 - ap, 1 - bp, 1 - cp, C);
+                            int64_t K = cid(c, ci, cj, ck);
+                            double s = c->sig[K];
+                            if (first) {
+                                for (int q = 0; q < 3; ++q) F[q] = s * C[q];
+                                M = c->m[K];
+                                first = 0;
+                            } else {
+                                for (int q = 0; q < 3; ++q) F[q] = F[q] + s * C[q];
+                                M = M + c->m[K];
+                            }
+                        }
+                M = 0.125 * M;
+                int64_t n = nid(c, i, j, k);
+                double un[3];
+                for (int q = 0; q < 3; ++q) un[q] = c->u[q][n] + ((F[q] / M) * dt);
+                reflect(c, i, j, k, un);
+                for (int q = 0; q < 3; ++q) {
+                    c->u1[q][n] = un[q];
+                    c->x1[q][n] = c->x[q][n] + (un[q] * dt);
+                }
+            }
+}
+
+/* c.3 step 7 for one cell (shared with the exported unit entry point) */
+static double energy_update(const double N0[8][3], const double U0[8][3],
+                            const double U1[8][3], double sigma, double m, double e,
+                            double dt)
+{
+    face_t F[6];
+    hex_faces(N0, F);
+    double W = 0.0;
+    for (int cc = 0; cc < 2; ++cc)
+        for (int b = 0; b < 2; ++b)
+            for (int a = 0; a < 2; ++a) {
+                int h = (cc * 2 + b) * 2 + a;
+                double C[3], ub[3];
+                corner_vector(F, a, b, cc, C);
+                for (int q = 0; q < 3; ++q) ub[q] = 0.5 * (U0[h][q] + U1[h][q]);
+                double term = (C[0] * ub[0] + C[1] * ub[1]) + C[2] * ub[2];
+                W = (h == 0) ? term : W + term;
+            }
+    return e - (((sigma * W) * dt) / m);
+}
+
+/* Step 7: V' (tangle check), compatible pdV energy update */
+static int32_t lagrange_energy(oracle_ctx* c, double dt)
+{
+    for (int64_t k = 0; k < c->nz; ++k)
+        for (int64_t j = 0; j < c->ny; ++j)
+            for (int64_t i = 0; i < c->nx; ++i) {
+                double N0[8][3], N1[8][3], U0[8][3], U1[8][3];
+                face_t F1[6];
+                cell_nodes(c, c->x, i, j, k, N0);
+                cell_nodes(c, c->x1, i, j, k, N1);
+                cell_nodes(c, c->u, i, j, k, U0);
+                cell_nodes(c, c->u1, i, j, k, U1);
+                hex_faces(N1, F1);
+                int64_t K = cid(c, i, j, k);
+                double V1 = hex_volume_from_faces(F1);
+                if (!(V1 > 0.0)) return fail(c, ORACLE_ETANGLED, K);
+                c->V1[K] = V1;
+                c->e1[K] = energy_update(N0, U0, U1, c->sig[K], c->m[K], c->e[K], dt);
+            }
+    return ORACLE_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* c.4 Eulerian remap                                                         */
+/* ------------------------------------------------------------------------- */
+/* c.4 step 1: hex (0,0,0)=P0^T (1,0,0)=P1^T (1,1,0)=P2^T (0,1,0)=P3^T,
+ *                 (0,0,1)=P0'  (1,0,1)=P1'  (1,1,1)=P2'  (0,1,1)=P3'        */
+static double swept_volume(const double PT[4][3], const double PL[4][3])
+{
+    double N[8][3];
+    static const int map[4][2] = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+    for (int v = 0; v < 4; ++v) {
+        int a = map[v][0], b = map[v][1];
+        for (int q = 0; q < 3; ++q) {
+            N[(0 * 2 + b) * 2 + a][q] = PT[v][q];
+            N[(1 * 2 + b) * 2 + a][q] = PL[v][q];
+        }
+    }
+    face_t F[6];
+    hex_faces(N, F);
+    return hex_volume_from_faces(F);
+}
+
+/* canonical P0..P3 of the physical face of axis `ax` at lower cell (i,j,k)'s
+ * +ax side, i.e. node plane (i+1 | j+1 | k+1), as global node indices. */
+static void face_node_ids(const oracle_ctx* c, int ax, int64_t i, int64_t j, int64_t k,
+                          int64_t ids[4])
+{
+    if (ax == 0) {        /* X-face at node plane i+1: (i',j,k)(i',j+1,k)(i',j+1,k+1)(i',j,k+1) */
+        int64_t I = i + 1;
+        ids[0] = nid(c, I, j, k); ids[1] = nid(c, I, j + 1, k);
+        ids[2] = nid(c, I, j + 1, k + 1); ids[3] = nid(c, I, j, k + 1);
+    } else if (ax == 1) { /* Y-face at node plane j+1: (i,j',k)(i,j',k+1)(i+1,j',k+1)(i+1,j',k) */
+        int64_t J = j + 1;
+        ids[0] = nid(c, i, J, k); ids[1] = nid(c, i, J, k + 1);
+        ids[2] = nid(c, i + 1, J, k + 1); ids[3] = nid(c, i + 1, J, k);
+    } else {              /* Z-face at node plane k+1: (i,j,k')(i+1,j,k')(i+1,j+1,k')(i,j+1,k') */
+        int64_t Kp = k + 1;
+        ids[0] = nid(c, i, j, Kp); ids[1] = nid(c, i + 1, j, Kp);
+        ids[2] = nid(c, i + 1, j + 1, Kp); ids[3] = nid(c, i, j + 1, Kp);
+    }
+}
+
+/* c.4 steps 1-2 for the interior face between cell L=(i,j,k) and its +ax
+ * neighbour U: mu, eps, pi[3] through the face (positive = toward +ax). */
+static void face_flux(oracle_ctx* c, int ax, int64_t i, int64_t j, int64_t k, double* mu,
+                      double* eps, double pi[3])
+{
+    int64_t ids[4];
+    face_node_ids(c, ax, i, j, k, ids);
+    double PT[4][3], PL[4][3];
+    for (int v = 0; v < 4; ++v)
+        for (int q = 0; q < 3; ++q) {
+            PT[v][q] = c->xT[q][ids[v]];
+            PL[v][q] = c->x1[q][ids[v]];
+        }
+    double dV = swept_volume(PT, PL);
+    int64_t di = i, dj = j, dk = k;             /* donor: lower if dV > 0 */
+    if (!(dV > 0.0)) {
+        if (ax == 0) di = i + 1; else if (ax == 1) dj = j + 1; else dk = k + 1;
+    }
+    int64_t D = cid(c, di, dj, dk);
+    double U[8][3];
+    cell_nodes(c, c->u1, di, dj, dk, U);
+    double Ub[3];
+    for (int q = 0; q < 3; ++q) {
+        double s = U[0][q];
+        for (int h = 1; h < 8; ++h) s = s + U[h][q];
+        Ub[q] = 0.125 * s;
+    }
+    *mu = (c->m[D] / c->V1[D]) * dV;
+    *eps = *mu * c->e1[D];
+    for (int q = 0; q < 3; ++q) pi[q] = *mu * Ub[q];
+}
+
+/* c.4 steps 1-3: per cell, fluxes through its six faces (boundary faces carry
+ * +0.0), Delta m/E/P, m'' = m + Delta m (ENEGMASS if !(m'' > 0)). */
+static int32_t euler_cells(oracle_ctx* c)
+{
+    const int64_t nmax[3] = {c->nx, c->ny, c->nz};
+    for (int64_t k = 0; k < c->nz; ++k)
+        for (int64_t j = 0; j < c->ny; ++j)
+            for (int64_t i = 0; i < c->nx; ++i) {
+                double mu[6], ep[6], pi[6][3];   /* order -x,+x,-y,+y,-z,+z */
+                const int64_t ijk[3] = {i, j, k};
+                for (int ax = 0; ax < 3; ++ax) {
+                    if (ijk[ax] > 0) {           /* -ax face: lower cell ijk - e_ax */
+                        int64_t l[3] = {i, j, k};
+                        l[ax] -= 1;
+                        face_flux(c, ax, l[0], l[1], l[2], &mu[2 * ax], &ep[2 * ax], pi[2 * ax]);
+                    } else {
+                        mu[2 * ax] = 0.0; ep[2 * ax] = 0.0;
+                        pi[2 * ax][0] = pi[2 * ax][1] = pi[2 * ax][2] = 0.0;
+                    }
+                    if (ijk[ax] < nmax[ax] - 1) { /* +ax face: lower cell is ijk */
+                        face_flux(c, ax, i, j, k, &mu[2 * ax + 1], &ep[2 * ax + 1], pi[2 * ax + 1]);
+                    } else {
+                        mu[2 * ax + 1] = 0.0; ep[2 * ax + 1] = 0.0;
+                        pi[2 * ax + 1][0] = pi[2 * ax + 1][1] = pi[2 * ax + 1][2] = 0.0;
+                    }
+                }
+                int64_t K = cid(c, i, j, k);
+                double dm = ((((mu[0] - mu[1]) + mu[2]) - mu[3]) + mu[4]) - mu[5];
+                double dE = ((((ep[0] - ep[1]) + ep[2]) - ep[3]) + ep[4]) - ep[5];
+                for (int q = 0; q < 3; ++q)
+                    c->dP[q][K] = ((((pi[0][q] - pi[1][q]) + pi[2][q]) - pi[3][q]) + pi[4][q]) - pi[5][q];
+                double m2 = c->m[K] + dm;
+                if (!(m2 > 0.0)) return fail(c, ORACLE_ENEGMASS, K);
+                c->dm[K] = dm;
+                c->dE[K] = dE;
+                c->m2[K] = m2;
+            }
+    return ORACLE_OK;
+}
+
+/* c.4 step 3 (e''), step 4 (node momentum, BC), step 5 (x := x^T) */
+static void euler_commit(oracle_ctx* c)
+{
+    for (int64_t K = 0; K < c->ncell; ++K) {
+        double e1 = c->e1[K];
+        c->e[K] = e1 + ((c->dE[K] - (e1 * c->dm[K])) / c->m2[K]);
+    }
+    for (int64_t k = 0; k < c->NZ; ++k)
+        for (int64_t j = 0; j < c->NY; ++j)
+            for (int64_t i = 0; i < c->NX; ++i) {
+                double Dm = 0.0, DP[3] = {0.0, 0.0, 0.0}, M2 = 0.0;
+                int first = 1;
+                for (int cp = 0; cp < 2; ++cp)
+                    for (int bp = 0; bp < 2; ++bp)
+                        for (int ap = 0; ap < 2; ++ap) {
+                            int64_t ci = i - 1 + ap, cj = j - 1 + bp, ck = k - 1 + cp;
+                            if (!cell_exists(c, ci, cj, ck)) continue;
+                            int64_t K = cid(c, ci, cj, ck);
+                            if (first) {
+                                Dm = c->dm[K];
+                                for (int q = 0; q < 3; ++q) DP[q] = c->dP[q][K];
+                                M2 = c->m2[K];
+                                first = 0;
+                            } else {
+                                Dm = Dm + c->dm[K];
+                                for (int q = 0; q < 3; ++q) DP[q] = DP[q] + c->dP[q][K];
+                                M2 = M2 + c->m2[K];
+                            }
+                        }
+                Dm = 0.125 * Dm;
+                for (int q = 0; q < 3; ++q) DP[q] = 0.125 * DP[q];
+                M2 = 0.125 * M2;
+                int64_t n = nid(c, i, j, k);
+                double un[3];
+                for (int q = 0; q < 3; ++q) {
+                    double u1 = c->u1[q][n];
+                    un[q] = u1 + ((DP[q] - (u1 * Dm)) / M2);
+                }
+                reflect(c, i, j, k, un);
+                for (int q = 0; q < 3; ++q) {
+                    c->u[q][n] = un[q];
+                    c->x[q][n] = c->xT[q][n];
+                }
+            }
+    for (int64_t K = 0; K < c->ncell; ++K) c->m[K] = c->m2[K];
+}
+
+/* ------------------------------------------------------------------------- */
+/* one cycle (c.3, then c.4 in EULER mode), clock (c.3 step 8)                */
+/* ------------------------------------------------------------------------- */
+static int32_t cycle_once(oracle_ctx* c, double dt)
+{
+    lagrange_sigma(c);
+    lagrange_nodes(c, dt);
+    int32_t rc = lagrange_energy(c, dt);
+    if (rc) return rc;
+    if (c->p.rezone == 1) {
+        rc = euler_cells(c);
+        if (rc) return rc;
+        euler_commit(c);
+    } else {
+        for (int q = 0; q < 3; ++q) {
+            double* t;
+            t = c->x[q]; c->x[q] = c->x1[q]; c->x1[q] = t;
+            t = c->u[q]; c->u[q] = c->u1[q]; c->u1[q] = t;
+        }
+        double* t = c->e; c->e = c->e1; c->e1 = t;
+    }
+    c->t = c->t + dt;
+    c->cycle = c->cycle + 1;
+    c->dt_prev = dt;
+    return ORACLE_OK;
+}
+
+int32_t oracle_step(oracle_ctx* c, int32_t ncycles, int32_t* cycles_done)
+{
+    if (cycles_done) *cycles_done = 0;
+    if (!c || ncycles < 0) return ORACLE_EINVAL;
+    if (c->poisoned) return ORACLE_EPOISONED;
+    int32_t done = 0;
+    for (int32_t n = 0; n < ncycles; ++n) {
+        if (c->p.t_end > 0.0 && c->t >= c->p.t_end) {   /* c.5 last line */
+            c->finished = 1;
+            break;
+        }
+        double dt;
+        int32_t rc = next_dt(c, &dt);
+        if (rc) {
+            if (cycles_done) *cycles_done = done;
+            return fail(c, rc, -1);
+        }
+        rc = cycle_once(c, dt);
+        if (rc) {
+            if (cycles_done) *cycles_done = done;
+            return rc;
+        }
+        ++done;
+    }
+    if (c->p.t_end > 0.0 && c->t >= c->p.t_end) c->finished = 1;
+    if (cycles_done) *cycles_done = done;
+    return ORACLE_OK;
+}
+
+int32_t oracle_next_dt(oracle_ctx* c, double* dt)
+{
+    if (!c || !dt) return ORACLE_EINVAL;
+    if (c->p.t_end > 0.0 && c->t >= c->p.t_end) { *dt = -1.0; return ORACLE_OK; }
+    return next_dt(c, dt);
+}
+
+/* ------------------------------------------------------------------------- */
+/* fields (SURVEY §8(b) sale_get_field / sale_set_field)                      */
+/* ------------------------------------------------------------------------- */
+static int is_node_field(int32_t f) { return f >= ORACLE_F_X && f <= ORACLE_F_NODE_MASS; }
+static int is_cell_field(int32_t f) { return f >= ORACLE_F_MASS && f <= ORACLE_F_CS; }
+
+int32_t oracle_get_field(oracle_ctx* c, int32_t field, double* dst, uint64_t count)
+{
+    if (!c || !dst) return ORACLE_EINVAL;
+    if (is_node_field(field)) {
+        if (count != (uint64_t)c->nnode) return ORACLE_EINVAL;
+        if (field <= ORACLE_F_Z) {
+            memcpy(dst, c->x[field - ORACLE_F_X], sizeof(double) * (size_t)c->nnode);
+        } else if (field <= ORACLE_F_UZ) {
+            memcpy(dst, c->u[field - ORACLE_F_UX], sizeof(double) * (size_t)c->nnode);
+        } else { /* NODE_MASS: c.3 step 5 */
+            for (int64_t k = 0; k < c->NZ; ++k)
+                for (int64_t j = 0; j < c->NY; ++j)
+                    for (int64_t i = 0; i < c->NX; ++i) {
+                        double M = 0.0;
+                        int first = 1;
+                        for (int cp = 0; cp < 2; ++cp)
+                            for (int bp = 0; bp < 2; ++bp)
+                                for (int ap = 0; ap < 2; ++ap) {
+                                    int64_t ci = i - 1 + ap, cj = j - 1 + bp, ck = k - 1 + cp;
+                                    if (!cell_exists(c, ci, cj, ck)) continue;
+                                    double mk = c->m[cid(c, ci, cj, ck)];
+                                    M = first ? mk : M + mk;
+                                    first = 0;
+                                }
+                        dst[nid(c, i, j, k)] = 0.125 * M;
+                    }
+        }
+        return ORACLE_OK;
+    }
+    if (!is_cell_field(field)) return ORACLE_EINVAL;
+    if (count != (uint64_t)c->ncell) return ORACLE_EINVAL;
+    if (field == ORACLE_F_MASS) { memcpy(dst, c->m, sizeof(double) * (size_t)c->ncell); return 0; }
+    if (field == ORACLE_F_E) { memcpy(dst, c->e, sizeof(double) * (size_t)c->ncell); return 0; }
+    for (int64_t k = 0; k < c->nz; ++k)
+        for (int64_t j = 0; j < c->ny; ++j)
+            for (int64_t i = 0; i < c->nx; ++i) {
+                double N[8][3], U[8][3];
+                face_t F[6];
+                cell_nodes(c, c->x, i, j, k, N);
+                hex_faces(N, F);
+                int64_t K = cid(c, i, j, k);
+                double V = hex_volume_from_faces(F);
+                double rho = c->m[K] / V, pr, pf, cs;
+                eos(c->p.gamma, rho, c->e[K], &pr, &pf, &cs);
+                double v;
+                switch (field) {
+                case ORACLE_F_RHO: v = rho; break;
+                case ORACLE_F_VOL: v = V; break;
+                case ORACLE_F_P: v = pr; break;
+                case ORACLE_F_CS: v = cs; break;
+                default: /* Q */
+                    cell_nodes(c, c->u, i, j, k, U);
+                    v = cell_q(F, U, rho, cs, c->p.q_lin, c->p.q_quad);
+                    break;
+                }
+                dst[K] = v;
+            }
+    return ORACLE_OK;
+}
+
+int32_t oracle_set_field(oracle_ctx* c, int32_t field, const double* src, uint64_t count)
+{
+    if (!c || !src) return ORACLE_EINVAL;
+    if (c->poisoned) return ORACLE_EPOISONED;
+    double* dst = NULL;
+    uint64_t need = 0;
+    if (field >= ORACLE_F_X && field <= ORACLE_F_Z) {
+        if (c->p.rezone == 1) return ORACLE_EINVAL;     /* Euler: x = x^T */
+        dst = c->x[field - ORACLE_F_X]; need = (uint64_t)c->nnode;
+    } else if (field >= ORACLE_F_UX && field <= ORACLE_F_UZ) {
+        dst = c->u[field - ORACLE_F_UX]; need = (uint64_t)c->nnode;
+    } else if (field == ORACLE_F_MASS) {
+        dst = c->m; need = (uint64_t)c->ncell;
+    } else if (field == ORACLE_F_E) {
+        dst = c->e; need = (uint64_t)c->ncell;
+    } else {
+        return ORACLE_EINVAL;
+    }
+    if (count != need) return ORACLE_EINVAL;
+    memcpy(dst, src, sizeof(double) * (size_t)need);
+    return ORACLE_OK;
+}
+
+int32_t oracle_get_clock(oracle_ctx* c, double* t, double* dt_last, int64_t* cycle,
+                         int32_t* finished)
+{
+    if (!c) return ORACLE_EINVAL;
+    if (t) *t = c->t;
+    if (dt_last) *dt_last = c->dt_prev;
+    if (cycle) *cycle = c->cycle;
+    if (finished) *finished = (c->p.t_end > 0.0 && c->t >= c->p.t_end) ? 1 : 0;
+    return ORACLE_OK;
+}
+
+int32_t oracle_set_clock(oracle_ctx* c, double t, double dt_last, int64_t cycle)
+{
+    if (!c || cycle < 0) return ORACLE_EINVAL;
+    if (c->poisoned) return ORACLE_EPOISONED;
+    c->t = t;
+    c->dt_prev = dt_last;
+    c->cycle = cycle;
+    c->finished = 0;
+    return ORACLE_OK;
+}
+
+const char* oracle_last_error(const oracle_ctx* c) { return c ? c->err : "null context"; }
+int64_t oracle_last_error_cell(const oracle_ctx* c) { return c ? c->err_cell : -1; }
+
+/* ------------------------------------------------------------------------- */
+/* unit entry points for the pins                                             */
+/* ------------------------------------------------------------------------- */
+void oracle_face(const double* P, double* A, double* Xbar, double* s)
+{
+    face_t f;
+    face_geom(P, P + 3, P + 6, P + 9, &f);
+    for (int q = 0; q < 3; ++q) { A[q] = f.A[q]; Xbar[q] = f.Xb[q]; }
+    *s = f.s;
+}
+
+double oracle_hex_volume(const double* Nflat)
+{
+    double N[8][3];
+    face_t F[6];
+    for (int h = 0; h < 8; ++h)
+        for (int q = 0; q < 3; ++q) N[h][q] = Nflat[h * 3 + q];
+    hex_faces(N, F);
+    return hex_volume_from_faces(F);
+}
+
+void oracle_eos(double gamma, double rho, double e, double* p, double* pf, double* cs)
+{
+    eos(gamma, rho, e, p, pf, cs);
+}
+
+double oracle_q_of_du(double rho, double cs, double du, double c1, double c2)
+{
+    return q_of_du(rho, cs, du, c1, c2);
+}
+
+double oracle_dt_cell(double cfl, double l2, double v2, double cs)
+{
+    return dt_cell(cfl, l2, v2, cs);
+}
+
+double oracle_swept_volume(const double* PTf, const double* PLf)
+{
+    double PT[4][3], PL[4][3];
+    for (int v = 0; v < 4; ++v)
+        for (int q = 0; q < 3; ++q) { PT[v][q] = PTf[v * 3 + q]; PL[v][q] = PLf[v * 3 + q]; }
+    return swept_volume(PT, PL);
+}
+
+double oracle_cell_energy(const double* N0f, const double* U0f, const double* U1f,
+                          double sigma, double m, double e, double dt)
+{
+    double N0[8][3], U0[8][3], U1[8][3];
+    for (int h = 0; h < 8; ++h)
+        for (int q = 0; q < 3; ++q) {
+            N0[h][q] = N0f[h * 3 + q]; U0[h][q] = U0f[h * 3 + q]; U1[h][q] = U1f[h * 3 + q];
+        }
+    return energy_update(N0, U0, U1, sigma, m, e, dt);
+}

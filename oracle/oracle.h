@@ -1,0 +1,104 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * The plain, slow, single-threaded CPU oracle of the SALE hot path
+ * (arXiv 2209.01983, "ScalSALE").  It exists to check the
+ * CUDA path; nothing in the product package may include, link or call it.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+ * leg may load liboracle.so.
+ *
+ * It shares no code with paper_2209_01983_b200/ (no headers, helpers, tables).
+ * Its ABI mirrors the product ABI (include/sale.h) with the prefix `oracle_`,
+ * host pointers only and a single rank.
+ *
+ * The paper never writes the discrete scheme (only the Steinberg
+ * loop P:442-459 and the efficiency formula P:509-516 are formulas).  Every
+ * operator here follows SURVEY §8(c) c.1-c.6 step by step, in its order and
+ * notation, with the readings Q1-Q23 listed in DESIGN.md §3.
+ *
+ * Build: gcc -O2 -ffp-contract=off -std=c11 (never -ffast-math): every + - * /
+ * sqrt is one correctly rounded IEEE binary64 operation in the written order.
+ */
+#ifndef SALE_ORACLE_H
+#define SALE_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORACLE_ABI_VERSION 1
+
+/* Same fields and meaning as sale_params (include/sale.h), minus the device /
+ * communication members.  SURVEY §8(b). */
+typedef struct oracle_params {
+    int32_t abi_version;          /* must be ORACLE_ABI_VERSION                */
+    int32_t nx, ny, nz;           /* cells per axis (global)                   */
+    double lx, ly, lz;            /* domain extents; node X_i = (lx*i)/nx      */
+    double gamma;                 /* ideal-gas gamma (> 1)                     */
+    double q_lin, q_quad;         /* viscosity c1 (linear), c2 (quadratic)     */
+    double cfl;                   /* CFL number                                */
+    double dt_growth;             /* dt_u <= dt_growth * dt_prev               */
+    double t_end;                 /* <= 0: no end time                         */
+    int32_t rezone;               /* 0 = LAGRANGE, 1 = EULER                   */
+    uint32_t reflect_mask;        /* bit f: face f in {-x,+x,-y,+y,-z,+z} reflects */
+    double rho0;                  /* Sedov ambient density                     */
+    double e_background;          /* Sedov background specific energy          */
+    double e_deposit;             /* Sedov energy E0 put in cell (0,0,0)       */
+} oracle_params;
+
+typedef struct oracle_ctx oracle_ctx;
+
+/* status codes (same numbering as the product) */
+enum {
+    ORACLE_OK = 0, ORACLE_EINVAL = 1, ORACLE_ENOMEM = 2,
+    ORACLE_ETANGLED = 5, ORACLE_EDTCOLLAPSE = 6, ORACLE_ENEGMASS = 7,
+    ORACLE_EPOISONED = 8
+};
+
+/* field ids (same numbering as the product) */
+enum {
+    ORACLE_F_X = 0, ORACLE_F_Y, ORACLE_F_Z, ORACLE_F_UX, ORACLE_F_UY, ORACLE_F_UZ,
+    ORACLE_F_NODE_MASS,                                   /* node fields 0..6  */
+    ORACLE_F_MASS = 7, ORACLE_F_E, ORACLE_F_RHO, ORACLE_F_VOL, ORACLE_F_P,
+    ORACLE_F_Q, ORACLE_F_CS                               /* cell fields 7..13 */
+};
+
+int32_t oracle_create(const oracle_params* p, oracle_ctx** out);
+int32_t oracle_step(oracle_ctx* c, int32_t ncycles, int32_t* cycles_done);
+int32_t oracle_get_field(oracle_ctx* c, int32_t field, double* dst, uint64_t count);
+int32_t oracle_set_field(oracle_ctx* c, int32_t field, const double* src, uint64_t count);
+int32_t oracle_get_clock(oracle_ctx* c, double* t, double* dt_last, int64_t* cycle,
+                         int32_t* finished);
+int32_t oracle_set_clock(oracle_ctx* c, double t, double dt_last, int64_t cycle);
+/* error detail: "<code name> cycle=<n> cell=<i,j,k>" of the last failure */
+const char* oracle_last_error(const oracle_ctx* c);
+/* linear cell index of the last ETANGLED/ENEGMASS cell, -1 if none */
+int64_t oracle_last_error_cell(const oracle_ctx* c);
+/* dt the next cycle would use (c.5), without advancing; <0 if finished. */
+int32_t oracle_next_dt(oracle_ctx* c, double* dt);
+void oracle_destroy(oracle_ctx* c);
+
+/* ---- unit entry points (the same primitives the cycle uses), for pins ---- */
+/* c.2: face from 4 points (P[4][3]) -> A[3], Xbar[3], s */
+void oracle_face(const double* P, double* A, double* Xbar, double* s);
+/* c.2: volume of the hex whose local node (a,b,c) is N[((c*2+b)*2+a)*3 + comp] */
+double oracle_hex_volume(const double* N);
+/* c.3 step 1: p, pf, c from (gamma, rho, e) */
+void oracle_eos(double gamma, double rho, double e, double* p, double* pf, double* cs);
+/* c.3 step 2 last line: q from rho, c, du */
+double oracle_q_of_du(double rho, double cs, double du, double c1, double c2);
+/* c.5: per-cell candidate from l2 = min edge^2, v2 = max node speed^2, c */
+double oracle_dt_cell(double cfl, double l2, double v2, double cs);
+/* c.4 step 1: swept volume between target face PT[4][3] and moved face PL[4][3] */
+double oracle_swept_volume(const double* PT, const double* PL);
+/* c.3 step 7 for one cell: N0/N1 = nodes at t^n / t^{n+1} in hex order,
+ * U0/U1 = node velocities u / u' in hex order; returns e'. */
+double oracle_cell_energy(const double* N0, const double* U0, const double* U1,
+                          double sigma, double m, double e, double dt);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

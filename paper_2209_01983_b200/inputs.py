@@ -1,0 +1,53 @@
+"""Seeded synthetic input generators shared by the tests of the oracle and of
+the CUDA path (inputs P0-P2).
+
+This module holds NONE of the method's arithmetic: it only draws random
+numbers (numpy ``Generator(PCG64(seed))``) and masks.  The caller adds the
+returned jitter to node coordinates it read back through ``get_field`` and
+multiplies the energy factor into ``e``, then loads the same bits into both the
+oracle and the GPU context with ``set_field``.
+
+Recipe: interior node coordinates jittered by U(-0.05h, 0.05h)
+per axis (boundary nodes are left on their planes); node velocity
+U(-1e-3, 1e-3) per component, with the normal component zeroed on reflecting
+planes; specific energy multiplied by U(0.5, 1.5).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def perturbation(cfg: dict, seed: int, u_scale: float = 1e-3, x_frac: float = 0.05,
+                 e_lo: float = 0.5, e_hi: float = 1.5):
+    """Return dict(dx, dy, dz, ux, uy, uz [node arrays (nz+1, ny+1, nx+1)],
+    e_factor [cell array (nz, ny, nx)])."""
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    hs = (cfg["lx"] / nx, cfg["ly"] / ny, cfg["lz"] / nz)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    nshape = (nz + 1, ny + 1, nx + 1)
+    k, j, i = np.meshgrid(np.arange(nz + 1), np.arange(ny + 1), np.arange(nx + 1),
+                          indexing="ij")
+    interior = (i > 0) & (i < nx) & (j > 0) & (j < ny) & (k > 0) & (k < nz)
+    out = {}
+    for name, h in zip(("dx", "dy", "dz"), hs):
+        d = rng.uniform(-x_frac * h, x_frac * h, size=nshape)
+        out[name] = np.where(interior, d, 0.0)
+    mask = int(cfg["reflect_mask"])
+    planes = (((i == 0), (i == nx)), ((j == 0), (j == ny)), ((k == 0), (k == nz)))
+    for ax, name in enumerate(("ux", "uy", "uz")):
+        u = rng.uniform(-u_scale, u_scale, size=nshape)
+        lo, hi = planes[ax]
+        zero = np.zeros(nshape, dtype=bool)
+        if mask & (1 << (2 * ax)):
+            zero |= lo
+        if mask & (1 << (2 * ax + 1)):
+            zero |= hi
+        out[name] = np.where(zero, 0.0, u)
+    out["e_factor"] = rng.uniform(e_lo, e_hi, size=(nz, ny, nx))
+    return out
+
+
+def uniform_velocity(cfg: dict, u: tuple[float, float, float]):
+    """Constant node velocity arrays (no randomness)."""
+    nshape = (cfg["nz"] + 1, cfg["ny"] + 1, cfg["nx"] + 1)
+    return {n: np.full(nshape, float(v)) for n, v in zip(("ux", "uy", "uz"), u)}

@@ -1,0 +1,292 @@
+"""Cycle-level pins of the oracle against what the physics and closed forms fix
+(SURVEY §8(c).9): conservation, fixed points, Galilean invariance, a closed-form
+one-cycle case, octant symmetry, the Sedov-Taylor similarity law, error paths
+and checkpoint/resume.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2209_01983_b200 import inputs
+from paper_2209_01983_b200.configs import EULER, LAGRANGE, config, sedov
+
+
+def energies(o):
+    m, e = o.get("MASS"), o.get("E")
+    M = o.get("NODE_MASS")
+    ux, uy, uz = o.get("UX"), o.get("UY"), o.get("UZ")
+    ie = math.fsum((m * e).ravel())
+    ke = math.fsum((0.5 * M * ((ux * ux + uy * uy) + uz * uz)).ravel())
+    return ie, ke
+
+
+def uniform_state(n, rezone, mask, gamma=1.5, e=2.0, **kw):
+    cfg = sedov((n, n, n), rezone, gamma=gamma, reflect_mask=mask, **kw)
+    o = O.Oracle(cfg)
+    o.set("E", np.full(o.cell_shape, e))
+    return cfg, o
+
+
+# --------------------------------------------------------------- closed form
+def test_single_free_cube_one_cycle_closed_form():
+    """One free unit cube, rho=1, e=2.5, gamma=1.4, cfl=0.3, all faces free.
+    Hand derivation from c.2-c.5 (exact arithmetic): p=(g-1)e, c=sqrt(g p),
+    dt = cfl*1/c; every corner vector is (+-1,+-1,+-1), sigma = p/4, M = m/8, so
+    |u'_a| = (sigma/M) dt = 2 p dt; side' = 1 + 2|u'_a| dt; compatible work
+    e' = e - sigma*W*dt/m with W = 8*3*|u'_a|/2 -> e' = e - 6 p^2 dt^2 = e - KE."""
+    cfg = sedov((1, 1, 1), LAGRANGE, reflect_mask=0, e_deposit=2.5, e_background=2.5)
+    o = O.Oracle(cfg)
+    assert o.get("E")[0, 0, 0] == 2.5
+    g, cfl, e = 1.4, 0.3, 2.5
+    p = (g - 1) * e
+    dt = cfl / math.sqrt(g * p)
+    rc, done = o.step(1)
+    assert rc == 0 and done == 1
+    assert o.clock()["dt_last"] == pytest.approx(dt, rel=1e-14)
+    ua = 2 * p * dt
+    ux = o.get("UX")
+    assert np.allclose(np.abs(ux), ua, rtol=1e-14, atol=0)
+    assert ux[0, 0, 0] < 0 < ux[0, 0, 1]           # outward: high p pushes walls out
+    X = o.get("X")
+    assert X[0, 0, 1] - X[0, 0, 0] == pytest.approx(1 + 2 * ua * dt, rel=1e-14)
+    assert o.get("E")[0, 0, 0] == pytest.approx(e - 6 * p * p * dt * dt, rel=1e-14)
+    ie, ke = energies(o)
+    assert ke == pytest.approx(1.5 * ua * ua, rel=1e-14)
+    assert ie + ke == pytest.approx(2.5, rel=1e-15)
+
+
+def test_spec_interface_force():
+    """1D two-cell p = (1, 0), width 0.5, unit cross-section, lateral
+    faces reflecting -> the interface nodes' x-forces sum to 1 toward the
+    low-pressure side.  Measured through one cycle: sum M du_x / dt = F_x."""
+    cfg = sedov((2, 1, 1), LAGRANGE, reflect_mask=0x3F, gamma=1.5)
+    o = O.Oracle(cfg)
+    # rho = 1 in both cells: p0 = (1.5-1)*1*2 = 1, p1 = 0 (all six faces reflect)
+    o.set("E", np.array([[[2.0, 0.0]]]))
+    rc, _ = o.step(1)
+    assert rc == 0
+    dt = o.clock()["dt_last"]
+    M = o.get("NODE_MASS")
+    ux = o.get("UX")
+    Fx = (M[:, :, 1] * ux[:, :, 1]).sum() / dt
+    assert Fx == pytest.approx(1.0, rel=1e-14)
+
+
+# ---------------------------------------------------------------- fixed points
+def test_quiescent_uniform_state_bitwise_fixed_point():
+    # S:365 / SURVEY c.9: gamma=1.5, e=2, rho=1 -> p=1; all faces reflecting
+    cfg, o = uniform_state(4, LAGRANGE, 0x3F)
+    before = {f: o.get(f) for f in ("X", "Y", "Z", "UX", "UY", "UZ", "E", "MASS")}
+    rc, done = o.step(5)
+    assert rc == 0 and done == 5
+    for f, v in before.items():
+        assert np.array_equal(o.get(f), v), f
+
+
+def test_quiescent_uniform_state_fixed_point_general_gamma():
+    cfg, o = uniform_state(5, LAGRANGE, 0x3F, gamma=1.4, e=2.5)
+    e0 = o.get("E")
+    o.step(5)
+    assert np.max(np.abs(o.get("E") - e0)) <= 1e-14
+    assert np.max(np.abs(o.get("UX"))) <= 1e-13
+
+
+def test_euler_quiescent_fixed_point_bitwise():
+    cfg, o = uniform_state(4, EULER, 0x3F)
+    before = {f: o.get(f) for f in ("UX", "UY", "UZ", "E", "MASS")}
+    rc, done = o.step(4)
+    assert rc == 0 and done == 4
+    for f, v in before.items():
+        assert np.array_equal(o.get(f), v), f
+
+
+def test_galilean_translation_zero_pressure():
+    # S:373 / c.9: p = 0, uniform u, all free -> q = 0, e == 0 bitwise, pure translation
+    cfg = sedov((4, 3, 5), LAGRANGE, reflect_mask=0, e_deposit=0.0, e_background=0.0)
+    o = O.Oracle(cfg)
+    U = inputs.uniform_velocity(cfg, (0.3, -0.2, 0.1))
+    for k in ("ux", "uy", "uz"):
+        o.set(k.upper(), U[k])
+    X0 = o.get("X"); V0 = o.get("VOL")
+    rc, done = o.step(7)
+    assert rc == 0
+    assert np.array_equal(o.get("E"), np.zeros(o.cell_shape))
+    assert np.array_equal(o.get("UX"), U["ux"])
+    t = o.clock()["t"]
+    assert np.allclose(o.get("X"), X0 + 0.3 * t, rtol=0, atol=1e-14)
+    assert np.allclose(o.get("VOL"), V0, rtol=1e-13)
+    assert np.array_equal(o.get("Q"), np.zeros(o.cell_shape))
+
+
+# -------------------------------------------------------------- conservation
+def test_lagrange_mass_bitwise_and_energy_conservation_C0():
+    cfg, cycles = config("C0")
+    o = O.Oracle(cfg)
+    m0 = o.get("MASS")
+    E0 = sum(energies(o))
+    rc, done = o.step(cycles)
+    assert rc == 0 and done == cycles
+    assert np.array_equal(o.get("MASS"), m0)
+    ie, ke = energies(o)
+    assert abs(ie + ke - E0) / E0 <= 1e-12
+    assert ke > 0.1  # the blast actually moved material
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_lagrange_energy_and_momentum_free_body(seed):
+    # all faces free: total momentum stays 0 (sum of face areas of a closed cell = 0)
+    cfg = sedov((6, 5, 4), LAGRANGE, reflect_mask=0, e_background=1.0, e_deposit=3.0)
+    o = O.Oracle(cfg)
+    pert = inputs.perturbation(cfg, seed, u_scale=0.0)
+    for a, f in (("dx", "X"), ("dy", "Y"), ("dz", "Z")):
+        o.set(f, o.get(f) + pert[a])
+    o.set("E", o.get("E") * pert["e_factor"])
+    E0 = sum(energies(o))
+    rc, _ = o.step(20)
+    assert rc == 0
+    M = o.get("NODE_MASS")
+    for f in ("UX", "UY", "UZ"):
+        mom = math.fsum((M * o.get(f)).ravel())
+        scale = math.fsum((M * np.abs(o.get(f))).ravel())
+        assert abs(mom) <= 1e-13 * scale
+    assert abs(sum(energies(o)) - E0) / E0 <= 1e-13
+
+
+def test_euler_mass_conservation_and_positivity():
+    cfg = sedov((12, 12, 12), EULER)
+    o = O.Oracle(cfg)
+    m0 = math.fsum(o.get("MASS").ravel())
+    rc, done = o.step(30)
+    assert rc == 0 and done == 30
+    m = o.get("MASS")
+    assert (m > 0).all()
+    assert math.fsum(m.ravel()) == pytest.approx(m0, rel=1e-13)
+    assert np.array_equal(o.get("X"), O.Oracle(cfg).get("X"))  # x := x^T
+
+
+def test_remap_uniform_translation_preserves_interior():
+    # uniform rho, e, u are preserved by the remap (interior cells)
+    cfg = sedov((8, 8, 8), EULER, reflect_mask=0, e_deposit=0.0, e_background=0.0)
+    o = O.Oracle(cfg)
+    U = inputs.uniform_velocity(cfg, (0.2, 0.1, -0.15))
+    for k in ("ux", "uy", "uz"):
+        o.set(k.upper(), U[k])
+    rc, _ = o.step(1)
+    assert rc == 0
+    rho = o.get("RHO")[1:-1, 1:-1, 1:-1]
+    assert np.max(np.abs(rho - 1.0)) <= 1e-13
+    ux = o.get("UX")[2:-2, 2:-2, 2:-2]
+    assert np.max(np.abs(ux - 0.2)) <= 1e-13
+
+
+# ------------------------------------------------------------------- Sedov
+def test_octant_symmetry_C0():
+    # SURVEY c.9: e(i,j,k) vs e(j,i,k) etc. to 1e-10 relative
+    cfg, cycles = config("C0")
+    o = O.Oracle(cfg)
+    o.step(cycles)
+    e = o.get("E")
+    s = np.abs(e).max()
+    for perm in ((0, 2, 1), (2, 1, 0), (1, 0, 2)):
+        assert np.max(np.abs(e - e.transpose(perm))) <= 1e-10 * s
+
+
+@pytest.mark.slow
+def test_sedov_similarity_law_euler():
+    """Shock radius vs R(t) = xi0 (E t^2 / rho0)^(1/5), full-space energy E = 8 E0
+    (Q13), xi0(gamma=1.4) = 1.0328 (Sedov 1959 / Taylor 1950 tabulated constant;
+    SURVEY Q14).  Within 10% and fitted exponent 0.4 +- 0.05."""
+    n = 32
+    cfg = sedov((n, n, n), EULER)
+    o = O.Oracle(cfg)
+    ts, rs = [], []
+    h = 1.0 / n
+    for _ in range(10):
+        assert o.step(20)[0] == 0
+        t = o.clock()["t"]
+        rho = o.get("RHO")
+        # shell-averaged radius of the density peak
+        k, j, i = np.meshgrid(*(np.arange(n) + 0.5,) * 3, indexing="ij")
+        r = h * np.sqrt(i * i + j * j + k * k)
+        bins = np.arange(0, 1.0, h)
+        idx = np.digitize(r.ravel(), bins)
+        prof = np.bincount(idx, weights=rho.ravel()) / np.maximum(np.bincount(idx), 1)
+        R = bins[np.argmax(prof) - 1] + 0.5 * h
+        Rth = 1.0328 * (8.0 * 1.0 * t * t / 1.0) ** 0.2
+        if Rth > 0.2:
+            assert abs(R - Rth) / Rth <= 0.10, (t, R, Rth)
+            ts.append(t); rs.append(R)
+    slope = np.polyfit(np.log(ts), np.log(rs), 1)[0]
+    assert abs(slope - 0.4) <= 0.05
+
+
+# ------------------------------------------------------------------ errors
+def test_invalid_params():
+    cfg = sedov((4, 4, 4), LAGRANGE, gamma=1.0)
+    with pytest.raises(ValueError):
+        O.Oracle(cfg)
+    cfg = sedov((0, 4, 4), LAGRANGE)
+    with pytest.raises(ValueError):
+        O.Oracle(cfg)
+
+
+def test_set_x_in_euler_is_einval():
+    cfg = sedov((4, 4, 4), EULER)
+    o = O.Oracle(cfg)
+    with pytest.raises(ValueError):
+        o.set("X", o.get("X"))
+
+
+def test_tangled_cell_reports_cycle_and_cell():
+    # fault injection: push an interior node through its neighbour plane
+    cfg = sedov((4, 4, 4), LAGRANGE)
+    o = O.Oracle(cfg)
+    X = o.get("X")
+    X[2, 2, 2] += 2.0   # node (2,2,2) jumps far past the +x cells: V < 0
+    o.set("X", X)
+    rc, done = o.step(3)
+    assert rc == O.ETANGLED and done == 0
+    assert "ETANGLED cycle=0" in o.last_error()
+    # lowest-index inverted cell: (i,j,k) = (2,1,1), the cells with the node as -x corner
+    assert o.last_error_cell() == 2 + 4 * (1 + 4 * 1)
+    assert o.step(1)[0] == O.EPOISONED
+
+
+def test_dt_collapse_with_t_end():
+    cfg = sedov((4, 4, 4), LAGRANGE, t_end=1e20)
+    o = O.Oracle(cfg)
+    rc, done = o.step(2)
+    assert rc == O.EDTCOLLAPSE and done == 0
+
+
+def test_t_end_landing_is_exact():
+    cfg = sedov((6, 6, 6), EULER, t_end=2e-3)
+    o = O.Oracle(cfg)
+    rc, done = o.step(100000)
+    assert rc == 0
+    clk = o.clock()
+    assert clk["t"] == 2e-3 and clk["finished"] == 1
+    rc, done2 = o.step(5)
+    assert rc == 0 and done2 == 0
+
+
+@pytest.mark.parametrize("rezone", [LAGRANGE, EULER])
+def test_checkpoint_resume_bitwise(rezone):
+    cfg = sedov((6, 6, 6), rezone)
+    a = O.Oracle(cfg)
+    a.step(10)
+    b = O.Oracle(cfg)
+    b.step(5)
+    fields = ["UX", "UY", "UZ", "MASS", "E"] + (["X", "Y", "Z"] if rezone == LAGRANGE else [])
+    snap = {f: b.get(f) for f in fields}
+    clk = b.clock()
+    c = O.Oracle(cfg)
+    for f, v in snap.items():
+        c.set(f, v)
+    c.set_clock(clk["t"], clk["dt_last"], clk["cycle"])
+    c.step(5)
+    for f in fields + ["RHO", "P", "Q", "CS", "VOL", "NODE_MASS"]:
+        assert np.array_equal(a.get(f), c.get(f)), f
+    assert a.clock() == c.clock()
