@@ -1,0 +1,179 @@
+/*
+ * sale.h -- C ABI of libsale, the B200-native SALE hot path.
+ *
+ * What it computes: the per-cycle staggered-grid hydro update of the SALE
+ * scheme that ScalSALE (arXiv 2209.01983) is built on -- P:133 ("3D
+ * multi-material hydrodynamic scheme ... based on ... SALE"), P:158 ("apply the
+ * ideal gas equation-of-state"), P:181 (Table I: "Lagrangian rezoning, Eulerian
+ * rezoning, Advection") -- on a structured 3D hexahedral mesh, for the
+ * Sedov-Taylor blast wave (Fig. 2b "3D Eulerian Sedov-Taylor").
+ * The paper gives no discrete equations; the operators are SURVEY.md §8(c)
+ * c.1-c.6 with the readings listed in DESIGN.md §3.  One cycle is:
+ *   Lagrangian phase  S1-S7  (geometry, EoS, viscosity, CFL dt, corner forces,
+ *                             kinematics + reflecting BC, compatible pdV energy)
+ *   Eulerian remap    R1-R5  (rezone = SALE_EULER only: swept volumes,
+ *                             donor-cell fluxes of mass/energy/momentum, reset)
+ *   X1 halo exchange, X2 dt min-reduction   (z-slabs over ranks)
+ *
+ * Data layout, not visible through this ABI: SoA fp64 arrays in HBM, x fastest,
+ * then y, then z planes; one z-slab per rank plus ghost planes.
+ *
+ * Ownership: the caller owns the device workspace, the CUDA stream and the
+ * process group; the library owns the context, its NCCL communicator and a few
+ * bytes of pinned host memory.  A context is not thread-safe.  create / step /
+ * destroy are collective over the ranks of one job.
+ *
+ * Error behaviour: every entry point returns a status code (SALE_OK = 0).  A
+ * numerical error in sale_step (ETANGLED, EDTCOLLAPSE, ENEGMASS) or a CUDA /
+ * NCCL failure poisons the context: later calls return SALE_EPOISONED, except
+ * get_field / get_clock / last_error / destroy.  No entry point aborts or
+ * prints.
+ */
+#ifndef SALE_H
+#define SALE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SALE_ABI_VERSION 1
+
+/* status codes */
+#define SALE_OK 0
+#define SALE_EINVAL 1        /* invalid argument / params / field / count           */
+#define SALE_ENOMEM 2        /* workspace too small or NULL                         */
+#define SALE_ECUDA 3         /* CUDA runtime error (detail in sale_last_error)      */
+#define SALE_ENCCL 4         /* NCCL error                                          */
+#define SALE_ETANGLED 5      /* some cell's new volume V' is not > 0 (c.3 step 7)   */
+#define SALE_EDTCOLLAPSE 6   /* dt_u not > 0, or < 1e-14 * t_end (c.5)             */
+#define SALE_ENEGMASS 7      /* remapped mass m'' not > 0 (c.4 step 3)              */
+#define SALE_EPOISONED 8     /* context unusable after an earlier error             */
+#define SALE_EREPLICA 9      /* replicated interface node planes differ (self-check) */
+
+/* rezone modes */
+#define SALE_LAGRANGE 0
+#define SALE_EULER 1
+
+/* kernel implementation (both are this library's own sm_100a kernels) */
+#define SALE_IMPL_FUSED 0    /* fused z-marching kernels (default)                 */
+#define SALE_IMPL_V0 1       /* one kernel per step, for bring-up and cross-checks */
+
+/* field ids; node fields 0..6, cell fields 7..13 */
+#define SALE_F_X 0
+#define SALE_F_Y 1
+#define SALE_F_Z 2
+#define SALE_F_UX 3
+#define SALE_F_UY 4
+#define SALE_F_UZ 5
+#define SALE_F_NODE_MASS 6   /* derived: M = 0.125 * sum of adjacent cell masses */
+#define SALE_F_MASS 7
+#define SALE_F_E 8           /* specific internal energy                          */
+#define SALE_F_RHO 9         /* derived: m / V                                    */
+#define SALE_F_VOL 10        /* derived: V from the 8 nodes (c.2)                 */
+#define SALE_F_P 11          /* derived: (gamma-1) rho e, not floored             */
+#define SALE_F_Q 12          /* derived: artificial viscosity at the current state */
+#define SALE_F_CS 13         /* derived: sqrt(gamma max(p,0) / rho)               */
+
+typedef struct sale_params {
+    int32_t abi_version;      /* = SALE_ABI_VERSION                                */
+    int32_t nx, ny, nz;       /* GLOBAL cells per axis, each >= 1                  */
+    double lx, ly, lz;        /* domain [0,lx]x[0,ly]x[0,lz]; X_i = (lx*i)/nx      */
+    double gamma;             /* ideal-gas gamma > 1                               */
+    double q_lin, q_quad;     /* viscosity c1 (linear), c2 (quadratic), >= 0       */
+    double cfl;               /* > 0                                               */
+    double dt_growth;         /* dt <= dt_growth * dt_prev, > 0                    */
+    double t_end;             /* <= 0: no end time; else stop when t >= t_end     */
+    int32_t rezone;           /* SALE_LAGRANGE or SALE_EULER                       */
+    uint32_t reflect_mask;    /* bit f set: face f of {-x,+x,-y,+y,-z,+z} reflects
+                                 (normal velocity zeroed); clear: free surface.
+                                 Sedov octant = 0x15                               */
+    double rho0;              /* Sedov ambient density > 0                         */
+    double e_background;      /* Sedov background specific energy                  */
+    double e_deposit;         /* Sedov energy E0 placed in global cell (0,0,0)    */
+    int32_t rank, nranks;     /* this process's rank in [0,nranks)                 */
+    const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0 (see
+                                   sale_nccl_unique_id); must be NULL iff nranks==1 */
+    void* stream;             /* cudaStream_t to enqueue on (NULL = legacy stream) */
+    void* workspace;          /* device memory, >= sale_workspace_bytes(), 256-B
+                                 aligned, owned by the caller, not freed by us     */
+    uint64_t workspace_bytes;
+    int32_t device;           /* CUDA device ordinal this context runs on          */
+    int32_t impl;             /* SALE_IMPL_FUSED or SALE_IMPL_V0                   */
+    int32_t local_slabs;      /* >= 1.  With nranks == 1, split the mesh into this
+                                 many z-slabs on the same device exchanging halos
+                                 by device copies (emulated ranks, used to prove
+                                 decomposition bit-exactness on one GPU).  Must be
+                                 1 when nranks > 1.                                */
+    int32_t reserved;
+} sale_params;
+
+typedef struct sale_ctx sale_ctx;
+
+/* Device bytes this rank needs (state ping-pong buffers + ghosts + scratch).
+ * Returns 0 if the parameters are invalid (same checks as sale_create). */
+uint64_t sale_workspace_bytes(const sale_params* p);
+
+/* Writes a fresh 128-byte NCCL unique id into id_out (call on rank 0, then
+ * broadcast it).  SALE_ENCCL on failure. */
+int32_t sale_nccl_unique_id(void* id_out_128);
+
+/* Validate; carve the workspace; NCCL init when nranks > 1; Sedov initial state
+ * (c.6: x = x^T, u = 0, m = rho0 V, e = e_bg, e_000 = E0/m_000); sync.
+ * On error *out is NULL and nothing leaks. */
+int32_t sale_create(const sale_params* p, sale_ctx** out);
+
+/* Enqueue up to ncycles cycles on the stream, then synchronise once.  Each
+ * step call starts with a halo exchange and a dt-candidate pass, so state set
+ * with sale_set_field / sale_set_clock is always honoured.  Stops early (status
+ * OK, *cycles_done < ncycles) when t >= t_end.  On a numerical error returns its
+ * code, sets *cycles_done to the number of good cycles, poisons the context. */
+int32_t sale_step(sale_ctx* c, int32_t ncycles, int32_t* cycles_done);
+
+/* Enqueue only (no synchronisation, no status read-back): for timing loops.
+ * The next sale_step / sale_sync reports errors that happened meanwhile. */
+int32_t sale_step_async(sale_ctx* c, int32_t ncycles);
+/* Synchronise the stream, read back status; *cycles_done = good cycles since the
+ * last sale_sync / sale_step. */
+int32_t sale_sync(sale_ctx* c, int32_t* cycles_done);
+
+/* Copy this rank's owned slab of a field.  Node fields cover global z node
+ * planes [k0, k1] (the interface plane is replicated on both owners), cell
+ * fields cover cell planes [k0, k1); with local_slabs > 1 the whole mesh is
+ * assembled (replicated planes are checked bit-equal, else SALE_EREPLICA).
+ * count must equal the slab size: (nx+1)(ny+1)(k1-k0+1) or nx*ny*(k1-k0),
+ * else SALE_EINVAL.  dst_on_device != 0: dst is device memory on this device.
+ * Layout of dst: x fastest, then y, then z. */
+int32_t sale_get_field(sale_ctx* c, int32_t field, double* dst, uint64_t count,
+                       int32_t dst_on_device);
+
+/* Overwrite a state field (X, Y, Z in Lagrange mode only; UX, UY, UZ; MASS; E)
+ * on this rank's owned slab (same shape and layout as get_field).  Replicated
+ * interface planes must be identical on both owners. */
+int32_t sale_set_field(sale_ctx* c, int32_t field, const double* src, uint64_t count,
+                       int32_t src_on_device);
+
+/* clock: t, dt of the last completed cycle (< 0: none yet), completed cycles,
+ * finished = (t_end > 0 && t >= t_end) */
+int32_t sale_get_clock(sale_ctx* c, double* t, double* dt_last, int64_t* cycle,
+                       int32_t* finished);
+int32_t sale_set_clock(sale_ctx* c, double t, double dt_last, int64_t cycle);
+
+/* owned global cell planes [k0, k1) of this rank (remainder planes go to the
+ * lowest ranks); with local_slabs > 1 the union [0, nz). */
+int32_t sale_get_layout(sale_ctx* c, int32_t* k0, int32_t* k1);
+
+/* kernels launched so far by this context (all of them are libsale's own) */
+int64_t sale_kernel_launches(const sale_ctx* c);
+
+/* human-readable detail of the last error: code, cycle, cell, CUDA/NCCL text */
+const char* sale_last_error(const sale_ctx* c);
+
+/* NULL-safe.  Destroys the NCCL communicator; never frees workspace or stream. */
+void sale_destroy(sale_ctx* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SALE_H */

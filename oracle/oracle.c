@@ -328,7 +328,7 @@ static double dt_cfl_of_state(oracle_ctx* c)
 {
     const oracle_params* p = &c->p;
     double best = 0.0;
-    int have = 0;
+    int have = 0, any_nan = 0;
     for (int64_t k = 0; k < c->nz; ++k)
         for (int64_t j = 0; j < c->ny; ++j)
             for (int64_t i = 0; i < c->nx; ++i) {
@@ -355,10 +355,13 @@ static double dt_cfl_of_state(oracle_ctx* c)
                     v2 = (h == 0) ? s2 : dmax(v2, s2);
                 }
                 double dtK = dt_cell(p->cfl, l2, v2, cs);
+                if (dtK != dtK) any_nan = 1;
                 if (!have) { best = dtK; have = 1; }
                 else best = dmin(best, dtK);
             }
-    return best;
+    /* a NaN candidate anywhere makes dt_cfl NaN (order-free), which trips the
+     * !(dt_u > 0) collapse check (reading Q21). */
+    return any_nan ? NAN : best;
 }
 
 /* c.5: returns 0 and *dt, or an error code. */

@@ -1,0 +1,280 @@
+// kernels_common.cu -- initialisation, clock / dt finalisation, dt candidate,
+// derived fields.  SURVEY §8(c) c.1, c.5, c.6.
+#include <cuda_runtime.h>
+
+#include "sale_mesh.cuh"
+
+namespace sale {
+
+static inline unsigned grid_for(long long n, int bs)
+{
+    long long g = (n + bs - 1) / bs;
+    return (unsigned)(g > 0 ? g : 1);
+}
+
+// c.1: X_i = (lx*i)/nx etc.; Z over the slab's local node planes
+__global__ void k_init_tables(Slab s, Phys p)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t <= p.nx) s.Xt[t] = (p.lx * (double)t) / (double)p.nx;
+    if (t <= p.ny) s.Yt[t] = (p.ly * (double)t) / (double)p.ny;
+    if (t < s.nzn) s.Zt[t] = (p.lz * (double)(s.kb + t)) / (double)p.nz;
+}
+
+// c.6 Sedov: x = x^T, u = 0 on every local node plane inside the domain
+__global__ void k_sedov_nodes(Slab s, Phys p)
+{
+    long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long total = s.pn * s.nzn;
+    if (n >= total) return;
+    int l = (int)(n / s.pn);
+    int k = s.kb + l;
+    if (k < 0 || k > p.nz) return;
+    long long r = n % s.pn;
+    int j = (int)(r / (p.nx + 1)), i = (int)(r % (p.nx + 1));
+    if (!p.rezone) {
+        s.x[0][0][n] = s.Xt[i];
+        s.x[0][1][n] = s.Yt[j];
+        s.x[0][2][n] = s.Zt[l];
+    }
+    s.u[0][0][n] = 0.0;
+    s.u[0][1][n] = 0.0;
+    s.u[0][2][n] = 0.0;
+}
+
+// c.6 Sedov: m = rho0 * V(x^T); e = e_bg; e_000 = E0 / m_000
+__global__ void k_sedov_cells(Slab s, Phys p)
+{
+    long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long total = s.pc * s.nzc;
+    if (c >= total) return;
+    int k = s.kb + (int)(c / s.pc);
+    if (k < 0 || k >= p.nz) return;
+    long long r = c % s.pc;
+    int j = (int)(r / p.nx), i = (int)(r % p.nx);
+    D3 N[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) N[h] = tpos(s, i + (h & 1), j + ((h >> 1) & 1), k + (h >> 2));
+    double m = p.rho0 * hex_volume(N);
+    s.m[0][c] = m;
+    s.e[0][c] = (i == 0 && j == 0 && k == 0) ? p.e_dep / m : p.e_bg;
+}
+
+int launch_init_tables(const Slab& s, const Phys& p, Stream st)
+{
+    int n = p.nx > p.ny ? p.nx : p.ny;
+    n = n > s.nzn ? n : s.nzn;
+    k_init_tables<<<grid_for(n + 1, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    return 1;
+}
+
+int launch_sedov_init(const Slab& s, const Phys& p, Stream st)
+{
+    k_sedov_nodes<<<grid_for(s.pn * s.nzn, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    k_sedov_cells<<<grid_for(s.pc * s.nzc, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    return 2;
+}
+
+// ---------------------------------------------------------------- clock
+__global__ void k_prep(DevState* d)
+{
+    d->cand_key = KEY_NONE;
+    d->err_key = KEY_NONE;
+    d->active = 0;
+}
+
+__device__ __forceinline__ void commit(DevState* d)
+{
+    if (!d->active) return;
+    d->active = 0;
+    if (d->err_key != KEY_NONE) {
+        unsigned long long order = d->err_key >> 48;
+        d->status = (order == ERR_ORDER_TANGLED) ? S_ETANGLED : S_ENEGMASS;
+        d->err_cycle = d->cycle;
+        d->err_cell = (long long)(d->err_key & 0xFFFFFFFFFFFFull);
+        return;
+    }
+    d->t = d->t + d->dt;
+    d->cycle = d->cycle + 1;
+    d->dt_prev = d->dt;
+    d->good = d->good + 1;
+}
+
+// commit the cycle in flight, then c.5: finalise dt from the reduced candidate
+__global__ void k_begin(DevState* d, Phys p)
+{
+    commit(d);
+    if (d->status) return;
+    if (p.t_end > 0.0 && d->t >= p.t_end) {
+        d->finished = 1;
+        return;
+    }
+    double dt_cfl = dt_unkey(d->cand_key);
+    double dt_u = (d->dt_prev < 0.0) ? dt_cfl : dmin(dt_cfl, p.growth * d->dt_prev);
+    if (!(dt_u > 0.0) || (p.t_end > 0.0 && dt_u < 1e-14 * p.t_end)) {
+        d->status = S_EDTCOLLAPSE;
+        d->err_cycle = d->cycle;
+        d->err_cell = -1;
+        return;
+    }
+    d->dt = (p.t_end > 0.0) ? dmin(dt_u, p.t_end - d->t) : dt_u;
+    d->cand_key = KEY_NONE;
+    d->err_key = KEY_NONE;
+    d->active = 1;
+}
+
+__global__ void k_commit(DevState* d, Phys p)
+{
+    commit(d);
+    if (!d->status && p.t_end > 0.0 && d->t >= p.t_end) d->finished = 1;
+}
+
+__global__ void k_reset_good(DevState* d) { d->good = 0; }
+
+int launch_prep(DevState* d, Stream st)
+{
+    k_prep<<<1, 1, 0, (cudaStream_t)st>>>(d);
+    return 1;
+}
+int launch_begin(DevState* d, const Phys& p, Stream st)
+{
+    k_begin<<<1, 1, 0, (cudaStream_t)st>>>(d, p);
+    return 1;
+}
+int launch_commit(DevState* d, const Phys& p, Stream st)
+{
+    k_commit<<<1, 1, 0, (cudaStream_t)st>>>(d, p);
+    return 1;
+}
+int launch_reset_good(DevState* d, Stream st)
+{
+    k_reset_good<<<1, 1, 0, (cudaStream_t)st>>>(d);
+    return 1;
+}
+
+// ------------------------------------------------------- c.5 dt candidate
+// per owned cell: dt_K from (x, u, m, e) of buffer `cur`; block min -> atomicMin
+template <bool EULER>
+__global__ void k_dt_candidate(Slab s, Phys p, int cur, int gate)
+{
+    if (gate && !s.st->active) return;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long total = s.pc * (s.k1 - s.k0);
+    unsigned long long key = KEY_NONE;
+    if (t < total) {
+        int k = s.k0 + (int)(t / s.pc);
+        long long r = t % s.pc;
+        int j = (int)(r / p.nx), i = (int)(r % p.nx);
+        D3 N[8], U[8];
+        load_hex_pos<EULER>(s, p, cur, i, j, k, N);
+        load_hex3(s, p, s.u[cur], i, j, k, U);
+        long long c = cidx(s, p, i, j, k);
+        double V = hex_volume(N);
+        double rho = mass_cur(s, p, cur)[c] / V, pr, pf, cs;
+        eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
+        key = dt_key(dt_cell(p.cfl, hex_min_edge2(N), hex_max_speed2(U), cs));
+    }
+    block_min_atomic(key, &s.st->cand_key);
+}
+
+static int dt_candidate(const Slab& s, const Phys& p, int cur, int gate, Stream st)
+{
+    long long n = s.pc * (s.k1 - s.k0);
+    if (p.rezone)
+        k_dt_candidate<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, gate);
+    else
+        k_dt_candidate<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, gate);
+    return 1;
+}
+// ungated: at the start of sale_step, on the current state
+int launch_dt_candidate(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    return dt_candidate(s, p, cur, 0, st);
+}
+// gated on DevState.active: at the end of a cycle, on the new state
+int launch_dt_candidate_gated(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    return dt_candidate(s, p, cur, 1, st);
+}
+
+// ------------------------------------------------------- derived fields
+// Writes the owned slab of a derived field into s.der, compact (plane k-k0).
+// field ids as in include/sale.h.
+template <bool EULER>
+__global__ void k_derive_cells(Slab s, Phys p, int cur, int field)
+{
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long total = s.pc * (s.k1 - s.k0);
+    if (t >= total) return;
+    int k = s.k0 + (int)(t / s.pc);
+    long long r = t % s.pc;
+    int j = (int)(r / p.nx), i = (int)(r % p.nx);
+    D3 N[8], A[6], Xb[6];
+    double sv[6];
+    load_hex_pos<EULER>(s, p, cur, i, j, k, N);
+    hex_faces(N, A, Xb, sv);
+    long long c = cidx(s, p, i, j, k);
+    double V = vol_from_s(sv);
+    double rho = mass_cur(s, p, cur)[c] / V, pr, pf, cs;
+    eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
+    double v;
+    switch (field) {
+    case 9: v = rho; break;
+    case 10: v = V; break;
+    case 11: v = pr; break;
+    case 13: v = cs; break;
+    default: {
+        D3 U[8];
+        load_hex3(s, p, s.u[cur], i, j, k, U);
+        v = hex_q(Xb, U, rho, cs, p.c1, p.c2);
+    }
+    }
+    s.der[t] = v;
+}
+
+// NODE_MASS (c.3 step 5) and, in Euler mode, X/Y/Z = x^T
+__global__ void k_derive_nodes(Slab s, Phys p, int cur, int field)
+{
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long total = s.pn * (s.k1 - s.k0 + 1);
+    if (t >= total) return;
+    int k = s.k0 + (int)(t / s.pn);
+    long long r = t % s.pn;
+    int j = (int)(r / (p.nx + 1)), i = (int)(r % (p.nx + 1));
+    double v;
+    if (field <= 2) {
+        D3 X = tpos(s, i, j, k);
+        v = field == 0 ? X.x : (field == 1 ? X.y : X.z);
+    } else {
+        const double* m = mass_cur(s, p, cur);
+        double M = 0.0;
+        bool first = true;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            int ci = i - 1 + (g & 1), cj = j - 1 + ((g >> 1) & 1), ck = k - 1 + (g >> 2);
+            if (!cell_in(p, ci, cj, ck)) continue;
+            double mk = m[cidx(s, p, ci, cj, ck)];
+            M = first ? mk : M + mk;
+            first = false;
+        }
+        v = 0.125 * M;
+    }
+    s.der[t] = v;
+}
+
+int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st)
+{
+    if (field <= 6) {
+        long long n = s.pn * (s.k1 - s.k0 + 1);
+        k_derive_nodes<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, field);
+    } else {
+        long long n = s.pc * (s.k1 - s.k0);
+        if (p.rezone)
+            k_derive_cells<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, field);
+        else
+            k_derive_cells<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, field);
+    }
+    return 1;
+}
+
+}  // namespace sale

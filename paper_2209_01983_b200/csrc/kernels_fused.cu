@@ -1,0 +1,12 @@
+// kernels_fused.cu -- fused z-marching kernels (not yet implemented).
+#include <cuda_runtime.h>
+
+#include "sale_mesh.cuh"
+
+namespace sale {
+
+bool fused_available() { return false; }
+
+int launch_cycle_fused(const Slab&, const Phys&, int, Stream) { return 0; }
+
+}  // namespace sale

@@ -1,0 +1,649 @@
+// sale_host.cu -- the C ABI of libsale (include/sale.h): parameter validation,
+// workspace carving, z-slab layout, cycle enqueueing, halo exchange (device
+// copies between local slabs, NCCL send/recv between ranks), dt / error
+// min-reduction (NCCL allreduce), field access.
+//
+// Paper context: ScalSALE's kernel layer owns the data structures
+// (Data3d with ghost frames) and the Communication / CommParams
+// classes doing blocking and non-blocking ghost exchange
+// (P:372-375).  Here that becomes: SoA fp64 slabs with ghost z-planes,
+// one grouped NCCL exchange + one 16-byte allreduce-min per cycle, all enqueued
+// on the caller's stream with no host synchronisation inside sale_step's loop.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sale.h"
+#include "sale_internal.h"
+
+static_assert(SALE_OK == sale::S_OK && SALE_ETANGLED == sale::S_ETANGLED &&
+                  SALE_EDTCOLLAPSE == sale::S_EDTCOLLAPSE && SALE_ENEGMASS == sale::S_ENEGMASS &&
+                  SALE_EREPLICA == sale::S_EREPLICA,
+              "status codes out of sync");
+static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+static_assert(offsetof(sale::DevState, err_key) == offsetof(sale::DevState, cand_key) + 8,
+              "cand_key / err_key must be adjacent for the 2-element allreduce");
+
+using sale::DevState;
+using sale::Phys;
+using sale::Slab;
+
+struct sale_ctx {
+    sale_params prm;
+    Phys phys;
+    int g = 1;                       // ghost depth
+    std::vector<Slab> slabs;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    DevState* dstate = nullptr;      // device
+    DevState* hstate = nullptr;      // pinned host mirror
+    int cur = 0;                     // parity of the current state at the last sync
+    int cur_enq = 0;                 // parity the next enqueued cycle reads
+    bool poisoned = false;
+    long long launches = 0;
+    std::string err = "OK";
+};
+
+namespace {
+
+const char* code_name(int c)
+{
+    switch (c) {
+    case SALE_OK: return "OK";
+    case SALE_EINVAL: return "EINVAL";
+    case SALE_ENOMEM: return "ENOMEM";
+    case SALE_ECUDA: return "ECUDA";
+    case SALE_ENCCL: return "ENCCL";
+    case SALE_ETANGLED: return "ETANGLED";
+    case SALE_EDTCOLLAPSE: return "EDTCOLLAPSE";
+    case SALE_ENEGMASS: return "ENEGMASS";
+    case SALE_EPOISONED: return "EPOISONED";
+    case SALE_EREPLICA: return "EREPLICA";
+    default: return "E?";
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int ghost_depth(const sale_params* p) { return p->rezone == SALE_EULER ? 3 : 1; }
+
+bool params_ok(const sale_params* p)
+{
+    if (!p || p->abi_version != SALE_ABI_VERSION) return false;
+    if (p->nx < 1 || p->ny < 1 || p->nz < 1) return false;
+    if (!(p->lx > 0.0) || !(p->ly > 0.0) || !(p->lz > 0.0)) return false;
+    if (!(p->gamma > 1.0) || !(p->cfl > 0.0) || !(p->dt_growth > 0.0)) return false;
+    if (!(p->q_lin >= 0.0) || !(p->q_quad >= 0.0)) return false;
+    if (p->rezone != SALE_LAGRANGE && p->rezone != SALE_EULER) return false;
+    if (p->reflect_mask > 0x3Fu) return false;
+    if (!(p->rho0 > 0.0)) return false;
+    if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return false;
+    if ((p->nranks == 1) != (p->nccl_unique_id == nullptr)) return false;
+    if (p->local_slabs < 1 || (p->nranks > 1 && p->local_slabs != 1)) return false;
+    if (p->impl != SALE_IMPL_V0 && p->impl != SALE_IMPL_FUSED) return false;
+    int T = p->nranks * p->local_slabs;
+    if (p->nz < T) return false;
+    if (T > 1 && p->nz / T < ghost_depth(p)) return false;  // every slab owns >= g planes
+    if ((long long)(p->nx + 1) * (p->ny + 1) > (1ll << 40)) return false;
+    return true;
+}
+
+// slab s of T: remainder planes go to the lowest slabs
+void slab_range(int nz, int T, int s, int& k0, int& k1)
+{
+    int base = nz / T, rem = nz % T;
+    k0 = s * base + (s < rem ? s : rem);
+    k1 = k0 + base + (s < rem ? 1 : 0);
+}
+
+const size_t ALIGN = 256;
+size_t align_up(size_t v) { return (v + ALIGN - 1) / ALIGN * ALIGN; }
+
+// carve one slab's arrays from base (nullptr: size only); returns bytes used
+size_t carve_slab(const sale_params* p, Slab& s, char* base)
+{
+    size_t off = 0;
+    auto take = [&](long long ndouble) -> double* {
+        double* ptr = base ? reinterpret_cast<double*>(base + off) : nullptr;
+        off += align_up(sizeof(double) * (size_t)ndouble);
+        return ptr;
+    };
+    long long nn = s.pn * s.nzn, nc = s.pc * s.nzc;
+    bool euler = p->rezone == SALE_EULER;
+    for (int b = 0; b < 2; ++b)
+        for (int a = 0; a < 3; ++a) {
+            s.x[b][a] = euler ? nullptr : take(nn);
+            s.u[b][a] = take(nn);
+        }
+    s.m[0] = take(nc);
+    s.m[1] = euler ? take(nc) : nullptr;
+    s.e[0] = take(nc);
+    s.e[1] = take(nc);
+    s.sig = take(nc);
+    for (int a = 0; a < 3; ++a) {
+        s.x1[a] = euler ? take(nn) : nullptr;
+        s.u1[a] = euler ? take(nn) : nullptr;
+        s.dP[a] = euler ? take(nc) : nullptr;
+    }
+    s.e1 = euler ? take(nc) : nullptr;
+    s.V1 = euler ? take(nc) : nullptr;
+    s.dm = euler ? take(nc) : nullptr;
+    s.der = take(s.pn * (long long)(s.k1 - s.k0 + 1));
+    s.Xt = take(p->nx + 1);
+    s.Yt = take(p->ny + 1);
+    s.Zt = take(s.nzn);
+    return off;
+}
+
+void layout_slabs(const sale_params* p, std::vector<Slab>& out)
+{
+    int g = ghost_depth(p);
+    int T = p->nranks * p->local_slabs;
+    out.clear();
+    for (int l = 0; l < p->local_slabs; ++l) {
+        Slab s;
+        std::memset(&s, 0, sizeof s);
+        int sid = p->rank * p->local_slabs + l;
+        slab_range(p->nz, T, sid, s.k0, s.k1);
+        s.g = g;
+        s.kb = s.k0 - g;
+        s.nzc = (s.k1 - s.k0) + 2 * g;
+        s.nzn = s.nzc + 1;
+        s.pn = (long long)(p->nx + 1) * (p->ny + 1);
+        s.pc = (long long)p->nx * p->ny;
+        out.push_back(s);
+    }
+}
+
+size_t total_bytes(const sale_params* p)
+{
+    std::vector<Slab> v;
+    layout_slabs(p, v);
+    size_t total = align_up(sizeof(DevState));
+    for (auto& s : v) total += carve_slab(p, s, nullptr);
+    return total;
+}
+
+int set_err(sale_ctx* c, int code, const std::string& msg)
+{
+    if (c) {
+        c->err = std::string(code_name(code)) + ": " + msg;
+        if (code != SALE_EINVAL && code != SALE_ENOMEM) c->poisoned = true;
+    }
+    return code;
+}
+
+int cuda_check(sale_ctx* c, cudaError_t e, const char* what)
+{
+    if (e == cudaSuccess) return SALE_OK;
+    return set_err(c, SALE_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int nccl_check(sale_ctx* c, ncclResult_t r, const char* what)
+{
+    if (r == ncclSuccess) return SALE_OK;
+    return set_err(c, SALE_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+int launch_check(sale_ctx* c)
+{
+    return cuda_check(c, cudaGetLastError(), "kernel launch");
+}
+
+// which arrays travel in a halo exchange
+struct FieldSet {
+    std::vector<double*> node_lo, node_hi;  // filled per slab pair
+};
+
+void state_arrays(const sale_ctx* c, const Slab& s, int b, bool include_mass,
+                  std::vector<double*>& nodes, std::vector<double*>& cells)
+{
+    nodes.clear();
+    cells.clear();
+    bool euler = c->prm.rezone == SALE_EULER;
+    if (!euler)
+        for (int a = 0; a < 3; ++a) nodes.push_back(s.x[b][a]);
+    for (int a = 0; a < 3; ++a) nodes.push_back(s.u[b][a]);
+    if (euler)
+        cells.push_back(s.m[b]);
+    else if (include_mass)
+        cells.push_back(s.m[0]);
+    cells.push_back(s.e[b]);
+}
+
+// X1: ghost planes between neighbouring slabs, buffer b
+int exchange(sale_ctx* c, int b, bool include_mass)
+{
+    const int g = c->g;
+    const size_t pn = (size_t)c->slabs[0].pn, pc = (size_t)c->slabs[0].pc;
+    std::vector<double*> nL, cL, nU, cU;
+    // local slab pairs: device-to-device copies
+    for (size_t l = 0; l + 1 < c->slabs.size(); ++l) {
+        const Slab& L = c->slabs[l];
+        const Slab& U = c->slabs[l + 1];
+        int kI = L.k1;
+        state_arrays(c, L, b, include_mass, nL, cL);
+        state_arrays(c, U, b, include_mass, nU, cU);
+        for (size_t f = 0; f < nL.size(); ++f) {
+            // U ghost nodes [kI-g, kI-1] <- L ; L ghost nodes [kI+1, kI+g] <- U
+            size_t bytes = sizeof(double) * pn * g;
+            cudaMemcpyAsync(nU[f] + (size_t)(kI - g - U.kb) * pn, nL[f] + (size_t)(kI - g - L.kb) * pn,
+                            bytes, cudaMemcpyDeviceToDevice, c->stream);
+            cudaMemcpyAsync(nL[f] + (size_t)(kI + 1 - L.kb) * pn, nU[f] + (size_t)(kI + 1 - U.kb) * pn,
+                            bytes, cudaMemcpyDeviceToDevice, c->stream);
+        }
+        for (size_t f = 0; f < cL.size(); ++f) {
+            size_t bytes = sizeof(double) * pc * g;
+            cudaMemcpyAsync(cU[f] + (size_t)(kI - g - U.kb) * pc, cL[f] + (size_t)(kI - g - L.kb) * pc,
+                            bytes, cudaMemcpyDeviceToDevice, c->stream);
+            cudaMemcpyAsync(cL[f] + (size_t)(kI - L.kb) * pc, cU[f] + (size_t)(kI - U.kb) * pc,
+                            bytes, cudaMemcpyDeviceToDevice, c->stream);
+        }
+    }
+    int rc = cuda_check(c, cudaGetLastError(), "halo copy");
+    if (rc) return rc;
+    if (c->prm.nranks == 1) return SALE_OK;
+    // ranks: one grouped NCCL exchange with r-1 and r+1 (one slab per rank)
+    const Slab& S = c->slabs[0];
+    int r = c->prm.rank, n = c->prm.nranks;
+    std::vector<double*> nd, cd;
+    state_arrays(c, S, b, include_mass, nd, cd);
+    ncclGroupStart();
+    for (double* a : nd) {
+        size_t cnt = pn * g;
+        if (r > 0) {
+            ncclSend(a + (size_t)(S.k0 + 1 - S.kb) * pn, cnt, ncclFloat64, r - 1, c->comm, c->stream);
+            ncclRecv(a + (size_t)(S.k0 - g - S.kb) * pn, cnt, ncclFloat64, r - 1, c->comm, c->stream);
+        }
+        if (r < n - 1) {
+            ncclSend(a + (size_t)(S.k1 - g - S.kb) * pn, cnt, ncclFloat64, r + 1, c->comm, c->stream);
+            ncclRecv(a + (size_t)(S.k1 + 1 - S.kb) * pn, cnt, ncclFloat64, r + 1, c->comm, c->stream);
+        }
+    }
+    for (double* a : cd) {
+        size_t cnt = pc * g;
+        if (r > 0) {
+            ncclSend(a + (size_t)(S.k0 - S.kb) * pc, cnt, ncclFloat64, r - 1, c->comm, c->stream);
+            ncclRecv(a + (size_t)(S.k0 - g - S.kb) * pc, cnt, ncclFloat64, r - 1, c->comm, c->stream);
+        }
+        if (r < n - 1) {
+            ncclSend(a + (size_t)(S.k1 - g - S.kb) * pc, cnt, ncclFloat64, r + 1, c->comm, c->stream);
+            ncclRecv(a + (size_t)(S.k1 - S.kb) * pc, cnt, ncclFloat64, r + 1, c->comm, c->stream);
+        }
+    }
+    return nccl_check(c, ncclGroupEnd(), "halo exchange");
+}
+
+// X2: min over ranks of (dt candidate key, error key)
+int reduce_keys(sale_ctx* c)
+{
+    if (c->prm.nranks == 1) return SALE_OK;
+    return nccl_check(c,
+                      ncclAllReduce(&c->dstate->cand_key, &c->dstate->cand_key, 2, ncclUint64, ncclMin,
+                                    c->comm, c->stream),
+                      "dt allreduce");
+}
+
+int enqueue_cycles(sale_ctx* c, int ncycles)
+{
+    int rc;
+    int b = c->cur_enq;
+    c->launches += sale::launch_prep(c->dstate, (sale::Stream)c->stream);
+    if ((rc = exchange(c, b, true))) return rc;
+    for (auto& s : c->slabs) c->launches += sale::launch_dt_candidate(s, c->phys, b, (sale::Stream)c->stream);
+    if ((rc = reduce_keys(c))) return rc;
+    for (int n = 0; n < ncycles; ++n) {
+        c->launches += sale::launch_begin(c->dstate, c->phys, (sale::Stream)c->stream);
+        for (auto& s : c->slabs) {
+            if (c->prm.impl == SALE_IMPL_V0)
+                c->launches += sale::launch_cycle_v0(s, c->phys, b, (sale::Stream)c->stream);
+            else
+                c->launches += sale::launch_cycle_fused(s, c->phys, b, (sale::Stream)c->stream);
+        }
+        if ((rc = launch_check(c))) return rc;
+        if ((rc = exchange(c, b ^ 1, false))) return rc;
+        if ((rc = reduce_keys(c))) return rc;
+        b ^= 1;
+    }
+    c->launches += sale::launch_commit(c->dstate, c->phys, (sale::Stream)c->stream);
+    c->cur_enq = b;
+    return launch_check(c);
+}
+
+// synchronise, read the device state, fix the parity from the committed cycles
+int sync_state(sale_ctx* c, int* good_out)
+{
+    int rc = cuda_check(c, cudaMemcpyAsync(c->hstate, c->dstate, sizeof(DevState), cudaMemcpyDeviceToHost,
+                                           c->stream),
+                        "state read");
+    if (rc) return rc;
+    if ((rc = cuda_check(c, cudaStreamSynchronize(c->stream), "stream sync"))) return rc;
+    if (c->prm.nranks > 1) {
+        ncclResult_t ar;
+        if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess)
+            return nccl_check(c, ar, "async");
+    }
+    int good = c->hstate->good;
+    c->cur = (c->cur + good) & 1;
+    c->cur_enq = c->cur;
+    if (good_out) *good_out = good;
+    if (good) {
+        c->launches += sale::launch_reset_good(c->dstate, (sale::Stream)c->stream);
+        c->hstate->good = 0;
+    }
+    int st = c->hstate->status;
+    if (st != SALE_OK && !c->poisoned) {
+        char buf[160];
+        long long cell = c->hstate->err_cell;
+        if (cell >= 0) {
+            long long nx = c->prm.nx, ny = c->prm.ny;
+            std::snprintf(buf, sizeof buf, "cycle=%lld cell=%lld,%lld,%lld", c->hstate->err_cycle, cell % nx,
+                          (cell / nx) % ny, cell / (nx * ny));
+        } else {
+            std::snprintf(buf, sizeof buf, "cycle=%lld", c->hstate->err_cycle);
+        }
+        set_err(c, st, buf);
+    }
+    return st;
+}
+
+bool is_node_field(int f) { return f >= SALE_F_X && f <= SALE_F_NODE_MASS; }
+bool is_cell_field(int f) { return f >= SALE_F_MASS && f <= SALE_F_CS; }
+
+uint64_t owned_count(const sale_ctx* c, const Slab& s, int field)
+{
+    return is_node_field(field) ? (uint64_t)s.pn * (uint64_t)(s.k1 - s.k0 + 1)
+                                : (uint64_t)s.pc * (uint64_t)(s.k1 - s.k0);
+}
+
+uint64_t expected_count(const sale_ctx* c, int field)
+{
+    if (c->prm.local_slabs == 1) return owned_count(c, c->slabs[0], field);
+    const Slab& s = c->slabs[0];
+    return is_node_field(field) ? (uint64_t)s.pn * (uint64_t)(c->prm.nz + 1)
+                                : (uint64_t)s.pc * (uint64_t)c->prm.nz;
+}
+
+// device pointer to the owned data of `field` of slab s (after deriving if needed)
+const double* field_src(sale_ctx* c, const Slab& s, int field)
+{
+    int b = c->cur;
+    bool euler = c->prm.rezone == SALE_EULER;
+    size_t on = (size_t)(s.k0 - s.kb) * s.pn, oc = (size_t)(s.k0 - s.kb) * s.pc;
+    switch (field) {
+    case SALE_F_X:
+    case SALE_F_Y:
+    case SALE_F_Z:
+        if (!euler) return s.x[b][field] + on;
+        break;
+    case SALE_F_UX:
+    case SALE_F_UY:
+    case SALE_F_UZ: return s.u[b][field - SALE_F_UX] + on;
+    case SALE_F_MASS: return (euler ? s.m[b] : s.m[0]) + oc;
+    case SALE_F_E: return s.e[b] + oc;
+    default: break;
+    }
+    c->launches += sale::launch_derive(s, c->phys, b, field, (sale::Stream)c->stream);
+    return s.der;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t sale_workspace_bytes(const sale_params* p)
+{
+    if (!params_ok(p)) return 0;
+    return (uint64_t)total_bytes(p);
+}
+
+int32_t sale_nccl_unique_id(void* id_out_128)
+{
+    if (!id_out_128) return SALE_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return SALE_ENCCL;
+    std::memcpy(id_out_128, &id, sizeof id);
+    return SALE_OK;
+}
+
+int32_t sale_create(const sale_params* p, sale_ctx** out)
+{
+    if (!out) return SALE_EINVAL;
+    *out = nullptr;
+    if (!params_ok(p)) return SALE_EINVAL;
+    size_t need = total_bytes(p);
+    if (!p->workspace || p->workspace_bytes < need || (reinterpret_cast<uintptr_t>(p->workspace) % ALIGN))
+        return SALE_ENOMEM;
+    DeviceGuard guard(p->device);
+    sale_ctx* c = new sale_ctx();
+    c->prm = *p;
+    c->g = ghost_depth(p);
+    c->stream = (cudaStream_t)p->stream;
+    Phys& ph = c->phys;
+    ph.lx = p->lx; ph.ly = p->ly; ph.lz = p->lz;
+    ph.gamma = p->gamma; ph.c1 = p->q_lin; ph.c2 = p->q_quad; ph.cfl = p->cfl;
+    ph.growth = p->dt_growth; ph.t_end = p->t_end;
+    ph.rho0 = p->rho0; ph.e_bg = p->e_background; ph.e_dep = p->e_deposit;
+    ph.nx = p->nx; ph.ny = p->ny; ph.nz = p->nz;
+    ph.reflect = p->reflect_mask; ph.rezone = p->rezone;
+    layout_slabs(p, c->slabs);
+    char* base = static_cast<char*>(p->workspace);
+    c->dstate = reinterpret_cast<DevState*>(base);
+    size_t off = align_up(sizeof(DevState));
+    for (auto& s : c->slabs) {
+        s.st = c->dstate;
+        off += carve_slab(p, s, base + off);
+    }
+    int rc = cuda_check(c, cudaHostAlloc((void**)&c->hstate, sizeof(DevState), cudaHostAllocDefault),
+                        "cudaHostAlloc");
+    if (rc) {
+        delete c;
+        return rc;
+    }
+    std::memset(c->hstate, 0, sizeof(DevState));
+    c->hstate->t = 0.0;
+    c->hstate->dt_prev = -1.0;
+    c->hstate->cand_key = sale::KEY_NONE;
+    c->hstate->err_key = sale::KEY_NONE;
+    c->hstate->err_cell = -1;
+    if (p->nranks > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, p->nccl_unique_id, sizeof id);
+        rc = nccl_check(c, ncclCommInitRank(&c->comm, p->nranks, id, p->rank), "ncclCommInitRank");
+        if (rc) {
+            cudaFreeHost(c->hstate);
+            delete c;
+            return rc;
+        }
+    }
+    rc = cuda_check(c, cudaMemcpyAsync(c->dstate, c->hstate, sizeof(DevState), cudaMemcpyHostToDevice, c->stream),
+                    "state init");
+    for (auto& s : c->slabs) {
+        if (rc) break;
+        c->launches += sale::launch_init_tables(s, ph, (sale::Stream)c->stream);
+        c->launches += sale::launch_sedov_init(s, ph, (sale::Stream)c->stream);
+        rc = launch_check(c);
+    }
+    if (!rc) rc = cuda_check(c, cudaStreamSynchronize(c->stream), "create sync");
+    if (rc) {
+        if (c->comm) ncclCommDestroy(c->comm);
+        cudaFreeHost(c->hstate);
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return SALE_OK;
+}
+
+int32_t sale_step_async(sale_ctx* c, int32_t ncycles)
+{
+    if (!c || ncycles < 0) return SALE_EINVAL;
+    if (c->poisoned) return SALE_EPOISONED;
+    DeviceGuard guard(c->prm.device);
+    return enqueue_cycles(c, ncycles);
+}
+
+int32_t sale_sync(sale_ctx* c, int32_t* cycles_done)
+{
+    if (cycles_done) *cycles_done = 0;
+    if (!c) return SALE_EINVAL;
+    DeviceGuard guard(c->prm.device);
+    int good = 0;
+    int rc = sync_state(c, &good);
+    if (cycles_done) *cycles_done = good;
+    return rc;
+}
+
+int32_t sale_step(sale_ctx* c, int32_t ncycles, int32_t* cycles_done)
+{
+    if (cycles_done) *cycles_done = 0;
+    if (!c || ncycles < 0) return SALE_EINVAL;
+    if (c->poisoned) return SALE_EPOISONED;
+    DeviceGuard guard(c->prm.device);
+    int rc = enqueue_cycles(c, ncycles);
+    if (rc) return rc;
+    return sale_sync(c, cycles_done);
+}
+
+int32_t sale_get_field(sale_ctx* c, int32_t field, double* dst, uint64_t count, int32_t dst_on_device)
+{
+    if (!c || !dst || !(is_node_field(field) || is_cell_field(field))) return SALE_EINVAL;
+    if (count != expected_count(c, field)) return SALE_EINVAL;
+    DeviceGuard guard(c->prm.device);
+    int rc = sync_state(c, nullptr);
+    if (rc && rc != c->hstate->status) return rc;  // CUDA/NCCL failure; numerical status still readable
+    cudaMemcpyKind kind = dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    bool node = is_node_field(field);
+    size_t plane = node ? (size_t)c->slabs[0].pn : (size_t)c->slabs[0].pc;
+    std::vector<double> rep_a, rep_b;
+    for (size_t l = 0; l < c->slabs.size(); ++l) {
+        const Slab& s = c->slabs[l];
+        const double* src = field_src(c, s, field);
+        size_t n = (size_t)owned_count(c, s, field);
+        size_t dst_off = c->prm.local_slabs > 1 ? (size_t)s.k0 * plane : 0;
+        if (node && l > 0) {
+            // replicated interface plane k0: compare with what the lower slab wrote
+            rep_a.resize(plane);
+            rep_b.resize(plane);
+            rc = cuda_check(c, cudaMemcpyAsync(rep_b.data(), src, plane * sizeof(double), cudaMemcpyDeviceToHost,
+                                               c->stream),
+                            "replica read");
+            if (rc) return rc;
+            rc = cuda_check(c, cudaMemcpyAsync(rep_a.data(), dst + dst_off, plane * sizeof(double),
+                                               dst_on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost,
+                                               c->stream),
+                            "replica read");
+            if (rc) return rc;
+            if ((rc = cuda_check(c, cudaStreamSynchronize(c->stream), "replica sync"))) return rc;
+            if (std::memcmp(rep_a.data(), rep_b.data(), plane * sizeof(double)) != 0) {
+                c->err = "EREPLICA: interface node plane differs between slabs";
+                return SALE_EREPLICA;
+            }
+        }
+        rc = cuda_check(c, cudaMemcpyAsync(dst + dst_off, src, n * sizeof(double), kind, c->stream), "field copy");
+        if (rc) return rc;
+        // der is reused per slab: finish this copy before the next derive
+        if ((rc = cuda_check(c, cudaStreamSynchronize(c->stream), "field sync"))) return rc;
+    }
+    return SALE_OK;
+}
+
+int32_t sale_set_field(sale_ctx* c, int32_t field, const double* src, uint64_t count, int32_t src_on_device)
+{
+    if (!c || !src) return SALE_EINVAL;
+    if (c->poisoned) return SALE_EPOISONED;
+    bool euler = c->prm.rezone == SALE_EULER;
+    bool ok = (field >= SALE_F_UX && field <= SALE_F_UZ) || field == SALE_F_MASS || field == SALE_F_E ||
+              (!euler && field >= SALE_F_X && field <= SALE_F_Z);
+    if (!ok || count != expected_count(c, field)) return SALE_EINVAL;
+    DeviceGuard guard(c->prm.device);
+    int rc = sync_state(c, nullptr);
+    if (rc) return rc;
+    bool node = is_node_field(field);
+    size_t plane = node ? (size_t)c->slabs[0].pn : (size_t)c->slabs[0].pc;
+    int b = c->cur;
+    cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (auto& s : c->slabs) {
+        double* arr;
+        if (field <= SALE_F_Z) arr = s.x[b][field];
+        else if (field <= SALE_F_UZ) arr = s.u[b][field - SALE_F_UX];
+        else if (field == SALE_F_MASS) arr = euler ? s.m[b] : s.m[0];
+        else arr = s.e[b];
+        size_t off = (size_t)(s.k0 - s.kb) * plane;
+        size_t src_off = c->prm.local_slabs > 1 ? (size_t)s.k0 * plane : 0;
+        size_t n = (size_t)owned_count(c, s, field);
+        rc = cuda_check(c, cudaMemcpyAsync(arr + off, src + src_off, n * sizeof(double), kind, c->stream),
+                        "set_field copy");
+        if (rc) return rc;
+    }
+    return cuda_check(c, cudaStreamSynchronize(c->stream), "set_field sync");
+}
+
+int32_t sale_get_clock(sale_ctx* c, double* t, double* dt_last, int64_t* cycle, int32_t* finished)
+{
+    if (!c) return SALE_EINVAL;
+    DeviceGuard guard(c->prm.device);
+    int rc = sync_state(c, nullptr);
+    if (rc && rc != c->hstate->status) return rc;
+    if (t) *t = c->hstate->t;
+    if (dt_last) *dt_last = c->hstate->dt_prev;
+    if (cycle) *cycle = c->hstate->cycle;
+    if (finished) *finished = (c->prm.t_end > 0.0 && c->hstate->t >= c->prm.t_end) ? 1 : 0;
+    return SALE_OK;
+}
+
+int32_t sale_set_clock(sale_ctx* c, double t, double dt_last, int64_t cycle)
+{
+    if (!c || cycle < 0) return SALE_EINVAL;
+    if (c->poisoned) return SALE_EPOISONED;
+    DeviceGuard guard(c->prm.device);
+    int rc = sync_state(c, nullptr);
+    if (rc) return rc;
+    c->hstate->t = t;
+    c->hstate->dt_prev = dt_last;
+    c->hstate->cycle = cycle;
+    c->hstate->finished = (c->prm.t_end > 0.0 && t >= c->prm.t_end) ? 1 : 0;
+    rc = cuda_check(c, cudaMemcpyAsync(c->dstate, c->hstate, sizeof(DevState), cudaMemcpyHostToDevice, c->stream),
+                    "set_clock");
+    if (rc) return rc;
+    return cuda_check(c, cudaStreamSynchronize(c->stream), "set_clock sync");
+}
+
+int32_t sale_get_layout(sale_ctx* c, int32_t* k0, int32_t* k1)
+{
+    if (!c) return SALE_EINVAL;
+    if (k0) *k0 = c->slabs.front().k0;
+    if (k1) *k1 = c->slabs.back().k1;
+    return SALE_OK;
+}
+
+int64_t sale_kernel_launches(const sale_ctx* c) { return c ? c->launches : 0; }
+
+const char* sale_last_error(const sale_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void sale_destroy(sale_ctx* c)
+{
+    if (!c) return;
+    DeviceGuard guard(c->prm.device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->hstate) cudaFreeHost(c->hstate);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// sale_internal.h -- structures shared by the libsale host code and kernels.
+// Not part of the ABI (include/sale.h is).
+#pragma once
+#include <cstdint>
+
+namespace sale {
+
+constexpr unsigned long long KEY_NONE = 0xFFFFFFFFFFFFFFFFull;
+
+// Physics and mesh parameters (validated copy of sale_params), by value into kernels.
+struct Phys {
+    double lx, ly, lz;
+    double gamma, c1, c2, cfl, growth, t_end;
+    double rho0, e_bg, e_dep;
+    int nx, ny, nz;           // global cells
+    unsigned reflect;         // bit f: face f of {-x,+x,-y,+y,-z,+z} reflects
+    int rezone;               // 0 Lagrange, 1 Euler
+};
+
+// Device-resident clock and status (one per context; all local slabs share it).
+struct DevState {
+    double t;                 // time of the current state
+    double dt_prev;           // dt of the last committed cycle (< 0: none)
+    double dt;                // dt of the cycle in flight
+    long long cycle;          // committed cycles
+    unsigned long long cand_key;  // min over cells of key(dt_K) for the next cycle
+    unsigned long long err_key;   // min over failing cells of (order << 48 | cell)
+    int status;               // sticky SALE_* code, 0 = OK
+    int active;               // 1 while a cycle is in flight
+    int finished;             // t_end reached
+    int good;                 // committed cycles since the last host read
+    long long err_cycle;      // cycle in which status became non-zero
+    long long err_cell;       // global linear cell index (-1 if none)
+};
+
+// One z-slab of the mesh with its ghost planes, by value into kernels.
+// Global cell planes [k0,k1) are owned; local plane 0 is global plane kb = k0-g.
+struct Slab {
+    int k0, k1, g, kb;
+    int nzc, nzn;             // allocated local cell / node planes
+    long long pn, pc;         // node / cell plane sizes (nx+1)(ny+1), nx*ny
+    double* x[2][3];          // Lagrange node positions (ping-pong); unused in Euler
+    double* u[2][3];          // node velocities (ping-pong)
+    double* m[2];             // cell mass (Euler ping-pong; Lagrange uses m[0])
+    double* e[2];             // specific internal energy (ping-pong)
+    double* sig;              // v0 scratch: sigma per cell
+    double* x1[3];            // Euler scratch: x' (post-Lagrange positions)
+    double* u1[3];            // Euler scratch: u'
+    double* e1;               // Euler scratch: e'
+    double* V1;               // Euler scratch: V'
+    double* dm;               // Euler scratch: Delta m
+    double* dP[3];            // Euler scratch: Delta P
+    double* der;              // derive / staging scratch (node-plane sized)
+    double* Xt;               // target node coordinates X_i, i in [0,nx]
+    double* Yt;               // Y_j, j in [0,ny]
+    double* Zt;               // Z_k for local node planes (index = k - kb)
+    DevState* st;
+};
+
+// status codes mirrored from include/sale.h (kept in sync by a static_assert in host code)
+enum { S_OK = 0, S_EINVAL = 1, S_ENOMEM = 2, S_ECUDA = 3, S_ENCCL = 4, S_ETANGLED = 5,
+       S_EDTCOLLAPSE = 6, S_ENEGMASS = 7, S_EPOISONED = 8, S_EREPLICA = 9 };
+
+// kernel-side error ordering inside a cycle: tangling (Lagrangian phase) first
+constexpr unsigned long long ERR_ORDER_TANGLED = 1, ERR_ORDER_NEGMASS = 2;
+
+// ---- launchers (kernels_*.cu) ----------------------------------------------
+// every launcher returns the number of kernels it launched
+typedef struct CUstream_st* Stream;
+
+int launch_init_tables(const Slab& s, const Phys& p, Stream st);
+int launch_sedov_init(const Slab& s, const Phys& p, Stream st);
+int launch_prep(DevState* d, Stream st);
+int launch_begin(DevState* d, const Phys& p, Stream st);
+int launch_commit(DevState* d, const Phys& p, Stream st);
+int launch_reset_good(DevState* d, Stream st);
+int launch_dt_candidate(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st);
+// one full cycle on one slab, reading buffers [cur], writing [cur^1]
+int launch_cycle_v0(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_cycle_fused(const Slab& s, const Phys& p, int cur, Stream st);
+
+}  // namespace sale

@@ -1,0 +1,80 @@
+// sale_mesh.cuh -- slab indexing and state loaders shared by the kernels.
+#pragma once
+#include "sale_geom.cuh"
+
+namespace sale {
+
+// local linear node / cell index of GLOBAL (i, j, k)
+__device__ __forceinline__ long long nidx(const Slab& s, const Phys& p, int i, int j, int k)
+{
+    return (long long)i + (long long)(p.nx + 1) * ((long long)j + (long long)(p.ny + 1) * (k - s.kb));
+}
+__device__ __forceinline__ long long cidx(const Slab& s, const Phys& p, int i, int j, int k)
+{
+    return (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
+}
+// global linear cell index (for error reports)
+__device__ __forceinline__ long long gcell(const Phys& p, int i, int j, int k)
+{
+    return (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * k);
+}
+__device__ __forceinline__ bool cell_in(const Phys& p, int i, int j, int k)
+{
+    return i >= 0 && i < p.nx && j >= 0 && j < p.ny && k >= 0 && k < p.nz;
+}
+
+// node position at the start of the cycle: Lagrange from x[b], Euler x^T
+template <bool EULER>
+__device__ __forceinline__ D3 pos(const Slab& s, const Phys& p, int b, int i, int j, int k)
+{
+    if (EULER) return D3{s.Xt[i], s.Yt[j], s.Zt[k - s.kb]};
+    long long n = nidx(s, p, i, j, k);
+    return D3{s.x[b][0][n], s.x[b][1][n], s.x[b][2][n]};
+}
+__device__ __forceinline__ D3 tpos(const Slab& s, int i, int j, int k)
+{
+    return D3{s.Xt[i], s.Yt[j], s.Zt[k - s.kb]};
+}
+__device__ __forceinline__ D3 ld3(double* const a[3], long long n)
+{
+    return D3{a[0][n], a[1][n], a[2][n]};
+}
+__device__ __forceinline__ void st3(double* const a[3], long long n, D3 v)
+{
+    a[0][n] = v.x;
+    a[1][n] = v.y;
+    a[2][n] = v.z;
+}
+
+// the 8 nodes of cell (i,j,k) in hex order (c*2+b)*2+a
+template <bool EULER>
+__device__ __forceinline__ void load_hex_pos(const Slab& s, const Phys& p, int b, int i, int j,
+                                             int k, D3 N[8])
+{
+#pragma unroll
+    for (int h = 0; h < 8; ++h) N[h] = pos<EULER>(s, p, b, i + (h & 1), j + ((h >> 1) & 1), k + (h >> 2));
+}
+__device__ __forceinline__ void load_hex3(const Slab& s, const Phys& p, double* const a[3], int i,
+                                          int j, int k, D3 N[8])
+{
+#pragma unroll
+    for (int h = 0; h < 8; ++h)
+        N[h] = ld3(a, nidx(s, p, i + (h & 1), j + ((h >> 1) & 1), k + (h >> 2)));
+}
+
+// reflecting boundary: zero the normal component on reflecting planes (c.3 step 6)
+__device__ __forceinline__ D3 reflect(const Phys& p, int i, int j, int k, D3 v)
+{
+    unsigned r = p.reflect;
+    if (((r & 1u) && i == 0) || ((r & 2u) && i == p.nx)) v.x = 0.0;
+    if (((r & 4u) && j == 0) || ((r & 8u) && j == p.ny)) v.y = 0.0;
+    if (((r & 16u) && k == 0) || ((r & 32u) && k == p.nz)) v.z = 0.0;
+    return v;
+}
+
+__device__ __forceinline__ double* mass_cur(const Slab& s, const Phys& p, int cur)
+{
+    return p.rezone ? s.m[cur] : s.m[0];
+}
+
+}  // namespace sale

@@ -1,0 +1,229 @@
+"""Thin Python binding of libsale (include/sale.h): argument marshalling only.
+
+Every step of the SALE cycle runs in libsale's CUDA kernels; PyTorch supplies
+the device workspace, the stream and (for multi-GPU) the process group that
+broadcasts the NCCL unique id.  There is no CPU fallback: if libsale.so is
+missing or no GPU is present, constructing a context raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsale.so")
+
+OK, EINVAL, ENOMEM, ECUDA, ENCCL, ETANGLED, EDTCOLLAPSE, ENEGMASS, EPOISONED, EREPLICA = range(10)
+CODE_NAMES = ["OK", "EINVAL", "ENOMEM", "ECUDA", "ENCCL", "ETANGLED", "EDTCOLLAPSE", "ENEGMASS",
+              "EPOISONED", "EREPLICA"]
+LAGRANGE, EULER = 0, 1
+IMPL = {"fused": 0, "v0": 1}
+FIELDS = {"X": 0, "Y": 1, "Z": 2, "UX": 3, "UY": 4, "UZ": 5, "NODE_MASS": 6,
+          "MASS": 7, "E": 8, "RHO": 9, "VOL": 10, "P": 11, "Q": 12, "CS": 13}
+NODE_FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "NODE_MASS")
+EXPORTS = ("sale_workspace_bytes", "sale_nccl_unique_id", "sale_create", "sale_step",
+           "sale_step_async", "sale_sync", "sale_get_field", "sale_set_field", "sale_get_clock",
+           "sale_set_clock", "sale_get_layout", "sale_kernel_launches", "sale_last_error",
+           "sale_destroy")
+
+
+class SaleParams(C.Structure):
+    _fields_ = [("abi_version", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32),
+                ("nz", C.c_int32), ("lx", C.c_double), ("ly", C.c_double), ("lz", C.c_double),
+                ("gamma", C.c_double), ("q_lin", C.c_double), ("q_quad", C.c_double),
+                ("cfl", C.c_double), ("dt_growth", C.c_double), ("t_end", C.c_double),
+                ("rezone", C.c_int32), ("reflect_mask", C.c_uint32), ("rho0", C.c_double),
+                ("e_background", C.c_double), ("e_deposit", C.c_double), ("rank", C.c_int32),
+                ("nranks", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
+                ("device", C.c_int32), ("impl", C.c_int32), ("local_slabs", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class SaleError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        self.code = code
+        super().__init__(f"{what}: {CODE_NAMES[code] if 0 <= code < len(CODE_NAMES) else code}")
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libsale.so (build it with paper_2209_01983_b200.build.build())."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"libsale.so not built ({LIB_PATH}); run __graft_entry__.build()")
+            L = C.CDLL(LIB_PATH)
+            P, vp = C.POINTER, C.c_void_p
+            d, i32, i64, u64 = C.c_double, C.c_int32, C.c_int64, C.c_uint64
+            L.sale_workspace_bytes.argtypes = [P(SaleParams)]
+            L.sale_workspace_bytes.restype = u64
+            L.sale_nccl_unique_id.argtypes = [vp]
+            L.sale_nccl_unique_id.restype = i32
+            L.sale_create.argtypes = [P(SaleParams), P(vp)]
+            L.sale_create.restype = i32
+            L.sale_step.argtypes = [vp, i32, P(i32)]
+            L.sale_step.restype = i32
+            L.sale_step_async.argtypes = [vp, i32]
+            L.sale_step_async.restype = i32
+            L.sale_sync.argtypes = [vp, P(i32)]
+            L.sale_sync.restype = i32
+            L.sale_get_field.argtypes = [vp, i32, vp, u64, i32]
+            L.sale_get_field.restype = i32
+            L.sale_set_field.argtypes = [vp, i32, vp, u64, i32]
+            L.sale_set_field.restype = i32
+            L.sale_get_clock.argtypes = [vp, P(d), P(d), P(i64), P(i32)]
+            L.sale_get_clock.restype = i32
+            L.sale_set_clock.argtypes = [vp, d, d, i64]
+            L.sale_set_clock.restype = i32
+            L.sale_get_layout.argtypes = [vp, P(i32), P(i32)]
+            L.sale_get_layout.restype = i32
+            L.sale_kernel_launches.argtypes = [vp]
+            L.sale_kernel_launches.restype = i64
+            L.sale_last_error.argtypes = [vp]
+            L.sale_last_error.restype = C.c_char_p
+            L.sale_destroy.argtypes = [vp]
+            L.sale_destroy.restype = None
+            _lib = L
+    return _lib
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    rc = lib().sale_nccl_unique_id(buf)
+    if rc:
+        raise SaleError(rc, "sale_nccl_unique_id")
+    return buf.raw
+
+
+def make_params(cfg: dict, *, rank=0, nranks=1, device=0, impl="v0", local_slabs=1) -> SaleParams:
+    p = SaleParams()
+    p.abi_version = 1
+    for k in ("nx", "ny", "nz", "lx", "ly", "lz", "gamma", "q_lin", "q_quad", "cfl", "dt_growth",
+              "t_end", "rezone", "reflect_mask", "rho0", "e_background", "e_deposit"):
+        setattr(p, k, cfg[k])
+    p.rank, p.nranks, p.device = rank, nranks, device
+    p.impl = IMPL[impl] if isinstance(impl, str) else int(impl)
+    p.local_slabs = local_slabs
+    return p
+
+
+def workspace_bytes(cfg: dict, **kw) -> int:
+    return int(lib().sale_workspace_bytes(C.byref(make_params(cfg, **kw))))
+
+
+class Sale:
+    """One libsale context on one GPU (one z-slab of the mesh per rank)."""
+
+    def __init__(self, cfg: dict, *, device: int = 0, stream=None, rank: int = 0, nranks: int = 1,
+                 nccl_id: bytes | None = None, impl: str = "v0", local_slabs: int = 1):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libsale needs a CUDA device (no CPU fallback)")
+        L = lib()
+        self.cfg = dict(cfg)
+        self._L = L
+        p = make_params(cfg, rank=rank, nranks=nranks, device=device, impl=impl,
+                        local_slabs=local_slabs)
+        nbytes = L.sale_workspace_bytes(C.byref(p))
+        if nbytes == 0:
+            raise SaleError(EINVAL, "sale_workspace_bytes")
+        self.torch_device = torch.device("cuda", device)
+        self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=self.torch_device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.torch_device)
+        p.workspace = self.workspace.data_ptr()
+        p.workspace_bytes = nbytes
+        p.stream = self.stream.cuda_stream
+        self._id = None
+        if nranks > 1:
+            self._id = C.create_string_buffer(nccl_id, 128)
+            p.nccl_unique_id = C.cast(self._id, C.c_void_p)
+        self._p = p
+        h = C.c_void_p()
+        rc = L.sale_create(C.byref(p), C.byref(h))
+        if rc:
+            raise SaleError(rc, "sale_create")
+        self._h = h
+        k0, k1 = C.c_int32(), C.c_int32()
+        L.sale_get_layout(h, C.byref(k0), C.byref(k1))
+        self.k0, self.k1 = k0.value, k1.value
+        nx, ny = cfg["nx"], cfg["ny"]
+        self.node_shape = (self.k1 - self.k0 + 1, ny + 1, nx + 1)
+        self.cell_shape = (self.k1 - self.k0, ny, nx)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.sale_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- stepping ---------------------------------------------------------
+    def step(self, n: int):
+        """Run n cycles (synchronous).  Returns (status code, cycles done)."""
+        done = C.c_int32(0)
+        rc = self._L.sale_step(self._h, int(n), C.byref(done))
+        return rc, done.value
+
+    def step_async(self, n: int) -> None:
+        rc = self._L.sale_step_async(self._h, int(n))
+        if rc:
+            raise SaleError(rc, "sale_step_async: " + self.last_error())
+
+    def sync(self):
+        done = C.c_int32(0)
+        rc = self._L.sale_sync(self._h, C.byref(done))
+        return rc, done.value
+
+    # ---- fields -----------------------------------------------------------
+    def get(self, field: str, out=None):
+        """Owned slab of a field: numpy (host) by default, or into `out` (a
+        contiguous float64 torch tensor on this device)."""
+        shape = self.node_shape if field in NODE_FIELDS else self.cell_shape
+        if out is None:
+            arr = np.empty(shape, dtype=np.float64)
+            rc = self._L.sale_get_field(self._h, FIELDS[field], arr.ctypes.data, arr.size, 0)
+        else:
+            arr = out
+            rc = self._L.sale_get_field(self._h, FIELDS[field], out.data_ptr(), out.numel(), 1)
+        if rc:
+            raise SaleError(rc, f"sale_get_field({field}): " + self.last_error())
+        return arr
+
+    def set(self, field: str, arr) -> None:
+        if hasattr(arr, "data_ptr"):
+            rc = self._L.sale_set_field(self._h, FIELDS[field], arr.data_ptr(), arr.numel(), 1)
+        else:
+            a = np.ascontiguousarray(arr, dtype=np.float64)
+            rc = self._L.sale_set_field(self._h, FIELDS[field], a.ctypes.data, a.size, 0)
+        if rc:
+            raise SaleError(rc, f"sale_set_field({field}): " + self.last_error())
+
+    def clock(self) -> dict:
+        t, dt, cyc, fin = C.c_double(), C.c_double(), C.c_int64(), C.c_int32()
+        rc = self._L.sale_get_clock(self._h, C.byref(t), C.byref(dt), C.byref(cyc), C.byref(fin))
+        if rc:
+            raise SaleError(rc, "sale_get_clock")
+        return {"t": t.value, "dt_last": dt.value, "cycle": cyc.value, "finished": fin.value}
+
+    def set_clock(self, t: float, dt_last: float, cycle: int) -> None:
+        rc = self._L.sale_set_clock(self._h, t, dt_last, cycle)
+        if rc:
+            raise SaleError(rc, "sale_set_clock")
+
+    def launches(self) -> int:
+        return int(self._L.sale_kernel_launches(self._h))
+
+    def last_error(self) -> str:
+        return self._L.sale_last_error(self._h).decode()
