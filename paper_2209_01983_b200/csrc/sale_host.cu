@@ -28,6 +28,9 @@ static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
 static_assert(offsetof(sale::DevState, err_key) == offsetof(sale::DevState, cand_key) + 8,
               "cand_key / err_key must be adjacent for the 2-element allreduce");
 
+namespace sale {
+bool fused_available();
+}
 using sale::DevState;
 using sale::Phys;
 using sale::Slab;
@@ -96,6 +99,7 @@ bool params_ok(const sale_params* p)
     if ((p->nranks == 1) != (p->nccl_unique_id == nullptr)) return false;
     if (p->local_slabs < 1 || (p->nranks > 1 && p->local_slabs != 1)) return false;
     if (p->impl != SALE_IMPL_V0 && p->impl != SALE_IMPL_FUSED) return false;
+    if (p->impl == SALE_IMPL_FUSED && !sale::fused_available()) return false;
     int T = p->nranks * p->local_slabs;
     if (p->nz < T) return false;
     if (T > 1 && p->nz / T < ghost_depth(p)) return false;  // every slab owns >= g planes
@@ -204,11 +208,6 @@ int launch_check(sale_ctx* c)
 {
     return cuda_check(c, cudaGetLastError(), "kernel launch");
 }
-
-// which arrays travel in a halo exchange
-struct FieldSet {
-    std::vector<double*> node_lo, node_hi;  // filled per slab pair
-};
 
 void state_arrays(const sale_ctx* c, const Slab& s, int b, bool include_mass,
                   std::vector<double*>& nodes, std::vector<double*>& cells)
