@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""bench.py -- zone-cycles/s of the fp64 SALE cycle (arXiv 2209.01983) on B200.
+
+A "step" is one SALE cycle (every §8(a) row: Lagrangian phase S1-S7, Eulerian
+remap R1-R5 in EULER mode, halo exchange X1, dt min-reduction X2) over the
+whole mesh.  Default workload: BASELINE.json config 4 ("C4": Sedov-Taylor 3D,
+256^3 cells per GPU, Eulerian rezoning, fp64, z-slabs over the GPUs -> weak
+scaling); --config C3 selects the strong-scaling Lagrangian 320^3 mesh.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4|C3] [--impl fused|v0]
+    python bench.py --impl reference ...   # the CPU oracle arm (rank 0 only)
+
+One JSON line on rank 0.  Timing: W untimed cycles, then K cycles bracketed by
+barrier + cuda.synchronize on both sides, CUDA events on the launching stream,
+max over ranks.  Inputs (the mesh state, >= 1.1 GB per GPU) are larger than L2.
+"""
+from __future__ import annotations
+
+import argparse
+import csv
+import io
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2209_01983_b200 import configs  # noqa: E402
+
+METRIC = "zone-cycles/s (fp64 SALE cycle)"
+UNIT = "zone-cycles/s"
+# algorithmic bytes per zone-cycle (state read + written once, fp64)
+ALGO_BYTES = {configs.LAGRANGE: 120.0, configs.EULER: 80.0}
+REASON_BITS = {"hw_slowdown": "hw_slowdown", "hw_thermal_slowdown": "hw_thermal_slowdown",
+               "sw_thermal_slowdown": "sw_thermal_slowdown", "sw_power_cap": "sw_power_cap"}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for r in csv.reader(f):
+                if len(r) >= 9:
+                    rows.append([x.strip() for x in r])
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        for r in rows:
+            for name, col in (("hw_slowdown", 5), ("hw_thermal_slowdown", 6),
+                              ("sw_thermal_slowdown", 7), ("sw_power_cap", 8)):
+                if r[col].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def oracle_rate(cfg_sample: dict, seconds: float, min_cycles: int = 3, warm: int = 1):
+    """Time the CPU oracle (as it stands, single thread) on a bounded sample."""
+    import oracle as O
+    o = O.Oracle(cfg_sample)
+    if warm:
+        o.step(warm)
+    cells = cfg_sample["nx"] * cfg_sample["ny"] * cfg_sample["nz"]
+    n, t0 = 0, time.perf_counter()
+    while n < min_cycles or time.perf_counter() - t0 < seconds:
+        rc, d = o.step(1)
+        if rc:
+            raise RuntimeError(f"oracle rc={rc}")
+        n += 1
+    dt = time.perf_counter() - t0
+    return cells * n / dt, n, dt
+
+
+def sample_cfg(name: str):
+    """A bounded slab of the workload with the same cell size and physics."""
+    cfg, _ = configs.config(name, 1)
+    nzs = 4
+    s = dict(cfg, nz=nzs, lz=cfg["lz"] * nzs / cfg["nz"])
+    return s, f"{s['nx']}x{s['ny']}x{nzs} cells of {name} (same h, physics, mode), Sedov initial state"
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    s, desc = sample_cfg(args.config)
+    import oracle as O
+    O.build()
+    o = O.Oracle(s)
+    o.step(args.warmup)
+    cells = s["nx"] * s["ny"] * s["nz"]
+    t0 = time.perf_counter()
+    rc, done = o.step(args.steps)
+    dt = time.perf_counter() - t0
+    if rc or done != args.steps:
+        raise RuntimeError(f"oracle rc={rc} done={done}")
+    v = cells * args.steps / dt
+    cfg, _ = configs.config(args.config, world)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak" if args.config == "C4" else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.config), "sample": desc},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def workload_name(name):
+    return {"C3": "C3: Sedov-Taylor 3D 320^3 cells, Lagrangian, fp64, strong scaling",
+            "C4": "C4: Sedov-Taylor 3D 256^3 cells per GPU, Eulerian rezoning, fp64, weak scaling",
+            }.get(name, name)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4", choices=["C3", "C4"])
+    ap.add_argument("--impl", default="auto", choices=["auto", "fused", "v0", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2209_01983_b200 import build as _build
+    from paper_2209_01983_b200 import sale as S
+
+    _build.build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")  # plumbing only: id broadcast, barrier, max
+    impl = args.impl
+    if impl == "auto":
+        impl = "fused" if S.workspace_bytes(configs.config("C0")[0], impl="fused") else "v0"
+    cfg, _ = configs.config(args.config, world)
+    nid = None
+    if world > 1:
+        obj = [S.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    ctx = S.Sale(cfg, device=local, rank=rank, nranks=world, nccl_id=nid, impl=impl)
+    stream = ctx.stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    rc, done = ctx.step(args.warmup)
+    if rc or done != args.warmup:
+        raise RuntimeError(f"warmup failed rc={rc} done={done}: {ctx.last_error()}")
+
+    # ---- timed region ------------------------------------------------------
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.2)
+    launches0 = ctx.launches()
+    ctx.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.step_async(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    rc, done = ctx.sync()
+    barrier()
+    clocks = sampler.stop()
+    if rc or done != args.steps:
+        raise RuntimeError(f"timed run failed rc={rc} done={done}: {ctx.last_error()}")
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = ctx.launches() - launches0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    gcells = cfg["nx"] * cfg["ny"] * cfg["nz"]
+    value = gcells * args.steps / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel class -------------------------------
+    peak, peak_src = peaks()
+    local_cells = cfg["nx"] * cfg["ny"] * (ctx.k1 - ctx.k0)
+    dom = max(("lagrange", "remap"), key=lambda k: prof[k][0])
+    dom_ms, dom_n = prof[dom]
+    per_launch_ms = dom_ms / max(dom_n, 1)
+    mode = cfg["rezone"]
+    # algorithmic bytes of one cycle of this rank's slab ...
+    cyc_bytes = ALGO_BYTES[mode] * local_cells
+    # ... achieved by the dominant kernel class alone and by the whole cycle
+    achieved = cyc_bytes / (per_launch_ms * 1e-3) / 1e9
+    cycle_gbs = cyc_bytes / (ms / args.steps * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "kernel": dom,
+                "kernel_ms": per_launch_ms, "kernel_share_of_step": dom_ms / ms,
+                "algo_bytes_per_zone_cycle": ALGO_BYTES[mode],
+                "whole_cycle_gbs": cycle_gbs, "whole_cycle_frac": cycle_gbs / peak,
+                "peak_source": peak_src}
+
+    # ---- end to end through the public API with host buffers ------------------
+    e2e = None
+    if args.e2e_steps > 0:
+        fields = ["UX", "UY", "UZ", "MASS", "E"] + (["X", "Y", "Z"] if mode == configs.LAGRANGE else [])
+        host = {}
+        for f in fields:
+            shape = ctx.node_shape if f in S.NODE_FIELDS else ctx.cell_shape
+            host[f] = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+            ctx.get(f, out=host[f])
+        nbytes = sum(t.numel() * 8 for t in host.values())
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for f in fields:
+                ctx.set(f, host[f])          # H2D: this step's inputs, pinned host
+            rc, done = ctx.step(1)
+            if rc:
+                raise RuntimeError(f"e2e step rc={rc}")
+            for f in fields:
+                ctx.get(f, out=host[f])      # D2H: this step's result (the new state)
+        torch.cuda.synchronize()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": gcells * args.e2e_steps / wall, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
+               "what": "per step: set_field of the full state from pinned host, sale_step(1), "
+                       "get_field of the full state to pinned host"}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only) -------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s, desc = sample_cfg(args.config)
+        import oracle as O
+        O.build()
+        v, n, dt = oracle_rate(s, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{desc}; {n} cycles in {dt:.1f} s, single thread, gcc -O2 -ffp-contract=off"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.config == "C4" else "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config), "global_cells": gcells,
+                       "cells_per_gpu": local_cells, "mesh": [cfg["nx"], cfg["ny"], cfg["nz"]],
+                       "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                       "impl": impl, "step": "one SALE cycle",
+                       "l2": "inputs larger than L2 (state >= 1.1 GB per GPU), no flush"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks,
+            "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -167,6 +167,20 @@ int32_t sale_get_layout(sale_ctx* c, int32_t* k0, int32_t* k1);
 /* kernels launched so far by this context (all of them are libsale's own) */
 int64_t sale_kernel_launches(const sale_ctx* c);
 
+/* Kernel-class timing: while enabled, every launch group of a class is
+ * bracketed by cudaEventRecord on the context's stream; the elapsed times are
+ * accumulated at the next synchronisation (sale_step / sale_sync).  Enabling
+ * resets the accumulators.  Classes: */
+#define SALE_K_BEGIN 0     /* dt finalisation + clock commit (one thread)          */
+#define SALE_K_PROLOGUE 1  /* per-call halo exchange + dt-candidate pass           */
+#define SALE_K_LAGRANGE 2  /* Lagrangian phase S1-S7 (+ next dt candidate, Lagrange) */
+#define SALE_K_REMAP 3     /* Eulerian remap R1-R5 + next dt candidate             */
+#define SALE_K_HALO 4      /* per-cycle halo exchange + dt/error allreduce         */
+#define SALE_K_NCLASS 5
+int32_t sale_profile_enable(sale_ctx* c, int32_t on);
+/* total device milliseconds and number of timed launch groups of a class */
+int32_t sale_profile_read(sale_ctx* c, int32_t kclass, double* total_ms, int64_t* count);
+
 /* human-readable detail of the last error: code, cycle, cell, CUDA/NCCL text */
 const char* sale_last_error(const sale_ctx* c);
 

@@ -7,6 +7,7 @@ namespace sale {
 
 bool fused_available() { return false; }
 
-int launch_cycle_fused(const Slab&, const Phys&, int, Stream) { return 0; }
+int launch_lagrange_fused(const Slab&, const Phys&, int, Stream) { return 0; }
+int launch_remap_fused(const Slab&, const Phys&, int, Stream) { return 0; }
 
 }  // namespace sale

@@ -275,11 +275,10 @@ __global__ void k0_remap_nodes(Slab s, Phys p, int cur)
 
 int launch_dt_candidate_gated(const Slab& s, const Phys& p, int cur, Stream st);
 
-int launch_cycle_v0(const Slab& s, const Phys& p, int cur, Stream st)
+int launch_lagrange_v0(const Slab& s, const Phys& p, int cur, Stream st)
 {
     cudaStream_t cs = (cudaStream_t)st;
     const int bs = 128;
-    int n = 0;
     if (!p.rezone) {
         int ka0 = s.k0 > 0 ? s.k0 - 1 : 0, ka1 = s.k1 < p.nz ? s.k1 + 1 : p.nz;
         k0_sigma<false><<<grid_for(s.pc * (ka1 - ka0), bs), bs, 0, cs>>>(s, p, cur, ka0, ka1);
@@ -287,18 +286,23 @@ int launch_cycle_v0(const Slab& s, const Phys& p, int cur, Stream st)
         k0_energy<false><<<grid_for(s.pc * (s.k1 - s.k0), bs), bs, 0, cs>>>(s, p, cur, s.k0, s.k1);
         return 3;
     }
+    // Euler: the Lagrangian phase also runs on the ghost region the remap needs
     int ka0 = s.k0 - 3 > 0 ? s.k0 - 3 : 0, ka1 = s.k1 + 3 < p.nz ? s.k1 + 3 : p.nz;
     int kb0 = s.k0 - 2 > 0 ? s.k0 - 2 : 0, kb1 = s.k1 + 2 < p.nz ? s.k1 + 2 : p.nz;
-    int kc0 = kb0, kc1 = kb1;
-    int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     k0_sigma<true><<<grid_for(s.pc * (ka1 - ka0), bs), bs, 0, cs>>>(s, p, cur, ka0, ka1);
     k0_nodes<true><<<grid_for(s.pn * (kb1 - kb0 + 1), bs), bs, 0, cs>>>(s, p, cur, kb0, kb1);
-    k0_energy<true><<<grid_for(s.pc * (kc1 - kc0), bs), bs, 0, cs>>>(s, p, cur, kc0, kc1);
+    k0_energy<true><<<grid_for(s.pc * (kb1 - kb0), bs), bs, 0, cs>>>(s, p, cur, kb0, kb1);
+    return 3;
+}
+
+int launch_remap_v0(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    cudaStream_t cs = (cudaStream_t)st;
+    const int bs = 128;
+    int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     k0_remap_cells<<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);
     k0_remap_nodes<<<grid_for(s.pn * (s.k1 - s.k0 + 1), bs), bs, 0, cs>>>(s, p, cur);
-    n = 5;
-    n += launch_dt_candidate_gated(s, p, cur ^ 1, st);
-    return n;
+    return 2 + launch_dt_candidate_gated(s, p, cur ^ 1, st);
 }
 
 }  // namespace sale

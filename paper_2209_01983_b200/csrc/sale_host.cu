@@ -49,6 +49,16 @@ struct sale_ctx {
     bool poisoned = false;
     long long launches = 0;
     std::string err = "OK";
+    // kernel-class timing (sale_profile_enable)
+    struct Pending {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    bool prof_on = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<Pending> pending;
+    double prof_ms[SALE_K_NCLASS] = {0};
+    long long prof_cnt[SALE_K_NCLASS] = {0};
 };
 
 namespace {
@@ -209,6 +219,46 @@ int launch_check(sale_ctx* c)
     return cuda_check(c, cudaGetLastError(), "kernel launch");
 }
 
+cudaEvent_t take_event(sale_ctx* c)
+{
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// bracket a launch group of class cls with events (no-op unless profiling)
+int prof_open(sale_ctx* c, int cls)
+{
+    if (!c->prof_on) return -1;
+    sale_ctx::Pending p{cls, take_event(c), take_event(c)};
+    cudaEventRecord(p.a, c->stream);
+    c->pending.push_back(p);
+    return (int)c->pending.size() - 1;
+}
+void prof_close(sale_ctx* c, int idx)
+{
+    if (idx >= 0) cudaEventRecord(c->pending[idx].b, c->stream);
+}
+// after a stream sync: accumulate and recycle
+void prof_collect(sale_ctx* c)
+{
+    for (auto& p : c->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            c->prof_ms[p.cls] += ms;
+            c->prof_cnt[p.cls] += 1;
+        }
+        c->ev_pool.push_back(p.a);
+        c->ev_pool.push_back(p.b);
+    }
+    c->pending.clear();
+}
+
 void state_arrays(const sale_ctx* c, const Slab& s, int b, bool include_mass,
                   std::vector<double*>& nodes, std::vector<double*>& cells)
 {
@@ -302,21 +352,35 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
 {
     int rc;
     int b = c->cur_enq;
-    c->launches += sale::launch_prep(c->dstate, (sale::Stream)c->stream);
+    sale::Stream st = (sale::Stream)c->stream;
+    bool v0 = c->prm.impl == SALE_IMPL_V0, euler = c->prm.rezone == SALE_EULER;
+    int pr = prof_open(c, SALE_K_PROLOGUE);
+    c->launches += sale::launch_prep(c->dstate, st);
     if ((rc = exchange(c, b, true))) return rc;
-    for (auto& s : c->slabs) c->launches += sale::launch_dt_candidate(s, c->phys, b, (sale::Stream)c->stream);
+    for (auto& s : c->slabs) c->launches += sale::launch_dt_candidate(s, c->phys, b, st);
     if ((rc = reduce_keys(c))) return rc;
+    prof_close(c, pr);
     for (int n = 0; n < ncycles; ++n) {
-        c->launches += sale::launch_begin(c->dstate, c->phys, (sale::Stream)c->stream);
+        pr = prof_open(c, SALE_K_BEGIN);
+        c->launches += sale::launch_begin(c->dstate, c->phys, st);
+        prof_close(c, pr);
         for (auto& s : c->slabs) {
-            if (c->prm.impl == SALE_IMPL_V0)
-                c->launches += sale::launch_cycle_v0(s, c->phys, b, (sale::Stream)c->stream);
-            else
-                c->launches += sale::launch_cycle_fused(s, c->phys, b, (sale::Stream)c->stream);
+            pr = prof_open(c, SALE_K_LAGRANGE);
+            c->launches += v0 ? sale::launch_lagrange_v0(s, c->phys, b, st)
+                              : sale::launch_lagrange_fused(s, c->phys, b, st);
+            prof_close(c, pr);
+            if (euler) {
+                pr = prof_open(c, SALE_K_REMAP);
+                c->launches += v0 ? sale::launch_remap_v0(s, c->phys, b, st)
+                                  : sale::launch_remap_fused(s, c->phys, b, st);
+                prof_close(c, pr);
+            }
         }
         if ((rc = launch_check(c))) return rc;
+        pr = prof_open(c, SALE_K_HALO);
         if ((rc = exchange(c, b ^ 1, false))) return rc;
         if ((rc = reduce_keys(c))) return rc;
+        prof_close(c, pr);
         b ^= 1;
     }
     c->launches += sale::launch_commit(c->dstate, c->phys, (sale::Stream)c->stream);
@@ -332,6 +396,7 @@ int sync_state(sale_ctx* c, int* good_out)
                         "state read");
     if (rc) return rc;
     if ((rc = cuda_check(c, cudaStreamSynchronize(c->stream), "stream sync"))) return rc;
+    prof_collect(c);
     if (c->prm.nranks > 1) {
         ncclResult_t ar;
         if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess)
@@ -633,6 +698,26 @@ int32_t sale_get_layout(sale_ctx* c, int32_t* k0, int32_t* k1)
 
 int64_t sale_kernel_launches(const sale_ctx* c) { return c ? c->launches : 0; }
 
+int32_t sale_profile_enable(sale_ctx* c, int32_t on)
+{
+    if (!c) return SALE_EINVAL;
+    c->prof_on = on != 0;
+    if (c->prof_on)
+        for (int k = 0; k < SALE_K_NCLASS; ++k) {
+            c->prof_ms[k] = 0.0;
+            c->prof_cnt[k] = 0;
+        }
+    return SALE_OK;
+}
+
+int32_t sale_profile_read(sale_ctx* c, int32_t kclass, double* total_ms, int64_t* count)
+{
+    if (!c || kclass < 0 || kclass >= SALE_K_NCLASS) return SALE_EINVAL;
+    if (total_ms) *total_ms = c->prof_ms[kclass];
+    if (count) *count = c->prof_cnt[kclass];
+    return SALE_OK;
+}
+
 const char* sale_last_error(const sale_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 void sale_destroy(sale_ctx* c)
@@ -642,6 +727,11 @@ void sale_destroy(sale_ctx* c)
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->hstate) cudaFreeHost(c->hstate);
+    for (auto& p : c->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
     delete c;
 }
 

@@ -76,8 +76,13 @@ int launch_commit(DevState* d, const Phys& p, Stream st);
 int launch_reset_good(DevState* d, Stream st);
 int launch_dt_candidate(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st);
-// one full cycle on one slab, reading buffers [cur], writing [cur^1]
-int launch_cycle_v0(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_cycle_fused(const Slab& s, const Phys& p, int cur, Stream st);
+// one cycle on one slab, reading buffers [cur], writing [cur^1]:
+// the Lagrangian phase (S1-S7; Lagrange mode also the next dt candidate), then
+// in Euler mode the remap (R1-R5 + next dt candidate)
+int launch_lagrange_v0(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_remap_v0(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st);
+bool fused_available();
 
 }  // namespace sale

@@ -26,8 +26,9 @@ FIELDS = {"X": 0, "Y": 1, "Z": 2, "UX": 3, "UY": 4, "UZ": 5, "NODE_MASS": 6,
 NODE_FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "NODE_MASS")
 EXPORTS = ("sale_workspace_bytes", "sale_nccl_unique_id", "sale_create", "sale_step",
            "sale_step_async", "sale_sync", "sale_get_field", "sale_set_field", "sale_get_clock",
-           "sale_set_clock", "sale_get_layout", "sale_kernel_launches", "sale_last_error",
-           "sale_destroy")
+           "sale_set_clock", "sale_get_layout", "sale_kernel_launches", "sale_profile_enable",
+           "sale_profile_read", "sale_last_error", "sale_destroy")
+K_CLASSES = ("begin", "prologue", "lagrange", "remap", "halo")
 
 
 class SaleParams(C.Structure):
@@ -87,6 +88,10 @@ def lib() -> C.CDLL:
             L.sale_get_layout.restype = i32
             L.sale_kernel_launches.argtypes = [vp]
             L.sale_kernel_launches.restype = i64
+            L.sale_profile_enable.argtypes = [vp, i32]
+            L.sale_profile_enable.restype = i32
+            L.sale_profile_read.argtypes = [vp, i32, P(d), P(i64)]
+            L.sale_profile_read.restype = i32
             L.sale_last_error.argtypes = [vp]
             L.sale_last_error.restype = C.c_char_p
             L.sale_destroy.argtypes = [vp]
@@ -196,14 +201,16 @@ class Sale:
             rc = self._L.sale_get_field(self._h, FIELDS[field], arr.ctypes.data, arr.size, 0)
         else:
             arr = out
-            rc = self._L.sale_get_field(self._h, FIELDS[field], out.data_ptr(), out.numel(), 1)
+            rc = self._L.sale_get_field(self._h, FIELDS[field], out.data_ptr(), out.numel(),
+                                        1 if out.is_cuda else 0)
         if rc:
             raise SaleError(rc, f"sale_get_field({field}): " + self.last_error())
         return arr
 
     def set(self, field: str, arr) -> None:
-        if hasattr(arr, "data_ptr"):
-            rc = self._L.sale_set_field(self._h, FIELDS[field], arr.data_ptr(), arr.numel(), 1)
+        if hasattr(arr, "data_ptr"):  # torch tensor: device, or (pinned) host memory
+            rc = self._L.sale_set_field(self._h, FIELDS[field], arr.data_ptr(), arr.numel(),
+                                        1 if arr.is_cuda else 0)
         else:
             a = np.ascontiguousarray(arr, dtype=np.float64)
             rc = self._L.sale_set_field(self._h, FIELDS[field], a.ctypes.data, a.size, 0)
@@ -224,6 +231,19 @@ class Sale:
 
     def launches(self) -> int:
         return int(self._L.sale_kernel_launches(self._h))
+
+    def profile(self, on: bool) -> None:
+        """Enable (and reset) / disable per-kernel-class CUDA-event timing."""
+        self._L.sale_profile_enable(self._h, 1 if on else 0)
+
+    def profile_read(self) -> dict:
+        """{class: (total device ms, timed launch groups)} since profile(True)."""
+        out = {}
+        for k, name in enumerate(K_CLASSES):
+            ms, n = C.c_double(), C.c_int64()
+            self._L.sale_profile_read(self._h, k, C.byref(ms), C.byref(n))
+            out[name] = (ms.value, n.value)
+        return out
 
     def last_error(self) -> str:
         return self._L.sale_last_error(self._h).decode()
