@@ -29,6 +29,7 @@ bool fused_available() { return true; }
 namespace {
 
 constexpr int FW = 32;  // columns per warp row
+constexpr int MINB = 2; // resident CTAs per SM the register budget is sized for
 
 // shared-memory 2D plane helper: [NW][32] doubles
 template <int NW>
@@ -64,7 +65,7 @@ __device__ __forceinline__ FaceQ faceq(D3 P0, D3 P1, D3 P2, D3 P3, D3 U0, D3 U1,
 // kf_force: node planes [kn0, kn1] (global, inclusive), z-chunked by blockIdx.z
 // ============================================================================
 template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, 1)
+__global__ void __launch_bounds__(FW * NW, MINB)
     kf_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
 {
     if (!s.st->active) return;
@@ -241,7 +242,7 @@ __global__ void __launch_bounds__(FW * NW, 1)
 // kf_energy: cell planes [kc0, kc1), z-chunked.  Columns i = i0 + ix (no lower halo).
 // ============================================================================
 template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, 1)
+__global__ void __launch_bounds__(FW * NW, MINB)
     kf_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
     if (!s.st->active) return;
@@ -386,7 +387,8 @@ __global__ void __launch_bounds__(FW * NW, 1)
                     v2 = dmax(v2, P(b1, 9, iy, ix + 1));
                     v2 = dmax(v2, P(b1, 9, iy + 1, ix));
                     v2 = dmax(v2, P(b1, 9, iy + 1, ix + 1));
-                    key = dt_key(dt_cell(p.cfl, l2, v2, cs));
+                    unsigned long long kk = dt_key(dt_cell(p.cfl, l2, v2, cs));
+                    key = kk < key ? kk : key;  // running min over this column's planes
                 }
             }
         }
