@@ -94,20 +94,36 @@ __global__ void __launch_bounds__(FW * NW, MINB)
     auto node_pos = [&](int par, int y, int x) { return D3{NODE(par, 0, y, x), NODE(par, 1, y, x), NODE(par, 2, y, x)}; };
     auto node_vel = [&](int par, int y, int x) { return D3{NODE(par, 3, y, x), NODE(par, 4, y, x), NODE(par, 5, y, x)}; };
 
-    auto load_plane = [&](int k) {
-        int par = k & 1;
-        D3 x = D3{0.0, 0.0, 0.0}, u = D3{0.0, 0.0, 0.0};
+    // Register prefetch, one plane ahead: the global loads for node plane k+1
+    // and cell (i,j,k) are issued at step k-1 and land in shared memory at step
+    // k, so their DRAM latency overlaps a whole step of arithmetic.
+    D3 px = D3{0.0, 0.0, 0.0}, pu = px;
+    double pm = 0.0, pe = 0.0;
+    auto fetch = [&](int k) {  // node plane k, cell plane k-1
+        px = D3{0.0, 0.0, 0.0};
+        pu = px;
         if (col_in && k >= 0 && k <= p.nz) {
             long long n = nidx(s, p, i, j, k);
-            x = pos<EULER>(s, p, cur, i, j, k);
-            u = ld3(s.u[cur], n);
+            px = pos<EULER>(s, p, cur, i, j, k);
+            pu = ld3(s.u[cur], n);
         }
-        NODE(par, 0, iy, ix) = x.x;
-        NODE(par, 1, iy, ix) = x.y;
-        NODE(par, 2, iy, ix) = x.z;
-        NODE(par, 3, iy, ix) = u.x;
-        NODE(par, 4, iy, ix) = u.y;
-        NODE(par, 5, iy, ix) = u.z;
+        pm = 0.0;
+        pe = 0.0;
+        const int kc = k - 1;
+        if (i >= 0 && i < p.nx && j >= 0 && j < p.ny && kc >= 0 && kc < p.nz) {
+            long long c = cidx(s, p, i, j, kc);
+            pm = mass_cur(s, p, cur)[c];
+            pe = s.e[cur][c];
+        }
+    };
+    auto put = [&](int k) {
+        int par = k & 1;
+        NODE(par, 0, iy, ix) = px.x;
+        NODE(par, 1, iy, ix) = px.y;
+        NODE(par, 2, iy, ix) = px.z;
+        NODE(par, 3, iy, ix) = pu.x;
+        NODE(par, 4, iy, ix) = pu.y;
+        NODE(par, 5, iy, ix) = pu.z;
     };
     // z-face at node plane k anchored at this column: nodes (i,j),(i+1,j),(i+1,j+1),(i,j+1)
     auto zface = [&](int k) {
@@ -117,21 +133,19 @@ __global__ void __launch_bounds__(FW * NW, MINB)
     };
 
     // prologue: node plane za-1 and its z-faces (the -z faces of cell plane za-1)
-    load_plane(za - 1);
+    fetch(za - 1);
+    put(za - 1);
+    fetch(za);
     __syncthreads();
     FaceQ zprev = zface(za - 1);
 
     for (int kz = za - 1; kz <= zb; ++kz) {
         const int b0 = kz & 1, b1 = (kz + 1) & 1;
-        // ---- P1: load node plane kz+1 and this column's cell (i,j,kz)
-        load_plane(kz + 1);
+        // ---- P1: node plane kz+1 and cell (i,j,kz) from the prefetch registers; prefetch the next
+        put(kz + 1);
         const bool cell_in = i >= 0 && i < p.nx && j >= 0 && j < p.ny && kz >= 0 && kz < p.nz;
-        double m = 0.0, e = 0.0;
-        if (cell_in) {
-            long long c = cidx(s, p, i, j, kz);
-            m = mass_cur(s, p, cur)[c];
-            e = s.e[cur][c];
-        }
+        const double m = pm, e = pe;
+        if (kz < zb) fetch(kz + 2);
         __syncthreads();
         // ---- P2: faces of cell plane kz anchored at this column
         // x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
@@ -269,28 +283,43 @@ __global__ void __launch_bounds__(FW * NW, MINB)
     auto x1_at = [&](int par, int y, int x) { return D3{P(par, 3, y, x), P(par, 4, y, x), P(par, 5, y, x)}; };
     auto ub_at = [&](int par, int y, int x) { return D3{P(par, 6, y, x), P(par, 7, y, x), P(par, 8, y, x)}; };
 
-    // stage node plane k: x^n, x', ubar = 0.5 (u + u'), |u'|^2
-    auto load_plane = [&](int k) {
-        int par = k & 1;
-        D3 x = D3{0.0, 0.0, 0.0}, x1 = x, ub = x;
-        double v2 = 0.0;
+    // stage node plane k: x^n, x', ubar = 0.5 (u + u'), |u'|^2.  The raw loads
+    // are issued one step ahead into registers (fetch) and staged next step (put).
+    D3 fx = D3{0.0, 0.0, 0.0}, fu = fx, fu1 = fx, fx1 = fx;
+    double fm = 0.0, fe = 0.0, fs = 0.0;
+    auto fetch = [&](int k) {  // node plane k, cell plane k-1
+        fx = D3{0.0, 0.0, 0.0};
+        fu = fx; fu1 = fx; fx1 = fx;
         if (col_in && k >= 0 && k <= p.nz) {
             long long n = nidx(s, p, i, j, k);
-            x = pos<EULER>(s, p, cur, i, j, k);
-            D3 u = ld3(s.u[cur], n);
-            D3 u1 = EULER ? ld3(s.u1, n) : ld3(s.u[cur ^ 1], n);
-            x1 = EULER ? ld3(s.x1, n) : ld3(s.x[cur ^ 1], n);
-            ub = scl(0.5, add(u, u1));
-            v2 = speed2(u1);
+            fx = pos<EULER>(s, p, cur, i, j, k);
+            fu = ld3(s.u[cur], n);
+            fu1 = EULER ? ld3(s.u1, n) : ld3(s.u[cur ^ 1], n);
+            fx1 = EULER ? ld3(s.x1, n) : ld3(s.x[cur ^ 1], n);
         }
-        P(par, 0, iy, ix) = x.x; P(par, 1, iy, ix) = x.y; P(par, 2, iy, ix) = x.z;
-        P(par, 3, iy, ix) = x1.x; P(par, 4, iy, ix) = x1.y; P(par, 5, iy, ix) = x1.z;
+        fm = 0.0; fe = 0.0; fs = 0.0;
+        const int kc = k - 1;
+        if (i < p.nx && j < p.ny && kc >= 0 && kc < p.nz && ix < TX && iy < TY) {
+            long long c = cidx(s, p, i, j, kc);
+            fm = mass_cur(s, p, cur)[c];
+            fe = s.e[cur][c];
+            fs = s.sig[c];
+        }
+    };
+    auto put = [&](int k) {
+        int par = k & 1;
+        D3 ub = scl(0.5, add(fu, fu1));
+        double v2 = speed2(fu1);
+        P(par, 0, iy, ix) = fx.x; P(par, 1, iy, ix) = fx.y; P(par, 2, iy, ix) = fx.z;
+        P(par, 3, iy, ix) = fx1.x; P(par, 4, iy, ix) = fx1.y; P(par, 5, iy, ix) = fx1.z;
         P(par, 6, iy, ix) = ub.x; P(par, 7, iy, ix) = ub.y; P(par, 8, iy, ix) = ub.z;
         P(par, 9, iy, ix) = v2;
     };
 
     // prologue: node plane za; its z-face (A^n, s') and in-plane edges of x'
-    load_plane(za);
+    fetch(za);
+    put(za);
+    fetch(za + 1);
     __syncthreads();
     D3 zA_prev;
     double zs_prev, ex_prev, ey_prev;
@@ -305,16 +334,11 @@ __global__ void __launch_bounds__(FW * NW, MINB)
 
     for (int kz = za; kz <= zb; ++kz) {
         const int b0 = kz & 1, b1 = (kz + 1) & 1;
-        // ---- P1
-        load_plane(kz + 1);
+        // ---- P1: stage node plane kz+1 / cell kz from the prefetch registers, prefetch the next
+        put(kz + 1);
         const bool cell_in = i < p.nx && j < p.ny && kz < p.nz;
-        double m = 0.0, e = 0.0, sig = 0.0;
-        if (cell_in && ix < TX && iy < TY) {
-            long long c = cidx(s, p, i, j, kz);
-            m = mass_cur(s, p, cur)[c];
-            e = s.e[cur][c];
-            sig = s.sig[c];
-        }
+        const double m = fm, e = fe, sig = fs;
+        if (kz < zb) fetch(kz + 2);
         __syncthreads();
         // ---- P2: faces anchored at this column (A at t^n, s' at t^{n+1}); x' edges
         D3 zA_next;
