@@ -1,23 +1,29 @@
 // kernels_fused.cu -- the fused Lagrangian phase as two z-marching kernels.
 //
 // Each CTA owns an x-y tile of columns and marches along z (2.5D): node planes
-// are loaded once from HBM (coalesced, one warp per x-row of 32 columns),
-// staged in shared memory, and every face quantity is computed ONCE per CTA and
-// shared by the cells / nodes that use it:
+// are loaded once from HBM (coalesced, one warp per x-row of 32 columns; the
+// loads for plane k+1 are issued one step ahead into registers), staged in
+// shared memory, and every face quantity is computed ONCE per CTA and shared
+// by the cells / nodes that use it:
 //
-//   kf_force  : S1 geometry at t^n (faces anchored at each column), S2 EoS,
-//               S3 viscosity, sigma; S5 corner forces gathered in the fixed
-//               order of c.2; S6 kinematics + reflecting BC.  Writes u', x'
-//               (Lagrange) or u' (Euler), and sigma.
+//   kf_force  : S1 geometry at t^n (three faces anchored at each column), S2
+//               EoS, S3 viscosity -> sigma; S5 corner forces gathered in the
+//               fixed order of c.2; S6 kinematics + reflecting BC.  Writes u',
+//               x' (Euler: u', x' to scratch) and sigma.
 //   kf_energy : S7 geometry at t^{n+1} (V', tangle check), compatible pdV
-//               energy, and (Lagrange) the next cycle's dt candidate with a
-//               warp-shuffle + block min and one atomicMin per CTA (S4).
+//               energy, and (Lagrange) the next cycle's dt candidate: running
+//               min per thread, warp-shuffle + block min, one atomicMin per CTA.
 //
-// The arithmetic of every quantity is the expression tree of SURVEY §8(c),
-// evaluated with the same association as the v0 kernels and the oracle, so
-// results are bit-identical; only where operands come from (registers / shared
-// memory instead of recomputation) differs.  Tiles: 32 columns per warp row in
-// x (one halo column each side), NW warp rows in y.
+// The arithmetic of every quantity is the expression tree of SURVEY §8(c)
+// with the association of the oracle and the v0 kernels, so results are
+// bit-identical; only the operand sources (registers / shared memory instead
+// of recomputation) differ.
+//
+// Performance structure: the plane parity is a template parameter of the step
+// function, so every shared-memory access is a per-thread base pointer plus an
+// immediate offset (no integer index arithmetic in the inner loop); the smem
+// window is padded by one row+column on both sides so neighbour reads never
+// need clamping; cell presence in the node gather is a predicate, not a branch.
 #include <cuda_runtime.h>
 
 #include "sale_mesh.cuh"
@@ -28,23 +34,13 @@ bool fused_available() { return true; }
 
 namespace {
 
-constexpr int FW = 32;  // columns per warp row
-constexpr int MINB = 2; // resident CTAs per SM the register budget is sized for
+constexpr int FW = 32;   // columns per warp row
+constexpr int MINB = 2;  // resident CTAs per SM the register budget is sized for
+constexpr int PAD = FW + 1;
 
-// shared-memory 2D plane helper: [NW][32] doubles
-template <int NW>
-struct Plane {
-    double* p;
-    __device__ __forceinline__ double& at(int y, int x) const { return p[y * FW + x]; }
-};
-
-__device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
-__device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 inline int imin_h(int a, int b) { return a < b ? a : b; }
 inline int imax_h(int a, int b) { return a > b ? a : b; }
-__device__ __forceinline__ bool cell_in_dom(const Phys& p, int i, int j, int k) { return cell_in(p, i, j, k); }
 
-// face from 4 points: A, centroid Xb, s, and (optionally) the face-average velocity
 struct FaceQ {
     D3 A, Xb, Ub;
     double s;
@@ -59,188 +55,186 @@ __device__ __forceinline__ FaceQ faceq(D3 P0, D3 P1, D3 P2, D3 P3, D3 U0, D3 U1,
     return f;
 }
 
+__device__ __forceinline__ D3 ld3s(const double* b, int o0, int stride) { return D3{b[o0], b[o0 + stride], b[o0 + 2 * stride]}; }
+__device__ __forceinline__ void st3s(double* b, int o0, int stride, D3 v)
+{
+    b[o0] = v.x;
+    b[o0 + stride] = v.y;
+    b[o0 + 2 * stride] = v.z;
+}
+
 }  // namespace
 
 // ============================================================================
-// kf_force: node planes [kn0, kn1] (global, inclusive), z-chunked by blockIdx.z
+// kf_force
 // ============================================================================
 template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, MINB)
-    kf_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
-{
-    if (!s.st->active) return;
-    constexpr int TX = FW - 2, TY = NW - 2;
-    extern __shared__ double smem[];
-    constexpr int PL = NW * FW;  // doubles per plane array
-    // layout
-    double* sN = smem;                  // [2 parity][6][PL]  x,y,z,ux,uy,uz of node planes
-    double* sQ = sN + 2 * 6 * PL;       // [2 x|y][7][PL]     s, Xb(3), Ub(3) of x/y faces of cell plane kz
-    double* sA = sQ + 2 * 7 * PL;       // [2 parity][2 x|y][3][PL]  A of x/y faces per cell plane
-    double* sZ = sA + 2 * 2 * 3 * PL;   // [2 parity][3][PL]  A of z-faces per node plane
-    double* sS = sZ + 2 * 3 * PL;       // [2 parity][2][PL]  sigma, m per cell plane
+struct ForceCTA {
+    static constexpr int PL = NW * FW, TX = FW - 2, TY = NW - 2;
+    // shared-memory words (doubles) relative to the per-thread base pointer
+    __host__ __device__ static constexpr int oN(int par, int c) { return (par * 6 + c) * PL; }          // node x,y,z,ux,uy,uz
+    __host__ __device__ static constexpr int oQ(int xy, int c) { return 12 * PL + (xy * 7 + c) * PL; }  // face s, Xb, Ub
+    __host__ __device__ static constexpr int oA(int par, int xy) { return 26 * PL + (par * 2 + xy) * 3 * PL; }  // x/y face A
+    __host__ __device__ static constexpr int oZ(int par) { return 38 * PL + par * 3 * PL; }            // z-face A
+    __host__ __device__ static constexpr int oS(int par, int c) { return 44 * PL + (par * 2 + c) * PL; }  // sigma, m
+    static constexpr int WORDS = 48 * PL + 2 * PAD;
 
-    const int ix = threadIdx.x, iy = threadIdx.y;
-    const int tid = iy * FW + ix;
-    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
-    const int i = i0 - 1 + ix, j = j0 - 1 + iy;
-    const int za = kn0 + blockIdx.z * zchunk;
-    const int zb = imin(kn1, za + zchunk - 1);
-    const double dt = s.st->dt;
-    const bool col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
-    const int ixp = imin(ix + 1, FW - 1), iyp = imin(iy + 1, NW - 1);
-    const int ixm = imax(ix - 1, 0), iym = imax(iy - 1, 0);
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, za, zb, kn0, kn1;
+    long long nb, cb;  // node / cell index of (i,j) at local plane 0
+    double dt;
+    bool col_in, cellcol_in, node_out, sig_col;
+    bool pxm, pxp, pym, pyp;
+    D3 px, pu;  // prefetch registers
+    double pm, pe;
+    FaceQ zprev;
 
-    auto NODE = [&](int par, int comp, int y, int x) -> double& { return sN[(par * 6 + comp) * PL + y * FW + x]; };
-    auto node_pos = [&](int par, int y, int x) { return D3{NODE(par, 0, y, x), NODE(par, 1, y, x), NODE(par, 2, y, x)}; };
-    auto node_vel = [&](int par, int y, int x) { return D3{NODE(par, 3, y, x), NODE(par, 4, y, x), NODE(par, 5, y, x)}; };
+    __device__ __forceinline__ ForceCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kn0_, int kn1_,
+                                        int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + PAD + iy * FW + ix;
+        i = blockIdx.x * TX - 1 + ix;
+        j = blockIdx.y * TY - 1 + iy;
+        kn0 = kn0_;
+        kn1 = kn1_;
+        za = kn0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kn1 ? za + zchunk - 1 : kn1;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        dt = s.st->dt;
+        col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
+        cellcol_in = i >= 0 && i < p.nx && j >= 0 && j < p.ny;
+        node_out = col_in && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY;
+        sig_col = cellcol_in && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY;
+        pxm = i >= 1 && i <= p.nx;  // cell i-1 exists
+        pxp = i >= 0 && i < p.nx;   // cell i exists
+        pym = j >= 1 && j <= p.ny;
+        pyp = j >= 0 && j < p.ny;
+    }
 
-    // Register prefetch, one plane ahead: the global loads for node plane k+1
-    // and cell (i,j,k) are issued at step k-1 and land in shared memory at step
-    // k, so their DRAM latency overlaps a whole step of arithmetic.
-    D3 px = D3{0.0, 0.0, 0.0}, pu = px;
-    double pm = 0.0, pe = 0.0;
-    auto fetch = [&](int k) {  // node plane k, cell plane k-1
+    // global loads of node plane k and cell (i,j,k-1) into registers
+    __device__ __forceinline__ void fetch(int k)
+    {
         px = D3{0.0, 0.0, 0.0};
         pu = px;
         if (col_in && k >= 0 && k <= p.nz) {
-            long long n = nidx(s, p, i, j, k);
-            px = pos<EULER>(s, p, cur, i, j, k);
+            long long n = nb + (long long)k * s.pn;
+            if (EULER) px = D3{s.Xt[i], s.Yt[j], s.Zt[k - s.kb]};
+            else px = ld3(s.x[cur], n);
             pu = ld3(s.u[cur], n);
         }
         pm = 0.0;
         pe = 0.0;
         const int kc = k - 1;
-        if (i >= 0 && i < p.nx && j >= 0 && j < p.ny && kc >= 0 && kc < p.nz) {
-            long long c = cidx(s, p, i, j, kc);
+        if (cellcol_in && kc >= 0 && kc < p.nz) {
+            long long c = cb + (long long)kc * s.pc;
             pm = mass_cur(s, p, cur)[c];
             pe = s.e[cur][c];
         }
-    };
-    auto put = [&](int k) {
-        int par = k & 1;
-        NODE(par, 0, iy, ix) = px.x;
-        NODE(par, 1, iy, ix) = px.y;
-        NODE(par, 2, iy, ix) = px.z;
-        NODE(par, 3, iy, ix) = pu.x;
-        NODE(par, 4, iy, ix) = pu.y;
-        NODE(par, 5, iy, ix) = pu.z;
-    };
-    // z-face at node plane k anchored at this column: nodes (i,j),(i+1,j),(i+1,j+1),(i,j+1)
-    auto zface = [&](int k) {
-        int par = k & 1;
-        return faceq(node_pos(par, iy, ix), node_pos(par, iy, ixp), node_pos(par, iyp, ixp), node_pos(par, iyp, ix),
-                     node_vel(par, iy, ix), node_vel(par, iy, ixp), node_vel(par, iyp, ixp), node_vel(par, iyp, ix));
-    };
+    }
+    template <int PAR>
+    __device__ __forceinline__ void put()
+    {
+        st3s(me, oN(PAR, 0), PL, px);
+        st3s(me, oN(PAR, 3), PL, pu);
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 X(int off) const { return ld3s(me + off, oN(PAR, 0), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oN(PAR, 3), PL); }
 
-    // prologue: node plane za-1 and its z-faces (the -z faces of cell plane za-1)
-    fetch(za - 1);
-    put(za - 1);
-    fetch(za);
-    __syncthreads();
-    FaceQ zprev = zface(za - 1);
+    template <int PAR>
+    __device__ __forceinline__ FaceQ zface() const
+    {
+        return faceq(X<PAR>(0), X<PAR>(1), X<PAR>(FW + 1), X<PAR>(FW), U<PAR>(0), U<PAR>(1), U<PAR>(FW + 1),
+                     U<PAR>(FW));
+    }
 
-    for (int kz = za - 1; kz <= zb; ++kz) {
-        const int b0 = kz & 1, b1 = (kz + 1) & 1;
-        // ---- P1: node plane kz+1 and cell (i,j,kz) from the prefetch registers; prefetch the next
-        put(kz + 1);
-        const bool cell_in = i >= 0 && i < p.nx && j >= 0 && j < p.ny && kz >= 0 && kz < p.nz;
+    template <int B0>
+    __device__ __forceinline__ void step(int kz)
+    {
+        constexpr int B1 = B0 ^ 1;
+        // ---- P1: stage node plane kz+1 and cell (i,j,kz); prefetch the next
+        put<B1>();
         const double m = pm, e = pe;
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
-        // ---- P2: faces of cell plane kz anchored at this column
+        // ---- P2: the three faces anchored at this column
         // x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
-        FaceQ fx = faceq(node_pos(b0, iy, ix), node_pos(b0, iyp, ix), node_pos(b1, iyp, ix), node_pos(b1, iy, ix),
-                         node_vel(b0, iy, ix), node_vel(b0, iyp, ix), node_vel(b1, iyp, ix), node_vel(b1, iy, ix));
+        const FaceQ fx = faceq(X<B0>(0), X<B0>(FW), X<B1>(FW), X<B1>(0), U<B0>(0), U<B0>(FW), U<B1>(FW), U<B1>(0));
         // y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
-        FaceQ fy = faceq(node_pos(b0, iy, ix), node_pos(b1, iy, ix), node_pos(b1, iy, ixp), node_pos(b0, iy, ixp),
-                         node_vel(b0, iy, ix), node_vel(b1, iy, ix), node_vel(b1, iy, ixp), node_vel(b0, iy, ixp));
-        FaceQ znext = zface(kz + 1);
-        {
-            double* q0 = sQ;            // x-face
-            double* q1 = sQ + 7 * PL;   // y-face
-            q0[0 * PL + tid] = fx.s;
-            q0[1 * PL + tid] = fx.Xb.x; q0[2 * PL + tid] = fx.Xb.y; q0[3 * PL + tid] = fx.Xb.z;
-            q0[4 * PL + tid] = fx.Ub.x; q0[5 * PL + tid] = fx.Ub.y; q0[6 * PL + tid] = fx.Ub.z;
-            q1[0 * PL + tid] = fy.s;
-            q1[1 * PL + tid] = fy.Xb.x; q1[2 * PL + tid] = fy.Xb.y; q1[3 * PL + tid] = fy.Xb.z;
-            q1[4 * PL + tid] = fy.Ub.x; q1[5 * PL + tid] = fy.Ub.y; q1[6 * PL + tid] = fy.Ub.z;
-            double* ax = sA + ((b0 * 2 + 0) * 3) * PL;
-            double* ay = sA + ((b0 * 2 + 1) * 3) * PL;
-            ax[0 * PL + tid] = fx.A.x; ax[1 * PL + tid] = fx.A.y; ax[2 * PL + tid] = fx.A.z;
-            ay[0 * PL + tid] = fy.A.x; ay[1 * PL + tid] = fy.A.y; ay[2 * PL + tid] = fy.A.z;
-            double* az = sZ + (b1 * 3) * PL;
-            az[0 * PL + tid] = znext.A.x; az[1 * PL + tid] = znext.A.y; az[2 * PL + tid] = znext.A.z;
-        }
+        const FaceQ fy = faceq(X<B0>(0), X<B1>(0), X<B1>(1), X<B0>(1), U<B0>(0), U<B1>(0), U<B1>(1), U<B0>(1));
+        // z-face at node plane kz+1
+        const FaceQ zn = zface<B1>();
+        me[oQ(0, 0)] = fx.s;
+        st3s(me, oQ(0, 1), PL, fx.Xb);
+        st3s(me, oQ(0, 4), PL, fx.Ub);
+        me[oQ(1, 0)] = fy.s;
+        st3s(me, oQ(1, 1), PL, fy.Xb);
+        st3s(me, oQ(1, 4), PL, fy.Ub);
+        st3s(me, oA(B0, 0), PL, fx.A);
+        st3s(me, oA(B0, 1), PL, fy.A);
+        st3s(me, oZ(B1), PL, zn.A);
         __syncthreads();
         // ---- P3: cell (i,j,kz): V, rho, EoS, q, sigma
         {
             double sig = 0.0;
-            if (cell_in) {
-                const double* q0 = sQ;
-                const double* q1 = sQ + 7 * PL;
-                const int tx = iy * FW + ixp, ty = iyp * FW + ix;
-                double sxp = q0[tx], syp = q1[ty];
-                double sv[6] = {fx.s, sxp, fy.s, syp, zprev.s, znext.s};
+            if (cellcol_in && kz >= 0 && kz < p.nz) {
+                const double* qx = me + 1;   // +x face (anchored at i+1)
+                const double* qy = me + FW;  // +y face (anchored at j+1)
+                double sv[6] = {fx.s, qx[oQ(0, 0)], fy.s, qy[oQ(1, 0)], zprev.s, zn.s};
                 double V = vol_from_s(sv);
                 double rho = m / V, pr, pf, cs;
                 eos(p.gamma, rho, e, pr, pf, cs);
-                D3 Xxp = D3{q0[1 * PL + tx], q0[2 * PL + tx], q0[3 * PL + tx]};
-                D3 Uxp = D3{q0[4 * PL + tx], q0[5 * PL + tx], q0[6 * PL + tx]};
-                D3 Xyp = D3{q1[1 * PL + ty], q1[2 * PL + ty], q1[3 * PL + ty]};
-                D3 Uyp = D3{q1[4 * PL + ty], q1[5 * PL + ty], q1[6 * PL + ty]};
-                double dx = axis_jump(fx.Xb, Xxp, fx.Ub, Uxp);
-                double dy = axis_jump(fy.Xb, Xyp, fy.Ub, Uyp);
-                double dz = axis_jump(zprev.Xb, znext.Xb, zprev.Ub, znext.Ub);
+                double dx = axis_jump(fx.Xb, ld3s(qx, oQ(0, 1), PL), fx.Ub, ld3s(qx, oQ(0, 4), PL));
+                double dy = axis_jump(fy.Xb, ld3s(qy, oQ(1, 1), PL), fy.Ub, ld3s(qy, oQ(1, 4), PL));
+                double dz = axis_jump(zprev.Xb, zn.Xb, zprev.Ub, zn.Ub);
                 double du = dmin(dmin(dx, dy), dz);
                 double q = q_of_du(rho, cs, du, p.c1, p.c2);
                 sig = 0.25 * (pf + q);
-                if (kz >= za && kz >= kn0 && kz < kn1 && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY)
-                    s.sig[cidx(s, p, i, j, kz)] = sig;
+                if (sig_col && kz >= za && kz >= kn0 && kz < kn1) s.sig[cb + (long long)kz * s.pc] = sig;
             }
-            sS[(b0 * 2 + 0) * PL + tid] = sig;
-            sS[(b0 * 2 + 1) * PL + tid] = m;
+            me[oS(B0, 0)] = sig;
+            me[oS(B0, 1)] = m;
         }
-        zprev = znext;
+        zprev = zn;
         __syncthreads();
         // ---- P4: node (i,j,kz): force + mass gather, kinematics, BC, move
-        if (kz >= za && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY && col_in) {
+        if (node_out && kz >= za) {
+            const bool pzm = kz >= 1, pzp = kz < p.nz;
             D3 F = D3{0.0, 0.0, 0.0};
             double M = 0.0;
             bool first = true;
-            const int bz = kz & 1;
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
                 const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
-                const int ci = i - 1 + ap, cj = j - 1 + bp, ck = kz - 1 + cp;
-                if (!cell_in_dom(p, ci, cj, ck)) continue;
-                const int pc = ck & 1;
-                const int cx = ix - 1 + ap, cy = iy - 1 + bp;
-                const double* ax = sA + ((pc * 2 + 0) * 3) * PL + cy * FW + ix;   // x-face at plane i, row cj
-                const double* ay = sA + ((pc * 2 + 1) * 3) * PL + iy * FW + cx;   // y-face at plane j, col ci
-                const double* az = sZ + (bz * 3) * PL + cy * FW + cx;             // z-face at plane kz, (ci,cj)
-                D3 Ax = D3{ax[0], ax[PL], ax[2 * PL]};
-                D3 Ay = D3{ay[0], ay[PL], ay[2 * PL]};
-                D3 Az = D3{az[0], az[PL], az[2 * PL]};
-                D3 C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
-                const double sg = sS[(pc * 2 + 0) * PL + cy * FW + cx];
-                const double mk = sS[(pc * 2 + 1) * PL + cy * FW + cx];
-                D3 term = scl(sg, C);
-                if (first) {
-                    F = term;
-                    M = mk;
+                const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
+                const int dx = ap ? 0 : -1, dy = bp ? 0 : -FW;
+                const int PAR = cp ? B0 : B1;  // plane parity of cell kz-1+cp
+                const D3 Ax = ld3s(me + dy, oA(PAR, 0), PL);       // x-face at node plane i, row j-1+bp
+                const D3 Ay = ld3s(me + dx, oA(PAR, 1), PL);       // y-face at node plane j, col i-1+ap
+                const D3 Az = ld3s(me + dx + dy, oZ(B0), PL);      // z-face at node plane kz
+                const D3 C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
+                const double sg = me[dx + dy + oS(PAR, 0)];
+                const double mk = me[dx + dy + oS(PAR, 1)];
+                const D3 term = scl(sg, C);
+                if (pres) {
+                    F = first ? term : add(F, term);
+                    M = first ? mk : M + mk;
                     first = false;
-                } else {
-                    F = add(F, term);
-                    M = M + mk;
                 }
             }
             M = 0.125 * M;
-            D3 u = node_vel(bz, iy, ix);
-            D3 x = node_pos(bz, iy, ix);
+            const D3 u = U<B0>(0), x = X<B0>(0);
             D3 un = d3(u.x + ((F.x / M) * dt), u.y + ((F.y / M) * dt), u.z + ((F.z / M) * dt));
             un = reflect(p, i, j, kz, un);
-            D3 xn = d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt));
-            long long n = nidx(s, p, i, j, kz);
+            const D3 xn = d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt));
+            const long long n = nb + (long long)kz * s.pn;
             if (EULER) {
                 st3(s.u1, n, un);
                 st3(s.x1, n, xn);
@@ -250,93 +244,135 @@ __global__ void __launch_bounds__(FW * NW, MINB)
             }
         }
     }
+
+    __device__ __forceinline__ void run()
+    {
+        // prologue: node plane za-1 and its z-faces (the -z faces of cell plane za-1)
+        fetch(za - 1);
+        if ((za - 1) & 1) put<1>();
+        else put<0>();
+        fetch(za);
+        __syncthreads();
+        zprev = ((za - 1) & 1) ? zface<1>() : zface<0>();
+        for (int kz = za - 1; kz <= zb; ++kz) {
+            if (kz & 1) step<1>(kz);
+            else step<0>(kz);
+        }
+    }
+};
+
+template <bool EULER, int NW>
+__global__ void __launch_bounds__(FW * NW, MINB)
+    kf_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    ForceCTA<EULER, NW> c(s, p, cur, smem, kn0, kn1, zchunk);
+    c.run();
 }
 
 // ============================================================================
-// kf_energy: cell planes [kc0, kc1), z-chunked.  Columns i = i0 + ix (no lower halo).
+// kf_energy
 // ============================================================================
 template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, MINB)
-    kf_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
-{
-    if (!s.st->active) return;
-    constexpr int TX = FW - 1, TY = NW - 1;
-    extern __shared__ double smem[];
-    constexpr int PL = NW * FW;
-    double* sP = smem;                  // [2 parity][10][PL] x^n(3), x'(3), ubar(3), |u'|^2 of node planes
-    double* sF = sP + 2 * 10 * PL;      // [2 x|y][4][PL]      A^n(3), s' of x/y faces of cell plane kz
-    double* sE = sF + 2 * 4 * PL;       // [3][PL]             edge^2 minima: x-edges, y-edges (2 planes), z-edge
+struct EnergyCTA {
+    static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
+    __host__ __device__ static constexpr int oP(int par, int c) { return (par * 10 + c) * PL; }  // x^n(3) x'(3) ubar(3) |u'|^2
+    __host__ __device__ static constexpr int oF(int xy, int c) { return 20 * PL + (xy * 4 + c) * PL; }  // A^n(3), s'
+    __host__ __device__ static constexpr int oE(int c) { return 28 * PL + c * PL; }                 // edge^2 minima
+    static constexpr int WORDS = 31 * PL + 2 * PAD;
 
-    const int ix = threadIdx.x, iy = threadIdx.y;
-    const int tid = iy * FW + ix;
-    const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
-    const int i = i0 + ix, j = j0 + iy;
-    const int za = kc0 + blockIdx.z * zchunk;
-    const int zb = imin(kc1 - 1, za + zchunk - 1);
-    const double dt = s.st->dt;
-    const bool col_in = i <= p.nx && j <= p.ny;
-    const int ixp = imin(ix + 1, FW - 1), iyp = imin(iy + 1, NW - 1);
-    unsigned long long key = KEY_NONE;
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, za, zb;
+    long long nb, cb;
+    double dt;
+    bool col_in, cell_col;
+    unsigned long long key;
+    D3 fx, fu, fu1, fx1;  // prefetch registers
+    double fm, fe, fs;
+    D3 zA_prev;
+    double zs_prev, ex_prev, ey_prev;
 
-    auto P = [&](int par, int comp, int y, int x) -> double& { return sP[(par * 10 + comp) * PL + y * FW + x]; };
-    auto xn_at = [&](int par, int y, int x) { return D3{P(par, 0, y, x), P(par, 1, y, x), P(par, 2, y, x)}; };
-    auto x1_at = [&](int par, int y, int x) { return D3{P(par, 3, y, x), P(par, 4, y, x), P(par, 5, y, x)}; };
-    auto ub_at = [&](int par, int y, int x) { return D3{P(par, 6, y, x), P(par, 7, y, x), P(par, 8, y, x)}; };
+    __device__ __forceinline__ EnergyCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kc0, int kc1,
+                                         int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + PAD + iy * FW + ix;
+        i = blockIdx.x * TX + ix;
+        j = blockIdx.y * TY + iy;
+        za = kc0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kc1 - 1 ? za + zchunk - 1 : kc1 - 1;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        dt = s.st->dt;
+        col_in = i <= p.nx && j <= p.ny;
+        cell_col = i < p.nx && j < p.ny && ix < TX && iy < TY;
+        key = KEY_NONE;
+    }
 
-    // stage node plane k: x^n, x', ubar = 0.5 (u + u'), |u'|^2.  The raw loads
-    // are issued one step ahead into registers (fetch) and staged next step (put).
-    D3 fx = D3{0.0, 0.0, 0.0}, fu = fx, fu1 = fx, fx1 = fx;
-    double fm = 0.0, fe = 0.0, fs = 0.0;
-    auto fetch = [&](int k) {  // node plane k, cell plane k-1
+    __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
+    {
         fx = D3{0.0, 0.0, 0.0};
-        fu = fx; fu1 = fx; fx1 = fx;
+        fu = fx;
+        fu1 = fx;
+        fx1 = fx;
         if (col_in && k >= 0 && k <= p.nz) {
-            long long n = nidx(s, p, i, j, k);
-            fx = pos<EULER>(s, p, cur, i, j, k);
+            long long n = nb + (long long)k * s.pn;
+            if (EULER) fx = D3{s.Xt[i], s.Yt[j], s.Zt[k - s.kb]};
+            else fx = ld3(s.x[cur], n);
             fu = ld3(s.u[cur], n);
             fu1 = EULER ? ld3(s.u1, n) : ld3(s.u[cur ^ 1], n);
             fx1 = EULER ? ld3(s.x1, n) : ld3(s.x[cur ^ 1], n);
         }
-        fm = 0.0; fe = 0.0; fs = 0.0;
+        fm = 0.0;
+        fe = 0.0;
+        fs = 0.0;
         const int kc = k - 1;
-        if (i < p.nx && j < p.ny && kc >= 0 && kc < p.nz && ix < TX && iy < TY) {
-            long long c = cidx(s, p, i, j, kc);
+        if (cell_col && kc >= 0 && kc < p.nz) {
+            long long c = cb + (long long)kc * s.pc;
             fm = mass_cur(s, p, cur)[c];
             fe = s.e[cur][c];
             fs = s.sig[c];
         }
-    };
-    auto put = [&](int k) {
-        int par = k & 1;
-        D3 ub = scl(0.5, add(fu, fu1));
-        double v2 = speed2(fu1);
-        P(par, 0, iy, ix) = fx.x; P(par, 1, iy, ix) = fx.y; P(par, 2, iy, ix) = fx.z;
-        P(par, 3, iy, ix) = fx1.x; P(par, 4, iy, ix) = fx1.y; P(par, 5, iy, ix) = fx1.z;
-        P(par, 6, iy, ix) = ub.x; P(par, 7, iy, ix) = ub.y; P(par, 8, iy, ix) = ub.z;
-        P(par, 9, iy, ix) = v2;
-    };
-
-    // prologue: node plane za; its z-face (A^n, s') and in-plane edges of x'
-    fetch(za);
-    put(za);
-    fetch(za + 1);
-    __syncthreads();
-    D3 zA_prev;
-    double zs_prev, ex_prev, ey_prev;
+    }
+    template <int PAR>
+    __device__ __forceinline__ void put()
     {
-        const int b = za & 1;
-        zA_prev = face_area(xn_at(b, iy, ix), xn_at(b, iy, ixp), xn_at(b, iyp, ixp), xn_at(b, iyp, ix));
-        D3 P0 = x1_at(b, iy, ix), P1 = x1_at(b, iy, ixp), P2 = x1_at(b, iyp, ixp), P3 = x1_at(b, iyp, ix);
-        zs_prev = face_s(avg4(P0, P1, P2, P3), face_area(P0, P1, P2, P3));
-        ex_prev = len2(P0, P1);
-        ey_prev = len2(P0, P3);
+        const D3 ub = scl(0.5, add(fu, fu1));
+        st3s(me, oP(PAR, 0), PL, fx);
+        st3s(me, oP(PAR, 3), PL, fx1);
+        st3s(me, oP(PAR, 6), PL, ub);
+        me[oP(PAR, 9)] = speed2(fu1);
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 Xn(int off) const { return ld3s(me + off, oP(PAR, 0), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 X1(int off) const { return ld3s(me + off, oP(PAR, 3), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 Ub(int off) const { return ld3s(me + off, oP(PAR, 6), PL); }
+    template <int PAR>
+    __device__ __forceinline__ double V2(int off) const { return me[off + oP(PAR, 9)]; }
+
+    template <int B>
+    __device__ __forceinline__ void zstate(D3& zA, double& zs, double& ex, double& ey) const
+    {
+        zA = face_area(Xn<B>(0), Xn<B>(1), Xn<B>(FW + 1), Xn<B>(FW));
+        const D3 T0 = X1<B>(0), T1 = X1<B>(1), T2 = X1<B>(FW + 1), T3 = X1<B>(FW);
+        zs = face_s(avg4(T0, T1, T2, T3), face_area(T0, T1, T2, T3));
+        ex = len2(T0, T1);
+        ey = len2(T0, T3);
     }
 
-    for (int kz = za; kz <= zb; ++kz) {
-        const int b0 = kz & 1, b1 = (kz + 1) & 1;
-        // ---- P1: stage node plane kz+1 / cell kz from the prefetch registers, prefetch the next
-        put(kz + 1);
-        const bool cell_in = i < p.nx && j < p.ny && kz < p.nz;
+    template <int B0>
+    __device__ __forceinline__ void step(int kz)
+    {
+        constexpr int B1 = B0 ^ 1;
+        // ---- P1
+        put<B1>();
         const double m = fm, e = fe, sig = fs;
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
@@ -345,53 +381,44 @@ __global__ void __launch_bounds__(FW * NW, MINB)
         double zs_next, ex_next, ey_next;
         {
             // x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
-            D3 Ax = face_area(xn_at(b0, iy, ix), xn_at(b0, iyp, ix), xn_at(b1, iyp, ix), xn_at(b1, iy, ix));
-            D3 Q0 = x1_at(b0, iy, ix), Q1 = x1_at(b0, iyp, ix), Q2 = x1_at(b1, iyp, ix), Q3 = x1_at(b1, iy, ix);
-            double sx = face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
+            const D3 Ax = face_area(Xn<B0>(0), Xn<B0>(FW), Xn<B1>(FW), Xn<B1>(0));
+            const D3 Q0 = X1<B0>(0), Q1 = X1<B0>(FW), Q2 = X1<B1>(FW), Q3 = X1<B1>(0);
+            const double sx = face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
             // y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
-            D3 Ay = face_area(xn_at(b0, iy, ix), xn_at(b1, iy, ix), xn_at(b1, iy, ixp), xn_at(b0, iy, ixp));
-            D3 R0 = x1_at(b0, iy, ix), R1 = x1_at(b1, iy, ix), R2 = x1_at(b1, iy, ixp), R3 = x1_at(b0, iy, ixp);
-            double sy = face_s(avg4(R0, R1, R2, R3), face_area(R0, R1, R2, R3));
-            // z-face at node plane kz+1
-            zA_next = face_area(xn_at(b1, iy, ix), xn_at(b1, iy, ixp), xn_at(b1, iyp, ixp), xn_at(b1, iyp, ix));
-            D3 T0 = x1_at(b1, iy, ix), T1 = x1_at(b1, iy, ixp), T2 = x1_at(b1, iyp, ixp), T3 = x1_at(b1, iyp, ix);
-            zs_next = face_s(avg4(T0, T1, T2, T3), face_area(T0, T1, T2, T3));
-            ex_next = len2(T0, T1);
-            ey_next = len2(T0, T3);
-            double ez = len2(Q0, Q3);  // z-edge (i,j): kz -> kz+1
-            double* f0 = sF;
-            double* f1 = sF + 4 * PL;
-            f0[0 * PL + tid] = Ax.x; f0[1 * PL + tid] = Ax.y; f0[2 * PL + tid] = Ax.z; f0[3 * PL + tid] = sx;
-            f1[0 * PL + tid] = Ay.x; f1[1 * PL + tid] = Ay.y; f1[2 * PL + tid] = Ay.z; f1[3 * PL + tid] = sy;
-            sE[0 * PL + tid] = dmin(ex_prev, ex_next);
-            sE[1 * PL + tid] = dmin(ey_prev, ey_next);
-            sE[2 * PL + tid] = ez;
+            const D3 Ay = face_area(Xn<B0>(0), Xn<B1>(0), Xn<B1>(1), Xn<B0>(1));
+            const D3 R0 = Q0, R1 = Q3, R2 = X1<B1>(1), R3 = X1<B0>(1);
+            const double sy = face_s(avg4(R0, R1, R2, R3), face_area(R0, R1, R2, R3));
+            zstate<B1>(zA_next, zs_next, ex_next, ey_next);
+            const double ez = len2(Q0, Q3);  // z-edge (i,j): kz -> kz+1
+            st3s(me, oF(0, 0), PL, Ax);
+            me[oF(0, 3)] = sx;
+            st3s(me, oF(1, 0), PL, Ay);
+            me[oF(1, 3)] = sy;
+            me[oE(0)] = dmin(ex_prev, ex_next);
+            me[oE(1)] = dmin(ey_prev, ey_next);
+            me[oE(2)] = ez;
         }
         __syncthreads();
         // ---- P3: cell (i,j,kz)
-        if (cell_in && ix < TX && iy < TY) {
-            const int tx = iy * FW + ixp, ty = iyp * FW + ix;
-            const double* f0 = sF;
-            const double* f1 = sF + 4 * PL;
-            double sv[6] = {f0[3 * PL + tid], f0[3 * PL + tx], f1[3 * PL + tid], f1[3 * PL + ty], zs_prev, zs_next};
-            double V1 = vol_from_s(sv);
+        if (cell_col && kz < p.nz) {
+            double sv[6] = {me[oF(0, 3)], me[1 + oF(0, 3)], me[oF(1, 3)], me[FW + oF(1, 3)], zs_prev, zs_next};
+            const double V1 = vol_from_s(sv);
             const bool owned = kz >= s.k0 && kz < s.k1;
             if (owned && !(V1 > 0.0))
                 atomicMin(&s.st->err_key, (ERR_ORDER_TANGLED << 48) | (unsigned long long)gcell(p, i, j, kz));
-            D3 A[6] = {D3{f0[tid], f0[PL + tid], f0[2 * PL + tid]}, D3{f0[tx], f0[PL + tx], f0[2 * PL + tx]},
-                       D3{f1[tid], f1[PL + tid], f1[2 * PL + tid]}, D3{f1[ty], f1[PL + ty], f1[2 * PL + ty]},
-                       zA_prev, zA_next};
+            const D3 A[6] = {ld3s(me, oF(0, 0), PL),      ld3s(me + 1, oF(0, 0), PL), ld3s(me, oF(1, 0), PL),
+                             ld3s(me + FW, oF(1, 0), PL), zA_prev,                    zA_next};
             double W = 0.0;
 #pragma unroll
             for (int h = 0; h < 8; ++h) {
                 const int a = h & 1, b = (h >> 1) & 1, c = h >> 2;
-                D3 C = corner_vec(A, a, b, c);
-                D3 ub = ub_at(c ? b1 : b0, iy + b, ix + a);
-                double term = dot(C, ub);
+                const D3 C = corner_vec(A, a, b, c);
+                const D3 ub = c ? Ub<B1>(a + b * FW) : Ub<B0>(a + b * FW);
+                const double term = dot(C, ub);
                 W = (h == 0) ? term : W + term;
             }
-            long long cc = cidx(s, p, i, j, kz);
-            double e1 = e - (((sig * W) * dt) / m);
+            const long long cc = cb + (long long)kz * s.pc;
+            const double e1 = e - (((sig * W) * dt) / m);
             if (EULER) {
                 s.e1[cc] = e1;
                 s.V1[cc] = V1;
@@ -400,18 +427,17 @@ __global__ void __launch_bounds__(FW * NW, MINB)
                 if (owned) {
                     double rho = m / V1, pr, pf, cs;
                     eos(p.gamma, rho, e1, pr, pf, cs);
-                    double l2 = dmin(dmin(sE[tid], sE[ty]), dmin(sE[PL + tid], sE[PL + tx]));
-                    l2 = dmin(l2, dmin(dmin(sE[2 * PL + tid], sE[2 * PL + tx]),
-                                       dmin(sE[2 * PL + ty], sE[2 * PL + iyp * FW + ixp])));
-                    double v2 = P(b0, 9, iy, ix);
-                    v2 = dmax(v2, P(b0, 9, iy, ix + 1));
-                    v2 = dmax(v2, P(b0, 9, iy + 1, ix));
-                    v2 = dmax(v2, P(b0, 9, iy + 1, ix + 1));
-                    v2 = dmax(v2, P(b1, 9, iy, ix));
-                    v2 = dmax(v2, P(b1, 9, iy, ix + 1));
-                    v2 = dmax(v2, P(b1, 9, iy + 1, ix));
-                    v2 = dmax(v2, P(b1, 9, iy + 1, ix + 1));
-                    unsigned long long kk = dt_key(dt_cell(p.cfl, l2, v2, cs));
+                    double l2 = dmin(dmin(me[oE(0)], me[FW + oE(0)]), dmin(me[oE(1)], me[1 + oE(1)]));
+                    l2 = dmin(l2, dmin(dmin(me[oE(2)], me[1 + oE(2)]), dmin(me[FW + oE(2)], me[FW + 1 + oE(2)])));
+                    double v2 = V2<B0>(0);
+                    v2 = dmax(v2, V2<B0>(1));
+                    v2 = dmax(v2, V2<B0>(FW));
+                    v2 = dmax(v2, V2<B0>(FW + 1));
+                    v2 = dmax(v2, V2<B1>(0));
+                    v2 = dmax(v2, V2<B1>(1));
+                    v2 = dmax(v2, V2<B1>(FW));
+                    v2 = dmax(v2, V2<B1>(FW + 1));
+                    const unsigned long long kk = dt_key(dt_cell(p.cfl, l2, v2, cs));
                     key = kk < key ? kk : key;  // running min over this column's planes
                 }
             }
@@ -422,26 +448,50 @@ __global__ void __launch_bounds__(FW * NW, MINB)
         ey_prev = ey_next;
         __syncthreads();
     }
-    if (!EULER) {
-        // warp + block min, then one atomicMin per CTA
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-            key = other < key ? other : key;
-        }
-        __shared__ unsigned long long red[32];
-        if (ix == 0) red[iy] = key;
+
+    __device__ __forceinline__ void run()
+    {
+        fetch(za);
+        if (za & 1) put<1>();
+        else put<0>();
+        fetch(za + 1);
         __syncthreads();
-        if (iy == 0) {
-            key = ix < NW ? red[ix] : KEY_NONE;
+        if (za & 1) zstate<1>(zA_prev, zs_prev, ex_prev, ey_prev);
+        else zstate<0>(zA_prev, zs_prev, ex_prev, ey_prev);
+        for (int kz = za; kz <= zb; ++kz) {
+            if (kz & 1) step<1>(kz);
+            else step<0>(kz);
+        }
+        if (!EULER) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
                 key = other < key ? other : key;
             }
-            if (ix == 0 && key != KEY_NONE) atomicMin(&s.st->cand_key, key);
+            __shared__ unsigned long long red[32];
+            if (threadIdx.x == 0) red[threadIdx.y] = key;
+            __syncthreads();
+            if (threadIdx.y == 0) {
+                key = threadIdx.x < NW ? red[threadIdx.x] : KEY_NONE;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+                    key = other < key ? other : key;
+                }
+                if (threadIdx.x == 0 && key != KEY_NONE) atomicMin(&s.st->cand_key, key);
+            }
         }
     }
+};
+
+template <bool EULER, int NW>
+__global__ void __launch_bounds__(FW * NW, MINB)
+    kf_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    EnergyCTA<EULER, NW> c(s, p, cur, smem, kc0, kc1, zchunk);
+    c.run();
 }
 
 // ============================================================================
@@ -451,9 +501,6 @@ namespace {
 constexpr int NW_FORCE = 8;
 constexpr int NW_ENERGY = 8;
 constexpr int ZCHUNK = 32;
-
-constexpr size_t force_smem(int nw) { return sizeof(double) * (size_t)nw * FW * (2 * 6 + 2 * 7 + 2 * 2 * 3 + 2 * 3 + 2 * 2); }
-constexpr size_t energy_smem(int nw) { return sizeof(double) * (size_t)nw * FW * (2 * 10 + 2 * 4 + 3); }
 
 template <typename K>
 void set_smem(K kernel, size_t bytes)
@@ -469,16 +516,18 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
     cudaStream_t cs = (cudaStream_t)st;
     // node planes updated / cell planes energised (Euler: plus the ghost region the remap needs)
-    int kn0, kn1, kc0, kc1;
+    int kn0, kn1;
     if (!EULER) {
-        kn0 = s.k0; kn1 = s.k1; kc0 = s.k0; kc1 = s.k1;
+        kn0 = s.k0;
+        kn1 = s.k1;
     } else {
-        kn0 = imax_h(s.k0 - 2, 0); kn1 = imin_h(s.k1 + 2, p.nz);
-        kc0 = kn0; kc1 = kn1;
+        kn0 = imax_h(s.k0 - 2, 0);
+        kn1 = imin_h(s.k1 + 2, p.nz);
     }
+    const int kc0 = kn0, kc1 = kn1;
     {
         constexpr int NW = NW_FORCE;
-        size_t sm = force_smem(NW);
+        const size_t sm = sizeof(double) * ForceCTA<EULER, NW>::WORDS;
         static bool init = false;
         if (!init) {
             set_smem(kf_force<EULER, NW>, sm);
@@ -489,7 +538,7 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     }
     {
         constexpr int NW = NW_ENERGY;
-        size_t sm = energy_smem(NW);
+        const size_t sm = sizeof(double) * EnergyCTA<EULER, NW>::WORDS;
         static bool init = false;
         if (!init) {
             set_smem(kf_energy<EULER, NW>, sm);
