@@ -57,6 +57,7 @@ __global__ void k_sedov_cells(Slab s, Phys p)
     for (int h = 0; h < 8; ++h) N[h] = tpos(s, i + (h & 1), j + ((h >> 1) & 1), k + (h >> 2));
     double m = p.rho0 * hex_volume(N);
     s.m[0][c] = m;
+    if (p.rezone) s.VT[c] = hex_volume(N) ;  // V^T (c.2 on x^T), constant in Euler mode
     s.e[0][c] = (i == 0 && j == 0 && k == 0) ? p.e_dep / m : p.e_bg;
 }
 

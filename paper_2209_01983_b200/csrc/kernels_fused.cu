@@ -26,6 +26,9 @@
 // need clamping; cell presence in the node gather is a predicate, not a branch.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "sale_mesh.cuh"
 
 namespace sale {
@@ -262,7 +265,7 @@ struct ForceCTA {
 };
 
 template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, MINB)
+__global__ void __launch_bounds__(FW * NW, NW >= 12 ? 1 : MINB)
     kf_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
 {
     if (!s.st->active) return;
@@ -485,7 +488,7 @@ struct EnergyCTA {
 };
 
 template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, MINB)
+__global__ void __launch_bounds__(FW * NW, NW >= 12 ? 1 : MINB)
     kf_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
     if (!s.st->active) return;
@@ -511,9 +514,45 @@ void set_smem(K kernel, size_t bytes)
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 }  // namespace
 
+template <bool EULER, int NW>
+static void force_launch(const Slab& s, const Phys& p, int cur, int kn0, int kn1, int zc, cudaStream_t cs)
+{
+    const size_t sm = sizeof(double) * ForceCTA<EULER, NW>::WORDS;
+    static bool init = false;
+    if (!init) {
+        set_smem(kf_force<EULER, NW>, sm);
+        init = true;
+    }
+    dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW - 2), cdiv(kn1 - kn0 + 1, zc));
+    kf_force<EULER, NW><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
+}
+template <bool EULER, int NW>
+static void energy_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
+{
+    const size_t sm = sizeof(double) * EnergyCTA<EULER, NW>::WORDS;
+    static bool init = false;
+    if (!init) {
+        set_smem(kf_energy<EULER, NW>, sm);
+        init = true;
+    }
+    dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
+    kf_energy<EULER, NW><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
+}
+
+// tile / chunk choice (SALE_TUNE="nwf,nwe,zchunk" overrides, for tuning runs)
+struct Tune {
+    int nwf = NW_FORCE, nwe = NW_ENERGY, zc = ZCHUNK;
+    Tune()
+    {
+        if (const char* t = getenv("SALE_TUNE")) sscanf(t, "%d,%d,%d", &nwf, &nwe, &zc);
+        if (zc < 4) zc = 4;
+    }
+};
+
 template <bool EULER>
 static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
+    static const Tune tune;
     cudaStream_t cs = (cudaStream_t)st;
     // node planes updated / cell planes energised (Euler: plus the ghost region the remap needs)
     int kn0, kn1;
@@ -525,28 +564,12 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
         kn1 = imin_h(s.k1 + 2, p.nz);
     }
     const int kc0 = kn0, kc1 = kn1;
-    {
-        constexpr int NW = NW_FORCE;
-        const size_t sm = sizeof(double) * ForceCTA<EULER, NW>::WORDS;
-        static bool init = false;
-        if (!init) {
-            set_smem(kf_force<EULER, NW>, sm);
-            init = true;
-        }
-        dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW - 2), cdiv(kn1 - kn0 + 1, ZCHUNK));
-        kf_force<EULER, NW><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, ZCHUNK);
-    }
-    {
-        constexpr int NW = NW_ENERGY;
-        const size_t sm = sizeof(double) * EnergyCTA<EULER, NW>::WORDS;
-        static bool init = false;
-        if (!init) {
-            set_smem(kf_energy<EULER, NW>, sm);
-            init = true;
-        }
-        dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, ZCHUNK));
-        kf_energy<EULER, NW><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, ZCHUNK);
-    }
+    if (tune.nwf >= 16) force_launch<EULER, 16>(s, p, cur, kn0, kn1, tune.zc, cs);
+    else if (tune.nwf >= 12) force_launch<EULER, 12>(s, p, cur, kn0, kn1, tune.zc, cs);
+    else force_launch<EULER, 8>(s, p, cur, kn0, kn1, tune.zc, cs);
+    if (tune.nwe >= 16) energy_launch<EULER, 16>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else if (tune.nwe >= 12) energy_launch<EULER, 12>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else energy_launch<EULER, 8>(s, p, cur, kc0, kc1, tune.zc, cs);
     return 2;
 }
 
@@ -555,7 +578,5 @@ int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     return p.rezone ? lagrange_fused<true>(s, p, cur, st) : lagrange_fused<false>(s, p, cur, st);
 }
 
-// remap: the v0 kernels for now (they read x1/u1/e1/V1 written above)
-int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st) { return launch_remap_v0(s, p, cur, st); }
 
 }  // namespace sale

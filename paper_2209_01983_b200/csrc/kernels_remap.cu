@@ -1,0 +1,485 @@
+// kernels_remap.cu -- the fused Eulerian remap
+// as two z-marching kernels:
+//
+//   kr_cells : R1 swept volume of the three faces anchored at each column (each
+//              physical face computed once per CTA), R2 donor-cell fluxes with
+//              the donor data (m/V', e', 8-node mean u') staged in shared
+//              memory, R3 cell update m'', e'', Delta m, Delta P.
+//   kr_nodes : R4 node momentum update u'' from the gathered Delta m, Delta P,
+//              m'' (fixed gather order) + reflecting BC; R5 (x := x^T) is
+//              implicit; then the next cycle's dt candidate (c.5) on the target
+//              mesh with a running min, warp-shuffle + block min, one atomicMin.
+//
+// Same expression trees and association as the oracle / v0 kernels, so the
+// results are bit-identical.  Shared-memory access pattern as in
+// kernels_fused.cu: compile-time plane parity, per-thread base + immediate.
+#include <cuda_runtime.h>
+
+#include "sale_mesh.cuh"
+
+namespace sale {
+
+namespace {
+
+constexpr int RW = 32;
+constexpr int RPAD = RW + 1;
+
+__device__ __forceinline__ D3 ld3r(const double* b, int o0, int stride) { return D3{b[o0], b[o0 + stride], b[o0 + 2 * stride]}; }
+__device__ __forceinline__ void st3r(double* b, int o0, int stride, D3 v)
+{
+    b[o0] = v.x;
+    b[o0 + stride] = v.y;
+    b[o0 + 2 * stride] = v.z;
+}
+
+struct Flux {
+    double mu, eps;
+    D3 pi;
+};
+
+}  // namespace
+
+// ============================================================================
+// kr_cells: cell planes [kr0, kr1) (global), z-chunked.  Columns i = i0-1+ix.
+// ============================================================================
+template <int NW>
+struct RemapCellsCTA {
+    static constexpr int PL = NW * RW, TX = RW - 3, TY = NW - 3;
+    __host__ __device__ static constexpr int oN(int par, int c) { return (par * 6 + c) * PL; }  // x'(3), u'(3)
+    __host__ __device__ static constexpr int oC(int c) { return 12 * PL + c * PL; }            // donor r, e', Ubar(3)
+    __host__ __device__ static constexpr int oF(int par, int xy, int c) { return 17 * PL + ((par * 2 + xy) * 5 + c) * PL; }
+    static constexpr int WORDS = 37 * PL + 2 * RPAD;
+
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, ix, iy, za, zb, kr0, kr1;
+    long long nb, cb;
+    bool col_in, cell_col, xface_on, yface_on, zface_on, upd_on;
+    D3 qx1, qu1;            // prefetch: node x', u'
+    double qm, qe, qv;      // prefetch: cell m, e', V'
+    // own column, previous cell plane (kz-1): donor data and pre-remap state
+    double r_prev, e_prev, m_prev;
+    D3 ub_prev;
+    Flux fz_prev;           // z-face flux at node plane kz-1... carried one step
+
+    __device__ __forceinline__ RemapCellsCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kr0_, int kr1_,
+                                             int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        ix = threadIdx.x;
+        iy = threadIdx.y;
+        me = smem + RPAD + iy * RW + ix;
+        i = blockIdx.x * TX - 1 + ix;
+        j = blockIdx.y * TY - 1 + iy;
+        kr0 = kr0_;
+        kr1 = kr1_;
+        za = kr0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kr1 - 1 ? za + zchunk - 1 : kr1 - 1;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
+        cell_col = i >= 0 && i < p.nx && j >= 0 && j < p.ny;
+        const bool in_x = ix >= 1 && ix <= TX, in_y = iy >= 1 && iy <= TY;
+        // x-faces at node planes [i0, i0+TX] of cell rows [j0, j0+TY); interior iff 1 <= i <= nx-1
+        xface_on = ix >= 1 && ix <= TX + 1 && in_y && i >= 1 && i <= p.nx - 1 && j >= 0 && j < p.ny;
+        yface_on = in_x && iy >= 1 && iy <= TY + 1 && j >= 1 && j <= p.ny - 1 && i >= 0 && i < p.nx;
+        zface_on = in_x && in_y && cell_col;
+        upd_on = in_x && in_y && cell_col;
+    }
+
+    __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
+    {
+        qx1 = D3{0.0, 0.0, 0.0};
+        qu1 = qx1;
+        if (col_in && k >= 0 && k <= p.nz) {
+            long long n = nb + (long long)k * s.pn;
+            qx1 = ld3(s.x1, n);
+            qu1 = ld3(s.u1, n);
+        }
+        qm = 0.0;
+        qe = 0.0;
+        qv = 1.0;
+        const int kc = k - 1;
+        if (cell_col && kc >= 0 && kc < p.nz) {
+            long long c = cb + (long long)kc * s.pc;
+            qm = s.m[cur][c];
+            qe = s.e1[c];
+            qv = s.V1[c];
+        }
+    }
+    template <int PAR>
+    __device__ __forceinline__ void put()
+    {
+        st3r(me, oN(PAR, 0), PL, qx1);
+        st3r(me, oN(PAR, 3), PL, qu1);
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 XL(int off) const { return ld3r(me + off, oN(PAR, 0), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 UL(int off) const { return ld3r(me + off, oN(PAR, 3), PL); }
+    __device__ __forceinline__ D3 XT(int di, int dj, int k) const
+    {
+        return D3{s.Xt[i + di], s.Yt[j + dj], s.Zt[k - s.kb]};
+    }
+
+    // donor-cell flux through a face with swept volume dV, donors lower (L) / upper (U)
+    __device__ __forceinline__ static Flux flux(double dV, double rL, double eL, D3 uL, double rU, double eU, D3 uU)
+    {
+        const bool low = dV > 0.0;
+        Flux f;
+        f.mu = (low ? rL : rU) * dV;
+        f.eps = f.mu * (low ? eL : eU);
+        f.pi = scl(f.mu, low ? uL : uU);
+        return f;
+    }
+
+    template <int B0>
+    __device__ __forceinline__ void step(int kz)
+    {
+        constexpr int B1 = B0 ^ 1;
+        // ---- P1: stage node plane kz+1, cell (i,j,kz); prefetch next
+        put<B1>();
+        const double m = qm, e1 = qe, V1 = qv;
+        if (kz < zb + 1) fetch(kz + 2);
+        __syncthreads();
+        // ---- P2: donor data of cell (i,j,kz); swept volumes of the anchored faces
+        const bool cell_ok = cell_col && kz >= 0 && kz < p.nz;
+        D3 ub = D3{0.0, 0.0, 0.0};
+        double r = 0.0;
+        if (cell_ok) {
+            // Ubar = 0.125 * (sum of u' over the 8 corners, corner order)
+            D3 sum = UL<B0>(0);
+            sum = add(sum, UL<B0>(1));
+            sum = add(sum, UL<B0>(RW));
+            sum = add(sum, UL<B0>(RW + 1));
+            sum = add(sum, UL<B1>(0));
+            sum = add(sum, UL<B1>(1));
+            sum = add(sum, UL<B1>(RW));
+            sum = add(sum, UL<B1>(RW + 1));
+            ub = scl(0.125, sum);
+            r = m / V1;
+        }
+        me[oC(0)] = r;
+        me[oC(1)] = e1;
+        st3r(me, oC(2), PL, ub);
+        double dVx = 0.0, dVy = 0.0, dVz = 0.0;
+        const bool do_x = xface_on && kz >= 0 && kz < p.nz && kz >= za && kz <= zb;
+        const bool do_y = yface_on && kz >= 0 && kz < p.nz && kz >= za && kz <= zb;
+        const bool do_z = zface_on && kz >= 1 && kz <= p.nz - 1 && kz >= za;
+        if (do_x)  // x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
+            dVx = swept_volume(XT(0, 0, kz), XT(0, 1, kz), XT(0, 1, kz + 1), XT(0, 0, kz + 1), XL<B0>(0),
+                               XL<B0>(RW), XL<B1>(RW), XL<B1>(0));
+        if (do_y)  // y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
+            dVy = swept_volume(XT(0, 0, kz), XT(0, 0, kz + 1), XT(1, 0, kz + 1), XT(1, 0, kz), XL<B0>(0),
+                               XL<B1>(0), XL<B1>(1), XL<B0>(1));
+        if (do_z)  // z-face at node plane kz: (i,j,kz) (i+1,j,kz) (i+1,j+1,kz) (i,j+1,kz)
+            dVz = swept_volume(XT(0, 0, kz), XT(1, 0, kz), XT(1, 1, kz), XT(0, 1, kz), XL<B0>(0), XL<B0>(1),
+                               XL<B0>(RW + 1), XL<B0>(RW));
+        __syncthreads();
+        // ---- P3: fluxes (boundary faces: +0.0)
+        Flux fx = Flux{0.0, 0.0, D3{0.0, 0.0, 0.0}}, fy = fx, fz = fx;
+        if (do_x) {
+            const double* L = me - 1;
+            fx = flux(dVx, L[oC(0)], L[oC(1)], ld3r(L, oC(2), PL), r, e1, ub);
+        }
+        if (do_y) {
+            const double* L = me - RW;
+            fy = flux(dVy, L[oC(0)], L[oC(1)], ld3r(L, oC(2), PL), r, e1, ub);
+        }
+        if (do_z) fz = flux(dVz, r_prev, e_prev, ub_prev, r, e1, ub);
+        me[oF(B0, 0, 0)] = fx.mu;
+        me[oF(B0, 0, 1)] = fx.eps;
+        st3r(me, oF(B0, 0, 2), PL, fx.pi);
+        me[oF(B0, 1, 0)] = fy.mu;
+        me[oF(B0, 1, 1)] = fy.eps;
+        st3r(me, oF(B0, 1, 2), PL, fy.pi);
+        __syncthreads();
+        // ---- P4: cell update for cell plane kz-1
+        const int kc = kz - 1;
+        if (upd_on && kc >= za && kc >= 0 && kc < p.nz) {
+            const double* own = me;
+            const double* xp = me + 1;
+            const double* yp = me + RW;
+            const double mu[6] = {own[oF(B1, 0, 0)], xp[oF(B1, 0, 0)], own[oF(B1, 1, 0)], yp[oF(B1, 1, 0)],
+                                  fz_prev.mu, fz.mu};
+            const double ep[6] = {own[oF(B1, 0, 1)], xp[oF(B1, 0, 1)], own[oF(B1, 1, 1)], yp[oF(B1, 1, 1)],
+                                  fz_prev.eps, fz.eps};
+            const D3 pi[6] = {ld3r(own, oF(B1, 0, 2), PL), ld3r(xp, oF(B1, 0, 2), PL), ld3r(own, oF(B1, 1, 2), PL),
+                              ld3r(yp, oF(B1, 1, 2), PL), fz_prev.pi, fz.pi};
+            const double dm = ((((mu[0] - mu[1]) + mu[2]) - mu[3]) + mu[4]) - mu[5];
+            const double dE = ((((ep[0] - ep[1]) + ep[2]) - ep[3]) + ep[4]) - ep[5];
+            const D3 dP = sub(add(sub(add(sub(pi[0], pi[1]), pi[2]), pi[3]), pi[4]), pi[5]);
+            const double m2 = m_prev + dm;
+            if (kc >= s.k0 && kc < s.k1 && !(m2 > 0.0))
+                atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, kc));
+            const long long c = cb + (long long)kc * s.pc;
+            s.e[cur ^ 1][c] = e_prev + ((dE - (e_prev * dm)) / m2);
+            s.m[cur ^ 1][c] = m2;
+            s.dm[c] = dm;
+            st3(s.dP, c, dP);
+        }
+        r_prev = r;
+        e_prev = e1;
+        m_prev = m;
+        ub_prev = ub;
+        fz_prev = fz;
+    }
+
+    __device__ __forceinline__ void run()
+    {
+        // prologue: node plane za-1 staged, prefetch node plane za + cell za-1
+        fetch(za - 1);
+        if ((za - 1) & 1) put<1>();
+        else put<0>();
+        fetch(za);
+        __syncthreads();
+        fz_prev = Flux{0.0, 0.0, D3{0.0, 0.0, 0.0}};
+        r_prev = 0.0;
+        e_prev = 0.0;
+        m_prev = 0.0;
+        ub_prev = D3{0.0, 0.0, 0.0};
+        // step kz computes donor data / fluxes of plane kz and updates plane kz-1
+        for (int kz = za - 1; kz <= zb + 1; ++kz) {
+            if (kz & 1) step<1>(kz);
+            else step<0>(kz);
+        }
+    }
+};
+
+template <int NW>
+__global__ void __launch_bounds__(RW * NW, 2) kr_cells(Slab s, Phys p, int cur, int kr0, int kr1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    RemapCellsCTA<NW> c(s, p, cur, smem, kr0, kr1, zchunk);
+    c.run();
+}
+
+// ============================================================================
+// kr_nodes: node planes [k0, k1] + dt candidate of cells [k0, k1).  Columns i = i0-1+ix.
+// ============================================================================
+template <int NW>
+struct RemapNodesCTA {
+    static constexpr int PL = NW * RW, TX = RW - 2, TY = NW - 2;
+    __host__ __device__ static constexpr int oU(int par, int c) { return (par * 5 + c) * PL; }  // dm, dP(3), m''
+    __host__ __device__ static constexpr int oV(int par) { return 10 * PL + par * PL; }         // |u''|^2
+    static constexpr int WORDS = 12 * PL + 2 * RPAD;
+
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, za, zb, zlast;
+    long long nb, cb;
+    bool col_in, cell_col, node_calc, node_out, dt_col, pxm, pxp, pym, pyp;
+    unsigned long long key;
+    double qdm, qm2, qe2, qvt;
+    D3 qdp, qu1;
+    double l2;
+
+    __device__ __forceinline__ RemapNodesCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + RPAD + iy * RW + ix;
+        i = blockIdx.x * TX - 1 + ix;
+        j = blockIdx.y * TY - 1 + iy;
+        za = s.k0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < s.k1 ? za + zchunk - 1 : s.k1;   // node planes written [za, zb]
+        zlast = zb + 1 <= s.k1 ? zb + 1 : s.k1;                  // node planes computed [za, zlast]
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
+        cell_col = i >= 0 && i < p.nx && j >= 0 && j < p.ny;
+        const bool in_x = ix >= 1 && ix <= TX, in_y = iy >= 1 && iy <= TY;
+        node_calc = col_in && ix >= 1 && iy >= 1;   // nodes [i0, i0+TX] (the last is the neighbour's)
+        node_out = node_calc && in_x && in_y;        // nodes owned by this CTA
+        dt_col = cell_col && in_x && in_y;
+        pxm = i >= 1 && i <= p.nx;
+        pxp = i >= 0 && i < p.nx;
+        pym = j >= 1 && j <= p.ny;
+        pyp = j >= 0 && j < p.ny;
+        key = KEY_NONE;
+        // c.5 on the target mesh: every edge of cell (i,j) along a is (X_{i+1}-X_i, 0, 0) etc.
+        l2 = 0.0;
+        if (dt_col) {
+            D3 a = D3{s.Xt[i], s.Yt[j], 0.0}, b = D3{s.Xt[i + 1], s.Yt[j + 1], 0.0};
+            const double lx = len2(D3{a.x, 0.0, 0.0}, D3{b.x, 0.0, 0.0});
+            const double ly = len2(D3{0.0, a.y, 0.0}, D3{0.0, b.y, 0.0});
+            l2 = dmin(lx, ly);
+        }
+    }
+
+    __device__ __forceinline__ void fetch(int k)  // cell plane k (Delta m, Delta P, m''), node plane k (u'), cell k-1 (e'', V^T)
+    {
+        qdm = 0.0;
+        qm2 = 0.0;
+        qdp = D3{0.0, 0.0, 0.0};
+        if (cell_col && k >= 0 && k < p.nz) {
+            long long c = cb + (long long)k * s.pc;
+            qdm = s.dm[c];
+            qdp = ld3(s.dP, c);
+            qm2 = s.m[cur ^ 1][c];
+        }
+        qu1 = D3{0.0, 0.0, 0.0};
+        if (col_in && k >= 0 && k <= p.nz) qu1 = ld3(s.u1, nb + (long long)k * s.pn);
+        qe2 = 0.0;
+        qvt = 1.0;
+        const int kc = k - 1;
+        if (dt_col && kc >= 0 && kc < p.nz) {
+            long long c = cb + (long long)kc * s.pc;
+            qe2 = s.e[cur ^ 1][c];
+            qvt = s.VT[c];
+        }
+    }
+
+    template <int B0>
+    __device__ __forceinline__ void step(int kz)
+    {
+        constexpr int B1 = B0 ^ 1;
+        // ---- P1: stage cell plane kz
+        me[oU(B0, 0)] = qdm;
+        st3r(me, oU(B0, 1), PL, qdp);
+        me[oU(B0, 4)] = qm2;
+        const D3 u1 = qu1;
+        const double e2 = qe2, vt = qvt;
+        if (kz < zlast) fetch(kz + 1);
+        __syncthreads();
+        // ---- P2: node (i,j,kz)
+        if (node_calc && kz >= za) {
+            const bool pzm = kz >= 1, pzp = kz < p.nz;
+            double Dm = 0.0, M2 = 0.0;
+            D3 DP = D3{0.0, 0.0, 0.0};
+            bool first = true;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
+                const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
+                const int off = (ap ? 0 : -1) + (bp ? 0 : -RW);
+                const int PAR = cp ? B0 : B1;
+                const double dm = me[off + oU(PAR, 0)];
+                const D3 dp = ld3r(me + off, oU(PAR, 1), PL);
+                const double mm = me[off + oU(PAR, 4)];
+                if (pres) {
+                    Dm = first ? dm : Dm + dm;
+                    DP = first ? dp : add(DP, dp);
+                    M2 = first ? mm : M2 + mm;
+                    first = false;
+                }
+            }
+            Dm = 0.125 * Dm;
+            DP = scl(0.125, DP);
+            M2 = 0.125 * M2;
+            D3 un = d3(u1.x + ((DP.x - (u1.x * Dm)) / M2), u1.y + ((DP.y - (u1.y * Dm)) / M2),
+                       u1.z + ((DP.z - (u1.z * Dm)) / M2));
+            un = reflect(p, i, j, kz, un);
+            if (node_out && kz <= zb) st3(s.u[cur ^ 1], nb + (long long)kz * s.pn, un);
+            me[oV(B0)] = speed2(un);
+        }
+        __syncthreads();
+        // ---- P3: dt candidate of cell (i,j,kz-1) on the target mesh
+        const int kc = kz - 1;
+        if (dt_col && kc >= za && kc <= zb && kc < s.k1) {
+            double v2 = me[oV(B1)];
+            v2 = dmax(v2, me[1 + oV(B1)]);
+            v2 = dmax(v2, me[RW + oV(B1)]);
+            v2 = dmax(v2, me[RW + 1 + oV(B1)]);
+            v2 = dmax(v2, me[oV(B0)]);
+            v2 = dmax(v2, me[1 + oV(B0)]);
+            v2 = dmax(v2, me[RW + oV(B0)]);
+            v2 = dmax(v2, me[RW + 1 + oV(B0)]);
+            const double lz = len2(D3{0.0, 0.0, s.Zt[kc - s.kb]}, D3{0.0, 0.0, s.Zt[kc + 1 - s.kb]});
+            const double m2 = me[oU(B1, 4)];
+            double rho = m2 / vt, pr, pf, cs;
+            eos(p.gamma, rho, e2, pr, pf, cs);
+            const unsigned long long kk = dt_key(dt_cell(p.cfl, dmin(l2, lz), v2, cs));
+            key = kk < key ? kk : key;
+        }
+        __syncthreads();
+    }
+
+    __device__ __forceinline__ void run()
+    {
+        fetch(za - 1);
+        // stage cell plane za-1 directly (B parity of za-1)
+        if ((za - 1) & 1) {
+            me[oU(1, 0)] = qdm;
+            st3r(me, oU(1, 1), PL, qdp);
+            me[oU(1, 4)] = qm2;
+        } else {
+            me[oU(0, 0)] = qdm;
+            st3r(me, oU(0, 1), PL, qdp);
+            me[oU(0, 4)] = qm2;
+        }
+        fetch(za);
+        for (int kz = za; kz <= zlast; ++kz) {
+            if (kz & 1) step<1>(kz);
+            else step<0>(kz);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+            key = other < key ? other : key;
+        }
+        __shared__ unsigned long long red[32];
+        if (threadIdx.x == 0) red[threadIdx.y] = key;
+        __syncthreads();
+        if (threadIdx.y == 0) {
+            key = threadIdx.x < NW ? red[threadIdx.x] : KEY_NONE;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+                key = other < key ? other : key;
+            }
+            if (threadIdx.x == 0 && key != KEY_NONE) atomicMin(&s.st->cand_key, key);
+        }
+    }
+};
+
+template <int NW>
+__global__ void __launch_bounds__(RW * NW, 2) kr_nodes(Slab s, Phys p, int cur, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    RemapNodesCTA<NW> c(s, p, cur, smem, zchunk);
+    c.run();
+}
+
+// ============================================================================
+namespace {
+inline int cdivr(int a, int b) { return (a + b - 1) / b; }
+constexpr int NW_RC = 8, NW_RN = 8, RZ = 32;
+}  // namespace
+
+int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    cudaStream_t cs = (cudaStream_t)st;
+    const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
+    {
+        constexpr int NW = NW_RC;
+        const size_t sm = sizeof(double) * RemapCellsCTA<NW>::WORDS;
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(kr_cells<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            init = true;
+        }
+        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
+        kr_cells<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+    }
+    {
+        constexpr int NW = NW_RN;
+        const size_t sm = sizeof(double) * RemapNodesCTA<NW>::WORDS;
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(kr_nodes<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            init = true;
+        }
+        dim3 grid(cdivr(p.nx + 1, RW - 2), cdivr(p.ny + 1, NW - 2), cdivr(s.k1 - s.k0 + 1, RZ));
+        kr_nodes<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, RZ);
+    }
+    return 2;
+}
+
+}  // namespace sale
