@@ -36,6 +36,11 @@ METRIC = "zone-cycles/s (fp64 SALE cycle)"
 UNIT = "zone-cycles/s"
 # algorithmic bytes per zone-cycle (state read + written once, fp64)
 ALGO_BYTES = {configs.LAGRANGE: 120.0, configs.EULER: 80.0}
+# algorithmic FP64-pipe instructions per zone-cycle of each kernel
+# class (faces / edges / nodes computed once; an IEEE fp64 div or sqrt = 8 FP64
+# instructions, its fast-path SASS sequence)
+ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 702.0, "remap": 0.0},
+             configs.EULER: {"lagrange": 601.0, "remap": 612.0}}
 REASON_BITS = {"hw_slowdown": "hw_slowdown", "hw_thermal_slowdown": "hw_thermal_slowdown",
                "sw_thermal_slowdown": "sw_thermal_slowdown", "sw_power_cap": "sw_power_cap"}
 
@@ -47,6 +52,19 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def fp64_peak():
+    """FP64-pipe instruction rate (T thread-instr/s): the DADD chain rate measured on
+    this pool's B200 by tools/fp64_peak.cu (profiles/r01_fp64_peak.json); fallback
+    derived from unit counts: 148 SM x 64 FP64 lanes x 1.965 GHz = 18.6 T/s."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as f:
+            rows = [json.loads(x) for x in f if x.strip()]
+        v = max(r["thread_inst_per_s_T"] for r in rows)
+        return v, "measured (tools/fp64_peak.cu DADD chains, profiles/r01_fp64_peak.json)"
+    except Exception:
+        return 148 * 64 * 1.965e9 / 1e12, "derived (148 SM x 64 FP64 lanes x 1.965 GHz)"
 
 
 class ClockSampler:
@@ -244,23 +262,29 @@ def main():
     value = gcells * args.steps / (ms * 1e-3)
 
     # ---- roofline of the dominant kernel class -------------------------------
+    # The SALE kernels are bound by the FP64 pipe: report that
+    # roofline ("alu") for the dominant kernel class; the HBM view rides along.
     peak, peak_src = peaks()
+    fpk, fpk_src = fp64_peak()
     local_cells = cfg["nx"] * cfg["ny"] * (ctx.k1 - ctx.k0)
+    mode = cfg["rezone"]
     dom = max(("lagrange", "remap"), key=lambda k: prof[k][0])
     dom_ms, dom_n = prof[dom]
     per_launch_ms = dom_ms / max(dom_n, 1)
-    mode = cfg["rezone"]
-    # algorithmic bytes of one cycle of this rank's slab ...
+    fp64_per_launch = ALGO_FP64[mode][dom] * local_cells          # FP64 instr per launch group
+    achieved_t = fp64_per_launch / (per_launch_ms * 1e-3) / 1e12   # T instr/s
+    cyc_fp64 = sum(ALGO_FP64[mode].values()) * local_cells
+    cyc_t = cyc_fp64 / (ms / args.steps * 1e-3) / 1e12
     cyc_bytes = ALGO_BYTES[mode] * local_cells
-    # ... achieved by the dominant kernel class alone and by the whole cycle
-    achieved = cyc_bytes / (per_launch_ms * 1e-3) / 1e9
     cycle_gbs = cyc_bytes / (ms / args.steps * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": dom,
-                "kernel_ms": per_launch_ms, "kernel_share_of_step": dom_ms / ms,
-                "algo_bytes_per_zone_cycle": ALGO_BYTES[mode],
-                "whole_cycle_gbs": cycle_gbs, "whole_cycle_frac": cycle_gbs / peak,
-                "peak_source": peak_src}
+    roofline = {"bound": "alu", "achieved": achieved_t, "peak": fpk, "unit": "T fp64-instr/s",
+                "frac": achieved_t / fpk, "traffic": None, "kernel": dom,
+                "kernel_ms_per_launch": per_launch_ms, "kernel_share_of_step": dom_ms / ms,
+                "algo_fp64_instr_per_zone": ALGO_FP64[mode][dom], "peak_source": fpk_src,
+                "whole_cycle": {"achieved": cyc_t, "frac": cyc_t / fpk,
+                                "algo_fp64_instr_per_zone": sum(ALGO_FP64[mode].values())},
+                "hbm": {"achieved_gbs": cycle_gbs, "peak_gbs": peak, "frac": cycle_gbs / peak,
+                        "algo_bytes_per_zone_cycle": ALGO_BYTES[mode], "peak_source": peak_src}}
 
     # ---- end to end through the public API with host buffers ------------------
     e2e = None

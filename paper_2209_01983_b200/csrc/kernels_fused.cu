@@ -158,6 +158,41 @@ struct ForceCTA {
                      U<PAR>(FW));
     }
 
+    // c.3 steps 4-5: F = sum over present cells (gather order) of sigma_K C_K,n; M = sum m_K
+    template <int B0, bool ALL>
+    __device__ __forceinline__ void gather(D3& F, double& M, bool pxm_, bool pxp_, bool pym_, bool pyp_, bool pzm,
+                                           bool pzp) const
+    {
+        constexpr int B1 = B0 ^ 1;
+        F = D3{0.0, 0.0, 0.0};
+        M = 0.0;
+        bool first = true;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
+            const int dx = ap ? 0 : -1, dy = bp ? 0 : -FW;
+            const int PAR = cp ? B0 : B1;  // plane parity of cell kz-1+cp
+            const D3 Ax = ld3s(me + dy, oA(PAR, 0), PL);   // x-face at node plane i, row j-1+bp
+            const D3 Ay = ld3s(me + dx, oA(PAR, 1), PL);   // y-face at node plane j, col i-1+ap
+            const D3 Az = ld3s(me + dx + dy, oZ(B0), PL);  // z-face at node plane kz
+            const D3 C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
+            const double sg = me[dx + dy + oS(PAR, 0)];
+            const double mk = me[dx + dy + oS(PAR, 1)];
+            const D3 term = scl(sg, C);
+            if (ALL) {
+                F = g == 0 ? term : add(F, term);
+                M = g == 0 ? mk : M + mk;
+            } else {
+                const bool pres = (ap ? pxp_ : pxm_) && (bp ? pyp_ : pym_) && (cp ? pzp : pzm);
+                if (pres) {
+                    F = first ? term : add(F, term);
+                    M = first ? mk : M + mk;
+                    first = false;
+                }
+            }
+        }
+    }
+
     template <int B0>
     __device__ __forceinline__ void step(int kz)
     {
@@ -210,28 +245,12 @@ struct ForceCTA {
         // ---- P4: node (i,j,kz): force + mass gather, kinematics, BC, move
         if (node_out && kz >= za) {
             const bool pzm = kz >= 1, pzp = kz < p.nz;
-            D3 F = D3{0.0, 0.0, 0.0};
-            double M = 0.0;
-            bool first = true;
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
-                const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
-                const int dx = ap ? 0 : -1, dy = bp ? 0 : -FW;
-                const int PAR = cp ? B0 : B1;  // plane parity of cell kz-1+cp
-                const D3 Ax = ld3s(me + dy, oA(PAR, 0), PL);       // x-face at node plane i, row j-1+bp
-                const D3 Ay = ld3s(me + dx, oA(PAR, 1), PL);       // y-face at node plane j, col i-1+ap
-                const D3 Az = ld3s(me + dx + dy, oZ(B0), PL);      // z-face at node plane kz
-                const D3 C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
-                const double sg = me[dx + dy + oS(PAR, 0)];
-                const double mk = me[dx + dy + oS(PAR, 1)];
-                const D3 term = scl(sg, C);
-                if (pres) {
-                    F = first ? term : add(F, term);
-                    M = first ? mk : M + mk;
-                    first = false;
-                }
-            }
+            D3 F;
+            double M;
+            // interior nodes (all 8 cells present, the common case) take the
+            // select-free path; both paths sum in the same gather order
+            if (pxm && pxp && pym && pyp && pzm && pzp) gather<B0, true>(F, M, true, true, true, true, true, true);
+            else gather<B0, false>(F, M, pxm, pxp, pym, pyp, pzm, pzp);
             M = 0.125 * M;
             const D3 u = U<B0>(0), x = X<B0>(0);
             D3 un = d3(u.x + ((F.x / M) * dt), u.y + ((F.y / M) * dt), u.z + ((F.z / M) * dt));

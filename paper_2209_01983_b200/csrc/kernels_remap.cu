@@ -335,6 +335,39 @@ struct RemapNodesCTA {
         }
     }
 
+    // c.4 step 4: D_m, D_P, M'' sums over the present cells in gather order
+    template <int B0, bool ALL>
+    __device__ __forceinline__ void gather(double& Dm, D3& DP, double& M2, bool pzm, bool pzp, bool) const
+    {
+        constexpr int B1 = B0 ^ 1;
+        Dm = 0.0;
+        M2 = 0.0;
+        DP = D3{0.0, 0.0, 0.0};
+        bool first = true;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
+            const int off = (ap ? 0 : -1) + (bp ? 0 : -RW);
+            const int PAR = cp ? B0 : B1;
+            const double dm = me[off + oU(PAR, 0)];
+            const D3 dp = ld3r(me + off, oU(PAR, 1), PL);
+            const double mm = me[off + oU(PAR, 4)];
+            if (ALL) {
+                Dm = g == 0 ? dm : Dm + dm;
+                DP = g == 0 ? dp : add(DP, dp);
+                M2 = g == 0 ? mm : M2 + mm;
+            } else {
+                const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
+                if (pres) {
+                    Dm = first ? dm : Dm + dm;
+                    DP = first ? dp : add(DP, dp);
+                    M2 = first ? mm : M2 + mm;
+                    first = false;
+                }
+            }
+        }
+    }
+
     template <int B0>
     __device__ __forceinline__ void step(int kz)
     {
@@ -350,25 +383,10 @@ struct RemapNodesCTA {
         // ---- P2: node (i,j,kz)
         if (node_calc && kz >= za) {
             const bool pzm = kz >= 1, pzp = kz < p.nz;
-            double Dm = 0.0, M2 = 0.0;
-            D3 DP = D3{0.0, 0.0, 0.0};
-            bool first = true;
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
-                const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
-                const int off = (ap ? 0 : -1) + (bp ? 0 : -RW);
-                const int PAR = cp ? B0 : B1;
-                const double dm = me[off + oU(PAR, 0)];
-                const D3 dp = ld3r(me + off, oU(PAR, 1), PL);
-                const double mm = me[off + oU(PAR, 4)];
-                if (pres) {
-                    Dm = first ? dm : Dm + dm;
-                    DP = first ? dp : add(DP, dp);
-                    M2 = first ? mm : M2 + mm;
-                    first = false;
-                }
-            }
+            double Dm, M2;
+            D3 DP;
+            if (pxm && pxp && pym && pyp && pzm && pzp) gather<B0, true>(Dm, DP, M2, true, true, true);
+            else gather<B0, false>(Dm, DP, M2, pzm, pzp, false);
             Dm = 0.125 * Dm;
             DP = scl(0.125, DP);
             M2 = 0.125 * M2;
