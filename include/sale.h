@@ -181,6 +181,28 @@ int32_t sale_profile_enable(sale_ctx* c, int32_t on);
 /* total device milliseconds and number of timed launch groups of a class */
 int32_t sale_profile_read(sale_ctx* c, int32_t kclass, double* total_ms, int64_t* count);
 
+/* ---- halo plan (host-only, no GPU): what X1 exchanges between ranks --------
+ * Local arrays of a rank hold global planes [k0-g, k1+g) (cells) / [k0-g, k1+g]
+ * (nodes), plane-major (x fastest), g = 1 (LAGRANGE) or 3 (EULER); see
+ * sale_local_layout.  One message = one contiguous run of whole planes of one
+ * state field.  sale_step executes exactly this plan with ncclSend/ncclRecv in
+ * one group per cycle (full = 0), and once with full = 1 at the start of every
+ * sale_step call (adds MASS in LAGRANGE mode, where m is otherwise constant). */
+typedef struct sale_halo_msg {
+    int32_t peer;    /* rank sent to / received from                          */
+    int32_t send;    /* 1 = send, 0 = receive                                 */
+    int32_t field;   /* SALE_F_X..SALE_F_UZ, SALE_F_MASS or SALE_F_E           */
+    int32_t first_plane; /* global plane index of the first plane moved       */
+    int64_t offset;  /* element offset into this rank's local array of field  */
+    int64_t count;   /* elements (whole planes)                               */
+} sale_halo_msg;
+/* Writes up to cap messages; returns their number, or -1 if p is invalid. */
+int32_t sale_halo_plan(const sale_params* p, int32_t full, sale_halo_msg* out, int32_t cap);
+/* Local slab geometry of rank p->rank: owned cell planes [k0,k1), ghost depth,
+ * allocated local node / cell planes.  SALE_EINVAL if p is invalid. */
+int32_t sale_local_layout(const sale_params* p, int32_t* k0, int32_t* k1, int32_t* ghost,
+                          int32_t* node_planes, int32_t* cell_planes);
+
 /* human-readable detail of the last error: code, cycle, cell, CUDA/NCCL text */
 const char* sale_last_error(const sale_ctx* c);
 

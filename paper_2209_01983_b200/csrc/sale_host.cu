@@ -117,6 +117,15 @@ bool params_ok(const sale_params* p)
     return true;
 }
 
+// parameter checks for the host-only planning entry points (no NCCL id needed)
+bool params_ok_layout(const sale_params* p)
+{
+    if (!p) return false;
+    sale_params q = *p;
+    q.nccl_unique_id = q.nranks > 1 ? (const void*)p : nullptr;
+    return params_ok(&q);
+}
+
 // slab s of T: remainder planes go to the lowest slabs
 void slab_range(int nz, int T, int s, int& k0, int& k1)
 {
@@ -276,6 +285,79 @@ void state_arrays(const sale_ctx* c, const Slab& s, int b, bool include_mass,
     cells.push_back(s.e[b]);
 }
 
+// the state fields a halo exchange moves, in plan order
+void plan_fields(const sale_params* p, int full, std::vector<int>& node_f, std::vector<int>& cell_f)
+{
+    node_f.clear();
+    cell_f.clear();
+    bool euler = p->rezone == SALE_EULER;
+    if (!euler) {
+        node_f.push_back(SALE_F_X);
+        node_f.push_back(SALE_F_Y);
+        node_f.push_back(SALE_F_Z);
+    }
+    node_f.push_back(SALE_F_UX);
+    node_f.push_back(SALE_F_UY);
+    node_f.push_back(SALE_F_UZ);
+    if (euler || full) cell_f.push_back(SALE_F_MASS);
+    cell_f.push_back(SALE_F_E);
+}
+
+// X1 plan of rank p->rank (one slab per rank): for every field, to / from r-1
+// then r+1; node planes [k0+1, k0+g] / [k1-g, k1-1] go out, ghosts [k0-g, k0-1] /
+// [k1+1, k1+g] come in; cell planes [k0, k0+g) / [k1-g, k1) out, [k0-g, k0) /
+// [k1, k1+g) in.  Offsets are into the local arrays (local plane = k - (k0-g)).
+void build_plan(const sale_params* p, int full, std::vector<sale_halo_msg>& out)
+{
+    out.clear();
+    if (p->nranks <= 1) return;
+    std::vector<Slab> v;
+    layout_slabs(p, v);
+    const Slab& S = v[0];
+    const int g = S.g, r = p->rank, n = p->nranks;
+    std::vector<int> nf, cf;
+    plan_fields(p, full, nf, cf);
+    auto push = [&](int peer, int send, int field, int k_first, long long plane, int kb) {
+        sale_halo_msg m;
+        m.peer = peer;
+        m.send = send;
+        m.field = field;
+        m.first_plane = k_first;
+        m.offset = (int64_t)(k_first - kb) * plane;
+        m.count = (int64_t)g * plane;
+        out.push_back(m);
+    };
+    for (int f : nf) {
+        if (r > 0) {
+            push(r - 1, 1, f, S.k0 + 1, S.pn, S.kb);
+            push(r - 1, 0, f, S.k0 - g, S.pn, S.kb);
+        }
+        if (r < n - 1) {
+            push(r + 1, 1, f, S.k1 - g, S.pn, S.kb);
+            push(r + 1, 0, f, S.k1 + 1, S.pn, S.kb);
+        }
+    }
+    for (int f : cf) {
+        if (r > 0) {
+            push(r - 1, 1, f, S.k0, S.pc, S.kb);
+            push(r - 1, 0, f, S.k0 - g, S.pc, S.kb);
+        }
+        if (r < n - 1) {
+            push(r + 1, 1, f, S.k1 - g, S.pc, S.kb);
+            push(r + 1, 0, f, S.k1, S.pc, S.kb);
+        }
+    }
+}
+
+double* field_array(const sale_ctx* c, const Slab& s, int b, int field)
+{
+    bool euler = c->prm.rezone == SALE_EULER;
+    if (field <= SALE_F_Z) return s.x[b][field];
+    if (field <= SALE_F_UZ) return s.u[b][field - SALE_F_UX];
+    if (field == SALE_F_MASS) return euler ? s.m[b] : s.m[0];
+    return s.e[b];
+}
+
 // X1: ghost planes between neighbouring slabs, buffer b
 int exchange(sale_ctx* c, int b, bool include_mass)
 {
@@ -308,33 +390,18 @@ int exchange(sale_ctx* c, int b, bool include_mass)
     int rc = cuda_check(c, cudaGetLastError(), "halo copy");
     if (rc) return rc;
     if (c->prm.nranks == 1) return SALE_OK;
-    // ranks: one grouped NCCL exchange with r-1 and r+1 (one slab per rank)
+    // ranks: one grouped NCCL exchange with r-1 and r+1, exactly the messages of
+    // the host-side plan (sale_halo_plan, tested on CPU with gloo)
     const Slab& S = c->slabs[0];
-    int r = c->prm.rank, n = c->prm.nranks;
-    std::vector<double*> nd, cd;
-    state_arrays(c, S, b, include_mass, nd, cd);
+    std::vector<sale_halo_msg> plan;
+    build_plan(&c->prm, include_mass ? 1 : 0, plan);
     ncclGroupStart();
-    for (double* a : nd) {
-        size_t cnt = pn * g;
-        if (r > 0) {
-            ncclSend(a + (size_t)(S.k0 + 1 - S.kb) * pn, cnt, ncclFloat64, r - 1, c->comm, c->stream);
-            ncclRecv(a + (size_t)(S.k0 - g - S.kb) * pn, cnt, ncclFloat64, r - 1, c->comm, c->stream);
-        }
-        if (r < n - 1) {
-            ncclSend(a + (size_t)(S.k1 - g - S.kb) * pn, cnt, ncclFloat64, r + 1, c->comm, c->stream);
-            ncclRecv(a + (size_t)(S.k1 + 1 - S.kb) * pn, cnt, ncclFloat64, r + 1, c->comm, c->stream);
-        }
-    }
-    for (double* a : cd) {
-        size_t cnt = pc * g;
-        if (r > 0) {
-            ncclSend(a + (size_t)(S.k0 - S.kb) * pc, cnt, ncclFloat64, r - 1, c->comm, c->stream);
-            ncclRecv(a + (size_t)(S.k0 - g - S.kb) * pc, cnt, ncclFloat64, r - 1, c->comm, c->stream);
-        }
-        if (r < n - 1) {
-            ncclSend(a + (size_t)(S.k1 - g - S.kb) * pc, cnt, ncclFloat64, r + 1, c->comm, c->stream);
-            ncclRecv(a + (size_t)(S.k1 - S.kb) * pc, cnt, ncclFloat64, r + 1, c->comm, c->stream);
-        }
+    for (const sale_halo_msg& m : plan) {
+        double* a = field_array(c, S, b, m.field);
+        if (m.send)
+            ncclSend(a + m.offset, (size_t)m.count, ncclFloat64, m.peer, c->comm, c->stream);
+        else
+            ncclRecv(a + m.offset, (size_t)m.count, ncclFloat64, m.peer, c->comm, c->stream);
     }
     return nccl_check(c, ncclGroupEnd(), "halo exchange");
 }
@@ -698,6 +765,30 @@ int32_t sale_get_layout(sale_ctx* c, int32_t* k0, int32_t* k1)
 }
 
 int64_t sale_kernel_launches(const sale_ctx* c) { return c ? c->launches : 0; }
+
+int32_t sale_halo_plan(const sale_params* p, int32_t full, sale_halo_msg* out, int32_t cap)
+{
+    if (!params_ok_layout(p)) return -1;
+    std::vector<sale_halo_msg> plan;
+    build_plan(p, full, plan);
+    int32_t n = (int32_t)plan.size();
+    for (int32_t k = 0; k < n && k < cap && out; ++k) out[k] = plan[k];
+    return n;
+}
+
+int32_t sale_local_layout(const sale_params* p, int32_t* k0, int32_t* k1, int32_t* ghost, int32_t* node_planes,
+                          int32_t* cell_planes)
+{
+    if (!params_ok_layout(p)) return SALE_EINVAL;
+    std::vector<Slab> v;
+    layout_slabs(p, v);
+    if (k0) *k0 = v.front().k0;
+    if (k1) *k1 = v.back().k1;
+    if (ghost) *ghost = v[0].g;
+    if (node_planes) *node_planes = v[0].nzn;
+    if (cell_planes) *cell_planes = v[0].nzc;
+    return SALE_OK;
+}
 
 int32_t sale_profile_enable(sale_ctx* c, int32_t on)
 {

@@ -27,7 +27,8 @@ NODE_FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "NODE_MASS")
 EXPORTS = ("sale_workspace_bytes", "sale_nccl_unique_id", "sale_create", "sale_step",
            "sale_step_async", "sale_sync", "sale_get_field", "sale_set_field", "sale_get_clock",
            "sale_set_clock", "sale_get_layout", "sale_kernel_launches", "sale_profile_enable",
-           "sale_profile_read", "sale_last_error", "sale_destroy")
+           "sale_profile_read", "sale_halo_plan", "sale_local_layout", "sale_last_error",
+           "sale_destroy")
 K_CLASSES = ("begin", "prologue", "lagrange", "remap", "halo")
 
 
@@ -42,6 +43,11 @@ class SaleParams(C.Structure):
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
                 ("device", C.c_int32), ("impl", C.c_int32), ("local_slabs", C.c_int32),
                 ("reserved", C.c_int32)]
+
+
+class SaleHaloMsg(C.Structure):
+    _fields_ = [("peer", C.c_int32), ("send", C.c_int32), ("field", C.c_int32),
+                ("first_plane", C.c_int32), ("offset", C.c_int64), ("count", C.c_int64)]
 
 
 class SaleError(RuntimeError):
@@ -92,6 +98,10 @@ def lib() -> C.CDLL:
             L.sale_profile_enable.restype = i32
             L.sale_profile_read.argtypes = [vp, i32, P(d), P(i64)]
             L.sale_profile_read.restype = i32
+            L.sale_halo_plan.argtypes = [P(SaleParams), i32, P(SaleHaloMsg), i32]
+            L.sale_halo_plan.restype = i32
+            L.sale_local_layout.argtypes = [P(SaleParams), P(i32), P(i32), P(i32), P(i32), P(i32)]
+            L.sale_local_layout.restype = i32
             L.sale_last_error.argtypes = [vp]
             L.sale_last_error.restype = C.c_char_p
             L.sale_destroy.argtypes = [vp]
@@ -118,6 +128,31 @@ def make_params(cfg: dict, *, rank=0, nranks=1, device=0, impl="v0", local_slabs
     p.impl = IMPL[impl] if isinstance(impl, str) else int(impl)
     p.local_slabs = local_slabs
     return p
+
+
+FIELD_NAMES = {v: k for k, v in FIELDS.items()}
+
+
+def halo_plan(cfg: dict, rank: int, nranks: int, full: bool = False) -> list[dict]:
+    """The X1 message plan of one rank (host-only; what sale_step sends via NCCL)."""
+    p = make_params(cfg, rank=rank, nranks=nranks)
+    n = lib().sale_halo_plan(C.byref(p), 1 if full else 0, None, 0)
+    if n < 0:
+        raise SaleError(EINVAL, "sale_halo_plan")
+    buf = (SaleHaloMsg * max(n, 1))()
+    lib().sale_halo_plan(C.byref(p), 1 if full else 0, buf, n)
+    return [{"peer": m.peer, "send": bool(m.send), "field": FIELD_NAMES[m.field],
+             "first_plane": m.first_plane, "offset": m.offset, "count": m.count} for m in buf[:n]]
+
+
+def local_layout(cfg: dict, rank: int, nranks: int) -> dict:
+    p = make_params(cfg, rank=rank, nranks=nranks)
+    k0, k1, g, nn, nc = (C.c_int32() for _ in range(5))
+    rc = lib().sale_local_layout(C.byref(p), C.byref(k0), C.byref(k1), C.byref(g), C.byref(nn), C.byref(nc))
+    if rc:
+        raise SaleError(rc, "sale_local_layout")
+    return {"k0": k0.value, "k1": k1.value, "ghost": g.value, "node_planes": nn.value,
+            "cell_planes": nc.value}
 
 
 def workspace_bytes(cfg: dict, **kw) -> int:
