@@ -55,9 +55,18 @@ __global__ void k_sedov_cells(Slab s, Phys p)
     D3 N[8];
 #pragma unroll
     for (int h = 0; h < 8; ++h) N[h] = tpos(s, i + (h & 1), j + ((h >> 1) & 1), k + (h >> 2));
-    double m = p.rho0 * hex_volume(N);
+    D3 A[6], Xb[6];
+    double sv[6];
+    hex_faces(N, A, Xb, sv);
+    const double V = vol_from_s(sv);
+    double m = p.rho0 * V;
     s.m[0][c] = m;
-    if (p.rezone) s.VT[c] = hex_volume(N) ;  // V^T (c.2 on x^T), constant in Euler mode
+    if (p.rezone) {  // constants of the fixed Euler mesh: V^T and s of the -x/-y/-z target faces
+        s.VT[c] = V;
+        s.sT[0][c] = sv[0];
+        s.sT[1][c] = sv[2];
+        s.sT[2][c] = sv[4];
+    }
     s.e[0][c] = (i == 0 && j == 0 && k == 0) ? p.e_dep / m : p.e_bg;
 }
 

@@ -48,7 +48,8 @@ struct RemapCellsCTA {
     __host__ __device__ static constexpr int oN(int par, int c) { return (par * 6 + c) * PL; }  // x'(3), u'(3)
     __host__ __device__ static constexpr int oC(int c) { return 12 * PL + c * PL; }            // donor r, e', Ubar(3)
     __host__ __device__ static constexpr int oF(int par, int xy, int c) { return 17 * PL + ((par * 2 + xy) * 5 + c) * PL; }
-    static constexpr int WORDS = 37 * PL + 2 * RPAD;
+    __host__ __device__ static constexpr int oR(int c) { return 37 * PL + c * PL; }  // ribbons Rxz Ryz Rzy Rzx
+    static constexpr int WORDS = 41 * PL + 2 * RPAD;
 
     const Slab& s;
     const Phys& p;
@@ -59,10 +60,16 @@ struct RemapCellsCTA {
     bool col_in, cell_col, xface_on, yface_on, zface_on, upd_on;
     D3 qx1, qu1;            // prefetch: node x', u'
     double qm, qe, qv;      // prefetch: cell m, e', V'
+    double qs0, qs1, qs2;   // prefetch: s^T of the cell's -x/-y/-z target faces
+    double qz;              // prefetch: Z of node plane k
+    double tx0, tx1, ty0, ty1;  // this column's X_i, X_{i+1}, Y_j, Y_{j+1}
+    double tz0, tz1;        // Z of node planes kz, kz+1
     // own column, previous cell plane (kz-1): donor data and pre-remap state
     double r_prev, e_prev, m_prev;
     D3 ub_prev;
     Flux fz_prev;           // z-face flux at node plane kz-1... carried one step
+    double rxy_prev, ryx_prev;  // ribbons Rxy, Ryx of node plane kz (computed at step kz-1)
+    bool rib_on;
 
     __device__ __forceinline__ RemapCellsCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kr0_, int kr1_,
                                              int zchunk)
@@ -87,6 +94,18 @@ struct RemapCellsCTA {
         yface_on = in_x && iy >= 1 && iy <= TY + 1 && j >= 1 && j <= p.ny - 1 && i >= 0 && i < p.nx;
         zface_on = in_x && in_y && cell_col;
         upd_on = in_x && in_y && cell_col;
+        rib_on = col_in && ix >= 1 && iy >= 1 && iy <= TY + 1;
+        tx0 = col_in ? s.Xt[i] : 0.0;
+        tx1 = (col_in && i + 1 <= p.nx) ? s.Xt[i + 1] : 0.0;
+        ty0 = col_in ? s.Yt[j] : 0.0;
+        ty1 = (col_in && j + 1 <= p.ny) ? s.Yt[j + 1] : 0.0;
+        tz0 = tz1 = 0.0;
+    }
+
+    // s of a ribbon / face from its 4 points in canonical order (c.2)
+    __device__ __forceinline__ static double fs(D3 Q0, D3 Q1, D3 Q2, D3 Q3)
+    {
+        return face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
     }
 
     __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
@@ -101,12 +120,17 @@ struct RemapCellsCTA {
         qm = 0.0;
         qe = 0.0;
         qv = 1.0;
+        qs0 = qs1 = qs2 = 0.0;
+        qz = (k - s.kb >= 0 && k - s.kb < s.nzn) ? s.Zt[k - s.kb] : 0.0;
         const int kc = k - 1;
         if (cell_col && kc >= 0 && kc < p.nz) {
             long long c = cb + (long long)kc * s.pc;
             qm = s.m[cur][c];
             qe = s.e1[c];
             qv = s.V1[c];
+            qs0 = s.sT[0][c];
+            qs1 = s.sT[1][c];
+            qs2 = s.sT[2][c];
         }
     }
     template <int PAR>
@@ -119,9 +143,10 @@ struct RemapCellsCTA {
     __device__ __forceinline__ D3 XL(int off) const { return ld3r(me + off, oN(PAR, 0), PL); }
     template <int PAR>
     __device__ __forceinline__ D3 UL(int off) const { return ld3r(me + off, oN(PAR, 3), PL); }
-    __device__ __forceinline__ D3 XT(int di, int dj, int k) const
+    // target node position from the per-thread table registers (dk = 0: plane kz, 1: kz+1)
+    __device__ __forceinline__ D3 XT(int di, int dj, int dk) const
     {
-        return D3{s.Xt[i + di], s.Yt[j + dj], s.Zt[k - s.kb]};
+        return D3{di ? tx1 : tx0, dj ? ty1 : ty0, dk ? tz1 : tz0};
     }
 
     // donor-cell flux through a face with swept volume dV, donors lower (L) / upper (U)
@@ -141,7 +166,9 @@ struct RemapCellsCTA {
         constexpr int B1 = B0 ^ 1;
         // ---- P1: stage node plane kz+1, cell (i,j,kz); prefetch next
         put<B1>();
-        const double m = qm, e1 = qe, V1 = qv;
+        const double m = qm, e1 = qe, V1 = qv, sT0 = qs0, sT1 = qs1, sT2 = qs2;
+        tz0 = tz1;
+        tz1 = qz;
         if (kz < zb + 1) fetch(kz + 2);
         __syncthreads();
         // ---- P2: donor data of cell (i,j,kz); swept volumes of the anchored faces
@@ -164,31 +191,63 @@ struct RemapCellsCTA {
         me[oC(0)] = r;
         me[oC(1)] = e1;
         st3r(me, oC(2), PL, ub);
-        double dVx = 0.0, dVy = 0.0, dVz = 0.0;
+        // c.4 step 1 with shared ribbons.  The swept hex of a face has the target
+        // face as bottom (Z0, constant: s^T precomputed), the moved face as top
+        // (Z1), and four lateral ribbons between a target edge and its moved
+        // edge.  Same-family neighbouring faces see the same ribbon with the same
+        // canonical node sequence, so it is computed once (bit-identical):
+        //   x-face (i,j,k): X0 Rxz(i,j)  X1 Rxz(i,j+1)  Y0 Rxy(k)  Y1 Rxy(k+1)
+        //   y-face (i,j,k): X0 Ryx(k)    X1 Ryx(k+1)    Y0 Ryz(i,j) Y1 Ryz(i+1,j)
+        //   z-face (i,j,k): X0 Rzy(i,j)  X1 Rzy(i+1,j)  Y0 Rzx(i,j) Y1 Rzx(i,j+1)
+        double rxy_next = 0.0, ryx_next = 0.0;
+        {
+            double rxz = 0.0, ryz = 0.0, rzy = 0.0, rzx = 0.0;
+            if (rib_on && kz + 1 >= 0 && kz + 1 <= p.nz) {  // edges in node plane kz+1
+                const D3 T1 = XT(0, 0, 1), L1 = XL<B1>(0);
+                if (j + 1 <= p.ny) rxy_next = fs(T1, L1, XL<B1>(RW), XT(0, 1, 1));  // Rxy(i,j,kz+1)
+                if (i + 1 <= p.nx) ryx_next = fs(T1, XT(1, 0, 1), XL<B1>(1), L1);  // Ryx(i,j,kz+1)
+            }
+            if (rib_on && kz >= 0 && kz < p.nz) {  // z-edge kz -> kz+1 and edges in plane kz
+                const D3 T0 = XT(0, 0, 0), T1 = XT(0, 0, 1), L0 = XL<B0>(0), L1 = XL<B1>(0);
+                rxz = fs(T0, T1, L1, L0);
+                ryz = fs(T0, L0, L1, T1);
+                if (j + 1 <= p.ny) rzy = fs(T0, XT(0, 1, 0), XL<B0>(RW), L0);  // Rzy(i,j,kz)
+                if (i + 1 <= p.nx) rzx = fs(T0, L0, XL<B0>(1), XT(1, 0, 0));  // Rzx(i,j,kz)
+            }
+            me[oR(0)] = rxz;
+            me[oR(1)] = ryz;
+            me[oR(2)] = rzy;
+            me[oR(3)] = rzx;
+        }
         const bool do_x = xface_on && kz >= 0 && kz < p.nz && kz >= za && kz <= zb;
         const bool do_y = yface_on && kz >= 0 && kz < p.nz && kz >= za && kz <= zb;
         const bool do_z = zface_on && kz >= 1 && kz <= p.nz - 1 && kz >= za;
-        if (do_x)  // x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
-            dVx = swept_volume(XT(0, 0, kz), XT(0, 1, kz), XT(0, 1, kz + 1), XT(0, 0, kz + 1), XL<B0>(0),
-                               XL<B0>(RW), XL<B1>(RW), XL<B1>(0));
-        if (do_y)  // y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
-            dVy = swept_volume(XT(0, 0, kz), XT(0, 0, kz + 1), XT(1, 0, kz + 1), XT(1, 0, kz), XL<B0>(0),
-                               XL<B1>(0), XL<B1>(1), XL<B0>(1));
-        if (do_z)  // z-face at node plane kz: (i,j,kz) (i+1,j,kz) (i+1,j+1,kz) (i,j+1,kz)
-            dVz = swept_volume(XT(0, 0, kz), XT(1, 0, kz), XT(1, 1, kz), XT(0, 1, kz), XL<B0>(0), XL<B0>(1),
-                               XL<B0>(RW + 1), XL<B0>(RW));
         __syncthreads();
-        // ---- P3: fluxes (boundary faces: +0.0)
+        // ---- P3: swept volumes and donor-cell fluxes (boundary faces: +0.0)
         Flux fx = Flux{0.0, 0.0, D3{0.0, 0.0, 0.0}}, fy = fx, fz = fx;
         if (do_x) {
+            // moved x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
+            const double sL = fs(XL<B0>(0), XL<B0>(RW), XL<B1>(RW), XL<B1>(0));
+            const double sT = sT0;
+            const double dV = (((((me[RW + oR(0)] - me[oR(0)]) + rxy_next) - rxy_prev) + sL) - sT) / 3.0;
             const double* L = me - 1;
-            fx = flux(dVx, L[oC(0)], L[oC(1)], ld3r(L, oC(2), PL), r, e1, ub);
+            fx = flux(dV, L[oC(0)], L[oC(1)], ld3r(L, oC(2), PL), r, e1, ub);
         }
         if (do_y) {
+            // moved y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
+            const double sL = fs(XL<B0>(0), XL<B1>(0), XL<B1>(1), XL<B0>(1));
+            const double sT = sT1;
+            const double dV = (((((ryx_next - ryx_prev) + me[1 + oR(1)]) - me[oR(1)]) + sL) - sT) / 3.0;
             const double* L = me - RW;
-            fy = flux(dVy, L[oC(0)], L[oC(1)], ld3r(L, oC(2), PL), r, e1, ub);
+            fy = flux(dV, L[oC(0)], L[oC(1)], ld3r(L, oC(2), PL), r, e1, ub);
         }
-        if (do_z) fz = flux(dVz, r_prev, e_prev, ub_prev, r, e1, ub);
+        if (do_z) {
+            // moved z-face at node plane kz: (i,j,kz) (i+1,j,kz) (i+1,j+1,kz) (i,j+1,kz)
+            const double sL = fs(XL<B0>(0), XL<B0>(1), XL<B0>(RW + 1), XL<B0>(RW));
+            const double sT = sT2;
+            const double dV = (((((me[1 + oR(2)] - me[oR(2)]) + me[RW + oR(3)]) - me[oR(3)]) + sL) - sT) / 3.0;
+            fz = flux(dV, r_prev, e_prev, ub_prev, r, e1, ub);
+        }
         me[oF(B0, 0, 0)] = fx.mu;
         me[oF(B0, 0, 1)] = fx.eps;
         st3r(me, oF(B0, 0, 2), PL, fx.pi);
@@ -225,6 +284,8 @@ struct RemapCellsCTA {
         m_prev = m;
         ub_prev = ub;
         fz_prev = fz;
+        rxy_prev = rxy_next;
+        ryx_prev = ryx_next;
     }
 
     __device__ __forceinline__ void run()
@@ -233,6 +294,7 @@ struct RemapCellsCTA {
         fetch(za - 1);
         if ((za - 1) & 1) put<1>();
         else put<0>();
+        tz1 = qz;  // Z of node plane za-1 (becomes tz0 at the first step)
         fetch(za);
         __syncthreads();
         fz_prev = Flux{0.0, 0.0, D3{0.0, 0.0, 0.0}};
@@ -240,6 +302,8 @@ struct RemapCellsCTA {
         e_prev = 0.0;
         m_prev = 0.0;
         ub_prev = D3{0.0, 0.0, 0.0};
+        rxy_prev = 0.0;
+        ryx_prev = 0.0;
         // step kz computes donor data / fluxes of plane kz and updates plane kz-1
         for (int kz = za - 1; kz <= zb + 1; ++kz) {
             if (kz & 1) step<1>(kz);

@@ -168,6 +168,7 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
     s.dm = euler ? take(nc) : nullptr;
     s.der = take(s.pn * (long long)(s.k1 - s.k0 + 1));
     s.VT = euler ? take(nc) : nullptr;
+    for (int a = 0; a < 3; ++a) s.sT[a] = euler ? take(nc) : nullptr;
     s.Xt = take(p->nx + 1);
     s.Yt = take(p->ny + 1);
     s.Zt = take(s.nzn);

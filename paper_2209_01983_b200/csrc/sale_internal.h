@@ -52,6 +52,7 @@ struct Slab {
     double* dP[3];            // Euler scratch: Delta P
     double* der;              // derive / staging scratch (node-plane sized)
     double* VT;               // Euler: target cell volume V^T (constant; set at create)
+    double* sT[3];            // Euler: s of the target x/y/z face anchored at each cell (-a faces)
     double* Xt;               // target node coordinates X_i, i in [0,nx]
     double* Yt;               // Y_j, j in [0,ny]
     double* Zt;               // Z_k for local node planes (index = k - kb)
