@@ -15,6 +15,8 @@
 // kernels_fused.cu: compile-time plane parity, per-thread base + immediate.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "sale_mesh.cuh"
 
 namespace sale {
@@ -322,6 +324,341 @@ __global__ void __launch_bounds__(RW * NW, 2) kr_cells(Slab s, Phys p, int cur, 
 }
 
 // ============================================================================
+// kr_cells_p: the same computation as kr_cells, software-pipelined along z so
+// that one __syncthreads per z-step suffices.  Step t runs, back to back,
+//   B(t)   swept volumes + fluxes of plane t      (reads A(t) outputs),
+//   C(t-1) cell update of plane t-1               (reads B(t-1) fluxes),
+//   A(t+1) donor data, ribbons, moved-face s' of plane t+1 (reads node planes t+1, t+2),
+//   put node plane t+3, prefetch node plane t+4 / cell plane t+2,
+// with every cross-thread hand-off double-buffered (node planes: ring of 3).
+// ============================================================================
+template <int NW>
+struct RemapCellsP {
+    static constexpr int PL = NW * RW, TX = RW - 3, TY = NW - 3;
+    __host__ __device__ static constexpr int oN(int slot, int c) { return (slot * 6 + c) * PL; }     // x'(3) u'(3)
+    __host__ __device__ static constexpr int oC(int par, int c) { return 18 * PL + (par * 5 + c) * PL; }  // r e' Ubar
+    __host__ __device__ static constexpr int oR(int par, int c) { return 28 * PL + (par * 4 + c) * PL; }  // Rxz Ryz Rzy Rzx
+    __host__ __device__ static constexpr int oF(int par, int xy, int c) { return 36 * PL + ((par * 2 + xy) * 5 + c) * PL; }
+    static constexpr int WORDS = 56 * PL + 2 * RPAD;
+
+    struct Cell {
+        double r, e1;
+        D3 ub;
+    };
+
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, ix, iy, za, zb;
+    long long nb, cb;
+    bool col_in, cell_col, xface_on, yface_on, zface_on, upd_on, rib_on;
+    double tx0, tx1, ty0, ty1;
+    // prefetch registers: node plane, cell plane
+    D3 qx1, qu1;
+    double qm, qe, qv, qs0, qs1, qs2;
+    // carried state
+    Cell c_tm1, c_t;            // own donor data of planes t-1, t
+    double rxy_t, rxy_t1, ryx_t, ryx_t1;  // Rxy/Ryx of node planes t, t+1
+    double sLx, sLy, sLz;       // moved-face s of plane t (from A(t))
+    double sTx, sTy, sTz;       // target-face s of plane t
+    double m_t, e_t, m_tm1, e_tm1;  // pre-remap m, e' of cells t, t-1
+    double sTx_n, sTy_n, sTz_n, m_n, e_n;  // the same for plane t+1 (from A(t+1))
+    Flux fz_tm1;                // z-face flux at node plane t-1
+
+    __device__ __forceinline__ RemapCellsP(const Slab& s_, const Phys& p_, int cur_, double* smem, int kr0, int kr1,
+                                           int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        ix = threadIdx.x;
+        iy = threadIdx.y;
+        me = smem + RPAD + iy * RW + ix;
+        i = blockIdx.x * TX - 1 + ix;
+        j = blockIdx.y * TY - 1 + iy;
+        za = kr0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kr1 - 1 ? za + zchunk - 1 : kr1 - 1;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
+        cell_col = i >= 0 && i < p.nx && j >= 0 && j < p.ny;
+        const bool in_x = ix >= 1 && ix <= TX, in_y = iy >= 1 && iy <= TY;
+        xface_on = ix >= 1 && ix <= TX + 1 && in_y && i >= 1 && i <= p.nx - 1 && j >= 0 && j < p.ny;
+        yface_on = in_x && iy >= 1 && iy <= TY + 1 && j >= 1 && j <= p.ny - 1 && i >= 0 && i < p.nx;
+        zface_on = in_x && in_y && cell_col;
+        upd_on = in_x && in_y && cell_col;
+        rib_on = col_in && ix >= 1 && iy >= 1 && iy <= TY + 1;
+        tx0 = col_in ? s.Xt[i] : 0.0;
+        tx1 = (col_in && i + 1 <= p.nx) ? s.Xt[i + 1] : 0.0;
+        ty0 = col_in ? s.Yt[j] : 0.0;
+        ty1 = (col_in && j + 1 <= p.ny) ? s.Yt[j + 1] : 0.0;
+    }
+
+    __device__ __forceinline__ static double fs(D3 Q0, D3 Q1, D3 Q2, D3 Q3)
+    {
+        return face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
+    }
+    __device__ __forceinline__ static Flux flux(double dV, const Cell& L, const Cell& U)
+    {
+        const bool low = dV > 0.0;
+        Flux f;
+        f.mu = (low ? L.r : U.r) * dV;
+        f.eps = f.mu * (low ? L.e1 : U.e1);
+        f.pi = scl(f.mu, low ? L.ub : U.ub);
+        return f;
+    }
+    __device__ __forceinline__ double zt(int k) const
+    {
+        return (k - s.kb >= 0 && k - s.kb < s.nzn) ? s.Zt[k - s.kb] : 0.0;
+    }
+    __device__ __forceinline__ void fetch_node(int k)
+    {
+        qx1 = D3{0.0, 0.0, 0.0};
+        qu1 = qx1;
+        if (col_in && k >= 0 && k <= p.nz) {
+            long long n = nb + (long long)k * s.pn;
+            qx1 = ld3(s.x1, n);
+            qu1 = ld3(s.u1, n);
+        }
+    }
+    __device__ __forceinline__ void fetch_cell(int k)
+    {
+        qm = 0.0;
+        qe = 0.0;
+        qv = 1.0;
+        qs0 = qs1 = qs2 = 0.0;
+        if (cell_col && k >= 0 && k < p.nz) {
+            long long c = cb + (long long)k * s.pc;
+            qm = s.m[cur][c];
+            qe = s.e1[c];
+            qv = s.V1[c];
+            qs0 = s.sT[0][c];
+            qs1 = s.sT[1][c];
+            qs2 = s.sT[2][c];
+        }
+    }
+    __device__ __forceinline__ void put(int k)
+    {
+        const int slot = ((k % 3) + 3) % 3;
+        double* b = me + oN(slot, 0);
+        b[0] = qx1.x;
+        b[PL] = qx1.y;
+        b[2 * PL] = qx1.z;
+        b[3 * PL] = qu1.x;
+        b[4 * PL] = qu1.y;
+        b[5 * PL] = qu1.z;
+    }
+
+    // A(tau): donor data, ribbons, moved-face s of plane tau (node planes tau, tau+1)
+    template <int PAR>
+    __device__ __forceinline__ void stageA(int tau, int slot0, int slot1, Cell& cell, double& rxy_n, double& ryx_n,
+                                           double& sx, double& sy, double& sz)
+    {
+        const double* N0 = me + oN(slot0, 0);
+        const double* N1 = me + oN(slot1, 0);
+        auto XL0 = [&](int off) { return ld3r(N0 + off, 0, PL); };
+        auto XL1 = [&](int off) { return ld3r(N1 + off, 0, PL); };
+        auto UL0 = [&](int off) { return ld3r(N0 + off, 3 * PL, PL); };
+        auto UL1 = [&](int off) { return ld3r(N1 + off, 3 * PL, PL); };
+        // donor data of cell (i,j,tau)
+        cell = Cell{0.0, qe, D3{0.0, 0.0, 0.0}};
+        if (cell_col && tau >= 0 && tau < p.nz) {
+            D3 sum = UL0(0);
+            sum = add(sum, UL0(1));
+            sum = add(sum, UL0(RW));
+            sum = add(sum, UL0(RW + 1));
+            sum = add(sum, UL1(0));
+            sum = add(sum, UL1(1));
+            sum = add(sum, UL1(RW));
+            sum = add(sum, UL1(RW + 1));
+            cell.ub = scl(0.125, sum);
+            cell.r = qm / qv;
+        }
+        me[oC(PAR, 0)] = cell.r;
+        me[oC(PAR, 1)] = cell.e1;
+        st3r(me, oC(PAR, 2), PL, cell.ub);
+        // ribbons (see kr_cells for the sharing rule) and moved faces
+        const double z0 = zt(tau), z1 = zt(tau + 1);
+        const D3 T0 = D3{tx0, ty0, z0}, T1 = D3{tx0, ty0, z1};
+        double rxz = 0.0, ryz = 0.0, rzy = 0.0, rzx = 0.0;
+        rxy_n = 0.0;
+        ryx_n = 0.0;
+        sx = sy = sz = 0.0;
+        if (rib_on && tau + 1 >= 0 && tau + 1 <= p.nz) {
+            const D3 L1 = XL1(0);
+            if (j + 1 <= p.ny) rxy_n = fs(T1, L1, XL1(RW), D3{tx0, ty1, z1});   // Rxy(i,j,tau+1)
+            if (i + 1 <= p.nx) ryx_n = fs(T1, D3{tx1, ty0, z1}, XL1(1), L1);    // Ryx(i,j,tau+1)
+        }
+        if (rib_on && tau >= 0 && tau < p.nz) {
+            const D3 L0 = XL0(0), L1 = XL1(0);
+            rxz = fs(T0, T1, L1, L0);
+            ryz = fs(T0, L0, L1, T1);
+            if (j + 1 <= p.ny) {
+                rzy = fs(T0, D3{tx0, ty1, z0}, XL0(RW), L0);  // Rzy(i,j,tau)
+                sx = fs(L0, XL0(RW), XL1(RW), L1);             // moved x-face
+            }
+            if (i + 1 <= p.nx) {
+                rzx = fs(T0, L0, XL0(1), D3{tx1, ty0, z0});   // Rzx(i,j,tau)
+                sy = fs(L0, L1, XL1(1), XL0(1));               // moved y-face
+            }
+            if (i + 1 <= p.nx && j + 1 <= p.ny) sz = fs(L0, XL0(1), XL0(RW + 1), XL0(RW));  // moved z-face
+        }
+        me[oR(PAR, 0)] = rxz;
+        me[oR(PAR, 1)] = ryz;
+        me[oR(PAR, 2)] = rzy;
+        me[oR(PAR, 3)] = rzx;
+    }
+
+    // B(t): swept volumes and fluxes of plane t (reads A(t) data of parity PAR)
+    template <int PAR>
+    __device__ __forceinline__ void stageB(int t, Flux& fzt)
+    {
+        Flux fx = Flux{0.0, 0.0, D3{0.0, 0.0, 0.0}}, fy = fx;
+        fzt = fx;
+        const bool do_x = xface_on && t >= 0 && t < p.nz && t >= za && t <= zb;
+        const bool do_y = yface_on && t >= 0 && t < p.nz && t >= za && t <= zb;
+        const bool do_z = zface_on && t >= 1 && t <= p.nz - 1 && t >= za;
+        if (do_x) {
+            const double dV = (((((me[RW + oR(PAR, 0)] - me[oR(PAR, 0)]) + rxy_t1) - rxy_t) + sLx) - sTx) / 3.0;
+            const double* L = me - 1;
+            fx = flux(dV, Cell{L[oC(PAR, 0)], L[oC(PAR, 1)], ld3r(L, oC(PAR, 2), PL)}, c_t);
+        }
+        if (do_y) {
+            const double dV = (((((ryx_t1 - ryx_t) + me[1 + oR(PAR, 1)]) - me[oR(PAR, 1)]) + sLy) - sTy) / 3.0;
+            const double* L = me - RW;
+            fy = flux(dV, Cell{L[oC(PAR, 0)], L[oC(PAR, 1)], ld3r(L, oC(PAR, 2), PL)}, c_t);
+        }
+        if (do_z) {
+            const double dV =
+                (((((me[1 + oR(PAR, 2)] - me[oR(PAR, 2)]) + me[RW + oR(PAR, 3)]) - me[oR(PAR, 3)]) + sLz) - sTz) / 3.0;
+            fzt = flux(dV, c_tm1, c_t);
+        }
+        me[oF(PAR, 0, 0)] = fx.mu;
+        me[oF(PAR, 0, 1)] = fx.eps;
+        st3r(me, oF(PAR, 0, 2), PL, fx.pi);
+        me[oF(PAR, 1, 0)] = fy.mu;
+        me[oF(PAR, 1, 1)] = fy.eps;
+        st3r(me, oF(PAR, 1, 2), PL, fy.pi);
+    }
+
+    // C(kc): cell update of plane kc = t-1 (reads B(t-1) fluxes of parity PAR)
+    template <int PAR>
+    __device__ __forceinline__ void stageC(int kc, const Flux& fz_lo, const Flux& fz_hi)
+    {
+        if (!(upd_on && kc >= za && kc <= zb && kc >= 0 && kc < p.nz)) return;
+        const double* own = me;
+        const double* xp = me + 1;
+        const double* yp = me + RW;
+        const double mu[6] = {own[oF(PAR, 0, 0)], xp[oF(PAR, 0, 0)], own[oF(PAR, 1, 0)], yp[oF(PAR, 1, 0)], fz_lo.mu,
+                              fz_hi.mu};
+        const double ep[6] = {own[oF(PAR, 0, 1)], xp[oF(PAR, 0, 1)], own[oF(PAR, 1, 1)], yp[oF(PAR, 1, 1)], fz_lo.eps,
+                              fz_hi.eps};
+        const D3 pi[6] = {ld3r(own, oF(PAR, 0, 2), PL), ld3r(xp, oF(PAR, 0, 2), PL), ld3r(own, oF(PAR, 1, 2), PL),
+                          ld3r(yp, oF(PAR, 1, 2), PL), fz_lo.pi, fz_hi.pi};
+        const double dm = ((((mu[0] - mu[1]) + mu[2]) - mu[3]) + mu[4]) - mu[5];
+        const double dE = ((((ep[0] - ep[1]) + ep[2]) - ep[3]) + ep[4]) - ep[5];
+        const D3 dP = sub(add(sub(add(sub(pi[0], pi[1]), pi[2]), pi[3]), pi[4]), pi[5]);
+        const double m2 = m_tm1 + dm;
+        if (kc >= s.k0 && kc < s.k1 && !(m2 > 0.0))
+            atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, kc));
+        const long long c = cb + (long long)kc * s.pc;
+        s.e[cur ^ 1][c] = e_tm1 + ((dE - (e_tm1 * dm)) / m2);
+        s.m[cur ^ 1][c] = m2;
+        s.dm[c] = dm;
+        st3(s.dP, c, dP);
+    }
+
+    template <int PT>  // PT = t & 1
+    __device__ __forceinline__ void step(int t)
+    {
+        constexpr int PN = PT ^ 1;
+        Flux fz_t;
+        stageB<PT>(t, fz_t);
+        stageC<PN>(t - 1, fz_tm1, fz_t);
+        // A(t+1): consume the cell prefetch of plane t+1
+        Cell cn;
+        double rxy_n, ryx_n, sx, sy, sz;
+        const int s1 = (((t + 1) % 3) + 3) % 3, s2 = (((t + 2) % 3) + 3) % 3;
+        stageA<PN>(t + 1, s1, s2, cn, rxy_n, ryx_n, sx, sy, sz);
+        const double nsT0 = qs0, nsT1 = qs1, nsT2 = qs2, nm = qm, ne = qe;
+        put(t + 3);
+        fetch_node(t + 4);
+        fetch_cell(t + 2);
+        // rotate carried state: plane t -> t-1, t+1 -> t
+        fz_tm1 = fz_t;
+        m_tm1 = m_t;
+        e_tm1 = e_t;
+        m_t = nm;
+        e_t = ne;
+        c_tm1 = c_t;
+        c_t = cn;
+        rxy_t = rxy_t1;
+        ryx_t = ryx_t1;
+        rxy_t1 = rxy_n;
+        ryx_t1 = ryx_n;
+        sLx = sx;
+        sLy = sy;
+        sLz = sz;
+        sTx = nsT0;
+        sTy = nsT1;
+        sTz = nsT2;
+        __syncthreads();
+    }
+
+    __device__ __forceinline__ void run()
+    {
+        // prologue: node planes za-1, za staged; cell za-1 and node plane za+1 prefetched
+        fetch_node(za - 1);
+        put(za - 1);
+        fetch_node(za);
+        put(za);
+        fetch_cell(za - 1);
+        fetch_node(za + 1);
+        __syncthreads();
+        // A(za-1) (step za-2 would also run B(za-2), C(za-3): nothing to do there)
+        {
+            Cell cn;
+            double rxy_n, ryx_n, sx, sy, sz;
+            const int s0 = (((za - 1) % 3) + 3) % 3, s1 = ((za % 3) + 3) % 3;
+            if ((za - 1) & 1) stageA<1>(za - 1, s0, s1, cn, rxy_n, ryx_n, sx, sy, sz);
+            else stageA<0>(za - 1, s0, s1, cn, rxy_n, ryx_n, sx, sy, sz);
+            c_t = cn;
+            c_tm1 = Cell{0.0, 0.0, D3{0.0, 0.0, 0.0}};
+            m_t = qm;
+            e_t = qe;
+            m_tm1 = e_tm1 = 0.0;
+            sTx = qs0;
+            sTy = qs1;
+            sTz = qs2;
+            rxy_t = ryx_t = 0.0;
+            rxy_t1 = rxy_n;
+            ryx_t1 = ryx_n;
+            sLx = sx;
+            sLy = sy;
+            sLz = sz;
+            fz_tm1 = Flux{0.0, 0.0, D3{0.0, 0.0, 0.0}};
+            put(za + 1);
+            fetch_node(za + 2);
+            fetch_cell(za);
+            __syncthreads();
+        }
+        // steps t = za-1 .. zb+1 (carried state now describes plane t = za-1)
+        for (int t = za - 1; t <= zb + 1; ++t) {
+            if (t & 1) step<1>(t);
+            else step<0>(t);
+        }
+    }
+};
+
+template <int NW, int MB>
+__global__ void __launch_bounds__(RW * NW, MB) kr_cells_p(Slab s, Phys p, int cur, int kr0, int kr1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    RemapCellsP<NW> c(s, p, cur, smem, kr0, kr1, zchunk);
+    c.run();
+}
+
+// ============================================================================
 // kr_nodes: node planes [k0, k1] + dt candidate of cells [k0, k1).  Columns i = i0-1+ix.
 // ============================================================================
 template <int NW>
@@ -530,6 +867,82 @@ __global__ void __launch_bounds__(RW * NW, 2) kr_nodes(Slab s, Phys p, int cur, 
 }
 
 // ============================================================================
+// kn_update / kn_dt: R4 and the Euler dt candidate as two barrier-free kernels
+// (one thread per node / per cell, operands through L1; high occupancy).
+// ============================================================================
+__global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
+{
+    if (!s.st->active) return;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= s.pn * (s.k1 - s.k0 + 1)) return;
+    const int k = s.k0 + (int)(t / s.pn);
+    const long long r = t % s.pn;
+    const int j = (int)(r / (p.nx + 1)), i = (int)(r % (p.nx + 1));
+    const bool pxm = i >= 1, pxp = i < p.nx, pym = j >= 1, pyp = j < p.ny, pzm = k >= 1, pzp = k < p.nz;
+    const long long c00 = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
+    const double* __restrict__ dm = s.dm;
+    const double* __restrict__ m2 = s.m[cur ^ 1];
+    double Dm = 0.0, M2 = 0.0;
+    D3 DP = D3{0.0, 0.0, 0.0};
+    bool first = true;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
+        const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
+        if (!pres) continue;
+        const long long c = c00 + (ap - 1) + (long long)p.nx * ((bp - 1) + (long long)p.ny * (cp - 1));
+        const double d = __ldg(dm + c), mm = __ldg(m2 + c);
+        const D3 dp = D3{__ldg(s.dP[0] + c), __ldg(s.dP[1] + c), __ldg(s.dP[2] + c)};
+        Dm = first ? d : Dm + d;
+        DP = first ? dp : add(DP, dp);
+        M2 = first ? mm : M2 + mm;
+        first = false;
+    }
+    Dm = 0.125 * Dm;
+    DP = scl(0.125, DP);
+    M2 = 0.125 * M2;
+    const long long n = (long long)i + (long long)(p.nx + 1) * ((long long)j + (long long)(p.ny + 1) * (k - s.kb));
+    const D3 u1 = ld3(s.u1, n);
+    D3 un = d3(u1.x + ((DP.x - (u1.x * Dm)) / M2), u1.y + ((DP.y - (u1.y * Dm)) / M2),
+               u1.z + ((DP.z - (u1.z * Dm)) / M2));
+    un = reflect(p, i, j, k, un);
+    st3(s.u[cur ^ 1], n, un);
+    s.x1[0][n] = speed2(un);  // |u''|^2 (x' scratch is free after kr_cells)
+}
+
+__global__ void __launch_bounds__(256) kn_dt(Slab s, Phys p, int cur)
+{
+    if (!s.st->active) return;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long key = KEY_NONE;
+    if (t < s.pc * (s.k1 - s.k0)) {
+        const int k = s.k0 + (int)(t / s.pc);
+        const long long r = t % s.pc;
+        const int j = (int)(r / p.nx), i = (int)(r % p.nx);
+        const long long n0 = (long long)i + (long long)(p.nx + 1) * ((long long)j + (long long)(p.ny + 1) * (k - s.kb));
+        const long long pn = s.pn, rw = p.nx + 1;
+        const double* __restrict__ v = s.x1[0];
+        double v2 = __ldg(v + n0);
+        v2 = dmax(v2, __ldg(v + n0 + 1));
+        v2 = dmax(v2, __ldg(v + n0 + rw));
+        v2 = dmax(v2, __ldg(v + n0 + rw + 1));
+        v2 = dmax(v2, __ldg(v + n0 + pn));
+        v2 = dmax(v2, __ldg(v + n0 + pn + 1));
+        v2 = dmax(v2, __ldg(v + n0 + pn + rw));
+        v2 = dmax(v2, __ldg(v + n0 + pn + rw + 1));
+        // c.5 on the target mesh: the 12 edges of a target cell are axis-aligned
+        const double lx = len2(D3{s.Xt[i], 0.0, 0.0}, D3{s.Xt[i + 1], 0.0, 0.0});
+        const double ly = len2(D3{0.0, s.Yt[j], 0.0}, D3{0.0, s.Yt[j + 1], 0.0});
+        const double lz = len2(D3{0.0, 0.0, s.Zt[k - s.kb]}, D3{0.0, 0.0, s.Zt[k + 1 - s.kb]});
+        const long long c = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
+        double rho = s.m[cur ^ 1][c] / s.VT[c], pr, pf, cs;
+        eos(p.gamma, rho, s.e[cur ^ 1][c], pr, pf, cs);
+        key = dt_key(dt_cell(p.cfl, dmin(dmin(lx, ly), lz), v2, cs));
+    }
+    block_min_atomic(key, &s.st->cand_key);
+}
+
+// ============================================================================
 namespace {
 inline int cdivr(int a, int b) { return (a + b - 1) / b; }
 constexpr int NW_RC = 8, NW_RN = 8, RZ = 32;
@@ -539,7 +952,11 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
     cudaStream_t cs = (cudaStream_t)st;
     const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
-    {
+    static const int variant = [] {
+        const char* v = getenv("SALE_REMAP");
+        return v ? atoi(v) : 2;
+    }();
+    if (variant == 0) {
         constexpr int NW = NW_RC;
         const size_t sm = sizeof(double) * RemapCellsCTA<NW>::WORDS;
         static bool init = false;
@@ -549,8 +966,32 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
         }
         dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
         kr_cells<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+    } else if (variant == 1) {
+        constexpr int NW = 7, MB = 2;
+        const size_t sm = sizeof(double) * RemapCellsP<NW>::WORDS;
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(kr_cells_p<NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            init = true;
+        }
+        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
+        kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+    } else {
+        constexpr int NW = 12, MB = 1;
+        const size_t sm = sizeof(double) * RemapCellsP<NW>::WORDS;
+        static bool init = false;
+        if (!init) {
+            cudaFuncSetAttribute(kr_cells_p<NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            init = true;
+        }
+        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
+        kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
     }
-    {
+    static const int nvariant = [] {
+        const char* v = getenv("SALE_RNODES");
+        return v ? atoi(v) : 1;
+    }();
+    if (nvariant == 0) {
         constexpr int NW = NW_RN;
         const size_t sm = sizeof(double) * RemapNodesCTA<NW>::WORDS;
         static bool init = false;
@@ -560,6 +1001,11 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
         }
         dim3 grid(cdivr(p.nx + 1, RW - 2), cdivr(p.ny + 1, NW - 2), cdivr(s.k1 - s.k0 + 1, RZ));
         kr_nodes<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, RZ);
+    } else {
+        const long long nn = s.pn * (s.k1 - s.k0 + 1), nc = s.pc * (s.k1 - s.k0);
+        kn_update<<<(unsigned)((nn + 255) / 256), 256, 0, cs>>>(s, p, cur);
+        kn_dt<<<(unsigned)((nc + 255) / 256), 256, 0, cs>>>(s, p, cur);
+        return 3;
     }
     return 2;
 }
