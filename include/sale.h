@@ -94,7 +94,10 @@ typedef struct sale_params {
     double e_deposit;         /* Sedov energy E0 placed in global cell (0,0,0)    */
     int32_t rank, nranks;     /* this process's rank in [0,nranks)                 */
     const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0 (see
-                                   sale_nccl_unique_id); must be NULL iff nranks==1 */
+                                   sale_nccl_unique_id); required when nranks > 1.
+                                   With nranks == 1 it is optional: a 1-rank NCCL
+                                   communicator then carries the dt allreduce (used
+                                   to exercise the NCCL path on a single GPU). */
     void* stream;             /* cudaStream_t to enqueue on (NULL = legacy stream) */
     void* workspace;          /* device memory, >= sale_workspace_bytes(), 256-B
                                  aligned, owned by the caller, not freed by us     */

@@ -106,7 +106,7 @@ bool params_ok(const sale_params* p)
     if (p->reflect_mask > 0x3Fu) return false;
     if (!(p->rho0 > 0.0)) return false;
     if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return false;
-    if ((p->nranks == 1) != (p->nccl_unique_id == nullptr)) return false;
+    if (p->nranks > 1 && p->nccl_unique_id == nullptr) return false;  // nranks == 1 + id: 1-rank NCCL comm
     if (p->local_slabs < 1 || (p->nranks > 1 && p->local_slabs != 1)) return false;
     if (p->impl != SALE_IMPL_V0 && p->impl != SALE_IMPL_FUSED) return false;
     if (p->impl == SALE_IMPL_FUSED && !sale::fused_available()) return false;
@@ -390,7 +390,7 @@ int exchange(sale_ctx* c, int b, bool include_mass)
     }
     int rc = cuda_check(c, cudaGetLastError(), "halo copy");
     if (rc) return rc;
-    if (c->prm.nranks == 1) return SALE_OK;
+    if (c->prm.nranks == 1) return SALE_OK;  // (a 1-rank communicator has no halo messages)
     // ranks: one grouped NCCL exchange with r-1 and r+1, exactly the messages of
     // the host-side plan (sale_halo_plan, tested on CPU with gloo)
     const Slab& S = c->slabs[0];
@@ -410,7 +410,7 @@ int exchange(sale_ctx* c, int b, bool include_mass)
 // X2: min over ranks of (dt candidate key, error key)
 int reduce_keys(sale_ctx* c)
 {
-    if (c->prm.nranks == 1) return SALE_OK;
+    if (!c->comm) return SALE_OK;
     return nccl_check(c,
                       ncclAllReduce(&c->dstate->cand_key, &c->dstate->cand_key, 2, ncclUint64, ncclMin,
                                     c->comm, c->stream),
@@ -466,7 +466,7 @@ int sync_state(sale_ctx* c, int* good_out)
     if (rc) return rc;
     if ((rc = cuda_check(c, cudaStreamSynchronize(c->stream), "stream sync"))) return rc;
     prof_collect(c);
-    if (c->prm.nranks > 1) {
+    if (c->comm) {
         ncclResult_t ar;
         if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess)
             return nccl_check(c, ar, "async");
@@ -594,7 +594,7 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
     c->hstate->cand_key = sale::KEY_NONE;
     c->hstate->err_key = sale::KEY_NONE;
     c->hstate->err_cell = -1;
-    if (p->nranks > 1) {
+    if (p->nccl_unique_id) {
         ncclUniqueId id;
         std::memcpy(&id, p->nccl_unique_id, sizeof id);
         rc = nccl_check(c, ncclCommInitRank(&c->comm, p->nranks, id, p->rank), "ncclCommInitRank");

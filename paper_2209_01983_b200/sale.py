@@ -182,7 +182,7 @@ class Sale:
         p.workspace_bytes = nbytes
         p.stream = self.stream.cuda_stream
         self._id = None
-        if nranks > 1:
+        if nccl_id is not None:
             self._id = C.create_string_buffer(nccl_id, 128)
             p.nccl_unique_id = C.cast(self._id, C.c_void_p)
         self._p = p

@@ -166,3 +166,20 @@ def test_fused_matches_v0_at_full_size(name, cycles):
         g = b.get(f)
         assert np.array_equal(g.view(np.int64), ref[f].view(np.int64)), f
     assert b.clock() == clk
+
+
+@pytest.mark.parametrize("rezone", [LAGRANGE, EULER])
+def test_nccl_one_rank_communicator(rezone):
+    """The NCCL plumbing on one GPU: a 1-rank communicator (ncclCommInitRank from
+    a unique id, the per-cycle 16-byte ncclAllReduce(min) on the stream, async
+    error polling, ncclCommDestroy) gives the same bits as the NCCL-free path."""
+    from paper_2209_01983_b200.sale import nccl_unique_id
+    cfg = sedov((12, 10, 9), rezone)
+    a = _sale(cfg, impl="fused", nccl_id=nccl_unique_id())
+    b = _sale(cfg, impl="fused")
+    o = O.Oracle(cfg)
+    for c in (a, b, o):
+        assert c.step(15) == (0, 15)
+    compare(a, b)
+    compare(a, o)
+    a.close()
