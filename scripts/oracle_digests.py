@@ -1,0 +1,71 @@
+"""Write golden digests of the CPU oracle for a BASELINE config (calls only oracle/).
+
+    python scripts/oracle_digests.py C2            # full length
+    python scripts/oracle_digests.py C3 --cycles 200
+
+Output tests/golden/<name>.json: the clock, the status, and for every state and
+derived field the SHA-256 of its float64 bytes (x fastest, then y, then z) plus a
+strided sample (every 4099th element) for a tolerance comparison if the bits ever
+differ.  The GPU tests recompute the same digests from libsale's fields.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle as O  # noqa: E402
+from paper_2209_01983_b200.configs import config  # noqa: E402
+
+FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "MASS", "E", "NODE_MASS", "RHO", "VOL", "P", "Q", "CS")
+STRIDE = 4099
+
+
+def digest(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("name")
+    ap.add_argument("--cycles", type=int, default=None)
+    ap.add_argument("--chunk", type=int, default=10)
+    args = ap.parse_args()
+    cfg, cycles = config(args.name)
+    if args.cycles is not None:
+        cycles = args.cycles
+    O.build()
+    o = O.Oracle(cfg)
+    t0 = time.time()
+    done, rc = 0, 0
+    target = cycles if cycles > 0 else 10 ** 9
+    while done < target:
+        rc, d = o.step(min(args.chunk, target - done))
+        done += d
+        print(f"{args.name}: {done} cycles, t={o.clock()['t']:.6g}, {time.time() - t0:.0f}s", flush=True)
+        if rc or d == 0:
+            break
+    out = {"config": args.name, "params": cfg, "requested_cycles": cycles, "cycles_done": done, "status": rc,
+           "last_error": o.last_error() if rc else "", "clock": o.clock(), "stride": STRIDE, "fields": {},
+           "oracle_seconds": time.time() - t0}
+    for f in FIELDS:
+        a = o.get(f).ravel()
+        out["fields"][f] = {"sha256": digest(a), "n": int(a.size),
+                            "sample": [float(v) for v in a[::STRIDE]]}
+    path = os.path.join(ROOT, "tests", "golden", f"{args.name}.json")
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path, "w") as fh:
+        json.dump(out, fh)
+    print("wrote", path)
+
+
+if __name__ == "__main__":
+    main()
