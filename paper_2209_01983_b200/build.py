@@ -36,7 +36,8 @@ def nccl_dirs():
 
 def flags():
     inc, _ = nccl_dirs()
-    return ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+    fmad = os.environ.get("SALE_FMAD", "false")
+    return ARCH + ["-O3", "-lineinfo", f"-fmad={fmad}", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
 
 

@@ -870,33 +870,44 @@ __global__ void __launch_bounds__(RW * NW, 2) kr_nodes(Slab s, Phys p, int cur, 
 // kn_update / kn_dt: R4 and the Euler dt candidate as two barrier-free kernels
 // (one thread per node / per cell, operands through L1; high occupancy).
 // ============================================================================
+// grid: x = ceil(nx+1 / 64) strips of 64 columns, y = ceil(ny+1 / 4) rows of 4, z = planes
 __global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
 {
     if (!s.st->active) return;
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= s.pn * (s.k1 - s.k0 + 1)) return;
-    const int k = s.k0 + (int)(t / s.pn);
-    const long long r = t % s.pn;
-    const int j = (int)(r / (p.nx + 1)), i = (int)(r % (p.nx + 1));
+    const int i = blockIdx.x * 64 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = s.k0 + blockIdx.z;
+    if (i > p.nx || j > p.ny) return;
     const bool pxm = i >= 1, pxp = i < p.nx, pym = j >= 1, pyp = j < p.ny, pzm = k >= 1, pzp = k < p.nz;
     const long long c00 = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
-    const double* __restrict__ dm = s.dm;
-    const double* __restrict__ m2 = s.m[cur ^ 1];
+    const int sx = 1, sy = p.nx, sz = p.nx * p.ny;
+    const double* __restrict__ dm = s.dm + c00;
+    const double* __restrict__ m2 = s.m[cur ^ 1] + c00;
+    const double* __restrict__ p0 = s.dP[0] + c00;
+    const double* __restrict__ p1 = s.dP[1] + c00;
+    const double* __restrict__ p2 = s.dP[2] + c00;
     double Dm = 0.0, M2 = 0.0;
     D3 DP = D3{0.0, 0.0, 0.0};
+    const bool all = pxm && pxp && pym && pyp && pzm && pzp;
     bool first = true;
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
         const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
-        const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
-        if (!pres) continue;
-        const long long c = c00 + (ap - 1) + (long long)p.nx * ((bp - 1) + (long long)p.ny * (cp - 1));
-        const double d = __ldg(dm + c), mm = __ldg(m2 + c);
-        const D3 dp = D3{__ldg(s.dP[0] + c), __ldg(s.dP[1] + c), __ldg(s.dP[2] + c)};
-        Dm = first ? d : Dm + d;
-        DP = first ? dp : add(DP, dp);
-        M2 = first ? mm : M2 + mm;
-        first = false;
+        const int off = (ap - 1) * sx + (bp - 1) * sy + (cp - 1) * sz;
+        if (all) {
+            const double d = __ldg(dm + off), mm = __ldg(m2 + off);
+            const D3 dp = D3{__ldg(p0 + off), __ldg(p1 + off), __ldg(p2 + off)};
+            Dm = g == 0 ? d : Dm + d;
+            DP = g == 0 ? dp : add(DP, dp);
+            M2 = g == 0 ? mm : M2 + mm;
+        } else {
+            const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
+            if (!pres) continue;
+            const double d = __ldg(dm + off), mm = __ldg(m2 + off);
+            const D3 dp = D3{__ldg(p0 + off), __ldg(p1 + off), __ldg(p2 + off)};
+            Dm = first ? d : Dm + d;
+            DP = first ? dp : add(DP, dp);
+            M2 = first ? mm : M2 + mm;
+            first = false;
+        }
     }
     Dm = 0.125 * Dm;
     DP = scl(0.125, DP);
@@ -910,26 +921,24 @@ __global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
     s.x1[0][n] = speed2(un);  // |u''|^2 (x' scratch is free after kr_cells)
 }
 
+// grid: x = ceil(nx / 64), y = ceil(ny / 4), z = owned cell planes
 __global__ void __launch_bounds__(256) kn_dt(Slab s, Phys p, int cur)
 {
     if (!s.st->active) return;
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * 64 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = s.k0 + blockIdx.z;
     unsigned long long key = KEY_NONE;
-    if (t < s.pc * (s.k1 - s.k0)) {
-        const int k = s.k0 + (int)(t / s.pc);
-        const long long r = t % s.pc;
-        const int j = (int)(r / p.nx), i = (int)(r % p.nx);
+    if (i < p.nx && j < p.ny) {
         const long long n0 = (long long)i + (long long)(p.nx + 1) * ((long long)j + (long long)(p.ny + 1) * (k - s.kb));
-        const long long pn = s.pn, rw = p.nx + 1;
-        const double* __restrict__ v = s.x1[0];
-        double v2 = __ldg(v + n0);
-        v2 = dmax(v2, __ldg(v + n0 + 1));
-        v2 = dmax(v2, __ldg(v + n0 + rw));
-        v2 = dmax(v2, __ldg(v + n0 + rw + 1));
-        v2 = dmax(v2, __ldg(v + n0 + pn));
-        v2 = dmax(v2, __ldg(v + n0 + pn + 1));
-        v2 = dmax(v2, __ldg(v + n0 + pn + rw));
-        v2 = dmax(v2, __ldg(v + n0 + pn + rw + 1));
+        const int pn = (p.nx + 1) * (p.ny + 1), rw = p.nx + 1;
+        const double* __restrict__ v = s.x1[0] + n0;
+        double v2 = __ldg(v);
+        v2 = dmax(v2, __ldg(v + 1));
+        v2 = dmax(v2, __ldg(v + rw));
+        v2 = dmax(v2, __ldg(v + rw + 1));
+        v2 = dmax(v2, __ldg(v + pn));
+        v2 = dmax(v2, __ldg(v + pn + 1));
+        v2 = dmax(v2, __ldg(v + pn + rw));
+        v2 = dmax(v2, __ldg(v + pn + rw + 1));
         // c.5 on the target mesh: the 12 edges of a target cell are axis-aligned
         const double lx = len2(D3{s.Xt[i], 0.0, 0.0}, D3{s.Xt[i + 1], 0.0, 0.0});
         const double ly = len2(D3{0.0, s.Yt[j], 0.0}, D3{0.0, s.Yt[j + 1], 0.0});
@@ -1002,9 +1011,8 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
         dim3 grid(cdivr(p.nx + 1, RW - 2), cdivr(p.ny + 1, NW - 2), cdivr(s.k1 - s.k0 + 1, RZ));
         kr_nodes<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, RZ);
     } else {
-        const long long nn = s.pn * (s.k1 - s.k0 + 1), nc = s.pc * (s.k1 - s.k0);
-        kn_update<<<(unsigned)((nn + 255) / 256), 256, 0, cs>>>(s, p, cur);
-        kn_dt<<<(unsigned)((nc + 255) / 256), 256, 0, cs>>>(s, p, cur);
+        kn_update<<<dim3(cdivr(p.nx + 1, 64), cdivr(p.ny + 1, 4), s.k1 - s.k0 + 1), dim3(64, 4), 0, cs>>>(s, p, cur);
+        kn_dt<<<dim3(cdivr(p.nx, 64), cdivr(p.ny, 4), s.k1 - s.k0), dim3(64, 4), 0, cs>>>(s, p, cur);
         return 3;
     }
     return 2;

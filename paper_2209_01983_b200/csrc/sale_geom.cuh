@@ -199,6 +199,7 @@ __device__ __forceinline__ double swept_volume(D3 T0, D3 T1, D3 T2, D3 T3, D3 L0
 }
 
 // warp + block min of an unsigned 64-bit key, then one atomicMin per block
+// (any block shape whose size is a multiple of 32; all threads must call it)
 __device__ __forceinline__ void block_min_atomic(unsigned long long key, unsigned long long* dst)
 {
     __shared__ unsigned long long red[32];
@@ -207,8 +208,9 @@ __device__ __forceinline__ void block_min_atomic(unsigned long long key, unsigne
         unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
         key = other < key ? other : key;
     }
-    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int nw = (blockDim.x + 31) >> 5;
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int lane = tid & 31, wid = tid >> 5;
+    const int nw = (blockDim.x * blockDim.y * blockDim.z + 31) >> 5;
     if (lane == 0) red[wid] = key;
     __syncthreads();
     if (wid == 0) {
