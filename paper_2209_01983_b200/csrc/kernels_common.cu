@@ -175,14 +175,27 @@ __global__ void k_dt_candidate(Slab s, Phys p, int cur, int gate)
         int k = s.k0 + (int)(t / s.pc);
         long long r = t % s.pc;
         int j = (int)(r / p.nx), i = (int)(r % p.nx);
-        D3 N[8], U[8];
-        load_hex_pos<EULER>(s, p, cur, i, j, k, N);
+        D3 U[8];
         load_hex3(s, p, s.u[cur], i, j, k, U);
         long long c = cidx(s, p, i, j, k);
-        double V = hex_volume(N);
+        double V, l2;
+        if (EULER) {
+            // fixed target mesh: V^T precomputed with the same hex formula, and the
+            // 12 target edges are axis-aligned (X_{i+1}-X_i, 0, 0) etc.
+            V = s.VT[c];
+            const double lx = len2(D3{s.Xt[i], 0.0, 0.0}, D3{s.Xt[i + 1], 0.0, 0.0});
+            const double ly = len2(D3{0.0, s.Yt[j], 0.0}, D3{0.0, s.Yt[j + 1], 0.0});
+            const double lz = len2(D3{0.0, 0.0, s.Zt[k - s.kb]}, D3{0.0, 0.0, s.Zt[k + 1 - s.kb]});
+            l2 = dmin(dmin(lx, ly), lz);
+        } else {
+            D3 N[8];
+            load_hex_pos<EULER>(s, p, cur, i, j, k, N);
+            V = hex_volume(N);
+            l2 = hex_min_edge2(N);
+        }
         double rho = mass_cur(s, p, cur)[c] / V, pr, pf, cs;
         eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
-        key = dt_key(dt_cell(p.cfl, hex_min_edge2(N), hex_max_speed2(U), cs));
+        key = dt_key(dt_cell(p.cfl, l2, hex_max_speed2(U), cs));
     }
     block_min_atomic(key, &s.st->cand_key);
 }
