@@ -183,3 +183,40 @@ def test_nccl_one_rank_communicator(rezone):
     compare(a, b)
     compare(a, o)
     a.close()
+
+
+@pytest.mark.parametrize("rezone", [LAGRANGE, EULER])
+@pytest.mark.parametrize("shape", [(67, 17, 70), (31, 44, 33)])
+def test_multi_tile_ragged_bitwise(rezone, shape):
+    """Meshes spanning several fused tiles in x (30/31/29-column tiles), y (5-9
+    rows) and z (32-plane chunks) with ragged tails, against the oracle."""
+    cfg = sedov(shape, rezone, e_background=0.3)
+    g, o = _sale(cfg, impl="fused"), O.Oracle(cfg)
+    apply_perturbation([o, g], cfg, 7, lagrange=(rezone == LAGRANGE))
+    assert g.step(6) == o.step(6) == (0, 6)
+    compare(g, o)
+    assert g.clock() == o.clock()
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+def test_degenerate_single_free_cube(impl):
+    cfg = sedov((1, 1, 1), LAGRANGE, reflect_mask=0, e_deposit=2.5, e_background=2.5)
+    g, o = _sale(cfg, impl=impl), O.Oracle(cfg)
+    assert g.step(3) == o.step(3) == (0, 3)
+    compare(g, o)
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+@pytest.mark.parametrize("rezone", [LAGRANGE, EULER])
+def test_quiescent_state_gpu(impl, rezone):
+    """Uniform state, all faces reflecting: equal to the oracle bit for bit; a
+    fixed point to round-off (bitwise only on power-of-two meshes, SURVEY c.9)."""
+    cfg = sedov((9, 7, 8), rezone, gamma=1.5, reflect_mask=0x3F)
+    g, o = _sale(cfg, impl=impl), O.Oracle(cfg)
+    for c in (g, o):
+        c.set("E", np.full(g.cell_shape, 2.0))
+    assert g.step(5) == o.step(5) == (0, 5)
+    compare(g, o)
+    for f in ("UX", "UY", "UZ"):
+        assert np.max(np.abs(g.get(f))) <= 1e-13
+    assert np.max(np.abs(g.get("E") - 2.0)) <= 1e-13
