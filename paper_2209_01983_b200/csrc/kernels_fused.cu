@@ -506,8 +506,8 @@ struct EnergyCTA {
     }
 };
 
-template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, NW >= 12 ? 1 : MINB)
+template <bool EULER, int NW, int MB>
+__global__ void __launch_bounds__(FW * NW, MB)
     kf_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
     if (!s.st->active) return;
@@ -545,17 +545,17 @@ static void force_launch(const Slab& s, const Phys& p, int cur, int kn0, int kn1
     dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW - 2), cdiv(kn1 - kn0 + 1, zc));
     kf_force<EULER, NW><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
 }
-template <bool EULER, int NW>
+template <bool EULER, int NW, int MB>
 static void energy_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
 {
     const size_t sm = sizeof(double) * EnergyCTA<EULER, NW>::WORDS;
     static bool init = false;
     if (!init) {
-        set_smem(kf_energy<EULER, NW>, sm);
+        set_smem(kf_energy<EULER, NW, MB>, sm);
         init = true;
     }
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
-    kf_energy<EULER, NW><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
+    kf_energy<EULER, NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
 }
 
 // tile / chunk choice (SALE_TUNE="nwf,nwe,zchunk" overrides, for tuning runs)
@@ -586,9 +586,9 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     if (tune.nwf >= 16) force_launch<EULER, 16>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (tune.nwf >= 12) force_launch<EULER, 12>(s, p, cur, kn0, kn1, tune.zc, cs);
     else force_launch<EULER, 8>(s, p, cur, kn0, kn1, tune.zc, cs);
-    if (tune.nwe >= 16) energy_launch<EULER, 16>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else if (tune.nwe >= 12) energy_launch<EULER, 12>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else energy_launch<EULER, 8>(s, p, cur, kc0, kc1, tune.zc, cs);
+    if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else if (tune.nwe >= 12) energy_launch<EULER, 12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else energy_launch<EULER, 8, MINB>(s, p, cur, kc0, kc1, tune.zc, cs);
     return 2;
 }
 
