@@ -957,13 +957,26 @@ inline int cdivr(int a, int b) { return (a + b - 1) / b; }
 constexpr int NW_RC = 8, NW_RN = 8, RZ = 32;
 }  // namespace
 
+template <int NW, int MB>
+static void cells_p_launch(const Slab& s, const Phys& p, int cur, int kr0, int kr1, cudaStream_t cs)
+{
+    const size_t sm = sizeof(double) * RemapCellsP<NW>::WORDS;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(kr_cells_p<NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        init = true;
+    }
+    dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
+    kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+}
+
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
     cudaStream_t cs = (cudaStream_t)st;
     const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     static const int variant = [] {
         const char* v = getenv("SALE_REMAP");
-        return v ? atoi(v) : 2;
+        return v ? atoi(v) : 6;
     }();
     if (variant == 0) {
         constexpr int NW = NW_RC;
@@ -985,16 +998,15 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
         }
         dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
         kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+    } else if (variant == 2) {
+        cells_p_launch<12, 1>(s, p, cur, kr0, kr1, cs);
+    } else if (variant == 3) {
+        cells_p_launch<8, 1>(s, p, cur, kr0, kr1, cs);
+    } else if (variant == 4) {
+        cells_p_launch<10, 1>(s, p, cur, kr0, kr1, cs);
     } else {
-        constexpr int NW = 12, MB = 1;
-        const size_t sm = sizeof(double) * RemapCellsP<NW>::WORDS;
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(kr_cells_p<NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            init = true;
-        }
-        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
-        kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+        if (variant == 5) cells_p_launch<14, 1>(s, p, cur, kr0, kr1, cs);
+        else cells_p_launch<15, 1>(s, p, cur, kr0, kr1, cs);
     }
     static const int nvariant = [] {
         const char* v = getenv("SALE_RNODES");
