@@ -583,10 +583,12 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
         kn1 = imin_h(s.k1 + 2, p.nz);
     }
     const int kc0 = kn0, kc1 = kn1;
-    if (tune.nwf >= 16) force_launch<EULER, 16>(s, p, cur, kn0, kn1, tune.zc, cs);
+    if (tune.nwf == 15) force_launch<EULER, 15>(s, p, cur, kn0, kn1, tune.zc, cs);
+    else if (tune.nwf >= 16) force_launch<EULER, 16>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (tune.nwf >= 12) force_launch<EULER, 12>(s, p, cur, kn0, kn1, tune.zc, cs);
     else force_launch<EULER, 8>(s, p, cur, kn0, kn1, tune.zc, cs);
-    if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
+    if (tune.nwe == 15) energy_launch<EULER, 15, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 12) energy_launch<EULER, 12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else energy_launch<EULER, 8, MINB>(s, p, cur, kc0, kc1, tune.zc, cs);
     return 2;
