@@ -193,7 +193,7 @@ __global__ void k_dt_candidate(Slab s, Phys p, int cur, int gate)
             V = hex_volume(N);
             l2 = hex_min_edge2(N);
         }
-        double rho = mass_cur(s, p, cur)[c] / V, pr, pf, cs;
+        double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
         eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
         key = dt_key(dt_cell(p.cfl, l2, hex_max_speed2(U), cs));
     }
@@ -238,7 +238,7 @@ __global__ void k_derive_cells(Slab s, Phys p, int cur, int field)
     hex_faces(N, A, Xb, sv);
     long long c = cidx(s, p, i, j, k);
     double V = vol_from_s(sv);
-    double rho = mass_cur(s, p, cur)[c] / V, pr, pf, cs;
+    double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
     eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
     double v;
     switch (field) {

@@ -227,7 +227,7 @@ struct ForceCTA {
                 const double* qy = me + FW;  // +y face (anchored at j+1)
                 double sv[6] = {fx.s, qx[oQ(0, 0)], fy.s, qy[oQ(1, 0)], zprev.s, zn.s};
                 double V = vol_from_s(sv);
-                double rho = m / V, pr, pf, cs;
+                double rho = ddiv(m, V), pr, pf, cs;
                 eos(p.gamma, rho, e, pr, pf, cs);
                 double dx = axis_jump(fx.Xb, ld3s(qx, oQ(0, 1), PL), fx.Ub, ld3s(qx, oQ(0, 4), PL));
                 double dy = axis_jump(fy.Xb, ld3s(qy, oQ(1, 1), PL), fy.Ub, ld3s(qy, oQ(1, 4), PL));
@@ -253,7 +253,7 @@ struct ForceCTA {
             else gather<B0, false>(F, M, pxm, pxp, pym, pyp, pzm, pzp);
             M = 0.125 * M;
             const D3 u = U<B0>(0), x = X<B0>(0);
-            D3 un = d3(u.x + ((F.x / M) * dt), u.y + ((F.y / M) * dt), u.z + ((F.z / M) * dt));
+            D3 un = d3(u.x + (ddiv(F.x, M) * dt), u.y + (ddiv(F.y, M) * dt), u.z + (ddiv(F.z, M) * dt));
             un = reflect(p, i, j, kz, un);
             const D3 xn = d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt));
             const long long n = nb + (long long)kz * s.pn;
@@ -440,14 +440,14 @@ struct EnergyCTA {
                 W = (h == 0) ? term : W + term;
             }
             const long long cc = cb + (long long)kz * s.pc;
-            const double e1 = e - (((sig * W) * dt) / m);
+            const double e1 = e - ddiv((sig * W) * dt, m);
             if (EULER) {
                 s.e1[cc] = e1;
                 s.V1[cc] = V1;
             } else {
                 s.e[cur ^ 1][cc] = e1;
                 if (owned) {
-                    double rho = m / V1, pr, pf, cs;
+                    double rho = ddiv(m, V1), pr, pf, cs;
                     eos(p.gamma, rho, e1, pr, pf, cs);
                     double l2 = dmin(dmin(me[oE(0)], me[FW + oE(0)]), dmin(me[oE(1)], me[1 + oE(1)]));
                     l2 = dmin(l2, dmin(dmin(me[oE(2)], me[1 + oE(2)]), dmin(me[FW + oE(2)], me[FW + 1 + oE(2)])));

@@ -188,7 +188,7 @@ struct RemapCellsCTA {
             sum = add(sum, UL<B1>(RW));
             sum = add(sum, UL<B1>(RW + 1));
             ub = scl(0.125, sum);
-            r = m / V1;
+            r = ddiv(m, V1);
         }
         me[oC(0)] = r;
         me[oC(1)] = e1;
@@ -231,7 +231,7 @@ struct RemapCellsCTA {
             // moved x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
             const double sL = fs(XL<B0>(0), XL<B0>(RW), XL<B1>(RW), XL<B1>(0));
             const double sT = sT0;
-            const double dV = (((((me[RW + oR(0)] - me[oR(0)]) + rxy_next) - rxy_prev) + sL) - sT) / 3.0;
+            const double dV = ddiv(((((me[RW + oR(0)] - me[oR(0)]) + rxy_next) - rxy_prev) + sL) - sT, 3.0);
             const double* L = me - 1;
             fx = flux(dV, L[oC(0)], L[oC(1)], ld3r(L, oC(2), PL), r, e1, ub);
         }
@@ -239,7 +239,7 @@ struct RemapCellsCTA {
             // moved y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
             const double sL = fs(XL<B0>(0), XL<B1>(0), XL<B1>(1), XL<B0>(1));
             const double sT = sT1;
-            const double dV = (((((ryx_next - ryx_prev) + me[1 + oR(1)]) - me[oR(1)]) + sL) - sT) / 3.0;
+            const double dV = ddiv(((((ryx_next - ryx_prev) + me[1 + oR(1)]) - me[oR(1)]) + sL) - sT, 3.0);
             const double* L = me - RW;
             fy = flux(dV, L[oC(0)], L[oC(1)], ld3r(L, oC(2), PL), r, e1, ub);
         }
@@ -247,7 +247,7 @@ struct RemapCellsCTA {
             // moved z-face at node plane kz: (i,j,kz) (i+1,j,kz) (i+1,j+1,kz) (i,j+1,kz)
             const double sL = fs(XL<B0>(0), XL<B0>(1), XL<B0>(RW + 1), XL<B0>(RW));
             const double sT = sT2;
-            const double dV = (((((me[1 + oR(2)] - me[oR(2)]) + me[RW + oR(3)]) - me[oR(3)]) + sL) - sT) / 3.0;
+            const double dV = ddiv(((((me[1 + oR(2)] - me[oR(2)]) + me[RW + oR(3)]) - me[oR(3)]) + sL) - sT, 3.0);
             fz = flux(dV, r_prev, e_prev, ub_prev, r, e1, ub);
         }
         me[oF(B0, 0, 0)] = fx.mu;
@@ -276,7 +276,7 @@ struct RemapCellsCTA {
             if (kc >= s.k0 && kc < s.k1 && !(m2 > 0.0))
                 atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, kc));
             const long long c = cb + (long long)kc * s.pc;
-            s.e[cur ^ 1][c] = e_prev + ((dE - (e_prev * dm)) / m2);
+            s.e[cur ^ 1][c] = e_prev + ddiv(dE - (e_prev * dm), m2);
             s.m[cur ^ 1][c] = m2;
             s.dm[c] = dm;
             st3(s.dP, c, dP);
@@ -471,7 +471,7 @@ struct RemapCellsP {
             sum = add(sum, UL1(RW));
             sum = add(sum, UL1(RW + 1));
             cell.ub = scl(0.125, sum);
-            cell.r = qm / qv;
+            cell.r = ddiv(qm, qv);
         }
         me[oC(PAR, 0)] = cell.r;
         me[oC(PAR, 1)] = cell.e1;
@@ -518,18 +518,18 @@ struct RemapCellsP {
         const bool do_y = yface_on && t >= 0 && t < p.nz && t >= za && t <= zb;
         const bool do_z = zface_on && t >= 1 && t <= p.nz - 1 && t >= za;
         if (do_x) {
-            const double dV = (((((me[RW + oR(PAR, 0)] - me[oR(PAR, 0)]) + rxy_t1) - rxy_t) + sLx) - sTx) / 3.0;
+            const double dV = ddiv(((((me[RW + oR(PAR, 0)] - me[oR(PAR, 0)]) + rxy_t1) - rxy_t) + sLx) - sTx, 3.0);
             const double* L = me - 1;
             fx = flux(dV, Cell{L[oC(PAR, 0)], L[oC(PAR, 1)], ld3r(L, oC(PAR, 2), PL)}, c_t);
         }
         if (do_y) {
-            const double dV = (((((ryx_t1 - ryx_t) + me[1 + oR(PAR, 1)]) - me[oR(PAR, 1)]) + sLy) - sTy) / 3.0;
+            const double dV = ddiv(((((ryx_t1 - ryx_t) + me[1 + oR(PAR, 1)]) - me[oR(PAR, 1)]) + sLy) - sTy, 3.0);
             const double* L = me - RW;
             fy = flux(dV, Cell{L[oC(PAR, 0)], L[oC(PAR, 1)], ld3r(L, oC(PAR, 2), PL)}, c_t);
         }
         if (do_z) {
             const double dV =
-                (((((me[1 + oR(PAR, 2)] - me[oR(PAR, 2)]) + me[RW + oR(PAR, 3)]) - me[oR(PAR, 3)]) + sLz) - sTz) / 3.0;
+                ddiv(((((me[1 + oR(PAR, 2)] - me[oR(PAR, 2)]) + me[RW + oR(PAR, 3)]) - me[oR(PAR, 3)]) + sLz) - sTz, 3.0);
             fzt = flux(dV, c_tm1, c_t);
         }
         me[oF(PAR, 0, 0)] = fx.mu;
@@ -561,7 +561,7 @@ struct RemapCellsP {
         if (kc >= s.k0 && kc < s.k1 && !(m2 > 0.0))
             atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, kc));
         const long long c = cb + (long long)kc * s.pc;
-        s.e[cur ^ 1][c] = e_tm1 + ((dE - (e_tm1 * dm)) / m2);
+        s.e[cur ^ 1][c] = e_tm1 + ddiv(dE - (e_tm1 * dm), m2);
         s.m[cur ^ 1][c] = m2;
         s.dm[c] = dm;
         st3(s.dP, c, dP);
@@ -791,8 +791,8 @@ struct RemapNodesCTA {
             Dm = 0.125 * Dm;
             DP = scl(0.125, DP);
             M2 = 0.125 * M2;
-            D3 un = d3(u1.x + ((DP.x - (u1.x * Dm)) / M2), u1.y + ((DP.y - (u1.y * Dm)) / M2),
-                       u1.z + ((DP.z - (u1.z * Dm)) / M2));
+            D3 un = d3(u1.x + ddiv(DP.x - (u1.x * Dm), M2), u1.y + ddiv(DP.y - (u1.y * Dm), M2),
+                       u1.z + ddiv(DP.z - (u1.z * Dm), M2));
             un = reflect(p, i, j, kz, un);
             if (node_out && kz <= zb) st3(s.u[cur ^ 1], nb + (long long)kz * s.pn, un);
             me[oV(B0)] = speed2(un);
@@ -811,7 +811,7 @@ struct RemapNodesCTA {
             v2 = dmax(v2, me[RW + 1 + oV(B0)]);
             const double lz = len2(D3{0.0, 0.0, s.Zt[kc - s.kb]}, D3{0.0, 0.0, s.Zt[kc + 1 - s.kb]});
             const double m2 = me[oU(B1, 4)];
-            double rho = m2 / vt, pr, pf, cs;
+            double rho = ddiv(m2, vt), pr, pf, cs;
             eos(p.gamma, rho, e2, pr, pf, cs);
             const unsigned long long kk = dt_key(dt_cell(p.cfl, dmin(l2, lz), v2, cs));
             key = kk < key ? kk : key;
@@ -914,8 +914,8 @@ __global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
     M2 = 0.125 * M2;
     const long long n = (long long)i + (long long)(p.nx + 1) * ((long long)j + (long long)(p.ny + 1) * (k - s.kb));
     const D3 u1 = ld3(s.u1, n);
-    D3 un = d3(u1.x + ((DP.x - (u1.x * Dm)) / M2), u1.y + ((DP.y - (u1.y * Dm)) / M2),
-               u1.z + ((DP.z - (u1.z * Dm)) / M2));
+    D3 un = d3(u1.x + ddiv(DP.x - (u1.x * Dm), M2), u1.y + ddiv(DP.y - (u1.y * Dm), M2),
+               u1.z + ddiv(DP.z - (u1.z * Dm), M2));
     un = reflect(p, i, j, k, un);
     st3(s.u[cur ^ 1], n, un);
     s.x1[0][n] = speed2(un);  // |u''|^2 (x' scratch is free after kr_cells)
@@ -944,7 +944,7 @@ __global__ void __launch_bounds__(256) kn_dt(Slab s, Phys p, int cur)
         const double ly = len2(D3{0.0, s.Yt[j], 0.0}, D3{0.0, s.Yt[j + 1], 0.0});
         const double lz = len2(D3{0.0, 0.0, s.Zt[k - s.kb]}, D3{0.0, 0.0, s.Zt[k + 1 - s.kb]});
         const long long c = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
-        double rho = s.m[cur ^ 1][c] / s.VT[c], pr, pf, cs;
+        double rho = ddiv(s.m[cur ^ 1][c], s.VT[c]), pr, pf, cs;
         eos(p.gamma, rho, s.e[cur ^ 1][c], pr, pf, cs);
         key = dt_key(dt_cell(p.cfl, dmin(dmin(lx, ly), lz), v2, cs));
     }

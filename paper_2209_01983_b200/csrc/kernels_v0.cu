@@ -31,7 +31,7 @@ __global__ void k0_sigma(Slab s, Phys p, int cur, int ka0, int ka1)
     hex_faces(N, A, Xb, sv);
     long long c = cidx(s, p, i, j, k);
     double V = vol_from_s(sv);
-    double rho = mass_cur(s, p, cur)[c] / V, pr, pf, cs;
+    double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
     eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
     double q = hex_q(Xb, U, rho, cs, p.c1, p.c2);
     s.sig[c] = 0.25 * (pf + q);
@@ -75,7 +75,7 @@ __global__ void k0_nodes(Slab s, Phys p, int cur, int kb0, int kb1)
     double dt = s.st->dt;
     long long n = nidx(s, p, i, j, k);
     D3 u = ld3(s.u[cur], n);
-    D3 un = d3(u.x + ((F.x / M) * dt), u.y + ((F.y / M) * dt), u.z + ((F.z / M) * dt));
+    D3 un = d3(u.x + (ddiv(F.x, M) * dt), u.y + (ddiv(F.y, M) * dt), u.z + (ddiv(F.z, M) * dt));
     un = reflect(p, i, j, k, un);
     D3 x = pos<EULER>(s, p, cur, i, j, k);
     D3 xn = d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt));
@@ -125,14 +125,14 @@ __global__ void k0_energy(Slab s, Phys p, int cur, int kc0, int kc1)
         }
         long long c = cidx(s, p, i, j, k);
         double m = mass_cur(s, p, cur)[c];
-        double e1 = s.e[cur][c] - (((s.sig[c] * W) * s.st->dt) / m);
+        double e1 = s.e[cur][c] - ddiv((s.sig[c] * W) * s.st->dt, m);
         if (EULER) {
             s.e1[c] = e1;
             s.V1[c] = V1;
         } else {
             s.e[cur ^ 1][c] = e1;
             if (owned) {
-                double rho = m / V1, pr, pf, cs;
+                double rho = ddiv(m, V1), pr, pf, cs;
                 eos(p.gamma, rho, e1, pr, pf, cs);
                 key = dt_key(dt_cell(p.cfl, hex_min_edge2(N1), hex_max_speed2(U1), cs));
             }
@@ -185,7 +185,7 @@ __device__ __forceinline__ void face_flux(const Slab& s, const Phys& p, int cur,
     for (int h = 1; h < 8; ++h) sum = add(sum, U[h]);
     D3 Ub = scl(0.125, sum);
     long long D = cidx(s, p, di, dj, dk);
-    mu = (s.m[cur][D] / s.V1[D]) * dV;
+    mu = ddiv(s.m[cur][D], s.V1[D]) * dV;
     eps = mu * s.e1[D];
     pi = scl(mu, Ub);
 }
@@ -229,7 +229,7 @@ __global__ void k0_remap_cells(Slab s, Phys p, int cur, int kr0, int kr1)
     if (k >= s.k0 && k < s.k1 && !(m2 > 0.0))
         atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, k));
     double e1 = s.e1[c];
-    s.e[cur ^ 1][c] = e1 + ((dE - (e1 * dm)) / m2);
+    s.e[cur ^ 1][c] = e1 + ddiv(dE - (e1 * dm), m2);
     s.m[cur ^ 1][c] = m2;
     s.dm[c] = dm;
     st3(s.dP, c, dP);
@@ -268,8 +268,8 @@ __global__ void k0_remap_nodes(Slab s, Phys p, int cur)
     M2 = 0.125 * M2;
     long long n = nidx(s, p, i, j, k);
     D3 u1 = ld3(s.u1, n);
-    D3 un = d3(u1.x + ((DP.x - (u1.x * Dm)) / M2), u1.y + ((DP.y - (u1.y * Dm)) / M2),
-               u1.z + ((DP.z - (u1.z * Dm)) / M2));
+    D3 un = d3(u1.x + ddiv(DP.x - (u1.x * Dm), M2), u1.y + ddiv(DP.y - (u1.y * Dm), M2),
+               u1.z + ddiv(DP.z - (u1.z * Dm), M2));
     st3(s.u[cur ^ 1], n, reflect(p, i, j, k, un));
 }
 
