@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsale.so")
+LIB_PATH = os.environ.get("SALE_LIB_PATH") or os.path.join(_HERE, "lib", "libsale.so")  # override: experiments only
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, ETANGLED, EDTCOLLAPSE, ENEGMASS, EPOISONED, EREPLICA = range(10)
 CODE_NAMES = ["OK", "EINVAL", "ENOMEM", "ECUDA", "ENCCL", "ETANGLED", "EDTCOLLAPSE", "ENEGMASS",
