@@ -85,6 +85,77 @@ int launch_sedov_init(const Slab& s, const Phys& p, Stream st)
     return 2;
 }
 
+// Euler target-mesh tables (Slab::TAx..TJz): the c.2 face area vectors and the
+// c.3 step 2 centroid separations of x^T, evaluated with the same primitives and
+// canonical node orders as every per-cycle evaluation, at a representative index
+// of the coordinates they do not depend on (x^T is a tensor product of X_i, Y_j,
+// Z_k, and every difference of equal coordinates is exactly +0).
+__global__ void k_target_tables(Slab s, Phys p)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nx = p.nx, ny = p.ny, nzc = s.nzc, kb = s.kb;
+    // x-faces (j, k): nodes (i,j,k) (i,j+1,k) (i,j+1,k+1) (i,j,k+1) at i = 0
+    if (t < ny * nzc) {
+        const int j = t % ny, k = kb + t / ny;
+        const D3 A = face_area(tpos(s, 0, j, k), tpos(s, 0, j + 1, k), tpos(s, 0, j + 1, k + 1), tpos(s, 0, j, k + 1));
+        s.TAx[0][t] = A.x;
+        s.TAx[1][t] = A.y;
+        s.TAx[2][t] = A.z;
+    }
+    // y-faces (i, k): nodes (i,j,k) (i,j,k+1) (i+1,j,k+1) (i+1,j,k) at j = 0
+    if (t < nx * nzc) {
+        const int i = t % nx, k = kb + t / nx;
+        const D3 A = face_area(tpos(s, i, 0, k), tpos(s, i, 0, k + 1), tpos(s, i + 1, 0, k + 1), tpos(s, i + 1, 0, k));
+        s.TAy[0][t] = A.x;
+        s.TAy[1][t] = A.y;
+        s.TAy[2][t] = A.z;
+    }
+    // z-faces (i, j): nodes (i,j,k) (i+1,j,k) (i+1,j+1,k) (i,j+1,k) at local plane 0
+    if (t < nx * ny) {
+        const int i = t % nx, j = t / nx;
+        const D3 A = face_area(tpos(s, i, j, kb), tpos(s, i + 1, j, kb), tpos(s, i + 1, j + 1, kb), tpos(s, i, j + 1, kb));
+        s.TAz[0][t] = A.x;
+        s.TAz[1][t] = A.y;
+        s.TAz[2][t] = A.z;
+    }
+    // axis-jump constants: d = Xbar(+a face) - Xbar(-a face), L = sqrt(d.d) (c.3 step 2)
+    auto jump = [](D3 Xm, D3 Xp, double* out) {
+        const D3 d = sub(Xp, Xm);
+        out[0] = d.x;
+        out[1] = d.y;
+        out[2] = d.z;
+        out[3] = dsqrt((d.x * d.x + d.y * d.y) + d.z * d.z);
+    };
+    const int k0 = kb;
+    if (t < nx) {
+        const int i = t;
+        const D3 Xm = avg4(tpos(s, i, 0, k0), tpos(s, i, 1, k0), tpos(s, i, 1, k0 + 1), tpos(s, i, 0, k0 + 1));
+        const D3 Xp = avg4(tpos(s, i + 1, 0, k0), tpos(s, i + 1, 1, k0), tpos(s, i + 1, 1, k0 + 1), tpos(s, i + 1, 0, k0 + 1));
+        jump(Xm, Xp, s.TJx + 4 * i);
+    }
+    if (t < ny) {
+        const int j = t;
+        const D3 Xm = avg4(tpos(s, 0, j, k0), tpos(s, 0, j, k0 + 1), tpos(s, 1, j, k0 + 1), tpos(s, 1, j, k0));
+        const D3 Xp = avg4(tpos(s, 0, j + 1, k0), tpos(s, 0, j + 1, k0 + 1), tpos(s, 1, j + 1, k0 + 1), tpos(s, 1, j + 1, k0));
+        jump(Xm, Xp, s.TJy + 4 * j);
+    }
+    if (t < nzc) {
+        const int k = kb + t;
+        const D3 Xm = avg4(tpos(s, 0, 0, k), tpos(s, 1, 0, k), tpos(s, 1, 1, k), tpos(s, 0, 1, k));
+        const D3 Xp = avg4(tpos(s, 0, 0, k + 1), tpos(s, 1, 0, k + 1), tpos(s, 1, 1, k + 1), tpos(s, 0, 1, k + 1));
+        jump(Xm, Xp, s.TJz + 4 * t);
+    }
+}
+
+int launch_target_tables(const Slab& s, const Phys& p, Stream st)
+{
+    long long n = (long long)p.ny * s.nzc;
+    n = n > (long long)p.nx * s.nzc ? n : (long long)p.nx * s.nzc;
+    n = n > (long long)p.nx * p.ny ? n : (long long)p.nx * p.ny;
+    k_target_tables<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    return 1;
+}
+
 // ---------------------------------------------------------------- clock
 __global__ void k_prep(DevState* d)
 {

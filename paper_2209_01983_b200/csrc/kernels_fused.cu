@@ -294,6 +294,207 @@ __global__ void __launch_bounds__(FW * NW, NW >= 12 ? 1 : MINB)
 }
 
 // ============================================================================
+// kf_force, Euler mode: the same computation with the t^n geometry of the fixed
+// target mesh taken from the tables built at create (Slab::TAx..TJz, V^T) instead
+// of being re-evaluated from x^T every cycle: face area vectors (corner forces),
+// cell volume, and the centroid separations of the viscosity (same bits).  Only
+// velocities are staged; per column and step the work is the three face-average
+// velocities, EoS + q + sigma of one cell, and the force gather of one node.
+// ============================================================================
+template <int NW>
+struct ForceEulerCTA {
+    static constexpr int PL = NW * FW, TX = FW - 2, TY = NW - 2;
+    __host__ __device__ static constexpr int oU(int par, int c) { return (par * 3 + c) * PL; }         // node u
+    __host__ __device__ static constexpr int oW(int xy, int c) { return 6 * PL + (xy * 3 + c) * PL; }    // x/y face Ubar
+    __host__ __device__ static constexpr int oA(int par, int xy) { return 12 * PL + (par * 2 + xy) * 3 * PL; }  // x/y face A
+    __host__ __device__ static constexpr int oZ() { return 24 * PL; }                                    // z-face A
+    __host__ __device__ static constexpr int oS(int par, int c) { return 27 * PL + (par * 2 + c) * PL; }  // sigma, m
+    static constexpr int WORDS = 31 * PL + 2 * PAD;
+
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, za, zb, kn0, kn1, ic, jc;  // ic, jc: i, j clamped into the cell range (table indices)
+    long long nb, cb;
+    double dt;
+    bool col_in, cellcol_in, node_out, sig_col;
+    bool pxm, pxp, pym, pyp;
+    D3 pu;  // prefetch: node u of plane k
+    double pm, pe, pv;  // prefetch: cell m, e, V^T of plane k-1
+    D3 zprev;  // Ubar of the z-face at node plane kz (the -z face of cell kz)
+
+    __device__ __forceinline__ ForceEulerCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kn0_, int kn1_,
+                                             int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + PAD + iy * FW + ix;
+        i = blockIdx.x * TX - 1 + ix;
+        j = blockIdx.y * TY - 1 + iy;
+        ic = i < 0 ? 0 : (i >= p.nx ? p.nx - 1 : i);
+        jc = j < 0 ? 0 : (j >= p.ny ? p.ny - 1 : j);
+        kn0 = kn0_;
+        kn1 = kn1_;
+        za = kn0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kn1 ? za + zchunk - 1 : kn1;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        dt = s.st->dt;
+        col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
+        cellcol_in = i >= 0 && i < p.nx && j >= 0 && j < p.ny;
+        node_out = col_in && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY;
+        sig_col = cellcol_in && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY;
+        pxm = i >= 1 && i <= p.nx;
+        pxp = i >= 0 && i < p.nx;
+        pym = j >= 1 && j <= p.ny;
+        pyp = j >= 0 && j < p.ny;
+        // the z-face area vectors do not depend on the plane: staged once
+        const long long tz = (long long)jc * p.nx + ic;
+        st3s(me, oZ(), PL, D3{s.TAz[0][tz], s.TAz[1][tz], s.TAz[2][tz]});
+    }
+
+    __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
+    {
+        pu = D3{0.0, 0.0, 0.0};
+        if (col_in && k >= 0 && k <= p.nz) pu = ld3(s.u[cur], nb + (long long)k * s.pn);
+        pm = 0.0;
+        pe = 0.0;
+        pv = 1.0;
+        const int kc = k - 1;
+        if (cellcol_in && kc >= 0 && kc < p.nz) {
+            const long long c = cb + (long long)kc * s.pc;
+            pm = s.m[cur][c];
+            pe = s.e[cur][c];
+            pv = s.VT[c];
+        }
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oU(PAR, 0), PL); }
+
+    template <int B0, bool ALL>
+    __device__ __forceinline__ void gather(D3& F, double& M, bool pzm, bool pzp) const
+    {
+        constexpr int B1 = B0 ^ 1;
+        F = D3{0.0, 0.0, 0.0};
+        M = 0.0;
+        bool first = true;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
+            const int dx = ap ? 0 : -1, dy = bp ? 0 : -FW;
+            const int PAR = cp ? B0 : B1;
+            const D3 Ax = ld3s(me + dy, oA(PAR, 0), PL);
+            const D3 Ay = ld3s(me + dx, oA(PAR, 1), PL);
+            const D3 Az = ld3s(me + dx + dy, oZ(), PL);
+            const D3 C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
+            const double sg = me[dx + dy + oS(PAR, 0)];
+            const double mk = me[dx + dy + oS(PAR, 1)];
+            const D3 term = scl(sg, C);
+            if (ALL) {
+                F = g == 0 ? term : add(F, term);
+                M = g == 0 ? mk : M + mk;
+            } else {
+                const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
+                if (pres) {
+                    F = first ? term : add(F, term);
+                    M = first ? mk : M + mk;
+                    first = false;
+                }
+            }
+        }
+    }
+
+    // c.3 step 2 on one axis with the table's d and L
+    __device__ __forceinline__ static double jump(const double* T, D3 Um, D3 Up)
+    {
+        const D3 w = sub(Up, Um);
+        return ddiv((w.x * T[0] + w.y * T[1]) + w.z * T[2], T[3]);
+    }
+
+    template <int B0>
+    __device__ __forceinline__ void step(int kz)
+    {
+        constexpr int B1 = B0 ^ 1;
+        // ---- P1: stage node plane kz+1 (u), cell (i,j,kz); prefetch the next
+        st3s(me, oU(B1, 0), PL, pu);
+        const double m = pm, e = pe, V = pv;
+        if (kz < zb) fetch(kz + 2);
+        __syncthreads();
+        // ---- P2: face-average velocities of the three faces anchored here; A from the tables
+        const D3 ux = avg4(U<B0>(0), U<B0>(FW), U<B1>(FW), U<B1>(0));
+        const D3 uy = avg4(U<B0>(0), U<B1>(0), U<B1>(1), U<B0>(1));
+        const D3 uz = avg4(U<B1>(0), U<B1>(1), U<B1>(FW + 1), U<B1>(FW));
+        st3s(me, oW(0, 0), PL, ux);
+        st3s(me, oW(1, 0), PL, uy);
+        const int kl = kz - s.kb;
+        const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
+        st3s(me, oA(B0, 0), PL, D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]});
+        st3s(me, oA(B0, 1), PL, D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]});
+        __syncthreads();
+        // ---- P3: cell (i,j,kz): rho, EoS, q, sigma
+        {
+            double sig = 0.0;
+            if (cellcol_in && kz >= 0 && kz < p.nz) {
+                double rho = ddiv(m, V), pr, pf, cs;
+                eos(p.gamma, rho, e, pr, pf, cs);
+                const double dx = jump(s.TJx + 4 * i, ux, ld3s(me + 1, oW(0, 0), PL));
+                const double dy = jump(s.TJy + 4 * j, uy, ld3s(me + FW, oW(1, 0), PL));
+                const double dz = jump(s.TJz + 4 * kl, zprev, uz);
+                const double du = dmin(dmin(dx, dy), dz);
+                const double q = q_of_du(rho, cs, du, p.c1, p.c2);
+                sig = 0.25 * (pf + q);
+                if (sig_col && kz >= za && kz >= kn0 && kz < kn1) s.sig[cb + (long long)kz * s.pc] = sig;
+            }
+            me[oS(B0, 0)] = sig;
+            me[oS(B0, 1)] = m;
+        }
+        zprev = uz;
+        __syncthreads();
+        // ---- P4: node (i,j,kz): force + mass gather, kinematics, BC, move
+        if (node_out && kz >= za) {
+            const bool pzm = kz >= 1, pzp = kz < p.nz;
+            D3 F;
+            double M;
+            if (pxm && pxp && pym && pyp && pzm && pzp) gather<B0, true>(F, M, true, true);
+            else gather<B0, false>(F, M, pzm, pzp);
+            M = 0.125 * M;
+            const D3 u = U<B0>(0), x = D3{s.Xt[i], s.Yt[j], s.Zt[kl]};
+            D3 un = d3(u.x + (ddiv(F.x, M) * dt), u.y + (ddiv(F.y, M) * dt), u.z + (ddiv(F.z, M) * dt));
+            un = reflect(p, i, j, kz, un);
+            const D3 xn = d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt));
+            const long long n = nb + (long long)kz * s.pn;
+            st3(s.u1, n, un);
+            st3(s.x1, n, xn);
+        }
+    }
+
+    __device__ __forceinline__ void run()
+    {
+        fetch(za - 1);
+        if ((za - 1) & 1) st3s(me, oU(1, 0), PL, pu);
+        else st3s(me, oU(0, 0), PL, pu);
+        fetch(za);
+        __syncthreads();
+        zprev = ((za - 1) & 1) ? avg4(U<1>(0), U<1>(1), U<1>(FW + 1), U<1>(FW))
+                               : avg4(U<0>(0), U<0>(1), U<0>(FW + 1), U<0>(FW));
+        for (int kz = za - 1; kz <= zb; ++kz) {
+            if (kz & 1) step<1>(kz);
+            else step<0>(kz);
+        }
+    }
+};
+
+template <int NW, int MB>
+__global__ void __launch_bounds__(FW * NW, MB) kf_force_e(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    ForceEulerCTA<NW> c(s, p, cur, smem, kn0, kn1, zchunk);
+    c.run();
+}
+
+// ============================================================================
 // kf_energy
 // ============================================================================
 template <bool EULER, int NW>
@@ -517,6 +718,159 @@ __global__ void __launch_bounds__(FW * NW, MB)
 }
 
 // ============================================================================
+// kf_energy, Euler mode: A^n from the target tables (as kf_force_e); stages only
+// x' and ubar = (u + u')/2.  Writes e' and V' (the remap's inputs).
+// ============================================================================
+template <int NW>
+struct EnergyEulerCTA {
+    static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
+    __host__ __device__ static constexpr int oP(int par, int c) { return (par * 6 + c) * PL; }        // x'(3) ubar(3)
+    __host__ __device__ static constexpr int oF(int xy, int c) { return 12 * PL + (xy * 4 + c) * PL; }  // A^n(3), s'
+    __host__ __device__ static constexpr int oZ() { return 20 * PL; }                                 // z-face A^n
+    static constexpr int WORDS = 23 * PL + 2 * PAD;
+
+    const Slab& s;
+    const Phys& p;
+    double* me;
+    int i, j, za, zb, ic, jc;
+    long long nb, cb;
+    double dt;
+    bool col_in, cell_col;
+    D3 fu, fu1, fx1;  // prefetch registers
+    double fm, fe, fs;
+    double zs_prev;
+
+    __device__ __forceinline__ EnergyEulerCTA(const Slab& s_, const Phys& p_, double* smem, int kc0, int kc1, int zchunk)
+        : s(s_), p(p_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + PAD + iy * FW + ix;
+        i = blockIdx.x * TX + ix;
+        j = blockIdx.y * TY + iy;
+        ic = i >= p.nx ? p.nx - 1 : i;
+        jc = j >= p.ny ? p.ny - 1 : j;
+        za = kc0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kc1 - 1 ? za + zchunk - 1 : kc1 - 1;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        dt = s.st->dt;
+        col_in = i <= p.nx && j <= p.ny;
+        cell_col = i < p.nx && j < p.ny && ix < TX && iy < TY;
+        const long long tz = (long long)jc * p.nx + ic;
+        st3s(me, oZ(), PL, D3{s.TAz[0][tz], s.TAz[1][tz], s.TAz[2][tz]});
+    }
+
+    __device__ __forceinline__ void fetch(int k, int cur)  // node plane k, cell plane k-1
+    {
+        fu = D3{0.0, 0.0, 0.0};
+        fu1 = fu;
+        fx1 = fu;
+        if (col_in && k >= 0 && k <= p.nz) {
+            const long long n = nb + (long long)k * s.pn;
+            fu = ld3(s.u[cur], n);
+            fu1 = ld3(s.u1, n);
+            fx1 = ld3(s.x1, n);
+        }
+        fm = 0.0;
+        fe = 0.0;
+        fs = 0.0;
+        const int kc = k - 1;
+        if (cell_col && kc >= 0 && kc < p.nz) {
+            const long long c = cb + (long long)kc * s.pc;
+            fm = s.m[cur][c];
+            fe = s.e[cur][c];
+            fs = s.sig[c];
+        }
+    }
+    template <int PAR>
+    __device__ __forceinline__ void put()
+    {
+        st3s(me, oP(PAR, 0), PL, fx1);
+        st3s(me, oP(PAR, 3), PL, scl(0.5, add(fu, fu1)));
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 X1(int off) const { return ld3s(me + off, oP(PAR, 0), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 Ub(int off) const { return ld3s(me + off, oP(PAR, 3), PL); }
+    template <int B>
+    __device__ __forceinline__ double zs() const  // s' of the moved z-face at this column, plane parity B
+    {
+        const D3 T0 = X1<B>(0), T1 = X1<B>(1), T2 = X1<B>(FW + 1), T3 = X1<B>(FW);
+        return face_s(avg4(T0, T1, T2, T3), face_area(T0, T1, T2, T3));
+    }
+
+    template <int B0>
+    __device__ __forceinline__ void step(int kz, int cur)
+    {
+        constexpr int B1 = B0 ^ 1;
+        put<B1>();
+        const double m = fm, e = fe, sig = fs;
+        if (kz < zb) fetch(kz + 2, cur);
+        __syncthreads();
+        // ---- P2: s' of the moved x- and y-faces anchored here, A^n from the tables
+        const int kl = kz - s.kb;
+        const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
+        const D3 Q0 = X1<B0>(0), Q1 = X1<B0>(FW), Q2 = X1<B1>(FW), Q3 = X1<B1>(0);
+        const double sx = face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
+        const D3 R2 = X1<B1>(1), R3 = X1<B0>(1);
+        const double sy = face_s(avg4(Q0, Q3, R2, R3), face_area(Q0, Q3, R2, R3));
+        const double zs_next = zs<B1>();
+        st3s(me, oF(0, 0), PL, D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]});
+        me[oF(0, 3)] = sx;
+        st3s(me, oF(1, 0), PL, D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]});
+        me[oF(1, 3)] = sy;
+        __syncthreads();
+        // ---- P3: cell (i,j,kz)
+        if (cell_col && kz < p.nz) {
+            double sv[6] = {me[oF(0, 3)], me[1 + oF(0, 3)], me[oF(1, 3)], me[FW + oF(1, 3)], zs_prev, zs_next};
+            const double V1 = vol_from_s(sv);
+            if (kz >= s.k0 && kz < s.k1 && !(V1 > 0.0))
+                atomicMin(&s.st->err_key, (ERR_ORDER_TANGLED << 48) | (unsigned long long)gcell(p, i, j, kz));
+            const D3 Az = ld3s(me, oZ(), PL);
+            const D3 A[6] = {ld3s(me, oF(0, 0), PL),      ld3s(me + 1, oF(0, 0), PL), ld3s(me, oF(1, 0), PL),
+                             ld3s(me + FW, oF(1, 0), PL), Az,                         Az};
+            double W = 0.0;
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                const int a = h & 1, b = (h >> 1) & 1, c = h >> 2;
+                const D3 C = corner_vec(A, a, b, c);
+                const D3 ub = c ? Ub<B1>(a + b * FW) : Ub<B0>(a + b * FW);
+                const double term = dot(C, ub);
+                W = (h == 0) ? term : W + term;
+            }
+            const long long cc = cb + (long long)kz * s.pc;
+            s.e1[cc] = e - ddiv((sig * W) * dt, m);
+            s.V1[cc] = V1;
+        }
+        zs_prev = zs_next;
+        __syncthreads();
+    }
+
+    __device__ __forceinline__ void run(int cur)
+    {
+        fetch(za, cur);
+        if (za & 1) put<1>();
+        else put<0>();
+        fetch(za + 1, cur);
+        __syncthreads();
+        zs_prev = (za & 1) ? zs<1>() : zs<0>();
+        for (int kz = za; kz <= zb; ++kz) {
+            if (kz & 1) step<1>(kz, cur);
+            else step<0>(kz, cur);
+        }
+    }
+};
+
+template <int NW, int MB>
+__global__ void __launch_bounds__(FW * NW, MB) kf_energy_e(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    EnergyEulerCTA<NW> c(s, p, smem, kc0, kc1, zchunk);
+    c.run(cur);
+}
+
+// ============================================================================
 // launchers
 // ============================================================================
 namespace {
@@ -568,6 +922,32 @@ struct Tune {
     }
 };
 
+template <int NW, int MB>
+static void force_e_launch(const Slab& s, const Phys& p, int cur, int kn0, int kn1, int zc, cudaStream_t cs)
+{
+    const size_t sm = sizeof(double) * ForceEulerCTA<NW>::WORDS;
+    static bool init = false;
+    if (!init) {
+        set_smem(kf_force_e<NW, MB>, sm);
+        init = true;
+    }
+    dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW - 2), cdiv(kn1 - kn0 + 1, zc));
+    kf_force_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
+}
+
+template <int NW, int MB>
+static void energy_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
+{
+    const size_t sm = sizeof(double) * EnergyEulerCTA<NW>::WORDS;
+    static bool init = false;
+    if (!init) {
+        set_smem(kf_energy_e<NW, MB>, sm);
+        init = true;
+    }
+    dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
+    kf_energy_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
+}
+
 template <bool EULER>
 static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
@@ -583,11 +963,27 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
         kn1 = imin_h(s.k1 + 2, p.nz);
     }
     const int kc0 = kn0, kc1 = kn1;
-    if (tune.nwf == 15) force_launch<EULER, 15>(s, p, cur, kn0, kn1, tune.zc, cs);
+    static const int fe = [] {
+        const char* v = getenv("SALE_FORCE_E");
+        return v ? atoi(v) : 2;
+    }();
+    if (EULER && fe == 1) force_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
+    else if (EULER && fe == 2) force_e_launch<8, 3>(s, p, cur, kn0, kn1, tune.zc, cs);
+    else if (EULER && fe == 3) force_e_launch<12, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
+    else if (EULER && fe == 4) force_e_launch<16, 1>(s, p, cur, kn0, kn1, tune.zc, cs);
+    else if (tune.nwf == 15) force_launch<EULER, 15>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (tune.nwf >= 16) force_launch<EULER, 16>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (tune.nwf >= 12) force_launch<EULER, 12>(s, p, cur, kn0, kn1, tune.zc, cs);
     else force_launch<EULER, 8>(s, p, cur, kn0, kn1, tune.zc, cs);
-    if (tune.nwe == 15) energy_launch<EULER, 15, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
+    static const int ee = [] {
+        const char* v = getenv("SALE_ENERGY_E");
+        return v ? atoi(v) : 1;
+    }();
+    if (EULER && ee == 1) energy_e_launch<8, 2>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else if (EULER && ee == 2) energy_e_launch<8, 3>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else if (EULER && ee == 3) energy_e_launch<12, 2>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else if (EULER && ee == 4) energy_e_launch<16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else if (tune.nwe == 15) energy_launch<EULER, 15, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 12) energy_launch<EULER, 12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else energy_launch<EULER, 8, MINB>(s, p, cur, kc0, kc1, tune.zc, cs);

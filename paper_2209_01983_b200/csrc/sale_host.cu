@@ -169,6 +169,14 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
     s.der = take(s.pn * (long long)(s.k1 - s.k0 + 1));
     s.VT = euler ? take(nc) : nullptr;
     for (int a = 0; a < 3; ++a) s.sT[a] = euler ? take(nc) : nullptr;
+    for (int a = 0; a < 3; ++a) {
+        s.TAx[a] = euler ? take((long long)p->ny * s.nzc) : nullptr;
+        s.TAy[a] = euler ? take((long long)p->nx * s.nzc) : nullptr;
+        s.TAz[a] = euler ? take((long long)p->nx * p->ny) : nullptr;
+    }
+    s.TJx = euler ? take(4LL * p->nx) : nullptr;
+    s.TJy = euler ? take(4LL * p->ny) : nullptr;
+    s.TJz = euler ? take(4LL * s.nzc) : nullptr;
     s.Xt = take(p->nx + 1);
     s.Yt = take(p->ny + 1);
     s.Zt = take(s.nzn);
@@ -610,6 +618,7 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
         if (rc) break;
         c->launches += sale::launch_init_tables(s, ph, (sale::Stream)c->stream);
         c->launches += sale::launch_sedov_init(s, ph, (sale::Stream)c->stream);
+        if (ph.rezone) c->launches += sale::launch_target_tables(s, ph, (sale::Stream)c->stream);
         rc = launch_check(c);
     }
     if (!rc) rc = cuda_check(c, cudaStreamSynchronize(c->stream), "create sync");

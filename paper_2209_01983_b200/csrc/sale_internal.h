@@ -53,6 +53,18 @@ struct Slab {
     double* der;              // derive / staging scratch (node-plane sized)
     double* VT;               // Euler: target cell volume V^T (constant; set at create)
     double* sT[3];            // Euler: s of the target x/y/z face anchored at each cell (-a faces)
+    // Euler: geometry of the fixed target mesh x^T at t^n (constant; computed once at
+    // create by k_target_tables with the same c.2 primitives the kernels would apply
+    // to x^T every cycle, so the values are the same bits).  x^T is a tensor
+    // product of the 1-D tables below, so each face family's area vector depends on
+    // two indices only, and a cell's centroid separation d / |d| along axis a (c.3
+    // step 2) on one:
+    double* TAx[3];           // A of x-faces, index (k-kb)*ny + j  (independent of i)
+    double* TAy[3];           // A of y-faces, index (k-kb)*nx + i  (independent of j)
+    double* TAz[3];           // A of z-faces, index j*nx + i       (independent of k)
+    double* TJx;              // cells i: d.x d.y d.z L at TJx[4*i + c] (x-axis jump)
+    double* TJy;              // cells j (y-axis)
+    double* TJz;              // cells at local plane k-kb (z-axis)
     double* Xt;               // target node coordinates X_i, i in [0,nx]
     double* Yt;               // Y_j, j in [0,ny]
     double* Zt;               // Z_k for local node planes (index = k - kb)
@@ -72,6 +84,7 @@ typedef struct CUstream_st* Stream;
 
 int launch_init_tables(const Slab& s, const Phys& p, Stream st);
 int launch_sedov_init(const Slab& s, const Phys& p, Stream st);
+int launch_target_tables(const Slab& s, const Phys& p, Stream st);
 int launch_prep(DevState* d, Stream st);
 int launch_begin(DevState* d, const Phys& p, Stream st);
 int launch_commit(DevState* d, const Phys& p, Stream st);
