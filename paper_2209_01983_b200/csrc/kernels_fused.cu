@@ -735,7 +735,7 @@ struct EnergyEulerCTA {
     int i, j, za, zb, ic, jc;
     long long nb, cb;
     double dt;
-    bool col_in, cell_col;
+    bool col_in, cell_col, own_col;
     D3 fu, fu1, fx1;  // prefetch registers
     double fm, fe, fs;
     double zs_prev;
@@ -756,6 +756,7 @@ struct EnergyEulerCTA {
         dt = s.st->dt;
         col_in = i <= p.nx && j <= p.ny;
         cell_col = i < p.nx && j < p.ny && ix < TX && iy < TY;
+        own_col = col_in && ix < TX && iy < TY;
         const long long tz = (long long)jc * p.nx + ic;
         st3s(me, oZ(), PL, D3{s.TAz[0][tz], s.TAz[1][tz], s.TAz[2][tz]});
     }
@@ -819,6 +820,12 @@ struct EnergyEulerCTA {
         me[oF(0, 3)] = sx;
         st3s(me, oF(1, 0), PL, D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]});
         me[oF(1, 3)] = sy;
+        if (own_col) {  // s' of the faces anchored at node (i,j,kz), for kr_sweep's swept volumes
+            const long long n = nb + (long long)kz * s.pn;
+            s.sF[0][n] = sx;
+            s.sF[1][n] = sy;
+            s.sF[2][n] = zs_prev;
+        }
         __syncthreads();
         // ---- P3: cell (i,j,kz)
         if (cell_col && kz < p.nz) {
@@ -975,14 +982,8 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     else if (tune.nwf >= 16) force_launch<EULER, 16>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (tune.nwf >= 12) force_launch<EULER, 12>(s, p, cur, kn0, kn1, tune.zc, cs);
     else force_launch<EULER, 8>(s, p, cur, kn0, kn1, tune.zc, cs);
-    static const int ee = [] {
-        const char* v = getenv("SALE_ENERGY_E");
-        return v ? atoi(v) : 1;
-    }();
-    if (EULER && ee == 1) energy_e_launch<8, 2>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else if (EULER && ee == 2) energy_e_launch<8, 3>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else if (EULER && ee == 3) energy_e_launch<12, 2>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else if (EULER && ee == 4) energy_e_launch<16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
+    // Euler: kf_energy_e also writes the moved-face s' kr_sweep reads (Slab::sF)
+    if (EULER) energy_e_launch<8, 2>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe == 15) energy_launch<EULER, 15, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 12) energy_launch<EULER, 12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);

@@ -952,6 +952,239 @@ __global__ void __launch_bounds__(256) kn_dt(Slab s, Phys p, int cur)
 }
 
 // ============================================================================
+// kr_sweep + kr_flux: the remap as two lean kernels (the alternative to the
+// pipelined kr_cells_p, whose carried state spills).
+//
+//   kr_sweep : z-march over cell planes; stages x', u' node planes; per column
+//              and plane the six ribbons and three moved faces of c.4 step 1
+//              (ribbons shared with the neighbouring faces as in kr_cells), the
+//              swept volumes dV of the cell's -x/-y/-z faces, and the donor data
+//              r = m/V', Ubar = 8-node mean of u' (c.4 step 2).  Writes
+//              Slab::dV, rD, UD.  Dependencies reach only the +x / +y neighbours,
+//              so a 32 x NW tile yields 31 x (NW-1) columns.
+//   kr_flux  : one thread per cell: the six face fluxes from dV and the donor
+//              data (c.4 step 2), the cell update (c.4 step 3).
+// Same expressions, operands and association as kr_cells / the oracle.
+// ============================================================================
+template <int NW>
+struct SweepCTA {
+    static constexpr int PL = NW * RW, TX = RW - 1, TY = NW - 1;
+    __host__ __device__ static constexpr int oN(int par, int c) { return (par * 6 + c) * PL; }  // x'(3) u'(3)
+    __host__ __device__ static constexpr int oR(int c) { return 12 * PL + c * PL; }           // Rxz Ryz Rzy Rzx
+    static constexpr int WORDS = 16 * PL + 2 * RPAD;
+
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, ix, iy, ta, tb, kr0, kr1;
+    long long nb, cb;
+    bool col_in, out_col;
+    double tx0, tx1, ty0, ty1;
+    D3 qx1, qu1;        // prefetch: node plane
+    double rxy_t, ryx_t;  // ribbons Rxy, Ryx of node plane t (own column)
+
+    __device__ __forceinline__ SweepCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kr0_, int kr1_,
+                                        int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        ix = threadIdx.x;
+        iy = threadIdx.y;
+        me = smem + RPAD + iy * RW + ix;
+        i = blockIdx.x * TX + ix;
+        j = blockIdx.y * TY + iy;
+        kr0 = kr0_;
+        kr1 = kr1_;
+        const int t0 = kr0 - 1 > 0 ? kr0 - 1 : 0, t1 = kr1 < p.nz - 1 ? kr1 : p.nz - 1;  // cell planes [t0, t1]
+        ta = t0 + blockIdx.z * zchunk;
+        tb = ta + zchunk - 1 < t1 ? ta + zchunk - 1 : t1;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        col_in = i <= p.nx && j <= p.ny;
+        out_col = i < p.nx && j < p.ny && ix < TX && iy < TY;
+        tx0 = col_in ? s.Xt[i] : 0.0;
+        tx1 = (col_in && i + 1 <= p.nx) ? s.Xt[i + 1] : 0.0;
+        ty0 = col_in ? s.Yt[j] : 0.0;
+        ty1 = (col_in && j + 1 <= p.ny) ? s.Yt[j + 1] : 0.0;
+    }
+
+    __device__ __forceinline__ static double fs(D3 Q0, D3 Q1, D3 Q2, D3 Q3)
+    {
+        return face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
+    }
+    __device__ __forceinline__ void fetch(int k)  // node plane k
+    {
+        qx1 = D3{0.0, 0.0, 0.0};
+        qu1 = qx1;
+        if (col_in && k >= 0 && k <= p.nz) {
+            const long long n = nb + (long long)k * s.pn;
+            qx1 = ld3(s.x1, n);
+            qu1 = ld3(s.u1, n);
+        }
+    }
+    template <int PAR>
+    __device__ __forceinline__ void put()
+    {
+        st3r(me, oN(PAR, 0), PL, qx1);
+        st3r(me, oN(PAR, 3), PL, qu1);
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 XL(int off) const { return ld3r(me + off, oN(PAR, 0), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 UL(int off) const { return ld3r(me + off, oN(PAR, 3), PL); }
+    // Rxy / Ryx of node plane k (parity PAR), own column
+    template <int PAR>
+    __device__ __forceinline__ void rib_xy(int k, double& rxy, double& ryx) const
+    {
+        rxy = 0.0;
+        ryx = 0.0;
+        if (col_in && k >= 0 && k <= p.nz) {
+            const double z = s.Zt[k - s.kb];
+            const D3 T = D3{tx0, ty0, z}, L = XL<PAR>(0);
+            if (j + 1 <= p.ny) rxy = fs(T, L, XL<PAR>(RW), D3{tx0, ty1, z});
+            if (i + 1 <= p.nx) ryx = fs(T, D3{tx1, ty0, z}, XL<PAR>(1), L);
+        }
+    }
+
+    template <int B0>
+    __device__ __forceinline__ void step(int t)
+    {
+        constexpr int B1 = B0 ^ 1;
+        // ---- P1: stage node plane t+1; prefetch t+2
+        put<B1>();
+        if (t < tb) fetch(t + 2);
+        __syncthreads();
+        // ---- P2: ribbons of this column, moved faces, donor data of cell (i,j,t)
+        double rxy_n, ryx_n;
+        rib_xy<B1>(t + 1, rxy_n, ryx_n);
+        double rxz = 0.0, ryz = 0.0, rzy = 0.0, rzx = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
+        if (col_in) {
+            const double z0 = s.Zt[t - s.kb], z1 = s.Zt[t + 1 - s.kb];
+            const D3 T0 = D3{tx0, ty0, z0}, T1 = D3{tx0, ty0, z1}, L0 = XL<B0>(0), L1 = XL<B1>(0);
+            rxz = fs(T0, T1, L1, L0);
+            ryz = fs(T0, L0, L1, T1);
+            if (j + 1 <= p.ny) rzy = fs(T0, D3{tx0, ty1, z0}, XL<B0>(RW), L0);
+            if (i + 1 <= p.nx) rzx = fs(T0, L0, XL<B0>(1), D3{tx1, ty0, z0});
+        }
+        if (out_col) {  // s' of the moved faces: evaluated by kf_energy_e (same nodes, same bits)
+            const long long n = nb + (long long)t * s.pn;
+            sx = s.sF[0][n];
+            sy = s.sF[1][n];
+            sz = s.sF[2][n];
+        }
+        me[oR(0)] = rxz;
+        me[oR(1)] = ryz;
+        me[oR(2)] = rzy;
+        me[oR(3)] = rzx;
+        const long long c = cb + (long long)t * s.pc;
+        if (out_col) {  // c.4 step 2 donor data: r = m / V', Ubar = 0.125 * (sum of u' in corner order)
+            D3 sum = UL<B0>(0);
+            sum = add(sum, UL<B0>(1));
+            sum = add(sum, UL<B0>(RW));
+            sum = add(sum, UL<B0>(RW + 1));
+            sum = add(sum, UL<B1>(0));
+            sum = add(sum, UL<B1>(1));
+            sum = add(sum, UL<B1>(RW));
+            sum = add(sum, UL<B1>(RW + 1));
+            st3(s.UD, c, scl(0.125, sum));
+            s.rD[c] = ddiv(s.m[cur][c], s.V1[c]);
+        }
+        __syncthreads();
+        // ---- P3: swept volumes of the cell's -x, -y, -z faces (interior faces only)
+        if (out_col && t >= kr0 && t <= kr1) {
+            if (t < kr1 && i >= 1) {
+                const double dV = ddiv(((((me[RW + oR(0)] - me[oR(0)]) + rxy_n) - rxy_t) + sx) - s.sT[0][c], 3.0);
+                s.dV[0][c] = dV;
+            }
+            if (t < kr1 && j >= 1) {
+                const double dV = ddiv(((((ryx_n - ryx_t) + me[1 + oR(1)]) - me[oR(1)]) + sy) - s.sT[1][c], 3.0);
+                s.dV[1][c] = dV;
+            }
+            if (t >= 1) {
+                const double dV = ddiv(((((me[1 + oR(2)] - me[oR(2)]) + me[RW + oR(3)]) - me[oR(3)]) + sz) - s.sT[2][c], 3.0);
+                s.dV[2][c] = dV;
+            }
+        }
+        rxy_t = rxy_n;
+        ryx_t = ryx_n;
+    }
+
+    __device__ __forceinline__ void run()
+    {
+        fetch(ta);
+        if (ta & 1) put<1>();
+        else put<0>();
+        fetch(ta + 1);
+        __syncthreads();
+        if (ta & 1) rib_xy<1>(ta, rxy_t, ryx_t);
+        else rib_xy<0>(ta, rxy_t, ryx_t);
+        for (int t = ta; t <= tb; ++t) {
+            if (t & 1) step<1>(t);
+            else step<0>(t);
+        }
+    }
+};
+
+template <int NW, int MB>
+__global__ void __launch_bounds__(RW * NW, MB) kr_sweep(Slab s, Phys p, int cur, int kr0, int kr1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    SweepCTA<NW> c(s, p, cur, smem, kr0, kr1, zchunk);
+    c.run();
+}
+
+// grid: x = ceil(nx / 32), y = ceil(ny / 8), z = cell planes [kr0, kr1)
+// All loads are independent of the swept volumes' signs (both candidate donors of
+// every face are loaded, the donor is selected afterwards), so they overlap.
+struct Donor {
+    double r, e;
+    D3 u;
+};
+__device__ __forceinline__ Donor donor_at(const Slab& s, long long d)
+{
+    return Donor{s.rD[d], s.e1[d], ld3(s.UD, d)};
+}
+__global__ void __launch_bounds__(256) kr_flux(Slab s, Phys p, int cur, int kr0)
+{
+    if (!s.st->active) return;
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, t = kr0 + blockIdx.z;
+    if (i >= p.nx || j >= p.ny) return;
+    const long long c = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (t - s.kb));
+    const long long sa[3] = {1, p.nx, s.pc};
+    const int ia[3] = {i, j, t}, na[3] = {p.nx, p.ny, p.nz};
+    const Donor own = donor_at(s, c);
+    // faces in the order of c.4 step 3: -x +x -y +y -z +z; boundary faces carry no flux
+    double mu[6], ep[6];
+    D3 pi[6];
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+        const int a = f >> 1;
+        const bool plus = f & 1;
+        const bool inner = plus ? ia[a] + 1 <= na[a] - 1 : ia[a] >= 1;  // a cell on both sides
+        const long long nbr = inner ? (plus ? c + sa[a] : c - sa[a]) : c;
+        const double dV = inner ? s.dV[a][plus ? nbr : c] : 0.0;  // the face is the -a face of the upper cell
+        const Donor other = donor_at(s, nbr);
+        // donor: the lower cell if the face moved toward +a (c.4 step 2)
+        const Donor& D = (dV > 0.0) == plus ? own : other;
+        mu[f] = inner ? D.r * dV : 0.0;
+        ep[f] = inner ? mu[f] * D.e : 0.0;
+        pi[f] = inner ? scl(mu[f], D.u) : D3{0.0, 0.0, 0.0};
+    }
+    const double dm = ((((mu[0] - mu[1]) + mu[2]) - mu[3]) + mu[4]) - mu[5];
+    const double dE = ((((ep[0] - ep[1]) + ep[2]) - ep[3]) + ep[4]) - ep[5];
+    const D3 dP = sub(add(sub(add(sub(pi[0], pi[1]), pi[2]), pi[3]), pi[4]), pi[5]);
+    const double m = s.m[cur][c], e1 = own.e;
+    const double m2 = m + dm;
+    if (t >= s.k0 && t < s.k1 && !(m2 > 0.0))
+        atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, t));
+    s.e[cur ^ 1][c] = e1 + ddiv(dE - (e1 * dm), m2);
+    s.m[cur ^ 1][c] = m2;
+    s.dm[c] = dm;
+    st3(s.dP, c, dP);
+}
+
+// ============================================================================
 namespace {
 inline int cdivr(int a, int b) { return (a + b - 1) / b; }
 constexpr int NW_RC = 8, NW_RN = 8, RZ = 32;
@@ -976,7 +1209,7 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
     const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     static const int variant = [] {
         const char* v = getenv("SALE_REMAP");
-        return v ? atoi(v) : 6;
+        return v ? atoi(v) : 8;
     }();
     if (variant == 0) {
         constexpr int NW = NW_RC;
@@ -1004,6 +1237,22 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
         cells_p_launch<8, 1>(s, p, cur, kr0, kr1, cs);
     } else if (variant == 4) {
         cells_p_launch<10, 1>(s, p, cur, kr0, kr1, cs);
+    } else if (variant >= 7) {
+        auto sweep = [&](auto kern, int nw, size_t words) {
+            static bool init = false;
+            if (!init) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * words));
+                init = true;
+            }
+            const int t0 = kr0 - 1 > 0 ? kr0 - 1 : 0, t1 = kr1 < p.nz - 1 ? kr1 : p.nz - 1;
+            dim3 grid(cdivr(p.nx, RW - 1), cdivr(p.ny, nw - 1), cdivr(t1 - t0 + 1, RZ));
+            kern<<<grid, dim3(RW, nw), sizeof(double) * words, cs>>>(s, p, cur, kr0, kr1, RZ);
+        };
+        if (variant == 7) sweep(kr_sweep<8, 2>, 8, SweepCTA<8>::WORDS);
+        else if (variant == 8) sweep(kr_sweep<8, 3>, 8, SweepCTA<8>::WORDS);
+        else if (variant == 9) sweep(kr_sweep<16, 1>, 16, SweepCTA<16>::WORDS);
+        else sweep(kr_sweep<12, 2>, 12, SweepCTA<12>::WORDS);
+        kr_flux<<<dim3(cdivr(p.nx, 32), cdivr(p.ny, 8), kr1 - kr0), dim3(32, 8), 0, cs>>>(s, p, cur, kr0);
     } else {
         if (variant == 5) cells_p_launch<14, 1>(s, p, cur, kr0, kr1, cs);
         else cells_p_launch<15, 1>(s, p, cur, kr0, kr1, cs);

@@ -166,6 +166,11 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
     s.e1 = euler ? take(nc) : nullptr;
     s.V1 = euler ? take(nc) : nullptr;
     s.dm = euler ? take(nc) : nullptr;
+    for (int a = 0; a < 3; ++a) {
+        s.dV[a] = euler ? take(nc) : nullptr;
+        s.UD[a] = euler ? take(nc) : nullptr;
+    }
+    s.rD = euler ? take(nc) : nullptr;
     s.der = take(s.pn * (long long)(s.k1 - s.k0 + 1));
     s.VT = euler ? take(nc) : nullptr;
     for (int a = 0; a < 3; ++a) s.sT[a] = euler ? take(nc) : nullptr;
@@ -174,6 +179,7 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
         s.TAy[a] = euler ? take((long long)p->nx * s.nzc) : nullptr;
         s.TAz[a] = euler ? take((long long)p->nx * p->ny) : nullptr;
     }
+    for (int a = 0; a < 3; ++a) s.sF[a] = euler ? take(nn) : nullptr;
     s.TJx = euler ? take(4LL * p->nx) : nullptr;
     s.TJy = euler ? take(4LL * p->ny) : nullptr;
     s.TJz = euler ? take(4LL * s.nzc) : nullptr;

@@ -50,6 +50,9 @@ struct Slab {
     double* V1;               // Euler scratch: V'
     double* dm;               // Euler scratch: Delta m
     double* dP[3];            // Euler scratch: Delta P
+    double* dV[3];            // Euler scratch: swept volume of the -x/-y/-z face of each cell (kr_sweep)
+    double* rD;               // Euler scratch: donor density m/V' of each cell (kr_sweep)
+    double* UD[3];            // Euler scratch: donor velocity (8-node mean of u') of each cell (kr_sweep)
     double* der;              // derive / staging scratch (node-plane sized)
     double* VT;               // Euler: target cell volume V^T (constant; set at create)
     double* sT[3];            // Euler: s of the target x/y/z face anchored at each cell (-a faces)
@@ -62,6 +65,9 @@ struct Slab {
     double* TAx[3];           // A of x-faces, index (k-kb)*ny + j  (independent of i)
     double* TAy[3];           // A of y-faces, index (k-kb)*nx + i  (independent of j)
     double* TAz[3];           // A of z-faces, index j*nx + i       (independent of k)
+    double* sF[3];            // Euler scratch: s' (c.2 s of the moved face) of the x-, y-, z-face
+                              // anchored at node (i,j,k), node-indexed; written by kf_energy_e
+                              // (which needs them for V'), read by kr_sweep's swept volumes
     double* TJx;              // cells i: d.x d.y d.z L at TJx[4*i + c] (x-axis jump)
     double* TJy;              // cells j (y-axis)
     double* TJz;              // cells at local plane k-kb (z-axis)
