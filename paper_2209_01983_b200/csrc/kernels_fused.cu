@@ -322,6 +322,7 @@ struct ForceEulerCTA {
     bool pxm, pxp, pym, pyp;
     D3 pu;  // prefetch: node u of plane k
     double pm, pe, pv;  // prefetch: cell m, e, V^T of plane k-1
+    D3 pax, pay;        // prefetch: x- / y-face area vectors of cell plane k-1 (tables)
     D3 zprev;  // Ubar of the z-face at node plane kz (the -z face of cell kz)
 
     __device__ __forceinline__ ForceEulerCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kn0_, int kn1_,
@@ -368,6 +369,11 @@ struct ForceEulerCTA {
             pe = s.e[cur][c];
             pv = s.VT[c];
         }
+        int kl = kc - s.kb;  // table plane, clamped into the slab (the value is unused outside)
+        kl = kl < 0 ? 0 : (kl >= s.nzc ? s.nzc - 1 : kl);
+        const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
+        pax = D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]};
+        pay = D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]};
     }
     template <int PAR>
     __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oU(PAR, 0), PL); }
@@ -419,6 +425,7 @@ struct ForceEulerCTA {
         // ---- P1: stage node plane kz+1 (u), cell (i,j,kz); prefetch the next
         st3s(me, oU(B1, 0), PL, pu);
         const double m = pm, e = pe, V = pv;
+        const D3 ax = pax, ay = pay;
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
         // ---- P2: face-average velocities of the three faces anchored here; A from the tables
@@ -428,9 +435,15 @@ struct ForceEulerCTA {
         st3s(me, oW(0, 0), PL, ux);
         st3s(me, oW(1, 0), PL, uy);
         const int kl = kz - s.kb;
-        const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
-        st3s(me, oA(B0, 0), PL, D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]});
-        st3s(me, oA(B0, 1), PL, D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]});
+        st3s(me, oA(B0, 0), PL, ax);
+        st3s(me, oA(B0, 1), PL, ay);
+        // the axis-jump constants of P3, loaded before the barrier
+        const double* TJ[3] = {s.TJx + 4 * ic, s.TJy + 4 * jc, s.TJz + 4 * kl};
+        double tj[3][4];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tj[a][c] = TJ[a][c];
         __syncthreads();
         // ---- P3: cell (i,j,kz): rho, EoS, q, sigma
         {
@@ -438,9 +451,9 @@ struct ForceEulerCTA {
             if (cellcol_in && kz >= 0 && kz < p.nz) {
                 double rho = ddiv(m, V), pr, pf, cs;
                 eos(p.gamma, rho, e, pr, pf, cs);
-                const double dx = jump(s.TJx + 4 * i, ux, ld3s(me + 1, oW(0, 0), PL));
-                const double dy = jump(s.TJy + 4 * j, uy, ld3s(me + FW, oW(1, 0), PL));
-                const double dz = jump(s.TJz + 4 * kl, zprev, uz);
+                const double dx = jump(tj[0], ux, ld3s(me + 1, oW(0, 0), PL));
+                const double dy = jump(tj[1], uy, ld3s(me + FW, oW(1, 0), PL));
+                const double dz = jump(tj[2], zprev, uz);
                 const double du = dmin(dmin(dx, dy), dz);
                 const double q = q_of_du(rho, cs, du, p.c1, p.c2);
                 sig = 0.25 * (pf + q);
@@ -972,7 +985,7 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     const int kc0 = kn0, kc1 = kn1;
     static const int fe = [] {
         const char* v = getenv("SALE_FORCE_E");
-        return v ? atoi(v) : 2;
+        return v ? atoi(v) : 1;
     }();
     if (EULER && fe == 1) force_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (EULER && fe == 2) force_e_launch<8, 3>(s, p, cur, kn0, kn1, tune.zc, cs);

@@ -978,7 +978,7 @@ struct SweepCTA {
     const int cur;
     double* me;
     int i, j, ix, iy, ta, tb, kr0, kr1;
-    long long nb, cb;
+    long long nb, cb, nbc, cbc;  // nbc / cbc: the column clamped into the mesh (always-valid addresses)
     bool col_in, out_col;
     double tx0, tx1, ty0, ty1;
     D3 qx1, qu1;        // prefetch: node plane
@@ -1002,6 +1002,11 @@ struct SweepCTA {
         cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
         col_in = i <= p.nx && j <= p.ny;
         out_col = i < p.nx && j < p.ny && ix < TX && iy < TY;
+        {
+            const int ic = i < p.nx ? i : p.nx - 1, jc = j < p.ny ? j : p.ny - 1;
+            nbc = (long long)ic + (long long)(p.nx + 1) * (jc - (long long)(p.ny + 1) * s.kb);
+            cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
+        }
         tx0 = col_in ? s.Xt[i] : 0.0;
         tx1 = (col_in && i + 1 <= p.nx) ? s.Xt[i + 1] : 0.0;
         ty0 = col_in ? s.Yt[j] : 0.0;
@@ -1055,9 +1060,15 @@ struct SweepCTA {
         if (t < tb) fetch(t + 2);
         __syncthreads();
         // ---- P2: ribbons of this column, moved faces, donor data of cell (i,j,t)
+        // (the s' / s^T operands of P3 are loaded first, from always-valid addresses,
+        // so their latency hides behind the ribbons)
+        const long long c = cb + (long long)t * s.pc;
+        const long long nL = nbc + (long long)t * s.pn, cL = cbc + (long long)t * s.pc;
+        const double sx = s.sF[0][nL], sy = s.sF[1][nL], sz = s.sF[2][nL];
+        const double sTx = s.sT[0][cL], sTy = s.sT[1][cL], sTz = s.sT[2][cL];
         double rxy_n, ryx_n;
         rib_xy<B1>(t + 1, rxy_n, ryx_n);
-        double rxz = 0.0, ryz = 0.0, rzy = 0.0, rzx = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
+        double rxz = 0.0, ryz = 0.0, rzy = 0.0, rzx = 0.0;
         if (col_in) {
             const double z0 = s.Zt[t - s.kb], z1 = s.Zt[t + 1 - s.kb];
             const D3 T0 = D3{tx0, ty0, z0}, T1 = D3{tx0, ty0, z1}, L0 = XL<B0>(0), L1 = XL<B1>(0);
@@ -1066,17 +1077,10 @@ struct SweepCTA {
             if (j + 1 <= p.ny) rzy = fs(T0, D3{tx0, ty1, z0}, XL<B0>(RW), L0);
             if (i + 1 <= p.nx) rzx = fs(T0, L0, XL<B0>(1), D3{tx1, ty0, z0});
         }
-        if (out_col) {  // s' of the moved faces: evaluated by kf_energy_e (same nodes, same bits)
-            const long long n = nb + (long long)t * s.pn;
-            sx = s.sF[0][n];
-            sy = s.sF[1][n];
-            sz = s.sF[2][n];
-        }
         me[oR(0)] = rxz;
         me[oR(1)] = ryz;
         me[oR(2)] = rzy;
         me[oR(3)] = rzx;
-        const long long c = cb + (long long)t * s.pc;
         if (out_col) {  // c.4 step 2 donor data: r = m / V', Ubar = 0.125 * (sum of u' in corner order)
             D3 sum = UL<B0>(0);
             sum = add(sum, UL<B0>(1));
@@ -1093,15 +1097,15 @@ struct SweepCTA {
         // ---- P3: swept volumes of the cell's -x, -y, -z faces (interior faces only)
         if (out_col && t >= kr0 && t <= kr1) {
             if (t < kr1 && i >= 1) {
-                const double dV = ddiv(((((me[RW + oR(0)] - me[oR(0)]) + rxy_n) - rxy_t) + sx) - s.sT[0][c], 3.0);
+                const double dV = ddiv(((((me[RW + oR(0)] - me[oR(0)]) + rxy_n) - rxy_t) + sx) - sTx, 3.0);
                 s.dV[0][c] = dV;
             }
             if (t < kr1 && j >= 1) {
-                const double dV = ddiv(((((ryx_n - ryx_t) + me[1 + oR(1)]) - me[oR(1)]) + sy) - s.sT[1][c], 3.0);
+                const double dV = ddiv(((((ryx_n - ryx_t) + me[1 + oR(1)]) - me[oR(1)]) + sy) - sTy, 3.0);
                 s.dV[1][c] = dV;
             }
             if (t >= 1) {
-                const double dV = ddiv(((((me[1 + oR(2)] - me[oR(2)]) + me[RW + oR(3)]) - me[oR(3)]) + sz) - s.sT[2][c], 3.0);
+                const double dV = ddiv(((((me[1 + oR(2)] - me[oR(2)]) + me[RW + oR(3)]) - me[oR(3)]) + sz) - sTz, 3.0);
                 s.dV[2][c] = dV;
             }
         }
@@ -1137,6 +1141,9 @@ __global__ void __launch_bounds__(RW * NW, MB) kr_sweep(Slab s, Phys p, int cur,
 // grid: x = ceil(nx / 32), y = ceil(ny / 8), z = cell planes [kr0, kr1)
 // All loads are independent of the swept volumes' signs (both candidate donors of
 // every face are loaded, the donor is selected afterwards), so they overlap.
+#ifndef KR_FLUX_MB
+#define KR_FLUX_MB 3
+#endif
 struct Donor {
     double r, e;
     D3 u;
@@ -1145,7 +1152,7 @@ __device__ __forceinline__ Donor donor_at(const Slab& s, long long d)
 {
     return Donor{s.rD[d], s.e1[d], ld3(s.UD, d)};
 }
-__global__ void __launch_bounds__(256) kr_flux(Slab s, Phys p, int cur, int kr0)
+__global__ void __launch_bounds__(256, KR_FLUX_MB) kr_flux(Slab s, Phys p, int cur, int kr0)
 {
     if (!s.st->active) return;
     const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, t = kr0 + blockIdx.z;
