@@ -266,6 +266,8 @@ __global__ void k_dt_candidate(Slab s, Phys p, int cur, int gate)
         }
         double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
         eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
+        s.rhoc[c] = rho;
+        s.csc[c] = cs;
         key = dt_key(dt_cell(p.cfl, l2, hex_max_speed2(U), cs));
     }
     block_min_atomic(key, &s.st->cand_key);

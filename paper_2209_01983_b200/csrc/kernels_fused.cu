@@ -92,7 +92,7 @@ struct ForceCTA {
     bool col_in, cellcol_in, node_out, sig_col;
     bool pxm, pxp, pym, pyp;
     D3 px, pu;  // prefetch registers
-    double pm, pe;
+    double pm, pe, prho, pcs;  // prefetch: cell m, e and (owned planes) the EoS cache
     FaceQ zprev;
 
     __device__ __forceinline__ ForceCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kn0_, int kn1_,
@@ -138,6 +138,10 @@ struct ForceCTA {
             long long c = cb + (long long)kc * s.pc;
             pm = mass_cur(s, p, cur)[c];
             pe = s.e[cur][c];
+            if (kc >= s.k0 && kc < s.k1) {
+                prho = s.rhoc[c];
+                pcs = s.csc[c];
+            }
         }
     }
     template <int PAR>
@@ -199,7 +203,7 @@ struct ForceCTA {
         constexpr int B1 = B0 ^ 1;
         // ---- P1: stage node plane kz+1 and cell (i,j,kz); prefetch the next
         put<B1>();
-        const double m = pm, e = pe;
+        const double m = pm, e = pe, crho = prho, ccs = pcs;
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
         // ---- P2: the three faces anchored at this column
@@ -225,10 +229,18 @@ struct ForceCTA {
             if (cellcol_in && kz >= 0 && kz < p.nz) {
                 const double* qx = me + 1;   // +x face (anchored at i+1)
                 const double* qy = me + FW;  // +y face (anchored at j+1)
-                double sv[6] = {fx.s, qx[oQ(0, 0)], fy.s, qy[oQ(1, 0)], zprev.s, zn.s};
-                double V = vol_from_s(sv);
-                double rho = ddiv(m, V), pr, pf, cs;
-                eos(p.gamma, rho, e, pr, pf, cs);
+                double rho, pf, cs;
+                if (kz >= s.k0 && kz < s.k1) {  // owned: rho, c from the EoS cache (c.5 pass, same state)
+                    rho = crho;
+                    cs = ccs;
+                    const double pr = ((p.gamma - 1.0) * rho) * e;
+                    pf = (pr > 0.0) ? pr : 0.0;
+                } else {
+                    double sv[6] = {fx.s, qx[oQ(0, 0)], fy.s, qy[oQ(1, 0)], zprev.s, zn.s};
+                    double V = vol_from_s(sv), pr;
+                    rho = ddiv(m, V);
+                    eos(p.gamma, rho, e, pr, pf, cs);
+                }
                 double dx = axis_jump(fx.Xb, ld3s(qx, oQ(0, 1), PL), fx.Ub, ld3s(qx, oQ(0, 4), PL));
                 double dy = axis_jump(fy.Xb, ld3s(qy, oQ(1, 1), PL), fy.Ub, ld3s(qy, oQ(1, 4), PL));
                 double dz = axis_jump(zprev.Xb, zn.Xb, zprev.Ub, zn.Ub);
@@ -663,6 +675,8 @@ struct EnergyCTA {
                 if (owned) {
                     double rho = ddiv(m, V1), pr, pf, cs;
                     eos(p.gamma, rho, e1, pr, pf, cs);
+                    s.rhoc[cc] = rho;
+                    s.csc[cc] = cs;
                     double l2 = dmin(dmin(me[oE(0)], me[FW + oE(0)]), dmin(me[oE(1)], me[1 + oE(1)]));
                     l2 = dmin(l2, dmin(dmin(me[oE(2)], me[1 + oE(2)]), dmin(me[FW + oE(2)], me[FW + 1 + oE(2)])));
                     double v2 = V2<B0>(0);

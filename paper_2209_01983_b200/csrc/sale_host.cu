@@ -158,6 +158,8 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
     s.e[0] = take(nc);
     s.e[1] = take(nc);
     s.sig = take(nc);
+    s.rhoc = take(nc);
+    s.csc = take(nc);
     for (int a = 0; a < 3; ++a) {
         s.x1[a] = euler ? take(nn) : nullptr;
         s.u1[a] = euler ? take(nn) : nullptr;

@@ -44,6 +44,9 @@ struct Slab {
     double* m[2];             // cell mass (Euler ping-pong; Lagrange uses m[0])
     double* e[2];             // specific internal energy (ping-pong)
     double* sig;              // v0 scratch: sigma per cell
+    double* rhoc;             // Lagrange EoS cache: rho and sound speed c of every owned cell at the
+    double* csc;              // state the last dt-candidate pass saw (kf_energy / the prologue pass
+                              // evaluate them for c.5); the next kf_force reuses them (same bits)
     double* x1[3];            // Euler scratch: x' (post-Lagrange positions)
     double* u1[3];            // Euler scratch: u'
     double* e1;               // Euler scratch: e'
