@@ -328,12 +328,16 @@ struct ForceEulerCTA {
     const int cur;
     double* me;
     int i, j, za, zb, kn0, kn1, ic, jc;  // ic, jc: i, j clamped into the cell range (table indices)
-    long long nb, cb;
+    long long nb, cb, nbc, cbc;  // nbc / cbc: the column clamped into the mesh (always-valid loads)
     double dt;
     bool col_in, cellcol_in, node_out, sig_col;
     bool pxm, pxp, pym, pyp;
-    D3 pu;  // prefetch: node u of plane k
-    double pm, pe, pv;  // prefetch: cell m, e, V^T of plane k-1
+    // prefetch registers.  Loads are unconditional (clamped addresses) and the
+    // out-of-mesh zero is selected where the value is consumed: a predicated load
+    // followed by a default write would make the write wait for the load.
+    D3 pu;  // node u of plane k
+    double pm, pe, pv;  // cell m, e, V^T of plane k-1
+    bool pnok, pcok;
     D3 pax, pay;        // prefetch: x- / y-face area vectors of cell plane k-1 (tables)
     D3 zprev;  // Ubar of the z-face at node plane kz (the -z face of cell kz)
 
@@ -353,6 +357,11 @@ struct ForceEulerCTA {
         zb = za + zchunk - 1 < kn1 ? za + zchunk - 1 : kn1;
         nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
         cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        {
+            const int in = i < 0 ? 0 : (i > p.nx ? p.nx : i), jn = j < 0 ? 0 : (j > p.ny ? p.ny : j);
+            nbc = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
+            cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
+        }
         dt = s.st->dt;
         col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
         cellcol_in = i >= 0 && i < p.nx && j >= 0 && j < p.ny;
@@ -369,20 +378,17 @@ struct ForceEulerCTA {
 
     __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
     {
-        pu = D3{0.0, 0.0, 0.0};
-        if (col_in && k >= 0 && k <= p.nz) pu = ld3(s.u[cur], nb + (long long)k * s.pn);
-        pm = 0.0;
-        pe = 0.0;
-        pv = 1.0;
+        pnok = col_in && k >= 0 && k <= p.nz;
+        const int kn = k < s.kb ? s.kb : (k > s.kb + s.nzn - 1 ? s.kb + s.nzn - 1 : k);
+        pu = ld3(s.u[cur], nbc + (long long)kn * s.pn);
         const int kc = k - 1;
-        if (cellcol_in && kc >= 0 && kc < p.nz) {
-            const long long c = cb + (long long)kc * s.pc;
-            pm = s.m[cur][c];
-            pe = s.e[cur][c];
-            pv = s.VT[c];
-        }
-        int kl = kc - s.kb;  // table plane, clamped into the slab (the value is unused outside)
+        pcok = cellcol_in && kc >= 0 && kc < p.nz;
+        int kl = kc - s.kb;  // cell / table plane clamped into the slab (values unused outside)
         kl = kl < 0 ? 0 : (kl >= s.nzc ? s.nzc - 1 : kl);
+        const long long c = cbc + (long long)(kl + s.kb) * s.pc;
+        pm = s.m[cur][c];
+        pe = s.e[cur][c];
+        pv = s.VT[c];
         const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
         pax = D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]};
         pay = D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]};
@@ -435,8 +441,8 @@ struct ForceEulerCTA {
     {
         constexpr int B1 = B0 ^ 1;
         // ---- P1: stage node plane kz+1 (u), cell (i,j,kz); prefetch the next
-        st3s(me, oU(B1, 0), PL, pu);
-        const double m = pm, e = pe, V = pv;
+        st3s(me, oU(B1, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
+        const double m = pcok ? pm : 0.0, e = pcok ? pe : 0.0, V = pcok ? pv : 1.0;
         const D3 ax = pax, ay = pay;
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
@@ -497,8 +503,8 @@ struct ForceEulerCTA {
     __device__ __forceinline__ void run()
     {
         fetch(za - 1);
-        if ((za - 1) & 1) st3s(me, oU(1, 0), PL, pu);
-        else st3s(me, oU(0, 0), PL, pu);
+        if ((za - 1) & 1) st3s(me, oU(1, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
+        else st3s(me, oU(0, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
         fetch(za);
         __syncthreads();
         zprev = ((za - 1) & 1) ? avg4(U<1>(0), U<1>(1), U<1>(FW + 1), U<1>(FW))
@@ -760,11 +766,13 @@ struct EnergyEulerCTA {
     const Phys& p;
     double* me;
     int i, j, za, zb, ic, jc;
-    long long nb, cb;
+    long long nb, cb, nbc, cbc;  // column clamped into the mesh (always-valid loads)
     double dt;
     bool col_in, cell_col, own_col;
-    D3 fu, fu1, fx1;  // prefetch registers
+    D3 fu, fu1, fx1;  // prefetch registers (unconditional loads, selected at use)
     double fm, fe, fs;
+    D3 fax, fay;      // prefetch: table A of the x- / y-face of cell plane k-1
+    bool fnok, fcok;
     double zs_prev;
 
     __device__ __forceinline__ EnergyEulerCTA(const Slab& s_, const Phys& p_, double* smem, int kc0, int kc1, int zchunk)
@@ -780,6 +788,11 @@ struct EnergyEulerCTA {
         zb = za + zchunk - 1 < kc1 - 1 ? za + zchunk - 1 : kc1 - 1;
         nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
         cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        {
+            const int in = i > p.nx ? p.nx : i, jn = j > p.ny ? p.ny : j;
+            nbc = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
+            cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
+        }
         dt = s.st->dt;
         col_in = i <= p.nx && j <= p.ny;
         cell_col = i < p.nx && j < p.ny && ix < TX && iy < TY;
@@ -790,31 +803,30 @@ struct EnergyEulerCTA {
 
     __device__ __forceinline__ void fetch(int k, int cur)  // node plane k, cell plane k-1
     {
-        fu = D3{0.0, 0.0, 0.0};
-        fu1 = fu;
-        fx1 = fu;
-        if (col_in && k >= 0 && k <= p.nz) {
-            const long long n = nb + (long long)k * s.pn;
-            fu = ld3(s.u[cur], n);
-            fu1 = ld3(s.u1, n);
-            fx1 = ld3(s.x1, n);
-        }
-        fm = 0.0;
-        fe = 0.0;
-        fs = 0.0;
+        fnok = col_in && k >= 0 && k <= p.nz;
+        const int kn = k < s.kb ? s.kb : (k > s.kb + s.nzn - 1 ? s.kb + s.nzn - 1 : k);
+        const long long n = nbc + (long long)kn * s.pn;
+        fu = ld3(s.u[cur], n);
+        fu1 = ld3(s.u1, n);
+        fx1 = ld3(s.x1, n);
         const int kc = k - 1;
-        if (cell_col && kc >= 0 && kc < p.nz) {
-            const long long c = cb + (long long)kc * s.pc;
-            fm = s.m[cur][c];
-            fe = s.e[cur][c];
-            fs = s.sig[c];
-        }
+        fcok = cell_col && kc >= 0 && kc < p.nz;
+        int kl = kc - s.kb;
+        kl = kl < 0 ? 0 : (kl >= s.nzc ? s.nzc - 1 : kl);
+        const long long c = cbc + (long long)(kl + s.kb) * s.pc;
+        fm = s.m[cur][c];
+        fe = s.e[cur][c];
+        fs = s.sig[c];
+        const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
+        fax = D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]};
+        fay = D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]};
     }
     template <int PAR>
     __device__ __forceinline__ void put()
     {
-        st3s(me, oP(PAR, 0), PL, fx1);
-        st3s(me, oP(PAR, 3), PL, scl(0.5, add(fu, fu1)));
+        const D3 z = D3{0.0, 0.0, 0.0};
+        st3s(me, oP(PAR, 0), PL, fnok ? fx1 : z);
+        st3s(me, oP(PAR, 3), PL, scl(0.5, add(fnok ? fu : z, fnok ? fu1 : z)));
     }
     template <int PAR>
     __device__ __forceinline__ D3 X1(int off) const { return ld3s(me + off, oP(PAR, 0), PL); }
@@ -832,20 +844,19 @@ struct EnergyEulerCTA {
     {
         constexpr int B1 = B0 ^ 1;
         put<B1>();
-        const double m = fm, e = fe, sig = fs;
+        const double m = fcok ? fm : 0.0, e = fcok ? fe : 0.0, sig = fcok ? fs : 0.0;
+        const D3 ax = fax, ay = fay;
         if (kz < zb) fetch(kz + 2, cur);
         __syncthreads();
         // ---- P2: s' of the moved x- and y-faces anchored here, A^n from the tables
-        const int kl = kz - s.kb;
-        const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
         const D3 Q0 = X1<B0>(0), Q1 = X1<B0>(FW), Q2 = X1<B1>(FW), Q3 = X1<B1>(0);
         const double sx = face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
         const D3 R2 = X1<B1>(1), R3 = X1<B0>(1);
         const double sy = face_s(avg4(Q0, Q3, R2, R3), face_area(Q0, Q3, R2, R3));
         const double zs_next = zs<B1>();
-        st3s(me, oF(0, 0), PL, D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]});
+        st3s(me, oF(0, 0), PL, ax);
         me[oF(0, 3)] = sx;
-        st3s(me, oF(1, 0), PL, D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]});
+        st3s(me, oF(1, 0), PL, ay);
         me[oF(1, 3)] = sy;
         if (own_col) {  // s' of the faces anchored at node (i,j,kz), for kr_sweep's swept volumes
             const long long n = nb + (long long)kz * s.pn;

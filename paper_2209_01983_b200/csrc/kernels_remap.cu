@@ -978,10 +978,13 @@ struct SweepCTA {
     const int cur;
     double* me;
     int i, j, ix, iy, ta, tb, kr0, kr1;
-    long long nb, cb, nbc, cbc;  // nbc / cbc: the column clamped into the mesh (always-valid addresses)
+    long long nb, cb, nbc, cbc;  // nbc / cbc: the column clamped into the cells (always-valid addresses)
+    long long nbn;               // the column clamped into the nodes
     bool col_in, out_col;
     double tx0, tx1, ty0, ty1;
-    D3 qx1, qu1;        // prefetch: node plane
+    D3 qx1, qu1;        // prefetch: node plane (unconditional loads, selected at use)
+    double qm, qv;      // prefetch: cell m, V' of the plane before
+    bool qnok;
     double rxy_t, ryx_t;  // ribbons Rxy, Ryx of node plane t (own column)
 
     __device__ __forceinline__ SweepCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kr0_, int kr1_,
@@ -1006,6 +1009,8 @@ struct SweepCTA {
             const int ic = i < p.nx ? i : p.nx - 1, jc = j < p.ny ? j : p.ny - 1;
             nbc = (long long)ic + (long long)(p.nx + 1) * (jc - (long long)(p.ny + 1) * s.kb);
             cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
+            const int in = i > p.nx ? p.nx : i, jn = j > p.ny ? p.ny : j;
+            nbn = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
         }
         tx0 = col_in ? s.Xt[i] : 0.0;
         tx1 = (col_in && i + 1 <= p.nx) ? s.Xt[i + 1] : 0.0;
@@ -1017,21 +1022,25 @@ struct SweepCTA {
     {
         return face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
     }
-    __device__ __forceinline__ void fetch(int k)  // node plane k
+    __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
     {
-        qx1 = D3{0.0, 0.0, 0.0};
-        qu1 = qx1;
-        if (col_in && k >= 0 && k <= p.nz) {
-            const long long n = nb + (long long)k * s.pn;
-            qx1 = ld3(s.x1, n);
-            qu1 = ld3(s.u1, n);
-        }
+        qnok = col_in && k >= 0 && k <= p.nz;
+        const int kn = k < s.kb ? s.kb : (k > s.kb + s.nzn - 1 ? s.kb + s.nzn - 1 : k);
+        const long long n = nbn + (long long)kn * s.pn;
+        qx1 = ld3(s.x1, n);
+        qu1 = ld3(s.u1, n);
+        int kc = k - 1;
+        kc = kc < s.kb ? s.kb : (kc > s.kb + s.nzc - 1 ? s.kb + s.nzc - 1 : kc);
+        const long long c = cbc + (long long)kc * s.pc;
+        qm = s.m[cur][c];
+        qv = s.V1[c];
     }
     template <int PAR>
     __device__ __forceinline__ void put()
     {
-        st3r(me, oN(PAR, 0), PL, qx1);
-        st3r(me, oN(PAR, 3), PL, qu1);
+        const D3 z = D3{0.0, 0.0, 0.0};
+        st3r(me, oN(PAR, 0), PL, qnok ? qx1 : z);
+        st3r(me, oN(PAR, 3), PL, qnok ? qu1 : z);
     }
     template <int PAR>
     __device__ __forceinline__ D3 XL(int off) const { return ld3r(me + off, oN(PAR, 0), PL); }
@@ -1055,8 +1064,9 @@ struct SweepCTA {
     __device__ __forceinline__ void step(int t)
     {
         constexpr int B1 = B0 ^ 1;
-        // ---- P1: stage node plane t+1; prefetch t+2
+        // ---- P1: stage node plane t+1 (its cell-plane t operands come with it); prefetch t+2
         put<B1>();
+        const double m = qm, V1 = qv;
         if (t < tb) fetch(t + 2);
         __syncthreads();
         // ---- P2: ribbons of this column, moved faces, donor data of cell (i,j,t)
@@ -1091,7 +1101,7 @@ struct SweepCTA {
             sum = add(sum, UL<B1>(RW));
             sum = add(sum, UL<B1>(RW + 1));
             st3(s.UD, c, scl(0.125, sum));
-            s.rD[c] = ddiv(s.m[cur][c], s.V1[c]);
+            s.rD[c] = ddiv(m, V1);
         }
         __syncthreads();
         // ---- P3: swept volumes of the cell's -x, -y, -z faces (interior faces only)
@@ -1216,7 +1226,7 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
     const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     static const int variant = [] {
         const char* v = getenv("SALE_REMAP");
-        return v ? atoi(v) : 8;
+        return v ? atoi(v) : 7;
     }();
     if (variant == 0) {
         constexpr int NW = NW_RC;
