@@ -39,8 +39,13 @@ ALGO_BYTES = {configs.LAGRANGE: 120.0, configs.EULER: 80.0}
 # algorithmic FP64-pipe instructions per zone-cycle of each kernel
 # class (faces / edges / nodes computed once; an IEEE fp64 div or sqrt = 8 FP64
 # instructions, its fast-path SASS sequence)
-ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 702.0, "remap": 0.0},
-             configs.EULER: {"lagrange": 601.0, "remap": 612.0}}
+# (Lagrange: the t^n EoS and volume are the previous cycle's t^{n+1} values, evaluated
+# once; Euler: the t^n geometry of the fixed target mesh is loop-invariant and the
+# moved-face s' of S7 are shared with R1 -- DESIGN.md §7)
+ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 661.0, "remap": 0.0},
+             configs.EULER: {"lagrange": 435.0, "remap": 507.0}}
+# kernel name prefixes of each timing class (for the ncu traffic file)
+CLASS_KERNELS = {"lagrange": ("kf_",), "remap": ("kr_", "kn_")}
 REASON_BITS = {"hw_slowdown": "hw_slowdown", "hw_thermal_slowdown": "hw_thermal_slowdown",
                "sw_thermal_slowdown": "sw_thermal_slowdown", "sw_power_cap": "sw_power_cap"}
 
@@ -52,6 +57,20 @@ def peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic(config_name: str, dom: str):
+    """DRAM bytes (read + write) per launch group of the dominant kernel class, from
+    the committed ncu --set full capture of this workload (profiles/traffic_<cfg>.json,
+    written by scripts/traffic_from_ncu.py); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"traffic_{config_name}.json")) as f:
+            d = json.load(f)
+        per = d["dram_bytes_per_launch"]
+        tot = sum(v for k, v in per.items() if k.startswith(CLASS_KERNELS[dom]))
+        return (tot if tot > 0 else None), d.get("source")
+    except Exception:
+        return None, None
 
 
 def fp64_peak():
@@ -277,8 +296,11 @@ def main():
     cyc_t = cyc_fp64 / (ms / args.steps * 1e-3) / 1e12
     cyc_bytes = ALGO_BYTES[mode] * local_cells
     cycle_gbs = cyc_bytes / (ms / args.steps * 1e-3) / 1e9
+    tr_bytes, tr_src = traffic(args.config, dom)
     roofline = {"bound": "alu", "achieved": achieved_t, "peak": fpk, "unit": "T fp64-instr/s",
-                "frac": achieved_t / fpk, "traffic": None, "kernel": dom,
+                "frac": achieved_t / fpk, "traffic": tr_bytes, "traffic_unit": "bytes per launch group",
+                "traffic_source": tr_src, "algo_bytes_per_launch_group": ALGO_BYTES[mode] * local_cells,
+                "kernel": dom,
                 "kernel_ms_per_launch": per_launch_ms, "kernel_share_of_step": dom_ms / ms,
                 "algo_fp64_instr_per_zone": ALGO_FP64[mode][dom], "peak_source": fpk_src,
                 "whole_cycle": {"achieved": cyc_t, "frac": cyc_t / fpk,
