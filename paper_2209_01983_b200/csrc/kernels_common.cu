@@ -126,6 +126,10 @@ __global__ void k_target_tables(Slab s, Phys p)
         out[2] = d.z;
         out[3] = dsqrt((d.x * d.x + d.y * d.y) + d.z * d.z);
     };
+    // dt numerator factors (c.5 on the target mesh: the edges of a cell are axis-aligned)
+    if (t < nx) s.TDx[t] = p.cfl * dsqrt(len2(D3{s.Xt[t], 0.0, 0.0}, D3{s.Xt[t + 1], 0.0, 0.0}));
+    if (t < ny) s.TDy[t] = p.cfl * dsqrt(len2(D3{0.0, s.Yt[t], 0.0}, D3{0.0, s.Yt[t + 1], 0.0}));
+    if (t < nzc) s.TDz[t] = p.cfl * dsqrt(len2(D3{0.0, 0.0, s.Zt[t]}, D3{0.0, 0.0, s.Zt[t + 1]}));
     const int k0 = kb;
     if (t < nx) {
         const int i = t;

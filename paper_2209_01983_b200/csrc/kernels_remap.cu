@@ -870,12 +870,13 @@ __global__ void __launch_bounds__(RW * NW, 2) kr_nodes(Slab s, Phys p, int cur, 
 // kn_update / kn_dt: R4 and the Euler dt candidate as two barrier-free kernels
 // (one thread per node / per cell, operands through L1; high occupancy).
 // ============================================================================
-// grid: x = ceil(nx+1 / 64) strips of 64 columns, y = ceil(ny+1 / 4) rows of 4, z = planes
+// grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane: no idle lanes), y = planes
 __global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
 {
     if (!s.st->active) return;
-    const int i = blockIdx.x * 64 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = s.k0 + blockIdx.z;
-    if (i > p.nx || j > p.ny) return;
+    const int t = blockIdx.x * 256 + threadIdx.x;
+    if (t >= (int)s.pn) return;
+    const int i = t % (p.nx + 1), j = t / (p.nx + 1), k = s.k0 + blockIdx.y;
     const bool pxm = i >= 1, pxp = i < p.nx, pym = j >= 1, pyp = j < p.ny, pzm = k >= 1, pzp = k < p.nz;
     const long long c00 = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
     const int sx = 1, sy = p.nx, sz = p.nx * p.ny;
@@ -912,22 +913,23 @@ __global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
     Dm = 0.125 * Dm;
     DP = scl(0.125, DP);
     M2 = 0.125 * M2;
-    const long long n = (long long)i + (long long)(p.nx + 1) * ((long long)j + (long long)(p.ny + 1) * (k - s.kb));
+    const long long n = (long long)t + s.pn * (long long)(k - s.kb);
     const D3 u1 = ld3(s.u1, n);
     D3 un = d3(u1.x + ddiv(DP.x - (u1.x * Dm), M2), u1.y + ddiv(DP.y - (u1.y * Dm), M2),
                u1.z + ddiv(DP.z - (u1.z * Dm), M2));
     un = reflect(p, i, j, k, un);
     st3(s.u[cur ^ 1], n, un);
-    s.x1[0][n] = speed2(un);  // |u''|^2 (x' scratch is free after kr_cells)
+    s.x1[0][n] = speed2(un);  // |u''|^2 (x' scratch is free after the remap's cell kernels)
 }
 
-// grid: x = ceil(nx / 64), y = ceil(ny / 4), z = owned cell planes
+// grid: x = ceil(nx*ny / 256) (flattened cell plane), y = owned cell planes
 __global__ void __launch_bounds__(256) kn_dt(Slab s, Phys p, int cur)
 {
     if (!s.st->active) return;
-    const int i = blockIdx.x * 64 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = s.k0 + blockIdx.z;
+    const int t = blockIdx.x * 256 + threadIdx.x, k = s.k0 + blockIdx.y;
     unsigned long long key = KEY_NONE;
-    if (i < p.nx && j < p.ny) {
+    if (t < (int)s.pc) {
+        const int i = t % p.nx, j = t / p.nx;
         const long long n0 = (long long)i + (long long)(p.nx + 1) * ((long long)j + (long long)(p.ny + 1) * (k - s.kb));
         const int pn = (p.nx + 1) * (p.ny + 1), rw = p.nx + 1;
         const double* __restrict__ v = s.x1[0] + n0;
@@ -939,14 +941,13 @@ __global__ void __launch_bounds__(256) kn_dt(Slab s, Phys p, int cur)
         v2 = dmax(v2, __ldg(v + pn + 1));
         v2 = dmax(v2, __ldg(v + pn + rw));
         v2 = dmax(v2, __ldg(v + pn + rw + 1));
-        // c.5 on the target mesh: the 12 edges of a target cell are axis-aligned
-        const double lx = len2(D3{s.Xt[i], 0.0, 0.0}, D3{s.Xt[i + 1], 0.0, 0.0});
-        const double ly = len2(D3{0.0, s.Yt[j], 0.0}, D3{0.0, s.Yt[j + 1], 0.0});
-        const double lz = len2(D3{0.0, 0.0, s.Zt[k - s.kb]}, D3{0.0, 0.0, s.Zt[k + 1 - s.kb]});
-        const long long c = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
+        const long long c = (long long)t + s.pc * (long long)(k - s.kb);
         double rho = ddiv(s.m[cur ^ 1][c], s.VT[c]), pr, pf, cs;
         eos(p.gamma, rho, s.e[cur ^ 1][c], pr, pf, cs);
-        key = dt_key(dt_cell(p.cfl, dmin(dmin(lx, ly), lz), v2, cs));
+        // c.5 on the target mesh: cfl * sqrt(min of the 12 axis-aligned edges^2) as the
+        // min of the per-axis tabled factors (monotone maps: same bits)
+        const double num = dmin(dmin(s.TDx[i], s.TDy[j]), s.TDz[k - s.kb]);
+        key = dt_key(ddiv(num, (cs + dsqrt(v2)) + 1e-30));
     }
     block_min_atomic(key, &s.st->cand_key);
 }
@@ -1289,8 +1290,8 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
         dim3 grid(cdivr(p.nx + 1, RW - 2), cdivr(p.ny + 1, NW - 2), cdivr(s.k1 - s.k0 + 1, RZ));
         kr_nodes<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, RZ);
     } else {
-        kn_update<<<dim3(cdivr(p.nx + 1, 64), cdivr(p.ny + 1, 4), s.k1 - s.k0 + 1), dim3(64, 4), 0, cs>>>(s, p, cur);
-        kn_dt<<<dim3(cdivr(p.nx, 64), cdivr(p.ny, 4), s.k1 - s.k0), dim3(64, 4), 0, cs>>>(s, p, cur);
+        kn_update<<<dim3(cdivr((int)s.pn, 256), s.k1 - s.k0 + 1), 256, 0, cs>>>(s, p, cur);
+        kn_dt<<<dim3(cdivr((int)s.pc, 256), s.k1 - s.k0), 256, 0, cs>>>(s, p, cur);
         return 3;
     }
     return 2;

@@ -182,6 +182,9 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
         s.TAz[a] = euler ? take((long long)p->nx * p->ny) : nullptr;
     }
     for (int a = 0; a < 3; ++a) s.sF[a] = euler ? take(nn) : nullptr;
+    s.TDx = euler ? take(p->nx) : nullptr;
+    s.TDy = euler ? take(p->ny) : nullptr;
+    s.TDz = euler ? take(s.nzc) : nullptr;
     s.TJx = euler ? take(4LL * p->nx) : nullptr;
     s.TJy = euler ? take(4LL * p->ny) : nullptr;
     s.TJz = euler ? take(4LL * s.nzc) : nullptr;

@@ -71,6 +71,9 @@ struct Slab {
     double* sF[3];            // Euler scratch: s' (c.2 s of the moved face) of the x-, y-, z-face
                               // anchored at node (i,j,k), node-indexed; written by kf_energy_e
                               // (which needs them for V'), read by kr_sweep's swept volumes
+    double* TDx;              // cells i: cfl * sqrt(edge length^2 along x) of the target mesh (c.5);
+    double* TDy;              //   the dt numerator cfl*sqrt(min(lx,ly,lz)) = min of these (sqrt and
+    double* TDz;              //   the positive scaling are monotone, so the same bits)
     double* TJx;              // cells i: d.x d.y d.z L at TJx[4*i + c] (x-axis jump)
     double* TJy;              // cells j (y-axis)
     double* TJz;              // cells at local plane k-kb (z-axis)
