@@ -337,9 +337,12 @@ struct ForceEulerCTA {
     // followed by a default write would make the write wait for the load.
     D3 pu;  // node u of plane k
     double pm, pe, pv;  // cell m, e, V^T of plane k-1
+    double pz;          // Z of node plane k
+    double xi, yj;      // X_i, Y_j of this column (clamped)
     bool pnok, pcok;
     D3 pax, pay;        // prefetch: x- / y-face area vectors of cell plane k-1 (tables)
     D3 zprev;  // Ubar of the z-face at node plane kz (the -z face of cell kz)
+    double zc;  // Z of node plane kz
 
     __device__ __forceinline__ ForceEulerCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kn0_, int kn1_,
                                              int zchunk)
@@ -366,6 +369,8 @@ struct ForceEulerCTA {
         col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
         cellcol_in = i >= 0 && i < p.nx && j >= 0 && j < p.ny;
         node_out = col_in && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY;
+        xi = s.Xt[i < 0 ? 0 : (i > p.nx ? p.nx : i)];
+        yj = s.Yt[j < 0 ? 0 : (j > p.ny ? p.ny : j)];
         sig_col = cellcol_in && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY;
         pxm = i >= 1 && i <= p.nx;
         pxp = i >= 0 && i < p.nx;
@@ -381,6 +386,7 @@ struct ForceEulerCTA {
         pnok = col_in && k >= 0 && k <= p.nz;
         const int kn = k < s.kb ? s.kb : (k > s.kb + s.nzn - 1 ? s.kb + s.nzn - 1 : k);
         pu = ld3(s.u[cur], nbc + (long long)kn * s.pn);
+        pz = s.Zt[kn - s.kb];
         const int kc = k - 1;
         pcok = cellcol_in && kc >= 0 && kc < p.nz;
         int kl = kc - s.kb;  // cell / table plane clamped into the slab (values unused outside)
@@ -443,6 +449,7 @@ struct ForceEulerCTA {
         // ---- P1: stage node plane kz+1 (u), cell (i,j,kz); prefetch the next
         st3s(me, oU(B1, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
         const double m = pcok ? pm : 0.0, e = pcok ? pe : 0.0, V = pcok ? pv : 1.0;
+        const double z1 = pz;  // Z of node plane kz+1
         const D3 ax = pax, ay = pay;
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
@@ -481,6 +488,8 @@ struct ForceEulerCTA {
             me[oS(B0, 1)] = m;
         }
         zprev = uz;
+        const double zcur = zc;  // Z of node plane kz (P4)
+        zc = z1;
         __syncthreads();
         // ---- P4: node (i,j,kz): force + mass gather, kinematics, BC, move
         if (node_out && kz >= za) {
@@ -490,7 +499,7 @@ struct ForceEulerCTA {
             if (pxm && pxp && pym && pyp && pzm && pzp) gather<B0, true>(F, M, true, true);
             else gather<B0, false>(F, M, pzm, pzp);
             M = 0.125 * M;
-            const D3 u = U<B0>(0), x = D3{s.Xt[i], s.Yt[j], s.Zt[kl]};
+            const D3 u = U<B0>(0), x = D3{xi, yj, zcur};
             D3 un = d3(u.x + (ddiv(F.x, M) * dt), u.y + (ddiv(F.y, M) * dt), u.z + (ddiv(F.z, M) * dt));
             un = reflect(p, i, j, kz, un);
             const D3 xn = d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt));
@@ -505,6 +514,7 @@ struct ForceEulerCTA {
         fetch(za - 1);
         if ((za - 1) & 1) st3s(me, oU(1, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
         else st3s(me, oU(0, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
+        zc = pz;
         fetch(za);
         __syncthreads();
         zprev = ((za - 1) & 1) ? avg4(U<1>(0), U<1>(1), U<1>(FW + 1), U<1>(FW))

@@ -985,6 +985,8 @@ struct SweepCTA {
     double tx0, tx1, ty0, ty1;
     D3 qx1, qu1;        // prefetch: node plane (unconditional loads, selected at use)
     double qm, qv;      // prefetch: cell m, V' of the plane before
+    double qz;          // prefetch: Z of node plane k
+    double zprev;       // Z of node plane t
     bool qnok;
     double rxy_t, ryx_t;  // ribbons Rxy, Ryx of node plane t (own column)
 
@@ -1035,6 +1037,7 @@ struct SweepCTA {
         const long long c = cbc + (long long)kc * s.pc;
         qm = s.m[cur][c];
         qv = s.V1[c];
+        qz = s.Zt[kn - s.kb];
     }
     template <int PAR>
     __device__ __forceinline__ void put()
@@ -1049,12 +1052,11 @@ struct SweepCTA {
     __device__ __forceinline__ D3 UL(int off) const { return ld3r(me + off, oN(PAR, 3), PL); }
     // Rxy / Ryx of node plane k (parity PAR), own column
     template <int PAR>
-    __device__ __forceinline__ void rib_xy(int k, double& rxy, double& ryx) const
+    __device__ __forceinline__ void rib_xy(int k, double z, double& rxy, double& ryx) const
     {
         rxy = 0.0;
         ryx = 0.0;
         if (col_in && k >= 0 && k <= p.nz) {
-            const double z = s.Zt[k - s.kb];
             const D3 T = D3{tx0, ty0, z}, L = XL<PAR>(0);
             if (j + 1 <= p.ny) rxy = fs(T, L, XL<PAR>(RW), D3{tx0, ty1, z});
             if (i + 1 <= p.nx) ryx = fs(T, D3{tx1, ty0, z}, XL<PAR>(1), L);
@@ -1067,7 +1069,7 @@ struct SweepCTA {
         constexpr int B1 = B0 ^ 1;
         // ---- P1: stage node plane t+1 (its cell-plane t operands come with it); prefetch t+2
         put<B1>();
-        const double m = qm, V1 = qv;
+        const double m = qm, V1 = qv, z0 = zprev, z1 = qz;
         if (t < tb) fetch(t + 2);
         __syncthreads();
         // ---- P2: ribbons of this column, moved faces, donor data of cell (i,j,t)
@@ -1078,10 +1080,9 @@ struct SweepCTA {
         const double sx = s.sF[0][nL], sy = s.sF[1][nL], sz = s.sF[2][nL];
         const double sTx = s.sT[0][cL], sTy = s.sT[1][cL], sTz = s.sT[2][cL];
         double rxy_n, ryx_n;
-        rib_xy<B1>(t + 1, rxy_n, ryx_n);
+        rib_xy<B1>(t + 1, z1, rxy_n, ryx_n);
         double rxz = 0.0, ryz = 0.0, rzy = 0.0, rzx = 0.0;
         if (col_in) {
-            const double z0 = s.Zt[t - s.kb], z1 = s.Zt[t + 1 - s.kb];
             const D3 T0 = D3{tx0, ty0, z0}, T1 = D3{tx0, ty0, z1}, L0 = XL<B0>(0), L1 = XL<B1>(0);
             rxz = fs(T0, T1, L1, L0);
             ryz = fs(T0, L0, L1, T1);
@@ -1122,6 +1123,7 @@ struct SweepCTA {
         }
         rxy_t = rxy_n;
         ryx_t = ryx_n;
+        zprev = z1;
     }
 
     __device__ __forceinline__ void run()
@@ -1129,10 +1131,11 @@ struct SweepCTA {
         fetch(ta);
         if (ta & 1) put<1>();
         else put<0>();
+        zprev = qz;
         fetch(ta + 1);
         __syncthreads();
-        if (ta & 1) rib_xy<1>(ta, rxy_t, ryx_t);
-        else rib_xy<0>(ta, rxy_t, ryx_t);
+        if (ta & 1) rib_xy<1>(ta, zprev, rxy_t, ryx_t);
+        else rib_xy<0>(ta, zprev, rxy_t, ryx_t);
         for (int t = ta; t <= tb; ++t) {
             if (t & 1) step<1>(t);
             else step<0>(t);
