@@ -536,6 +536,175 @@ __global__ void __launch_bounds__(FW * NW, MB) kf_force_e(Slab s, Phys p, int cu
 }
 
 // ============================================================================
+// Euler mode, split form of kf_force_e (SALE_FORCE_E=9):
+//   kf_sigma_e : z-march; face-average velocities of the three faces anchored at a
+//                column, then EoS + q + sigma of the cell (S2, S3).  Dependencies
+//                reach only the +x / +y neighbours: a 32 x NW tile yields
+//                31 x (NW-1) cells.  Writes sigma.
+//   kn_force_e : one thread per node: the corner-force and mass gather in the
+//                fixed order of c.2 with the target face areas from the tables,
+//                kinematics + reflecting BC (S5, S6).  Writes u', x'.
+// ============================================================================
+template <int NW>
+struct SigmaEulerCTA {
+    static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
+    __host__ __device__ static constexpr int oU(int par, int c) { return (par * 3 + c) * PL; }       // node u
+    __host__ __device__ static constexpr int oW(int xy, int c) { return 6 * PL + (xy * 3 + c) * PL; }  // x/y face Ubar
+    static constexpr int WORDS = 12 * PL + 2 * PAD;
+
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, za, zb, kc0, kc1, ic, jc;
+    long long nbn, cb, cbc;
+    bool col_in, out_cell;
+    D3 pu;
+    double pm, pe, pv;
+    bool pnok;
+    D3 zprev;
+
+    __device__ __forceinline__ SigmaEulerCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kc0_, int kc1_,
+                                             int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + PAD + iy * FW + ix;
+        i = blockIdx.x * TX + ix;
+        j = blockIdx.y * TY + iy;
+        ic = i < p.nx ? i : p.nx - 1;
+        jc = j < p.ny ? j : p.ny - 1;
+        kc0 = kc0_;
+        kc1 = kc1_;
+        za = kc0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kc1 - 1 ? za + zchunk - 1 : kc1 - 1;
+        const int in = i < p.nx ? i : p.nx, jn = j < p.ny ? j : p.ny;
+        nbn = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
+        col_in = i <= p.nx && j <= p.ny;
+        out_cell = i < p.nx && j < p.ny && ix < TX && iy < TY;
+    }
+    __device__ __forceinline__ void fetch(int k)  // node plane k (u), cell plane k-1 (m, e, V^T)
+    {
+        pnok = col_in && k >= 0 && k <= p.nz;
+        const int kn = k < s.kb ? s.kb : (k > s.kb + s.nzn - 1 ? s.kb + s.nzn - 1 : k);
+        pu = ld3(s.u[cur], nbn + (long long)kn * s.pn);
+        int kc = k - 1;
+        kc = kc < s.kb ? s.kb : (kc > s.kb + s.nzc - 1 ? s.kb + s.nzc - 1 : kc);
+        const long long c = cbc + (long long)kc * s.pc;
+        pm = s.m[cur][c];
+        pe = s.e[cur][c];
+        pv = s.VT[c];
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oU(PAR, 0), PL); }
+    __device__ __forceinline__ static double jump(const double* T, D3 Um, D3 Up)
+    {
+        const D3 w = sub(Up, Um);
+        return ddiv((w.x * T[0] + w.y * T[1]) + w.z * T[2], T[3]);
+    }
+
+    template <int B0>
+    __device__ __forceinline__ void step(int kz)
+    {
+        constexpr int B1 = B0 ^ 1;
+        st3s(me, oU(B1, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
+        const double m = pm, e = pe, V = pv;
+        if (kz < zb) fetch(kz + 2);
+        __syncthreads();
+        const D3 ux = avg4(U<B0>(0), U<B0>(FW), U<B1>(FW), U<B1>(0));
+        const D3 uy = avg4(U<B0>(0), U<B1>(0), U<B1>(1), U<B0>(1));
+        const D3 uz = avg4(U<B1>(0), U<B1>(1), U<B1>(FW + 1), U<B1>(FW));
+        st3s(me, oW(0, 0), PL, ux);
+        st3s(me, oW(1, 0), PL, uy);
+        const int kl = kz - s.kb;
+        const double* TJ[3] = {s.TJx + 4 * ic, s.TJy + 4 * jc, s.TJz + 4 * kl};
+        double tj[3][4];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tj[a][c] = TJ[a][c];
+        __syncthreads();
+        if (out_cell && kz >= 0 && kz < p.nz) {
+            double rho = ddiv(m, V), pr, pf, cs;
+            eos(p.gamma, rho, e, pr, pf, cs);
+            const double dx = jump(tj[0], ux, ld3s(me + 1, oW(0, 0), PL));
+            const double dy = jump(tj[1], uy, ld3s(me + FW, oW(1, 0), PL));
+            const double dz = jump(tj[2], zprev, uz);
+            const double du = dmin(dmin(dx, dy), dz);
+            const double q = q_of_du(rho, cs, du, p.c1, p.c2);
+            s.sig[cb + (long long)kz * s.pc] = 0.25 * (pf + q);
+        }
+        zprev = uz;
+    }
+
+    __device__ __forceinline__ void run()
+    {
+        fetch(za);
+        if (za & 1) st3s(me, oU(1, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
+        else st3s(me, oU(0, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
+        fetch(za + 1);
+        __syncthreads();
+        zprev = (za & 1) ? avg4(U<1>(0), U<1>(1), U<1>(FW + 1), U<1>(FW)) : avg4(U<0>(0), U<0>(1), U<0>(FW + 1), U<0>(FW));
+        for (int kz = za; kz <= zb; ++kz) {
+            if (kz & 1) step<1>(kz);
+            else step<0>(kz);
+        }
+    }
+};
+
+template <int NW, int MB>
+__global__ void __launch_bounds__(FW * NW, MB) kf_sigma_e(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    SigmaEulerCTA<NW> c(s, p, cur, smem, kc0, kc1, zchunk);
+    c.run();
+}
+
+// grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane), y = node planes [kn0, kn1]
+__global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int kn0)
+{
+    if (!s.st->active) return;
+    const int t = blockIdx.x * 256 + threadIdx.x;
+    if (t >= (int)s.pn) return;
+    const int i = t % (p.nx + 1), j = t / (p.nx + 1), k = kn0 + blockIdx.y;
+    const bool pxm = i >= 1, pxp = i < p.nx, pym = j >= 1, pyp = j < p.ny, pzm = k >= 1, pzp = k < p.nz;
+    const long long c11 = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
+    const double dt = s.st->dt;
+    D3 F = D3{0.0, 0.0, 0.0};
+    double M = 0.0;
+    bool first = true;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
+        const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
+        if (!pres) continue;
+        const int ci = i - 1 + ap, cj = j - 1 + bp, ckl = k - 1 + cp - s.kb;
+        const long long tx = (long long)ckl * p.ny + cj, ty = (long long)ckl * p.nx + ci, tz = (long long)cj * p.nx + ci;
+        const D3 Ax = D3{__ldg(s.TAx[0] + tx), __ldg(s.TAx[1] + tx), __ldg(s.TAx[2] + tx)};
+        const D3 Ay = D3{__ldg(s.TAy[0] + ty), __ldg(s.TAy[1] + ty), __ldg(s.TAy[2] + ty)};
+        const D3 Az = D3{__ldg(s.TAz[0] + tz), __ldg(s.TAz[1] + tz), __ldg(s.TAz[2] + tz)};
+        // cell (i-1+ap, j-1+bp, k-1+cp): the node is its corner (1-ap, 1-bp, 1-cp)
+        const D3 C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
+        const long long c = c11 + (ap - 1) + (long long)p.nx * (bp - 1) + s.pc * (cp - 1);
+        const D3 term = scl(__ldg(s.sig + c), C);
+        const double mk = __ldg(s.m[cur] + c);
+        F = first ? term : add(F, term);
+        M = first ? mk : M + mk;
+        first = false;
+    }
+    M = 0.125 * M;
+    const long long n = (long long)t + s.pn * (long long)(k - s.kb);
+    const D3 u = ld3(s.u[cur], n), x = D3{s.Xt[i], s.Yt[j], s.Zt[k - s.kb]};
+    D3 un = d3(u.x + (ddiv(F.x, M) * dt), u.y + (ddiv(F.y, M) * dt), u.z + (ddiv(F.z, M) * dt));
+    un = reflect(p, i, j, k, un);
+    st3(s.u1, n, un);
+    st3(s.x1, n, d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt)));
+}
+
+// ============================================================================
 // kf_energy
 // ============================================================================
 template <bool EULER, int NW>
@@ -1003,6 +1172,19 @@ static void energy_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int 
     kf_energy_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
 }
 
+template <int NW, int MB>
+static void sigma_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
+{
+    const size_t sm = sizeof(double) * SigmaEulerCTA<NW>::WORDS;
+    static bool init = false;
+    if (!init) {
+        set_smem(kf_sigma_e<NW, MB>, sm);
+        init = true;
+    }
+    dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
+    kf_sigma_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
+}
+
 template <bool EULER>
 static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
@@ -1020,9 +1202,18 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     const int kc0 = kn0, kc1 = kn1;
     static const int fe = [] {
         const char* v = getenv("SALE_FORCE_E");
-        return v ? atoi(v) : 1;
+        return v ? atoi(v) : 12;
     }();
-    if (EULER && fe == 1) force_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
+    int extra = 0;
+    if (EULER && fe >= 9) {  // split form: sigma of cell planes [kn0-1, kn1], then the node kernel
+        const int sc0 = kn0 - 1 > 0 ? kn0 - 1 : 0, sc1 = kn1 + 1 < p.nz ? kn1 + 1 : p.nz;
+        if (fe == 9) sigma_e_launch<8, 3>(s, p, cur, sc0, sc1, tune.zc, cs);
+        else if (fe == 10) sigma_e_launch<8, 4>(s, p, cur, sc0, sc1, tune.zc, cs);
+        else if (fe == 12) sigma_e_launch<8, 2>(s, p, cur, sc0, sc1, tune.zc, cs);
+        else sigma_e_launch<16, 2>(s, p, cur, sc0, sc1, tune.zc, cs);
+        kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, cs>>>(s, p, cur, kn0);
+        extra = 1;
+    } else if (EULER && fe == 1) force_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (EULER && fe == 2) force_e_launch<8, 3>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (EULER && fe == 3) force_e_launch<12, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (EULER && fe == 4) force_e_launch<16, 1>(s, p, cur, kn0, kn1, tune.zc, cs);
@@ -1036,7 +1227,7 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     else if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 12) energy_launch<EULER, 12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else energy_launch<EULER, 8, MINB>(s, p, cur, kc0, kc1, tune.zc, cs);
-    return 2;
+    return 2 + extra;
 }
 
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
