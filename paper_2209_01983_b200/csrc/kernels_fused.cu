@@ -563,6 +563,7 @@ struct SigmaEulerCTA {
     double pm, pe, pv;
     bool pnok;
     D3 zprev;
+    unsigned long long key;  // running min of the owned cells' dt keys (c.5)
 
     __device__ __forceinline__ SigmaEulerCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kc0_, int kc1_,
                                              int zchunk)
@@ -584,6 +585,7 @@ struct SigmaEulerCTA {
         cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
         col_in = i <= p.nx && j <= p.ny;
         out_cell = i < p.nx && j < p.ny && ix < TX && iy < TY;
+        key = KEY_NONE;
     }
     __device__ __forceinline__ void fetch(int k)  // node plane k (u), cell plane k-1 (m, e, V^T)
     {
@@ -618,6 +620,16 @@ struct SigmaEulerCTA {
         const D3 uz = avg4(U<B1>(0), U<B1>(1), U<B1>(FW + 1), U<B1>(FW));
         st3s(me, oW(0, 0), PL, ux);
         st3s(me, oW(1, 0), PL, uy);
+        // max node speed^2 of the cell in corner order (read here, before the barrier:
+        // the next step's P1 overwrites the plane-kz slot)
+        double v2 = speed2(U<B0>(0));
+        v2 = dmax(v2, speed2(U<B0>(1)));
+        v2 = dmax(v2, speed2(U<B0>(FW)));
+        v2 = dmax(v2, speed2(U<B0>(FW + 1)));
+        v2 = dmax(v2, speed2(U<B1>(0)));
+        v2 = dmax(v2, speed2(U<B1>(1)));
+        v2 = dmax(v2, speed2(U<B1>(FW)));
+        v2 = dmax(v2, speed2(U<B1>(FW + 1)));
         const int kl = kz - s.kb;
         const double* TJ[3] = {s.TJx + 4 * ic, s.TJy + 4 * jc, s.TJz + 4 * kl};
         double tj[3][4];
@@ -635,6 +647,13 @@ struct SigmaEulerCTA {
             const double du = dmin(dmin(dx, dy), dz);
             const double q = q_of_du(rho, cs, du, p.c1, p.c2);
             s.sig[cb + (long long)kz * s.pc] = 0.25 * (pf + q);
+            if (kz >= s.k0 && kz < s.k1) {
+                // c.5 dt candidate of this (cycle-start) state: v2 (P2), cfl * sqrt(min
+                // edge^2) from the per-axis tables (as kn_dt)
+                const double num = dmin(dmin(s.TDx[ic], s.TDy[jc]), s.TDz[kl]);
+                const unsigned long long kk = dt_key(ddiv(num, (cs + dsqrt(v2)) + 1e-30));
+                key = kk < key ? kk : key;
+            }
         }
         zprev = uz;
     }
@@ -651,13 +670,15 @@ struct SigmaEulerCTA {
             if (kz & 1) step<1>(kz);
             else step<0>(kz);
         }
+        block_min_atomic(key, &s.st->cand_key);
     }
 };
 
+// gate = 0 for the first cycle of a sale_step call (DevState.active is still 0 there)
 template <int NW, int MB>
-__global__ void __launch_bounds__(FW * NW, MB) kf_sigma_e(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
+__global__ void __launch_bounds__(FW * NW, MB) kf_sigma_e(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk, int gate)
 {
-    if (!s.st->active) return;
+    if (gate && !s.st->active) return;
     extern __shared__ double smem[];
     SigmaEulerCTA<NW> c(s, p, cur, smem, kc0, kc1, zchunk);
     c.run();
@@ -1173,7 +1194,7 @@ static void energy_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int 
 }
 
 template <int NW, int MB>
-static void sigma_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
+static void sigma_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, int gate, cudaStream_t cs)
 {
     const size_t sm = sizeof(double) * SigmaEulerCTA<NW>::WORDS;
     static bool init = false;
@@ -1182,7 +1203,7 @@ static void sigma_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int k
         init = true;
     }
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
-    kf_sigma_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
+    kf_sigma_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc, gate);
 }
 
 template <bool EULER>
@@ -1204,15 +1225,8 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
         const char* v = getenv("SALE_FORCE_E");
         return v ? atoi(v) : 12;
     }();
-    int extra = 0;
-    if (EULER && fe >= 9) {  // split form: sigma of cell planes [kn0-1, kn1], then the node kernel
-        const int sc0 = kn0 - 1 > 0 ? kn0 - 1 : 0, sc1 = kn1 + 1 < p.nz ? kn1 + 1 : p.nz;
-        if (fe == 9) sigma_e_launch<8, 3>(s, p, cur, sc0, sc1, tune.zc, cs);
-        else if (fe == 10) sigma_e_launch<8, 4>(s, p, cur, sc0, sc1, tune.zc, cs);
-        else if (fe == 12) sigma_e_launch<8, 2>(s, p, cur, sc0, sc1, tune.zc, cs);
-        else sigma_e_launch<16, 2>(s, p, cur, sc0, sc1, tune.zc, cs);
+    if (EULER && fe >= 9) {  // split form: kf_sigma_e ran before the cycle's k_begin (euler_pre)
         kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, cs>>>(s, p, cur, kn0);
-        extra = 1;
     } else if (EULER && fe == 1) force_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (EULER && fe == 2) force_e_launch<8, 3>(s, p, cur, kn0, kn1, tune.zc, cs);
     else if (EULER && fe == 3) force_e_launch<12, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
@@ -1227,7 +1241,26 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     else if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 12) energy_launch<EULER, 12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else energy_launch<EULER, 8, MINB>(s, p, cur, kc0, kc1, tune.zc, cs);
-    return 2 + extra;
+    return 2;
+}
+
+// Euler, split force: sigma (and the cycle-start dt candidate, which replaces the
+// remap's kn_dt pass) of cell planes [kn0-1, kn1], launched before k_begin
+bool euler_pre_sigma()
+{
+    static const int fe = [] {
+        const char* v = getenv("SALE_FORCE_E");
+        return v ? atoi(v) : 12;
+    }();
+    return fe >= 9;
+}
+int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
+{
+    static const Tune tune;
+    const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
+    const int sc0 = kn0 - 1 > 0 ? kn0 - 1 : 0, sc1 = kn1 + 1 < p.nz ? kn1 + 1 : p.nz;
+    sigma_e_launch<8, 2>(s, p, cur, sc0, sc1, tune.zc, gate, (cudaStream_t)st);
+    return 1;
 }
 
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)

@@ -1294,8 +1294,9 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
         kr_nodes<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, RZ);
     } else {
         kn_update<<<dim3(cdivr((int)s.pn, 256), s.k1 - s.k0 + 1), 256, 0, cs>>>(s, p, cur);
+        if (euler_pre_sigma()) return 3;  // the next cycle's kf_sigma_e evaluates the dt candidate
         kn_dt<<<dim3(cdivr((int)s.pc, 256), s.k1 - s.k0), 256, 0, cs>>>(s, p, cur);
-        return 3;
+        return 4;
     }
     return 2;
 }

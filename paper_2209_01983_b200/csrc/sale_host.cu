@@ -442,13 +442,26 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
     int b = c->cur_enq;
     sale::Stream st = (sale::Stream)c->stream;
     bool v0 = c->prm.impl == SALE_IMPL_V0, euler = c->prm.rezone == SALE_EULER;
+    // Euler fused with the split force: each cycle's kf_sigma_e evaluates sigma and the
+    // dt candidate of its start state before k_begin (no separate dt pass)
+    const bool pre = !v0 && euler && sale::euler_pre_sigma();
     int pr = prof_open(c, SALE_K_PROLOGUE);
     c->launches += sale::launch_prep(c->dstate, st);
     if ((rc = exchange(c, b, true))) return rc;
-    for (auto& s : c->slabs) c->launches += sale::launch_dt_candidate(s, c->phys, b, st);
-    if ((rc = reduce_keys(c))) return rc;
+    if (!pre) {
+        for (auto& s : c->slabs) c->launches += sale::launch_dt_candidate(s, c->phys, b, st);
+        if ((rc = reduce_keys(c))) return rc;
+    }
     prof_close(c, pr);
     for (int n = 0; n < ncycles; ++n) {
+        if (pre) {
+            pr = prof_open(c, SALE_K_LAGRANGE);
+            for (auto& s : c->slabs) c->launches += sale::launch_euler_pre(s, c->phys, b, n > 0 ? 1 : 0, st);
+            prof_close(c, pr);
+            pr = prof_open(c, SALE_K_HALO);
+            if ((rc = reduce_keys(c))) return rc;
+            prof_close(c, pr);
+        }
         pr = prof_open(c, SALE_K_BEGIN);
         c->launches += sale::launch_begin(c->dstate, c->phys, st);
         prof_close(c, pr);
@@ -467,10 +480,11 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
         if ((rc = launch_check(c))) return rc;
         pr = prof_open(c, SALE_K_HALO);
         if ((rc = exchange(c, b ^ 1, false))) return rc;
-        if ((rc = reduce_keys(c))) return rc;
+        if (!pre && (rc = reduce_keys(c))) return rc;
         prof_close(c, pr);
         b ^= 1;
     }
+    if (pre && ncycles > 0 && (rc = reduce_keys(c))) return rc;  // the last cycle's error key
     c->launches += sale::launch_commit(c->dstate, c->phys, (sale::Stream)c->stream);
     c->cur_enq = b;
     return launch_check(c);

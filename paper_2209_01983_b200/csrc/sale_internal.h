@@ -111,5 +111,9 @@ int launch_remap_v0(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st);
 bool fused_available();
+// Euler fused, split force: kf_sigma_e (sigma + the dt candidate of the cycle-start
+// state) is launched before the cycle's k_begin; the remap then has no dt pass
+bool euler_pre_sigma();
+int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st);
 
 }  // namespace sale
