@@ -685,14 +685,16 @@ __global__ void __launch_bounds__(FW * NW, MB) kf_sigma_e(Slab s, Phys p, int cu
 }
 
 // grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane), y = node planes [kn0, kn1]
+// (32-bit index arithmetic: a slab holds < 2^31 cells)
 __global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int kn0)
 {
     if (!s.st->active) return;
     const int t = blockIdx.x * 256 + threadIdx.x;
     if (t >= (int)s.pn) return;
-    const int i = t % (p.nx + 1), j = t / (p.nx + 1), k = kn0 + blockIdx.y;
-    const bool pxm = i >= 1, pxp = i < p.nx, pym = j >= 1, pyp = j < p.ny, pzm = k >= 1, pzp = k < p.nz;
-    const long long c11 = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
+    const int nx = p.nx, ny = p.ny, pc = (int)s.pc;
+    const int i = t % (nx + 1), j = t / (nx + 1), k = kn0 + blockIdx.y, kl = k - s.kb;
+    const bool pxm = i >= 1, pxp = i < nx, pym = j >= 1, pyp = j < ny, pzm = k >= 1, pzp = k < p.nz;
+    const int c11 = i + nx * (j + ny * kl);
     const double dt = s.st->dt;
     D3 F = D3{0.0, 0.0, 0.0};
     double M = 0.0;
@@ -702,14 +704,14 @@ __global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int k
         const int ap = g & 1, bp = (g >> 1) & 1, cp = g >> 2;
         const bool pres = (ap ? pxp : pxm) && (bp ? pyp : pym) && (cp ? pzp : pzm);
         if (!pres) continue;
-        const int ci = i - 1 + ap, cj = j - 1 + bp, ckl = k - 1 + cp - s.kb;
-        const long long tx = (long long)ckl * p.ny + cj, ty = (long long)ckl * p.nx + ci, tz = (long long)cj * p.nx + ci;
-        const D3 Ax = D3{__ldg(s.TAx[0] + tx), __ldg(s.TAx[1] + tx), __ldg(s.TAx[2] + tx)};
-        const D3 Ay = D3{__ldg(s.TAy[0] + ty), __ldg(s.TAy[1] + ty), __ldg(s.TAy[2] + ty)};
-        const D3 Az = D3{__ldg(s.TAz[0] + tz), __ldg(s.TAz[1] + tz), __ldg(s.TAz[2] + tz)};
+        const int ci = i - 1 + ap, cj = j - 1 + bp, ckl = kl - 1 + cp;
+        const int ox = ckl * ny + cj, oy = ckl * nx + ci, oz = cj * nx + ci;
+        const D3 Ax = D3{__ldg(s.TAx[0] + ox), __ldg(s.TAx[1] + ox), __ldg(s.TAx[2] + ox)};
+        const D3 Ay = D3{__ldg(s.TAy[0] + oy), __ldg(s.TAy[1] + oy), __ldg(s.TAy[2] + oy)};
+        const D3 Az = D3{__ldg(s.TAz[0] + oz), __ldg(s.TAz[1] + oz), __ldg(s.TAz[2] + oz)};
         // cell (i-1+ap, j-1+bp, k-1+cp): the node is its corner (1-ap, 1-bp, 1-cp)
         const D3 C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
-        const long long c = c11 + (ap - 1) + (long long)p.nx * (bp - 1) + s.pc * (cp - 1);
+        const int c = c11 + (ap - 1) + nx * (bp - 1) + pc * (cp - 1);
         const D3 term = scl(__ldg(s.sig + c), C);
         const double mk = __ldg(s.m[cur] + c);
         F = first ? term : add(F, term);
@@ -717,8 +719,8 @@ __global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int k
         first = false;
     }
     M = 0.125 * M;
-    const long long n = (long long)t + s.pn * (long long)(k - s.kb);
-    const D3 u = ld3(s.u[cur], n), x = D3{s.Xt[i], s.Yt[j], s.Zt[k - s.kb]};
+    const long long n = (long long)t + s.pn * (long long)kl;
+    const D3 u = ld3(s.u[cur], n), x = D3{s.Xt[i], s.Yt[j], s.Zt[kl]};
     D3 un = d3(u.x + (ddiv(F.x, M) * dt), u.y + (ddiv(F.y, M) * dt), u.z + (ddiv(F.z, M) * dt));
     un = reflect(p, i, j, k, un);
     st3(s.u1, n, un);
