@@ -878,7 +878,7 @@ __global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
     if (t >= (int)s.pn) return;
     const int i = t % (p.nx + 1), j = t / (p.nx + 1), k = s.k0 + blockIdx.y;
     const bool pxm = i >= 1, pxp = i < p.nx, pym = j >= 1, pyp = j < p.ny, pzm = k >= 1, pzp = k < p.nz;
-    const long long c00 = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (k - s.kb));
+    const int c00 = i + p.nx * (j + p.ny * (k - s.kb));  // 32-bit: a slab holds < 2^31 cells
     const int sx = 1, sy = p.nx, sz = p.nx * p.ny;
     const double* __restrict__ dm = s.dm + c00;
     const double* __restrict__ m2 = s.m[cur ^ 1] + c00;
