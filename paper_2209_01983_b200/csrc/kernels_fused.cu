@@ -1108,6 +1108,243 @@ struct EnergyEulerCTA {
     }
 };
 
+// ============================================================================
+// kx_energy_sweep (Euler): kf_energy_e and the remap's kr_sweep in one z-march.
+// Both read the same moved nodes x' and depend only on +x / +y neighbour columns;
+// fused, the moved-face s' (V' and the swept-hex tops) and V' (V' and the donor
+// density) stay on chip.  Per column and cell plane t:
+//   P2: s' of the x-, y-faces anchored here and of the z-face at t+1; the six
+//       ribbons of c.4 step 1 (shared as in kr_sweep); the 8-node mean of u'
+//   P3: V' (tangle check), W and e' (S7); the swept volumes of the -x/-y/-z faces;
+//       the donor data r = m/V', Ubar (R2)
+// Writes e', dV, rD, UD (kr_flux's inputs).
+// ============================================================================
+template <int NW>
+struct EnergySweepCTA {
+    static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
+    __host__ __device__ static constexpr int oP(int par, int c) { return (par * 9 + c) * PL; }  // x'(3) ubar(3) u'(3)
+    __host__ __device__ static constexpr int oF(int xy, int c) { return 18 * PL + (xy * 4 + c) * PL; }  // A^n(3), s'
+    __host__ __device__ static constexpr int oZ() { return 26 * PL; }                                 // z-face A^n
+    __host__ __device__ static constexpr int oR(int c) { return 29 * PL + c * PL; }                   // Rxz Ryz Rzy Rzx
+    static constexpr int WORDS = 33 * PL + 2 * PAD;
+
+    const Slab& s;
+    const Phys& p;
+    double* me;
+    int i, j, za, zb, ic, jc, kr0, kr1;
+    long long nb, cb, nbc, cbc;
+    double dt, tx0, tx1, ty0, ty1;
+    bool col_in, cell_col;
+    D3 fu, fu1, fx1;  // prefetch: node plane k (unconditional loads, selected at use)
+    double fm, fe, fs, fsx, fsy, fsz, fz;  // prefetch: cell plane k-1 (m, e, sigma, s^T x3), Z_k
+    D3 fax, fay;
+    bool fnok, fcok;
+    double zs_prev, rxy_t, ryx_t, zprev;
+
+    __device__ __forceinline__ EnergySweepCTA(const Slab& s_, const Phys& p_, double* smem, int kc0, int kc1, int kr0_,
+                                              int kr1_, int zchunk)
+        : s(s_), p(p_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + PAD + iy * FW + ix;
+        i = blockIdx.x * TX + ix;
+        j = blockIdx.y * TY + iy;
+        ic = i >= p.nx ? p.nx - 1 : i;
+        jc = j >= p.ny ? p.ny - 1 : j;
+        kr0 = kr0_;
+        kr1 = kr1_;
+        za = kc0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kc1 - 1 ? za + zchunk - 1 : kc1 - 1;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        {
+            const int in = i > p.nx ? p.nx : i, jn = j > p.ny ? p.ny : j;
+            nbc = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
+            cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
+        }
+        dt = s.st->dt;
+        col_in = i <= p.nx && j <= p.ny;
+        cell_col = i < p.nx && j < p.ny && ix < TX && iy < TY;
+        tx0 = col_in ? s.Xt[i] : 0.0;
+        tx1 = (col_in && i + 1 <= p.nx) ? s.Xt[i + 1] : 0.0;
+        ty0 = col_in ? s.Yt[j] : 0.0;
+        ty1 = (col_in && j + 1 <= p.ny) ? s.Yt[j + 1] : 0.0;
+        const long long tz = (long long)jc * p.nx + ic;
+        st3s(me, oZ(), PL, D3{s.TAz[0][tz], s.TAz[1][tz], s.TAz[2][tz]});
+    }
+
+    __device__ __forceinline__ static double fs4(D3 Q0, D3 Q1, D3 Q2, D3 Q3)
+    {
+        return face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
+    }
+    __device__ __forceinline__ void fetch(int k, int cur)  // node plane k, cell plane k-1
+    {
+        fnok = col_in && k >= 0 && k <= p.nz;
+        const int kn = k < s.kb ? s.kb : (k > s.kb + s.nzn - 1 ? s.kb + s.nzn - 1 : k);
+        const long long n = nbc + (long long)kn * s.pn;
+        fu = ld3(s.u[cur], n);
+        fu1 = ld3(s.u1, n);
+        fx1 = ld3(s.x1, n);
+        fz = s.Zt[kn - s.kb];
+        const int kc = k - 1;
+        fcok = cell_col && kc >= 0 && kc < p.nz;
+        int kl = kc - s.kb;
+        kl = kl < 0 ? 0 : (kl >= s.nzc ? s.nzc - 1 : kl);
+        const long long c = cbc + (long long)(kl + s.kb) * s.pc;
+        fm = s.m[cur][c];
+        fe = s.e[cur][c];
+        fs = s.sig[c];
+        fsx = s.sT[0][c];
+        fsy = s.sT[1][c];
+        fsz = s.sT[2][c];
+        const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
+        fax = D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]};
+        fay = D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]};
+    }
+    template <int PAR>
+    __device__ __forceinline__ void put()
+    {
+        const D3 z = D3{0.0, 0.0, 0.0};
+        const D3 u0 = fnok ? fu : z, u1 = fnok ? fu1 : z;
+        st3s(me, oP(PAR, 0), PL, fnok ? fx1 : z);
+        st3s(me, oP(PAR, 3), PL, scl(0.5, add(u0, u1)));
+        st3s(me, oP(PAR, 6), PL, u1);
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 X1(int off) const { return ld3s(me + off, oP(PAR, 0), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 Ub(int off) const { return ld3s(me + off, oP(PAR, 3), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 U1(int off) const { return ld3s(me + off, oP(PAR, 6), PL); }
+    template <int B>
+    __device__ __forceinline__ double zs() const
+    {
+        return fs4(X1<B>(0), X1<B>(1), X1<B>(FW + 1), X1<B>(FW));
+    }
+    // ribbons Rxy, Ryx of node plane k (parity PAR), own column, Z of that plane z
+    template <int PAR>
+    __device__ __forceinline__ void rib_xy(int k, double z, double& rxy, double& ryx) const
+    {
+        rxy = 0.0;
+        ryx = 0.0;
+        if (col_in && k >= 0 && k <= p.nz) {
+            const D3 T = D3{tx0, ty0, z}, L = X1<PAR>(0);
+            if (j + 1 <= p.ny) rxy = fs4(T, L, X1<PAR>(FW), D3{tx0, ty1, z});
+            if (i + 1 <= p.nx) ryx = fs4(T, D3{tx1, ty0, z}, X1<PAR>(1), L);
+        }
+    }
+
+    template <int B0>
+    __device__ __forceinline__ void step(int t, int cur)
+    {
+        constexpr int B1 = B0 ^ 1;
+        put<B1>();
+        const double m = fcok ? fm : 0.0, e = fcok ? fe : 0.0, sig = fcok ? fs : 0.0;
+        const double sTx = fsx, sTy = fsy, sTz = fsz, z0 = zprev, z1 = fz;
+        const D3 ax = fax, ay = fay;
+        if (t < zb) fetch(t + 2, cur);
+        __syncthreads();
+        // ---- P2: moved faces (s'), ribbons, A^n from the tables, Ubar of u'
+        const D3 L0 = X1<B0>(0), L1 = X1<B1>(0);
+        const double sx = fs4(L0, X1<B0>(FW), X1<B1>(FW), L1);
+        const double sy = fs4(L0, L1, X1<B1>(1), X1<B0>(1));
+        const double zs_next = zs<B1>();
+        st3s(me, oF(0, 0), PL, ax);
+        me[oF(0, 3)] = sx;
+        st3s(me, oF(1, 0), PL, ay);
+        me[oF(1, 3)] = sy;
+        double rxy_n, ryx_n;
+        rib_xy<B1>(t + 1, z1, rxy_n, ryx_n);
+        double rxz = 0.0, ryz = 0.0, rzy = 0.0, rzx = 0.0;
+        if (col_in) {
+            const D3 T0 = D3{tx0, ty0, z0}, T1 = D3{tx0, ty0, z1};
+            rxz = fs4(T0, T1, L1, L0);
+            ryz = fs4(T0, L0, L1, T1);
+            if (j + 1 <= p.ny) rzy = fs4(T0, D3{tx0, ty1, z0}, X1<B0>(FW), L0);
+            if (i + 1 <= p.nx) rzx = fs4(T0, L0, X1<B0>(1), D3{tx1, ty0, z0});
+        }
+        me[oR(0)] = rxz;
+        me[oR(1)] = ryz;
+        me[oR(2)] = rzy;
+        me[oR(3)] = rzx;
+        D3 ubar = D3{0.0, 0.0, 0.0};
+        if (cell_col) {
+            D3 sum = U1<B0>(0);
+            sum = add(sum, U1<B0>(1));
+            sum = add(sum, U1<B0>(FW));
+            sum = add(sum, U1<B0>(FW + 1));
+            sum = add(sum, U1<B1>(0));
+            sum = add(sum, U1<B1>(1));
+            sum = add(sum, U1<B1>(FW));
+            sum = add(sum, U1<B1>(FW + 1));
+            ubar = scl(0.125, sum);
+        }
+        __syncthreads();
+        // ---- P3: cell (i,j,t): V', W, e' (S7); swept volumes, donor data (R1, R2)
+        if (cell_col && t < p.nz) {
+            double sv[6] = {sx, me[1 + oF(0, 3)], sy, me[FW + oF(1, 3)], zs_prev, zs_next};
+            const double V1 = vol_from_s(sv);
+            if (t >= s.k0 && t < s.k1 && !(V1 > 0.0))
+                atomicMin(&s.st->err_key, (ERR_ORDER_TANGLED << 48) | (unsigned long long)gcell(p, i, j, t));
+            const D3 Az = ld3s(me, oZ(), PL);
+            const D3 A[6] = {ax, ld3s(me + 1, oF(0, 0), PL), ay, ld3s(me + FW, oF(1, 0), PL), Az, Az};
+            double W = 0.0;
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                const int a = h & 1, b = (h >> 1) & 1, c = h >> 2;
+                const D3 C = corner_vec(A, a, b, c);
+                const D3 ub = c ? Ub<B1>(a + b * FW) : Ub<B0>(a + b * FW);
+                const double term = dot(C, ub);
+                W = (h == 0) ? term : W + term;
+            }
+            const long long cc = cb + (long long)t * s.pc;
+            s.e1[cc] = e - ddiv((sig * W) * dt, m);
+            st3(s.UD, cc, ubar);
+            s.rD[cc] = ddiv(m, V1);
+            if (t >= kr0 && t <= kr1) {
+                if (t < kr1 && i >= 1)
+                    s.dV[0][cc] = ddiv(((((me[FW + oR(0)] - me[oR(0)]) + rxy_n) - rxy_t) + sx) - sTx, 3.0);
+                if (t < kr1 && j >= 1)
+                    s.dV[1][cc] = ddiv(((((ryx_n - ryx_t) + me[1 + oR(1)]) - me[oR(1)]) + sy) - sTy, 3.0);
+                if (t >= 1)
+                    s.dV[2][cc] = ddiv(((((me[1 + oR(2)] - me[oR(2)]) + me[FW + oR(3)]) - me[oR(3)]) + zs_prev) - sTz, 3.0);
+            }
+        }
+        zs_prev = zs_next;
+        rxy_t = rxy_n;
+        ryx_t = ryx_n;
+        zprev = z1;
+        __syncthreads();
+    }
+
+    __device__ __forceinline__ void run(int cur)
+    {
+        fetch(za, cur);
+        if (za & 1) put<1>();
+        else put<0>();
+        zprev = fz;
+        fetch(za + 1, cur);
+        __syncthreads();
+        zs_prev = (za & 1) ? zs<1>() : zs<0>();
+        if (za & 1) rib_xy<1>(za, zprev, rxy_t, ryx_t);
+        else rib_xy<0>(za, zprev, rxy_t, ryx_t);
+        for (int t = za; t <= zb; ++t) {
+            if (t & 1) step<1>(t, cur);
+            else step<0>(t, cur);
+        }
+    }
+};
+
+template <int NW, int MB>
+__global__ void __launch_bounds__(FW * NW, MB)
+    kx_energy_sweep(Slab s, Phys p, int cur, int kc0, int kc1, int kr0, int kr1, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    EnergySweepCTA<NW> c(s, p, smem, kc0, kc1, kr0, kr1, zchunk);
+    c.run(cur);
+}
+
 template <int NW, int MB>
 __global__ void __launch_bounds__(FW * NW, MB) kf_energy_e(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
@@ -1208,6 +1445,31 @@ static void sigma_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int k
     kf_sigma_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc, gate);
 }
 
+template <int NW, int MB>
+static void esweep_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
+{
+    const size_t sm = sizeof(double) * EnergySweepCTA<NW>::WORDS;
+    static bool init = false;
+    if (!init) {
+        set_smem(kx_energy_sweep<NW, MB>, sm);
+        init = true;
+    }
+    const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
+    dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
+    kx_energy_sweep<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, kr0, kr1, zc);
+}
+
+// Euler: kf_energy_e + kr_sweep as one kernel (SALE_ESWEEP=1).  Measured 2% slower
+// than the two kernels on C4 (210 registers: 12 warps/SM), so off by default.
+int euler_esweep_variant()
+{
+    static const int v = [] {
+        const char* e = getenv("SALE_ESWEEP");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <bool EULER>
 static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
@@ -1238,7 +1500,9 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
     else if (tune.nwf >= 12) force_launch<EULER, 12>(s, p, cur, kn0, kn1, tune.zc, cs);
     else force_launch<EULER, 8>(s, p, cur, kn0, kn1, tune.zc, cs);
     // Euler: kf_energy_e also writes the moved-face s' kr_sweep reads (Slab::sF)
-    if (EULER) energy_e_launch<8, 2>(s, p, cur, kc0, kc1, tune.zc, cs);
+    const int esw = euler_esweep_variant();
+    if (EULER && esw > 0) esweep_launch<12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
+    else if (EULER) energy_e_launch<8, 2>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe == 15) energy_launch<EULER, 15, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
     else if (tune.nwe >= 12) energy_launch<EULER, 12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);

@@ -1269,7 +1269,9 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
             dim3 grid(cdivr(p.nx, RW - 1), cdivr(p.ny, nw - 1), cdivr(t1 - t0 + 1, RZ));
             kern<<<grid, dim3(RW, nw), sizeof(double) * words, cs>>>(s, p, cur, kr0, kr1, RZ);
         };
-        if (variant == 7) sweep(kr_sweep<8, 2>, 8, SweepCTA<8>::WORDS);
+        if (euler_esweep_variant() > 0) {
+        }  // swept volumes and donor data came with kx_energy_sweep
+        else if (variant == 7) sweep(kr_sweep<8, 2>, 8, SweepCTA<8>::WORDS);
         else if (variant == 8) sweep(kr_sweep<8, 3>, 8, SweepCTA<8>::WORDS);
         else if (variant == 9) sweep(kr_sweep<16, 1>, 16, SweepCTA<16>::WORDS);
         else sweep(kr_sweep<12, 2>, 12, SweepCTA<12>::WORDS);

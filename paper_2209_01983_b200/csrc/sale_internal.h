@@ -115,5 +115,8 @@ bool fused_available();
 // state) is launched before the cycle's k_begin; the remap then has no dt pass
 bool euler_pre_sigma();
 int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st);
+// Euler fused: > 0 when the Lagrangian phase's energy kernel also does the remap's
+// swept volumes and donor data (kx_energy_sweep); the remap then starts at kr_flux
+int euler_esweep_variant();
 
 }  // namespace sale

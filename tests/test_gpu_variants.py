@@ -1,0 +1,41 @@
+"""The alternative kernel schedules kept behind environment switches (read once per
+process, so each runs in a subprocess) must stay bit-identical to the oracle:
+SALE_ESWEEP=1 (kf_energy_e + kr_sweep fused), SALE_REMAP=6 (pipelined kr_cells_p),
+SALE_REMAP=0 (three-barrier kr_cells), SALE_FORCE_E=1 (one-kernel kf_force_e with
+the remap's kn_dt pass), SALE_RNODES=0 (z-march kr_nodes)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import oracle as O
+from paper_2209_01983_b200.configs import sedov, EULER
+from paper_2209_01983_b200.sale import Sale
+from tests.helpers import apply_perturbation, compare
+for shape, seed in (((13, 7, 9), None), ((40, 11, 37), 1), ((1, 1, 6), None)):
+    cfg = sedov(shape, EULER)
+    g, o = Sale(cfg, impl="fused"), O.Oracle(cfg)
+    if seed is not None:
+        apply_perturbation([g, o], cfg, seed, lagrange=False)
+    for chunk in (1, 7, 12):  # several sale_step calls (prologue paths) of different lengths
+        rg, ro = g.step(chunk), o.step(chunk)
+        assert rg == ro, (shape, rg, ro)
+    compare(g, o)
+    assert g.clock() == o.clock()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"SALE_ESWEEP": "1"}, {"SALE_REMAP": "6"}, {"SALE_REMAP": "0"},
+                                 {"SALE_FORCE_E": "1"}, {"SALE_FORCE_E": "1", "SALE_RNODES": "0"}])
+def test_variant_bitwise(env):
+    e = dict(os.environ, **env)
+    out = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=e, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
