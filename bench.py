@@ -45,7 +45,7 @@ ALGO_BYTES = {configs.LAGRANGE: 120.0, configs.EULER: 80.0}
 ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 661.0, "remap": 0.0},
              configs.EULER: {"lagrange": 500.0, "remap": 406.0}}
 # kernel name prefixes of each timing class (for the ncu traffic file)
-CLASS_KERNELS = {"lagrange": ("kf_",), "remap": ("kr_", "kn_")}
+CLASS_KERNELS = {"lagrange": ("kf_", "kn_force", "kx_"), "remap": ("kr_", "kn_update", "kn_dt")}
 REASON_BITS = {"hw_slowdown": "hw_slowdown", "hw_thermal_slowdown": "hw_thermal_slowdown",
                "sw_thermal_slowdown": "sw_thermal_slowdown", "sw_power_cap": "sw_power_cap"}
 
@@ -289,19 +289,19 @@ def main():
     mode = cfg["rezone"]
     dom = max(("lagrange", "remap"), key=lambda k: prof[k][0])
     dom_ms, dom_n = prof[dom]
-    per_launch_ms = dom_ms / max(dom_n, 1)
-    fp64_per_launch = ALGO_FP64[mode][dom] * local_cells          # FP64 instr per launch group
-    achieved_t = fp64_per_launch / (per_launch_ms * 1e-3) / 1e12   # T instr/s
+    per_cycle_ms = dom_ms / args.steps                             # the class may launch >1 group per cycle
+    fp64_per_cycle = ALGO_FP64[mode][dom] * local_cells           # FP64 instr of the class per cycle
+    achieved_t = fp64_per_cycle / (per_cycle_ms * 1e-3) / 1e12     # T instr/s
     cyc_fp64 = sum(ALGO_FP64[mode].values()) * local_cells
     cyc_t = cyc_fp64 / (ms / args.steps * 1e-3) / 1e12
     cyc_bytes = ALGO_BYTES[mode] * local_cells
     cycle_gbs = cyc_bytes / (ms / args.steps * 1e-3) / 1e9
     tr_bytes, tr_src = traffic(args.config, dom)
     roofline = {"bound": "alu", "achieved": achieved_t, "peak": fpk, "unit": "T fp64-instr/s",
-                "frac": achieved_t / fpk, "traffic": tr_bytes, "traffic_unit": "bytes per launch group",
-                "traffic_source": tr_src, "algo_bytes_per_launch_group": ALGO_BYTES[mode] * local_cells,
-                "kernel": dom,
-                "kernel_ms_per_launch": per_launch_ms, "kernel_share_of_step": dom_ms / ms,
+                "frac": achieved_t / fpk, "traffic": tr_bytes, "traffic_unit": "DRAM bytes per cycle of the class",
+                "traffic_source": tr_src, "algo_bytes_per_cycle": ALGO_BYTES[mode] * local_cells,
+                "kernel": dom, "kernel_launch_groups_per_cycle": dom_n / args.steps,
+                "kernel_ms_per_cycle": per_cycle_ms, "kernel_share_of_step": dom_ms / ms,
                 "algo_fp64_instr_per_zone": ALGO_FP64[mode][dom], "peak_source": fpk_src,
                 "whole_cycle": {"achieved": cyc_t, "frac": cyc_t / fpk,
                                 "algo_fp64_instr_per_zone": sum(ALGO_FP64[mode].values())},
