@@ -19,9 +19,12 @@
  * then y, then z planes; one z-slab per rank plus ghost planes.
  *
  * Ownership: the caller owns the device workspace, the CUDA stream and the
- * process group; the library owns the context, its NCCL communicator and a few
- * bytes of pinned host memory.  A context is not thread-safe.  create / step /
- * destroy are collective over the ranks of one job.
+ * process group; the library owns the context, its NCCL communicator, a few
+ * bytes of pinned host memory and, on single-rank contexts, a private stream plus
+ * up to two CUDA graphs (a captured pair of cycles, replayed by sale_step on the
+ * caller's stream; SALE_GRAPHS=0 in the environment disables them).  A context is
+ * not thread-safe.  create / step / destroy are collective over the ranks of one
+ * job.
  *
  * Error behaviour: every entry point returns a status code (SALE_OK = 0).  A
  * numerical error in sale_step (ETANGLED, EDTCOLLAPSE, ENEGMASS) or a CUDA /

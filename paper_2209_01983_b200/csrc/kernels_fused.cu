@@ -1380,6 +1380,7 @@ static void force_launch(const Slab& s, const Phys& p, int cur, int kn0, int kn1
         set_smem(kf_force<EULER, NW>, sm);
         init = true;
     }
+    zc = zchunk_for((long long)cdiv(p.nx + 1, FW - 2) * cdiv(p.ny + 1, NW - 2), kn1 - kn0 + 1, zc);
     dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW - 2), cdiv(kn1 - kn0 + 1, zc));
     kf_force<EULER, NW><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
 }
@@ -1392,6 +1393,7 @@ static void energy_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc
         set_smem(kf_energy<EULER, NW, MB>, sm);
         init = true;
     }
+    zc = zchunk_for((long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW - 1), kc1 - kc0, zc);
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
     kf_energy<EULER, NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
 }
@@ -1415,6 +1417,7 @@ static void force_e_launch(const Slab& s, const Phys& p, int cur, int kn0, int k
         set_smem(kf_force_e<NW, MB>, sm);
         init = true;
     }
+    zc = zchunk_for((long long)cdiv(p.nx + 1, FW - 2) * cdiv(p.ny + 1, NW - 2), kn1 - kn0 + 1, zc);
     dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW - 2), cdiv(kn1 - kn0 + 1, zc));
     kf_force_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
 }
@@ -1428,6 +1431,7 @@ static void energy_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int 
         set_smem(kf_energy_e<NW, MB>, sm);
         init = true;
     }
+    zc = zchunk_for((long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW - 1), kc1 - kc0, zc);
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
     kf_energy_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
 }
@@ -1441,6 +1445,7 @@ static void sigma_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int k
         set_smem(kf_sigma_e<NW, MB>, sm);
         init = true;
     }
+    zc = zchunk_for((long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW - 1), kc1 - kc0, zc);
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
     kf_sigma_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc, gate);
 }
@@ -1455,6 +1460,7 @@ static void esweep_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc
         init = true;
     }
     const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
+    zc = zchunk_for((long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW - 1), kc1 - kc0, zc);
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
     kx_energy_sweep<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, kr0, kr1, zc);
 }

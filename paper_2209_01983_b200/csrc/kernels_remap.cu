@@ -1220,8 +1220,10 @@ static void cells_p_launch(const Slab& s, const Phys& p, int cur, int kr0, int k
         cudaFuncSetAttribute(kr_cells_p<NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         init = true;
     }
-    dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
-    kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+    const int zc = zchunk_for((long long)cdivr(p.nx, RW - 3) * cdivr(p.ny, NW - 3), kr1 - kr0, RZ);
+
+    dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, zc));
+    kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zc);
 }
 
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
@@ -1240,8 +1242,10 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
             cudaFuncSetAttribute(kr_cells<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             init = true;
         }
-        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
-        kr_cells<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+        const int zc = zchunk_for((long long)cdivr(p.nx, RW - 3) * cdivr(p.ny, NW - 3), kr1 - kr0, RZ);
+
+        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, zc));
+        kr_cells<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zc);
     } else if (variant == 1) {
         constexpr int NW = 7, MB = 2;
         const size_t sm = sizeof(double) * RemapCellsP<NW>::WORDS;
@@ -1250,8 +1254,10 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
             cudaFuncSetAttribute(kr_cells_p<NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             init = true;
         }
-        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, RZ));
-        kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, RZ);
+        const int zc = zchunk_for((long long)cdivr(p.nx, RW - 3) * cdivr(p.ny, NW - 3), kr1 - kr0, RZ);
+
+        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, zc));
+        kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zc);
     } else if (variant == 2) {
         cells_p_launch<12, 1>(s, p, cur, kr0, kr1, cs);
     } else if (variant == 3) {
@@ -1266,8 +1272,10 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
                 init = true;
             }
             const int t0 = kr0 - 1 > 0 ? kr0 - 1 : 0, t1 = kr1 < p.nz - 1 ? kr1 : p.nz - 1;
-            dim3 grid(cdivr(p.nx, RW - 1), cdivr(p.ny, nw - 1), cdivr(t1 - t0 + 1, RZ));
-            kern<<<grid, dim3(RW, nw), sizeof(double) * words, cs>>>(s, p, cur, kr0, kr1, RZ);
+            const int zc = zchunk_for((long long)cdivr(p.nx, RW - 1) * cdivr(p.ny, nw - 1), t1 - t0 + 1, RZ);
+
+            dim3 grid(cdivr(p.nx, RW - 1), cdivr(p.ny, nw - 1), cdivr(t1 - t0 + 1, zc));
+            kern<<<grid, dim3(RW, nw), sizeof(double) * words, cs>>>(s, p, cur, kr0, kr1, zc);
         };
         if (euler_esweep_variant() > 0) {
         }  // swept volumes and donor data came with kx_energy_sweep
@@ -1292,8 +1300,10 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
             cudaFuncSetAttribute(kr_nodes<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             init = true;
         }
-        dim3 grid(cdivr(p.nx + 1, RW - 2), cdivr(p.ny + 1, NW - 2), cdivr(s.k1 - s.k0 + 1, RZ));
-        kr_nodes<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, RZ);
+        const int zc = zchunk_for((long long)cdivr(p.nx + 1, RW - 2) * cdivr(p.ny + 1, NW - 2), s.k1 - s.k0 + 1, RZ);
+
+        dim3 grid(cdivr(p.nx + 1, RW - 2), cdivr(p.ny + 1, NW - 2), cdivr(s.k1 - s.k0 + 1, zc));
+        kr_nodes<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, zc);
     } else {
         kn_update<<<dim3(cdivr((int)s.pn, 256), s.k1 - s.k0 + 1), 256, 0, cs>>>(s, p, cur);
         if (euler_pre_sigma()) return 3;  // the next cycle's kf_sigma_e evaluates the dt candidate

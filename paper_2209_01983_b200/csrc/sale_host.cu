@@ -59,6 +59,10 @@ struct sale_ctx {
     std::vector<Pending> pending;
     double prof_ms[SALE_K_NCLASS] = {0};
     long long prof_cnt[SALE_K_NCLASS] = {0};
+    // captured two-cycle CUDA graphs by starting buffer parity, and their kernel count
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    long long glaunches[2] = {0, 0};
+    cudaStream_t cap_stream = nullptr;  // private stream the graphs are captured on
 };
 
 namespace {
@@ -436,6 +440,95 @@ int reduce_keys(sale_ctx* c)
                       "dt allreduce");
 }
 
+// one cycle reading buffers [b]; first = the first cycle of a sale_step call (its
+// kf_sigma_e runs ungated: DevState.active is still 0 then)
+int enqueue_one_cycle(sale_ctx* c, int b, bool first, bool pre)
+{
+    int rc;
+    sale::Stream st = (sale::Stream)c->stream;
+    const bool v0 = c->prm.impl == SALE_IMPL_V0, euler = c->prm.rezone == SALE_EULER;
+    int pr;
+    if (pre) {
+        pr = prof_open(c, SALE_K_LAGRANGE);
+        for (auto& s : c->slabs) c->launches += sale::launch_euler_pre(s, c->phys, b, first ? 0 : 1, st);
+        prof_close(c, pr);
+        pr = prof_open(c, SALE_K_HALO);
+        if ((rc = reduce_keys(c))) return rc;
+        prof_close(c, pr);
+    }
+    pr = prof_open(c, SALE_K_BEGIN);
+    c->launches += sale::launch_begin(c->dstate, c->phys, st);
+    prof_close(c, pr);
+    for (auto& s : c->slabs) {
+        pr = prof_open(c, SALE_K_LAGRANGE);
+        c->launches += v0 ? sale::launch_lagrange_v0(s, c->phys, b, st) : sale::launch_lagrange_fused(s, c->phys, b, st);
+        prof_close(c, pr);
+        if (euler) {
+            pr = prof_open(c, SALE_K_REMAP);
+            c->launches += v0 ? sale::launch_remap_v0(s, c->phys, b, st) : sale::launch_remap_fused(s, c->phys, b, st);
+            prof_close(c, pr);
+        }
+    }
+    if ((rc = launch_check(c))) return rc;
+    pr = prof_open(c, SALE_K_HALO);
+    if ((rc = exchange(c, b ^ 1, false))) return rc;
+    if (!pre && (rc = reduce_keys(c))) return rc;
+    prof_close(c, pr);
+    return SALE_OK;
+}
+
+// CUDA graph of two consecutive cycles starting from buffer parity b (they return to
+// b), captured once per context and parity, then replayed: a cycle is 6-9 kernel
+// launches plus copies, which dominate small meshes.  Single-rank contexts only (the
+// NCCL calls of a multi-rank cycle stay on the plain path), never while profiling.
+bool graphs_enabled(const sale_ctx* c)
+{
+    static const int on = [] {
+        const char* v = getenv("SALE_GRAPHS");
+        return v ? atoi(v) : 1;
+    }();
+    return on && !c->comm && !c->prof_on;
+}
+
+int graph_for(sale_ctx* c, int b, bool pre, cudaGraphExec_t* out)
+{
+    if (c->gexec[b]) {
+        *out = c->gexec[b];
+        return SALE_OK;
+    }
+    const long long before = c->launches;
+    cudaGraph_t g = nullptr;
+    // capture on a private stream (the caller's may be the legacy default stream,
+    // which cannot capture); the graph is then launched on the caller's stream
+    int rc = SALE_OK;
+    if (!c->cap_stream)
+        rc = cuda_check(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "capture stream");
+    if (rc) return rc;
+    cudaStream_t user = c->stream;
+    c->stream = c->cap_stream;
+    rc = cuda_check(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "graph capture");
+    if (rc) {
+        c->stream = user;
+        return rc;
+    }
+    int rc1 = enqueue_one_cycle(c, b, false, pre);
+    if (!rc1) rc1 = enqueue_one_cycle(c, b ^ 1, false, pre);
+    rc = cuda_check(c, cudaStreamEndCapture(c->stream, &g), "graph capture end");
+    c->stream = user;
+    if (rc1 || rc) {
+        if (g) cudaGraphDestroy(g);
+        c->launches = before;
+        return rc1 ? rc1 : rc;
+    }
+    rc = cuda_check(c, cudaGraphInstantiate(&c->gexec[b], g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+    c->glaunches[b] = c->launches - before;
+    c->launches = before;
+    if (rc) return rc;
+    *out = c->gexec[b];
+    return SALE_OK;
+}
+
 int enqueue_cycles(sale_ctx* c, int ncycles)
 {
     int rc;
@@ -453,35 +546,22 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
         if ((rc = reduce_keys(c))) return rc;
     }
     prof_close(c, pr);
-    for (int n = 0; n < ncycles; ++n) {
-        if (pre) {
-            pr = prof_open(c, SALE_K_LAGRANGE);
-            for (auto& s : c->slabs) c->launches += sale::launch_euler_pre(s, c->phys, b, n > 0 ? 1 : 0, st);
-            prof_close(c, pr);
-            pr = prof_open(c, SALE_K_HALO);
-            if ((rc = reduce_keys(c))) return rc;
-            prof_close(c, pr);
+    int n = 0;
+    if (ncycles > 0) {  // the first cycle on the plain path (ungated sigma)
+        if ((rc = enqueue_one_cycle(c, b, true, pre))) return rc;
+        b ^= 1;
+        n = 1;
+    }
+    if (graphs_enabled(c) && ncycles - n >= 2) {
+        cudaGraphExec_t ge = nullptr;
+        if ((rc = graph_for(c, b, pre, &ge))) return rc;
+        for (; n + 2 <= ncycles; n += 2) {
+            if ((rc = cuda_check(c, cudaGraphLaunch(ge, c->stream), "graph launch"))) return rc;
+            c->launches += c->glaunches[b];
         }
-        pr = prof_open(c, SALE_K_BEGIN);
-        c->launches += sale::launch_begin(c->dstate, c->phys, st);
-        prof_close(c, pr);
-        for (auto& s : c->slabs) {
-            pr = prof_open(c, SALE_K_LAGRANGE);
-            c->launches += v0 ? sale::launch_lagrange_v0(s, c->phys, b, st)
-                              : sale::launch_lagrange_fused(s, c->phys, b, st);
-            prof_close(c, pr);
-            if (euler) {
-                pr = prof_open(c, SALE_K_REMAP);
-                c->launches += v0 ? sale::launch_remap_v0(s, c->phys, b, st)
-                                  : sale::launch_remap_fused(s, c->phys, b, st);
-                prof_close(c, pr);
-            }
-        }
-        if ((rc = launch_check(c))) return rc;
-        pr = prof_open(c, SALE_K_HALO);
-        if ((rc = exchange(c, b ^ 1, false))) return rc;
-        if (!pre && (rc = reduce_keys(c))) return rc;
-        prof_close(c, pr);
+    }
+    for (; n < ncycles; ++n) {
+        if ((rc = enqueue_one_cycle(c, b, false, pre))) return rc;
         b ^= 1;
     }
     if (pre && ncycles > 0 && (rc = reduce_keys(c))) return rc;  // the last cycle's error key
@@ -859,6 +939,9 @@ void sale_destroy(sale_ctx* c)
         cudaEventDestroy(p.b);
     }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (auto ge : c->gexec)
+        if (ge) cudaGraphExecDestroy(ge);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     delete c;
 }
 

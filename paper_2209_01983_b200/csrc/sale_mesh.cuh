@@ -77,4 +77,15 @@ __device__ __forceinline__ double* mass_cur(const Slab& s, const Phys& p, int cu
     return p.rezone ? s.m[cur] : s.m[0];
 }
 
+// host: z-chunk length of a z-marching grid.  Large meshes use zc0 planes per CTA;
+// small ones shorter chunks (down to 4) so the grid still covers the 148 SMs twice
+// (a z-march is a chain of dependent plane steps; its length is the small-mesh time).
+// Chunking changes only which CTA computes a plane, never the arithmetic.
+inline int zchunk_for(long long ctas_xy, int planes, int zc0)
+{
+    int zc = zc0;
+    while (zc > 4 && ctas_xy * ((planes + zc - 1) / zc) < 2 * 148) zc /= 2;
+    return zc;
+}
+
 }  // namespace sale

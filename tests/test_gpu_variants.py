@@ -2,7 +2,8 @@
 process, so each runs in a subprocess) must stay bit-identical to the oracle:
 SALE_ESWEEP=1 (kf_energy_e + kr_sweep fused), SALE_REMAP=6 (pipelined kr_cells_p),
 SALE_REMAP=0 (three-barrier kr_cells), SALE_FORCE_E=1 (one-kernel kf_force_e with
-the remap's kn_dt pass), SALE_RNODES=0 (z-march kr_nodes)."""
+the remap's kn_dt pass), SALE_RNODES=0 (z-march kr_nodes), SALE_GRAPHS=0 (no CUDA-graph
+replay of the cycle pairs)."""
 import os
 import subprocess
 import sys
@@ -34,7 +35,8 @@ print("ok")
 
 
 @pytest.mark.parametrize("env", [{"SALE_ESWEEP": "1"}, {"SALE_REMAP": "6"}, {"SALE_REMAP": "0"},
-                                 {"SALE_FORCE_E": "1"}, {"SALE_FORCE_E": "1", "SALE_RNODES": "0"}])
+                                 {"SALE_FORCE_E": "1"}, {"SALE_FORCE_E": "1", "SALE_RNODES": "0"},
+                                 {"SALE_GRAPHS": "0"}])
 def test_variant_bitwise(env):
     e = dict(os.environ, **env)
     out = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=e, capture_output=True, text=True, timeout=600)
