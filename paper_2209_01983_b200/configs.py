@@ -39,3 +39,27 @@ def config(name: str, n_gpus: int = 1) -> tuple[dict, int]:
 
 
 CONFIG_NAMES = ("C0", "C1", "C2", "C3", "C4")
+
+
+# ---- further workloads on the same path -----------------
+# One-dimensional problems as degenerate 3D meshes: n cubic cells along x, one
+# cell across, every y/z face reflecting so the flow stays planar.  Their initial
+# states are loaded through set_field (inputs.shock_tube_state / noh_state).
+
+def shock_tube(n: int, rezone: int, **over) -> dict:
+    """Sod's shock tube on [0,1]: walls at both ends,
+    diaphragm at x = 0.5, gamma = 1.4, run to t = 0.2."""
+    cfg = dict(_SEDOV, nx=n, ny=1, nz=1, ly=1.0 / n, lz=1.0 / n, rezone=rezone, gamma=1.4, t_end=0.2,
+               reflect_mask=0x3F)
+    cfg.update(over)
+    return cfg
+
+
+def noh_planar(n: int, **over) -> dict:
+    """Planar Noh implosion on [0,1]: cold gas at u = -1
+    onto a wall at x = 0, free face at x = 1, gamma = 5/3, run to t = 0.6.
+    Lagrangian mode (the Eulerian remap has no inflow boundary: Q18)."""
+    cfg = dict(_SEDOV, nx=n, ny=1, nz=1, ly=1.0 / n, lz=1.0 / n, rezone=LAGRANGE, gamma=5.0 / 3.0,
+               t_end=0.6, reflect_mask=0x3D)
+    cfg.update(over)
+    return cfg

@@ -51,3 +51,33 @@ def uniform_velocity(cfg: dict, u: tuple[float, float, float]):
     """Constant node velocity arrays (no randomness)."""
     nshape = (cfg["nz"] + 1, cfg["ny"] + 1, cfg["nx"] + 1)
     return {n: np.full(nshape, float(v)) for n, v in zip(("ux", "uy", "uz"), u)}
+
+
+# ---- initial states of the further workloads (configs.shock_tube / noh_planar) ----
+# Problem data, not method arithmetic: the caller passes the MASS a fresh context
+# holds (the Sedov init with rho0 = 1 sets m = V, the cell volume), and loads the
+# returned fields into the oracle and the GPU context alike with set_field.
+
+def shock_tube_state(cfg: dict, volume: np.ndarray, x0: float = 0.5, left=(1.0, 1.0), right=(0.125, 0.1)):
+    """Sod: (rho, p) = (1, 1) for cell centres x < x0, (0.125, 0.1) beyond, at rest.
+    volume: the cells' V (cell array).  Returns {"MASS", "E"}; specific energy
+    e = p / ((gamma - 1) rho)."""
+    nx = cfg["nx"]
+    xc = (np.arange(nx) + 0.5) * (cfg["lx"] / nx)
+    lft = (xc < x0)[None, None, :]
+    rho = np.where(lft, left[0], right[0])
+    p = np.where(lft, left[1], right[1])
+    g = cfg["gamma"]
+    return {"MASS": rho * volume, "E": np.broadcast_to(p / ((g - 1.0) * rho), volume.shape).copy()}
+
+
+def noh_state(cfg: dict, u0: float = -1.0, p0: float = 1e-6):
+    """Planar Noh: rho = 1 (the Sedov init's m with rho0 = 1), u_x = u0
+    on every node except the wall plane x = 0 (reflecting, u_x = 0), and a pressure
+    floor p0 = 1e-6 of the dynamic pressure rho u0^2, i.e. e = p0 / ((gamma-1) rho).
+    Returns {"UX", "E"}."""
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    ux = np.full((nz + 1, ny + 1, nx + 1), u0)
+    ux[:, :, 0] = 0.0
+    e = p0 * u0 * u0 / (cfg["gamma"] - 1.0)
+    return {"UX": ux, "E": np.full((nz, ny, nx), e)}
