@@ -159,6 +159,26 @@ def oracle_rate(cfg_sample: dict, seconds: float, min_cycles: int = 3, warm: int
     return cells * n / dt, n, dt
 
 
+def oracle_allcore(name: str, seconds: float):
+    """All-core aggregate of the CPU oracle: one independent
+    single-threaded oracle process per available core on the same bounded sample,
+    run concurrently; the sum of their zone-cycles/s (replica throughput)."""
+    ncore = len(os.sched_getaffinity(0))
+    code = ("import json,sys; sys.path.insert(0, %r); import bench; "
+            "s, _ = bench.sample_cfg(%r); v, n, dt = bench.oracle_rate(s, %r); print(json.dumps(v))"
+            % (ROOT, name, seconds))
+    procs = [subprocess.Popen([sys.executable, "-c", code], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                              text=True) for _ in range(ncore)]
+    rates = []
+    for pr in procs:
+        out, _ = pr.communicate()
+        try:
+            rates.append(float(out.strip().splitlines()[-1]))
+        except Exception:
+            pass
+    return sum(rates), len(rates), ncore
+
+
 def sample_cfg(name: str):
     """A bounded slab of the workload with the same cell size and physics."""
     cfg, _ = configs.config(name, 1)
@@ -210,6 +230,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-allcore", type=int, default=1, help="also time one oracle per host core (0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -345,6 +366,11 @@ def main():
         v, n, dt = oracle_rate(s, args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{desc}; {n} cycles in {dt:.1f} s, single thread, gcc -O2 -ffp-contract=off"}
+        if args.cpu_allcore:
+            agg, nproc, ncore = oracle_allcore(args.config, args.cpu_seconds / 2)
+            cpu["all_cores"] = {"value": agg, "unit": UNIT, "cores": ncore, "processes": nproc,
+                                "what": "one single-threaded oracle process per core on the same sample, "
+                                        "concurrently; sum of their rates (replica throughput)"}
 
     if rank == 0:
         line = {
