@@ -871,12 +871,24 @@ __global__ void __launch_bounds__(RW * NW, 2) kr_nodes(Slab s, Phys p, int cur, 
 // (one thread per node / per cell, operands through L1; high occupancy).
 // ============================================================================
 // grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane: no idle lanes), y = planes
+template <bool TILE>  // TILE: 32 x 8 node tiles (grid x = x-tiles * y-tiles) instead of flattened rows
 __global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
 {
     if (!s.st->active) return;
-    const int t = blockIdx.x * 256 + threadIdx.x;
-    if (t >= (int)s.pn) return;
-    const int i = t % (p.nx + 1), j = t / (p.nx + 1), k = s.k0 + blockIdx.y;
+    int i, j, t;
+    if (TILE) {
+        const int tx = (p.nx + 32) / 32;
+        i = (blockIdx.x % tx) * 32 + (threadIdx.x & 31);
+        j = (blockIdx.x / tx) * 8 + (threadIdx.x >> 5);
+        if (i > p.nx || j > p.ny) return;
+        t = i + (p.nx + 1) * j;
+    } else {
+        t = blockIdx.x * 256 + threadIdx.x;
+        if (t >= (int)s.pn) return;
+        i = t % (p.nx + 1);
+        j = t / (p.nx + 1);
+    }
+    const int k = s.k0 + blockIdx.y;
     const bool pxm = i >= 1, pxp = i < p.nx, pym = j >= 1, pyp = j < p.ny, pzm = k >= 1, pzp = k < p.nz;
     const int c00 = i + p.nx * (j + p.ny * (k - s.kb));  // 32-bit: a slab holds < 2^31 cells
     const int sx = 1, sy = p.nx, sz = p.nx * p.ny;
@@ -1305,7 +1317,9 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
         dim3 grid(cdivr(p.nx + 1, RW - 2), cdivr(p.ny + 1, NW - 2), cdivr(s.k1 - s.k0 + 1, zc));
         kr_nodes<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, zc);
     } else {
-        kn_update<<<dim3(cdivr((int)s.pn, 256), s.k1 - s.k0 + 1), 256, 0, cs>>>(s, p, cur);
+        // 32 x 8 node tiles: the gathered cell values are reused inside a block through L1
+        // (measured faster than full-lane flattened rows despite the ragged last tile)
+        kn_update<true><<<dim3(cdivr(p.nx + 1, 32) * cdivr(p.ny + 1, 8), s.k1 - s.k0 + 1), 256, 0, cs>>>(s, p, cur);
         if (euler_pre_sigma()) return 3;  // the next cycle's kf_sigma_e evaluates the dt candidate
         kn_dt<<<dim3(cdivr((int)s.pc, 256), s.k1 - s.k0), 256, 0, cs>>>(s, p, cur);
         return 4;
