@@ -1398,12 +1398,12 @@ static void energy_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc
     kf_energy<EULER, NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
 }
 
-// tile / chunk choice (SALE_TUNE="nwf,nwe,zchunk" overrides, for tuning runs)
+// z-chunk length of the z-marching grids (SALE_ZCHUNK overrides, for tuning runs)
 struct Tune {
-    int nwf = NW_FORCE, nwe = NW_ENERGY, zc = ZCHUNK;
+    int zc = ZCHUNK;
     Tune()
     {
-        if (const char* t = getenv("SALE_TUNE")) sscanf(t, "%d,%d,%d", &nwf, &nwe, &zc);
+        if (const char* t = getenv("SALE_ZCHUNK")) zc = atoi(t);
         if (zc < 4) zc = 4;
     }
 };
@@ -1481,38 +1481,20 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
     static const Tune tune;
     cudaStream_t cs = (cudaStream_t)st;
-    // node planes updated / cell planes energised (Euler: plus the ghost region the remap needs)
-    int kn0, kn1;
-    if (!EULER) {
-        kn0 = s.k0;
-        kn1 = s.k1;
+    if constexpr (EULER) {
+        // node planes updated / cell planes energised, plus the ghost region the remap needs
+        const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
+        if (euler_pre_sigma())  // split form: kf_sigma_e ran before the cycle's k_begin
+            kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, cs>>>(s, p, cur, kn0);
+        else  // SALE_FORCE_E=1: the one-kernel form
+            force_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
+        // kf_energy_e also writes the moved-face s' kr_sweep reads (Slab::sF)
+        if (euler_esweep_variant() > 0) esweep_launch<12, 1>(s, p, cur, kn0, kn1, tune.zc, cs);
+        else energy_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
     } else {
-        kn0 = imax_h(s.k0 - 2, 0);
-        kn1 = imin_h(s.k1 + 2, p.nz);
+        force_launch<false, NW_FORCE>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, MINB>(s, p, cur, s.k0, s.k1, tune.zc, cs);
     }
-    const int kc0 = kn0, kc1 = kn1;
-    static const int fe = [] {
-        const char* v = getenv("SALE_FORCE_E");
-        return v ? atoi(v) : 12;
-    }();
-    if (EULER && fe >= 9) {  // split form: kf_sigma_e ran before the cycle's k_begin (euler_pre)
-        kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, cs>>>(s, p, cur, kn0);
-    } else if (EULER && fe == 1) force_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
-    else if (EULER && fe == 2) force_e_launch<8, 3>(s, p, cur, kn0, kn1, tune.zc, cs);
-    else if (EULER && fe == 3) force_e_launch<12, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
-    else if (EULER && fe == 4) force_e_launch<16, 1>(s, p, cur, kn0, kn1, tune.zc, cs);
-    else if (tune.nwf == 15) force_launch<EULER, 15>(s, p, cur, kn0, kn1, tune.zc, cs);
-    else if (tune.nwf >= 16) force_launch<EULER, 16>(s, p, cur, kn0, kn1, tune.zc, cs);
-    else if (tune.nwf >= 12) force_launch<EULER, 12>(s, p, cur, kn0, kn1, tune.zc, cs);
-    else force_launch<EULER, 8>(s, p, cur, kn0, kn1, tune.zc, cs);
-    // Euler: kf_energy_e also writes the moved-face s' kr_sweep reads (Slab::sF)
-    const int esw = euler_esweep_variant();
-    if (EULER && esw > 0) esweep_launch<12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else if (EULER) energy_e_launch<8, 2>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else if (tune.nwe == 15) energy_launch<EULER, 15, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else if (tune.nwe >= 16) energy_launch<EULER, 16, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else if (tune.nwe >= 12) energy_launch<EULER, 12, 1>(s, p, cur, kc0, kc1, tune.zc, cs);
-    else energy_launch<EULER, 8, MINB>(s, p, cur, kc0, kc1, tune.zc, cs);
     return 2;
 }
 
@@ -1522,9 +1504,9 @@ bool euler_pre_sigma()
 {
     static const int fe = [] {
         const char* v = getenv("SALE_FORCE_E");
-        return v ? atoi(v) : 12;
+        return v ? atoi(v) : 0;
     }();
-    return fe >= 9;
+    return fe != 1;
 }
 int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
 {

@@ -1258,25 +1258,7 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
 
         dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, zc));
         kr_cells<NW><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zc);
-    } else if (variant == 1) {
-        constexpr int NW = 7, MB = 2;
-        const size_t sm = sizeof(double) * RemapCellsP<NW>::WORDS;
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(kr_cells_p<NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            init = true;
-        }
-        const int zc = zchunk_for((long long)cdivr(p.nx, RW - 3) * cdivr(p.ny, NW - 3), kr1 - kr0, RZ);
-
-        dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, zc));
-        kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zc);
-    } else if (variant == 2) {
-        cells_p_launch<12, 1>(s, p, cur, kr0, kr1, cs);
-    } else if (variant == 3) {
-        cells_p_launch<8, 1>(s, p, cur, kr0, kr1, cs);
-    } else if (variant == 4) {
-        cells_p_launch<10, 1>(s, p, cur, kr0, kr1, cs);
-    } else if (variant >= 7) {
+    } else if (variant == 7) {  // default: kr_sweep + kr_flux
         auto sweep = [&](auto kern, int nw, size_t words) {
             static bool init = false;
             if (!init) {
@@ -1289,16 +1271,11 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
             dim3 grid(cdivr(p.nx, RW - 1), cdivr(p.ny, nw - 1), cdivr(t1 - t0 + 1, zc));
             kern<<<grid, dim3(RW, nw), sizeof(double) * words, cs>>>(s, p, cur, kr0, kr1, zc);
         };
-        if (euler_esweep_variant() > 0) {
-        }  // swept volumes and donor data came with kx_energy_sweep
-        else if (variant == 7) sweep(kr_sweep<8, 2>, 8, SweepCTA<8>::WORDS);
-        else if (variant == 8) sweep(kr_sweep<8, 3>, 8, SweepCTA<8>::WORDS);
-        else if (variant == 9) sweep(kr_sweep<16, 1>, 16, SweepCTA<16>::WORDS);
-        else sweep(kr_sweep<12, 2>, 12, SweepCTA<12>::WORDS);
+        // (with kx_energy_sweep the swept volumes and donor data came with the energy kernel)
+        if (euler_esweep_variant() == 0) sweep(kr_sweep<8, 2>, 8, SweepCTA<8>::WORDS);
         kr_flux<<<dim3(cdivr(p.nx, 32), cdivr(p.ny, 8), kr1 - kr0), dim3(32, 8), 0, cs>>>(s, p, cur, kr0);
-    } else {
-        if (variant == 5) cells_p_launch<14, 1>(s, p, cur, kr0, kr1, cs);
-        else cells_p_launch<15, 1>(s, p, cur, kr0, kr1, cs);
+    } else {  // SALE_REMAP=6: the one-kernel software-pipelined remap
+        cells_p_launch<15, 1>(s, p, cur, kr0, kr1, cs);
     }
     static const int nvariant = [] {
         const char* v = getenv("SALE_RNODES");
