@@ -209,6 +209,31 @@ int32_t sale_halo_plan(const sale_params* p, int32_t full, sale_halo_msg* out, i
 int32_t sale_local_layout(const sale_params* p, int32_t* k0, int32_t* k1, int32_t* ghost,
                           int32_t* node_planes, int32_t* cell_planes);
 
+/* ---- Steinberg shear modulus and yield stress --------
+ * The paper's own extension example (Fig. 6b): for every owned cell of
+ * the current state,
+ *   eta   = rho0 / rho                      rho = m / V   (as get_field RHO)
+ *   shear = (G0 + (GP * p) * eta^(1/3)) + GT * (T - T0)     p as get_field P
+ *   yield = min(Y0 * (1 + beta * eps_p)^n, Ymax) * (shear / G0)
+ * with the readings of DESIGN.md §10c: T = e / cv (ideal gas), uniform reference
+ * density rho0 and initial temperature T0.  eta^(1/3) is cbrt(eta) here and the
+ * paper's eta**(1d0/3) = pow(eta, 1/3) in the oracle; neither cbrt nor pow is
+ * correctly rounded, so results agree with the oracle to a few ulp (tests: 1e-14
+ * relative), not bitwise. */
+typedef struct sale_steinberg_params {
+    double G0, GP, GT;        /* shear modulus at reference; pressure / temperature slopes */
+    double Y0, Ymax, beta, n; /* yield: Y0 (1 + beta eps_p)^n capped at Ymax             */
+    double cv, rho0, T0;      /* T = e / cv; eta = rho0 / rho; T - T0                     */
+} sale_steinberg_params;
+/* eps_p: plastic strain per owned cell, or NULL for zero; shear, yield: outputs.
+ * All three are DEVICE pointers with the layout and count of get_field's cell
+ * fields (count = owned cells; emulated slabs concatenated in plane order).
+ * Asynchronous on the context's stream (synchronises first with pending cycles);
+ * the call launches one kernel per slab.  SALE_EINVAL on NULL / count mismatch,
+ * SALE_EPOISONED on a poisoned context. */
+int32_t sale_steinberg(sale_ctx* c, const sale_steinberg_params* sp, const double* eps_p, double* shear,
+                       double* yield, uint64_t count);
+
 /* human-readable detail of the last error: code, cycle, cell, CUDA/NCCL text */
 const char* sale_last_error(const sale_ctx* c);
 

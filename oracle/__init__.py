@@ -81,6 +81,10 @@ def lib() -> C.CDLL:
             L.oracle_last_error_cell.restype = i64
             L.oracle_next_dt.argtypes = [vp, P(d)]
             L.oracle_next_dt.restype = i32
+            L.oracle_steinberg_point.argtypes = [P(OracleSteinberg), d, d, d, d, P(d), P(d)]
+            L.oracle_steinberg_point.restype = None
+            L.oracle_steinberg.argtypes = [vp, P(OracleSteinberg), vp, P(d), P(d), u64]
+            L.oracle_steinberg.restype = i32
             L.oracle_destroy.argtypes = [vp]
             L.oracle_destroy.restype = None
             L.oracle_face.argtypes = [P(d), P(d), P(d), P(d)]
@@ -99,6 +103,20 @@ def lib() -> C.CDLL:
             L.oracle_cell_energy.restype = d
             _lib = L
     return _lib
+
+
+class OracleSteinberg(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("G0", "GP", "GT", "Y0", "Ymax", "beta", "n", "cv", "rho0", "T0")]
+
+
+def steinberg_params(d: dict) -> OracleSteinberg:
+    return OracleSteinberg(*[float(d[n]) for n, _ in OracleSteinberg._fields_])
+
+
+def steinberg_point(params: dict, p, rho, e, eps_p=0.0):
+    sh, y = C.c_double(), C.c_double()
+    lib().oracle_steinberg_point(C.byref(steinberg_params(params)), p, rho, e, eps_p, C.byref(sh), C.byref(y))
+    return sh.value, y.value
 
 
 def _dp(a: np.ndarray):
@@ -171,6 +189,17 @@ class Oracle:
         dt = C.c_double()
         rc = self._L.oracle_next_dt(self._h, C.byref(dt))
         return rc, dt.value
+
+    def steinberg(self, params: dict, eps_p=None):
+        """Shear modulus and yield stress of every cell (Fig. 6b; oracle.h)."""
+        sh = np.empty(self.cell_shape)
+        y = np.empty(self.cell_shape)
+        e = None if eps_p is None else np.ascontiguousarray(eps_p, dtype=np.float64)
+        rc = self._L.oracle_steinberg(self._h, C.byref(steinberg_params(params)),
+                                      None if e is None else e.ctypes.data, _dp(sh), _dp(y), sh.size)
+        if rc != OK:
+            raise ValueError(f"oracle_steinberg rc={rc}")
+        return sh, y
 
     def last_error(self) -> str:
         return self._L.oracle_last_error(self._h).decode()

@@ -891,3 +891,36 @@ double oracle_cell_energy(const double* N0f, const double* U0f, const double* U1
         }
     return energy_update(N0, U0, U1, sigma, m, e, dt);
 }
+
+/* ---- Steinberg (Fig. 6b) ------------------------ */
+void oracle_steinberg_point(const oracle_steinberg_params* sp, double p, double rho, double e, double eps_p,
+                            double* shear, double* yield)
+{
+    const double eta = sp->rho0 / rho;
+    const double T = e / sp->cv;
+    const double G = (sp->G0 + (sp->GP * p) * pow(eta, 1.0 / 3.0)) + sp->GT * (T - sp->T0);
+    const double h = sp->Y0 * pow(1.0 + sp->beta * eps_p, sp->n);
+    *shear = G;
+    *yield = ((h < sp->Ymax) ? h : sp->Ymax) * (G / sp->G0);
+}
+
+int32_t oracle_steinberg(oracle_ctx* c, const oracle_steinberg_params* sp, const double* eps_p, double* shear,
+                         double* yield, uint64_t count)
+{
+    if (!c || !sp || !shear || !yield || count != (uint64_t)c->ncell) return ORACLE_EINVAL;
+    double* rho = (double*)malloc(sizeof(double) * (size_t)c->ncell);
+    double* pr = (double*)malloc(sizeof(double) * (size_t)c->ncell);
+    if (!rho || !pr) {
+        free(rho);
+        free(pr);
+        return ORACLE_EINVAL;
+    }
+    int32_t rc = oracle_get_field(c, ORACLE_F_RHO, rho, count);
+    if (!rc) rc = oracle_get_field(c, ORACLE_F_P, pr, count);
+    for (int64_t K = 0; !rc && K < c->ncell; ++K)
+        oracle_steinberg_point(sp, pr[K], rho[K], c->e[K], eps_p ? eps_p[K] : 0.0, &shear[K], &yield[K]);
+    free(rho);
+    free(pr);
+    return rc;
+}
+

@@ -98,6 +98,28 @@ double oracle_swept_volume(const double* PT, const double* PL);
 double oracle_cell_energy(const double* N0, const double* U0, const double* U1,
                           double sigma, double m, double e, double dt);
 
+/* ---- Steinberg shear modulus and yield stress --------
+ * The paper's extension example, Fig. 6b, per cell:
+ *   eta = rho0 / rho
+ *   shear = (G0 + (GP * p) * eta^(1/3)) + GT * (T - T0)
+ *   yield = min(Y0 * (1 + beta * eps_p)^n, Ymax) * (shear / G0)
+ * with p the cell pressure of the EoS and rho = m / V of the current state; the
+ * readings: temperature T = e / cv (ideal gas), a uniform
+ * reference density rho0 and initial temperature T0, eta^(1/3) = pow(eta, 1/3) as
+ * the paper's eta**(1d0/3). */
+typedef struct oracle_steinberg_params {
+    double G0, GP, GT;        /* shear modulus at reference; pressure, temperature slopes */
+    double Y0, Ymax, beta, n; /* yield: Y0 (1 + beta eps_p)^n capped at Ymax             */
+    double cv, rho0, T0;      /* T = e / cv; eta = rho0 / rho; T - T0                     */
+} oracle_steinberg_params;
+/* one cell from its (p, rho, e, eps_p) */
+void oracle_steinberg_point(const oracle_steinberg_params* sp, double p, double rho, double e, double eps_p,
+                            double* shear, double* yield);
+/* every cell of the current state; eps_p: cell array or NULL (all zero); shear,
+ * yield: cell arrays (count = nx*ny*nz). */
+int32_t oracle_steinberg(oracle_ctx* c, const oracle_steinberg_params* sp, const double* eps_p, double* shear,
+                         double* yield, uint64_t count);
+
 #ifdef __cplusplus
 }
 #endif

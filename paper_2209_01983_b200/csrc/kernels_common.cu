@@ -377,4 +377,49 @@ int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st)
     return 1;
 }
 
+// ------------------------------------------------ Steinberg (Fig. 6b)
+// One thread per owned cell: rho = m / V and p exactly as get_field's RHO / P, then
+// the paper's shear / yield loop body (association as written there).
+template <bool EULER>
+__global__ void __launch_bounds__(256) k_steinberg(Slab s, Phys p, int cur, SteinbergP sp, const double* eps,
+                                                   double* sh, double* y)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long total = s.pc * (s.k1 - s.k0);
+    if (t >= total) return;
+    const int k = s.k0 + (int)(t / s.pc);
+    const long long r = t % s.pc;
+    const int j = (int)(r / p.nx), i = (int)(r % p.nx);
+    const long long c = cidx(s, p, i, j, k);
+    double V;
+    if (EULER) {
+        V = s.VT[c];  // the fixed mesh's volume (same formula, evaluated at create)
+    } else {
+        D3 N[8], A[6], Xb[6];
+        double sv[6];
+        load_hex_pos<EULER>(s, p, cur, i, j, k, N);
+        hex_faces(N, A, Xb, sv);
+        V = vol_from_s(sv);
+    }
+    const double e = s.e[cur][c];
+    double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
+    eos(p.gamma, rho, e, pr, pf, cs);
+    const double eta = sp.rho0 / rho;
+    const double T = e / sp.cv;
+    // eta^(1/3): cbrt (within an ulp of the paper's pow(eta, 1/3), at a fraction of its cost)
+    const double G = (sp.G0 + (sp.GP * pr) * cbrt(eta)) + sp.GT * (T - sp.T0);
+    const double h = sp.Y0 * pow(1.0 + sp.beta * (eps ? eps[t] : 0.0), sp.n);
+    sh[t] = G;
+    y[t] = ((h < sp.Ymax) ? h : sp.Ymax) * (G / sp.G0);
+}
+
+int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergP& sp, const double* eps, double* sh,
+                     double* y, Stream st)
+{
+    const long long n = s.pc * (s.k1 - s.k0);
+    if (p.rezone) k_steinberg<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, sp, eps, sh, y);
+    else k_steinberg<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, sp, eps, sh, y);
+    return 1;
+}
+
 }  // namespace sale

@@ -767,6 +767,25 @@ int32_t sale_step(sale_ctx* c, int32_t ncycles, int32_t* cycles_done)
     return sale_sync(c, cycles_done);
 }
 
+int32_t sale_steinberg(sale_ctx* c, const sale_steinberg_params* sp, const double* eps_p, double* shear,
+                       double* yield, uint64_t count)
+{
+    if (!c || !sp || !shear || !yield) return SALE_EINVAL;
+    if (count != expected_count(c, SALE_F_MASS)) return SALE_EINVAL;
+    if (c->poisoned) return SALE_EPOISONED;
+    DeviceGuard guard(c->prm.device);
+    int rc = sync_state(c, nullptr);
+    if (rc) return rc;
+    const sale::SteinbergP P{sp->G0, sp->GP, sp->GT, sp->Y0, sp->Ymax, sp->beta, sp->n, sp->cv, sp->rho0, sp->T0};
+    const size_t plane = (size_t)c->slabs[0].pc;
+    for (auto& s : c->slabs) {
+        const size_t off = c->prm.local_slabs > 1 ? (size_t)s.k0 * plane : 0;
+        c->launches += sale::launch_steinberg(s, c->phys, c->cur, P, eps_p ? eps_p + off : nullptr, shear + off,
+                                              yield + off, (sale::Stream)c->stream);
+    }
+    return launch_check(c);
+}
+
 int32_t sale_get_field(sale_ctx* c, int32_t field, double* dst, uint64_t count, int32_t dst_on_device)
 {
     if (!c || !dst || !(is_node_field(field) || is_cell_field(field))) return SALE_EINVAL;

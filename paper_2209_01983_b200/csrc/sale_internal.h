@@ -83,6 +83,11 @@ struct Slab {
     DevState* st;
 };
 
+// Steinberg model parameters (copy of sale_steinberg_params, by value into the kernel)
+struct SteinbergP {
+    double G0, GP, GT, Y0, Ymax, beta, n, cv, rho0, T0;
+};
+
 // status codes mirrored from include/sale.h (kept in sync by a static_assert in host code)
 enum { S_OK = 0, S_EINVAL = 1, S_ENOMEM = 2, S_ECUDA = 3, S_ENCCL = 4, S_ETANGLED = 5,
        S_EDTCOLLAPSE = 6, S_ENEGMASS = 7, S_EPOISONED = 8, S_EREPLICA = 9 };
@@ -103,6 +108,9 @@ int launch_commit(DevState* d, const Phys& p, Stream st);
 int launch_reset_good(DevState* d, Stream st);
 int launch_dt_candidate(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st);
+// Steinberg shear / yield of the owned cells (include/sale.h); outputs at sh / y (device)
+int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergP& sp, const double* eps, double* sh,
+                     double* y, Stream st);
 // one cycle on one slab, reading buffers [cur], writing [cur^1]:
 // the Lagrangian phase (S1-S7; Lagrange mode also the next dt candidate), then
 // in Euler mode the remap (R1-R5 + next dt candidate)

@@ -27,8 +27,8 @@ NODE_FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "NODE_MASS")
 EXPORTS = ("sale_workspace_bytes", "sale_nccl_unique_id", "sale_create", "sale_step",
            "sale_step_async", "sale_sync", "sale_get_field", "sale_set_field", "sale_get_clock",
            "sale_set_clock", "sale_get_layout", "sale_kernel_launches", "sale_profile_enable",
-           "sale_profile_read", "sale_halo_plan", "sale_local_layout", "sale_last_error",
-           "sale_destroy")
+           "sale_profile_read", "sale_halo_plan", "sale_local_layout", "sale_steinberg",
+           "sale_last_error", "sale_destroy")
 K_CLASSES = ("begin", "prologue", "lagrange", "remap", "halo")
 
 
@@ -43,6 +43,10 @@ class SaleParams(C.Structure):
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
                 ("device", C.c_int32), ("impl", C.c_int32), ("local_slabs", C.c_int32),
                 ("reserved", C.c_int32)]
+
+
+class SaleSteinberg(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("G0", "GP", "GT", "Y0", "Ymax", "beta", "n", "cv", "rho0", "T0")]
 
 
 class SaleHaloMsg(C.Structure):
@@ -102,6 +106,8 @@ def lib() -> C.CDLL:
             L.sale_halo_plan.restype = i32
             L.sale_local_layout.argtypes = [P(SaleParams), P(i32), P(i32), P(i32), P(i32), P(i32)]
             L.sale_local_layout.restype = i32
+            L.sale_steinberg.argtypes = [vp, P(SaleSteinberg), vp, vp, vp, u64]
+            L.sale_steinberg.restype = i32
             L.sale_last_error.argtypes = [vp]
             L.sale_last_error.restype = C.c_char_p
             L.sale_destroy.argtypes = [vp]
@@ -241,6 +247,25 @@ class Sale:
         if rc:
             raise SaleError(rc, f"sale_get_field({field}): " + self.last_error())
         return arr
+
+    def steinberg(self, params: dict, eps_p=None, out=None):
+        """Steinberg shear modulus and yield stress of the owned cells (Fig. 6b;
+        include/sale.h sale_steinberg).  eps_p: plastic strain (array of the cell
+        shape) or None.  Returns (shear, yield) as float64 device tensors (or fills
+        the pair `out`)."""
+        import torch
+        sp = SaleSteinberg(*[float(params[n]) for n, _ in SaleSteinberg._fields_])
+        sh, y = out if out is not None else (torch.empty(self.cell_shape, dtype=torch.float64, device=self.torch_device),
+                                             torch.empty(self.cell_shape, dtype=torch.float64, device=self.torch_device))
+        ep = None
+        if eps_p is not None:
+            ep = torch.as_tensor(np.ascontiguousarray(eps_p, dtype=np.float64)).to(self.torch_device) \
+                if not hasattr(eps_p, "data_ptr") else eps_p
+        rc = self._L.sale_steinberg(self._h, C.byref(sp), None if ep is None else ep.data_ptr(), sh.data_ptr(),
+                                    y.data_ptr(), sh.numel())
+        if rc:
+            raise SaleError(rc, "sale_steinberg: " + self.last_error())
+        return sh, y
 
     def set(self, field: str, arr) -> None:
         if hasattr(arr, "data_ptr"):  # torch tensor: device, or (pinned) host memory
