@@ -706,11 +706,17 @@ __global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int k
         if (!pres) continue;
         const int ci = i - 1 + ap, cj = j - 1 + bp, ckl = kl - 1 + cp;
         const int ox = ckl * ny + cj, oy = ckl * nx + ci, oz = cj * nx + ci;
-        const D3 Ax = D3{__ldg(s.TAx[0] + ox), __ldg(s.TAx[1] + ox), __ldg(s.TAx[2] + ox)};
-        const D3 Ay = D3{__ldg(s.TAy[0] + oy), __ldg(s.TAy[1] + oy), __ldg(s.TAy[2] + oy)};
-        const D3 Az = D3{__ldg(s.TAz[0] + oz), __ldg(s.TAz[1] + oz), __ldg(s.TAz[2] + oz)};
         // cell (i-1+ap, j-1+bp, k-1+cp): the node is its corner (1-ap, 1-bp, 1-cp)
-        const D3 C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
+        D3 C;
+        if (p.diag_areas) {  // axis-aligned areas: ((+-a, 0, 0) + (0, +-b, 0)) + (0, 0, +-c) exactly
+            const double ax = __ldg(s.TAx[0] + ox), ay = __ldg(s.TAy[1] + oy), az = __ldg(s.TAz[2] + oz);
+            C = D3{ap ? -ax : ax, bp ? -ay : ay, cp ? -az : az};
+        } else {
+            const D3 Ax = D3{__ldg(s.TAx[0] + ox), __ldg(s.TAx[1] + ox), __ldg(s.TAx[2] + ox)};
+            const D3 Ay = D3{__ldg(s.TAy[0] + oy), __ldg(s.TAy[1] + oy), __ldg(s.TAy[2] + oy)};
+            const D3 Az = D3{__ldg(s.TAz[0] + oz), __ldg(s.TAz[1] + oz), __ldg(s.TAz[2] + oz)};
+            C = add(add(ap ? neg(Ax) : Ax, bp ? neg(Ay) : Ay), cp ? neg(Az) : Az);
+        }
         const int c = c11 + (ap - 1) + nx * (bp - 1) + pc * (cp - 1);
         const D3 term = scl(__ldg(s.sig + c), C);
         const double mk = __ldg(s.m[cur] + c);
@@ -1077,10 +1083,13 @@ struct EnergyEulerCTA {
             const D3 A[6] = {ld3s(me, oF(0, 0), PL),      ld3s(me + 1, oF(0, 0), PL), ld3s(me, oF(1, 0), PL),
                              ld3s(me + FW, oF(1, 0), PL), Az,                         Az};
             double W = 0.0;
+            const bool dg = p.diag_areas;
 #pragma unroll
             for (int h = 0; h < 8; ++h) {
                 const int a = h & 1, b = (h >> 1) & 1, c = h >> 2;
-                const D3 C = corner_vec(A, a, b, c);
+                // axis-aligned areas: the corner vector is exactly (+-Ax.x, +-Ay.y, +-Az.z)
+                const D3 C = dg ? D3{a ? A[1].x : -A[0].x, b ? A[3].y : -A[2].y, c ? A[5].z : -A[4].z}
+                                : corner_vec(A, a, b, c);
                 const D3 ub = c ? Ub<B1>(a + b * FW) : Ub<B0>(a + b * FW);
                 const double term = dot(C, ub);
                 W = (h == 0) ? term : W + term;
@@ -1289,10 +1298,13 @@ struct EnergySweepCTA {
             const D3 Az = ld3s(me, oZ(), PL);
             const D3 A[6] = {ax, ld3s(me + 1, oF(0, 0), PL), ay, ld3s(me + FW, oF(1, 0), PL), Az, Az};
             double W = 0.0;
+            const bool dg = p.diag_areas;
 #pragma unroll
             for (int h = 0; h < 8; ++h) {
                 const int a = h & 1, b = (h >> 1) & 1, c = h >> 2;
-                const D3 C = corner_vec(A, a, b, c);
+                // axis-aligned areas: the corner vector is exactly (+-Ax.x, +-Ay.y, +-Az.z)
+                const D3 C = dg ? D3{a ? A[1].x : -A[0].x, b ? A[3].y : -A[2].y, c ? A[5].z : -A[4].z}
+                                : corner_vec(A, a, b, c);
                 const D3 ub = c ? Ub<B1>(a + b * FW) : Ub<B0>(a + b * FW);
                 const double term = dot(C, ub);
                 W = (h == 0) ? term : W + term;

@@ -648,6 +648,37 @@ const double* field_src(sale_ctx* c, const Slab& s, int field)
     return s.der;
 }
 
+
+// Euler: read the target face-area tables back once and set Phys::diag_areas when
+// every x-face area is (a, 0, 0), y-face (0, b, 0), z-face (0, 0, c) with a, b, c
+// non-zero and the zeros exact (true for the tensor-product target mesh): the
+// kernels then form corner vectors from the diagonal components only (same bits).
+int check_diag_areas(sale_ctx* c)
+{
+    bool diag = true;
+    std::vector<double> h;
+    for (auto& s : c->slabs) {
+        const long long n[3] = {(long long)c->phys.ny * s.nzc, (long long)c->phys.nx * s.nzc,
+                                (long long)c->phys.nx * c->phys.ny};
+        double* const* T[3] = {s.TAx, s.TAy, s.TAz};
+        for (int f = 0; f < 3 && diag; ++f)
+            for (int comp = 0; comp < 3 && diag; ++comp) {
+                h.resize((size_t)n[f]);
+                int rc = cuda_check(c, cudaMemcpy(h.data(), T[f][comp], sizeof(double) * (size_t)n[f],
+                                                  cudaMemcpyDeviceToHost),
+                                    "area tables");
+                if (rc) return rc;
+                for (double v : h)
+                    if ((comp == f) ? !(v != 0.0) : v != 0.0) {
+                        diag = false;
+                        break;
+                    }
+            }
+    }
+    c->phys.diag_areas = diag ? 1 : 0;
+    return SALE_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -727,6 +758,7 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
         rc = launch_check(c);
     }
     if (!rc) rc = cuda_check(c, cudaStreamSynchronize(c->stream), "create sync");
+    if (!rc && ph.rezone) rc = check_diag_areas(c);
     if (rc) {
         if (c->comm) ncclCommDestroy(c->comm);
         cudaFreeHost(c->hstate);

@@ -15,6 +15,9 @@ struct Phys {
     int nx, ny, nz;           // global cells
     unsigned reflect;         // bit f: face f of {-x,+x,-y,+y,-z,+z} reflects
     int rezone;               // 0 Lagrange, 1 Euler
+    int diag_areas;           // Euler: every target face area vector is axis-aligned (off-diagonal
+                              // components exactly zero, diagonal non-zero; checked at create), so
+                              // a corner vector (c.2) is exactly (+-Ax.x, +-Ay.y, +-Az.z)
 };
 
 // Device-resident clock and status (one per context; all local slabs share it).
