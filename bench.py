@@ -43,7 +43,7 @@ ALGO_BYTES = {configs.LAGRANGE: 120.0, configs.EULER: 80.0}
 # once; Euler: the t^n geometry of the fixed target mesh is loop-invariant and the
 # moved-face s' of S7 are shared with R1 -- DESIGN.md §7)
 ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 661.0, "remap": 0.0},
-             configs.EULER: {"lagrange": 404.0, "remap": 406.0}}
+             configs.EULER: {"lagrange": 362.0, "remap": 406.0}}
 # kernel name prefixes of each timing class (for the ncu traffic file)
 CLASS_KERNELS = {"lagrange": ("kf_", "kn_force", "kx_"), "remap": ("kr_", "kn_update", "kn_dt")}
 REASON_BITS = {"hw_slowdown": "hw_slowdown", "hw_thermal_slowdown": "hw_thermal_slowdown",

@@ -545,7 +545,12 @@ __global__ void __launch_bounds__(FW * NW, MB) kf_force_e(Slab s, Phys p, int cu
 //                fixed order of c.2 with the target face areas from the tables,
 //                kinematics + reflecting BC (S5, S6).  Writes u', x'.
 // ============================================================================
-template <int NW>
+// DIAG: the target mesh's axis-jump separations lie on their axes (Phys::diag_jumps).
+// Then w . d = (w_a d_a + w_b * 0) + w_c * 0 equals w_a d_a whenever that is non-zero,
+// and when it is zero the jump is a zero of some sign, which q ignores (q depends on
+// du only through du < 0 and, when negative, its value): sigma is the same bits with
+// only the a-component of the face-average velocity on axis a.
+template <int NW, bool DIAG>
 struct SigmaEulerCTA {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
     __host__ __device__ static constexpr int oU(int par, int c) { return (par * 3 + c) * PL; }       // node u
@@ -615,11 +620,25 @@ struct SigmaEulerCTA {
         const double m = pm, e = pe, V = pv;
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
-        const D3 ux = avg4(U<B0>(0), U<B0>(FW), U<B1>(FW), U<B1>(0));
-        const D3 uy = avg4(U<B0>(0), U<B1>(0), U<B1>(1), U<B0>(1));
-        const D3 uz = avg4(U<B1>(0), U<B1>(1), U<B1>(FW + 1), U<B1>(FW));
-        st3s(me, oW(0, 0), PL, ux);
-        st3s(me, oW(1, 0), PL, uy);
+        D3 ux, uy, uz;
+        if constexpr (DIAG) {  // the a-component of the face average on axis a only (c.3 step 2)
+            const double* Ux0 = me + oU(B0, 0);
+            const double* Ux1 = me + oU(B1, 0);
+            const double* Uy0 = me + oU(B0, 1);
+            const double* Uy1 = me + oU(B1, 1);
+            const double* Uz1 = me + oU(B1, 2);
+            ux.x = 0.25 * (((Ux0[0] + Ux0[FW]) + Ux1[FW]) + Ux1[0]);
+            uy.y = 0.25 * (((Uy0[0] + Uy1[0]) + Uy1[1]) + Uy0[1]);
+            uz.z = 0.25 * (((Uz1[0] + Uz1[1]) + Uz1[FW + 1]) + Uz1[FW]);
+            me[oW(0, 0)] = ux.x;
+            me[oW(1, 0)] = uy.y;
+        } else {
+            ux = avg4(U<B0>(0), U<B0>(FW), U<B1>(FW), U<B1>(0));
+            uy = avg4(U<B0>(0), U<B1>(0), U<B1>(1), U<B0>(1));
+            uz = avg4(U<B1>(0), U<B1>(1), U<B1>(FW + 1), U<B1>(FW));
+            st3s(me, oW(0, 0), PL, ux);
+            st3s(me, oW(1, 0), PL, uy);
+        }
         // max node speed^2 of the cell in corner order (read here, before the barrier:
         // the next step's P1 overwrites the plane-kz slot)
         double v2 = speed2(U<B0>(0));
@@ -641,9 +660,16 @@ struct SigmaEulerCTA {
         if (out_cell && kz >= 0 && kz < p.nz) {
             double rho = ddiv(m, V), pr, pf, cs;
             eos(p.gamma, rho, e, pr, pf, cs);
-            const double dx = jump(tj[0], ux, ld3s(me + 1, oW(0, 0), PL));
-            const double dy = jump(tj[1], uy, ld3s(me + FW, oW(1, 0), PL));
-            const double dz = jump(tj[2], zprev, uz);
+            double dx, dy, dz;
+            if constexpr (DIAG) {
+                dx = ddiv((me[1 + oW(0, 0)] - ux.x) * tj[0][0], tj[0][3]);
+                dy = ddiv((me[FW + oW(1, 0)] - uy.y) * tj[1][1], tj[1][3]);
+                dz = ddiv((uz.z - zprev.z) * tj[2][2], tj[2][3]);
+            } else {
+                dx = jump(tj[0], ux, ld3s(me + 1, oW(0, 0), PL));
+                dy = jump(tj[1], uy, ld3s(me + FW, oW(1, 0), PL));
+                dz = jump(tj[2], zprev, uz);
+            }
             const double du = dmin(dmin(dx, dy), dz);
             const double q = q_of_du(rho, cs, du, p.c1, p.c2);
             s.sig[cb + (long long)kz * s.pc] = 0.25 * (pf + q);
@@ -666,6 +692,7 @@ struct SigmaEulerCTA {
         fetch(za + 1);
         __syncthreads();
         zprev = (za & 1) ? avg4(U<1>(0), U<1>(1), U<1>(FW + 1), U<1>(FW)) : avg4(U<0>(0), U<0>(1), U<0>(FW + 1), U<0>(FW));
+        if constexpr (DIAG) zprev = D3{0.0, 0.0, zprev.z};
         for (int kz = za; kz <= zb; ++kz) {
             if (kz & 1) step<1>(kz);
             else step<0>(kz);
@@ -675,12 +702,12 @@ struct SigmaEulerCTA {
 };
 
 // gate = 0 for the first cycle of a sale_step call (DevState.active is still 0 there)
-template <int NW, int MB>
+template <int NW, int MB, bool DIAG>
 __global__ void __launch_bounds__(FW * NW, MB) kf_sigma_e(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk, int gate)
 {
     if (gate && !s.st->active) return;
     extern __shared__ double smem[];
-    SigmaEulerCTA<NW> c(s, p, cur, smem, kc0, kc1, zchunk);
+    SigmaEulerCTA<NW, DIAG> c(s, p, cur, smem, kc0, kc1, zchunk);
     c.run();
 }
 
@@ -1448,18 +1475,18 @@ static void energy_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int 
     kf_energy_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
 }
 
-template <int NW, int MB>
+template <int NW, int MB, bool DIAG>
 static void sigma_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, int gate, cudaStream_t cs)
 {
-    const size_t sm = sizeof(double) * SigmaEulerCTA<NW>::WORDS;
+    const size_t sm = sizeof(double) * SigmaEulerCTA<NW, DIAG>::WORDS;
     static bool init = false;
     if (!init) {
-        set_smem(kf_sigma_e<NW, MB>, sm);
+        set_smem(kf_sigma_e<NW, MB, DIAG>, sm);
         init = true;
     }
     zc = zchunk_for((long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW - 1), kc1 - kc0, zc);
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
-    kf_sigma_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc, gate);
+    kf_sigma_e<NW, MB, DIAG><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc, gate);
 }
 
 template <int NW, int MB>
@@ -1525,7 +1552,8 @@ int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
     static const Tune tune;
     const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
     const int sc0 = kn0 - 1 > 0 ? kn0 - 1 : 0, sc1 = kn1 + 1 < p.nz ? kn1 + 1 : p.nz;
-    sigma_e_launch<8, 2>(s, p, cur, sc0, sc1, tune.zc, gate, (cudaStream_t)st);
+    if (p.diag_jumps) sigma_e_launch<8, 2, true>(s, p, cur, sc0, sc1, tune.zc, gate, (cudaStream_t)st);
+    else sigma_e_launch<8, 2, false>(s, p, cur, sc0, sc1, tune.zc, gate, (cudaStream_t)st);
     return 1;
 }
 

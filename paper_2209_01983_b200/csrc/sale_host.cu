@@ -676,6 +676,22 @@ int check_diag_areas(sale_ctx* c)
             }
     }
     c->phys.diag_areas = diag ? 1 : 0;
+    // axis-jump separations: d = (dx, 0, 0) on x, (0, dy, 0) on y, (0, 0, dz) on z
+    bool dj = true;
+    for (auto& s : c->slabs) {
+        const long long n[3] = {c->phys.nx, c->phys.ny, s.nzc};
+        const double* T[3] = {s.TJx, s.TJy, s.TJz};
+        for (int a = 0; a < 3 && dj; ++a) {
+            h.resize((size_t)(4 * n[a]));
+            int rc = cuda_check(c, cudaMemcpy(h.data(), T[a], sizeof(double) * (size_t)(4 * n[a]), cudaMemcpyDeviceToHost),
+                                "jump tables");
+            if (rc) return rc;
+            for (long long t = 0; t < n[a] && dj; ++t)
+                for (int comp = 0; comp < 3; ++comp)
+                    if (comp != a && h[(size_t)(4 * t + comp)] != 0.0) dj = false;
+        }
+    }
+    c->phys.diag_jumps = dj ? 1 : 0;
     return SALE_OK;
 }
 

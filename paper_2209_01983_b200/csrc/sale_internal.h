@@ -18,6 +18,8 @@ struct Phys {
     int diag_areas;           // Euler: every target face area vector is axis-aligned (off-diagonal
                               // components exactly zero, diagonal non-zero; checked at create), so
                               // a corner vector (c.2) is exactly (+-Ax.x, +-Ay.y, +-Az.z)
+    int diag_jumps;           // Euler: every axis-jump separation d of the target mesh lies on its
+                              // axis (off-axis components exactly zero; checked at create)
 };
 
 // Device-resident clock and status (one per context; all local slabs share it).
