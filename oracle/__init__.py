@@ -26,6 +26,9 @@ OK, EINVAL, ENOMEM, ETANGLED, EDTCOLLAPSE, ENEGMASS, EPOISONED = 0, 1, 2, 5, 6, 
 
 FIELDS = {"X": 0, "Y": 1, "Z": 2, "UX": 3, "UY": 4, "UZ": 5, "NODE_MASS": 6,
           "MASS": 7, "E": 8, "RHO": 9, "VOL": 10, "P": 11, "Q": 12, "CS": 13}
+MAX_MAT = 4
+for _m in range(MAX_MAT):  # material fields (nmat >= 1): volume fraction, mass, specific energy
+    FIELDS[f"MAT_F{_m}"], FIELDS[f"MAT_M{_m}"], FIELDS[f"MAT_E{_m}"] = 16 + _m, 20 + _m, 24 + _m
 NODE_FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "NODE_MASS")
 
 
@@ -36,7 +39,8 @@ class OracleParams(C.Structure):
                 ("q_quad", C.c_double), ("cfl", C.c_double), ("dt_growth", C.c_double),
                 ("t_end", C.c_double), ("rezone", C.c_int32), ("reflect_mask", C.c_uint32),
                 ("rho0", C.c_double), ("e_background", C.c_double),
-                ("e_deposit", C.c_double)]
+                ("e_deposit", C.c_double), ("nmat", C.c_int32), ("pad0", C.c_int32),
+                ("mat_gamma", C.c_double * 4)]
 
 
 _lock = threading.Lock()
@@ -93,6 +97,8 @@ def lib() -> C.CDLL:
             L.oracle_hex_volume.restype = d
             L.oracle_eos.argtypes = [d, d, d, P(d), P(d), P(d)]
             L.oracle_eos.restype = None
+            L.oracle_mix_eos.argtypes = [i32, P(d), P(d), P(d), P(d), d, d, P(d), P(d), P(d)]
+            L.oracle_mix_eos.restype = None
             L.oracle_q_of_du.argtypes = [d, d, d, d, d]
             L.oracle_q_of_du.restype = d
             L.oracle_dt_cell.argtypes = [d, d, d, d]
@@ -125,11 +131,14 @@ def _dp(a: np.ndarray):
 
 def make_params(cfg: dict) -> OracleParams:
     p = OracleParams()
-    p.abi_version = 1
+    p.abi_version = 2
     for name, _ in OracleParams._fields_:
-        if name == "abi_version":
+        if name in ("abi_version", "pad0", "nmat", "mat_gamma"):
             continue
         setattr(p, name, cfg[name])
+    gam = list(cfg.get("mat_gamma", ()))[:4]  # nmat > 4 is rejected by oracle_create
+    p.nmat = int(cfg.get("nmat", 0))
+    p.mat_gamma = (C.c_double * 4)(*(gam + [0.0] * (4 - len(gam))))
     return p
 
 
@@ -225,6 +234,15 @@ def eos(gamma, rho, e):
     p, pf, cs = C.c_double(), C.c_double(), C.c_double()
     lib().oracle_eos(gamma, rho, e, C.byref(p), C.byref(pf), C.byref(cs))
     return p.value, pf.value, cs.value
+
+
+def mix_eos(gammas, f, mm, e, V, rho):
+    """MM1 mixed-cell closure: (p, P, cs) of one cell."""
+    n = len(gammas)
+    arr = [np.ascontiguousarray(a, dtype=np.float64) for a in (gammas, f, mm, e)]
+    p, P, cs = C.c_double(), C.c_double(), C.c_double()
+    lib().oracle_mix_eos(n, *[_dp(a) for a in arr], V, rho, C.byref(p), C.byref(P), C.byref(cs))
+    return p.value, P.value, cs.value
 
 
 def q_of_du(rho, cs, du, c1, c2):

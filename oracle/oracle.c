@@ -40,6 +40,14 @@ struct oracle_ctx {
     double *x1[3], *u1[3];       /* x', u' (c.3 step 6)               */
     double *e1, *V1;             /* e', V' (c.3 step 7)               */
     double *dm, *dE, *dP[3], *m2; /* Delta m, Delta E, Delta P, m'' (c.4 step 3) */
+    /* multi-material cells (nmat >= 1, readings MM1-MM7): per
+     * material m the volume fraction f_m, mass m_m, specific energy e_m; m above
+     * then holds the cell total sum_m m_m and e is unused */
+    int32_t nmat;
+    double *mf[ORACLE_MAX_MAT], *mmat[ORACLE_MAX_MAT], *me[ORACLE_MAX_MAT];
+    double *qv, *pfm[ORACLE_MAX_MAT];   /* MM3/MM4 scratch: q and pf_m of the cycle start */
+    double *e1m[ORACLE_MAX_MAT];        /* e'_m (MM4)                                      */
+    double *dmm[ORACLE_MAX_MAT], *dEm[ORACLE_MAX_MAT], *vm2[ORACLE_MAX_MAT]; /* MM6         */
     /* clock (c.3 step 8, c.5) */
     double t, dt_prev;
     int64_t cycle;
@@ -145,6 +153,36 @@ static double q_of_du(double rho, double cs, double du, double c1, double c2)
     return (du < 0.0) ? rho * ((c2 * (du * du)) + ((c1 * cs) * (-du))) : 0.0;
 }
 
+/* MM1 (multi-material closure; "mixed_cell_pressure"):
+ * each present material (f_m > 0) at its own density rho_m = m_m / (f_m V) and the
+ * ideal-gas EoS of c.3 step 1, p_m = ((gamma_m - 1) rho_m) e_m, pf_m = max(p_m, 0);
+ * the cell pressure is the volume-fraction-weighted sum p = sum_m f_m p_m (floored:
+ * P = sum_m f_m pf_m), the sound speed c = sqrt((sum_m f_m (gamma_m pf_m)) / rho)
+ * with rho = m / V of the whole cell.  Sums run m = 0, 1, ... left to right from
+ * the first present material.  With one material and f_0 = 1 every line reduces to
+ * eos() bit for bit (1.0 * a = a, m / (1.0 * V) = m / V).  pf[m] = 0 for absent
+ * materials. */
+static void mix_eos(int nmat, const double* gam, const double* f, const double* mm, const double* e,
+                    double V, double rho, double* p, double* P, double* cs, double* pf)
+{
+    double ps = 0.0, Ps = 0.0, G = 0.0;
+    int first = 1;
+    for (int k = 0; k < nmat; ++k) {
+        pf[k] = 0.0;
+        if (!(f[k] > 0.0)) continue;
+        double rk = mm[k] / (f[k] * V);
+        double pk = ((gam[k] - 1.0) * rk) * e[k];
+        double pfk = (pk > 0.0) ? pk : 0.0;
+        pf[k] = pfk;
+        double a = f[k] * pk, b = f[k] * pfk, g = f[k] * (gam[k] * pfk);
+        if (first) { ps = a; Ps = b; G = g; first = 0; }
+        else { ps = ps + a; Ps = Ps + b; G = G + g; }
+    }
+    *p = ps;
+    *P = Ps;
+    *cs = sqrt(G / rho);
+}
+
 static inline double dmin(double a, double b) { return (b < a) ? b : a; }
 static inline double dmax(double a, double b) { return (b > a) ? b : a; }
 
@@ -230,6 +268,9 @@ static int params_valid(const oracle_params* p)
     if (p->rezone != 0 && p->rezone != 1) return 0;
     if (p->reflect_mask > 0x3Fu) return 0;
     if (!(p->rho0 > 0.0)) return 0;
+    if (p->nmat < 0 || p->nmat > ORACLE_MAX_MAT) return 0;
+    for (int k = 0; k < p->nmat; ++k)
+        if (!(p->mat_gamma[k] > 1.0)) return 0;
     return 1;
 }
 
@@ -269,6 +310,18 @@ int32_t oracle_create(const oracle_params* p, oracle_ctx** out)
     c->dm = alloc_d(c->ncell, &ok);
     c->dE = alloc_d(c->ncell, &ok);
     c->m2 = alloc_d(c->ncell, &ok);
+    c->nmat = p->nmat;
+    if (c->nmat > 0) c->qv = alloc_d(c->ncell, &ok);
+    for (int k = 0; k < c->nmat; ++k) {
+        c->mf[k] = alloc_d(c->ncell, &ok);
+        c->mmat[k] = alloc_d(c->ncell, &ok);
+        c->me[k] = alloc_d(c->ncell, &ok);
+        c->pfm[k] = alloc_d(c->ncell, &ok);
+        c->e1m[k] = alloc_d(c->ncell, &ok);
+        c->dmm[k] = alloc_d(c->ncell, &ok);
+        c->dEm[k] = alloc_d(c->ncell, &ok);
+        c->vm2[k] = alloc_d(c->ncell, &ok);
+    }
     if (!ok) {
         oracle_destroy(c);
         return ORACLE_ENOMEM;
@@ -299,6 +352,14 @@ int32_t oracle_create(const oracle_params* p, oracle_ctx** out)
                 c->e[K] = p->e_background;
             }
     c->e[0] = p->e_deposit / c->m[0];
+    /* MM7: the whole Sedov cell is material 0 (f_0 = 1, m_0 = m, e_0 = e); the
+     * other materials are absent (f = m = e = 0) until set through the fields */
+    if (c->nmat > 0)
+        for (int64_t K = 0; K < c->ncell; ++K) {
+            c->mf[0][K] = 1.0;
+            c->mmat[0][K] = c->m[K];
+            c->me[0][K] = c->e[K];
+        }
     c->t = 0.0;
     c->dt_prev = -1.0;
     c->cycle = 0;
@@ -317,7 +378,25 @@ void oracle_destroy(oracle_ctx* c)
     }
     free(c->m); free(c->e); free(c->sig); free(c->e1); free(c->V1);
     free(c->dm); free(c->dE); free(c->m2);
+    free(c->qv);
+    for (int k = 0; k < c->nmat; ++k) {
+        free(c->mf[k]); free(c->mmat[k]); free(c->me[k]); free(c->pfm[k]);
+        free(c->e1m[k]); free(c->dmm[k]); free(c->dEm[k]); free(c->vm2[k]);
+    }
     free(c);
+}
+
+/* MM1 for cell K of the current state at volume V (rho = m / V of the cell) */
+static void cell_mix(const oracle_ctx* c, int64_t K, double V, double rho, double* p, double* P,
+                     double* cs, double* pf)
+{
+    double f[ORACLE_MAX_MAT], mm[ORACLE_MAX_MAT], e[ORACLE_MAX_MAT];
+    for (int k = 0; k < c->nmat; ++k) {
+        f[k] = c->mf[k][K];
+        mm[k] = c->mmat[k][K];
+        e[k] = c->me[k][K];
+    }
+    mix_eos(c->nmat, c->p.mat_gamma, f, mm, e, V, rho, p, P, cs, pf);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -340,7 +419,12 @@ static double dt_cfl_of_state(oracle_ctx* c)
                 int64_t K = cid(c, i, j, k);
                 double V = hex_volume_from_faces(F);
                 double rho = c->m[K] / V, pr, pf, cs;
-                eos(p->gamma, rho, c->e[K], &pr, &pf, &cs);
+                if (c->nmat > 0) {
+                    double pfk[ORACLE_MAX_MAT];
+                    cell_mix(c, K, V, rho, &pr, &pf, &cs, pfk);
+                } else {
+                    eos(p->gamma, rho, c->e[K], &pr, &pf, &cs);
+                }
                 double l2 = 0.0;
                 for (int ed = 0; ed < 12; ++ed) {
                     const double* A = N[EDGES[ed][0]];
@@ -409,8 +493,17 @@ static void lagrange_sigma(oracle_ctx* c)
                 int64_t K = cid(c, i, j, k);
                 double V = hex_volume_from_faces(F);
                 double rho = c->m[K] / V, pr, pf, cs;
-                eos(p->gamma, rho, c->e[K], &pr, &pf, &cs);
+                if (c->nmat > 0) {
+                    /* MM2-MM3: q from the cell density and the mixed sound speed;
+                     * sigma from the mixed floored pressure P (pf here) */
+                    double pfk[ORACLE_MAX_MAT];
+                    cell_mix(c, K, V, rho, &pr, &pf, &cs, pfk);
+                    for (int m = 0; m < c->nmat; ++m) c->pfm[m][K] = pfk[m];
+                } else {
+                    eos(p->gamma, rho, c->e[K], &pr, &pf, &cs);
+                }
                 double q = cell_q(F, U, rho, cs, p->q_lin, p->q_quad);
+                if (c->nmat > 0) c->qv[K] = q;
                 c->sig[K] = 0.25 * (pf + q);
             }
 }
@@ -457,10 +550,8 @@ static void lagrange_nodes(oracle_ctx* c, double dt)
             }
 }
 
-/* c.3 step 7 for one cell (shared with the exported unit entry point) */
-static double energy_update(const double N0[8][3], const double U0[8][3],
-                            const double U1[8][3], double sigma, double m, double e,
-                            double dt)
+/* c.3 step 7: W = sum over corners of C_h(x^n) . (u_h + u'_h)/2 */
+static double cell_work(const double N0[8][3], const double U0[8][3], const double U1[8][3])
 {
     face_t F[6];
     hex_faces(N0, F);
@@ -475,6 +566,15 @@ static double energy_update(const double N0[8][3], const double U0[8][3],
                 double term = (C[0] * ub[0] + C[1] * ub[1]) + C[2] * ub[2];
                 W = (h == 0) ? term : W + term;
             }
+    return W;
+}
+
+/* c.3 step 7 for one cell (shared with the exported unit entry point) */
+static double energy_update(const double N0[8][3], const double U0[8][3],
+                            const double U1[8][3], double sigma, double m, double e,
+                            double dt)
+{
+    double W = cell_work(N0, U0, U1);
     return e - (((sigma * W) * dt) / m);
 }
 
@@ -495,7 +595,23 @@ static int32_t lagrange_energy(oracle_ctx* c, double dt)
                 double V1 = hex_volume_from_faces(F1);
                 if (!(V1 > 0.0)) return fail(c, ORACLE_ETANGLED, K);
                 c->V1[K] = V1;
-                c->e1[K] = energy_update(N0, U0, U1, c->sig[K], c->m[K], c->e[K], dt);
+                if (c->nmat > 0) {
+                    /* MM4: each present material does the cell's work with its own
+                     * stress sigma_m = 0.25 (pf_m + q) on its volume share f_m (shared
+                     * strain: f_m is constant through the Lagrangian phase) */
+                    double W = cell_work(N0, U0, U1);
+                    for (int m = 0; m < c->nmat; ++m) {
+                        double f = c->mf[m][K], mm = c->mmat[m][K], em = c->me[m][K];
+                        if (f > 0.0 && mm > 0.0) {
+                            double sm = 0.25 * (c->pfm[m][K] + c->qv[K]);
+                            c->e1m[m][K] = em - ((((sm * W) * dt) * f) / mm);
+                        } else {
+                            c->e1m[m][K] = em;
+                        }
+                    }
+                } else {
+                    c->e1[K] = energy_update(N0, U0, U1, c->sig[K], c->m[K], c->e[K], dt);
+                }
             }
     return ORACLE_OK;
 }
@@ -542,9 +658,9 @@ static void face_node_ids(const oracle_ctx* c, int ax, int64_t i, int64_t j, int
 }
 
 /* c.4 steps 1-2 for the interior face between cell L=(i,j,k) and its +ax
- * neighbour U: mu, eps, pi[3] through the face (positive = toward +ax). */
-static void face_flux(oracle_ctx* c, int ax, int64_t i, int64_t j, int64_t k, double* mu,
-                      double* eps, double pi[3])
+ * neighbour U: the swept volume dV, the donor cell D and its mean velocity Ub. */
+static void face_donor(oracle_ctx* c, int ax, int64_t i, int64_t j, int64_t k, double* dVout,
+                       int64_t* Dout, double Ub[3])
 {
     int64_t ids[4];
     face_node_ids(c, ax, i, j, k, ids);
@@ -562,12 +678,22 @@ static void face_flux(oracle_ctx* c, int ax, int64_t i, int64_t j, int64_t k, do
     int64_t D = cid(c, di, dj, dk);
     double U[8][3];
     cell_nodes(c, c->u1, di, dj, dk, U);
-    double Ub[3];
     for (int q = 0; q < 3; ++q) {
         double s = U[0][q];
         for (int h = 1; h < 8; ++h) s = s + U[h][q];
         Ub[q] = 0.125 * s;
     }
+    *dVout = dV;
+    *Dout = D;
+}
+
+/* c.4 steps 1-2: mu, eps, pi[3] through the face (positive = toward +ax). */
+static void face_flux(oracle_ctx* c, int ax, int64_t i, int64_t j, int64_t k, double* mu,
+                      double* eps, double pi[3])
+{
+    double dV, Ub[3];
+    int64_t D;
+    face_donor(c, ax, i, j, k, &dV, &D, Ub);
     *mu = (c->m[D] / c->V1[D]) * dV;
     *eps = *mu * c->e1[D];
     for (int q = 0; q < 3; ++q) pi[q] = *mu * Ub[q];
@@ -613,6 +739,100 @@ static int32_t euler_cells(oracle_ctx* c)
     return ORACLE_OK;
 }
 
+/* MM5: per material m through the face: mass mu_m = (m_m,D / V'_D) dV (the
+ * donor's material mass per unit cell volume), volume phi_m = f_m,D dV, energy
+ * eps_m = mu_m e'_m,D; the face total mu = sum_m mu_m carries the momentum
+ * pi = mu Ub.  With one material, mu = mu_0 = (m_D / V'_D) dV as in c.4. */
+typedef struct { double mu, pi[3], mum[ORACLE_MAX_MAT], phim[ORACLE_MAX_MAT], epm[ORACLE_MAX_MAT]; } mflux_t;
+
+static void face_flux_mm(oracle_ctx* c, int ax, int64_t i, int64_t j, int64_t k, mflux_t* o)
+{
+    double dV, Ub[3];
+    int64_t D;
+    face_donor(c, ax, i, j, k, &dV, &D, Ub);
+    for (int m = 0; m < c->nmat; ++m) {
+        o->mum[m] = (c->mmat[m][D] / c->V1[D]) * dV;
+        o->phim[m] = c->mf[m][D] * dV;
+        o->epm[m] = o->mum[m] * c->e1m[m][D];
+        o->mu = (m == 0) ? o->mum[0] : o->mu + o->mum[m];
+    }
+    for (int q = 0; q < 3; ++q) o->pi[q] = o->mu * Ub[q];
+}
+
+static void mflux_zero(mflux_t* o)
+{
+    memset(o, 0, sizeof *o);   /* boundary faces carry +0.0 */
+}
+
+/* c.4 steps 1-3 with materials (MM6): six-face sums (order -x +x -y +y -z +z, as
+ * c.4 step 3) per material of mu_m, eps_m, phi_m, and of the totals mu and pi;
+ * m''_m = m_m + Dm_m, V''_m = (f_m V') + Dphi_m, m'' = sum_m m''_m.  ENEGMASS if
+ * !(m'' > 0), or any m''_m < 0 or V''_m < 0, or !(sum_m V''_m > 0). */
+static int32_t euler_cells_mm(oracle_ctx* c)
+{
+    const int64_t nmax[3] = {c->nx, c->ny, c->nz};
+    for (int64_t k = 0; k < c->nz; ++k)
+        for (int64_t j = 0; j < c->ny; ++j)
+            for (int64_t i = 0; i < c->nx; ++i) {
+                mflux_t F[6];
+                const int64_t ijk[3] = {i, j, k};
+                for (int ax = 0; ax < 3; ++ax) {
+                    if (ijk[ax] > 0) {
+                        int64_t l[3] = {i, j, k};
+                        l[ax] -= 1;
+                        face_flux_mm(c, ax, l[0], l[1], l[2], &F[2 * ax]);
+                    } else {
+                        mflux_zero(&F[2 * ax]);
+                    }
+                    if (ijk[ax] < nmax[ax] - 1) face_flux_mm(c, ax, i, j, k, &F[2 * ax + 1]);
+                    else mflux_zero(&F[2 * ax + 1]);
+                }
+                int64_t K = cid(c, i, j, k);
+                c->dm[K] = ((((F[0].mu - F[1].mu) + F[2].mu) - F[3].mu) + F[4].mu) - F[5].mu;
+                for (int q = 0; q < 3; ++q)
+                    c->dP[q][K] = ((((F[0].pi[q] - F[1].pi[q]) + F[2].pi[q]) - F[3].pi[q]) + F[4].pi[q]) - F[5].pi[q];
+                double m2 = 0.0, VV = 0.0;
+                int bad = 0;
+                for (int m = 0; m < c->nmat; ++m) {
+                    double dmm = ((((F[0].mum[m] - F[1].mum[m]) + F[2].mum[m]) - F[3].mum[m]) + F[4].mum[m]) - F[5].mum[m];
+                    double dEm = ((((F[0].epm[m] - F[1].epm[m]) + F[2].epm[m]) - F[3].epm[m]) + F[4].epm[m]) - F[5].epm[m];
+                    double dph = ((((F[0].phim[m] - F[1].phim[m]) + F[2].phim[m]) - F[3].phim[m]) + F[4].phim[m]) - F[5].phim[m];
+                    double mm2 = c->mmat[m][K] + dmm;
+                    double vm2 = (c->mf[m][K] * c->V1[K]) + dph;
+                    if (mm2 < 0.0 || vm2 < 0.0) bad = 1;
+                    c->dmm[m][K] = dmm;
+                    c->dEm[m][K] = dEm;
+                    c->vm2[m][K] = vm2;
+                    m2 = (m == 0) ? mm2 : m2 + mm2;
+                    VV = (m == 0) ? vm2 : VV + vm2;
+                }
+                if (bad || !(m2 > 0.0) || !(VV > 0.0)) return fail(c, ORACLE_ENEGMASS, K);
+                c->m2[K] = m2;
+            }
+    return ORACLE_OK;
+}
+
+static void euler_nodes(oracle_ctx* c);
+
+/* MM6 commit: e''_m = e'_m + ((DE_m - e'_m Dm_m) / m''_m) (c.4 step 3 per material;
+ * 0 for a material whose mass is 0), f''_m = V''_m / sum_k V''_k, m_m := m''_m;
+ * then the node update and x := x^T as c.4 steps 4-5 with the cell totals. */
+static void euler_commit_mm(oracle_ctx* c)
+{
+    for (int64_t K = 0; K < c->ncell; ++K) {
+        double VV = 0.0;
+        for (int m = 0; m < c->nmat; ++m) VV = (m == 0) ? c->vm2[0][K] : VV + c->vm2[m][K];
+        for (int m = 0; m < c->nmat; ++m) {
+            double mm2 = c->mmat[m][K] + c->dmm[m][K];
+            double e1 = c->e1m[m][K];
+            c->me[m][K] = (mm2 > 0.0) ? e1 + ((c->dEm[m][K] - (e1 * c->dmm[m][K])) / mm2) : 0.0;
+            c->mf[m][K] = c->vm2[m][K] / VV;
+            c->mmat[m][K] = mm2;
+        }
+    }
+    euler_nodes(c);
+}
+
 /* c.4 step 3 (e''), step 4 (node momentum, BC), step 5 (x := x^T) */
 static void euler_commit(oracle_ctx* c)
 {
@@ -620,6 +840,12 @@ static void euler_commit(oracle_ctx* c)
         double e1 = c->e1[K];
         c->e[K] = e1 + ((c->dE[K] - (e1 * c->dm[K])) / c->m2[K]);
     }
+    euler_nodes(c);
+}
+
+/* c.4 step 4 (node momentum from the gathered Dm, DP, m''; BC), step 5 (x := x^T), m := m'' */
+static void euler_nodes(oracle_ctx* c)
+{
     for (int64_t k = 0; k < c->NZ; ++k)
         for (int64_t j = 0; j < c->NY; ++j)
             for (int64_t i = 0; i < c->NX; ++i) {
@@ -669,7 +895,11 @@ static int32_t cycle_once(oracle_ctx* c, double dt)
     lagrange_nodes(c, dt);
     int32_t rc = lagrange_energy(c, dt);
     if (rc) return rc;
-    if (c->p.rezone == 1) {
+    if (c->p.rezone == 1 && c->nmat > 0) {
+        rc = euler_cells_mm(c);
+        if (rc) return rc;
+        euler_commit_mm(c);
+    } else if (c->p.rezone == 1) {
         rc = euler_cells(c);
         if (rc) return rc;
         euler_commit(c);
@@ -680,6 +910,9 @@ static int32_t cycle_once(oracle_ctx* c, double dt)
             t = c->u[q]; c->u[q] = c->u1[q]; c->u1[q] = t;
         }
         double* t = c->e; c->e = c->e1; c->e1 = t;
+        for (int m = 0; m < c->nmat; ++m) {
+            t = c->me[m]; c->me[m] = c->e1m[m]; c->e1m[m] = t;
+        }
     }
     c->t = c->t + dt;
     c->cycle = c->cycle + 1;
@@ -728,6 +961,18 @@ int32_t oracle_next_dt(oracle_ctx* c, double* dt)
 /* ------------------------------------------------------------------------- */
 static int is_node_field(int32_t f) { return f >= ORACLE_F_X && f <= ORACLE_F_NODE_MASS; }
 static int is_cell_field(int32_t f) { return f >= ORACLE_F_MASS && f <= ORACLE_F_CS; }
+/* material field -> (kind 0 f / 1 m / 2 e, material), or -1 */
+static int mat_field(const oracle_ctx* c, int32_t f, int* mat)
+{
+    if (f < ORACLE_F_MAT_F || f >= ORACLE_F_MAT_E + ORACLE_MAX_MAT) return -1;
+    int kind = (f - ORACLE_F_MAT_F) / ORACLE_MAX_MAT;
+    *mat = (f - ORACLE_F_MAT_F) % ORACLE_MAX_MAT;
+    return (*mat < c->nmat) ? kind : -1;
+}
+static double* mat_array(oracle_ctx* c, int kind, int mat)
+{
+    return kind == 0 ? c->mf[mat] : (kind == 1 ? c->mmat[mat] : c->me[mat]);
+}
 
 int32_t oracle_get_field(oracle_ctx* c, int32_t field, double* dst, uint64_t count)
 {
@@ -758,9 +1003,23 @@ int32_t oracle_get_field(oracle_ctx* c, int32_t field, double* dst, uint64_t cou
         }
         return ORACLE_OK;
     }
-    if (!is_cell_field(field)) return ORACLE_EINVAL;
+    int mat, kind = mat_field(c, field, &mat);
+    if (!is_cell_field(field) && kind < 0) return ORACLE_EINVAL;
     if (count != (uint64_t)c->ncell) return ORACLE_EINVAL;
+    if (kind >= 0) { memcpy(dst, mat_array(c, kind, mat), sizeof(double) * (size_t)c->ncell); return 0; }
     if (field == ORACLE_F_MASS) { memcpy(dst, c->m, sizeof(double) * (size_t)c->ncell); return 0; }
+    if (field == ORACLE_F_E && c->nmat > 0) {
+        /* mixture specific energy (sum_m m_m e_m) / m */
+        for (int64_t K = 0; K < c->ncell; ++K) {
+            double s = 0.0;
+            for (int m = 0; m < c->nmat; ++m) {
+                double t = c->mmat[m][K] * c->me[m][K];
+                s = (m == 0) ? t : s + t;
+            }
+            dst[K] = s / c->m[K];
+        }
+        return 0;
+    }
     if (field == ORACLE_F_E) { memcpy(dst, c->e, sizeof(double) * (size_t)c->ncell); return 0; }
     for (int64_t k = 0; k < c->nz; ++k)
         for (int64_t j = 0; j < c->ny; ++j)
@@ -772,7 +1031,12 @@ int32_t oracle_get_field(oracle_ctx* c, int32_t field, double* dst, uint64_t cou
                 int64_t K = cid(c, i, j, k);
                 double V = hex_volume_from_faces(F);
                 double rho = c->m[K] / V, pr, pf, cs;
-                eos(c->p.gamma, rho, c->e[K], &pr, &pf, &cs);
+                if (c->nmat > 0) {
+                    double pfk[ORACLE_MAX_MAT];
+                    cell_mix(c, K, V, rho, &pr, &pf, &cs, pfk);
+                } else {
+                    eos(c->p.gamma, rho, c->e[K], &pr, &pf, &cs);
+                }
                 double v;
                 switch (field) {
                 case ORACLE_F_RHO: v = rho; break;
@@ -795,6 +1059,19 @@ int32_t oracle_set_field(oracle_ctx* c, int32_t field, const double* src, uint64
     if (c->poisoned) return ORACLE_EPOISONED;
     double* dst = NULL;
     uint64_t need = 0;
+    int mat, kind = mat_field(c, field, &mat);
+    if (kind >= 0) {
+        if (count != (uint64_t)c->ncell) return ORACLE_EINVAL;
+        memcpy(mat_array(c, kind, mat), src, sizeof(double) * (size_t)c->ncell);
+        if (kind == 1)   /* the cell mass is the sum of the material masses */
+            for (int64_t K = 0; K < c->ncell; ++K) {
+                double s = 0.0;
+                for (int m = 0; m < c->nmat; ++m) s = (m == 0) ? c->mmat[0][K] : s + c->mmat[m][K];
+                c->m[K] = s;
+            }
+        return ORACLE_OK;
+    }
+    if (c->nmat > 0 && (field == ORACLE_F_MASS || field == ORACLE_F_E)) return ORACLE_EINVAL;
     if (field >= ORACLE_F_X && field <= ORACLE_F_Z) {
         if (c->p.rezone == 1) return ORACLE_EINVAL;     /* Euler: x = x^T */
         dst = c->x[field - ORACLE_F_X]; need = (uint64_t)c->nnode;
@@ -863,6 +1140,14 @@ void oracle_eos(double gamma, double rho, double e, double* p, double* pf, doubl
     eos(gamma, rho, e, p, pf, cs);
 }
 
+void oracle_mix_eos(int32_t nmat, const double* gamma, const double* f, const double* mm, const double* e,
+                    double V, double rho, double* p, double* P, double* cs)
+{
+    double pf[ORACLE_MAX_MAT];
+    if (nmat < 1 || nmat > ORACLE_MAX_MAT) return;
+    mix_eos(nmat, gamma, f, mm, e, V, rho, p, P, cs, pf);
+}
+
 double oracle_q_of_du(double rho, double cs, double du, double c1, double c2)
 {
     return q_of_du(rho, cs, du, c1, c2);
@@ -907,7 +1192,7 @@ void oracle_steinberg_point(const oracle_steinberg_params* sp, double p, double 
 int32_t oracle_steinberg(oracle_ctx* c, const oracle_steinberg_params* sp, const double* eps_p, double* shear,
                          double* yield, uint64_t count)
 {
-    if (!c || !sp || !shear || !yield || count != (uint64_t)c->ncell) return ORACLE_EINVAL;
+    if (!c || !sp || !shear || !yield || count != (uint64_t)c->ncell || c->nmat > 0) return ORACLE_EINVAL;
     double* rho = (double*)malloc(sizeof(double) * (size_t)c->ncell);
     double* pr = (double*)malloc(sizeof(double) * (size_t)c->ncell);
     if (!rho || !pr) {

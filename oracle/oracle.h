@@ -28,7 +28,8 @@
 extern "C" {
 #endif
 
-#define ORACLE_ABI_VERSION 1
+#define ORACLE_ABI_VERSION 2
+#define ORACLE_MAX_MAT 4
 
 /* Same fields and meaning as sale_params (include/sale.h), minus the device /
  * communication members.  SURVEY §8(b). */
@@ -46,6 +47,15 @@ typedef struct oracle_params {
     double rho0;                  /* Sedov ambient density                     */
     double e_background;          /* Sedov background specific energy          */
     double e_deposit;             /* Sedov energy E0 put in cell (0,0,0)       */
+    /* multi-material cells (readings MM1-MM7 in DESIGN.md
+     * §10d).  nmat = 0: the single-material scheme above.  nmat in [1,4]: every
+     * cell carries per material m a volume fraction f_m, a mass m_m and a specific
+     * energy e_m, each material its own ideal-gas gamma mat_gamma[m] (> 1); the
+     * initial state puts the whole Sedov cell in material 0.  With nmat = 1 the
+     * material path reproduces the single-material scheme bit for bit. */
+    int32_t nmat;
+    int32_t pad0;
+    double mat_gamma[ORACLE_MAX_MAT];
 } oracle_params;
 
 typedef struct oracle_ctx oracle_ctx;
@@ -62,7 +72,11 @@ enum {
     ORACLE_F_X = 0, ORACLE_F_Y, ORACLE_F_Z, ORACLE_F_UX, ORACLE_F_UY, ORACLE_F_UZ,
     ORACLE_F_NODE_MASS,                                   /* node fields 0..6  */
     ORACLE_F_MASS = 7, ORACLE_F_E, ORACLE_F_RHO, ORACLE_F_VOL, ORACLE_F_P,
-    ORACLE_F_Q, ORACLE_F_CS                               /* cell fields 7..13 */
+    ORACLE_F_Q, ORACLE_F_CS,                              /* cell fields 7..13 */
+    /* material fields (nmat >= 1), material m in [0, nmat): */
+    ORACLE_F_MAT_F = 16,   /* + m: volume fraction f_m                           */
+    ORACLE_F_MAT_M = 20,   /* + m: material mass m_m (MASS = sum over m)          */
+    ORACLE_F_MAT_E = 24    /* + m: material specific internal energy e_m          */
 };
 
 int32_t oracle_create(const oracle_params* p, oracle_ctx** out);
@@ -87,6 +101,11 @@ void oracle_face(const double* P, double* A, double* Xbar, double* s);
 double oracle_hex_volume(const double* N);
 /* c.3 step 1: p, pf, c from (gamma, rho, e) */
 void oracle_eos(double gamma, double rho, double e, double* p, double* pf, double* cs);
+/* MM1: mixed-cell closure of nmat materials (gamma[m], f[m], m_m[m], e[m]) in a
+ * cell of volume V and density rho: p = sum f_m p_m, P = sum f_m max(p_m, 0),
+ * cs = sqrt(sum f_m gamma_m max(p_m,0) / rho) */
+void oracle_mix_eos(int32_t nmat, const double* gamma, const double* f, const double* mm, const double* e,
+                    double V, double rho, double* p, double* P, double* cs);
 /* c.3 step 2 last line: q from rho, c, du */
 double oracle_q_of_du(double rho, double cs, double du, double c1, double c2);
 /* c.5: per-cell candidate from l2 = min edge^2, v2 = max node speed^2, c */

@@ -81,3 +81,22 @@ def noh_state(cfg: dict, u0: float = -1.0, p0: float = 1e-6):
     ux[:, :, 0] = 0.0
     e = p0 * u0 * u0 / (cfg["gamma"] - 1.0)
     return {"UX": ux, "E": np.full((nz, ny, nx), e)}
+
+
+def two_material_tube_state(cfg: dict, volume: np.ndarray, x0: float = 0.5, left=(1.0, 1.0),
+                            right=(0.125, 0.1)):
+    """Sod's tube with two materials: material 0 (gamma
+    cfg["mat_gamma"][0]) fills the cells with centre x < x0 at (rho, p) = left, material
+    1 (mat_gamma[1]) the others at right; every cell is pure (f = 1 or 0).  volume: the
+    cells' V.  Returns the material fields {"MAT_F0", "MAT_M0", "MAT_E0", "MAT_F1", ...};
+    e_m = p / ((gamma_m - 1) rho)."""
+    nx = cfg["nx"]
+    xc = (np.arange(nx) + 0.5) * (cfg["lx"] / nx)
+    lft = np.broadcast_to((xc < x0)[None, None, :], volume.shape)
+    out = {}
+    for m, (side, (rho, p)) in enumerate(((lft, left), (~lft, right))):
+        g = cfg["mat_gamma"][m]
+        out[f"MAT_F{m}"] = np.where(side, 1.0, 0.0)
+        out[f"MAT_M{m}"] = np.where(side, rho * volume, 0.0)
+        out[f"MAT_E{m}"] = np.where(side, p / ((g - 1.0) * rho), 0.0)
+    return out

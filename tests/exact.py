@@ -4,7 +4,9 @@ the oracle.  Plain textbook gas dynamics, independent of the oracle and the CUDA
 * exact_riemann: the ideal-gas Riemann problem (two shocks / rarefactions meeting at a
   contact), star pressure by bisection on f_L(p) + f_R(p) + (u_R - u_L) = 0 and the
   self-similar sampling of the wave fan (the standard construction, e.g. Toro,
-  "Riemann Solvers and Numerical Methods for Fluid Dynamics", ch. 4).
+  "Riemann Solvers and Numerical Methods for Fluid Dynamics", ch. 4).  g may be a
+  pair (gamma_L, gamma_R): two ideal gases meeting at the contact (each wave
+  function f_K and each side's fan only involve that side's gamma).
 * noh_planar: the planar Noh solution -- a strong shock reflecting off the wall at
   speed D = (gamma-1)/2 |u0|, gas at rest behind it with rho = rho0 (gamma+1)/(gamma-1),
   p = rho0 |u0| (D + |u0|) ... i.e. all kinetic energy turned into internal energy.
@@ -23,19 +25,24 @@ def _f(p, r, pk, ck, g):
     return 2.0 * ck / (g - 1.0) * ((p / pk) ** ((g - 1.0) / (2.0 * g)) - 1.0)  # rarefaction
 
 
+def _gammas(g):
+    return (float(g[0]), float(g[1])) if isinstance(g, (tuple, list)) else (float(g), float(g))
+
+
 def star_state(WL, WR, g):
     rL, uL, pL = WL
     rR, uR, pR = WR
-    cL, cR = math.sqrt(g * pL / rL), math.sqrt(g * pR / rR)
+    gL, gR = _gammas(g)
+    cL, cR = math.sqrt(gL * pL / rL), math.sqrt(gR * pR / rR)
     lo, hi = 1e-12, 1e3 * max(pL, pR)
     for _ in range(200):
         pm = 0.5 * (lo + hi)
-        if _f(pm, rL, pL, cL, g) + _f(pm, rR, pR, cR, g) + uR - uL > 0.0:
+        if _f(pm, rL, pL, cL, gL) + _f(pm, rR, pR, cR, gR) + uR - uL > 0.0:
             hi = pm
         else:
             lo = pm
     ps = 0.5 * (lo + hi)
-    us = 0.5 * (uL + uR) + 0.5 * (_f(ps, rR, pR, cR, g) - _f(ps, rL, pL, cL, g))
+    us = 0.5 * (uL + uR) + 0.5 * (_f(ps, rR, pR, cR, gR) - _f(ps, rL, pL, cL, gL))
     return ps, us
 
 
@@ -43,12 +50,14 @@ def exact_riemann(x, t, WL=(1.0, 0.0, 1.0), WR=(0.125, 0.0, 0.1), g=1.4, x0=0.5)
     """(rho, u, p) at positions x and time t > 0 for the initial discontinuity at x0."""
     rL, uL, pL = WL
     rR, uR, pR = WR
-    cL, cR = math.sqrt(g * pL / rL), math.sqrt(g * pR / rR)
-    ps, us = star_state(WL, WR, g)
+    gL, gR = _gammas(g)
+    cL, cR = math.sqrt(gL * pL / rL), math.sqrt(gR * pR / rR)
+    ps, us = star_state(WL, WR, (gL, gR))
     out = np.zeros((3, len(x)))
     for n, xx in enumerate(np.asarray(x, dtype=float)):
         S = (xx - x0) / t
         if S < us:
+            g = gL
             if ps > pL:
                 rs = rL * ((ps / pL + (g - 1) / (g + 1)) / ((g - 1) / (g + 1) * ps / pL + 1))
                 SL = uL - cL * math.sqrt((g + 1) / (2 * g) * ps / pL + (g - 1) / (2 * g))
@@ -65,6 +74,7 @@ def exact_riemann(x, t, WL=(1.0, 0.0, 1.0), WR=(0.125, 0.0, 0.1), g=1.4, x0=0.5)
                     c = 2 / (g + 1) * (cL + (g - 1) / 2 * (uL - S))
                     W = (rL * (c / cL) ** (2 / (g - 1)), u, pL * (c / cL) ** (2 * g / (g - 1)))
         else:
+            g = gR
             if ps > pR:
                 rs = rR * ((ps / pR + (g - 1) / (g + 1)) / ((g - 1) / (g + 1) * ps / pR + 1))
                 SR = uR + cR * math.sqrt((g + 1) / (2 * g) * ps / pR + (g - 1) / (2 * g))
