@@ -41,7 +41,8 @@
 extern "C" {
 #endif
 
-#define SALE_ABI_VERSION 1
+#define SALE_ABI_VERSION 2
+#define SALE_MAX_MAT 4       /* materials per cell (multi-material mode)            */
 
 /* status codes */
 #define SALE_OK 0
@@ -78,6 +79,10 @@ extern "C" {
 #define SALE_F_P 11          /* derived: (gamma-1) rho e, not floored             */
 #define SALE_F_Q 12          /* derived: artificial viscosity at the current state */
 #define SALE_F_CS 13         /* derived: sqrt(gamma max(p,0) / rho)               */
+/* material fields (nmat >= 1; material m in [0, nmat)); cell fields, read and write */
+#define SALE_F_MAT_F(m) (16 + (m))  /* volume fraction f_m                          */
+#define SALE_F_MAT_M(m) (20 + (m))  /* material mass m_m; writing it re-sums MASS    */
+#define SALE_F_MAT_E(m) (24 + (m))  /* material specific internal energy e_m         */
 
 typedef struct sale_params {
     int32_t abi_version;      /* = SALE_ABI_VERSION                                */
@@ -112,7 +117,23 @@ typedef struct sale_params {
                                  by device copies (emulated ranks, used to prove
                                  decomposition bit-exactness on one GPU).  Must be
                                  1 when nranks > 1.                                */
-    int32_t reserved;
+    int32_t nmat;             /* multi-material cells (DESIGN.md
+                                 §10d readings MM0-MM7; P:133, P:183, P:403 name them,
+                                 SPEC S:255-263 the closure).  0: single material
+                                 (gamma above).  1..SALE_MAX_MAT: every cell carries
+                                 per material a volume fraction, mass and specific
+                                 energy (fields SALE_F_MAT_*), material m has the
+                                 ideal-gas gamma mat_gamma[m] (> 1); the Sedov init puts
+                                 the whole cell in material 0; the cell pressure is the
+                                 volume-fraction-weighted sum of the material
+                                 pressures; the remap moves each material's mass,
+                                 volume and energy from the donor cell.  MASS and E
+                                 are then read-only (MASS = sum of material masses,
+                                 E = mass-weighted mixture energy).  The material
+                                 kernels are one per step (the v0 schedule) whatever
+                                 impl says; nmat = 1 gives the single-material
+                                 results bit for bit.                              */
+    double mat_gamma[SALE_MAX_MAT];
 } sale_params;
 
 typedef struct sale_ctx sale_ctx;
@@ -154,8 +175,8 @@ int32_t sale_sync(sale_ctx* c, int32_t* cycles_done);
 int32_t sale_get_field(sale_ctx* c, int32_t field, double* dst, uint64_t count,
                        int32_t dst_on_device);
 
-/* Overwrite a state field (X, Y, Z in Lagrange mode only; UX, UY, UZ; MASS; E)
- * on this rank's owned slab (same shape and layout as get_field).  Replicated
+/* Overwrite a state field (X, Y, Z in Lagrange mode only; UX, UY, UZ; MASS and E
+ * with nmat = 0; SALE_F_MAT_* with nmat >= 1) on this rank's owned slab (same shape and layout as get_field).  Replicated
  * interface planes must be identical on both owners. */
 int32_t sale_set_field(sale_ctx* c, int32_t field, const double* src, uint64_t count,
                        int32_t src_on_device);
@@ -229,8 +250,8 @@ typedef struct sale_steinberg_params {
  * All three are DEVICE pointers with the layout and count of get_field's cell
  * fields (count = owned cells; emulated slabs concatenated in plane order).
  * Asynchronous on the context's stream (synchronises first with pending cycles);
- * the call launches one kernel per slab.  SALE_EINVAL on NULL / count mismatch,
- * SALE_EPOISONED on a poisoned context. */
+ * the call launches one kernel per slab.  SALE_EINVAL on NULL / count mismatch
+ * or nmat >= 1 (single-material only), SALE_EPOISONED on a poisoned context. */
 int32_t sale_steinberg(sale_ctx* c, const sale_steinberg_params* sp, const double* eps_p, double* shear,
                        double* yield, uint64_t count);
 

@@ -1,0 +1,316 @@
+// kernels_mat.cu -- multi-material cells (readings MM0-MM7 in
+// DESIGN.md §10d; the paper's multi-material ScalSALE, with the
+// closure of SPEC S:255-263).  The v0 schedule (one kernel per step, one thread per
+// cell or node) with a material axis: the cell carries f_k, m_k, e_k of up to MAX_MAT
+// materials (material-major arrays, Slab::mf/mm/me), the EoS is the mixed closure
+// mix_eos (sale_mesh.cuh), each material does its share of the cell's pdV work, and
+// the remap moves each material's mass, volume and energy from the donor cell.  The
+// node kernels (force gather, momentum remap) are v0's, on the cell totals.
+#include <cuda_runtime.h>
+
+#include "sale_mesh.cuh"
+
+namespace sale {
+
+static inline unsigned grid_for(long long n, int bs)
+{
+    long long g = (n + bs - 1) / bs;
+    return (unsigned)(g > 0 ? g : 1);
+}
+
+int launch_nodes_v0(const Slab& s, const Phys& p, int cur, int kb0, int kb1, Stream st);  // kernels_v0.cu
+int launch_remap_nodes_v0(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_dt_candidate_gated(const Slab& s, const Phys& p, int cur, Stream st);
+
+// MM1-MM3: geometry at t^n, mixed EoS, q from the cell density and mixed sound speed;
+// sigma = 0.25 (P + q); q is kept for the materials' stresses (MM4)
+template <bool EULER>
+__global__ void k_mat_sigma(Slab s, Phys p, int cur, int ka0, int ka1)
+{
+    if (!s.st->active) return;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= s.pc * (ka1 - ka0)) return;
+    int k = ka0 + (int)(t / s.pc);
+    long long r = t % s.pc;
+    int j = (int)(r / p.nx), i = (int)(r % p.nx);
+    D3 N[8], U[8], A[6], Xb[6];
+    double sv[6], pf[MAX_MAT];
+    load_hex_pos<EULER>(s, p, cur, i, j, k, N);
+    load_hex3(s, p, s.u[cur], i, j, k, U);
+    hex_faces(N, A, Xb, sv);
+    long long c = cidx(s, p, i, j, k);
+    double V = vol_from_s(sv);
+    double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, P, cs;
+    mix_eos(p, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, P, cs, pf);
+    double q = hex_q(Xb, U, rho, cs, p.c1, p.c2);
+    s.qv[c] = q;
+    s.sig[c] = 0.25 * (P + q);
+}
+
+// MM4: V' + tangle check; each present material's e'_k from its stress
+// sigma_k = 0.25 (pf_k + q) on its share f_k of the cell's work W (c.3 step 7);
+// Lagrange: the next dt candidate from the mixed EoS of the new state
+template <bool EULER>
+__global__ void k_mat_energy(Slab s, Phys p, int cur, int kc0, int kc1)
+{
+    if (!s.st->active) return;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long key = KEY_NONE;
+    if (t < s.pc * (kc1 - kc0)) {
+        int k = kc0 + (int)(t / s.pc);
+        long long r = t % s.pc;
+        int j = (int)(r / p.nx), i = (int)(r % p.nx);
+        bool owned = k >= s.k0 && k < s.k1;
+        D3 N0[8], N1[8], U0[8], U1[8], A[6], Xb[6];
+        double sv[6], pf[MAX_MAT];
+        load_hex_pos<EULER>(s, p, cur, i, j, k, N0);
+        load_hex3(s, p, s.u[cur], i, j, k, U0);
+        if (EULER) {
+            load_hex3(s, p, s.x1, i, j, k, N1);
+            load_hex3(s, p, s.u1, i, j, k, U1);
+        } else {
+            load_hex3(s, p, s.x[cur ^ 1], i, j, k, N1);
+            load_hex3(s, p, s.u[cur ^ 1], i, j, k, U1);
+        }
+        double V1 = hex_volume(N1);
+        if (owned && !(V1 > 0.0))
+            atomicMin(&s.st->err_key, (ERR_ORDER_TANGLED << 48) | (unsigned long long)gcell(p, i, j, k));
+        hex_faces(N0, A, Xb, sv);
+        double W = 0.0;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            D3 C = corner_vec(A, h & 1, (h >> 1) & 1, h >> 2);
+            D3 ub = scl(0.5, add(U0[h], U1[h]));
+            double term = dot(C, ub);
+            W = (h == 0) ? term : W + term;
+        }
+        const long long c = cidx(s, p, i, j, k), st = mat_stride(s);
+        const double m = mass_cur(s, p, cur)[c];
+        const double* f = mat_f(s, p, cur);
+        const double* mk = mat_m(s, p, cur);
+        {  // the materials' floored pressures at t^n (the same bits k_mat_sigma saw)
+            double pr, P, cs;
+            const double V0 = vol_from_s(sv);
+            mix_eos(p, f, mk, s.me[cur], c, st, V0, ddiv(m, V0), pr, P, cs, pf);
+        }
+        const double q = s.qv[c], dt = s.st->dt;
+        double* e1 = EULER ? s.e1m : s.me[cur ^ 1];
+        for (int a = 0; a < p.nmat; ++a) {
+            const long long ca = c + a * st;
+            const double fa = f[ca], ma = mk[ca], ea = s.me[cur][ca];
+            if (fa > 0.0 && ma > 0.0) {
+                const double sa = 0.25 * (pf[a] + q);
+                e1[ca] = ea - ddiv(((sa * W) * dt) * fa, ma);
+            } else {
+                e1[ca] = ea;
+            }
+        }
+        if (EULER) {
+            s.V1[c] = V1;
+        } else if (owned) {
+            double pr, P, cs;
+            mix_eos(p, f, mk, s.me[cur ^ 1], c, st, V1, ddiv(m, V1), pr, P, cs, pf);
+            key = dt_key(dt_cell(p.cfl, hex_min_edge2(N1), hex_max_speed2(U1), cs));
+        }
+    }
+    if (!EULER) block_min_atomic(key, &s.st->cand_key);
+}
+
+// c.4 steps 1-2 for the interior face on the +ax side of lower cell (li,lj,lk): swept
+// volume dV, donor cell D (the lower cell if dV > 0), the donor's mean velocity Ub
+__device__ __forceinline__ void face_donor(const Slab& s, const Phys& p, int ax, int li, int lj, int lk, double& dV,
+                                           long long& D, D3& Ub)
+{
+    int I[4], J[4], K[4];
+    if (ax == 0) {
+        int X = li + 1;
+        I[0] = X; J[0] = lj;     K[0] = lk;
+        I[1] = X; J[1] = lj + 1; K[1] = lk;
+        I[2] = X; J[2] = lj + 1; K[2] = lk + 1;
+        I[3] = X; J[3] = lj;     K[3] = lk + 1;
+    } else if (ax == 1) {
+        int Y = lj + 1;
+        I[0] = li;     J[0] = Y; K[0] = lk;
+        I[1] = li;     J[1] = Y; K[1] = lk + 1;
+        I[2] = li + 1; J[2] = Y; K[2] = lk + 1;
+        I[3] = li + 1; J[3] = Y; K[3] = lk;
+    } else {
+        int Z = lk + 1;
+        I[0] = li;     J[0] = lj;     K[0] = Z;
+        I[1] = li + 1; J[1] = lj;     K[1] = Z;
+        I[2] = li + 1; J[2] = lj + 1; K[2] = Z;
+        I[3] = li;     J[3] = lj + 1; K[3] = Z;
+    }
+    D3 T[4], L[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        T[v] = tpos(s, I[v], J[v], K[v]);
+        L[v] = ld3(s.x1, nidx(s, p, I[v], J[v], K[v]));
+    }
+    dV = swept_volume(T[0], T[1], T[2], T[3], L[0], L[1], L[2], L[3]);
+    int di = li, dj = lj, dk = lk;
+    if (!(dV > 0.0)) {
+        if (ax == 0) di = li + 1;
+        else if (ax == 1) dj = lj + 1;
+        else dk = lk + 1;
+    }
+    D3 U[8];
+    load_hex3(s, p, s.u1, di, dj, dk, U);
+    D3 sum = U[0];
+#pragma unroll
+    for (int h = 1; h < 8; ++h) sum = add(sum, U[h]);
+    Ub = scl(0.125, sum);
+    D = cidx(s, p, di, dj, dk);
+}
+
+// six-face sum in c.4 step 3's order, built face by face:
+// ((((v0 - v1) + v2) - v3) + v4) - v5
+__device__ __forceinline__ double acc6(int f, double acc, double v)
+{
+    return f == 0 ? v : ((f & 1) ? acc - v : acc + v);
+}
+
+// MM5-MM6: per cell, the materials' fluxes through its six faces (boundary faces carry
+// +0.0), m''_k, V''_k, e''_k, f''_k, the totals Delta m, Delta P, m'' for the node update
+__global__ void k_mat_remap_cells(Slab s, Phys p, int cur, int kr0, int kr1)
+{
+    if (!s.st->active) return;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= s.pc * (kr1 - kr0)) return;
+    int k = kr0 + (int)(t / s.pc);
+    long long r = t % s.pc;
+    int j = (int)(r / p.nx), i = (int)(r % p.nx);
+    const int ijk[3] = {i, j, k};
+    const int nmax[3] = {p.nx, p.ny, p.nz};
+    const long long st = mat_stride(s);
+    double dmk[MAX_MAT] = {0.0}, dEk[MAX_MAT] = {0.0}, dphk[MAX_MAT] = {0.0};
+    double dm = 0.0;
+    D3 dP = d3(0.0, 0.0, 0.0);
+    for (int f = 0; f < 6; ++f) {
+        const int ax = f >> 1;
+        const bool plus = f & 1;
+        const bool inner = plus ? ijk[ax] < nmax[ax] - 1 : ijk[ax] > 0;
+        double mu = 0.0;
+        D3 pi = d3(0.0, 0.0, 0.0);
+        double dV = 0.0;
+        long long D = 0;
+        D3 Ub = d3(0.0, 0.0, 0.0);
+        if (inner) {
+            int l[3] = {i, j, k};
+            if (!plus) l[ax] -= 1;
+            face_donor(s, p, ax, l[0], l[1], l[2], dV, D, Ub);
+        }
+        for (int a = 0; a < p.nmat; ++a) {
+            double mua = 0.0, pha = 0.0, epa = 0.0;
+            if (inner) {
+                const long long Da = D + a * st;
+                mua = ddiv(s.mm[cur][Da], s.V1[D]) * dV;
+                pha = s.mf[cur][Da] * dV;
+                epa = mua * s.e1m[Da];
+                mu = (a == 0) ? mua : mu + mua;
+            }
+            dmk[a] = acc6(f, dmk[a], mua);
+            dEk[a] = acc6(f, dEk[a], epa);
+            dphk[a] = acc6(f, dphk[a], pha);
+        }
+        if (inner) pi = scl(mu, Ub);
+        dm = acc6(f, dm, mu);
+        dP = d3(acc6(f, dP.x, pi.x), acc6(f, dP.y, pi.y), acc6(f, dP.z, pi.z));
+    }
+    const long long c = cidx(s, p, i, j, k);
+    double m2 = 0.0, VV = 0.0, vm2[MAX_MAT];
+    bool bad = false;
+    for (int a = 0; a < p.nmat; ++a) {
+        const long long ca = c + a * st;
+        const double mm2 = s.mm[cur][ca] + dmk[a];
+        vm2[a] = (s.mf[cur][ca] * s.V1[c]) + dphk[a];
+        if (mm2 < 0.0 || vm2[a] < 0.0) bad = true;
+        m2 = (a == 0) ? mm2 : m2 + mm2;
+        VV = (a == 0) ? vm2[a] : VV + vm2[a];
+    }
+    if (k >= s.k0 && k < s.k1 && (bad || !(m2 > 0.0) || !(VV > 0.0)))
+        atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, k));
+    for (int a = 0; a < p.nmat; ++a) {
+        const long long ca = c + a * st;
+        const double mm2 = s.mm[cur][ca] + dmk[a];
+        const double e1 = s.e1m[ca];
+        s.me[cur ^ 1][ca] = (mm2 > 0.0) ? e1 + ddiv(dEk[a] - (e1 * dmk[a]), mm2) : 0.0;
+        s.mf[cur ^ 1][ca] = ddiv(vm2[a], VV);
+        s.mm[cur ^ 1][ca] = mm2;
+    }
+    s.m[cur ^ 1][c] = m2;
+    s.dm[c] = dm;
+    st3(s.dP, c, dP);
+}
+
+// MM7: the Sedov cell is material 0; the others are absent.  Every local cell plane
+// (ghost planes outside the mesh: all zero).
+__global__ void k_mat_init(Slab s, Phys p)
+{
+    long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= mat_stride(s)) return;
+    const int k = s.kb + (int)(c / s.pc);
+    const bool in = k >= 0 && k < p.nz;
+    const long long st = mat_stride(s);
+    for (int a = 0; a < p.nmat; ++a) {
+        const long long ca = c + a * st;
+        s.mf[0][ca] = (in && a == 0) ? 1.0 : 0.0;
+        s.mm[0][ca] = (in && a == 0) ? s.m[0][c] : 0.0;
+        s.me[0][ca] = (in && a == 0) ? s.e[0][c] : 0.0;
+    }
+}
+
+// the cell mass is the sum of the material masses (after set_field of MAT_M)
+__global__ void k_mat_total(Slab s, Phys p, int cur)
+{
+    long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= mat_stride(s)) return;
+    const double* mk = mat_m(s, p, cur);
+    const long long st = mat_stride(s);
+    double m = 0.0;
+    for (int a = 0; a < p.nmat; ++a) m = (a == 0) ? mk[c] : m + mk[c + a * st];
+    (p.rezone ? s.m[cur] : s.m[0])[c] = m;
+}
+
+int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    cudaStream_t cs = (cudaStream_t)st;
+    const int bs = 128;
+    if (!p.rezone) {
+        int ka0 = s.k0 > 0 ? s.k0 - 1 : 0, ka1 = s.k1 < p.nz ? s.k1 + 1 : p.nz;
+        k_mat_sigma<false><<<grid_for(s.pc * (ka1 - ka0), bs), bs, 0, cs>>>(s, p, cur, ka0, ka1);
+        launch_nodes_v0(s, p, cur, s.k0, s.k1, st);
+        k_mat_energy<false><<<grid_for(s.pc * (s.k1 - s.k0), bs), bs, 0, cs>>>(s, p, cur, s.k0, s.k1);
+        return 3;
+    }
+    int ka0 = s.k0 - 3 > 0 ? s.k0 - 3 : 0, ka1 = s.k1 + 3 < p.nz ? s.k1 + 3 : p.nz;
+    int kb0 = s.k0 - 2 > 0 ? s.k0 - 2 : 0, kb1 = s.k1 + 2 < p.nz ? s.k1 + 2 : p.nz;
+    k_mat_sigma<true><<<grid_for(s.pc * (ka1 - ka0), bs), bs, 0, cs>>>(s, p, cur, ka0, ka1);
+    launch_nodes_v0(s, p, cur, kb0, kb1, st);
+    k_mat_energy<true><<<grid_for(s.pc * (kb1 - kb0), bs), bs, 0, cs>>>(s, p, cur, kb0, kb1);
+    return 3;
+}
+
+int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    cudaStream_t cs = (cudaStream_t)st;
+    const int bs = 128;
+    int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
+    k_mat_remap_cells<<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);
+    launch_remap_nodes_v0(s, p, cur, st);
+    return 2 + launch_dt_candidate_gated(s, p, cur ^ 1, st);
+}
+
+int launch_mat_init(const Slab& s, const Phys& p, Stream st)
+{
+    k_mat_init<<<grid_for(s.pc * s.nzc, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    return 1;
+}
+
+int launch_mat_total(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    k_mat_total<<<grid_for(s.pc * s.nzc, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur);
+    return 1;
+}
+
+}  // namespace sale

@@ -25,6 +25,7 @@ static_assert(SALE_OK == sale::S_OK && SALE_ETANGLED == sale::S_ETANGLED &&
                   SALE_EREPLICA == sale::S_EREPLICA,
               "status codes out of sync");
 static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+static_assert(SALE_MAX_MAT == sale::MAX_MAT, "material count out of sync");
 static_assert(offsetof(sale::DevState, err_key) == offsetof(sale::DevState, cand_key) + 8,
               "cand_key / err_key must be adjacent for the 2-element allreduce");
 
@@ -118,6 +119,9 @@ bool params_ok(const sale_params* p)
     if (p->nz < T) return false;
     if (T > 1 && p->nz / T < ghost_depth(p)) return false;  // every slab owns >= g planes
     if ((long long)(p->nx + 1) * (p->ny + 1) > (1ll << 40)) return false;
+    if (p->nmat < 0 || p->nmat > SALE_MAX_MAT) return false;
+    for (int k = 0; k < p->nmat; ++k)
+        if (!(p->mat_gamma[k] > 1.0)) return false;
     return true;
 }
 
@@ -195,6 +199,14 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
     s.Xt = take(p->nx + 1);
     s.Yt = take(p->ny + 1);
     s.Zt = take(s.nzn);
+    const long long M = p->nmat;
+    for (int b = 0; b < 2; ++b) {  // Lagrange: f_k and m_k never change (index [0] only)
+        s.mf[b] = M && (b == 0 || euler) ? take(M * nc) : nullptr;
+        s.mm[b] = M && (b == 0 || euler) ? take(M * nc) : nullptr;
+        s.me[b] = M ? take(M * nc) : nullptr;
+    }
+    s.qv = M ? take(nc) : nullptr;
+    s.e1m = M && euler ? take(M * nc) : nullptr;
     return off;
 }
 
@@ -307,6 +319,15 @@ void state_arrays(const sale_ctx* c, const Slab& s, int b, bool include_mass,
     else if (include_mass)
         cells.push_back(s.m[0]);
     cells.push_back(s.e[b]);
+    // material axis: one cell array per material and quantity (the same field order
+    // as plan_fields)
+    const long long nc = s.pc * (long long)s.nzc;
+    if (euler || include_mass)
+        for (int k = 0; k < c->prm.nmat; ++k) {
+            cells.push_back(s.mf[euler ? b : 0] + k * nc);
+            cells.push_back(s.mm[euler ? b : 0] + k * nc);
+        }
+    for (int k = 0; k < c->prm.nmat; ++k) cells.push_back(s.me[b] + k * nc);
 }
 
 // the state fields a halo exchange moves, in plan order
@@ -325,6 +346,12 @@ void plan_fields(const sale_params* p, int full, std::vector<int>& node_f, std::
     node_f.push_back(SALE_F_UZ);
     if (euler || full) cell_f.push_back(SALE_F_MASS);
     cell_f.push_back(SALE_F_E);
+    if (euler || full)
+        for (int k = 0; k < p->nmat; ++k) {
+            cell_f.push_back(SALE_F_MAT_F(k));
+            cell_f.push_back(SALE_F_MAT_M(k));
+        }
+    for (int k = 0; k < p->nmat; ++k) cell_f.push_back(SALE_F_MAT_E(k));
 }
 
 // X1 plan of rank p->rank (one slab per rank): for every field, to / from r-1
@@ -373,9 +400,29 @@ void build_plan(const sale_params* p, int full, std::vector<sale_halo_msg>& out)
     }
 }
 
+// material field -> 0 (f) / 1 (m) / 2 (e) and the material, or -1
+int mat_kind(int nmat, int field, int* mat)
+{
+    if (field < SALE_F_MAT_F(0) || field >= SALE_F_MAT_E(SALE_MAX_MAT)) return -1;
+    *mat = (field - SALE_F_MAT_F(0)) % SALE_MAX_MAT;
+    return *mat < nmat ? (field - SALE_F_MAT_F(0)) / SALE_MAX_MAT : -1;
+}
+
+// the (local, whole-slab) array of material field `field` in buffer b
+double* mat_array(const sale_ctx* c, const Slab& s, int b, int field)
+{
+    int mat, kind = mat_kind(c->prm.nmat, field, &mat);
+    if (kind < 0) return nullptr;
+    const bool euler = c->prm.rezone == SALE_EULER;
+    const long long off = (long long)mat * s.pc * s.nzc;
+    if (kind == 2) return s.me[b] + off;
+    return (kind == 0 ? s.mf[euler ? b : 0] : s.mm[euler ? b : 0]) + off;
+}
+
 double* field_array(const sale_ctx* c, const Slab& s, int b, int field)
 {
     bool euler = c->prm.rezone == SALE_EULER;
+    if (field >= SALE_F_MAT_F(0)) return mat_array(c, s, b, field);
     if (field <= SALE_F_Z) return s.x[b][field];
     if (field <= SALE_F_UZ) return s.u[b][field - SALE_F_UX];
     if (field == SALE_F_MASS) return euler ? s.m[b] : s.m[0];
@@ -446,7 +493,8 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first, bool pre)
 {
     int rc;
     sale::Stream st = (sale::Stream)c->stream;
-    const bool v0 = c->prm.impl == SALE_IMPL_V0, euler = c->prm.rezone == SALE_EULER;
+    const bool mat = c->prm.nmat > 0;  // the material kernels (v0 schedule) whatever impl says
+    const bool v0 = c->prm.impl == SALE_IMPL_V0 || mat, euler = c->prm.rezone == SALE_EULER;
     int pr;
     if (pre) {
         pr = prof_open(c, SALE_K_LAGRANGE);
@@ -461,11 +509,15 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first, bool pre)
     prof_close(c, pr);
     for (auto& s : c->slabs) {
         pr = prof_open(c, SALE_K_LAGRANGE);
-        c->launches += v0 ? sale::launch_lagrange_v0(s, c->phys, b, st) : sale::launch_lagrange_fused(s, c->phys, b, st);
+        c->launches += mat  ? sale::launch_lagrange_mat(s, c->phys, b, st)
+                       : v0 ? sale::launch_lagrange_v0(s, c->phys, b, st)
+                            : sale::launch_lagrange_fused(s, c->phys, b, st);
         prof_close(c, pr);
         if (euler) {
             pr = prof_open(c, SALE_K_REMAP);
-            c->launches += v0 ? sale::launch_remap_v0(s, c->phys, b, st) : sale::launch_remap_fused(s, c->phys, b, st);
+            c->launches += mat  ? sale::launch_remap_mat(s, c->phys, b, st)
+                           : v0 ? sale::launch_remap_v0(s, c->phys, b, st)
+                                : sale::launch_remap_fused(s, c->phys, b, st);
             prof_close(c, pr);
         }
     }
@@ -534,7 +586,7 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
     int rc;
     int b = c->cur_enq;
     sale::Stream st = (sale::Stream)c->stream;
-    bool v0 = c->prm.impl == SALE_IMPL_V0, euler = c->prm.rezone == SALE_EULER;
+    bool v0 = c->prm.impl == SALE_IMPL_V0 || c->prm.nmat > 0, euler = c->prm.rezone == SALE_EULER;
     // Euler fused with the split force: each cycle's kf_sigma_e evaluates sigma and the
     // dt candidate of its start state before k_begin (no separate dt pass)
     const bool pre = !v0 && euler && sale::euler_pre_sigma();
@@ -610,6 +662,11 @@ int sync_state(sale_ctx* c, int* good_out)
 
 bool is_node_field(int f) { return f >= SALE_F_X && f <= SALE_F_NODE_MASS; }
 bool is_cell_field(int f) { return f >= SALE_F_MASS && f <= SALE_F_CS; }
+bool is_cell_field(const sale_ctx* c, int f)
+{
+    int mat;
+    return is_cell_field(f) || mat_kind(c->prm.nmat, f, &mat) >= 0;
+}
 
 uint64_t owned_count(const sale_ctx* c, const Slab& s, int field)
 {
@@ -641,8 +698,12 @@ const double* field_src(sale_ctx* c, const Slab& s, int field)
     case SALE_F_UY:
     case SALE_F_UZ: return s.u[b][field - SALE_F_UX] + on;
     case SALE_F_MASS: return (euler ? s.m[b] : s.m[0]) + oc;
-    case SALE_F_E: return s.e[b] + oc;
-    default: break;
+    case SALE_F_E:
+        if (c->prm.nmat == 0) return s.e[b] + oc;
+        break;  // the mixture's (sum_k m_k e_k) / m, derived
+    default:
+        if (double* a = mat_array(c, s, b, field)) return a + oc;
+        break;
     }
     c->launches += sale::launch_derive(s, c->phys, b, field, (sale::Stream)c->stream);
     return s.der;
@@ -734,6 +795,8 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
     ph.rho0 = p->rho0; ph.e_bg = p->e_background; ph.e_dep = p->e_deposit;
     ph.nx = p->nx; ph.ny = p->ny; ph.nz = p->nz;
     ph.reflect = p->reflect_mask; ph.rezone = p->rezone;
+    ph.nmat = p->nmat;
+    for (int k = 0; k < sale::MAX_MAT; ++k) ph.mg[k] = k < p->nmat ? p->mat_gamma[k] : 0.0;
     layout_slabs(p, c->slabs);
     char* base = static_cast<char*>(p->workspace);
     c->dstate = reinterpret_cast<DevState*>(base);
@@ -770,6 +833,7 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
         if (rc) break;
         c->launches += sale::launch_init_tables(s, ph, (sale::Stream)c->stream);
         c->launches += sale::launch_sedov_init(s, ph, (sale::Stream)c->stream);
+        if (ph.nmat) c->launches += sale::launch_mat_init(s, ph, (sale::Stream)c->stream);
         if (ph.rezone) c->launches += sale::launch_target_tables(s, ph, (sale::Stream)c->stream);
         rc = launch_check(c);
     }
@@ -819,7 +883,7 @@ int32_t sale_steinberg(sale_ctx* c, const sale_steinberg_params* sp, const doubl
                        double* yield, uint64_t count)
 {
     if (!c || !sp || !shear || !yield) return SALE_EINVAL;
-    if (count != expected_count(c, SALE_F_MASS)) return SALE_EINVAL;
+    if (count != expected_count(c, SALE_F_MASS) || c->prm.nmat > 0) return SALE_EINVAL;
     if (c->poisoned) return SALE_EPOISONED;
     DeviceGuard guard(c->prm.device);
     int rc = sync_state(c, nullptr);
@@ -836,7 +900,7 @@ int32_t sale_steinberg(sale_ctx* c, const sale_steinberg_params* sp, const doubl
 
 int32_t sale_get_field(sale_ctx* c, int32_t field, double* dst, uint64_t count, int32_t dst_on_device)
 {
-    if (!c || !dst || !(is_node_field(field) || is_cell_field(field))) return SALE_EINVAL;
+    if (!c || !dst || !(is_node_field(field) || is_cell_field(c, field))) return SALE_EINVAL;
     if (count != expected_count(c, field)) return SALE_EINVAL;
     DeviceGuard guard(c->prm.device);
     int rc = sync_state(c, nullptr);
@@ -882,7 +946,10 @@ int32_t sale_set_field(sale_ctx* c, int32_t field, const double* src, uint64_t c
     if (!c || !src) return SALE_EINVAL;
     if (c->poisoned) return SALE_EPOISONED;
     bool euler = c->prm.rezone == SALE_EULER;
-    bool ok = (field >= SALE_F_UX && field <= SALE_F_UZ) || field == SALE_F_MASS || field == SALE_F_E ||
+    int mat;
+    const bool matf = mat_kind(c->prm.nmat, field, &mat) >= 0;
+    bool ok = (field >= SALE_F_UX && field <= SALE_F_UZ) ||
+              (c->prm.nmat == 0 && (field == SALE_F_MASS || field == SALE_F_E)) || matf ||
               (!euler && field >= SALE_F_X && field <= SALE_F_Z);
     if (!ok || count != expected_count(c, field)) return SALE_EINVAL;
     DeviceGuard guard(c->prm.device);
@@ -894,7 +961,8 @@ int32_t sale_set_field(sale_ctx* c, int32_t field, const double* src, uint64_t c
     cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     for (auto& s : c->slabs) {
         double* arr;
-        if (field <= SALE_F_Z) arr = s.x[b][field];
+        if (matf) arr = mat_array(c, s, b, field);
+        else if (field <= SALE_F_Z) arr = s.x[b][field];
         else if (field <= SALE_F_UZ) arr = s.u[b][field - SALE_F_UX];
         else if (field == SALE_F_MASS) arr = euler ? s.m[b] : s.m[0];
         else arr = s.e[b];
@@ -904,6 +972,9 @@ int32_t sale_set_field(sale_ctx* c, int32_t field, const double* src, uint64_t c
         rc = cuda_check(c, cudaMemcpyAsync(arr + off, src + src_off, n * sizeof(double), kind, c->stream),
                         "set_field copy");
         if (rc) return rc;
+        // the cell mass is the sum of the material masses (MM0)
+        if (matf && field >= SALE_F_MAT_M(0) && field < SALE_F_MAT_E(0))
+            c->launches += sale::launch_mat_total(s, c->phys, b, (sale::Stream)c->stream);
     }
     return cuda_check(c, cudaStreamSynchronize(c->stream), "set_field sync");
 }

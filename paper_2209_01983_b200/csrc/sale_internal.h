@@ -6,6 +6,7 @@
 namespace sale {
 
 constexpr unsigned long long KEY_NONE = 0xFFFFFFFFFFFFFFFFull;
+constexpr int MAX_MAT = 4;
 
 // Physics and mesh parameters (validated copy of sale_params), by value into kernels.
 struct Phys {
@@ -20,6 +21,8 @@ struct Phys {
                               // a corner vector (c.2) is exactly (+-Ax.x, +-Ay.y, +-Az.z)
     int diag_jumps;           // Euler: every axis-jump separation d of the target mesh lies on its
                               // axis (off-axis components exactly zero; checked at create)
+    int nmat;                 // 0: single material; 1..MAX_MAT: material axis
+    double mg[MAX_MAT];       // gamma of each material
 };
 
 // Device-resident clock and status (one per context; all local slabs share it).
@@ -85,6 +88,14 @@ struct Slab {
     double* Xt;               // target node coordinates X_i, i in [0,nx]
     double* Yt;               // Y_j, j in [0,ny]
     double* Zt;               // Z_k for local node planes (index = k - kb)
+    // multi-material cells (Phys::nmat >= 1): material k's cell array
+    // starts at k * pc * nzc (a material-major Data4d).  Lagrange mode: f and m_k are
+    // constant (index [0]), e_k ping-pongs; Euler mode: all three ping-pong.
+    double* mf[2];            // volume fraction f_k
+    double* mm[2];            // material mass m_k (m above holds the sum over k)
+    double* me[2];            // material specific energy e_k
+    double* qv;               // scratch: q of the cycle start (the materials' stress needs it)
+    double* e1m;              // Euler scratch: e'_k
     DevState* st;
 };
 
@@ -121,6 +132,11 @@ int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergP& sp
 // in Euler mode the remap (R1-R5 + next dt candidate)
 int launch_lagrange_v0(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_remap_v0(const Slab& s, const Phys& p, int cur, Stream st);
+// multi-material cells (kernels_mat.cu): the v0 schedule with the material axis
+int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_mat_init(const Slab& s, const Phys& p, Stream st);
+int launch_mat_total(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st);
 bool fused_available();

@@ -77,6 +77,56 @@ __device__ __forceinline__ double* mass_cur(const Slab& s, const Phys& p, int cu
     return p.rezone ? s.m[cur] : s.m[0];
 }
 
+// ---- multi-material cells (Phys::nmat >= 1) -----------------
+__device__ __forceinline__ long long mat_stride(const Slab& s) { return s.pc * (long long)s.nzc; }
+// the material arrays of the state in buffer b (Lagrange: f_k and m_k never change)
+__device__ __forceinline__ const double* mat_f(const Slab& s, const Phys& p, int b)
+{
+    return p.rezone ? s.mf[b] : s.mf[0];
+}
+__device__ __forceinline__ const double* mat_m(const Slab& s, const Phys& p, int b)
+{
+    return p.rezone ? s.mm[b] : s.mm[0];
+}
+
+// MM1: the mixed-cell closure of cell c (material k at c + k*stride) at volume V and
+// cell density rho: each present material (f_k > 0) at rho_k = m_k / (f_k V) through
+// the c.3 step 1 EoS with its own gamma; pr = sum f_k p_k, P = sum f_k pf_k,
+// cs = sqrt((sum f_k (gamma_k pf_k)) / rho); sums left to right from the first present
+// material.  pf[k] = 0 for absent materials.  One material with f_0 = 1 gives eos()'s
+// bits (1.0 * a = a).
+__device__ __forceinline__ void mix_eos(const Phys& p, const double* f, const double* mm, const double* e,
+                                        long long c, long long stride, double V, double rho, double& pr,
+                                        double& P, double& cs, double pf[MAX_MAT])
+{
+    double ps = 0.0, Ps = 0.0, G = 0.0;
+    bool first = true;
+    for (int k = 0; k < p.nmat; ++k) {
+        pf[k] = 0.0;
+        const long long ck = c + k * stride;
+        const double fk = f[ck];
+        if (!(fk > 0.0)) continue;
+        const double rk = ddiv(mm[ck], fk * V);
+        const double pk = ((p.mg[k] - 1.0) * rk) * e[ck];
+        const double pfk = (pk > 0.0) ? pk : 0.0;
+        pf[k] = pfk;
+        const double a = fk * pk, b = fk * pfk, g = fk * (p.mg[k] * pfk);
+        if (first) {
+            ps = a;
+            Ps = b;
+            G = g;
+            first = false;
+        } else {
+            ps = ps + a;
+            Ps = Ps + b;
+            G = G + g;
+        }
+    }
+    pr = ps;
+    P = Ps;
+    cs = dsqrt(ddiv(G, rho));
+}
+
 // host: z-chunk length of a z-marching grid.  Large meshes use zc0 planes per CTA;
 // small ones shorter chunks (down to 4) so the grid still covers the 148 SMs twice
 // (a z-march is a chain of dependent plane steps; its length is the small-mesh time).

@@ -100,3 +100,23 @@ def two_material_tube_state(cfg: dict, volume: np.ndarray, x0: float = 0.5, left
         out[f"MAT_M{m}"] = np.where(side, rho * volume, 0.0)
         out[f"MAT_E{m}"] = np.where(side, p / ((g - 1.0) * rho), 0.0)
     return out
+
+
+def material_mix(cfg: dict, seed: int, mass: np.ndarray, energy: np.ndarray, pure_frac: float = 0.3):
+    """Seeded mixed cells for nmat = cfg["nmat"] materials: in a
+    random pure_frac of the cells material 0 alone (f = 1, the others absent); elsewhere
+    fractions w_k / sum w (w ~ U(0.1, 1)), masses f_k * mass * U(0.5, 2), energies
+    energy * U(0.5, 1.5).  Returns {"MAT_F<k>", "MAT_M<k>", "MAT_E<k>"} (cell arrays)."""
+    n = int(cfg["nmat"])
+    rng = np.random.Generator(np.random.PCG64(seed))
+    shape = mass.shape
+    w = rng.uniform(0.1, 1.0, size=(n,) + shape)
+    pure = rng.uniform(size=shape) < pure_frac
+    out = {}
+    for k in range(n):
+        f = w[k] / w.sum(axis=0)
+        f = np.where(pure, 1.0 if k == 0 else 0.0, f)
+        out[f"MAT_F{k}"] = f
+        out[f"MAT_M{k}"] = f * mass * rng.uniform(0.5, 2.0, size=shape)
+        out[f"MAT_E{k}"] = np.where(f > 0, energy * rng.uniform(0.5, 1.5, size=shape), 0.0)
+    return out

@@ -23,6 +23,9 @@ LAGRANGE, EULER = 0, 1
 IMPL = {"fused": 0, "v0": 1}
 FIELDS = {"X": 0, "Y": 1, "Z": 2, "UX": 3, "UY": 4, "UZ": 5, "NODE_MASS": 6,
           "MASS": 7, "E": 8, "RHO": 9, "VOL": 10, "P": 11, "Q": 12, "CS": 13}
+MAX_MAT = 4
+for _m in range(MAX_MAT):  # material fields (nmat >= 1): volume fraction, mass, specific energy
+    FIELDS[f"MAT_F{_m}"], FIELDS[f"MAT_M{_m}"], FIELDS[f"MAT_E{_m}"] = 16 + _m, 20 + _m, 24 + _m
 NODE_FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "NODE_MASS")
 EXPORTS = ("sale_workspace_bytes", "sale_nccl_unique_id", "sale_create", "sale_step",
            "sale_step_async", "sale_sync", "sale_get_field", "sale_set_field", "sale_get_clock",
@@ -42,7 +45,7 @@ class SaleParams(C.Structure):
                 ("nranks", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
                 ("device", C.c_int32), ("impl", C.c_int32), ("local_slabs", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("nmat", C.c_int32), ("mat_gamma", C.c_double * MAX_MAT)]
 
 
 class SaleSteinberg(C.Structure):
@@ -126,13 +129,16 @@ def nccl_unique_id() -> bytes:
 
 def make_params(cfg: dict, *, rank=0, nranks=1, device=0, impl="v0", local_slabs=1) -> SaleParams:
     p = SaleParams()
-    p.abi_version = 1
+    p.abi_version = 2
     for k in ("nx", "ny", "nz", "lx", "ly", "lz", "gamma", "q_lin", "q_quad", "cfl", "dt_growth",
               "t_end", "rezone", "reflect_mask", "rho0", "e_background", "e_deposit"):
         setattr(p, k, cfg[k])
     p.rank, p.nranks, p.device = rank, nranks, device
     p.impl = IMPL[impl] if isinstance(impl, str) else int(impl)
     p.local_slabs = local_slabs
+    gam = list(cfg.get("mat_gamma", ()))[:MAX_MAT]  # nmat > MAX_MAT is rejected by libsale
+    p.nmat = int(cfg.get("nmat", 0))
+    p.mat_gamma = (C.c_double * MAX_MAT)(*(gam + [0.0] * (MAX_MAT - len(gam))))
     return p
 
 
