@@ -1557,6 +1557,14 @@ int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
     return 1;
 }
 
+// Euler S5-S6 node gather on sigma and the cell totals (the material path reuses it)
+int launch_kn_force_e(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
+    kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, (cudaStream_t)st>>>(s, p, cur, kn0);
+    return 1;
+}
+
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
     return p.rezone ? lagrange_fused<true>(s, p, cur, st) : lagrange_fused<false>(s, p, cur, st);

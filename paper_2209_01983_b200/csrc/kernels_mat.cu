@@ -19,32 +19,42 @@ static inline unsigned grid_for(long long n, int bs)
 }
 
 int launch_nodes_v0(const Slab& s, const Phys& p, int cur, int kb0, int kb1, Stream st);  // kernels_v0.cu
-int launch_remap_nodes_v0(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_dt_candidate_gated(const Slab& s, const Phys& p, int cur, Stream st);
 
 // MM1-MM3: geometry at t^n, mixed EoS, q from the cell density and mixed sound speed;
-// sigma = 0.25 (P + q); q is kept for the materials' stresses (MM4)
+// sigma = 0.25 (P + q); q is kept for the materials' stresses (MM4).  Euler: launched
+// before the cycle's k_begin (gate = 0 for the first cycle of a sale_step call, when
+// DevState.active is still 0), it also forms the c.5 dt candidate of the owned cells
+// from the same mixed sound speed (the fixed target mesh's edges: as k_dt_candidate)
 template <bool EULER>
-__global__ void k_mat_sigma(Slab s, Phys p, int cur, int ka0, int ka1)
+__global__ void k_mat_sigma(Slab s, Phys p, int cur, int ka0, int ka1, int gate)
 {
-    if (!s.st->active) return;
+    if (gate && !s.st->active) return;
     long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= s.pc * (ka1 - ka0)) return;
-    int k = ka0 + (int)(t / s.pc);
-    long long r = t % s.pc;
-    int j = (int)(r / p.nx), i = (int)(r % p.nx);
-    D3 N[8], U[8], A[6], Xb[6];
-    double sv[6], pf[MAX_MAT];
-    load_hex_pos<EULER>(s, p, cur, i, j, k, N);
-    load_hex3(s, p, s.u[cur], i, j, k, U);
-    hex_faces(N, A, Xb, sv);
-    long long c = cidx(s, p, i, j, k);
-    double V = vol_from_s(sv);
-    double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, P, cs;
-    mix_eos(p, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, P, cs, pf);
-    double q = hex_q(Xb, U, rho, cs, p.c1, p.c2);
-    s.qv[c] = q;
-    s.sig[c] = 0.25 * (P + q);
+    unsigned long long key = KEY_NONE;
+    if (t < s.pc * (ka1 - ka0)) {
+        int k = ka0 + (int)(t / s.pc);
+        long long r = t % s.pc;
+        int j = (int)(r / p.nx), i = (int)(r % p.nx);
+        D3 N[8], U[8], A[6], Xb[6];
+        double sv[6], pf[MAX_MAT];
+        load_hex_pos<EULER>(s, p, cur, i, j, k, N);
+        load_hex3(s, p, s.u[cur], i, j, k, U);
+        hex_faces(N, A, Xb, sv);
+        long long c = cidx(s, p, i, j, k);
+        double V = vol_from_s(sv);
+        double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, P, cs;
+        mix_eos(p, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, P, cs, pf);
+        double q = hex_q(Xb, U, rho, cs, p.c1, p.c2);
+        s.qv[c] = q;
+        s.sig[c] = 0.25 * (P + q);
+        if (EULER && k >= s.k0 && k < s.k1) {
+            const double lx = len2(D3{s.Xt[i], 0.0, 0.0}, D3{s.Xt[i + 1], 0.0, 0.0});
+            const double ly = len2(D3{0.0, s.Yt[j], 0.0}, D3{0.0, s.Yt[j + 1], 0.0});
+            const double lz = len2(D3{0.0, 0.0, s.Zt[k - s.kb]}, D3{0.0, 0.0, s.Zt[k + 1 - s.kb]});
+            key = dt_key(dt_cell(p.cfl, dmin(dmin(lx, ly), lz), hex_max_speed2(U), cs));
+        }
+    }
+    if (EULER) block_min_atomic(key, &s.st->cand_key);
 }
 
 // MM4: V' + tangle check; each present material's e'_k from its stress
@@ -116,51 +126,58 @@ __global__ void k_mat_energy(Slab s, Phys p, int cur, int kc0, int kc1)
     if (!EULER) block_min_atomic(key, &s.st->cand_key);
 }
 
-// c.4 steps 1-2 for the interior face on the +ax side of lower cell (li,lj,lk): swept
-// volume dV, donor cell D (the lower cell if dV > 0), the donor's mean velocity Ub
-__device__ __forceinline__ void face_donor(const Slab& s, const Phys& p, int ax, int li, int lj, int lk, double& dV,
-                                           long long& D, D3& Ub)
+// c.4 steps 1-2, per cell c: the swept volumes of its -x / -y / -z faces (interior
+// faces only; stored at the upper cell, as kr_sweep does), and the cell's donor data:
+// mean node velocity Ub = 0.125 * sum of u' and, per material, m_k / V' (MM5)
+__global__ void k_mat_sweep(Slab s, Phys p, int cur, int ks0, int ks1)
 {
-    int I[4], J[4], K[4];
-    if (ax == 0) {
-        int X = li + 1;
-        I[0] = X; J[0] = lj;     K[0] = lk;
-        I[1] = X; J[1] = lj + 1; K[1] = lk;
-        I[2] = X; J[2] = lj + 1; K[2] = lk + 1;
-        I[3] = X; J[3] = lj;     K[3] = lk + 1;
-    } else if (ax == 1) {
-        int Y = lj + 1;
-        I[0] = li;     J[0] = Y; K[0] = lk;
-        I[1] = li;     J[1] = Y; K[1] = lk + 1;
-        I[2] = li + 1; J[2] = Y; K[2] = lk + 1;
-        I[3] = li + 1; J[3] = Y; K[3] = lk;
-    } else {
-        int Z = lk + 1;
-        I[0] = li;     J[0] = lj;     K[0] = Z;
-        I[1] = li + 1; J[1] = lj;     K[1] = Z;
-        I[2] = li + 1; J[2] = lj + 1; K[2] = Z;
-        I[3] = li;     J[3] = lj + 1; K[3] = Z;
-    }
-    D3 T[4], L[4];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        T[v] = tpos(s, I[v], J[v], K[v]);
-        L[v] = ld3(s.x1, nidx(s, p, I[v], J[v], K[v]));
-    }
-    dV = swept_volume(T[0], T[1], T[2], T[3], L[0], L[1], L[2], L[3]);
-    int di = li, dj = lj, dk = lk;
-    if (!(dV > 0.0)) {
-        if (ax == 0) di = li + 1;
-        else if (ax == 1) dj = lj + 1;
-        else dk = lk + 1;
-    }
+    if (!s.st->active) return;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= s.pc * (ks1 - ks0)) return;
+    const int k = ks0 + (int)(t / s.pc);
+    const long long r = t % s.pc;
+    const int j = (int)(r / p.nx), i = (int)(r % p.nx);
+    const long long c = cidx(s, p, i, j, k);
     D3 U[8];
-    load_hex3(s, p, s.u1, di, dj, dk, U);
+    load_hex3(s, p, s.u1, i, j, k, U);
     D3 sum = U[0];
 #pragma unroll
     for (int h = 1; h < 8; ++h) sum = add(sum, U[h]);
-    Ub = scl(0.125, sum);
-    D = cidx(s, p, di, dj, dk);
+    st3(s.UD, c, scl(0.125, sum));
+    const double V1 = s.V1[c];
+    const long long st = mat_stride(s);
+    for (int a = 0; a < p.nmat; ++a) s.rDm[c + a * st] = ddiv(s.mm[cur][c + a * st], V1);
+    // faces at node planes i / j / k, their lower cell at -1 on that axis; canonical
+    // P0..P3 as c.4 step 1 / face_node_ids
+    const int lo[3] = {i, j, k};
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        if (lo[ax] < 1) continue;
+        int I[4], J[4], K[4];
+        if (ax == 0) {
+            I[0] = i; J[0] = j;     K[0] = k;
+            I[1] = i; J[1] = j + 1; K[1] = k;
+            I[2] = i; J[2] = j + 1; K[2] = k + 1;
+            I[3] = i; J[3] = j;     K[3] = k + 1;
+        } else if (ax == 1) {
+            I[0] = i;     J[0] = j; K[0] = k;
+            I[1] = i;     J[1] = j; K[1] = k + 1;
+            I[2] = i + 1; J[2] = j; K[2] = k + 1;
+            I[3] = i + 1; J[3] = j; K[3] = k;
+        } else {
+            I[0] = i;     J[0] = j;     K[0] = k;
+            I[1] = i + 1; J[1] = j;     K[1] = k;
+            I[2] = i + 1; J[2] = j + 1; K[2] = k;
+            I[3] = i;     J[3] = j + 1; K[3] = k;
+        }
+        D3 T[4], L[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            T[v] = tpos(s, I[v], J[v], K[v]);
+            L[v] = ld3(s.x1, nidx(s, p, I[v], J[v], K[v]));
+        }
+        s.dV[ax][c] = swept_volume(T[0], T[1], T[2], T[3], L[0], L[1], L[2], L[3]);
+    }
 }
 
 // six-face sum in c.4 step 3's order, built face by face:
@@ -172,16 +189,17 @@ __device__ __forceinline__ double acc6(int f, double acc, double v)
 
 // MM5-MM6: per cell, the materials' fluxes through its six faces (boundary faces carry
 // +0.0), m''_k, V''_k, e''_k, f''_k, the totals Delta m, Delta P, m'' for the node update
-__global__ void k_mat_remap_cells(Slab s, Phys p, int cur, int kr0, int kr1)
+__global__ void k_mat_flux(Slab s, Phys p, int cur, int kr0, int kr1)
 {
     if (!s.st->active) return;
     long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= s.pc * (kr1 - kr0)) return;
-    int k = kr0 + (int)(t / s.pc);
-    long long r = t % s.pc;
-    int j = (int)(r / p.nx), i = (int)(r % p.nx);
+    const int k = kr0 + (int)(t / s.pc);
+    const long long r = t % s.pc;
+    const int j = (int)(r / p.nx), i = (int)(r % p.nx);
     const int ijk[3] = {i, j, k};
     const int nmax[3] = {p.nx, p.ny, p.nz};
+    const long long c = cidx(s, p, i, j, k), sa[3] = {1, p.nx, s.pc};
     const long long st = mat_stride(s);
     double dmk[MAX_MAT] = {0.0}, dEk[MAX_MAT] = {0.0}, dphk[MAX_MAT] = {0.0};
     double dm = 0.0;
@@ -193,18 +211,17 @@ __global__ void k_mat_remap_cells(Slab s, Phys p, int cur, int kr0, int kr1)
         double mu = 0.0;
         D3 pi = d3(0.0, 0.0, 0.0);
         double dV = 0.0;
-        long long D = 0;
-        D3 Ub = d3(0.0, 0.0, 0.0);
+        long long D = c;
         if (inner) {
-            int l[3] = {i, j, k};
-            if (!plus) l[ax] -= 1;
-            face_donor(s, p, ax, l[0], l[1], l[2], dV, D, Ub);
+            const long long nbr = plus ? c + sa[ax] : c - sa[ax];
+            dV = s.dV[ax][plus ? nbr : c];  // the face is the -ax face of the upper cell
+            D = (dV > 0.0) == plus ? c : nbr; // donor: the lower cell if the face moved toward +ax
         }
         for (int a = 0; a < p.nmat; ++a) {
             double mua = 0.0, pha = 0.0, epa = 0.0;
             if (inner) {
                 const long long Da = D + a * st;
-                mua = ddiv(s.mm[cur][Da], s.V1[D]) * dV;
+                mua = s.rDm[Da] * dV;
                 pha = s.mf[cur][Da] * dV;
                 epa = mua * s.e1m[Da];
                 mu = (a == 0) ? mua : mu + mua;
@@ -213,11 +230,10 @@ __global__ void k_mat_remap_cells(Slab s, Phys p, int cur, int kr0, int kr1)
             dEk[a] = acc6(f, dEk[a], epa);
             dphk[a] = acc6(f, dphk[a], pha);
         }
-        if (inner) pi = scl(mu, Ub);
+        if (inner) pi = scl(mu, ld3(s.UD, D));
         dm = acc6(f, dm, mu);
         dP = d3(acc6(f, dP.x, pi.x), acc6(f, dP.y, pi.y), acc6(f, dP.z, pi.z));
     }
-    const long long c = cidx(s, p, i, j, k);
     double m2 = 0.0, VV = 0.0, vm2[MAX_MAT];
     bool bad = false;
     for (int a = 0; a < p.nmat; ++a) {
@@ -272,33 +288,48 @@ __global__ void k_mat_total(Slab s, Phys p, int cur)
     (p.rezone ? s.m[cur] : s.m[0])[c] = m;
 }
 
+// Lagrange: the v0 schedule on the material kernels.  Euler: sigma and the dt
+// candidate ran before k_begin (launch_mat_pre); the node gather is the fused
+// kn_force_e (it reads sigma and the cell totals only).
 int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st)
 {
     cudaStream_t cs = (cudaStream_t)st;
     const int bs = 128;
     if (!p.rezone) {
         int ka0 = s.k0 > 0 ? s.k0 - 1 : 0, ka1 = s.k1 < p.nz ? s.k1 + 1 : p.nz;
-        k_mat_sigma<false><<<grid_for(s.pc * (ka1 - ka0), bs), bs, 0, cs>>>(s, p, cur, ka0, ka1);
+        k_mat_sigma<false><<<grid_for(s.pc * (ka1 - ka0), bs), bs, 0, cs>>>(s, p, cur, ka0, ka1, 1);
         launch_nodes_v0(s, p, cur, s.k0, s.k1, st);
         k_mat_energy<false><<<grid_for(s.pc * (s.k1 - s.k0), bs), bs, 0, cs>>>(s, p, cur, s.k0, s.k1);
         return 3;
     }
-    int ka0 = s.k0 - 3 > 0 ? s.k0 - 3 : 0, ka1 = s.k1 + 3 < p.nz ? s.k1 + 3 : p.nz;
     int kb0 = s.k0 - 2 > 0 ? s.k0 - 2 : 0, kb1 = s.k1 + 2 < p.nz ? s.k1 + 2 : p.nz;
-    k_mat_sigma<true><<<grid_for(s.pc * (ka1 - ka0), bs), bs, 0, cs>>>(s, p, cur, ka0, ka1);
-    launch_nodes_v0(s, p, cur, kb0, kb1, st);
+    launch_kn_force_e(s, p, cur, st);
     k_mat_energy<true><<<grid_for(s.pc * (kb1 - kb0), bs), bs, 0, cs>>>(s, p, cur, kb0, kb1);
-    return 3;
+    return 2;
 }
 
+// Euler: sigma of cell planes [k0-3, k1+3) (the node gather's reach) and the dt
+// candidate of the owned cells, before the cycle's k_begin
+int launch_mat_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
+{
+    int ka0 = s.k0 - 3 > 0 ? s.k0 - 3 : 0, ka1 = s.k1 + 3 < p.nz ? s.k1 + 3 : p.nz;
+    k_mat_sigma<true><<<grid_for(s.pc * (ka1 - ka0), 128), 128, 0, (cudaStream_t)st>>>(s, p, cur, ka0, ka1, gate);
+    return 1;
+}
+
+// R1-R4: swept volumes and donor data, the material fluxes and cell update, the fused
+// node momentum update (kn_update) on the totals; no dt pass (the next cycle's
+// k_mat_sigma forms the candidate)
 int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st)
 {
     cudaStream_t cs = (cudaStream_t)st;
     const int bs = 128;
     int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
-    k_mat_remap_cells<<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);
-    launch_remap_nodes_v0(s, p, cur, st);
-    return 2 + launch_dt_candidate_gated(s, p, cur ^ 1, st);
+    int ks0 = kr0 - 1 > 0 ? kr0 - 1 : 0, ks1 = kr1 + 1 < p.nz ? kr1 + 1 : p.nz;
+    k_mat_sweep<<<grid_for(s.pc * (ks1 - ks0), bs), bs, 0, cs>>>(s, p, cur, ks0, ks1);
+    k_mat_flux<<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);
+    launch_kn_update(s, p, cur, st);
+    return 3;
 }
 
 int launch_mat_init(const Slab& s, const Phys& p, Stream st)

@@ -1238,6 +1238,14 @@ static void cells_p_launch(const Slab& s, const Phys& p, int cur, int kr0, int k
     kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zc);
 }
 
+// R4 node momentum update on the cell totals (the material path reuses it)
+int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    kn_update<true><<<dim3(cdivr(p.nx + 1, 32) * cdivr(p.ny + 1, 8), s.k1 - s.k0 + 1), 256, 0, (cudaStream_t)st>>>(
+        s, p, cur);
+    return 1;
+}
+
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
 {
     cudaStream_t cs = (cudaStream_t)st;

@@ -207,6 +207,7 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
     }
     s.qv = M ? take(nc) : nullptr;
     s.e1m = M && euler ? take(M * nc) : nullptr;
+    s.rDm = M && euler ? take(M * nc) : nullptr;
     return off;
 }
 
@@ -498,7 +499,9 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first, bool pre)
     int pr;
     if (pre) {
         pr = prof_open(c, SALE_K_LAGRANGE);
-        for (auto& s : c->slabs) c->launches += sale::launch_euler_pre(s, c->phys, b, first ? 0 : 1, st);
+        for (auto& s : c->slabs)
+            c->launches += c->prm.nmat ? sale::launch_mat_pre(s, c->phys, b, first ? 0 : 1, st)
+                                       : sale::launch_euler_pre(s, c->phys, b, first ? 0 : 1, st);
         prof_close(c, pr);
         pr = prof_open(c, SALE_K_HALO);
         if ((rc = reduce_keys(c))) return rc;
@@ -589,7 +592,7 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
     bool v0 = c->prm.impl == SALE_IMPL_V0 || c->prm.nmat > 0, euler = c->prm.rezone == SALE_EULER;
     // Euler fused with the split force: each cycle's kf_sigma_e evaluates sigma and the
     // dt candidate of its start state before k_begin (no separate dt pass)
-    const bool pre = !v0 && euler && sale::euler_pre_sigma();
+    const bool pre = euler && (c->prm.nmat ? true : !v0 && sale::euler_pre_sigma());
     int pr = prof_open(c, SALE_K_PROLOGUE);
     c->launches += sale::launch_prep(c->dstate, st);
     if ((rc = exchange(c, b, true))) return rc;

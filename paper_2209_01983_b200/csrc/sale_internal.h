@@ -96,6 +96,7 @@ struct Slab {
     double* me[2];            // material specific energy e_k
     double* qv;               // scratch: q of the cycle start (the materials' stress needs it)
     double* e1m;              // Euler scratch: e'_k
+    double* rDm;              // Euler scratch: donor material density m_k / V' of each cell (k_mat_sweep)
     DevState* st;
 };
 
@@ -137,6 +138,10 @@ int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_mat_init(const Slab& s, const Phys& p, Stream st);
 int launch_mat_total(const Slab& s, const Phys& p, int cur, Stream st);
+// Euler: sigma + the cycle-start dt candidate, before the cycle's k_begin (gate as launch_euler_pre)
+int launch_mat_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st);
+int launch_kn_force_e(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st);
 bool fused_available();
