@@ -71,7 +71,10 @@ __device__ __forceinline__ void st3s(double* b, int o0, int stride, D3 v)
 // ============================================================================
 // kf_force
 // ============================================================================
-template <bool EULER, int NW>
+// NM > 0 (Lagrange, multi-material cells): sigma from the mixed
+// closure MM1 of the NM materials (always from V; the single-material EoS cache does
+// not apply), and q is stored for the materials' energy update (k_mat_energy)
+template <bool EULER, int NW, int NM = 0>
 struct ForceCTA {
     static constexpr int PL = NW * FW, TX = FW - 2, TY = NW - 2;
     // shared-memory words (doubles) relative to the per-thread base pointer
@@ -93,6 +96,7 @@ struct ForceCTA {
     bool pxm, pxp, pym, pyp;
     D3 px, pu;  // prefetch registers
     double pm, pe, prho, pcs;  // prefetch: cell m, e and (owned planes) the EoS cache
+    double pmf[NM > 0 ? NM : 1], pmm[NM > 0 ? NM : 1], pme[NM > 0 ? NM : 1];  // prefetch: materials
     FaceQ zprev;
 
     __device__ __forceinline__ ForceCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kn0_, int kn1_,
@@ -138,9 +142,15 @@ struct ForceCTA {
             long long c = cb + (long long)kc * s.pc;
             pm = mass_cur(s, p, cur)[c];
             pe = s.e[cur][c];
-            if (kc >= s.k0 && kc < s.k1) {
+            if (NM == 0 && kc >= s.k0 && kc < s.k1) {
                 prho = s.rhoc[c];
                 pcs = s.csc[c];
+            }
+#pragma unroll
+            for (int a = 0; a < NM; ++a) {
+                pmf[a] = mat_f(s, p, cur)[c + a * mat_stride(s)];
+                pmm[a] = mat_m(s, p, cur)[c + a * mat_stride(s)];
+                pme[a] = s.me[cur][c + a * mat_stride(s)];
             }
         }
     }
@@ -204,6 +214,13 @@ struct ForceCTA {
         // ---- P1: stage node plane kz+1 and cell (i,j,kz); prefetch the next
         put<B1>();
         const double m = pm, e = pe, crho = prho, ccs = pcs;
+        double cmf[NM > 0 ? NM : 1], cmm[NM > 0 ? NM : 1], cme[NM > 0 ? NM : 1], pfk[MAX_MAT];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            cmf[a] = pmf[a];
+            cmm[a] = pmm[a];
+            cme[a] = pme[a];
+        }
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
         // ---- P2: the three faces anchored at this column
@@ -230,7 +247,12 @@ struct ForceCTA {
                 const double* qx = me + 1;   // +x face (anchored at i+1)
                 const double* qy = me + FW;  // +y face (anchored at j+1)
                 double rho, pf, cs;
-                if (kz >= s.k0 && kz < s.k1) {  // owned: rho, c from the EoS cache (c.5 pass, same state)
+                if constexpr (NM > 0) {
+                    double sv[6] = {fx.s, qx[oQ(0, 0)], fy.s, qy[oQ(1, 0)], zprev.s, zn.s};
+                    double V = vol_from_s(sv), pr;
+                    rho = ddiv(m, V);
+                    mix_eos_r<NM>(p, cmf, cmm, cme, V, rho, pr, pf, cs, pfk);
+                } else if (kz >= s.k0 && kz < s.k1) {  // owned: rho, c from the EoS cache (c.5 pass, same state)
                     rho = crho;
                     cs = ccs;
                     const double pr = ((p.gamma - 1.0) * rho) * e;
@@ -247,7 +269,12 @@ struct ForceCTA {
                 double du = dmin(dmin(dx, dy), dz);
                 double q = q_of_du(rho, cs, du, p.c1, p.c2);
                 sig = 0.25 * (pf + q);
-                if (sig_col && kz >= za && kz >= kn0 && kz < kn1) s.sig[cb + (long long)kz * s.pc] = sig;
+                if (sig_col && kz >= za && kz >= kn0 && kz < kn1) {
+                    s.sig[cb + (long long)kz * s.pc] = sig;
+#pragma unroll
+                    for (int a = 0; a < NM; ++a)  // each material's stress (MM4)
+                        s.sgm[cb + (long long)kz * s.pc + a * mat_stride(s)] = 0.25 * (pfk[a] + q);
+                }
             }
             me[oS(B0, 0)] = sig;
             me[oS(B0, 1)] = m;
@@ -295,13 +322,13 @@ struct ForceCTA {
     }
 };
 
-template <bool EULER, int NW>
+template <bool EULER, int NW, int NM = 0>
 __global__ void __launch_bounds__(FW * NW, NW >= 12 ? 1 : MINB)
     kf_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];
-    ForceCTA<EULER, NW> c(s, p, cur, smem, kn0, kn1, zchunk);
+    ForceCTA<EULER, NW, NM> c(s, p, cur, smem, kn0, kn1, zchunk);
     c.run();
 }
 
@@ -763,7 +790,9 @@ __global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int k
 // ============================================================================
 // kf_energy
 // ============================================================================
-template <bool EULER, int NW>
+// NM > 0 (Lagrange, multi-material cells): MM4 per material from the
+// stresses kf_force stored (Slab::sgm), and the dt candidate from the mixed closure
+template <bool EULER, int NW, int NM = 0>
 struct EnergyCTA {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
     __host__ __device__ static constexpr int oP(int par, int c) { return (par * 10 + c) * PL; }  // x^n(3) x'(3) ubar(3) |u'|^2
@@ -782,6 +811,7 @@ struct EnergyCTA {
     unsigned long long key;
     D3 fx, fu, fu1, fx1;  // prefetch registers
     double fm, fe, fs;
+    double gf[NM > 0 ? NM : 1], gm[NM > 0 ? NM : 1], ge[NM > 0 ? NM : 1], gs[NM > 0 ? NM : 1];  // materials
     D3 zA_prev;
     double zs_prev, ex_prev, ey_prev;
 
@@ -826,6 +856,14 @@ struct EnergyCTA {
             fm = mass_cur(s, p, cur)[c];
             fe = s.e[cur][c];
             fs = s.sig[c];
+#pragma unroll
+            for (int a = 0; a < NM; ++a) {
+                const long long ca = c + a * mat_stride(s);
+                gf[a] = mat_f(s, p, cur)[ca];
+                gm[a] = mat_m(s, p, cur)[ca];
+                ge[a] = s.me[cur][ca];
+                gs[a] = s.sgm[ca];
+            }
         }
     }
     template <int PAR>
@@ -863,6 +901,14 @@ struct EnergyCTA {
         // ---- P1
         put<B1>();
         const double m = fm, e = fe, sig = fs;
+        double cf[NM > 0 ? NM : 1], cm[NM > 0 ? NM : 1], ce[NM > 0 ? NM : 1], csg[NM > 0 ? NM : 1];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            cf[a] = gf[a];
+            cm[a] = gm[a];
+            ce[a] = ge[a];
+            csg[a] = gs[a];
+        }
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
         // ---- P2: faces anchored at this column (A at t^n, s' at t^{n+1}); x' edges
@@ -907,15 +953,28 @@ struct EnergyCTA {
                 W = (h == 0) ? term : W + term;
             }
             const long long cc = cb + (long long)kz * s.pc;
-            const double e1 = e - ddiv((sig * W) * dt, m);
+            double e1k[NM > 0 ? NM : 1];
+            if constexpr (NM > 0) {  // MM4: each present material's share of the work
+#pragma unroll
+                for (int a = 0; a < NM; ++a) {
+                    e1k[a] = (cf[a] > 0.0 && cm[a] > 0.0) ? ce[a] - ddiv(((csg[a] * W) * dt) * cf[a], cm[a]) : ce[a];
+                    s.me[cur ^ 1][cc + a * mat_stride(s)] = e1k[a];
+                }
+            }
+            const double e1 = NM > 0 ? 0.0 : e - ddiv((sig * W) * dt, m);
             if (EULER) {
                 s.e1[cc] = e1;
                 s.V1[cc] = V1;
             } else {
-                s.e[cur ^ 1][cc] = e1;
+                if (NM == 0) s.e[cur ^ 1][cc] = e1;
                 if (owned) {
                     double rho = ddiv(m, V1), pr, pf, cs;
-                    eos(p.gamma, rho, e1, pr, pf, cs);
+                    if constexpr (NM > 0) {
+                        double pfk[MAX_MAT];
+                        mix_eos_r<NM>(p, cf, cm, e1k, V1, rho, pr, pf, cs, pfk);
+                    } else {
+                        eos(p.gamma, rho, e1, pr, pf, cs);
+                    }
                     s.rhoc[cc] = rho;
                     s.csc[cc] = cs;
                     double l2 = dmin(dmin(me[oE(0)], me[FW + oE(0)]), dmin(me[oE(1)], me[1 + oE(1)]));
@@ -975,13 +1034,13 @@ struct EnergyCTA {
     }
 };
 
-template <bool EULER, int NW, int MB>
+template <bool EULER, int NW, int MB, int NM = 0>
 __global__ void __launch_bounds__(FW * NW, MB)
     kf_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];
-    EnergyCTA<EULER, NW> c(s, p, cur, smem, kc0, kc1, zchunk);
+    EnergyCTA<EULER, NW, NM> c(s, p, cur, smem, kc0, kc1, zchunk);
     c.run();
 }
 
@@ -1410,31 +1469,31 @@ void set_smem(K kernel, size_t bytes)
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 }  // namespace
 
-template <bool EULER, int NW>
+template <bool EULER, int NW, int NM = 0>
 static void force_launch(const Slab& s, const Phys& p, int cur, int kn0, int kn1, int zc, cudaStream_t cs)
 {
-    const size_t sm = sizeof(double) * ForceCTA<EULER, NW>::WORDS;
+    const size_t sm = sizeof(double) * ForceCTA<EULER, NW, NM>::WORDS;
     static bool init = false;
     if (!init) {
-        set_smem(kf_force<EULER, NW>, sm);
+        set_smem(kf_force<EULER, NW, NM>, sm);
         init = true;
     }
     zc = zchunk_for((long long)cdiv(p.nx + 1, FW - 2) * cdiv(p.ny + 1, NW - 2), kn1 - kn0 + 1, zc);
     dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW - 2), cdiv(kn1 - kn0 + 1, zc));
-    kf_force<EULER, NW><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
+    kf_force<EULER, NW, NM><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
 }
-template <bool EULER, int NW, int MB>
+template <bool EULER, int NW, int MB, int NM = 0>
 static void energy_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
 {
-    const size_t sm = sizeof(double) * EnergyCTA<EULER, NW>::WORDS;
+    const size_t sm = sizeof(double) * EnergyCTA<EULER, NW, NM>::WORDS;
     static bool init = false;
     if (!init) {
-        set_smem(kf_energy<EULER, NW, MB>, sm);
+        set_smem(kf_energy<EULER, NW, MB, NM>, sm);
         init = true;
     }
     zc = zchunk_for((long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW - 1), kc1 - kc0, zc);
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
-    kf_energy<EULER, NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
+    kf_energy<EULER, NW, MB, NM><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
 }
 
 // z-chunk length of the z-marching grids (SALE_ZCHUNK overrides, for tuning runs)
@@ -1555,6 +1614,34 @@ int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
     if (p.diag_jumps) sigma_e_launch<8, 2, true>(s, p, cur, sc0, sc1, tune.zc, gate, (cudaStream_t)st);
     else sigma_e_launch<8, 2, false>(s, p, cur, sc0, sc1, tune.zc, gate, (cudaStream_t)st);
     return 1;
+}
+
+// Lagrange, multi-material cells: S1-S6 in one z-march with the mixed closure (kf_force
+// with NM materials; writes sigma, the materials' stresses, x', u'), then S7 per
+// material + the dt candidate (kf_energy with NM materials)
+int launch_force_mat(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    static const Tune tune;
+    cudaStream_t cs = (cudaStream_t)st;
+    switch (p.nmat) {
+    case 1:
+        force_launch<false, NW_FORCE, 1>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, 1, 1>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        break;
+    case 2:
+        force_launch<false, NW_FORCE, 2>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, 1, 2>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        break;
+    case 3:
+        force_launch<false, NW_FORCE, 3>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, 1, 3>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        break;
+    default:
+        force_launch<false, NW_FORCE, 4>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, 1, 4>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        break;
+    }
+    return 2;
 }
 
 // Euler S5-S6 node gather on sigma and the cell totals (the material path reuses it)

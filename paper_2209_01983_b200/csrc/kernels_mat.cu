@@ -18,6 +18,23 @@ static inline unsigned grid_for(long long n, int bs)
     return (unsigned)(g > 0 ? g : 1);
 }
 
+// call f(std::integral_constant<int, nmat>) -- the kernels are instantiated per
+// material count so the material loops unroll into registers
+template <int N>
+struct IC {
+    static constexpr int value = N;
+};
+template <class F>
+static void by_nmat(int nmat, F&& f)
+{
+    switch (nmat) {
+    case 1: f(IC<1>{}); break;
+    case 2: f(IC<2>{}); break;
+    case 3: f(IC<3>{}); break;
+    default: f(IC<4>{}); break;
+    }
+}
+
 int launch_nodes_v0(const Slab& s, const Phys& p, int cur, int kb0, int kb1, Stream st);  // kernels_v0.cu
 
 // MM1-MM3: geometry at t^n, mixed EoS, q from the cell density and mixed sound speed;
@@ -25,7 +42,7 @@ int launch_nodes_v0(const Slab& s, const Phys& p, int cur, int kb0, int kb1, Str
 // before the cycle's k_begin (gate = 0 for the first cycle of a sale_step call, when
 // DevState.active is still 0), it also forms the c.5 dt candidate of the owned cells
 // from the same mixed sound speed (the fixed target mesh's edges: as k_dt_candidate)
-template <bool EULER>
+template <bool EULER, int NM>
 __global__ void k_mat_sigma(Slab s, Phys p, int cur, int ka0, int ka1, int gate)
 {
     if (gate && !s.st->active) return;
@@ -43,10 +60,11 @@ __global__ void k_mat_sigma(Slab s, Phys p, int cur, int ka0, int ka1, int gate)
         long long c = cidx(s, p, i, j, k);
         double V = vol_from_s(sv);
         double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, P, cs;
-        mix_eos(p, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, P, cs, pf);
+        mix_eos_t<NM>(p, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, P, cs, pf);
         double q = hex_q(Xb, U, rho, cs, p.c1, p.c2);
-        s.qv[c] = q;
         s.sig[c] = 0.25 * (P + q);
+#pragma unroll
+        for (int a = 0; a < NM; ++a) s.sgm[c + a * mat_stride(s)] = 0.25 * (pf[a] + q);
         if (EULER && k >= s.k0 && k < s.k1) {
             const double lx = len2(D3{s.Xt[i], 0.0, 0.0}, D3{s.Xt[i + 1], 0.0, 0.0});
             const double ly = len2(D3{0.0, s.Yt[j], 0.0}, D3{0.0, s.Yt[j + 1], 0.0});
@@ -60,7 +78,7 @@ __global__ void k_mat_sigma(Slab s, Phys p, int cur, int ka0, int ka1, int gate)
 // MM4: V' + tangle check; each present material's e'_k from its stress
 // sigma_k = 0.25 (pf_k + q) on its share f_k of the cell's work W (c.3 step 7);
 // Lagrange: the next dt candidate from the mixed EoS of the new state
-template <bool EULER>
+template <bool EULER, int NM>
 __global__ void k_mat_energy(Slab s, Phys p, int cur, int kc0, int kc1)
 {
     if (!s.st->active) return;
@@ -98,18 +116,15 @@ __global__ void k_mat_energy(Slab s, Phys p, int cur, int kc0, int kc1)
         const double m = mass_cur(s, p, cur)[c];
         const double* f = mat_f(s, p, cur);
         const double* mk = mat_m(s, p, cur);
-        {  // the materials' floored pressures at t^n (the same bits k_mat_sigma saw)
-            double pr, P, cs;
-            const double V0 = vol_from_s(sv);
-            mix_eos(p, f, mk, s.me[cur], c, st, V0, ddiv(m, V0), pr, P, cs, pf);
-        }
-        const double q = s.qv[c], dt = s.st->dt;
+        const double dt = s.st->dt;
         double* e1 = EULER ? s.e1m : s.me[cur ^ 1];
-        for (int a = 0; a < p.nmat; ++a) {
+#pragma unroll
+    #pragma unroll
+    for (int a = 0; a < NM; ++a) {
             const long long ca = c + a * st;
             const double fa = f[ca], ma = mk[ca], ea = s.me[cur][ca];
             if (fa > 0.0 && ma > 0.0) {
-                const double sa = 0.25 * (pf[a] + q);
+                const double sa = s.sgm[ca];  // 0.25 (pf_k + q), from the sigma pass
                 e1[ca] = ea - ddiv(((sa * W) * dt) * fa, ma);
             } else {
                 e1[ca] = ea;
@@ -119,7 +134,7 @@ __global__ void k_mat_energy(Slab s, Phys p, int cur, int kc0, int kc1)
             s.V1[c] = V1;
         } else if (owned) {
             double pr, P, cs;
-            mix_eos(p, f, mk, s.me[cur ^ 1], c, st, V1, ddiv(m, V1), pr, P, cs, pf);
+            mix_eos_t<NM>(p, f, mk, s.me[cur ^ 1], c, st, V1, ddiv(m, V1), pr, P, cs, pf);
             key = dt_key(dt_cell(p.cfl, hex_min_edge2(N1), hex_max_speed2(U1), cs));
         }
     }
@@ -129,6 +144,7 @@ __global__ void k_mat_energy(Slab s, Phys p, int cur, int kc0, int kc1)
 // c.4 steps 1-2, per cell c: the swept volumes of its -x / -y / -z faces (interior
 // faces only; stored at the upper cell, as kr_sweep does), and the cell's donor data:
 // mean node velocity Ub = 0.125 * sum of u' and, per material, m_k / V' (MM5)
+template <int NM>
 __global__ void k_mat_sweep(Slab s, Phys p, int cur, int ks0, int ks1)
 {
     if (!s.st->active) return;
@@ -146,7 +162,7 @@ __global__ void k_mat_sweep(Slab s, Phys p, int cur, int ks0, int ks1)
     st3(s.UD, c, scl(0.125, sum));
     const double V1 = s.V1[c];
     const long long st = mat_stride(s);
-    for (int a = 0; a < p.nmat; ++a) s.rDm[c + a * st] = ddiv(s.mm[cur][c + a * st], V1);
+    for (int a = 0; a < NM; ++a) s.rDm[c + a * st] = ddiv(s.mm[cur][c + a * st], V1);
     // faces at node planes i / j / k, their lower cell at -1 on that axis; canonical
     // P0..P3 as c.4 step 1 / face_node_ids
     const int lo[3] = {i, j, k};
@@ -189,6 +205,7 @@ __device__ __forceinline__ double acc6(int f, double acc, double v)
 
 // MM5-MM6: per cell, the materials' fluxes through its six faces (boundary faces carry
 // +0.0), m''_k, V''_k, e''_k, f''_k, the totals Delta m, Delta P, m'' for the node update
+template <int NM>
 __global__ void k_mat_flux(Slab s, Phys p, int cur, int kr0, int kr1)
 {
     if (!s.st->active) return;
@@ -217,7 +234,9 @@ __global__ void k_mat_flux(Slab s, Phys p, int cur, int kr0, int kr1)
             dV = s.dV[ax][plus ? nbr : c];  // the face is the -ax face of the upper cell
             D = (dV > 0.0) == plus ? c : nbr; // donor: the lower cell if the face moved toward +ax
         }
-        for (int a = 0; a < p.nmat; ++a) {
+#pragma unroll
+    #pragma unroll
+    for (int a = 0; a < NM; ++a) {
             double mua = 0.0, pha = 0.0, epa = 0.0;
             if (inner) {
                 const long long Da = D + a * st;
@@ -236,7 +255,8 @@ __global__ void k_mat_flux(Slab s, Phys p, int cur, int kr0, int kr1)
     }
     double m2 = 0.0, VV = 0.0, vm2[MAX_MAT];
     bool bad = false;
-    for (int a = 0; a < p.nmat; ++a) {
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
         const long long ca = c + a * st;
         const double mm2 = s.mm[cur][ca] + dmk[a];
         vm2[a] = (s.mf[cur][ca] * s.V1[c]) + dphk[a];
@@ -246,7 +266,8 @@ __global__ void k_mat_flux(Slab s, Phys p, int cur, int kr0, int kr1)
     }
     if (k >= s.k0 && k < s.k1 && (bad || !(m2 > 0.0) || !(VV > 0.0)))
         atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, k));
-    for (int a = 0; a < p.nmat; ++a) {
+#pragma unroll
+    for (int a = 0; a < NM; ++a) {
         const long long ca = c + a * st;
         const double mm2 = s.mm[cur][ca] + dmk[a];
         const double e1 = s.e1m[ca];
@@ -296,15 +317,15 @@ int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st)
     cudaStream_t cs = (cudaStream_t)st;
     const int bs = 128;
     if (!p.rezone) {
-        int ka0 = s.k0 > 0 ? s.k0 - 1 : 0, ka1 = s.k1 < p.nz ? s.k1 + 1 : p.nz;
-        k_mat_sigma<false><<<grid_for(s.pc * (ka1 - ka0), bs), bs, 0, cs>>>(s, p, cur, ka0, ka1, 1);
-        launch_nodes_v0(s, p, cur, s.k0, s.k1, st);
-        k_mat_energy<false><<<grid_for(s.pc * (s.k1 - s.k0), bs), bs, 0, cs>>>(s, p, cur, s.k0, s.k1);
-        return 3;
+        // the fused z-march kernels with the material axis (kernels_fused.cu)
+        return launch_force_mat(s, p, cur, st);
     }
     int kb0 = s.k0 - 2 > 0 ? s.k0 - 2 : 0, kb1 = s.k1 + 2 < p.nz ? s.k1 + 2 : p.nz;
     launch_kn_force_e(s, p, cur, st);
-    k_mat_energy<true><<<grid_for(s.pc * (kb1 - kb0), bs), bs, 0, cs>>>(s, p, cur, kb0, kb1);
+    by_nmat(p.nmat, [&](auto nm) {
+        constexpr int NM = decltype(nm)::value;
+        k_mat_energy<true, NM><<<grid_for(s.pc * (kb1 - kb0), bs), bs, 0, cs>>>(s, p, cur, kb0, kb1);
+    });
     return 2;
 }
 
@@ -313,7 +334,11 @@ int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st)
 int launch_mat_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
 {
     int ka0 = s.k0 - 3 > 0 ? s.k0 - 3 : 0, ka1 = s.k1 + 3 < p.nz ? s.k1 + 3 : p.nz;
-    k_mat_sigma<true><<<grid_for(s.pc * (ka1 - ka0), 128), 128, 0, (cudaStream_t)st>>>(s, p, cur, ka0, ka1, gate);
+    by_nmat(p.nmat, [&](auto nm) {
+        constexpr int NM = decltype(nm)::value;
+        k_mat_sigma<true, NM><<<grid_for(s.pc * (ka1 - ka0), 128), 128, 0, (cudaStream_t)st>>>(s, p, cur, ka0, ka1,
+                                                                                               gate);
+    });
     return 1;
 }
 
@@ -326,8 +351,11 @@ int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st)
     const int bs = 128;
     int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     int ks0 = kr0 - 1 > 0 ? kr0 - 1 : 0, ks1 = kr1 + 1 < p.nz ? kr1 + 1 : p.nz;
-    k_mat_sweep<<<grid_for(s.pc * (ks1 - ks0), bs), bs, 0, cs>>>(s, p, cur, ks0, ks1);
-    k_mat_flux<<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);
+    by_nmat(p.nmat, [&](auto nm) {
+        constexpr int NM = decltype(nm)::value;
+        k_mat_sweep<NM><<<grid_for(s.pc * (ks1 - ks0), bs), bs, 0, cs>>>(s, p, cur, ks0, ks1);
+        k_mat_flux<NM><<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);
+    });
     launch_kn_update(s, p, cur, st);
     return 3;
 }

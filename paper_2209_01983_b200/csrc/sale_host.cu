@@ -205,7 +205,7 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
         s.mm[b] = M && (b == 0 || euler) ? take(M * nc) : nullptr;
         s.me[b] = M ? take(M * nc) : nullptr;
     }
-    s.qv = M ? take(nc) : nullptr;
+    s.sgm = M ? take(M * nc) : nullptr;
     s.e1m = M && euler ? take(M * nc) : nullptr;
     s.rDm = M && euler ? take(M * nc) : nullptr;
     return off;

@@ -94,7 +94,7 @@ struct Slab {
     double* mf[2];            // volume fraction f_k
     double* mm[2];            // material mass m_k (m above holds the sum over k)
     double* me[2];            // material specific energy e_k
-    double* qv;               // scratch: q of the cycle start (the materials' stress needs it)
+    double* sgm;              // scratch: each material's stress 0.25 (pf_k + q) at the cycle start (MM4)
     double* e1m;              // Euler scratch: e'_k
     double* rDm;              // Euler scratch: donor material density m_k / V' of each cell (k_mat_sweep)
     DevState* st;
@@ -141,6 +141,7 @@ int launch_mat_total(const Slab& s, const Phys& p, int cur, Stream st);
 // Euler: sigma + the cycle-start dt candidate, before the cycle's k_begin (gate as launch_euler_pre)
 int launch_mat_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st);
 int launch_kn_force_e(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_force_mat(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st);

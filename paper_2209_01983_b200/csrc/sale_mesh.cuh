@@ -94,20 +94,21 @@ __device__ __forceinline__ const double* mat_m(const Slab& s, const Phys& p, int
 // the c.3 step 1 EoS with its own gamma; pr = sum f_k p_k, P = sum f_k pf_k,
 // cs = sqrt((sum f_k (gamma_k pf_k)) / rho); sums left to right from the first present
 // material.  pf[k] = 0 for absent materials.  One material with f_0 = 1 gives eos()'s
-// bits (1.0 * a = a).
-__device__ __forceinline__ void mix_eos(const Phys& p, const double* f, const double* mm, const double* e,
-                                        long long c, long long stride, double V, double rho, double& pr,
-                                        double& P, double& cs, double pf[MAX_MAT])
+// bits (1.0 * a = a).  NM > 0: the material count as a compile-time constant (the
+// loop unrolls, pf stays in registers); NM = 0: p.nmat.
+template <int NM>
+__device__ __forceinline__ void mix_eos_r(const Phys& p, const double* f, const double* mm, const double* e, double V,
+                                          double rho, double& pr, double& P, double& cs, double pf[MAX_MAT])
 {
     double ps = 0.0, Ps = 0.0, G = 0.0;
     bool first = true;
-    for (int k = 0; k < p.nmat; ++k) {
+#pragma unroll
+    for (int k = 0; k < (NM ? NM : p.nmat); ++k) {
         pf[k] = 0.0;
-        const long long ck = c + k * stride;
-        const double fk = f[ck];
+        const double fk = f[k];
         if (!(fk > 0.0)) continue;
-        const double rk = ddiv(mm[ck], fk * V);
-        const double pk = ((p.mg[k] - 1.0) * rk) * e[ck];
+        const double rk = ddiv(mm[k], fk * V);
+        const double pk = ((p.mg[k] - 1.0) * rk) * e[k];
         const double pfk = (pk > 0.0) ? pk : 0.0;
         pf[k] = pfk;
         const double a = fk * pk, b = fk * pfk, g = fk * (p.mg[k] * pfk);
@@ -125,6 +126,27 @@ __device__ __forceinline__ void mix_eos(const Phys& p, const double* f, const do
     pr = ps;
     P = Ps;
     cs = dsqrt(ddiv(G, rho));
+}
+// the same from the material arrays of cell c (material k at c + k*stride)
+template <int NM>
+__device__ __forceinline__ void mix_eos_t(const Phys& p, const double* f, const double* mm, const double* e,
+                                          long long c, long long stride, double V, double rho, double& pr,
+                                          double& P, double& cs, double pf[MAX_MAT])
+{
+    double fr[MAX_MAT], mr[MAX_MAT], er[MAX_MAT];
+#pragma unroll
+    for (int k = 0; k < (NM ? NM : p.nmat); ++k) {
+        fr[k] = f[c + k * stride];
+        mr[k] = mm[c + k * stride];
+        er[k] = e[c + k * stride];
+    }
+    mix_eos_r<NM>(p, fr, mr, er, V, rho, pr, P, cs, pf);
+}
+__device__ __forceinline__ void mix_eos(const Phys& p, const double* f, const double* mm, const double* e,
+                                        long long c, long long stride, double V, double rho, double& pr,
+                                        double& P, double& cs, double pf[MAX_MAT])
+{
+    mix_eos_t<0>(p, f, mm, e, c, stride, V, rho, pr, P, cs, pf);
 }
 
 // host: z-chunk length of a z-marching grid.  Large meshes use zc0 planes per CTA;
