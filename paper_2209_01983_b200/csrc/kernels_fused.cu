@@ -26,6 +26,8 @@
 // need clamping; cell presence in the node gather is a predicate, not a branch.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -577,7 +579,9 @@ __global__ void __launch_bounds__(FW * NW, MB) kf_force_e(Slab s, Phys p, int cu
 // and when it is zero the jump is a zero of some sign, which q ignores (q depends on
 // du only through du < 0 and, when negative, its value): sigma is the same bits with
 // only the a-component of the face-average velocity on axis a.
-template <int NW, bool DIAG>
+// NM > 0: multi-material cells: the mixed closure MM1, and each
+// material's stress 0.25 (pf_k + q) stored for the energy kernel (Slab::sgm)
+template <int NW, bool DIAG, int NM = 0>
 struct SigmaEulerCTA {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
     __host__ __device__ static constexpr int oU(int par, int c) { return (par * 3 + c) * PL; }       // node u
@@ -593,6 +597,7 @@ struct SigmaEulerCTA {
     bool col_in, out_cell;
     D3 pu;
     double pm, pe, pv;
+    double pmf[NM > 0 ? NM : 1], pmm[NM > 0 ? NM : 1], pme[NM > 0 ? NM : 1];  // prefetch: materials
     bool pnok;
     D3 zprev;
     unsigned long long key;  // running min of the owned cells' dt keys (c.5)
@@ -630,6 +635,12 @@ struct SigmaEulerCTA {
         pm = s.m[cur][c];
         pe = s.e[cur][c];
         pv = s.VT[c];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            pmf[a] = s.mf[cur][c + a * mat_stride(s)];
+            pmm[a] = s.mm[cur][c + a * mat_stride(s)];
+            pme[a] = s.me[cur][c + a * mat_stride(s)];
+        }
     }
     template <int PAR>
     __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oU(PAR, 0), PL); }
@@ -645,6 +656,13 @@ struct SigmaEulerCTA {
         constexpr int B1 = B0 ^ 1;
         st3s(me, oU(B1, 0), PL, pnok ? pu : D3{0.0, 0.0, 0.0});
         const double m = pm, e = pe, V = pv;
+        double cmf[NM > 0 ? NM : 1], cmm[NM > 0 ? NM : 1], cme[NM > 0 ? NM : 1];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            cmf[a] = pmf[a];
+            cmm[a] = pmm[a];
+            cme[a] = pme[a];
+        }
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
         D3 ux, uy, uz;
@@ -685,8 +703,9 @@ struct SigmaEulerCTA {
             for (int c = 0; c < 4; ++c) tj[a][c] = TJ[a][c];
         __syncthreads();
         if (out_cell && kz >= 0 && kz < p.nz) {
-            double rho = ddiv(m, V), pr, pf, cs;
-            eos(p.gamma, rho, e, pr, pf, cs);
+            double rho = ddiv(m, V), pr, pf, cs, pfk[MAX_MAT];
+            if constexpr (NM > 0) mix_eos_r<NM>(p, cmf, cmm, cme, V, rho, pr, pf, cs, pfk);
+            else eos(p.gamma, rho, e, pr, pf, cs);
             double dx, dy, dz;
             if constexpr (DIAG) {
                 dx = ddiv((me[1 + oW(0, 0)] - ux.x) * tj[0][0], tj[0][3]);
@@ -700,6 +719,8 @@ struct SigmaEulerCTA {
             const double du = dmin(dmin(dx, dy), dz);
             const double q = q_of_du(rho, cs, du, p.c1, p.c2);
             s.sig[cb + (long long)kz * s.pc] = 0.25 * (pf + q);
+#pragma unroll
+            for (int a = 0; a < NM; ++a) s.sgm[cb + (long long)kz * s.pc + a * mat_stride(s)] = 0.25 * (pfk[a] + q);
             if (kz >= s.k0 && kz < s.k1) {
                 // c.5 dt candidate of this (cycle-start) state: v2 (P2), cfl * sqrt(min
                 // edge^2) from the per-axis tables (as kn_dt)
@@ -729,12 +750,12 @@ struct SigmaEulerCTA {
 };
 
 // gate = 0 for the first cycle of a sale_step call (DevState.active is still 0 there)
-template <int NW, int MB, bool DIAG>
+template <int NW, int MB, bool DIAG, int NM = 0>
 __global__ void __launch_bounds__(FW * NW, MB) kf_sigma_e(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk, int gate)
 {
     if (gate && !s.st->active) return;
     extern __shared__ double smem[];
-    SigmaEulerCTA<NW, DIAG> c(s, p, cur, smem, kc0, kc1, zchunk);
+    SigmaEulerCTA<NW, DIAG, NM> c(s, p, cur, smem, kc0, kc1, zchunk);
     c.run();
 }
 
@@ -1048,7 +1069,9 @@ __global__ void __launch_bounds__(FW * NW, MB)
 // kf_energy, Euler mode: A^n from the target tables (as kf_force_e); stages only
 // x' and ubar = (u + u')/2.  Writes e' and V' (the remap's inputs).
 // ============================================================================
-template <int NW>
+// NM > 0: multi-material cells: MM4 per material (e'_k into
+// Slab::e1m) from the stresses kf_sigma_e stored, instead of e'
+template <int NW, int NM = 0>
 struct EnergyEulerCTA {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
     __host__ __device__ static constexpr int oP(int par, int c) { return (par * 6 + c) * PL; }        // x'(3) ubar(3)
@@ -1065,6 +1088,7 @@ struct EnergyEulerCTA {
     bool col_in, cell_col, own_col;
     D3 fu, fu1, fx1;  // prefetch registers (unconditional loads, selected at use)
     double fm, fe, fs;
+    double gf[NM > 0 ? NM : 1], gm[NM > 0 ? NM : 1], ge[NM > 0 ? NM : 1], gs[NM > 0 ? NM : 1];  // materials
     D3 fax, fay;      // prefetch: table A of the x- / y-face of cell plane k-1
     bool fnok, fcok;
     double zs_prev;
@@ -1111,6 +1135,14 @@ struct EnergyEulerCTA {
         fm = s.m[cur][c];
         fe = s.e[cur][c];
         fs = s.sig[c];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            const long long ca = c + a * mat_stride(s);
+            gf[a] = s.mf[cur][ca];
+            gm[a] = s.mm[cur][ca];
+            ge[a] = s.me[cur][ca];
+            gs[a] = s.sgm[ca];
+        }
         const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
         fax = D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]};
         fay = D3{s.TAy[0][ty], s.TAy[1][ty], s.TAy[2][ty]};
@@ -1139,6 +1171,14 @@ struct EnergyEulerCTA {
         constexpr int B1 = B0 ^ 1;
         put<B1>();
         const double m = fcok ? fm : 0.0, e = fcok ? fe : 0.0, sig = fcok ? fs : 0.0;
+        double cf[NM > 0 ? NM : 1], cm[NM > 0 ? NM : 1], ce[NM > 0 ? NM : 1], csg[NM > 0 ? NM : 1];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            cf[a] = gf[a];
+            cm[a] = gm[a];
+            ce[a] = ge[a];
+            csg[a] = gs[a];
+        }
         const D3 ax = fax, ay = fay;
         if (kz < zb) fetch(kz + 2, cur);
         __syncthreads();
@@ -1181,7 +1221,14 @@ struct EnergyEulerCTA {
                 W = (h == 0) ? term : W + term;
             }
             const long long cc = cb + (long long)kz * s.pc;
-            s.e1[cc] = e - ddiv((sig * W) * dt, m);
+            if constexpr (NM > 0) {  // MM4: each present material's share of the work
+#pragma unroll
+                for (int a = 0; a < NM; ++a)
+                    s.e1m[cc + a * mat_stride(s)] =
+                        (cf[a] > 0.0 && cm[a] > 0.0) ? ce[a] - ddiv(((csg[a] * W) * dt) * cf[a], cm[a]) : ce[a];
+            } else {
+                s.e1[cc] = e - ddiv((sig * W) * dt, m);
+            }
             s.V1[cc] = V1;
         }
         zs_prev = zs_next;
@@ -1443,12 +1490,12 @@ __global__ void __launch_bounds__(FW * NW, MB)
     c.run(cur);
 }
 
-template <int NW, int MB>
+template <int NW, int MB, int NM = 0>
 __global__ void __launch_bounds__(FW * NW, MB) kf_energy_e(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];
-    EnergyEulerCTA<NW> c(s, p, smem, kc0, kc1, zchunk);
+    EnergyEulerCTA<NW, NM> c(s, p, smem, kc0, kc1, zchunk);
     c.run(cur);
 }
 
@@ -1520,32 +1567,32 @@ static void force_e_launch(const Slab& s, const Phys& p, int cur, int kn0, int k
     kf_force_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
 }
 
-template <int NW, int MB>
+template <int NW, int MB, int NM = 0>
 static void energy_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
 {
-    const size_t sm = sizeof(double) * EnergyEulerCTA<NW>::WORDS;
+    const size_t sm = sizeof(double) * EnergyEulerCTA<NW, NM>::WORDS;
     static bool init = false;
     if (!init) {
-        set_smem(kf_energy_e<NW, MB>, sm);
+        set_smem(kf_energy_e<NW, MB, NM>, sm);
         init = true;
     }
     zc = zchunk_for((long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW - 1), kc1 - kc0, zc);
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
-    kf_energy_e<NW, MB><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
+    kf_energy_e<NW, MB, NM><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc);
 }
 
-template <int NW, int MB, bool DIAG>
+template <int NW, int MB, bool DIAG, int NM = 0>
 static void sigma_e_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, int gate, cudaStream_t cs)
 {
-    const size_t sm = sizeof(double) * SigmaEulerCTA<NW, DIAG>::WORDS;
+    const size_t sm = sizeof(double) * SigmaEulerCTA<NW, DIAG, NM>::WORDS;
     static bool init = false;
     if (!init) {
-        set_smem(kf_sigma_e<NW, MB, DIAG>, sm);
+        set_smem(kf_sigma_e<NW, MB, DIAG, NM>, sm);
         init = true;
     }
     zc = zchunk_for((long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW - 1), kc1 - kc0, zc);
     dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW - 1), cdiv(kc1 - kc0, zc));
-    kf_sigma_e<NW, MB, DIAG><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc, gate);
+    kf_sigma_e<NW, MB, DIAG, NM><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kc0, kc1, zc, gate);
 }
 
 template <int NW, int MB>
@@ -1616,6 +1663,28 @@ int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
     return 1;
 }
 
+// Euler, multi-material cells: kf_sigma_e with the mixed closure (sigma, the materials'
+// stresses, the dt candidate), before the cycle's k_begin, over launch_euler_pre's planes
+int launch_sigma_e_mat(const Slab& s, const Phys& p, int cur, int gate, Stream st)
+{
+    static const Tune tune;
+    const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
+    const int sc0 = kn0 - 1 > 0 ? kn0 - 1 : 0, sc1 = kn1 + 1 < p.nz ? kn1 + 1 : p.nz;
+    cudaStream_t cs = (cudaStream_t)st;
+    auto go = [&](auto dg) {
+        constexpr bool DG = decltype(dg)::value;
+        switch (p.nmat) {
+        case 1: sigma_e_launch<8, 2, DG, 1>(s, p, cur, sc0, sc1, tune.zc, gate, cs); break;
+        case 2: sigma_e_launch<8, 2, DG, 2>(s, p, cur, sc0, sc1, tune.zc, gate, cs); break;
+        case 3: sigma_e_launch<8, 2, DG, 3>(s, p, cur, sc0, sc1, tune.zc, gate, cs); break;
+        default: sigma_e_launch<8, 2, DG, 4>(s, p, cur, sc0, sc1, tune.zc, gate, cs); break;
+        }
+    };
+    if (p.diag_jumps) go(std::true_type{});
+    else go(std::false_type{});
+    return 1;
+}
+
 // Lagrange, multi-material cells: S1-S6 in one z-march with the mixed closure (kf_force
 // with NM materials; writes sigma, the materials' stresses, x', u'), then S7 per
 // material + the dt candidate (kf_energy with NM materials)
@@ -1642,6 +1711,22 @@ int launch_force_mat(const Slab& s, const Phys& p, int cur, Stream st)
         break;
     }
     return 2;
+}
+
+// Euler, multi-material cells: S7 per material (kf_energy_e with NM materials; writes
+// e'_k, V', and the moved-face s' kr_sweep reads), over lagrange_fused's planes
+int launch_energy_e_mat(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    static const Tune tune;
+    const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
+    cudaStream_t cs = (cudaStream_t)st;
+    switch (p.nmat) {
+    case 1: energy_e_launch<8, 2, 1>(s, p, cur, kn0, kn1, tune.zc, cs); break;
+    case 2: energy_e_launch<8, 2, 2>(s, p, cur, kn0, kn1, tune.zc, cs); break;
+    case 3: energy_e_launch<8, 2, 3>(s, p, cur, kn0, kn1, tune.zc, cs); break;
+    default: energy_e_launch<8, 2, 4>(s, p, cur, kn0, kn1, tune.zc, cs); break;
+    }
+    return 1;
 }
 
 // Euler S5-S6 node gather on sigma and the cell totals (the material path reuses it)

@@ -8,6 +8,8 @@
 // node kernels (force gather, momentum remap) are v0's, on the cell totals.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "sale_mesh.cuh"
 
 namespace sale {
@@ -16,6 +18,18 @@ static inline unsigned grid_for(long long n, int bs)
 {
     long long g = (n + bs - 1) / bs;
     return (unsigned)(g > 0 ? g : 1);
+}
+
+// SALE_MAT_V0=1: the Euler material path on its one-thread-per-cell kernels
+// (k_mat_sigma, k_mat_energy, k_mat_sweep) instead of the z-march kernels with the
+// material axis (kf_sigma_e, kf_energy_e, kr_sweep) -- a cross-check, same bits
+static bool mat_v0()
+{
+    static const int v = [] {
+        const char* e = getenv("SALE_MAT_V0");
+        return e ? atoi(e) : 0;
+    }();
+    return v == 1;
 }
 
 // call f(std::integral_constant<int, nmat>) -- the kernels are instantiated per
@@ -322,6 +336,7 @@ int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st)
     }
     int kb0 = s.k0 - 2 > 0 ? s.k0 - 2 : 0, kb1 = s.k1 + 2 < p.nz ? s.k1 + 2 : p.nz;
     launch_kn_force_e(s, p, cur, st);
+    if (!mat_v0()) return 1 + launch_energy_e_mat(s, p, cur, st);
     by_nmat(p.nmat, [&](auto nm) {
         constexpr int NM = decltype(nm)::value;
         k_mat_energy<true, NM><<<grid_for(s.pc * (kb1 - kb0), bs), bs, 0, cs>>>(s, p, cur, kb0, kb1);
@@ -333,6 +348,7 @@ int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st)
 // candidate of the owned cells, before the cycle's k_begin
 int launch_mat_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
 {
+    if (!mat_v0()) return launch_sigma_e_mat(s, p, cur, gate, st);
     int ka0 = s.k0 - 3 > 0 ? s.k0 - 3 : 0, ka1 = s.k1 + 3 < p.nz ? s.k1 + 3 : p.nz;
     by_nmat(p.nmat, [&](auto nm) {
         constexpr int NM = decltype(nm)::value;
@@ -351,9 +367,11 @@ int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st)
     const int bs = 128;
     int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     int ks0 = kr0 - 1 > 0 ? kr0 - 1 : 0, ks1 = kr1 + 1 < p.nz ? kr1 + 1 : p.nz;
+    const bool v0 = mat_v0();
+    if (!v0) launch_sweep_mat(s, p, cur, st);
     by_nmat(p.nmat, [&](auto nm) {
         constexpr int NM = decltype(nm)::value;
-        k_mat_sweep<NM><<<grid_for(s.pc * (ks1 - ks0), bs), bs, 0, cs>>>(s, p, cur, ks0, ks1);
+        if (v0) k_mat_sweep<NM><<<grid_for(s.pc * (ks1 - ks0), bs), bs, 0, cs>>>(s, p, cur, ks0, ks1);
         k_mat_flux<NM><<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);
     });
     launch_kn_update(s, p, cur, st);

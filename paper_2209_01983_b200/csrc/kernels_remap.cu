@@ -979,7 +979,9 @@ __global__ void __launch_bounds__(256) kn_dt(Slab s, Phys p, int cur)
 //              data (c.4 step 2), the cell update (c.4 step 3).
 // Same expressions, operands and association as kr_cells / the oracle.
 // ============================================================================
-template <int NW>
+// NM > 0: multi-material cells: the donor data per material,
+// m_k / V' (Slab::rDm, MM5), instead of r = m / V'
+template <int NW, int NM = 0>
 struct SweepCTA {
     static constexpr int PL = NW * RW, TX = RW - 1, TY = NW - 1;
     __host__ __device__ static constexpr int oN(int par, int c) { return (par * 6 + c) * PL; }  // x'(3) u'(3)
@@ -997,6 +999,7 @@ struct SweepCTA {
     double tx0, tx1, ty0, ty1;
     D3 qx1, qu1;        // prefetch: node plane (unconditional loads, selected at use)
     double qm, qv;      // prefetch: cell m, V' of the plane before
+    double qmm[NM > 0 ? NM : 1];  // prefetch: material masses
     double qz;          // prefetch: Z of node plane k
     double zprev;       // Z of node plane t
     bool qnok;
@@ -1049,6 +1052,8 @@ struct SweepCTA {
         const long long c = cbc + (long long)kc * s.pc;
         qm = s.m[cur][c];
         qv = s.V1[c];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) qmm[a] = s.mm[cur][c + a * mat_stride(s)];
         qz = s.Zt[kn - s.kb];
     }
     template <int PAR>
@@ -1082,6 +1087,9 @@ struct SweepCTA {
         // ---- P1: stage node plane t+1 (its cell-plane t operands come with it); prefetch t+2
         put<B1>();
         const double m = qm, V1 = qv, z0 = zprev, z1 = qz;
+        double cmm[NM > 0 ? NM : 1];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) cmm[a] = qmm[a];
         if (t < tb) fetch(t + 2);
         __syncthreads();
         // ---- P2: ribbons of this column, moved faces, donor data of cell (i,j,t)
@@ -1115,7 +1123,12 @@ struct SweepCTA {
             sum = add(sum, UL<B1>(RW));
             sum = add(sum, UL<B1>(RW + 1));
             st3(s.UD, c, scl(0.125, sum));
-            s.rD[c] = ddiv(m, V1);
+            if constexpr (NM > 0) {
+#pragma unroll
+                for (int a = 0; a < NM; ++a) s.rDm[c + a * mat_stride(s)] = ddiv(cmm[a], V1);
+            } else {
+                s.rD[c] = ddiv(m, V1);
+            }
         }
         __syncthreads();
         // ---- P3: swept volumes of the cell's -x, -y, -z faces (interior faces only)
@@ -1155,12 +1168,12 @@ struct SweepCTA {
     }
 };
 
-template <int NW, int MB>
+template <int NW, int MB, int NM = 0>
 __global__ void __launch_bounds__(RW * NW, MB) kr_sweep(Slab s, Phys p, int cur, int kr0, int kr1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];
-    SweepCTA<NW> c(s, p, cur, smem, kr0, kr1, zchunk);
+    SweepCTA<NW, NM> c(s, p, cur, smem, kr0, kr1, zchunk);
     c.run();
 }
 
@@ -1236,6 +1249,31 @@ static void cells_p_launch(const Slab& s, const Phys& p, int cur, int kr0, int k
 
     dim3 grid(cdivr(p.nx, RW - 3), cdivr(p.ny, NW - 3), cdivr(kr1 - kr0, zc));
     kr_cells_p<NW, MB><<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zc);
+}
+
+// multi-material cells: kr_sweep with the per-material donor densities (Slab::rDm)
+int launch_sweep_mat(const Slab& s, const Phys& p, int cur, Stream st)
+{
+    const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
+    auto sweep = [&](auto kern) {
+        static bool init = false;
+        const size_t words = SweepCTA<8>::WORDS;
+        if (!init) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * words));
+            init = true;
+        }
+        const int t0 = kr0 - 1 > 0 ? kr0 - 1 : 0, t1 = kr1 < p.nz - 1 ? kr1 : p.nz - 1;
+        const int zc = zchunk_for((long long)cdivr(p.nx, RW - 1) * cdivr(p.ny, 8 - 1), t1 - t0 + 1, RZ);
+        dim3 grid(cdivr(p.nx, RW - 1), cdivr(p.ny, 8 - 1), cdivr(t1 - t0 + 1, zc));
+        kern<<<grid, dim3(RW, 8), sizeof(double) * words, (cudaStream_t)st>>>(s, p, cur, kr0, kr1, zc);
+    };
+    switch (p.nmat) {
+    case 1: sweep(kr_sweep<8, 2, 1>); break;
+    case 2: sweep(kr_sweep<8, 2, 2>); break;
+    case 3: sweep(kr_sweep<8, 2, 3>); break;
+    default: sweep(kr_sweep<8, 2, 4>); break;
+    }
+    return 1;
 }
 
 // R4 node momentum update on the cell totals (the material path reuses it)

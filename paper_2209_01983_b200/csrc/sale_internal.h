@@ -142,6 +142,9 @@ int launch_mat_total(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_mat_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st);
 int launch_kn_force_e(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_force_mat(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_sigma_e_mat(const Slab& s, const Phys& p, int cur, int gate, Stream st);
+int launch_energy_e_mat(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_sweep_mat(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st);

@@ -41,3 +41,37 @@ def test_variant_bitwise(env):
     e = dict(os.environ, **env)
     out = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=e, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+MAT_SCRIPT = r"""
+import sys
+sys.path.insert(0, %r)
+import oracle as O
+from paper_2209_01983_b200 import inputs
+from paper_2209_01983_b200.configs import sedov, EULER, LAGRANGE
+from paper_2209_01983_b200.sale import Sale
+from tests.helpers import ALL_FIELDS, compare
+from tests.test_gpu_materials import apply_perturbation_mm, mat_fields
+for rezone in (EULER, LAGRANGE):
+    for shape, nmat in (((13, 7, 9), 2), ((21, 5, 8), 3), ((1, 1, 6), 1)):
+        cfg = sedov(shape, rezone, nmat=nmat, mat_gamma=[1.4, 5.0 / 3.0, 1.2][:nmat])
+        g, o = Sale(cfg, impl="fused"), O.Oracle(cfg)
+        apply_perturbation_mm((g, o), cfg, 6)
+        for chunk in (1, 7, 12):
+            rg, ro = g.step(chunk), o.step(chunk)
+            assert rg == ro, (shape, rg, ro)
+        compare(g, o, ALL_FIELDS + mat_fields(nmat))
+        assert g.clock() == o.clock()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"SALE_MAT_V0": "1"}, {"SALE_GRAPHS": "0"}])
+def test_material_variant_bitwise(env):
+    """The material path's one-thread-per-cell Euler kernels (SALE_MAT_V0=1, the
+    cross-check of the z-march kernels with the material axis), and the material path
+    without CUDA-graph replay."""
+    e = dict(os.environ, **env)
+    out = subprocess.run([sys.executable, "-c", MAT_SCRIPT % ROOT], env=e, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
