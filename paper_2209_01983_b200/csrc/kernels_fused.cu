@@ -1692,14 +1692,16 @@ int launch_force_mat(const Slab& s, const Phys& p, int cur, Stream st)
 {
     static const Tune tune;
     cudaStream_t cs = (cudaStream_t)st;
+    // (energy: two 8-warp CTAs per SM at 128 registers for 1-2 materials, measured
+    // faster despite the spill; one CTA for 3-4, whose larger spill made it slower)
     switch (p.nmat) {
     case 1:
         force_launch<false, NW_FORCE, 1>(s, p, cur, s.k0, s.k1, tune.zc, cs);
-        energy_launch<false, NW_ENERGY, 1, 1>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, 2, 1>(s, p, cur, s.k0, s.k1, tune.zc, cs);
         break;
     case 2:
         force_launch<false, NW_FORCE, 2>(s, p, cur, s.k0, s.k1, tune.zc, cs);
-        energy_launch<false, NW_ENERGY, 1, 2>(s, p, cur, s.k0, s.k1, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, 2, 2>(s, p, cur, s.k0, s.k1, tune.zc, cs);
         break;
     case 3:
         force_launch<false, NW_FORCE, 3>(s, p, cur, s.k0, s.k1, tune.zc, cs);
