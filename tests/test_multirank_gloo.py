@@ -89,10 +89,13 @@ def _worker(rank, world, port, cfg, full, q):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("rezone,full", [(LAGRANGE, False), (LAGRANGE, True), (EULER, False)])
-def test_halo_plan_over_gloo(world, rezone, full):
+@pytest.mark.parametrize("rezone,full,nmat", [(LAGRANGE, False, 0), (LAGRANGE, True, 0), (EULER, False, 0),
+                                              (EULER, False, 2), (LAGRANGE, True, 3)])
+def test_halo_plan_over_gloo(world, rezone, full, nmat):
     build.build()
     cfg = sedov((5, 4, 13), rezone)
+    if nmat:  # the material axis: one cell array per material and quantity joins the plan
+        cfg = dict(cfg, nmat=nmat, mat_gamma=[1.4, 1.6, 1.8][:nmat])
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -135,3 +138,8 @@ def test_plan_field_sets():
     e = {m["field"] for m in sale.halo_plan(sedov((4, 4, 8), EULER), 1, 2)}
     assert e == {"UX", "UY", "UZ", "MASS", "E"}
     assert sale.halo_plan(cfg, 0, 1) == []
+    m = {m["field"] for m in sale.halo_plan(sedov((4, 4, 8), EULER, nmat=2, mat_gamma=[1.4, 1.6]), 1, 2)}
+    assert m == e | {"MAT_F0", "MAT_M0", "MAT_E0", "MAT_F1", "MAT_M1", "MAT_E1"}
+    lm = sedov((4, 4, 8), LAGRANGE, nmat=2, mat_gamma=[1.4, 1.6])
+    assert {m["field"] for m in sale.halo_plan(lm, 0, 2)} == f | {"MAT_E0", "MAT_E1"}  # f_k, m_k constant
+    assert {m["field"] for m in sale.halo_plan(lm, 0, 2, full=True)} >= {"MAT_F1", "MAT_M1", "MASS"}
