@@ -32,3 +32,27 @@ def test_random_shapes_bitwise(case):
         assert rg == ro, (shape, rezone, slabs, rg, ro)
     compare(g, o)
     assert g.clock() == o.clock()
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_shapes_materials_bitwise(case):
+    """The same sweep through the material kernels: 1-4 materials, a seeded mixed state
+    (inputs.material_mix), random gammas."""
+    from paper_2209_01983_b200.sale import Sale
+    from tests.test_gpu_materials import apply_perturbation_mm, mat_fields
+    from tests.helpers import ALL_FIELDS
+    rng = np.random.Generator(np.random.PCG64(5000 + case))
+    shape = tuple(int(x) for x in rng.integers(1, 34, size=3))
+    rezone = (LAGRANGE, EULER)[case % 2]
+    g_depth = 1 if rezone == LAGRANGE else 3
+    slabs = max(1, min(int(rng.integers(1, 4)), shape[2] // g_depth))
+    nmat = int(rng.integers(1, 5))
+    cfg = sedov(shape, rezone, nmat=nmat, mat_gamma=[float(x) for x in rng.uniform(1.1, 3.0, size=nmat)])
+    g = Sale(cfg, impl="fused", local_slabs=slabs)
+    o = O.Oracle(cfg)
+    apply_perturbation_mm((g, o), cfg, int(rng.integers(0, 1000)))
+    for n in rng.integers(1, 9, size=3):
+        rg, ro = g.step(int(n)), o.step(int(n))
+        assert rg == ro, (shape, rezone, slabs, nmat, rg, ro)
+    compare(g, o, ALL_FIELDS + mat_fields(nmat))
+    assert g.clock() == o.clock()
