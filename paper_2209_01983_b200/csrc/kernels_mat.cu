@@ -1,11 +1,17 @@
 // kernels_mat.cu -- multi-material cells (readings MM0-MM7 in
 // DESIGN.md §10d; the paper's multi-material ScalSALE, with the
-// closure of SPEC S:255-263).  The v0 schedule (one kernel per step, one thread per
-// cell or node) with a material axis: the cell carries f_k, m_k, e_k of up to MAX_MAT
-// materials (material-major arrays, Slab::mf/mm/me), the EoS is the mixed closure
-// mix_eos (sale_mesh.cuh), each material does its share of the cell's pdV work, and
-// the remap moves each material's mass, volume and energy from the donor cell.  The
-// node kernels (force gather, momentum remap) are v0's, on the cell totals.
+// closure of SPEC S:255-263).  The cell carries f_k, m_k, e_k of up to MAX_MAT materials
+// (material-major arrays, Slab::mf/mm/me); the EoS is the mixed closure (mix_eos_*,
+// sale_mesh.cuh), each material does its share of the cell's pdV work, and the remap
+// moves each material's mass, volume and energy from the donor cell.
+//
+// The cycle runs on the z-march kernels with a material axis (kernels_fused.cu
+// kf_force / kf_energy / kf_sigma_e / kf_energy_e and kernels_remap.cu kr_sweep, each
+// with NM materials as a template parameter) and the single-material node kernels
+// (kn_force_e, kn_update: they read sigma and the cell totals only).  This file holds
+// the launch sequences, the per-material flux + cell update (k_mat_flux), init / mass
+// re-summing, and the one-thread-per-cell Euler kernels k_mat_sigma / k_mat_energy /
+// k_mat_sweep (SALE_MAT_V0=1: the first cut of the path, kept as a cross-check).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -49,7 +55,6 @@ static void by_nmat(int nmat, F&& f)
     }
 }
 
-int launch_nodes_v0(const Slab& s, const Phys& p, int cur, int kb0, int kb1, Stream st);  // kernels_v0.cu
 
 // MM1-MM3: geometry at t^n, mixed EoS, q from the cell density and mixed sound speed;
 // sigma = 0.25 (P + q); q is kept for the materials' stresses (MM4).  Euler: launched
@@ -133,7 +138,6 @@ __global__ void k_mat_energy(Slab s, Phys p, int cur, int kc0, int kc1)
         const double dt = s.st->dt;
         double* e1 = EULER ? s.e1m : s.me[cur ^ 1];
 #pragma unroll
-    #pragma unroll
     for (int a = 0; a < NM; ++a) {
             const long long ca = c + a * st;
             const double fa = f[ca], ma = mk[ca], ea = s.me[cur][ca];
@@ -235,22 +239,28 @@ __global__ void k_mat_flux(Slab s, Phys p, int cur, int kr0, int kr1)
     double dmk[MAX_MAT] = {0.0}, dEk[MAX_MAT] = {0.0}, dphk[MAX_MAT] = {0.0};
     double dm = 0.0;
     D3 dP = d3(0.0, 0.0, 0.0);
+    // the six swept volumes first (independent loads), then every face's donor loads
+    double dVf[6];
+    long long Df[6];
+    bool inf[6];
+#pragma unroll
     for (int f = 0; f < 6; ++f) {
         const int ax = f >> 1;
         const bool plus = f & 1;
-        const bool inner = plus ? ijk[ax] < nmax[ax] - 1 : ijk[ax] > 0;
+        inf[f] = plus ? ijk[ax] < nmax[ax] - 1 : ijk[ax] > 0;
+        const long long nbr = inf[f] ? (plus ? c + sa[ax] : c - sa[ax]) : c;
+        dVf[f] = inf[f] ? s.dV[ax][plus ? nbr : c] : 0.0;  // the face is the -ax face of the upper cell
+        Df[f] = (dVf[f] > 0.0) == plus ? c : nbr;          // donor: the lower cell if the face moved toward +ax
+    }
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+        const bool inner = inf[f];
+        const double dV = dVf[f];
+        const long long D = Df[f];
         double mu = 0.0;
         D3 pi = d3(0.0, 0.0, 0.0);
-        double dV = 0.0;
-        long long D = c;
-        if (inner) {
-            const long long nbr = plus ? c + sa[ax] : c - sa[ax];
-            dV = s.dV[ax][plus ? nbr : c];  // the face is the -ax face of the upper cell
-            D = (dV > 0.0) == plus ? c : nbr; // donor: the lower cell if the face moved toward +ax
-        }
 #pragma unroll
-    #pragma unroll
-    for (int a = 0; a < NM; ++a) {
+        for (int a = 0; a < NM; ++a) {
             double mua = 0.0, pha = 0.0, epa = 0.0;
             if (inner) {
                 const long long Da = D + a * st;

@@ -275,21 +275,6 @@ __global__ void k0_remap_nodes(Slab s, Phys p, int cur)
 
 int launch_dt_candidate_gated(const Slab& s, const Phys& p, int cur, Stream st);
 
-// the node kernels on their own (kernels_mat.cu reuses them on the cell totals)
-int launch_nodes_v0(const Slab& s, const Phys& p, int cur, int kb0, int kb1, Stream st)
-{
-    cudaStream_t cs = (cudaStream_t)st;
-    if (p.rezone)
-        k0_nodes<true><<<grid_for(s.pn * (kb1 - kb0 + 1), 128), 128, 0, cs>>>(s, p, cur, kb0, kb1);
-    else
-        k0_nodes<false><<<grid_for(s.pn * (kb1 - kb0 + 1), 128), 128, 0, cs>>>(s, p, cur, kb0, kb1);
-    return 1;
-}
-int launch_remap_nodes_v0(const Slab& s, const Phys& p, int cur, Stream st)
-{
-    k0_remap_nodes<<<grid_for(s.pn * (s.k1 - s.k0 + 1), 128), 128, 0, (cudaStream_t)st>>>(s, p, cur);
-    return 1;
-}
 
 int launch_lagrange_v0(const Slab& s, const Phys& p, int cur, Stream st)
 {
