@@ -45,6 +45,8 @@ constexpr int PAD = FW + 1;
 
 inline int imin_h(int a, int b) { return a < b ? a : b; }
 inline int imax_h(int a, int b) { return a > b ? a : b; }
+__device__ __forceinline__ int imin_d(int a, int b) { return a < b ? a : b; }
+__device__ __forceinline__ int imax_d(int a, int b) { return a > b ? a : b; }
 
 struct FaceQ {
     D3 A, Xb, Ub;
@@ -271,7 +273,11 @@ struct ForceCTA {
                 double du = dmin(dmin(dx, dy), dz);
                 double q = q_of_du(rho, cs, du, p.c1, p.c2);
                 sig = 0.25 * (pf + q);
-                if (sig_col && kz >= za && kz >= kn0 && kz < kn1) {
+                // sigma of the cells between and next to the node planes [kn0, kn1] that
+                // this launch owns (clipped to the slab's cells): the full range writes
+                // [k0, k1); split ranges (launch_lagrange_fused_part) also write the cell
+                // just below kn0 / above kn1 (the same bits as the neighbouring launch)
+                if (sig_col && (kz >= za || za == kn0) && kz >= imax_d(kn0 - 1, s.k0) && kz < imin_d(kn1 + 1, s.k1)) {
                     s.sig[cb + (long long)kz * s.pc] = sig;
 #pragma unroll
                     for (int a = 0; a < NM; ++a)  // each material's stress (MM4)
@@ -1737,6 +1743,29 @@ int launch_kn_force_e(const Slab& s, const Phys& p, int cur, Stream st)
     const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
     kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, (cudaStream_t)st>>>(s, p, cur, kn0);
     return 1;
+}
+
+// Lagrange, boundary-first: part 0 = what the halo exchange sends
+// (node planes [k0, k0+g] and [k1-g, k1] with their cells [k0, k0+g) and [k1-g, k1)),
+// part 1 = the interior (node planes (k0+g, k1-g), cells [k0+g, k1-g)).  The two parts
+// are exactly the work of launch_lagrange_fused; the exchange can start after part 0.
+// A slab too thin to have an interior runs whole as part 0.
+int launch_lagrange_fused_part(const Slab& s, const Phys& p, int cur, int part, Stream st)
+{
+    static const Tune tune;
+    cudaStream_t cs = (cudaStream_t)st;
+    const int g = s.g, k0 = s.k0, k1 = s.k1;
+    if (k1 - k0 < 2 * g + 2) return part == 0 ? lagrange_fused<false>(s, p, cur, st) : 0;
+    if (part == 0) {
+        force_launch<false, NW_FORCE>(s, p, cur, k0, k0 + g, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, MINB>(s, p, cur, k0, k0 + g, tune.zc, cs);
+        force_launch<false, NW_FORCE>(s, p, cur, k1 - g, k1, tune.zc, cs);
+        energy_launch<false, NW_ENERGY, MINB>(s, p, cur, k1 - g, k1, tune.zc, cs);
+        return 4;
+    }
+    force_launch<false, NW_FORCE>(s, p, cur, k0 + g + 1, k1 - g - 1, tune.zc, cs);
+    energy_launch<false, NW_ENERGY, MINB>(s, p, cur, k0 + g, k1 - g, tune.zc, cs);
+    return 2;
 }
 
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)

@@ -147,6 +147,8 @@ int launch_energy_e_mat(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_sweep_mat(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st);
+// Lagrange fused in two parts: 0 = the planes the halo exchange sends, 1 = the interior
+int launch_lagrange_fused_part(const Slab& s, const Phys& p, int cur, int part, Stream st);
 int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st);
 bool fused_available();
 // Euler fused, split force: kf_sigma_e (sigma + the dt candidate of the cycle-start

@@ -75,3 +75,36 @@ def test_material_variant_bitwise(env):
     out = subprocess.run([sys.executable, "-c", MAT_SCRIPT % ROOT], env=e, capture_output=True, text=True,
                          timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+SLAB_SCRIPT = r"""
+import sys
+sys.path.insert(0, %r)
+import oracle as O
+from paper_2209_01983_b200.configs import sedov, LAGRANGE
+from paper_2209_01983_b200.sale import Sale
+from tests.helpers import apply_perturbation, compare
+for shape, slabs, seed in (((13, 7, 9), 2, 1), ((20, 9, 23), 3, 2), ((8, 8, 5), 5, 3), ((5, 6, 17), 4, None)):
+    cfg = sedov(shape, LAGRANGE)
+    g, o = Sale(cfg, impl="fused", local_slabs=slabs), O.Oracle(cfg)
+    if seed is not None:
+        apply_perturbation([g, o], cfg, seed, lagrange=True)
+    for chunk in (1, 7, 12):
+        rg, ro = g.step(chunk), o.step(chunk)
+        assert rg == ro, (shape, rg, ro)
+    compare(g, o)
+    assert g.clock() == o.clock()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"SALE_OVERLAP": "1"}, {"SALE_OVERLAP": "1", "SALE_GRAPHS": "0"}, {}])
+def test_lagrange_slabs_overlap_bitwise(env):
+    """Lagrange with emulated slabs: boundary planes first and the halo exchange on a
+    side stream overlapping the interior (SALE_OVERLAP=1, with and without graph replay),
+    and the default single-stream cycle; thin slabs (< 2g+2 planes) take the whole-slab
+    path."""
+    e = dict(os.environ, **env)
+    out = subprocess.run([sys.executable, "-c", SLAB_SCRIPT % ROOT], env=e, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
