@@ -64,7 +64,7 @@ extern "C" {
 #define SALE_IMPL_FUSED 0    /* fused z-marching kernels (default)                 */
 #define SALE_IMPL_V0 1       /* one kernel per step, for bring-up and cross-checks */
 
-/* field ids; node fields 0..6, cell fields 7..13 */
+/* field ids; node fields 0..6, cell fields 7..13 (and the material fields 16..27 below) */
 #define SALE_F_X 0
 #define SALE_F_Y 1
 #define SALE_F_Z 2
@@ -170,14 +170,17 @@ int32_t sale_sync(sale_ctx* c, int32_t* cycles_done);
  * fields cover cell planes [k0, k1); with local_slabs > 1 the whole mesh is
  * assembled (replicated planes are checked bit-equal, else SALE_EREPLICA).
  * count must equal the slab size: (nx+1)(ny+1)(k1-k0+1) or nx*ny*(k1-k0),
- * else SALE_EINVAL.  dst_on_device != 0: dst is device memory on this device.
+ * else SALE_EINVAL.  Material fields are cell fields (SALE_EINVAL for a material
+ * >= nmat); with nmat >= 1, E reads the mixture's (sum_k m_k e_k) / m and P, CS, Q
+ * the mixed closure.  dst_on_device != 0: dst is device memory on this device.
  * Layout of dst: x fastest, then y, then z. */
 int32_t sale_get_field(sale_ctx* c, int32_t field, double* dst, uint64_t count,
                        int32_t dst_on_device);
 
 /* Overwrite a state field (X, Y, Z in Lagrange mode only; UX, UY, UZ; MASS and E
- * with nmat = 0; SALE_F_MAT_* with nmat >= 1) on this rank's owned slab (same shape and layout as get_field).  Replicated
- * interface planes must be identical on both owners. */
+ * with nmat = 0; SALE_F_MAT_* with nmat >= 1, a MAT_M write re-summing MASS) on this
+ * rank's owned slab (same shape and layout as get_field).  Replicated interface
+ * planes must be identical on both owners. */
 int32_t sale_set_field(sale_ctx* c, int32_t field, const double* src, uint64_t count,
                        int32_t src_on_device);
 
