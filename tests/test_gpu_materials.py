@@ -118,3 +118,43 @@ def test_material_argument_checks():
         g.steinberg(dict(G0=1.0, GP=0.0, GT=0.0, Y0=1.0, Ymax=2.0, beta=0.0, n=1.0, cv=1.0, rho0=1.0, T0=0.0))
     g.set("MAT_M1", np.full(g.cell_shape, 0.25))
     assert np.array_equal(g.get("MASS"), g.get("MAT_M0") + 0.25)
+
+
+@pytest.mark.parametrize("name", ["C4", "C3"])
+def test_full_size_material_properties(name):
+    """At the benchmark sizes (the launch configuration materials_bench times): one
+    material through the material kernels equals the single-material kernels bit for
+    bit, and two copies of the gas splitting every cell (1/4, 3/4) conserve each
+    material's mass and track the single gas to round-off."""
+    from paper_2209_01983_b200.configs import config
+    from paper_2209_01983_b200.sale import Sale
+    cfg, _ = config(name)
+    cycles = 6
+    a = Sale(cfg, impl="fused")
+    assert a.step(cycles) == (0, cycles)
+    ref = {f: a.get(f) for f in ("UX", "MASS", "E", "P")}
+    a.close()
+    del a
+    torch.cuda.empty_cache()
+    b = Sale(dict(cfg, nmat=1, mat_gamma=[cfg["gamma"]]), impl="fused")
+    assert b.step(cycles) == (0, cycles)
+    for f in ("UX", "MASS", "P"):
+        assert np.array_equal(b.get(f), ref[f]), f
+    assert np.array_equal(b.get("MAT_E0"), ref["E"])
+    b.close()
+    del b
+    torch.cuda.empty_cache()
+    c = Sale(dict(cfg, nmat=2, mat_gamma=[cfg["gamma"]] * 2), impl="fused")
+    m, e = c.get("MAT_M0"), c.get("MAT_E0")
+    c.set("MAT_F0", np.full(c.cell_shape, 0.25))
+    c.set("MAT_F1", np.full(c.cell_shape, 0.75))
+    c.set("MAT_M0", 0.25 * m)
+    c.set("MAT_M1", 0.75 * m)
+    c.set("MAT_E1", e)
+    m0 = [float(np.sum(c.get(f"MAT_M{k}"), dtype=np.float64)) for k in (0, 1)]
+    assert c.step(cycles) == (0, cycles)
+    for k in (0, 1):
+        assert abs(float(np.sum(c.get(f"MAT_M{k}"), dtype=np.float64)) - m0[k]) <= 1e-12 * m0[k]
+    ux = c.get("UX")
+    assert np.max(np.abs(ux - ref["UX"])) <= 1e-10 * max(np.max(np.abs(ref["UX"])), 1e-300)
+    assert np.max(np.abs(c.get("MASS") - ref["MASS"])) <= 1e-12 * np.max(ref["MASS"])
