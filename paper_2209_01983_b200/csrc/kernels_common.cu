@@ -269,9 +269,9 @@ __global__ void k_dt_candidate(Slab s, Phys p, int cur, int gate)
             l2 = hex_min_edge2(N);
         }
         double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
-        if (p.nmat) {
+        if (s.nmat) {
             double pfk[MAX_MAT];
-            mix_eos(p, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, pf, cs, pfk);
+            mix_eos(s, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, pf, cs, pfk);
         } else {
             eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
         }
@@ -321,9 +321,9 @@ __global__ void k_derive_cells(Slab s, Phys p, int cur, int field)
     long long c = cidx(s, p, i, j, k);
     double V = vol_from_s(sv);
     double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
-    if (p.nmat) {
+    if (s.nmat) {
         double pfk[MAX_MAT];
-        mix_eos(p, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, pf, cs, pfk);
+        mix_eos(s, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, pf, cs, pfk);
     } else {
         eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
     }
@@ -332,7 +332,7 @@ __global__ void k_derive_cells(Slab s, Phys p, int cur, int field)
     case 8: {  // materials: the mixture's specific energy (sum_k m_k e_k) / m
         const double* mk = mat_m(s, p, cur);
         double sum = 0.0;
-        for (int a = 0; a < p.nmat; ++a) {
+        for (int a = 0; a < s.nmat; ++a) {
             const double t = mk[c + a * mat_stride(s)] * s.me[cur][c + a * mat_stride(s)];
             sum = (a == 0) ? t : sum + t;
         }

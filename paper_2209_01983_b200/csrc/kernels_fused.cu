@@ -45,8 +45,6 @@ constexpr int PAD = FW + 1;
 
 inline int imin_h(int a, int b) { return a < b ? a : b; }
 inline int imax_h(int a, int b) { return a > b ? a : b; }
-__device__ __forceinline__ int imin_d(int a, int b) { return a < b ? a : b; }
-__device__ __forceinline__ int imax_d(int a, int b) { return a > b ? a : b; }
 
 struct FaceQ {
     D3 A, Xb, Ub;
@@ -94,6 +92,7 @@ struct ForceCTA {
     const int cur;
     double* me;
     int i, j, za, zb, kn0, kn1;
+    int swlo, sw1;     // this CTA writes sigma of cell planes [swlo, sw1)
     long long nb, cb;  // node / cell index of (i,j) at local plane 0
     double dt;
     bool col_in, cellcol_in, node_out, sig_col;
@@ -103,8 +102,11 @@ struct ForceCTA {
     double pmf[NM > 0 ? NM : 1], pmm[NM > 0 ? NM : 1], pme[NM > 0 ? NM : 1];  // prefetch: materials
     FaceQ zprev;
 
+    // sigma is written for cell planes [sw0, sw1) (kf_force's launch range: [kn0, kn1);
+    // a split range also writes the cell just outside it, launch_lagrange_fused_part):
+    // each cell by the z-chunk that owns it, the first chunk also owning cell kn0-1
     __device__ __forceinline__ ForceCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kn0_, int kn1_,
-                                        int zchunk)
+                                        int zchunk, int sw0_, int sw1_)
         : s(s_), p(p_), cur(cur_)
     {
         const int ix = threadIdx.x, iy = threadIdx.y;
@@ -115,6 +117,8 @@ struct ForceCTA {
         kn1 = kn1_;
         za = kn0 + blockIdx.z * zchunk;
         zb = za + zchunk - 1 < kn1 ? za + zchunk - 1 : kn1;
+        swlo = (za == kn0) ? sw0_ : (za > sw0_ ? za : sw0_);
+        sw1 = sw1_;
         nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
         cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
         dt = s.st->dt;
@@ -255,7 +259,7 @@ struct ForceCTA {
                     double sv[6] = {fx.s, qx[oQ(0, 0)], fy.s, qy[oQ(1, 0)], zprev.s, zn.s};
                     double V = vol_from_s(sv), pr;
                     rho = ddiv(m, V);
-                    mix_eos_r<NM>(p, cmf, cmm, cme, V, rho, pr, pf, cs, pfk);
+                    mix_eos_r<NM>(s, cmf, cmm, cme, V, rho, pr, pf, cs, pfk);
                 } else if (kz >= s.k0 && kz < s.k1) {  // owned: rho, c from the EoS cache (c.5 pass, same state)
                     rho = crho;
                     cs = ccs;
@@ -273,11 +277,7 @@ struct ForceCTA {
                 double du = dmin(dmin(dx, dy), dz);
                 double q = q_of_du(rho, cs, du, p.c1, p.c2);
                 sig = 0.25 * (pf + q);
-                // sigma of the cells between and next to the node planes [kn0, kn1] that
-                // this launch owns (clipped to the slab's cells): the full range writes
-                // [k0, k1); split ranges (launch_lagrange_fused_part) also write the cell
-                // just below kn0 / above kn1 (the same bits as the neighbouring launch)
-                if (sig_col && (kz >= za || za == kn0) && kz >= imax_d(kn0 - 1, s.k0) && kz < imin_d(kn1 + 1, s.k1)) {
+                if (sig_col && kz >= swlo && kz < sw1) {
                     s.sig[cb + (long long)kz * s.pc] = sig;
 #pragma unroll
                     for (int a = 0; a < NM; ++a)  // each material's stress (MM4)
@@ -332,11 +332,11 @@ struct ForceCTA {
 
 template <bool EULER, int NW, int NM = 0>
 __global__ void __launch_bounds__(FW * NW, NW >= 12 ? 1 : MINB)
-    kf_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
+    kf_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk, int sw0, int sw1)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];
-    ForceCTA<EULER, NW, NM> c(s, p, cur, smem, kn0, kn1, zchunk);
+    ForceCTA<EULER, NW, NM> c(s, p, cur, smem, kn0, kn1, zchunk, sw0, sw1);
     c.run();
 }
 
@@ -710,7 +710,7 @@ struct SigmaEulerCTA {
         __syncthreads();
         if (out_cell && kz >= 0 && kz < p.nz) {
             double rho = ddiv(m, V), pr, pf, cs, pfk[MAX_MAT];
-            if constexpr (NM > 0) mix_eos_r<NM>(p, cmf, cmm, cme, V, rho, pr, pf, cs, pfk);
+            if constexpr (NM > 0) mix_eos_r<NM>(s, cmf, cmm, cme, V, rho, pr, pf, cs, pfk);
             else eos(p.gamma, rho, e, pr, pf, cs);
             double dx, dy, dz;
             if constexpr (DIAG) {
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int k
 // NM > 0 (Lagrange, multi-material cells): MM4 per material from the
 // stresses kf_force stored (Slab::sgm), and the dt candidate from the mixed closure
 template <bool EULER, int NW, int NM = 0>
-struct EnergyCTA {
+struct EnergyCTA : MatRegs<NM> {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
     __host__ __device__ static constexpr int oP(int par, int c) { return (par * 10 + c) * PL; }  // x^n(3) x'(3) ubar(3) |u'|^2
     __host__ __device__ static constexpr int oF(int xy, int c) { return 20 * PL + (xy * 4 + c) * PL; }  // A^n(3), s'
@@ -838,7 +838,6 @@ struct EnergyCTA {
     unsigned long long key;
     D3 fx, fu, fu1, fx1;  // prefetch registers
     double fm, fe, fs;
-    double gf[NM > 0 ? NM : 1], gm[NM > 0 ? NM : 1], ge[NM > 0 ? NM : 1], gs[NM > 0 ? NM : 1];  // materials
     D3 zA_prev;
     double zs_prev, ex_prev, ey_prev;
 
@@ -883,13 +882,15 @@ struct EnergyCTA {
             fm = mass_cur(s, p, cur)[c];
             fe = s.e[cur][c];
             fs = s.sig[c];
+            if constexpr (NM > 0) {
 #pragma unroll
-            for (int a = 0; a < NM; ++a) {
-                const long long ca = c + a * mat_stride(s);
-                gf[a] = mat_f(s, p, cur)[ca];
-                gm[a] = mat_m(s, p, cur)[ca];
-                ge[a] = s.me[cur][ca];
-                gs[a] = s.sgm[ca];
+                for (int a = 0; a < NM; ++a) {
+                    const long long ca = c + a * mat_stride(s);
+                    this->rf[a] = mat_f(s, p, cur)[ca];
+                    this->rm[a] = mat_m(s, p, cur)[ca];
+                    this->re[a] = s.me[cur][ca];
+                    this->rs[a] = s.sgm[ca];
+                }
             }
         }
     }
@@ -928,14 +929,7 @@ struct EnergyCTA {
         // ---- P1
         put<B1>();
         const double m = fm, e = fe, sig = fs;
-        double cf[NM > 0 ? NM : 1], cm[NM > 0 ? NM : 1], ce[NM > 0 ? NM : 1], csg[NM > 0 ? NM : 1];
-#pragma unroll
-        for (int a = 0; a < NM; ++a) {
-            cf[a] = gf[a];
-            cm[a] = gm[a];
-            ce[a] = ge[a];
-            csg[a] = gs[a];
-        }
+        const MatRegs<NM> cmat = *this;  // this plane's material operands (the prefetch moves on)
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
         // ---- P2: faces anchored at this column (A at t^n, s' at t^{n+1}); x' edges
@@ -984,7 +978,9 @@ struct EnergyCTA {
             if constexpr (NM > 0) {  // MM4: each present material's share of the work
 #pragma unroll
                 for (int a = 0; a < NM; ++a) {
-                    e1k[a] = (cf[a] > 0.0 && cm[a] > 0.0) ? ce[a] - ddiv(((csg[a] * W) * dt) * cf[a], cm[a]) : ce[a];
+                    e1k[a] = (cmat.rf[a] > 0.0 && cmat.rm[a] > 0.0)
+                                 ? cmat.re[a] - ddiv(((cmat.rs[a] * W) * dt) * cmat.rf[a], cmat.rm[a])
+                                 : cmat.re[a];
                     s.me[cur ^ 1][cc + a * mat_stride(s)] = e1k[a];
                 }
             }
@@ -998,7 +994,7 @@ struct EnergyCTA {
                     double rho = ddiv(m, V1), pr, pf, cs;
                     if constexpr (NM > 0) {
                         double pfk[MAX_MAT];
-                        mix_eos_r<NM>(p, cf, cm, e1k, V1, rho, pr, pf, cs, pfk);
+                        mix_eos_r<NM>(s, cmat.rf, cmat.rm, e1k, V1, rho, pr, pf, cs, pfk);
                     } else {
                         eos(p.gamma, rho, e1, pr, pf, cs);
                     }
@@ -1078,7 +1074,7 @@ __global__ void __launch_bounds__(FW * NW, MB)
 // NM > 0: multi-material cells: MM4 per material (e'_k into
 // Slab::e1m) from the stresses kf_sigma_e stored, instead of e'
 template <int NW, int NM = 0>
-struct EnergyEulerCTA {
+struct EnergyEulerCTA : MatRegs<NM> {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
     __host__ __device__ static constexpr int oP(int par, int c) { return (par * 6 + c) * PL; }        // x'(3) ubar(3)
     __host__ __device__ static constexpr int oF(int xy, int c) { return 12 * PL + (xy * 4 + c) * PL; }  // A^n(3), s'
@@ -1094,7 +1090,6 @@ struct EnergyEulerCTA {
     bool col_in, cell_col, own_col;
     D3 fu, fu1, fx1;  // prefetch registers (unconditional loads, selected at use)
     double fm, fe, fs;
-    double gf[NM > 0 ? NM : 1], gm[NM > 0 ? NM : 1], ge[NM > 0 ? NM : 1], gs[NM > 0 ? NM : 1];  // materials
     D3 fax, fay;      // prefetch: table A of the x- / y-face of cell plane k-1
     bool fnok, fcok;
     double zs_prev;
@@ -1141,13 +1136,15 @@ struct EnergyEulerCTA {
         fm = s.m[cur][c];
         fe = s.e[cur][c];
         fs = s.sig[c];
+        if constexpr (NM > 0) {
 #pragma unroll
-        for (int a = 0; a < NM; ++a) {
-            const long long ca = c + a * mat_stride(s);
-            gf[a] = s.mf[cur][ca];
-            gm[a] = s.mm[cur][ca];
-            ge[a] = s.me[cur][ca];
-            gs[a] = s.sgm[ca];
+            for (int a = 0; a < NM; ++a) {
+                const long long ca = c + a * mat_stride(s);
+                this->rf[a] = s.mf[cur][ca];
+                this->rm[a] = s.mm[cur][ca];
+                this->re[a] = s.me[cur][ca];
+                this->rs[a] = s.sgm[ca];
+            }
         }
         const long long tx = (long long)kl * p.ny + jc, ty = (long long)kl * p.nx + ic;
         fax = D3{s.TAx[0][tx], s.TAx[1][tx], s.TAx[2][tx]};
@@ -1177,14 +1174,7 @@ struct EnergyEulerCTA {
         constexpr int B1 = B0 ^ 1;
         put<B1>();
         const double m = fcok ? fm : 0.0, e = fcok ? fe : 0.0, sig = fcok ? fs : 0.0;
-        double cf[NM > 0 ? NM : 1], cm[NM > 0 ? NM : 1], ce[NM > 0 ? NM : 1], csg[NM > 0 ? NM : 1];
-#pragma unroll
-        for (int a = 0; a < NM; ++a) {
-            cf[a] = gf[a];
-            cm[a] = gm[a];
-            ce[a] = ge[a];
-            csg[a] = gs[a];
-        }
+        const MatRegs<NM> cmat = *this;  // this plane's material operands (the prefetch moves on)
         const D3 ax = fax, ay = fay;
         if (kz < zb) fetch(kz + 2, cur);
         __syncthreads();
@@ -1231,7 +1221,9 @@ struct EnergyEulerCTA {
 #pragma unroll
                 for (int a = 0; a < NM; ++a)
                     s.e1m[cc + a * mat_stride(s)] =
-                        (cf[a] > 0.0 && cm[a] > 0.0) ? ce[a] - ddiv(((csg[a] * W) * dt) * cf[a], cm[a]) : ce[a];
+                        (cmat.rf[a] > 0.0 && cmat.rm[a] > 0.0)
+                            ? cmat.re[a] - ddiv(((cmat.rs[a] * W) * dt) * cmat.rf[a], cmat.rm[a])
+                            : cmat.re[a];
             } else {
                 s.e1[cc] = e - ddiv((sig * W) * dt, m);
             }
@@ -1523,8 +1515,13 @@ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 }  // namespace
 
 template <bool EULER, int NW, int NM = 0>
-static void force_launch(const Slab& s, const Phys& p, int cur, int kn0, int kn1, int zc, cudaStream_t cs)
+static void force_launch(const Slab& s, const Phys& p, int cur, int kn0, int kn1, int zc, cudaStream_t cs,
+                         int sw0 = -1, int sw1 = -1)
 {
+    if (sw0 < 0) {  // sigma of the launch's own cell planes [kn0, kn1)
+        sw0 = kn0;
+        sw1 = kn1;
+    }
     const size_t sm = sizeof(double) * ForceCTA<EULER, NW, NM>::WORDS;
     static bool init = false;
     if (!init) {
@@ -1533,7 +1530,7 @@ static void force_launch(const Slab& s, const Phys& p, int cur, int kn0, int kn1
     }
     zc = zchunk_for((long long)cdiv(p.nx + 1, FW - 2) * cdiv(p.ny + 1, NW - 2), kn1 - kn0 + 1, zc);
     dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW - 2), cdiv(kn1 - kn0 + 1, zc));
-    kf_force<EULER, NW, NM><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc);
+    kf_force<EULER, NW, NM><<<grid, dim3(FW, NW), sm, cs>>>(s, p, cur, kn0, kn1, zc, sw0, sw1);
 }
 template <bool EULER, int NW, int MB, int NM = 0>
 static void energy_launch(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int zc, cudaStream_t cs)
@@ -1679,7 +1676,7 @@ int launch_sigma_e_mat(const Slab& s, const Phys& p, int cur, int gate, Stream s
     cudaStream_t cs = (cudaStream_t)st;
     auto go = [&](auto dg) {
         constexpr bool DG = decltype(dg)::value;
-        switch (p.nmat) {
+        switch (s.nmat) {
         case 1: sigma_e_launch<8, 2, DG, 1>(s, p, cur, sc0, sc1, tune.zc, gate, cs); break;
         case 2: sigma_e_launch<8, 2, DG, 2>(s, p, cur, sc0, sc1, tune.zc, gate, cs); break;
         case 3: sigma_e_launch<8, 2, DG, 3>(s, p, cur, sc0, sc1, tune.zc, gate, cs); break;
@@ -1700,7 +1697,7 @@ int launch_force_mat(const Slab& s, const Phys& p, int cur, Stream st)
     cudaStream_t cs = (cudaStream_t)st;
     // (energy: two 8-warp CTAs per SM at 128 registers for 1-2 materials, measured
     // faster despite the spill; one CTA for 3-4, whose larger spill made it slower)
-    switch (p.nmat) {
+    switch (s.nmat) {
     case 1:
         force_launch<false, NW_FORCE, 1>(s, p, cur, s.k0, s.k1, tune.zc, cs);
         energy_launch<false, NW_ENERGY, 2, 1>(s, p, cur, s.k0, s.k1, tune.zc, cs);
@@ -1728,7 +1725,7 @@ int launch_energy_e_mat(const Slab& s, const Phys& p, int cur, Stream st)
     static const Tune tune;
     const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
     cudaStream_t cs = (cudaStream_t)st;
-    switch (p.nmat) {
+    switch (s.nmat) {
     case 1: energy_e_launch<8, 2, 1>(s, p, cur, kn0, kn1, tune.zc, cs); break;
     case 2: energy_e_launch<8, 2, 2>(s, p, cur, kn0, kn1, tune.zc, cs); break;
     case 3: energy_e_launch<8, 2, 3>(s, p, cur, kn0, kn1, tune.zc, cs); break;
@@ -1756,14 +1753,16 @@ int launch_lagrange_fused_part(const Slab& s, const Phys& p, int cur, int part, 
     cudaStream_t cs = (cudaStream_t)st;
     const int g = s.g, k0 = s.k0, k1 = s.k1;
     if (k1 - k0 < 2 * g + 2) return part == 0 ? lagrange_fused<false>(s, p, cur, st) : 0;
+    // sigma write ranges: the cell next to each split is written by both neighbouring
+    // launches (same bits, stream order), so every energy range finds its sigma
     if (part == 0) {
-        force_launch<false, NW_FORCE>(s, p, cur, k0, k0 + g, tune.zc, cs);
+        force_launch<false, NW_FORCE>(s, p, cur, k0, k0 + g, tune.zc, cs, k0, k0 + g + 1);
         energy_launch<false, NW_ENERGY, MINB>(s, p, cur, k0, k0 + g, tune.zc, cs);
-        force_launch<false, NW_FORCE>(s, p, cur, k1 - g, k1, tune.zc, cs);
+        force_launch<false, NW_FORCE>(s, p, cur, k1 - g, k1, tune.zc, cs, k1 - g - 1, k1);
         energy_launch<false, NW_ENERGY, MINB>(s, p, cur, k1 - g, k1, tune.zc, cs);
         return 4;
     }
-    force_launch<false, NW_FORCE>(s, p, cur, k0 + g + 1, k1 - g - 1, tune.zc, cs);
+    force_launch<false, NW_FORCE>(s, p, cur, k0 + g + 1, k1 - g - 1, tune.zc, cs, k0 + g, k1 - g);
     energy_launch<false, NW_ENERGY, MINB>(s, p, cur, k0 + g, k1 - g, tune.zc, cs);
     return 2;
 }

@@ -79,7 +79,7 @@ __global__ void k_mat_sigma(Slab s, Phys p, int cur, int ka0, int ka1, int gate)
         long long c = cidx(s, p, i, j, k);
         double V = vol_from_s(sv);
         double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, P, cs;
-        mix_eos_t<NM>(p, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, P, cs, pf);
+        mix_eos_t<NM>(s, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, P, cs, pf);
         double q = hex_q(Xb, U, rho, cs, p.c1, p.c2);
         s.sig[c] = 0.25 * (P + q);
 #pragma unroll
@@ -152,7 +152,7 @@ __global__ void k_mat_energy(Slab s, Phys p, int cur, int kc0, int kc1)
             s.V1[c] = V1;
         } else if (owned) {
             double pr, P, cs;
-            mix_eos_t<NM>(p, f, mk, s.me[cur ^ 1], c, st, V1, ddiv(m, V1), pr, P, cs, pf);
+            mix_eos_t<NM>(s, f, mk, s.me[cur ^ 1], c, st, V1, ddiv(m, V1), pr, P, cs, pf);
             key = dt_key(dt_cell(p.cfl, hex_min_edge2(N1), hex_max_speed2(U1), cs));
         }
     }
@@ -313,7 +313,7 @@ __global__ void k_mat_init(Slab s, Phys p)
     const int k = s.kb + (int)(c / s.pc);
     const bool in = k >= 0 && k < p.nz;
     const long long st = mat_stride(s);
-    for (int a = 0; a < p.nmat; ++a) {
+    for (int a = 0; a < s.nmat; ++a) {
         const long long ca = c + a * st;
         s.mf[0][ca] = (in && a == 0) ? 1.0 : 0.0;
         s.mm[0][ca] = (in && a == 0) ? s.m[0][c] : 0.0;
@@ -329,7 +329,7 @@ __global__ void k_mat_total(Slab s, Phys p, int cur)
     const double* mk = mat_m(s, p, cur);
     const long long st = mat_stride(s);
     double m = 0.0;
-    for (int a = 0; a < p.nmat; ++a) m = (a == 0) ? mk[c] : m + mk[c + a * st];
+    for (int a = 0; a < s.nmat; ++a) m = (a == 0) ? mk[c] : m + mk[c + a * st];
     (p.rezone ? s.m[cur] : s.m[0])[c] = m;
 }
 
@@ -347,7 +347,7 @@ int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st)
     int kb0 = s.k0 - 2 > 0 ? s.k0 - 2 : 0, kb1 = s.k1 + 2 < p.nz ? s.k1 + 2 : p.nz;
     launch_kn_force_e(s, p, cur, st);
     if (!mat_v0()) return 1 + launch_energy_e_mat(s, p, cur, st);
-    by_nmat(p.nmat, [&](auto nm) {
+    by_nmat(s.nmat, [&](auto nm) {
         constexpr int NM = decltype(nm)::value;
         k_mat_energy<true, NM><<<grid_for(s.pc * (kb1 - kb0), bs), bs, 0, cs>>>(s, p, cur, kb0, kb1);
     });
@@ -360,7 +360,7 @@ int launch_mat_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st)
 {
     if (!mat_v0()) return launch_sigma_e_mat(s, p, cur, gate, st);
     int ka0 = s.k0 - 3 > 0 ? s.k0 - 3 : 0, ka1 = s.k1 + 3 < p.nz ? s.k1 + 3 : p.nz;
-    by_nmat(p.nmat, [&](auto nm) {
+    by_nmat(s.nmat, [&](auto nm) {
         constexpr int NM = decltype(nm)::value;
         k_mat_sigma<true, NM><<<grid_for(s.pc * (ka1 - ka0), 128), 128, 0, (cudaStream_t)st>>>(s, p, cur, ka0, ka1,
                                                                                                gate);
@@ -379,7 +379,7 @@ int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st)
     int ks0 = kr0 - 1 > 0 ? kr0 - 1 : 0, ks1 = kr1 + 1 < p.nz ? kr1 + 1 : p.nz;
     const bool v0 = mat_v0();
     if (!v0) launch_sweep_mat(s, p, cur, st);
-    by_nmat(p.nmat, [&](auto nm) {
+    by_nmat(s.nmat, [&](auto nm) {
         constexpr int NM = decltype(nm)::value;
         if (v0) k_mat_sweep<NM><<<grid_for(s.pc * (ks1 - ks0), bs), bs, 0, cs>>>(s, p, cur, ks0, ks1);
         k_mat_flux<NM><<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);

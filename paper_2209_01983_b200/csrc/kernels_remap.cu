@@ -1267,7 +1267,7 @@ int launch_sweep_mat(const Slab& s, const Phys& p, int cur, Stream st)
         dim3 grid(cdivr(p.nx, RW - 1), cdivr(p.ny, 8 - 1), cdivr(t1 - t0 + 1, zc));
         kern<<<grid, dim3(RW, 8), sizeof(double) * words, (cudaStream_t)st>>>(s, p, cur, kr0, kr1, zc);
     };
-    switch (p.nmat) {
+    switch (s.nmat) {
     case 1: sweep(kr_sweep<8, 2, 1>); break;
     case 2: sweep(kr_sweep<8, 2, 2>); break;
     case 3: sweep(kr_sweep<8, 2, 3>); break;

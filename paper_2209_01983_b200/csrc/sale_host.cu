@@ -231,6 +231,8 @@ void layout_slabs(const sale_params* p, std::vector<Slab>& out)
         s.nzn = s.nzc + 1;
         s.pn = (long long)(p->nx + 1) * (p->ny + 1);
         s.pc = (long long)p->nx * p->ny;
+        s.nmat = p->nmat;
+        for (int k = 0; k < sale::MAX_MAT; ++k) s.mg[k] = k < p->nmat ? p->mat_gamma[k] : 0.0;
         out.push_back(s);
     }
 }
@@ -859,8 +861,6 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
     ph.rho0 = p->rho0; ph.e_bg = p->e_background; ph.e_dep = p->e_deposit;
     ph.nx = p->nx; ph.ny = p->ny; ph.nz = p->nz;
     ph.reflect = p->reflect_mask; ph.rezone = p->rezone;
-    ph.nmat = p->nmat;
-    for (int k = 0; k < sale::MAX_MAT; ++k) ph.mg[k] = k < p->nmat ? p->mat_gamma[k] : 0.0;
     layout_slabs(p, c->slabs);
     char* base = static_cast<char*>(p->workspace);
     c->dstate = reinterpret_cast<DevState*>(base);
@@ -897,7 +897,7 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
         if (rc) break;
         c->launches += sale::launch_init_tables(s, ph, (sale::Stream)c->stream);
         c->launches += sale::launch_sedov_init(s, ph, (sale::Stream)c->stream);
-        if (ph.nmat) c->launches += sale::launch_mat_init(s, ph, (sale::Stream)c->stream);
+        if (s.nmat) c->launches += sale::launch_mat_init(s, ph, (sale::Stream)c->stream);
         if (ph.rezone) c->launches += sale::launch_target_tables(s, ph, (sale::Stream)c->stream);
         rc = launch_check(c);
     }

@@ -21,8 +21,6 @@ struct Phys {
                               // a corner vector (c.2) is exactly (+-Ax.x, +-Ay.y, +-Az.z)
     int diag_jumps;           // Euler: every axis-jump separation d of the target mesh lies on its
                               // axis (off-axis components exactly zero; checked at create)
-    int nmat;                 // 0: single material; 1..MAX_MAT: material axis
-    double mg[MAX_MAT];       // gamma of each material
 };
 
 // Device-resident clock and status (one per context; all local slabs share it).
@@ -97,6 +95,9 @@ struct Slab {
     double* sgm;              // scratch: each material's stress 0.25 (pf_k + q) at the cycle start (MM4)
     double* e1m;              // Euler scratch: e'_k
     double* rDm;              // Euler scratch: donor material density m_k / V' of each cell (k_mat_sweep)
+    double mg[MAX_MAT];       // gamma of each material (here rather than in Phys: growing Phys
+    int nmat;                 //   perturbed the single-material kernels' code generation)
+                              // nmat: 0 single material; 1..MAX_MAT the material axis (§10d)
     DevState* st;
 };
 

@@ -89,6 +89,17 @@ __device__ __forceinline__ const double* mat_m(const Slab& s, const Phys& p, int
     return p.rezone ? s.mm[b] : s.mm[0];
 }
 
+// per-cell material operands a z-march kernel prefetches into registers: volume
+// fraction, mass, specific energy, stress (NM = 0: an empty base, so the single-material
+// instantiations keep their original layout and code)
+template <int NM>
+struct MatRegs {
+    double rf[NM], rm[NM], re[NM], rs[NM];
+};
+template <>
+struct MatRegs<0> {
+};
+
 // MM1: the mixed-cell closure of cell c (material k at c + k*stride) at volume V and
 // cell density rho: each present material (f_k > 0) at rho_k = m_k / (f_k V) through
 // the c.3 step 1 EoS with its own gamma; pr = sum f_k p_k, P = sum f_k pf_k,
@@ -97,21 +108,21 @@ __device__ __forceinline__ const double* mat_m(const Slab& s, const Phys& p, int
 // bits (1.0 * a = a).  NM > 0: the material count as a compile-time constant (the
 // loop unrolls, pf stays in registers); NM = 0: p.nmat.
 template <int NM>
-__device__ __forceinline__ void mix_eos_r(const Phys& p, const double* f, const double* mm, const double* e, double V,
+__device__ __forceinline__ void mix_eos_r(const Slab& s, const double* f, const double* mm, const double* e, double V,
                                           double rho, double& pr, double& P, double& cs, double pf[MAX_MAT])
 {
     double ps = 0.0, Ps = 0.0, G = 0.0;
     bool first = true;
 #pragma unroll
-    for (int k = 0; k < (NM ? NM : p.nmat); ++k) {
+    for (int k = 0; k < (NM ? NM : s.nmat); ++k) {
         pf[k] = 0.0;
         const double fk = f[k];
         if (!(fk > 0.0)) continue;
         const double rk = ddiv(mm[k], fk * V);
-        const double pk = ((p.mg[k] - 1.0) * rk) * e[k];
+        const double pk = ((s.mg[k] - 1.0) * rk) * e[k];
         const double pfk = (pk > 0.0) ? pk : 0.0;
         pf[k] = pfk;
-        const double a = fk * pk, b = fk * pfk, g = fk * (p.mg[k] * pfk);
+        const double a = fk * pk, b = fk * pfk, g = fk * (s.mg[k] * pfk);
         if (first) {
             ps = a;
             Ps = b;
@@ -129,24 +140,24 @@ __device__ __forceinline__ void mix_eos_r(const Phys& p, const double* f, const 
 }
 // the same from the material arrays of cell c (material k at c + k*stride)
 template <int NM>
-__device__ __forceinline__ void mix_eos_t(const Phys& p, const double* f, const double* mm, const double* e,
+__device__ __forceinline__ void mix_eos_t(const Slab& s, const double* f, const double* mm, const double* e,
                                           long long c, long long stride, double V, double rho, double& pr,
                                           double& P, double& cs, double pf[MAX_MAT])
 {
     double fr[MAX_MAT], mr[MAX_MAT], er[MAX_MAT];
 #pragma unroll
-    for (int k = 0; k < (NM ? NM : p.nmat); ++k) {
+    for (int k = 0; k < (NM ? NM : s.nmat); ++k) {
         fr[k] = f[c + k * stride];
         mr[k] = mm[c + k * stride];
         er[k] = e[c + k * stride];
     }
-    mix_eos_r<NM>(p, fr, mr, er, V, rho, pr, P, cs, pf);
+    mix_eos_r<NM>(s, fr, mr, er, V, rho, pr, P, cs, pf);
 }
-__device__ __forceinline__ void mix_eos(const Phys& p, const double* f, const double* mm, const double* e,
+__device__ __forceinline__ void mix_eos(const Slab& s, const double* f, const double* mm, const double* e,
                                         long long c, long long stride, double V, double rho, double& pr,
                                         double& P, double& cs, double pf[MAX_MAT])
 {
-    mix_eos_t<0>(p, f, mm, e, c, stride, V, rho, pr, P, cs, pf);
+    mix_eos_t<0>(s, f, mm, e, c, stride, V, rho, pr, P, cs, pf);
 }
 
 // host: z-chunk length of a z-marching grid.  Large meshes use zc0 planes per CTA;
