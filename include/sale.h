@@ -252,9 +252,12 @@ typedef struct sale_steinberg_params {
 /* eps_p: plastic strain per owned cell, or NULL for zero; shear, yield: outputs.
  * All three are DEVICE pointers with the layout and count of get_field's cell
  * fields (count = owned cells; emulated slabs concatenated in plane order).
- * Asynchronous on the context's stream (synchronises first with pending cycles);
- * the call launches one kernel per slab.  SALE_EINVAL on NULL / count mismatch
- * or nmat >= 1 (single-material only), SALE_EPOISONED on a poisoned context. */
+ * With a material axis (nmat >= 1) sp points to nmat parameter sets and shear /
+ * yield hold nmat * count values, material m's at offset m * count (Fig. 6b's
+ * shear(m,i,j,k): every material's constants applied to the cell's rho, p and
+ * mixture energy, as get_field RHO / P / E).  Asynchronous on the context's stream
+ * (synchronises first with pending cycles); the call launches one kernel per slab.
+ * SALE_EINVAL on NULL / count mismatch, SALE_EPOISONED on a poisoned context. */
 int32_t sale_steinberg(sale_ctx* c, const sale_steinberg_params* sp, const double* eps_p, double* shear,
                        double* yield, uint64_t count);
 

@@ -199,13 +199,20 @@ class Oracle:
         rc = self._L.oracle_next_dt(self._h, C.byref(dt))
         return rc, dt.value
 
-    def steinberg(self, params: dict, eps_p=None):
-        """Shear modulus and yield stress of every cell (Fig. 6b; oracle.h)."""
-        sh = np.empty(self.cell_shape)
-        y = np.empty(self.cell_shape)
+    def steinberg(self, params, eps_p=None):
+        """Shear modulus and yield stress of every cell (Fig. 6b; oracle.h).  params:
+        one dict, or with a material axis a list of nmat dicts (outputs then gain a
+        leading material axis)."""
+        plist = list(params) if isinstance(params, (list, tuple)) else [params]
+        if len(plist) != max(int(self.cfg.get("nmat", 0)), 1):
+            raise ValueError("oracle_steinberg needs one parameter set per material")
+        shape = ((len(plist),) + self.cell_shape) if isinstance(params, (list, tuple)) else self.cell_shape
+        arr = (OracleSteinberg * len(plist))(*[steinberg_params(d) for d in plist])
+        sh = np.empty(shape)
+        y = np.empty(shape)
         e = None if eps_p is None else np.ascontiguousarray(eps_p, dtype=np.float64)
-        rc = self._L.oracle_steinberg(self._h, C.byref(steinberg_params(params)),
-                                      None if e is None else e.ctypes.data, _dp(sh), _dp(y), sh.size)
+        rc = self._L.oracle_steinberg(self._h, C.cast(arr, C.POINTER(OracleSteinberg)),
+                                      None if e is None else e.ctypes.data, _dp(sh), _dp(y), sh.size // len(plist))
         if rc != OK:
             raise ValueError(f"oracle_steinberg rc={rc}")
         return sh, y

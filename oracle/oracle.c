@@ -1192,20 +1192,28 @@ void oracle_steinberg_point(const oracle_steinberg_params* sp, double p, double 
 int32_t oracle_steinberg(oracle_ctx* c, const oracle_steinberg_params* sp, const double* eps_p, double* shear,
                          double* yield, uint64_t count)
 {
-    if (!c || !sp || !shear || !yield || count != (uint64_t)c->ncell || c->nmat > 0) return ORACLE_EINVAL;
+    if (!c || !sp || !shear || !yield || count != (uint64_t)c->ncell) return ORACLE_EINVAL;
     double* rho = (double*)malloc(sizeof(double) * (size_t)c->ncell);
     double* pr = (double*)malloc(sizeof(double) * (size_t)c->ncell);
-    if (!rho || !pr) {
+    double* e = (double*)malloc(sizeof(double) * (size_t)c->ncell);
+    if (!rho || !pr || !e) {
         free(rho);
         free(pr);
+        free(e);
         return ORACLE_EINVAL;
     }
     int32_t rc = oracle_get_field(c, ORACLE_F_RHO, rho, count);
     if (!rc) rc = oracle_get_field(c, ORACLE_F_P, pr, count);
-    for (int64_t K = 0; !rc && K < c->ncell; ++K)
-        oracle_steinberg_point(sp, pr[K], rho[K], c->e[K], eps_p ? eps_p[K] : 0.0, &shear[K], &yield[K]);
+    if (!rc) rc = oracle_get_field(c, ORACLE_F_E, e, count);
+    /* Fig. 6b: do m = 1, nmats -- every material's constants on the cell quantities */
+    const int nm = c->nmat > 0 ? c->nmat : 1;
+    for (int m = 0; !rc && m < nm; ++m)
+        for (int64_t K = 0; K < c->ncell; ++K)
+            oracle_steinberg_point(&sp[m], pr[K], rho[K], e[K], eps_p ? eps_p[K] : 0.0,
+                                   &shear[(int64_t)m * c->ncell + K], &yield[(int64_t)m * c->ncell + K]);
     free(rho);
     free(pr);
+    free(e);
     return rc;
 }
 

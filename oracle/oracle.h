@@ -135,7 +135,10 @@ typedef struct oracle_steinberg_params {
 void oracle_steinberg_point(const oracle_steinberg_params* sp, double p, double rho, double e, double eps_p,
                             double* shear, double* yield);
 /* every cell of the current state; eps_p: cell array or NULL (all zero); shear,
- * yield: cell arrays (count = nx*ny*nz). */
+ * yield: cell arrays (count = nx*ny*nz).  With nmat >= 1 materials: sp holds nmat
+ * parameter sets and shear / yield nmat * count values, material m's at m * count
+ * (Fig. 6b's loop over materials; rho, p and the mixture energy of the cell as
+ * oracle_get_field RHO / P / E). */
 int32_t oracle_steinberg(oracle_ctx* c, const oracle_steinberg_params* sp, const double* eps_p, double* shear,
                          double* yield, uint64_t count);
 

@@ -398,11 +398,13 @@ int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st)
 }
 
 // ------------------------------------------------ Steinberg (Fig. 6b)
-// One thread per owned cell: rho = m / V and p exactly as get_field's RHO / P, then
-// the paper's shear / yield loop body (association as written there).
-template <bool EULER>
-__global__ void __launch_bounds__(256) k_steinberg(Slab s, Phys p, int cur, SteinbergP sp, const double* eps,
-                                                   double* sh, double* y)
+// One thread per owned cell: rho = m / V, p and e exactly as get_field's RHO / P / E,
+// then the paper's shear / yield loop body (association as written there) once per
+// material with that material's constants (Fig. 6b's "do m=1, nmats"; one set when
+// the context has no material axis).  Material m's outputs at sh / y + m * mstride.
+template <bool EULER, int NM>  // NM: materials (0: no material axis, one parameter set)
+__global__ void __launch_bounds__(256) k_steinberg(Slab s, Phys p, int cur, SteinbergSet set, const double* eps,
+                                                   double* sh, double* y, long long mstride)
 {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long total = s.pc * (s.k1 - s.k0);
@@ -421,24 +423,54 @@ __global__ void __launch_bounds__(256) k_steinberg(Slab s, Phys p, int cur, Stei
         hex_faces(N, A, Xb, sv);
         V = vol_from_s(sv);
     }
-    const double e = s.e[cur][c];
-    double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
-    eos(p.gamma, rho, e, pr, pf, cs);
-    const double eta = sp.rho0 / rho;
-    const double T = e / sp.cv;
-    // eta^(1/3): cbrt (within an ulp of the paper's pow(eta, 1/3), at a fraction of its cost)
-    const double G = (sp.G0 + (sp.GP * pr) * cbrt(eta)) + sp.GT * (T - sp.T0);
-    const double h = sp.Y0 * pow(1.0 + sp.beta * (eps ? eps[t] : 0.0), sp.n);
-    sh[t] = G;
-    y[t] = ((h < sp.Ymax) ? h : sp.Ymax) * (G / sp.G0);
+    const double m = mass_cur(s, p, cur)[c];
+    double rho = ddiv(m, V), pr, pf, cs, e;
+    if constexpr (NM > 0) {  // the mixed closure and the mixture's specific energy (as get_field P / E)
+        double pfk[MAX_MAT];
+        mix_eos_t<NM>(s, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, pf, cs, pfk);
+        const double* mk = mat_m(s, p, cur);
+        double sum = 0.0;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            const double tt = mk[c + a * mat_stride(s)] * s.me[cur][c + a * mat_stride(s)];
+            sum = (a == 0) ? tt : sum + tt;
+        }
+        e = ddiv(sum, m);
+    } else {
+        e = s.e[cur][c];
+        eos(p.gamma, rho, e, pr, pf, cs);
+    }
+    const double ep = eps ? eps[t] : 0.0;
+#pragma unroll
+    for (int a = 0; a < (NM > 0 ? NM : 1); ++a) {
+        const SteinbergP& sp = set.m[a];
+        const double eta = sp.rho0 / rho;
+        const double T = e / sp.cv;
+        // eta^(1/3): cbrt (within an ulp of the paper's pow(eta, 1/3), at a fraction of its cost)
+        const double G = (sp.G0 + (sp.GP * pr) * cbrt(eta)) + sp.GT * (T - sp.T0);
+        const double h = sp.Y0 * pow(1.0 + sp.beta * ep, sp.n);
+        sh[t + a * mstride] = G;
+        y[t + a * mstride] = ((h < sp.Ymax) ? h : sp.Ymax) * (G / sp.G0);
+    }
 }
 
-int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergP& sp, const double* eps, double* sh,
-                     double* y, Stream st)
+int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& set, const double* eps, double* sh,
+                     double* y, long long mstride, Stream st)
 {
     const long long n = s.pc * (s.k1 - s.k0);
-    if (p.rezone) k_steinberg<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, sp, eps, sh, y);
-    else k_steinberg<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, sp, eps, sh, y);
+    auto go = [&](auto kern) { kern<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, set, eps, sh, y, mstride); };
+    switch (s.nmat * 2 + (p.rezone ? 1 : 0)) {
+    case 0: go(k_steinberg<false, 0>); break;
+    case 1: go(k_steinberg<true, 0>); break;
+    case 2: go(k_steinberg<false, 1>); break;
+    case 3: go(k_steinberg<true, 1>); break;
+    case 4: go(k_steinberg<false, 2>); break;
+    case 5: go(k_steinberg<true, 2>); break;
+    case 6: go(k_steinberg<false, 3>); break;
+    case 7: go(k_steinberg<true, 3>); break;
+    case 8: go(k_steinberg<false, 4>); break;
+    default: go(k_steinberg<true, 4>); break;
+    }
     return 1;
 }
 

@@ -947,17 +947,22 @@ int32_t sale_steinberg(sale_ctx* c, const sale_steinberg_params* sp, const doubl
                        double* yield, uint64_t count)
 {
     if (!c || !sp || !shear || !yield) return SALE_EINVAL;
-    if (count != expected_count(c, SALE_F_MASS) || c->prm.nmat > 0) return SALE_EINVAL;
+    if (count != expected_count(c, SALE_F_MASS)) return SALE_EINVAL;
     if (c->poisoned) return SALE_EPOISONED;
     DeviceGuard guard(c->prm.device);
     int rc = sync_state(c, nullptr);
     if (rc) return rc;
-    const sale::SteinbergP P{sp->G0, sp->GP, sp->GT, sp->Y0, sp->Ymax, sp->beta, sp->n, sp->cv, sp->rho0, sp->T0};
+    sale::SteinbergSet set{};
+    set.n = c->prm.nmat > 0 ? c->prm.nmat : 1;
+    for (int a = 0; a < set.n; ++a) {
+        const sale_steinberg_params& q = sp[a];
+        set.m[a] = sale::SteinbergP{q.G0, q.GP, q.GT, q.Y0, q.Ymax, q.beta, q.n, q.cv, q.rho0, q.T0};
+    }
     const size_t plane = (size_t)c->slabs[0].pc;
     for (auto& s : c->slabs) {
         const size_t off = c->prm.local_slabs > 1 ? (size_t)s.k0 * plane : 0;
-        c->launches += sale::launch_steinberg(s, c->phys, c->cur, P, eps_p ? eps_p + off : nullptr, shear + off,
-                                              yield + off, (sale::Stream)c->stream);
+        c->launches += sale::launch_steinberg(s, c->phys, c->cur, set, eps_p ? eps_p + off : nullptr, shear + off,
+                                              yield + off, (long long)count, (sale::Stream)c->stream);
     }
     return launch_check(c);
 }

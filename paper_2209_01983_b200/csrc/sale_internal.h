@@ -105,6 +105,11 @@ struct Slab {
 struct SteinbergP {
     double G0, GP, GT, Y0, Ymax, beta, n, cv, rho0, T0;
 };
+// one parameter set per material (n = nmat, or 1 without a material axis)
+struct SteinbergSet {
+    SteinbergP m[MAX_MAT];
+    int n;
+};
 
 // status codes mirrored from include/sale.h (kept in sync by a static_assert in host code)
 enum { S_OK = 0, S_EINVAL = 1, S_ENOMEM = 2, S_ECUDA = 3, S_ENCCL = 4, S_ETANGLED = 5,
@@ -127,8 +132,8 @@ int launch_reset_good(DevState* d, Stream st);
 int launch_dt_candidate(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st);
 // Steinberg shear / yield of the owned cells (include/sale.h); outputs at sh / y (device)
-int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergP& sp, const double* eps, double* sh,
-                     double* y, Stream st);
+int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& set, const double* eps, double* sh,
+                     double* y, long long mstride, Stream st);
 // one cycle on one slab, reading buffers [cur], writing [cur^1]:
 // the Lagrangian phase (S1-S7; Lagrange mode also the next dt candidate), then
 // in Euler mode the remap (R1-R5 + next dt candidate)

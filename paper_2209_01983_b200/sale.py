@@ -254,21 +254,28 @@ class Sale:
             raise SaleError(rc, f"sale_get_field({field}): " + self.last_error())
         return arr
 
-    def steinberg(self, params: dict, eps_p=None, out=None):
+    def steinberg(self, params, eps_p=None, out=None):
         """Steinberg shear modulus and yield stress of the owned cells (Fig. 6b;
-        include/sale.h sale_steinberg).  eps_p: plastic strain (array of the cell
-        shape) or None.  Returns (shear, yield) as float64 device tensors (or fills
-        the pair `out`)."""
+        include/sale.h sale_steinberg).  params: one dict, or with a material axis a
+        list of nmat dicts (outputs then gain a leading material axis).  eps_p: plastic
+        strain (array of the cell shape) or None.  Returns (shear, yield) as float64
+        device tensors (or fills the pair `out`)."""
         import torch
-        sp = SaleSteinberg(*[float(params[n]) for n, _ in SaleSteinberg._fields_])
-        sh, y = out if out is not None else (torch.empty(self.cell_shape, dtype=torch.float64, device=self.torch_device),
-                                             torch.empty(self.cell_shape, dtype=torch.float64, device=self.torch_device))
+        plist = list(params) if isinstance(params, (list, tuple)) else [params]
+        if len(plist) != max(int(self.cfg.get("nmat", 0)), 1):
+            raise ValueError("sale_steinberg needs one parameter set per material")
+        arr = (SaleSteinberg * len(plist))(*[SaleSteinberg(*[float(d[n]) for n, _ in SaleSteinberg._fields_])
+                                             for d in plist])
+        shape = ((len(plist),) + self.cell_shape) if isinstance(params, (list, tuple)) else self.cell_shape
+        sh, y = out if out is not None else (torch.empty(shape, dtype=torch.float64, device=self.torch_device),
+                                             torch.empty(shape, dtype=torch.float64, device=self.torch_device))
+        sp = arr
         ep = None
         if eps_p is not None:
             ep = torch.as_tensor(np.ascontiguousarray(eps_p, dtype=np.float64)).to(self.torch_device) \
                 if not hasattr(eps_p, "data_ptr") else eps_p
-        rc = self._L.sale_steinberg(self._h, C.byref(sp), None if ep is None else ep.data_ptr(), sh.data_ptr(),
-                                    y.data_ptr(), sh.numel())
+        rc = self._L.sale_steinberg(self._h, C.cast(sp, C.POINTER(SaleSteinberg)), None if ep is None else ep.data_ptr(),
+                                    sh.data_ptr(), y.data_ptr(), sh.numel() // len(plist))
         if rc:
             raise SaleError(rc, "sale_steinberg: " + self.last_error())
         return sh, y

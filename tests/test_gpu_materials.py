@@ -114,7 +114,7 @@ def test_material_argument_checks():
             g.set(f, np.ones(g.cell_shape))
     with pytest.raises(SaleError):
         g.get("MAT_F2")
-    with pytest.raises(SaleError):
+    with pytest.raises(ValueError):  # one Steinberg parameter set per material
         g.steinberg(dict(G0=1.0, GP=0.0, GT=0.0, Y0=1.0, Ymax=2.0, beta=0.0, n=1.0, cv=1.0, rho0=1.0, T0=0.0))
     g.set("MAT_M1", np.full(g.cell_shape, 0.25))
     assert np.array_equal(g.get("MASS"), g.get("MAT_M0") + 0.25)
