@@ -135,6 +135,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (core count plus the lscpu model)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -209,7 +221,8 @@ def run_reference(args, world, rank):
         "higher_is_better": True, "scaling": "weak" if args.config == "C4" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config), "sample": desc},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -364,7 +377,7 @@ def main():
         import oracle as O
         O.build()
         v, n, dt = oracle_rate(s, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"{desc}; {n} cycles in {dt:.1f} s, single thread, gcc -O2 -ffp-contract=off"}
         if args.cpu_allcore:
             agg, nproc, ncore = oracle_allcore(args.config, args.cpu_seconds / 2)
