@@ -70,6 +70,21 @@ __device__ __forceinline__ void st3s(double* b, int o0, int stride, D3 v)
 
 }  // namespace
 
+// Euler: does any active kernel load x' from memory?  The default path forms it from
+// u' (kf_energy_e, kr_sweep); SALE_ESWEEP=1 (kx_energy_sweep), SALE_REMAP != 7
+// (kr_cells / kr_cells_p) and SALE_MAT_V0=1 (k_mat_energy / k_mat_sweep) load it.
+bool euler_x1_stored()
+{
+    static const bool v = [] {
+        auto env = [](const char* n, int d) {
+            const char* e = getenv(n);
+            return e ? atoi(e) : d;
+        };
+        return env("SALE_ESWEEP", 0) > 0 || env("SALE_REMAP", 7) != 7 || env("SALE_MAT_V0", 0) == 1;
+    }();
+    return v;
+}
+
 // ============================================================================
 // kf_force
 // ============================================================================
@@ -767,7 +782,11 @@ __global__ void __launch_bounds__(FW * NW, MB) kf_sigma_e(Slab s, Phys p, int cu
 
 // grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane), y = node planes [kn0, kn1]
 // (32-bit index arithmetic: a slab holds < 2^31 cells)
-__global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int kn0)
+// wx1 = 0: x' is not stored -- its consumers on the default path (kf_energy_e,
+// kr_sweep) form x' = x^T + u' dt from u' and the target tables when they stage a
+// node plane (the same expression, the same bits); the alternative kernels that load
+// x' need wx1 = 1 (euler_x1_stored)
+__global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int kn0, int wx1)
 {
     if (!s.st->active) return;
     const int t = blockIdx.x * 256 + threadIdx.x;
@@ -811,7 +830,7 @@ __global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int k
     D3 un = d3(u.x + (ddiv(F.x, M) * dt), u.y + (ddiv(F.y, M) * dt), u.z + (ddiv(F.z, M) * dt));
     un = reflect(p, i, j, k, un);
     st3(s.u1, n, un);
-    st3(s.x1, n, d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt)));
+    if (wx1) st3(s.x1, n, d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt)));
 }
 
 // ============================================================================
@@ -1088,7 +1107,9 @@ struct EnergyEulerCTA : MatRegs<NM> {
     long long nb, cb, nbc, cbc;  // column clamped into the mesh (always-valid loads)
     double dt;
     bool col_in, cell_col, own_col;
-    D3 fu, fu1, fx1;  // prefetch registers (unconditional loads, selected at use)
+    D3 fu, fu1;       // prefetch registers (unconditional loads, selected at use)
+    double fz;        // prefetch: target Z of the node plane
+    double xcol, ycol;  // target X, Y of the (clamped) node column
     double fm, fe, fs;
     D3 fax, fay;      // prefetch: table A of the x- / y-face of cell plane k-1
     bool fnok, fcok;
@@ -1111,6 +1132,8 @@ struct EnergyEulerCTA : MatRegs<NM> {
             const int in = i > p.nx ? p.nx : i, jn = j > p.ny ? p.ny : j;
             nbc = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
             cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
+            xcol = s.Xt[in];
+            ycol = s.Yt[jn];
         }
         dt = s.st->dt;
         col_in = i <= p.nx && j <= p.ny;
@@ -1127,7 +1150,7 @@ struct EnergyEulerCTA : MatRegs<NM> {
         const long long n = nbc + (long long)kn * s.pn;
         fu = ld3(s.u[cur], n);
         fu1 = ld3(s.u1, n);
-        fx1 = ld3(s.x1, n);
+        fz = s.Zt[kn - s.kb];
         const int kc = k - 1;
         fcok = cell_col && kc >= 0 && kc < p.nz;
         int kl = kc - s.kb;
@@ -1154,7 +1177,9 @@ struct EnergyEulerCTA : MatRegs<NM> {
     __device__ __forceinline__ void put()
     {
         const D3 z = D3{0.0, 0.0, 0.0};
-        st3s(me, oP(PAR, 0), PL, fnok ? fx1 : z);
+        // x' = x^T + u' dt, kn_force_e's expression (c.3 step 6), formed when staged
+        const D3 x1 = D3{xcol + (fu1.x * dt), ycol + (fu1.y * dt), fz + (fu1.z * dt)};
+        st3s(me, oP(PAR, 0), PL, fnok ? x1 : z);
         st3s(me, oP(PAR, 3), PL, scl(0.5, add(fnok ? fu : z, fnok ? fu1 : z)));
     }
     template <int PAR>
@@ -1633,7 +1658,8 @@ static int lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st)
         // node planes updated / cell planes energised, plus the ghost region the remap needs
         const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
         if (euler_pre_sigma())  // split form: kf_sigma_e ran before the cycle's k_begin
-            kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, cs>>>(s, p, cur, kn0);
+            kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, cs>>>(s, p, cur, kn0,
+                                                                                  euler_x1_stored() ? 1 : 0);
         else  // SALE_FORCE_E=1: the one-kernel form
             force_e_launch<8, 2>(s, p, cur, kn0, kn1, tune.zc, cs);
         // kf_energy_e also writes the moved-face s' kr_sweep reads (Slab::sF)
@@ -1738,7 +1764,8 @@ int launch_energy_e_mat(const Slab& s, const Phys& p, int cur, Stream st)
 int launch_kn_force_e(const Slab& s, const Phys& p, int cur, Stream st)
 {
     const int kn0 = imax_h(s.k0 - 2, 0), kn1 = imin_h(s.k1 + 2, p.nz);
-    kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, (cudaStream_t)st>>>(s, p, cur, kn0);
+    kn_force_e<<<dim3(cdiv((int)s.pn, 256), kn1 - kn0 + 1), 256, 0, (cudaStream_t)st>>>(s, p, cur, kn0,
+                                                                                         euler_x1_stored() ? 1 : 0);
     return 1;
 }
 

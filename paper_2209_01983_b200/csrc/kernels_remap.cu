@@ -997,7 +997,8 @@ struct SweepCTA {
     long long nbn;               // the column clamped into the nodes
     bool col_in, out_col;
     double tx0, tx1, ty0, ty1;
-    D3 qx1, qu1;        // prefetch: node plane (unconditional loads, selected at use)
+    D3 qu1;             // prefetch: node plane (unconditional loads, selected at use)
+    double xcol, ycol, dt;  // target X, Y of the (clamped) node column; the cycle's dt
     double qm, qv;      // prefetch: cell m, V' of the plane before
     double qmm[NM > 0 ? NM : 1];  // prefetch: material masses
     double qz;          // prefetch: Z of node plane k
@@ -1029,7 +1030,10 @@ struct SweepCTA {
             cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
             const int in = i > p.nx ? p.nx : i, jn = j > p.ny ? p.ny : j;
             nbn = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
+            xcol = s.Xt[in];
+            ycol = s.Yt[jn];
         }
+        dt = s.st->dt;
         tx0 = col_in ? s.Xt[i] : 0.0;
         tx1 = (col_in && i + 1 <= p.nx) ? s.Xt[i + 1] : 0.0;
         ty0 = col_in ? s.Yt[j] : 0.0;
@@ -1045,7 +1049,6 @@ struct SweepCTA {
         qnok = col_in && k >= 0 && k <= p.nz;
         const int kn = k < s.kb ? s.kb : (k > s.kb + s.nzn - 1 ? s.kb + s.nzn - 1 : k);
         const long long n = nbn + (long long)kn * s.pn;
-        qx1 = ld3(s.x1, n);
         qu1 = ld3(s.u1, n);
         int kc = k - 1;
         kc = kc < s.kb ? s.kb : (kc > s.kb + s.nzc - 1 ? s.kb + s.nzc - 1 : kc);
@@ -1060,7 +1063,9 @@ struct SweepCTA {
     __device__ __forceinline__ void put()
     {
         const D3 z = D3{0.0, 0.0, 0.0};
-        st3r(me, oN(PAR, 0), PL, qnok ? qx1 : z);
+        // x' = x^T + u' dt, kn_force_e's expression (c.3 step 6), formed when staged
+        const D3 x1 = D3{xcol + (qu1.x * dt), ycol + (qu1.y * dt), qz + (qu1.z * dt)};
+        st3r(me, oN(PAR, 0), PL, qnok ? x1 : z);
         st3r(me, oN(PAR, 3), PL, qnok ? qu1 : z);
     }
     template <int PAR>
