@@ -872,7 +872,8 @@ __global__ void __launch_bounds__(RW * NW, 2) kr_nodes(Slab s, Phys p, int cur, 
 // ============================================================================
 // grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane: no idle lanes), y = planes
 template <bool TILE>  // TILE: 32 x 8 node tiles (grid x = x-tiles * y-tiles) instead of flattened rows
-__global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
+// spd = 1: also store |u''|^2 per node for kn_dt (only when kn_dt runs)
+__global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur, int spd)
 {
     if (!s.st->active) return;
     int i, j, t;
@@ -931,7 +932,7 @@ __global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur)
                u1.z + ddiv(DP.z - (u1.z * Dm), M2));
     un = reflect(p, i, j, k, un);
     st3(s.u[cur ^ 1], n, un);
-    s.x1[0][n] = speed2(un);  // |u''|^2 (x' scratch is free after the remap's cell kernels)
+    if (spd) s.x1[0][n] = speed2(un);  // |u''|^2 (x' scratch is free after the remap's cell kernels)
 }
 
 // grid: x = ceil(nx*ny / 256) (flattened cell plane), y = owned cell planes
@@ -1285,7 +1286,7 @@ int launch_sweep_mat(const Slab& s, const Phys& p, int cur, Stream st)
 int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st)
 {
     kn_update<true><<<dim3(cdivr(p.nx + 1, 32) * cdivr(p.ny + 1, 8), s.k1 - s.k0 + 1), 256, 0, (cudaStream_t)st>>>(
-        s, p, cur);
+        s, p, cur, 0);
     return 1;
 }
 
@@ -1347,7 +1348,8 @@ int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st)
     } else {
         // 32 x 8 node tiles: the gathered cell values are reused inside a block through L1
         // (measured faster than full-lane flattened rows despite the ragged last tile)
-        kn_update<true><<<dim3(cdivr(p.nx + 1, 32) * cdivr(p.ny + 1, 8), s.k1 - s.k0 + 1), 256, 0, cs>>>(s, p, cur);
+        kn_update<true><<<dim3(cdivr(p.nx + 1, 32) * cdivr(p.ny + 1, 8), s.k1 - s.k0 + 1), 256, 0, cs>>>(
+            s, p, cur, euler_pre_sigma() ? 0 : 1);
         if (euler_pre_sigma()) return 3;  // the next cycle's kf_sigma_e evaluates the dt candidate
         kn_dt<<<dim3(cdivr((int)s.pc, 256), s.k1 - s.k0), 256, 0, cs>>>(s, p, cur);
         return 4;
