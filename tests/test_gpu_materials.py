@@ -158,3 +158,25 @@ def test_full_size_material_properties(name):
     ux = c.get("UX")
     assert np.max(np.abs(ux - ref["UX"])) <= 1e-10 * max(np.max(np.abs(ref["UX"])), 1e-300)
     assert np.max(np.abs(c.get("MASS") - ref["MASS"])) <= 1e-12 * np.max(ref["MASS"])
+
+
+def test_material_error_paths_same_cycle_and_cell():
+    """The material path reports the oracle's status, cycle and cell: a tangled cell in
+    Lagrange mode, and ENEGMASS in Euler mode when a CFL number far above 1 lets the
+    faces sweep more than a cell's volume out of it."""
+    from paper_2209_01983_b200.sale import Sale
+    cfg = sedov((4, 4, 4), LAGRANGE, nmat=2, mat_gamma=[1.4, 1.6])
+    g, o = Sale(cfg, impl="fused"), O.Oracle(cfg)
+    X = o.get("X")
+    X[2, 2, 2] += 2.0
+    for c in (g, o):
+        c.set("X", X)
+    assert g.step(3) == o.step(3) == (O.ETANGLED, 0)
+    assert o.last_error().split()[-1] in g.last_error()
+    cfg = sedov((7, 6, 5), EULER, nmat=2, mat_gamma=[1.4, 1.6], cfl=1.5)
+    g, o = Sale(cfg, impl="fused"), O.Oracle(cfg)
+    apply_perturbation_mm((g, o), cfg, 2)
+    rg, ro = g.step(20), o.step(20)
+    assert rg == ro == (O.ENEGMASS, 0), (rg, ro)
+    assert o.last_error().split()[-1] in g.last_error()
+    assert g.clock() == o.clock()
