@@ -24,7 +24,12 @@ def sedov(n: tuple[int, int, int], rezone: int, **over) -> dict:
 
 
 def config(name: str, n_gpus: int = 1) -> tuple[dict, int]:
-    """Return (params, cycles) for C0..C4.  cycles = -1 means 'until t_end'."""
+    """Return (params, cycles) for C0..C4.  cycles = -1 means 'until t_end'.
+    C0M2 / C2M2: the C0 / C2 runs with two materials (gammas 1.4 and 5/3; the initial
+    layout is inputs.material_halves) -- the multi-material cells of SURVEY §8(f) NEXT-2."""
+    if name in ("C0M2", "C2M2"):
+        cfg, cycles = config(name[:2], n_gpus)
+        return dict(cfg, nmat=2, mat_gamma=[1.4, 5.0 / 3.0]), cycles
     if name == "C0":
         return sedov((16, 16, 16), LAGRANGE), 100
     if name == "C1":

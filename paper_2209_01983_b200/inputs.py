@@ -120,3 +120,16 @@ def material_mix(cfg: dict, seed: int, mass: np.ndarray, energy: np.ndarray, pur
         out[f"MAT_M{k}"] = f * mass * rng.uniform(0.5, 2.0, size=shape)
         out[f"MAT_E{k}"] = np.where(f > 0, energy * rng.uniform(0.5, 1.5, size=shape), 0.0)
     return out
+
+
+def material_halves(cfg: dict, mass: np.ndarray, energy: np.ndarray, x0: float = 0.125):
+    """The C0M2 / C2M2 layout (configs.config): cells whose centre lies at x > x0 (the
+    blast crosses that plane within the run) hold
+    material 1 (same mass and specific energy as the Sedov state there), the others
+    material 0; every cell pure.  Returns the MAT_* fields."""
+    nx = cfg["nx"]
+    xc = (np.arange(nx) + 0.5) * (cfg["lx"] / nx)
+    right = np.broadcast_to((xc > x0)[None, None, :], mass.shape)
+    return {"MAT_F0": np.where(right, 0.0, 1.0), "MAT_M0": np.where(right, 0.0, mass),
+            "MAT_E0": np.where(right, 0.0, energy), "MAT_F1": np.where(right, 1.0, 0.0),
+            "MAT_M1": np.where(right, mass, 0.0), "MAT_E1": np.where(right, energy, 0.0)}

@@ -23,6 +23,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import oracle as O  # noqa: E402
+from paper_2209_01983_b200 import inputs  # noqa: E402
 from paper_2209_01983_b200.configs import config  # noqa: E402
 
 FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "MASS", "E", "NODE_MASS", "RHO", "VOL", "P", "Q", "CS")
@@ -44,6 +45,11 @@ def main():
         cycles = args.cycles
     O.build()
     o = O.Oracle(cfg)
+    fields = FIELDS
+    if cfg.get("nmat"):  # the material runs: initial layout, and the material fields too
+        for f, v in inputs.material_halves(cfg, o.get("MASS"), o.get("MAT_E0")).items():
+            o.set(f, v)
+        fields = FIELDS + tuple(f"MAT_{q}{k}" for k in range(cfg["nmat"]) for q in "FME")
     t0 = time.time()
     done, rc = 0, 0
     target = cycles if cycles > 0 else 10 ** 9
@@ -56,7 +62,7 @@ def main():
     out = {"config": args.name, "params": cfg, "requested_cycles": cycles, "cycles_done": done, "status": rc,
            "last_error": o.last_error() if rc else "", "clock": o.clock(), "stride": STRIDE, "fields": {},
            "oracle_seconds": time.time() - t0}
-    for f in FIELDS:
+    for f in fields:
         a = o.get(f).ravel()
         out["fields"][f] = {"sha256": digest(a), "n": int(a.size),
                             "sample": [float(v) for v in a[::STRIDE]]}

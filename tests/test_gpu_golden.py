@@ -1,4 +1,5 @@
-"""Full-length parity on BASELINE's configs C1-C4 against golden oracle digests.
+"""Full-length parity on BASELINE's configs C1-C4 (and the two-material runs C0M2 / C2M2
+of SURVEY §8(f) NEXT-2) against golden oracle digests.
 
 tests/golden/<C>.json is written by scripts/oracle_digests.py, which calls only
 oracle/ (hours of single-core CPU for C3/C4, so it is not rerun at test time).
@@ -25,7 +26,7 @@ GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 def _cases():
     out = []
-    for name in ("C1", "C2", "C3", "C4"):
+    for name in ("C1", "C2", "C3", "C4", "C0M2", "C2M2"):
         if os.path.exists(os.path.join(GOLD, f"{name}.json")):
             out.append(name)
     return out
@@ -39,6 +40,10 @@ def test_full_length_digest(name):
     cfg, _ = config(name)
     assert cfg == {k: g["params"][k] for k in cfg}
     ctx = Sale(cfg, impl="fused")
+    if cfg.get("nmat"):  # the multi-material runs start from inputs.material_halves
+        from paper_2209_01983_b200 import inputs
+        for f, v in inputs.material_halves(cfg, ctx.get("MASS"), ctx.get("MAT_E0")).items():
+            ctx.set(f, v)
     want = g["requested_cycles"] if g["requested_cycles"] > 0 else 10 ** 9
     done, rc = 0, 0
     while done < want:
