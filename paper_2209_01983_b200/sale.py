@@ -172,7 +172,12 @@ def workspace_bytes(cfg: dict, **kw) -> int:
 
 
 class Sale:
-    """One libsale context on one GPU (one z-slab of the mesh per rank)."""
+    """One libsale context on one GPU (one z-slab of the mesh per rank).
+
+    cfg: the sale_params values (configs.config / configs.sedov ...); optional
+    cfg["nmat"] (1..4) and cfg["mat_gamma"] add the material axis (fields MAT_F<k>,
+    MAT_M<k>, MAT_E<k>; include/sale.h).  impl: "fused" (the z-marching kernels) or
+    "v0" (one kernel per step); local_slabs > 1 splits the mesh into emulated ranks."""
 
     def __init__(self, cfg: dict, *, device: int = 0, stream=None, rank: int = 0, nranks: int = 1,
                  nccl_id: bytes | None = None, impl: str = "v0", local_slabs: int = 1):
