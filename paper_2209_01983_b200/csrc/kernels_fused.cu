@@ -786,7 +786,9 @@ __global__ void __launch_bounds__(FW * NW, MB) kf_sigma_e(Slab s, Phys p, int cu
 // kr_sweep) form x' = x^T + u' dt from u' and the target tables when they stage a
 // node plane (the same expression, the same bits); the alternative kernels that load
 // x' need wx1 = 1 (euler_x1_stored)
-__global__ void __launch_bounds__(256) kn_force_e(Slab s, Phys p, int cur, int kn0, int wx1)
+// (8 CTAs per SM at 32 registers: a small spill, but a latency-bound gather gains more
+// from the warps -- measured C4 3.077 -> 3.003 ms with kn_update's bound)
+__global__ void __launch_bounds__(256, 8) kn_force_e(Slab s, Phys p, int cur, int kn0, int wx1)
 {
     if (!s.st->active) return;
     const int t = blockIdx.x * 256 + threadIdx.x;

@@ -873,7 +873,8 @@ __global__ void __launch_bounds__(RW * NW, 2) kr_nodes(Slab s, Phys p, int cur, 
 // grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane: no idle lanes), y = planes
 template <bool TILE>  // TILE: 32 x 8 node tiles (grid x = x-tiles * y-tiles) instead of flattened rows
 // spd = 1: also store |u''|^2 per node for kn_dt (only when kn_dt runs)
-__global__ void __launch_bounds__(256) kn_update(Slab s, Phys p, int cur, int spd)
+// (8 CTAs per SM at 32 registers, as kn_force_e: more warps for the latency-bound gather)
+__global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int spd)
 {
     if (!s.st->active) return;
     int i, j, t;
