@@ -40,7 +40,7 @@ class OracleParams(C.Structure):
                 ("t_end", C.c_double), ("rezone", C.c_int32), ("reflect_mask", C.c_uint32),
                 ("rho0", C.c_double), ("e_background", C.c_double),
                 ("e_deposit", C.c_double), ("nmat", C.c_int32), ("pad0", C.c_int32),
-                ("mat_gamma", C.c_double * 4)]
+                ("mat_gamma", C.c_double * 4), ("hg", C.c_double)]
 
 
 _lock = threading.Lock()
@@ -58,11 +58,26 @@ def build(force: bool = False) -> str:
     return LIB_PATH
 
 
+def use_openmp() -> str:
+    """Switch this process to the -fopenmp build of the same source (liboracle_omp.so):
+    the whole-mesh loops run on OMP_NUM_THREADS threads with bit-identical results
+    (oracle.c header).  For the full-size golden digests only; call before lib()."""
+    global LIB_PATH
+    path = os.path.join(_HERE, "liboracle_omp.so")
+    if not os.path.exists(path) or os.path.getmtime(path) < max(os.path.getmtime(_SRC), os.path.getmtime(_HDR)):
+        tmp = path + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-fopenmp", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, path)
+    LIB_PATH = path
+    return path
+
+
 def lib() -> C.CDLL:
     global _lib
     with _lock:
         if _lib is None:
-            build()
+            if not LIB_PATH.endswith("liboracle_omp.so"):
+                build()
             L = C.CDLL(LIB_PATH)
             P = C.POINTER
             d, i32, i64, u64 = C.c_double, C.c_int32, C.c_int64, C.c_uint64
@@ -101,12 +116,18 @@ def lib() -> C.CDLL:
             L.oracle_mix_eos.restype = None
             L.oracle_q_of_du.argtypes = [d, d, d, d, d]
             L.oracle_q_of_du.restype = d
-            L.oracle_dt_cell.argtypes = [d, d, d, d]
+            L.oracle_dt_cell.argtypes = [d, d, d, d, d, d, d]
             L.oracle_dt_cell.restype = d
             L.oracle_swept_volume.argtypes = [P(d), P(d)]
             L.oracle_swept_volume.restype = d
-            L.oracle_cell_energy.argtypes = [P(d), P(d), P(d), d, d, d, d]
+            L.oracle_cell_energy.argtypes = [P(d), P(d), P(d), d, d, d, d, d]
             L.oracle_cell_energy.restype = d
+            L.oracle_hg_modes.argtypes = [P(d), P(d)]
+            L.oracle_hg_modes.restype = None
+            L.oracle_hg_corner.argtypes = [P(d), d, i32, P(d)]
+            L.oracle_hg_corner.restype = None
+            L.oracle_hg_nu.argtypes = [d, d, d, d, d]
+            L.oracle_hg_nu.restype = d
             _lib = L
     return _lib
 
@@ -131,11 +152,12 @@ def _dp(a: np.ndarray):
 
 def make_params(cfg: dict) -> OracleParams:
     p = OracleParams()
-    p.abi_version = 2
+    p.abi_version = 3
     for name, _ in OracleParams._fields_:
-        if name in ("abi_version", "pad0", "nmat", "mat_gamma"):
+        if name in ("abi_version", "pad0", "nmat", "mat_gamma", "hg"):
             continue
         setattr(p, name, cfg[name])
+    p.hg = float(cfg.get("hg", 0.0))
     gam = list(cfg.get("mat_gamma", ()))[:4]  # nmat > 4 is rejected by oracle_create
     p.nmat = int(cfg.get("nmat", 0))
     p.mat_gamma = (C.c_double * 4)(*(gam + [0.0] * (4 - len(gam))))
@@ -256,8 +278,28 @@ def q_of_du(rho, cs, du, c1, c2):
     return lib().oracle_q_of_du(rho, cs, du, c1, c2)
 
 
-def dt_cell(cfl, l2, v2, cs):
-    return lib().oracle_dt_cell(cfl, l2, v2, cs)
+def dt_cell(cfl, l2, v2, cs, du=0.0, c1=0.25, c2=2.0):
+    """c.5 candidate with the viscous signal speed of reading DT-Q (du < 0 compresses)."""
+    return lib().oracle_dt_cell(cfl, l2, v2, cs, du, c1, c2)
+
+
+def hg_modes(U):
+    """Reading HG: mode amplitudes g[4, 3] of the 8 hex-corner velocities U[8, 3]."""
+    U = np.ascontiguousarray(U, dtype=np.float64).reshape(8, 3)
+    g = np.zeros((4, 3))
+    lib().oracle_hg_modes(_dp(U), _dp(g))
+    return g
+
+
+def hg_corner(g, nu, h):
+    g = np.ascontiguousarray(g, dtype=np.float64).reshape(4, 3)
+    f = np.zeros(3)
+    lib().oracle_hg_corner(_dp(g), nu, int(h), _dp(f))
+    return f
+
+
+def hg_nu(hg, m, cs, Lsum, dt):
+    return lib().oracle_hg_nu(hg, m, cs, Lsum, dt)
 
 
 def swept_volume(PT, PL):
@@ -266,8 +308,8 @@ def swept_volume(PT, PL):
     return lib().oracle_swept_volume(_dp(PT), _dp(PL))
 
 
-def cell_energy(N0, U0, U1, sigma, m, e, dt):
+def cell_energy(N0, U0, U1, sigma, m, e, dt, nu=0.0):
     N0 = np.ascontiguousarray(N0, dtype=np.float64).reshape(8, 3)
     U0 = np.ascontiguousarray(U0, dtype=np.float64).reshape(8, 3)
     U1 = np.ascontiguousarray(U1, dtype=np.float64).reshape(8, 3)
-    return lib().oracle_cell_energy(_dp(N0), _dp(U0), _dp(U1), sigma, m, e, dt)
+    return lib().oracle_cell_energy(_dp(N0), _dp(U0), _dp(U1), sigma, nu, m, e, dt)

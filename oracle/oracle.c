@@ -14,10 +14,16 @@
  * radius/symmetry checks; long-time C1 behaviour without hourglass control).
  *
  * Compile: gcc -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+ * The whole-mesh loops carry OpenMP work-sharing pragmas that only a -fopenmp
+ * build honours (scripts/oracle_digests.py, for the full-size golden digests):
+ * every iteration writes its own cell or node, the dt min is order-free and the
+ * failure reports take the lowest failing cell index, so the results are the
+ * single-threaded ones bit for bit.  The default build (tests, bench) is serial.
  */
 #include "oracle.h"
 
 #include <math.h>
+#include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -37,6 +43,7 @@ struct oracle_ctx {
     double *xT[3];
     /* cycle scratch */
     double *sig;                 /* sigma_K (c.3 step 3)              */
+    double *hnu, *hgm;           /* HG: nu_K and the mode amplitudes g_K (4 x 3 per cell) */
     double *x1[3], *u1[3];       /* x', u' (c.3 step 6)               */
     double *e1, *V1;             /* e', V' (c.3 step 7)               */
     double *dm, *dE, *dP[3], *m2; /* Delta m, Delta E, Delta P, m'' (c.4 step 3) */
@@ -55,6 +62,14 @@ struct oracle_ctx {
     int64_t err_cell;
     char err[256];
 };
+
+#ifdef _OPENMP
+#define OMP_FOR _Pragma("omp parallel for schedule(static)")
+#define OMP_FOR_MIN_BAD _Pragma("omp parallel for schedule(static) reduction(min:bad)")
+#else
+#define OMP_FOR
+#define OMP_FOR_MIN_BAD
+#endif
 
 static inline int64_t nid(const oracle_ctx* c, int64_t i, int64_t j, int64_t k)
 {
@@ -187,11 +202,11 @@ static inline double dmin(double a, double b) { return (b < a) ? b : a; }
 static inline double dmax(double a, double b) { return (b > a) ? b : a; }
 
 /* c.3 step 2: per logical axis, face-centroid separation d, face-average
- * velocity jump w, delta_a = (w . d)/|d|; du = min over axes; q. */
-static double cell_q(const face_t F[6], const double U[8][3], double rho, double cs,
-                     double c1, double c2)
+ * velocity jump w, delta_a = (w . d)/|d|; du = min over axes.  Also returns
+ * Lsum = ((L_x + L_y) + L_z), the sum of the separations |d| (reading HG). */
+static double cell_jumps(const face_t F[6], const double U[8][3], double* Lsum)
 {
-    double delta[3];
+    double delta[3], Ls[3];
     for (int ax = 0; ax < 3; ++ax) {
         const face_t* fm = &F[2 * ax];
         const face_t* fp = &F[2 * ax + 1];
@@ -206,15 +221,17 @@ static double cell_q(const face_t F[6], const double U[8][3], double rho, double
         }
         double L = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
         delta[ax] = ((w[0] * d[0] + w[1] * d[1]) + w[2] * d[2]) / L;
+        Ls[ax] = L;
     }
-    double du = dmin(dmin(delta[0], delta[1]), delta[2]);
-    return q_of_du(rho, cs, du, c1, c2);
+    if (Lsum) *Lsum = (Ls[0] + Ls[1]) + Ls[2];
+    return dmin(dmin(delta[0], delta[1]), delta[2]);
 }
 
-/* c.5: dt_K = (cfl*sqrt(l2)) / ((c + sqrt(v2)) + 1e-30) */
-static double dt_cell(double cfl, double l2, double v2, double cs)
+/* c.3 step 2: q of the cell */
+static double cell_q(const face_t F[6], const double U[8][3], double rho, double cs,
+                     double c1, double c2)
 {
-    return (cfl * sqrt(l2)) / ((cs + sqrt(v2)) + 1e-30);
+    return q_of_du(rho, cs, cell_jumps(F, U, NULL), c1, c2);
 }
 
 /* the 12 edges of a hex as pairs of hex-local node indices */
@@ -223,6 +240,89 @@ static const int EDGES[12][2] = {
     {0, 2}, {1, 3}, {4, 6}, {5, 7},   /* along b */
     {0, 4}, {1, 5}, {2, 6}, {3, 7},   /* along c */
 };
+
+/* reading DT-Q: the viscous signal speed of a compressing cell
+ * (du < 0, c.3 step 2), cq = 2*((c1*c) + (c2*(-du))), else 0 */
+static double visc_speed(double cs, double du, double c1, double c2)
+{
+    return (du < 0.0) ? 2.0 * ((c1 * cs) + (c2 * (-du))) : 0.0;
+}
+
+/* c.5 with reading DT-Q: the signal speed adds cq:
+ * dt_K = (cfl*sqrt(l2)) / (((c + sqrt(v2)) + cq) + 1e-30) */
+static double dt_cell(double cfl, double l2, double v2, double cs, double du, double c1,
+                      double c2)
+{
+    double cq = visc_speed(cs, du, c1, c2);
+    return (cfl * sqrt(l2)) / (((cs + sqrt(v2)) + cq) + 1e-30);
+}
+
+/* ------------------------------------------------------------------------- */
+/* reading HG: viscous hourglass damping                      */
+/* ------------------------------------------------------------------------- */
+/* Gamma_m(h) on hex-local node h = (c*2+b)*2+a with xi = 2a-1, eta = 2b-1,
+ * zeta = 2c-1: m = 0 xi*eta, 1 eta*zeta, 2 zeta*xi, 3 xi*eta*zeta (all +-1). */
+static double hg_gamma(int m, int h)
+{
+    double xi = (h & 1) ? 1.0 : -1.0, eta = (h & 2) ? 1.0 : -1.0, zeta = (h & 4) ? 1.0 : -1.0;
+    switch (m) {
+    case 0: return xi * eta;
+    case 1: return eta * zeta;
+    case 2: return zeta * xi;
+    default: return (xi * eta) * zeta;
+    }
+}
+
+/* g_m = sum over h = 0..7 (left to right) of Gamma_m(h) * U_h, componentwise */
+static void hg_modes(const double U[8][3], double g[4][3])
+{
+    for (int m = 0; m < 4; ++m)
+        for (int q = 0; q < 3; ++q) {
+            double s = hg_gamma(m, 0) * U[0][q];
+            for (int h = 1; h < 8; ++h) s = s + hg_gamma(m, h) * U[h][q];
+            g[m][q] = s;
+        }
+}
+
+/* corner force of hex corner h: f = -(nu * (((G0 g0 + G1 g1) + G2 g2) + G3 g3)) */
+static void hg_corner(const double g[4][3], double nu, int h, double f[3])
+{
+    for (int q = 0; q < 3; ++q) {
+        double s = ((hg_gamma(0, h) * g[0][q] + hg_gamma(1, h) * g[1][q]) + hg_gamma(2, h) * g[2][q])
+                   + hg_gamma(3, h) * g[3][q];
+        f[q] = -(nu * s);
+    }
+}
+
+/* uncapped coefficient nu_u = (hg*(m*c)) / lbar, lbar = Lsum/3 the mean of the
+ * cell's three face-centroid separations (c.3 step 2) */
+static double hg_nu(double hg, double m, double cs, double Lsum)
+{
+    return (hg * (m * cs)) / (Lsum / 3.0);
+}
+
+/* nu = min(nu_u, (m/64)/dt): the cap keeps the explicit damping of a mesh-wide
+ * checkerboard (64 nu dt / M per cycle) at most 1 */
+static double hg_cap(double nu_u, double m, double dt)
+{
+    return dmin(nu_u, (m / 64.0) / dt);
+}
+
+/* c.5 per-cell l2 = min over the 12 edges of the squared edge length */
+static double min_edge2(const double N[8][3])
+{
+    double l2 = 0.0;
+    for (int ed = 0; ed < 12; ++ed) {
+        const double* A = N[EDGES[ed][0]];
+        const double* B = N[EDGES[ed][1]];
+        double d0 = B[0] - A[0], d1 = B[1] - A[1], d2 = B[2] - A[2];
+        double len2 = (d0 * d0 + d1 * d1) + d2 * d2;
+        l2 = (ed == 0) ? len2 : dmin(l2, len2);
+    }
+    return l2;
+}
+
+
 
 /* ------------------------------------------------------------------------- */
 /* errors                                                                     */
@@ -268,6 +368,7 @@ static int params_valid(const oracle_params* p)
     if (p->rezone != 0 && p->rezone != 1) return 0;
     if (p->reflect_mask > 0x3Fu) return 0;
     if (!(p->rho0 > 0.0)) return 0;
+    if (!(p->hg >= 0.0)) return 0;
     if (p->nmat < 0 || p->nmat > ORACLE_MAX_MAT) return 0;
     for (int k = 0; k < p->nmat; ++k)
         if (!(p->mat_gamma[k] > 1.0)) return 0;
@@ -305,6 +406,8 @@ int32_t oracle_create(const oracle_params* p, oracle_ctx** out)
     c->m = alloc_d(c->ncell, &ok);
     c->e = alloc_d(c->ncell, &ok);
     c->sig = alloc_d(c->ncell, &ok);
+    c->hnu = alloc_d(c->ncell, &ok);
+    c->hgm = alloc_d(12 * c->ncell, &ok);
     c->e1 = alloc_d(c->ncell, &ok);
     c->V1 = alloc_d(c->ncell, &ok);
     c->dm = alloc_d(c->ncell, &ok);
@@ -376,6 +479,7 @@ void oracle_destroy(oracle_ctx* c)
         free(c->x[q]); free(c->u[q]); free(c->xT[q]);
         free(c->x1[q]); free(c->u1[q]); free(c->dP[q]);
     }
+    free(c->hnu); free(c->hgm);
     free(c->m); free(c->e); free(c->sig); free(c->e1); free(c->V1);
     free(c->dm); free(c->dE); free(c->m2);
     free(c->qv);
@@ -406,8 +510,11 @@ static void cell_mix(const oracle_ctx* c, int64_t K, double V, double rho, doubl
 static double dt_cfl_of_state(oracle_ctx* c)
 {
     const oracle_params* p = &c->p;
-    double best = 0.0;
-    int have = 0, any_nan = 0;
+    double best = INFINITY;
+    int any_nan = 0;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) reduction(min : best) reduction(| : any_nan)
+#endif
     for (int64_t k = 0; k < c->nz; ++k)
         for (int64_t j = 0; j < c->ny; ++j)
             for (int64_t i = 0; i < c->nx; ++i) {
@@ -425,22 +532,15 @@ static double dt_cfl_of_state(oracle_ctx* c)
                 } else {
                     eos(p->gamma, rho, c->e[K], &pr, &pf, &cs);
                 }
-                double l2 = 0.0;
-                for (int ed = 0; ed < 12; ++ed) {
-                    const double* A = N[EDGES[ed][0]];
-                    const double* B = N[EDGES[ed][1]];
-                    double d0 = B[0] - A[0], d1 = B[1] - A[1], d2 = B[2] - A[2];
-                    double len2 = (d0 * d0 + d1 * d1) + d2 * d2;
-                    l2 = (ed == 0) ? len2 : dmin(l2, len2);
-                }
+                double du = cell_jumps(F, U, NULL);
+                double l2 = min_edge2(N);
                 double v2 = 0.0;
                 for (int h = 0; h < 8; ++h) {
                     double s2 = (U[h][0] * U[h][0] + U[h][1] * U[h][1]) + U[h][2] * U[h][2];
                     v2 = (h == 0) ? s2 : dmax(v2, s2);
                 }
-                double dtK = dt_cell(p->cfl, l2, v2, cs);
+                double dtK = dt_cell(p->cfl, l2, v2, cs, du, p->q_lin, p->q_quad);
                 if (dtK != dtK) any_nan = 1;
-                if (!have) { best = dtK; have = 1; }
                 else best = dmin(best, dtK);
             }
     /* a NaN candidate anywhere makes dt_cfl NaN (order-free), which trips the
@@ -454,7 +554,10 @@ static int32_t next_dt(oracle_ctx* c, double* dt)
     const oracle_params* p = &c->p;
     double dt_cfl = dt_cfl_of_state(c);
     double dt_u = (c->dt_prev < 0.0) ? dt_cfl : dmin(dt_cfl, p->dt_growth * c->dt_prev);
-    if (!(dt_u > 0.0) || (p->t_end > 0.0 && dt_u < 1e-14 * p->t_end))
+    /* collapse: relative to t_end, or without an end time to the time
+     * reached so far (reading DT-C) */
+    double tref = (p->t_end > 0.0) ? p->t_end : c->t;
+    if (!(dt_u > 0.0) || dt_u < 1e-14 * tref)
         return ORACLE_EDTCOLLAPSE;
     double d = dt_u;
     if (p->t_end > 0.0) d = dmin(dt_u, p->t_end - c->t);
@@ -478,10 +581,12 @@ static int cell_exists(const oracle_ctx* c, int64_t i, int64_t j, int64_t k)
     return i >= 0 && i < c->nx && j >= 0 && j < c->ny && k >= 0 && k < c->nz;
 }
 
-/* Steps 1-3: per cell rho, p, pf, c, q, sigma = 0.25*(pf+q) */
-static void lagrange_sigma(oracle_ctx* c)
+/* Steps 1-3: per cell rho, p, pf, c, q, sigma = 0.25*(pf+q); reading HG: the
+ * cell's hourglass coefficient nu and mode amplitudes g of u^n */
+static void lagrange_sigma(oracle_ctx* c, double dt)
 {
     const oracle_params* p = &c->p;
+    OMP_FOR
     for (int64_t k = 0; k < c->nz; ++k)
         for (int64_t j = 0; j < c->ny; ++j)
             for (int64_t i = 0; i < c->nx; ++i) {
@@ -502,15 +607,30 @@ static void lagrange_sigma(oracle_ctx* c)
                 } else {
                     eos(p->gamma, rho, c->e[K], &pr, &pf, &cs);
                 }
-                double q = cell_q(F, U, rho, cs, p->q_lin, p->q_quad);
+                double Lsum;
+                double du = cell_jumps(F, U, &Lsum);
+                double q = q_of_du(rho, cs, du, p->q_lin, p->q_quad);
                 if (c->nmat > 0) c->qv[K] = q;
                 c->sig[K] = 0.25 * (pf + q);
+                double g[4][3];
+                hg_modes(U, g);
+                c->hnu[K] = hg_cap(hg_nu(p->hg, c->m[K], cs, Lsum), c->m[K], dt);
+                for (int m = 0; m < 4; ++m)
+                    for (int q3 = 0; q3 < 3; ++q3) c->hgm[12 * K + 3 * m + q3] = g[m][q3];
             }
 }
 
-/* Steps 4-6: nodal force and mass by gather, kinematics, BC, move */
+static void cell_hg_modes(const oracle_ctx* c, int64_t K, double g[4][3])
+{
+    for (int m = 0; m < 4; ++m)
+        for (int q = 0; q < 3; ++q) g[m][q] = c->hgm[12 * K + 3 * m + q];
+}
+
+/* Steps 4-6: nodal force and mass by gather, kinematics, BC, move.  Reading HG:
+ * cell K's contribution to node n is (sigma_K C_K,n) + f_K,h (h = n's corner). */
 static void lagrange_nodes(oracle_ctx* c, double dt)
 {
+    OMP_FOR
     for (int64_t k = 0; k < c->NZ; ++k)
         for (int64_t j = 0; j < c->NY; ++j)
             for (int64_t i = 0; i < c->NX; ++i) {
@@ -528,13 +648,15 @@ static void lagrange_nodes(oracle_ctx* c, double dt)
                             hex_faces(N, Fc);
                             corner_vector(Fc, 1 - ap, 1 - bp, 1 - cp, C);
                             int64_t K = cid(c, ci, cj, ck);
-                            double s = c->sig[K];
+                            double s = c->sig[K], g[4][3], fh[3];
+                            cell_hg_modes(c, K, g);
+                            hg_corner(g, c->hnu[K], ((1 - cp) * 2 + (1 - bp)) * 2 + (1 - ap), fh);
                             if (first) {
-                                for (int q = 0; q < 3; ++q) F[q] = s * C[q];
+                                for (int q = 0; q < 3; ++q) F[q] = (s * C[q]) + fh[q];
                                 M = c->m[K];
                                 first = 0;
                             } else {
-                                for (int q = 0; q < 3; ++q) F[q] = F[q] + s * C[q];
+                                for (int q = 0; q < 3; ++q) F[q] = F[q] + ((s * C[q]) + fh[q]);
                                 M = M + c->m[K];
                             }
                         }
@@ -569,18 +691,40 @@ static double cell_work(const double N0[8][3], const double U0[8][3], const doub
     return W;
 }
 
-/* c.3 step 7 for one cell (shared with the exported unit entry point) */
+/* reading HG: W_hg = sum over corners of f_h . (u_h + u'_h)/2, f_h the cell's
+ * hourglass corner force (from u^n) */
+static double cell_hg_work(const double g[4][3], double nu, const double U0[8][3],
+                           const double U1[8][3])
+{
+    double W = 0.0;
+    for (int h = 0; h < 8; ++h) {
+        double f[3], ub[3];
+        hg_corner(g, nu, h, f);
+        for (int q = 0; q < 3; ++q) ub[q] = 0.5 * (U0[h][q] + U1[h][q]);
+        double term = (f[0] * ub[0] + f[1] * ub[1]) + f[2] * ub[2];
+        W = (h == 0) ? term : W + term;
+    }
+    return W;
+}
+
+/* c.3 step 7 for one cell (shared with the exported unit entry point), with the
+ * hourglass work of reading HG: e' = e - ((((sigma W) + W_hg) dt) / m) */
 static double energy_update(const double N0[8][3], const double U0[8][3],
-                            const double U1[8][3], double sigma, double m, double e,
-                            double dt)
+                            const double U1[8][3], double sigma, double nu, double m,
+                            double e, double dt)
 {
     double W = cell_work(N0, U0, U1);
-    return e - (((sigma * W) * dt) / m);
+    double g[4][3];
+    hg_modes(U0, g);
+    double Wh = cell_hg_work(g, nu, U0, U1);
+    return e - ((((sigma * W) + Wh) * dt) / m);
 }
 
 /* Step 7: V' (tangle check), compatible pdV energy update */
 static int32_t lagrange_energy(oracle_ctx* c, double dt)
 {
+    int64_t bad = INT64_MAX;   /* lowest tangled cell (the serial scan's first) */
+    OMP_FOR_MIN_BAD
     for (int64_t k = 0; k < c->nz; ++k)
         for (int64_t j = 0; j < c->ny; ++j)
             for (int64_t i = 0; i < c->nx; ++i) {
@@ -593,26 +737,36 @@ static int32_t lagrange_energy(oracle_ctx* c, double dt)
                 hex_faces(N1, F1);
                 int64_t K = cid(c, i, j, k);
                 double V1 = hex_volume_from_faces(F1);
-                if (!(V1 > 0.0)) return fail(c, ORACLE_ETANGLED, K);
+                if (!(V1 > 0.0)) {
+                    bad = (K < bad) ? K : bad;
+                    continue;
+                }
                 c->V1[K] = V1;
                 if (c->nmat > 0) {
                     /* MM4: each present material does the cell's work with its own
                      * stress sigma_m = 0.25 (pf_m + q) on its volume share f_m (shared
                      * strain: f_m is constant through the Lagrangian phase) */
-                    double W = cell_work(N0, U0, U1);
+                    double W = cell_work(N0, U0, U1), g[4][3];
+                    cell_hg_modes(c, K, g);
+                    double Wh = cell_hg_work(g, c->hnu[K], U0, U1);
                     for (int m = 0; m < c->nmat; ++m) {
                         double f = c->mf[m][K], mm = c->mmat[m][K], em = c->me[m][K];
                         if (f > 0.0 && mm > 0.0) {
+                            /* HG: the hourglass heat is shared by volume fraction */
                             double sm = 0.25 * (c->pfm[m][K] + c->qv[K]);
-                            c->e1m[m][K] = em - ((((sm * W) * dt) * f) / mm);
+                            c->e1m[m][K] = em - (((((sm * W) + Wh) * dt) * f) / mm);
                         } else {
                             c->e1m[m][K] = em;
                         }
                     }
                 } else {
-                    c->e1[K] = energy_update(N0, U0, U1, c->sig[K], c->m[K], c->e[K], dt);
+                    double W = cell_work(N0, U0, U1), g[4][3];
+                    cell_hg_modes(c, K, g);
+                    double Wh = cell_hg_work(g, c->hnu[K], U0, U1);
+                    c->e1[K] = c->e[K] - ((((c->sig[K] * W) + Wh) * dt) / c->m[K]);
                 }
             }
+    if (bad != INT64_MAX) return fail(c, ORACLE_ETANGLED, bad);
     return ORACLE_OK;
 }
 
@@ -704,6 +858,8 @@ static void face_flux(oracle_ctx* c, int ax, int64_t i, int64_t j, int64_t k, do
 static int32_t euler_cells(oracle_ctx* c)
 {
     const int64_t nmax[3] = {c->nx, c->ny, c->nz};
+    int64_t bad = INT64_MAX;   /* lowest cell with m'' !> 0 (the serial scan's first) */
+    OMP_FOR_MIN_BAD
     for (int64_t k = 0; k < c->nz; ++k)
         for (int64_t j = 0; j < c->ny; ++j)
             for (int64_t i = 0; i < c->nx; ++i) {
@@ -731,11 +887,15 @@ static int32_t euler_cells(oracle_ctx* c)
                 for (int q = 0; q < 3; ++q)
                     c->dP[q][K] = ((((pi[0][q] - pi[1][q]) + pi[2][q]) - pi[3][q]) + pi[4][q]) - pi[5][q];
                 double m2 = c->m[K] + dm;
-                if (!(m2 > 0.0)) return fail(c, ORACLE_ENEGMASS, K);
+                if (!(m2 > 0.0)) {
+                    bad = (K < bad) ? K : bad;
+                    continue;
+                }
                 c->dm[K] = dm;
                 c->dE[K] = dE;
                 c->m2[K] = m2;
             }
+    if (bad != INT64_MAX) return fail(c, ORACLE_ENEGMASS, bad);
     return ORACLE_OK;
 }
 
@@ -771,6 +931,8 @@ static void mflux_zero(mflux_t* o)
 static int32_t euler_cells_mm(oracle_ctx* c)
 {
     const int64_t nmax[3] = {c->nx, c->ny, c->nz};
+    int64_t bad = INT64_MAX;   /* lowest failing cell (the serial scan's first) */
+    OMP_FOR_MIN_BAD
     for (int64_t k = 0; k < c->nz; ++k)
         for (int64_t j = 0; j < c->ny; ++j)
             for (int64_t i = 0; i < c->nx; ++i) {
@@ -792,23 +954,27 @@ static int32_t euler_cells_mm(oracle_ctx* c)
                 for (int q = 0; q < 3; ++q)
                     c->dP[q][K] = ((((F[0].pi[q] - F[1].pi[q]) + F[2].pi[q]) - F[3].pi[q]) + F[4].pi[q]) - F[5].pi[q];
                 double m2 = 0.0, VV = 0.0;
-                int bad = 0;
+                int neg = 0;
                 for (int m = 0; m < c->nmat; ++m) {
                     double dmm = ((((F[0].mum[m] - F[1].mum[m]) + F[2].mum[m]) - F[3].mum[m]) + F[4].mum[m]) - F[5].mum[m];
                     double dEm = ((((F[0].epm[m] - F[1].epm[m]) + F[2].epm[m]) - F[3].epm[m]) + F[4].epm[m]) - F[5].epm[m];
                     double dph = ((((F[0].phim[m] - F[1].phim[m]) + F[2].phim[m]) - F[3].phim[m]) + F[4].phim[m]) - F[5].phim[m];
                     double mm2 = c->mmat[m][K] + dmm;
                     double vm2 = (c->mf[m][K] * c->V1[K]) + dph;
-                    if (mm2 < 0.0 || vm2 < 0.0) bad = 1;
+                    if (mm2 < 0.0 || vm2 < 0.0) neg = 1;
                     c->dmm[m][K] = dmm;
                     c->dEm[m][K] = dEm;
                     c->vm2[m][K] = vm2;
                     m2 = (m == 0) ? mm2 : m2 + mm2;
                     VV = (m == 0) ? vm2 : VV + vm2;
                 }
-                if (bad || !(m2 > 0.0) || !(VV > 0.0)) return fail(c, ORACLE_ENEGMASS, K);
+                if (neg || !(m2 > 0.0) || !(VV > 0.0)) {
+                    bad = (K < bad) ? K : bad;
+                    continue;
+                }
                 c->m2[K] = m2;
             }
+    if (bad != INT64_MAX) return fail(c, ORACLE_ENEGMASS, bad);
     return ORACLE_OK;
 }
 
@@ -819,6 +985,7 @@ static void euler_nodes(oracle_ctx* c);
  * then the node update and x := x^T as c.4 steps 4-5 with the cell totals. */
 static void euler_commit_mm(oracle_ctx* c)
 {
+    OMP_FOR
     for (int64_t K = 0; K < c->ncell; ++K) {
         double VV = 0.0;
         for (int m = 0; m < c->nmat; ++m) VV = (m == 0) ? c->vm2[0][K] : VV + c->vm2[m][K];
@@ -836,6 +1003,7 @@ static void euler_commit_mm(oracle_ctx* c)
 /* c.4 step 3 (e''), step 4 (node momentum, BC), step 5 (x := x^T) */
 static void euler_commit(oracle_ctx* c)
 {
+    OMP_FOR
     for (int64_t K = 0; K < c->ncell; ++K) {
         double e1 = c->e1[K];
         c->e[K] = e1 + ((c->dE[K] - (e1 * c->dm[K])) / c->m2[K]);
@@ -846,6 +1014,7 @@ static void euler_commit(oracle_ctx* c)
 /* c.4 step 4 (node momentum from the gathered Dm, DP, m''; BC), step 5 (x := x^T), m := m'' */
 static void euler_nodes(oracle_ctx* c)
 {
+    OMP_FOR
     for (int64_t k = 0; k < c->NZ; ++k)
         for (int64_t j = 0; j < c->NY; ++j)
             for (int64_t i = 0; i < c->NX; ++i) {
@@ -891,7 +1060,7 @@ static void euler_nodes(oracle_ctx* c)
 /* ------------------------------------------------------------------------- */
 static int32_t cycle_once(oracle_ctx* c, double dt)
 {
-    lagrange_sigma(c);
+    lagrange_sigma(c, dt);
     lagrange_nodes(c, dt);
     int32_t rc = lagrange_energy(c, dt);
     if (rc) return rc;
@@ -1153,9 +1322,32 @@ double oracle_q_of_du(double rho, double cs, double du, double c1, double c2)
     return q_of_du(rho, cs, du, c1, c2);
 }
 
-double oracle_dt_cell(double cfl, double l2, double v2, double cs)
+double oracle_dt_cell(double cfl, double l2, double v2, double cs, double du, double c1, double c2)
 {
-    return dt_cell(cfl, l2, v2, cs);
+    return dt_cell(cfl, l2, v2, cs, du, c1, c2);
+}
+
+void oracle_hg_modes(const double* Uf, double* gf)
+{
+    double U[8][3], g[4][3];
+    for (int h = 0; h < 8; ++h)
+        for (int q = 0; q < 3; ++q) U[h][q] = Uf[h * 3 + q];
+    hg_modes(U, g);
+    for (int m = 0; m < 4; ++m)
+        for (int q = 0; q < 3; ++q) gf[m * 3 + q] = g[m][q];
+}
+
+void oracle_hg_corner(const double* gf, double nu, int32_t h, double* f)
+{
+    double g[4][3];
+    for (int m = 0; m < 4; ++m)
+        for (int q = 0; q < 3; ++q) g[m][q] = gf[m * 3 + q];
+    hg_corner(g, nu, (int)h, f);
+}
+
+double oracle_hg_nu(double hg, double m, double cs, double Lsum, double dt)
+{
+    return hg_cap(hg_nu(hg, m, cs, Lsum), m, dt);
 }
 
 double oracle_swept_volume(const double* PTf, const double* PLf)
@@ -1167,14 +1359,14 @@ double oracle_swept_volume(const double* PTf, const double* PLf)
 }
 
 double oracle_cell_energy(const double* N0f, const double* U0f, const double* U1f,
-                          double sigma, double m, double e, double dt)
+                          double sigma, double nu, double m, double e, double dt)
 {
     double N0[8][3], U0[8][3], U1[8][3];
     for (int h = 0; h < 8; ++h)
         for (int q = 0; q < 3; ++q) {
             N0[h][q] = N0f[h * 3 + q]; U0[h][q] = U0f[h * 3 + q]; U1[h][q] = U1f[h * 3 + q];
         }
-    return energy_update(N0, U0, U1, sigma, m, e, dt);
+    return energy_update(N0, U0, U1, sigma, nu, m, e, dt);
 }
 
 /* ---- Steinberg (Fig. 6b) ------------------------ */

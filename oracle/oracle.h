@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define ORACLE_ABI_VERSION 2
+#define ORACLE_ABI_VERSION 3
 #define ORACLE_MAX_MAT 4
 
 /* Same fields and meaning as sale_params (include/sale.h), minus the device /
@@ -56,6 +56,11 @@ typedef struct oracle_params {
     int32_t nmat;
     int32_t pad0;
     double mat_gamma[ORACLE_MAX_MAT];
+    /* hourglass viscosity coefficient (reading HG): the cell's
+     * viscous hourglass coefficient is nu = min((hg*(m*c))/(Lsum/3), (m/64)/dt)
+     * (Lsum: the sum of its three face-centroid separations); hg = 0 switches it
+     * off.  ABI version 3. */
+    double hg;
 } oracle_params;
 
 typedef struct oracle_ctx oracle_ctx;
@@ -108,14 +113,24 @@ void oracle_mix_eos(int32_t nmat, const double* gamma, const double* f, const do
                     double V, double rho, double* p, double* P, double* cs);
 /* c.3 step 2 last line: q from rho, c, du */
 double oracle_q_of_du(double rho, double cs, double du, double c1, double c2);
-/* c.5: per-cell candidate from l2 = min edge^2, v2 = max node speed^2, c */
-double oracle_dt_cell(double cfl, double l2, double v2, double cs);
+/* c.5 with reading DT-Q: per-cell candidate from l2 = min edge^2, v2 = max node
+ * speed^2, c and the compressive jump du (c.3 step 2; du >= 0: no viscous term):
+ * (cfl*sqrt(l2)) / (((c + sqrt(v2)) + cq) + 1e-30), cq = 2*((c1*c) + (c2*(-du))) */
+double oracle_dt_cell(double cfl, double l2, double v2, double cs, double du, double c1, double c2);
+/* reading HG: hourglass mode amplitudes g[m*3+comp] = sum_h Gamma_m(h) U[h*3+comp]
+ * (m = xi*eta, eta*zeta, zeta*xi, xi*eta*zeta; xi = 2a-1 on hex-local (a,b,c)) */
+void oracle_hg_modes(const double* U, double* g);
+/* reading HG: corner force f[3] = -(nu * sum_m Gamma_m(h) g_m) of hex corner h */
+void oracle_hg_corner(const double* g, double nu, int32_t h, double* f);
+/* reading HG: nu = min((hg*(m*c))/(Lsum/3), (m/64)/dt), Lsum = ((Lx+Ly)+Lz) */
+double oracle_hg_nu(double hg, double m, double cs, double Lsum, double dt);
 /* c.4 step 1: swept volume between target face PT[4][3] and moved face PL[4][3] */
 double oracle_swept_volume(const double* PT, const double* PL);
-/* c.3 step 7 for one cell: N0/N1 = nodes at t^n / t^{n+1} in hex order,
- * U0/U1 = node velocities u / u' in hex order; returns e'. */
+/* c.3 step 7 for one cell: N0 = nodes at t^n in hex order, U0/U1 = node
+ * velocities u / u' in hex order, nu = the cell's hourglass coefficient (HG; 0:
+ * none); returns e' = e - ((((sigma*W) + W_hg)*dt)/m). */
 double oracle_cell_energy(const double* N0, const double* U0, const double* U1,
-                          double sigma, double m, double e, double dt);
+                          double sigma, double nu, double m, double e, double dt);
 
 /* ---- Steinberg shear modulus and yield stress --------
  * The paper's extension example, Fig. 6b, per cell:

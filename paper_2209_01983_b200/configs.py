@@ -2,7 +2,7 @@
 
 Parameter values only -- no arithmetic of the method lives here.  Readings
 (DESIGN.md §3): viscosity c1 = 0.25, c2 = 2.0 (Q3, SPEC S:378 fixes them, which
-BASELINE.json config 0 defers to); Sedov octant with reflecting planes
+BASELINE.json config 0 defers to); hourglass viscosity hg = 0.5 (reading HG); Sedov octant with reflecting planes
 x = y = z = 0 (reflect_mask 0x15) and free outer faces (Fig. 2b; SPEC
 S:480-488); C4 grows lz with the GPU count so that every GPU holds 256^3 cubic
 cells of side 1/256 (Q15).
@@ -14,7 +14,7 @@ SEDOV_REFLECT = 0x15  # -x, -y, -z reflect; +x, +y, +z free
 
 _SEDOV = dict(lx=1.0, ly=1.0, lz=1.0, gamma=1.4, q_lin=0.25, q_quad=2.0, cfl=0.3,
               dt_growth=1.1, t_end=0.0, reflect_mask=SEDOV_REFLECT, rho0=1.0,
-              e_background=1e-10, e_deposit=1.0)
+              e_background=1e-10, e_deposit=1.0, hg=0.5)
 
 
 def sedov(n: tuple[int, int, int], rezone: int, **over) -> dict:

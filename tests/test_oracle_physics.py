@@ -3,7 +3,9 @@
 one-cycle case, octant symmetry, the Sedov-Taylor similarity law, error paths
 and checkpoint/resume.
 """
+import json
 import math
+import os
 
 import numpy as np
 import pytest
@@ -11,6 +13,8 @@ import pytest
 import oracle as O
 from paper_2209_01983_b200 import inputs
 from paper_2209_01983_b200.configs import EULER, LAGRANGE, config, sedov
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def energies(o):
@@ -220,6 +224,58 @@ def test_sedov_similarity_law_euler():
             ts.append(t); rs.append(R)
     slope = np.polyfit(np.log(ts), np.log(rs), 1)[0]
     assert abs(slope - 0.4) <= 0.05
+
+
+def _similarity(ts, rs):
+    ts, rs = np.asarray(ts), np.asarray(rs)
+    Rth = 1.0328 * (8.0 * 1.0 * ts * ts / 1.0) ** 0.2
+    return np.max(np.abs(rs - Rth) / Rth), np.polyfit(np.log(ts), np.log(rs), 1)[0]
+
+
+def test_sedov_similarity_law_lagrange_C1_trajectory():
+    """C1 (64^3, Lagrange, to t = 0.5) as the oracle ran it (tests/golden/C1.json,
+    written by scripts/oracle_digests.py, which calls only oracle/): status OK at
+    t_end, and on the snapshots with t in [0.010, 0.134] (predicted
+    R in [0.25, 0.70]) the shell-averaged density-peak radius is within 10% of
+    xi0 (8 E0 t^2 / rho0)^(1/5) with a fitted exponent 0.4 +- 0.05; total
+    energy conserved to 1e-12 over the whole run (compatible scheme with HG)."""
+    d = json.load(open(os.path.join(GOLDEN, "C1.json")))
+    assert d["status"] == 0 and d["clock"]["t"] == 0.5 and d["clock"]["finished"] == 1
+    tr = d["trajectory"]
+    win = [x for x in tr if 0.010 <= x["t"] <= 0.134]
+    assert len(win) >= 20
+    err, slope = _similarity([x["t"] for x in win], [x["R"] for x in win])
+    assert err <= 0.10 and abs(slope - 0.4) <= 0.05, (err, slope)
+    E0 = tr[0]["E_total"]
+    assert max(abs(x["E_total"] - E0) for x in tr) <= 1e-12 * E0
+
+
+@pytest.mark.slow
+def test_sedov_similarity_law_lagrange_live():
+    """The same law on a live 32^3 Lagrangian run (shell-averaged radius of the
+    density peak over cell centroids; window t in [0.010, 0.134])."""
+    n = 32
+    cfg = sedov((n, n, n), LAGRANGE)
+    o = O.Oracle(cfg)
+    ts, rs = [], []
+    h = 1.0 / n
+    while o.clock()["t"] < 0.134:
+        assert o.step(20)[0] == 0
+        t = o.clock()["t"]
+        if t < 0.010 or t > 0.134:
+            continue
+        rho = o.get("RHO")
+        X, Y, Z = (o.get(f) for f in ("X", "Y", "Z"))
+        cc = [0.125 * (A[:-1, :-1, :-1] + A[1:, :-1, :-1] + A[:-1, 1:, :-1] + A[1:, 1:, :-1]
+                       + A[:-1, :-1, 1:] + A[1:, :-1, 1:] + A[:-1, 1:, 1:] + A[1:, 1:, 1:]) for A in (X, Y, Z)]
+        r = np.sqrt(cc[0] ** 2 + cc[1] ** 2 + cc[2] ** 2)
+        bins = np.arange(0, 2.0, h)
+        idx = np.digitize(r.ravel(), bins)
+        prof = np.bincount(idx, weights=rho.ravel()) / np.maximum(np.bincount(idx), 1)
+        ts.append(t)
+        rs.append(bins[np.argmax(prof) - 1] + 0.5 * h)
+    err, slope = _similarity(ts, rs)
+    assert err <= 0.10 and abs(slope - 0.4) <= 0.05, (err, slope)
 
 
 # ------------------------------------------------------------------ errors
