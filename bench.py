@@ -7,7 +7,7 @@ whole mesh.  Default workload: BASELINE.json config 4 ("C4": Sedov-Taylor 3D,
 256^3 cells per GPU, Eulerian rezoning, fp64, z-slabs over the GPUs -> weak
 scaling); --config C3 selects the strong-scaling Lagrangian 320^3 mesh.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4|C3] [--impl fused|v0]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4|C3]
     python bench.py --impl reference ...   # the CPU oracle arm (rank 0 only)
 
 One JSON line on rank 0.  Timing: W untimed cycles, then K cycles bracketed by
@@ -45,7 +45,7 @@ ALGO_BYTES = {configs.LAGRANGE: 120.0, configs.EULER: 80.0}
 ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 661.0, "remap": 0.0},
              configs.EULER: {"lagrange": 362.0, "remap": 406.0}}
 # kernel name prefixes of each timing class (for the ncu traffic file)
-CLASS_KERNELS = {"lagrange": ("kf_", "kn_force", "kx_"), "remap": ("kr_", "kn_update", "kn_dt")}
+CLASS_KERNELS = {"lagrange": ("kc_", "ke_state", "k_state"), "remap": ("kr_", "kn_update", "k_mat_flux")}
 REASON_BITS = {"hw_slowdown": "hw_slowdown", "hw_thermal_slowdown": "hw_thermal_slowdown",
                "sw_thermal_slowdown": "sw_thermal_slowdown", "sw_power_cap": "sw_power_cap"}
 
@@ -239,7 +239,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4", choices=["C3", "C4"])
-    ap.add_argument("--impl", default="auto", choices=["auto", "fused", "v0", "reference"])
+    ap.add_argument("--impl", default="auto", choices=["auto", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -262,16 +262,13 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo")  # plumbing only: id broadcast, barrier, max
-    impl = args.impl
-    if impl == "auto":
-        impl = "fused" if S.workspace_bytes(configs.config("C0")[0], impl="fused") else "v0"
     cfg, _ = configs.config(args.config, world)
     nid = None
     if world > 1:
         obj = [S.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    ctx = S.Sale(cfg, device=local, rank=rank, nranks=world, nccl_id=nid, impl=impl)
+    ctx = S.Sale(cfg, device=local, rank=rank, nranks=world, nccl_id=nid)
     stream = ctx.stream
 
     def barrier():
@@ -394,7 +391,7 @@ def main():
             "config": {"workload": workload_name(args.config), "global_cells": gcells,
                        "cells_per_gpu": local_cells, "mesh": [cfg["nx"], cfg["ny"], cfg["nz"]],
                        "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
-                       "impl": impl, "step": "one SALE cycle",
+                       "step": "one SALE cycle",
                        "l2": "inputs larger than L2 (state >= 1.1 GB per GPU), no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,

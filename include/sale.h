@@ -8,9 +8,11 @@
  * rezoning, Advection") -- on a structured 3D hexahedral mesh, for the
  * Sedov-Taylor blast wave (Fig. 2b "3D Eulerian Sedov-Taylor").
  * The paper gives no discrete equations; the operators are SURVEY.md §8(c)
- * c.1-c.6 with the readings listed in DESIGN.md §3.  One cycle is:
- *   Lagrangian phase  S1-S7  (geometry, EoS, viscosity, CFL dt, corner forces,
- *                             kinematics + reflecting BC, compatible pdV energy)
+ * c.1-c.6 with the readings listed in DESIGN.md §3 (round 2: the viscous hourglass
+ * damping HG and the viscous signal speed in the time step DT-Q).  One cycle is:
+ *   Lagrangian phase  S1-S7  (geometry, EoS, viscosity, CFL dt, corner forces with
+ *                             hourglass damping, kinematics + reflecting BC,
+ *                             compatible pdV energy)
  *   Eulerian remap    R1-R5  (rezone = SALE_EULER only: swept volumes,
  *                             donor-cell fluxes of mass/energy/momentum, reset)
  *   X1 halo exchange, X2 dt min-reduction   (z-slabs over ranks)
@@ -41,7 +43,7 @@
 extern "C" {
 #endif
 
-#define SALE_ABI_VERSION 2
+#define SALE_ABI_VERSION 3
 #define SALE_MAX_MAT 4       /* materials per cell (multi-material mode)            */
 
 /* status codes */
@@ -51,7 +53,8 @@ extern "C" {
 #define SALE_ECUDA 3         /* CUDA runtime error (detail in sale_last_error)      */
 #define SALE_ENCCL 4         /* NCCL error                                          */
 #define SALE_ETANGLED 5      /* some cell's new volume V' is not > 0 (c.3 step 7)   */
-#define SALE_EDTCOLLAPSE 6   /* dt_u not > 0, or < 1e-14 * t_end (c.5)             */
+#define SALE_EDTCOLLAPSE 6   /* dt_u not > 0, or < 1e-14 * t_end (c.5; without an
+                                end time: < 1e-14 * t, reading DT-C)                 */
 #define SALE_ENEGMASS 7      /* remapped mass m'' not > 0 (c.4 step 3)              */
 #define SALE_EPOISONED 8     /* context unusable after an earlier error             */
 #define SALE_EREPLICA 9      /* replicated interface node planes differ (self-check) */
@@ -59,10 +62,6 @@ extern "C" {
 /* rezone modes */
 #define SALE_LAGRANGE 0
 #define SALE_EULER 1
-
-/* kernel implementation (both are this library's own sm_100a kernels) */
-#define SALE_IMPL_FUSED 0    /* fused z-marching kernels (default)                 */
-#define SALE_IMPL_V0 1       /* one kernel per step, for bring-up and cross-checks */
 
 /* field ids; node fields 0..6, cell fields 7..13 (and the material fields 16..27 below) */
 #define SALE_F_X 0
@@ -111,7 +110,7 @@ typedef struct sale_params {
                                  aligned, owned by the caller, not freed by us     */
     uint64_t workspace_bytes;
     int32_t device;           /* CUDA device ordinal this context runs on          */
-    int32_t impl;             /* SALE_IMPL_FUSED or SALE_IMPL_V0                   */
+    int32_t pad0;             /* zero                                              */
     int32_t local_slabs;      /* >= 1.  With nranks == 1, split the mesh into this
                                  many z-slabs on the same device exchanging halos
                                  by device copies (emulated ranks, used to prove
@@ -129,11 +128,18 @@ typedef struct sale_params {
                                  pressures; the remap moves each material's mass,
                                  volume and energy from the donor cell.  MASS and E
                                  are then read-only (MASS = sum of material masses,
-                                 E = mass-weighted mixture energy).  The material
-                                 kernels are one per step (the v0 schedule) whatever
-                                 impl says; nmat = 1 gives the single-material
+                                 E = mass-weighted mixture energy).  The cycle
+                                 kernels carry the material count as a compile-time
+                                 parameter; nmat = 1 gives the single-material
                                  results bit for bit.                              */
     double mat_gamma[SALE_MAX_MAT];
+    double hg;                /* hourglass viscosity coefficient >= 0 (reading HG,
+                                 DESIGN.md §3; 0 = none, the Sedov configs use 0.5):
+                                 per cell nu = min((hg (m c)) / (Lsum / 3), (m / 64) / dt)
+                                 with Lsum the sum of its three face-centroid
+                                 separations; the corner force -nu sum_m Gamma_m g_m
+                                 damps the four hourglass modes g_m of u^n, its work
+                                 heats the cell (total energy is conserved).       */
 } sale_params;
 
 typedef struct sale_ctx sale_ctx;
@@ -152,8 +158,8 @@ int32_t sale_nccl_unique_id(void* id_out_128);
 int32_t sale_create(const sale_params* p, sale_ctx** out);
 
 /* Enqueue up to ncycles cycles on the stream, then synchronise once.  Each
- * step call starts with a halo exchange and a dt-candidate pass, so state set
- * with sale_set_field / sale_set_clock is always honoured.  Stops early (status
+ * step call starts with a halo exchange and a cell-state + dt-candidate pass, so
+ * state set with sale_set_field / sale_set_clock is always honoured.  Stops early (status
  * OK, *cycles_done < ncycles) when t >= t_end.  On a numerical error returns its
  * code, sets *cycles_done to the number of good cycles, poisons the context. */
 int32_t sale_step(sale_ctx* c, int32_t ncycles, int32_t* cycles_done);
@@ -202,9 +208,11 @@ int64_t sale_kernel_launches(const sale_ctx* c);
  * accumulated at the next synchronisation (sale_step / sale_sync).  Enabling
  * resets the accumulators.  Classes: */
 #define SALE_K_BEGIN 0     /* dt finalisation + clock commit (one thread)          */
-#define SALE_K_PROLOGUE 1  /* per-call halo exchange + dt-candidate pass           */
-#define SALE_K_LAGRANGE 2  /* Lagrangian phase S1-S7 (+ next dt candidate, Lagrange) */
-#define SALE_K_REMAP 3     /* Eulerian remap R1-R5 + next dt candidate             */
+#define SALE_K_PROLOGUE 1  /* per-call halo exchange + cell-state / dt-candidate pass */
+#define SALE_K_LAGRANGE 2  /* Lagrangian phase S1-S7 (+ the cell state and dt
+                              candidate: Lagrange of the new state, Euler of the
+                              cycle-start state)                                    */
+#define SALE_K_REMAP 3     /* Eulerian remap R1-R5                                 */
 #define SALE_K_HALO 4      /* per-cycle halo exchange + dt/error allreduce         */
 #define SALE_K_NCLASS 5
 int32_t sale_profile_enable(sale_ctx* c, int32_t on);

@@ -1,10 +1,24 @@
-// kernels_common.cu -- initialisation, clock / dt finalisation, dt candidate,
-// derived fields.  SURVEY §8(c) c.1, c.5, c.6.
+// kernels_common.cu -- initialisation, target-mesh tables, clock / dt
+// finalisation, derived fields, the Steinberg cell kernel.  SURVEY §8(c) c.1, c.5,
+// c.6; the dt candidates come with the cell-state passes (kernels_lag.cu).
 #include <cuda_runtime.h>
 
 #include "sale_mesh.cuh"
 
 namespace sale {
+
+static thread_local cudaError_t g_launch_err = cudaSuccess;
+void note_launch()
+{
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess && g_launch_err == cudaSuccess) g_launch_err = e;
+}
+int take_launch_error()
+{
+    const cudaError_t e = g_launch_err;
+    g_launch_err = cudaSuccess;
+    return (int)e;
+}
 
 static inline unsigned grid_for(long long n, int bs)
 {
@@ -75,13 +89,16 @@ int launch_init_tables(const Slab& s, const Phys& p, Stream st)
     int n = p.nx > p.ny ? p.nx : p.ny;
     n = n > s.nzn ? n : s.nzn;
     k_init_tables<<<grid_for(n + 1, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    note_launch();
     return 1;
 }
 
 int launch_sedov_init(const Slab& s, const Phys& p, Stream st)
 {
     k_sedov_nodes<<<grid_for(s.pn * s.nzn, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    note_launch();
     k_sedov_cells<<<grid_for(s.pc * s.nzc, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    note_launch();
     return 2;
 }
 
@@ -157,6 +174,7 @@ int launch_target_tables(const Slab& s, const Phys& p, Stream st)
     n = n > (long long)p.nx * s.nzc ? n : (long long)p.nx * s.nzc;
     n = n > (long long)p.nx * p.ny ? n : (long long)p.nx * p.ny;
     k_target_tables<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p);
+    note_launch();
     return 1;
 }
 
@@ -196,7 +214,9 @@ __global__ void k_begin(DevState* d, Phys p)
     }
     double dt_cfl = dt_unkey(d->cand_key);
     double dt_u = (d->dt_prev < 0.0) ? dt_cfl : dmin(dt_cfl, p.growth * d->dt_prev);
-    if (!(dt_u > 0.0) || (p.t_end > 0.0 && dt_u < 1e-14 * p.t_end)) {
+    // collapse: relative to t_end, without an end time to the time reached (DT-C)
+    const double tref = (p.t_end > 0.0) ? p.t_end : d->t;
+    if (!(dt_u > 0.0) || dt_u < 1e-14 * tref) {
         d->status = S_EDTCOLLAPSE;
         d->err_cycle = d->cycle;
         d->err_cell = -1;
@@ -219,87 +239,26 @@ __global__ void k_reset_good(DevState* d) { d->good = 0; }
 int launch_prep(DevState* d, Stream st)
 {
     k_prep<<<1, 1, 0, (cudaStream_t)st>>>(d);
+    note_launch();
     return 1;
 }
 int launch_begin(DevState* d, const Phys& p, Stream st)
 {
     k_begin<<<1, 1, 0, (cudaStream_t)st>>>(d, p);
+    note_launch();
     return 1;
 }
 int launch_commit(DevState* d, const Phys& p, Stream st)
 {
     k_commit<<<1, 1, 0, (cudaStream_t)st>>>(d, p);
+    note_launch();
     return 1;
 }
 int launch_reset_good(DevState* d, Stream st)
 {
     k_reset_good<<<1, 1, 0, (cudaStream_t)st>>>(d);
+    note_launch();
     return 1;
-}
-
-// ------------------------------------------------------- c.5 dt candidate
-// per owned cell: dt_K from (x, u, m, e) of buffer `cur`; block min -> atomicMin
-template <bool EULER>
-__global__ void k_dt_candidate(Slab s, Phys p, int cur, int gate)
-{
-    if (gate && !s.st->active) return;
-    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    long long total = s.pc * (s.k1 - s.k0);
-    unsigned long long key = KEY_NONE;
-    if (t < total) {
-        int k = s.k0 + (int)(t / s.pc);
-        long long r = t % s.pc;
-        int j = (int)(r / p.nx), i = (int)(r % p.nx);
-        D3 U[8];
-        load_hex3(s, p, s.u[cur], i, j, k, U);
-        long long c = cidx(s, p, i, j, k);
-        double V, l2;
-        if (EULER) {
-            // fixed target mesh: V^T precomputed with the same hex formula, and the
-            // 12 target edges are axis-aligned (X_{i+1}-X_i, 0, 0) etc.
-            V = s.VT[c];
-            const double lx = len2(D3{s.Xt[i], 0.0, 0.0}, D3{s.Xt[i + 1], 0.0, 0.0});
-            const double ly = len2(D3{0.0, s.Yt[j], 0.0}, D3{0.0, s.Yt[j + 1], 0.0});
-            const double lz = len2(D3{0.0, 0.0, s.Zt[k - s.kb]}, D3{0.0, 0.0, s.Zt[k + 1 - s.kb]});
-            l2 = dmin(dmin(lx, ly), lz);
-        } else {
-            D3 N[8];
-            load_hex_pos<EULER>(s, p, cur, i, j, k, N);
-            V = hex_volume(N);
-            l2 = hex_min_edge2(N);
-        }
-        double rho = ddiv(mass_cur(s, p, cur)[c], V), pr, pf, cs;
-        if (s.nmat) {
-            double pfk[MAX_MAT];
-            mix_eos(s, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, pf, cs, pfk);
-        } else {
-            eos(p.gamma, rho, s.e[cur][c], pr, pf, cs);
-        }
-        s.rhoc[c] = rho;
-        s.csc[c] = cs;
-        key = dt_key(dt_cell(p.cfl, l2, hex_max_speed2(U), cs));
-    }
-    block_min_atomic(key, &s.st->cand_key);
-}
-
-static int dt_candidate(const Slab& s, const Phys& p, int cur, int gate, Stream st)
-{
-    long long n = s.pc * (s.k1 - s.k0);
-    if (p.rezone)
-        k_dt_candidate<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, gate);
-    else
-        k_dt_candidate<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, gate);
-    return 1;
-}
-// ungated: at the start of sale_step, on the current state
-int launch_dt_candidate(const Slab& s, const Phys& p, int cur, Stream st)
-{
-    return dt_candidate(s, p, cur, 0, st);
-}
-// gated on DevState.active: at the end of a cycle, on the new state
-int launch_dt_candidate_gated(const Slab& s, const Phys& p, int cur, Stream st)
-{
-    return dt_candidate(s, p, cur, 1, st);
 }
 
 // ------------------------------------------------------- derived fields
@@ -387,12 +346,14 @@ int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st)
     if (field <= 6) {
         long long n = s.pn * (s.k1 - s.k0 + 1);
         k_derive_nodes<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, field);
+        note_launch();
     } else {
         long long n = s.pc * (s.k1 - s.k0);
         if (p.rezone)
             k_derive_cells<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, field);
         else
             k_derive_cells<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, field);
+        note_launch();
     }
     return 1;
 }
@@ -458,7 +419,7 @@ int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& 
                      double* y, long long mstride, Stream st)
 {
     const long long n = s.pc * (s.k1 - s.k0);
-    auto go = [&](auto kern) { kern<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, set, eps, sh, y, mstride); };
+    auto go = [&](auto kern) { kern<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, set, eps, sh, y, mstride); note_launch(); };
     switch (s.nmat * 2 + (p.rezone ? 1 : 0)) {
     case 0: go(k_steinberg<false, 0>); break;
     case 1: go(k_steinberg<true, 0>); break;

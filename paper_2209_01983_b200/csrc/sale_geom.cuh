@@ -137,11 +137,20 @@ __device__ __forceinline__ double q_of_du(double rho, double cs, double du, doub
     return (du < 0.0) ? rho * ((c2 * (du * du)) + ((c1 * cs) * (-du))) : 0.0;
 }
 
-// c.3 step 2 for a hex: face-average velocities over the canonical face nodes
-__device__ __forceinline__ double hex_q(const D3 Xb[6], const D3 U[8], double rho, double cs,
-                                        double c1, double c2)
+// c.3 step 2 (per axis) also returning the separation L = sqrt(d . d) (reading HG)
+__device__ __forceinline__ double axis_jump_L(D3 Xm, D3 Xp, D3 Um, D3 Up, double& L)
 {
-    double dl[3];
+    D3 d = sub(Xp, Xm);
+    D3 w = sub(Up, Um);
+    L = dsqrt((d.x * d.x + d.y * d.y) + d.z * d.z);
+    return ddiv((w.x * d.x + w.y * d.y) + w.z * d.z, L);
+}
+
+// c.3 step 2 for a hex: face-average velocities over the canonical face nodes;
+// du = min over the axes, Lsum = ((Lx + Ly) + Lz)
+__device__ __forceinline__ double hex_du(const D3 Xb[6], const D3 U[8], double& Lsum)
+{
+    double dl[3], L[3];
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
         int a, b, c, d;
@@ -149,16 +158,97 @@ __device__ __forceinline__ double hex_q(const D3 Xb[6], const D3 U[8], double rh
         D3 Um = avg4(U[a], U[b], U[c], U[d]);
         hex_face_nodes(2 * ax + 1, a, b, c, d);
         D3 Up = avg4(U[a], U[b], U[c], U[d]);
-        dl[ax] = axis_jump(Xb[2 * ax], Xb[2 * ax + 1], Um, Up);
+        dl[ax] = axis_jump_L(Xb[2 * ax], Xb[2 * ax + 1], Um, Up, L[ax]);
     }
-    double du = dmin(dmin(dl[0], dl[1]), dl[2]);
-    return q_of_du(rho, cs, du, c1, c2);
+    Lsum = (L[0] + L[1]) + L[2];
+    return dmin(dmin(dl[0], dl[1]), dl[2]);
+}
+__device__ __forceinline__ double hex_q(const D3 Xb[6], const D3 U[8], double rho, double cs,
+                                        double c1, double c2)
+{
+    double Lsum;
+    return q_of_du(rho, cs, hex_du(Xb, U, Lsum), c1, c2);
 }
 
-// c.5: dt_K = (cfl*sqrt(l2)) / ((c + sqrt(v2)) + 1e-30)
-__device__ __forceinline__ double dt_cell(double cfl, double l2, double v2, double cs)
+// reading DT-Q: viscous signal speed of a compressing cell,
+// cq = 2*((c1*c) + (c2*(-du))) for du < 0, else 0
+__device__ __forceinline__ double visc_speed(double cs, double du, double c1, double c2)
 {
-    return ddiv(cfl * dsqrt(l2), (cs + dsqrt(v2)) + 1e-30);
+    return (du < 0.0) ? 2.0 * ((c1 * cs) + (c2 * (-du))) : 0.0;
+}
+
+// c.5 with DT-Q: dt_K = (cfl*sqrt(l2)) / (((c + sqrt(v2)) + cq) + 1e-30)
+__device__ __forceinline__ double dt_cell(double cfl, double l2, double v2, double cs, double cq)
+{
+    return ddiv(cfl * dsqrt(l2), ((cs + dsqrt(v2)) + cq) + 1e-30);
+}
+// the same with the numerator cfl*sqrt(l2) given (tabled on the Euler target mesh)
+__device__ __forceinline__ double dt_cell_num(double num, double v2, double cs, double cq)
+{
+    return ddiv(num, ((cs + dsqrt(v2)) + cq) + 1e-30);
+}
+
+// ---- reading HG: viscous hourglass damping ---------------------
+// Gamma_m(h) on hex corner h = (c*2+b)*2+a, xi = 2a-1, eta = 2b-1, zeta = 2c-1:
+// m = 0 xi*eta, 1 eta*zeta, 2 zeta*xi, 3 xi*eta*zeta.  Returns +1 / -1.
+__host__ __device__ constexpr int hg_gamma(int m, int h)
+{
+    return (m == 0)   ? (((h & 1) ? 1 : -1) * ((h & 2) ? 1 : -1))
+           : (m == 1) ? (((h & 2) ? 1 : -1) * ((h & 4) ? 1 : -1))
+           : (m == 2) ? (((h & 4) ? 1 : -1) * ((h & 1) ? 1 : -1))
+                      : (((h & 1) ? 1 : -1) * ((h & 2) ? 1 : -1) * ((h & 4) ? 1 : -1));
+}
+// a + G*b for G = +-1 (exact: the product is a sign flip)
+__device__ __forceinline__ D3 addsg(D3 a, D3 b, int G) { return G > 0 ? add(a, b) : sub(a, b); }
+__device__ __forceinline__ double addsg(double a, double b, int G) { return G > 0 ? a + b : a - b; }
+// g_m = sum over h = 0..7, left to right, of Gamma_m(h) U_h (componentwise)
+template <int M>
+__device__ __forceinline__ D3 hg_mode(const D3 U[8])
+{
+    D3 s = hg_gamma(M, 0) > 0 ? U[0] : neg(U[0]);
+#pragma unroll
+    for (int h = 1; h < 8; ++h) s = addsg(s, U[h], hg_gamma(M, h));
+    return s;
+}
+__device__ __forceinline__ void hg_modes(const D3 U[8], D3 g[4])
+{
+    g[0] = hg_mode<0>(U);
+    g[1] = hg_mode<1>(U);
+    g[2] = hg_mode<2>(U);
+    g[3] = hg_mode<3>(U);
+}
+// corner force of corner H: f = -(nu * (((G0 g0 + G1 g1) + G2 g2) + G3 g3))
+template <int H>
+__device__ __forceinline__ D3 hg_corner(const D3 g[4], double nu)
+{
+    D3 t = hg_gamma(0, H) > 0 ? g[0] : neg(g[0]);
+    t = addsg(t, g[1], hg_gamma(1, H));
+    t = addsg(t, g[2], hg_gamma(2, H));
+    t = addsg(t, g[3], hg_gamma(3, H));
+    return D3{-(nu * t.x), -(nu * t.y), -(nu * t.z)};
+}
+__device__ __forceinline__ D3 hg_corner_rt(const D3 g[4], double nu, int h)
+{
+    switch (h) {
+    case 0: return hg_corner<0>(g, nu);
+    case 1: return hg_corner<1>(g, nu);
+    case 2: return hg_corner<2>(g, nu);
+    case 3: return hg_corner<3>(g, nu);
+    case 4: return hg_corner<4>(g, nu);
+    case 5: return hg_corner<5>(g, nu);
+    case 6: return hg_corner<6>(g, nu);
+    default: return hg_corner<7>(g, nu);
+    }
+}
+// uncapped coefficient nu_u = (hg*(m*c)) / (Lsum/3), Lsum = ((Lx+Ly)+Lz)
+__device__ __forceinline__ double hg_nu(double hg, double m, double cs, double Lsum)
+{
+    return ddiv(hg * (m * cs), ddiv(Lsum, 3.0));
+}
+// nu = min(nu_u, (m/64)/dt)
+__device__ __forceinline__ double hg_cap(double nu_u, double m, double dt)
+{
+    return dmin(nu_u, ddiv(ddiv(m, 64.0), dt));
 }
 
 __device__ __forceinline__ double len2(D3 a, D3 b)

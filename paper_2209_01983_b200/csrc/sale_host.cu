@@ -29,9 +29,6 @@ static_assert(SALE_MAX_MAT == sale::MAX_MAT, "material count out of sync");
 static_assert(offsetof(sale::DevState, err_key) == offsetof(sale::DevState, cand_key) + 8,
               "cand_key / err_key must be adjacent for the 2-element allreduce");
 
-namespace sale {
-bool fused_available();
-}
 using sale::DevState;
 using sale::Phys;
 using sale::Slab;
@@ -64,10 +61,6 @@ struct sale_ctx {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     long long glaunches[2] = {0, 0};
     cudaStream_t cap_stream = nullptr;  // private stream the graphs are captured on
-    // boundary-first overlap (Lagrange, >1 slab): the halo exchange runs on `side`
-    // while the interior computes; evB = boundary planes done, evX = exchange done
-    cudaStream_t side = nullptr;
-    cudaEvent_t evB = nullptr, evX = nullptr;
 };
 
 namespace {
@@ -117,8 +110,7 @@ bool params_ok(const sale_params* p)
     if (p->nranks < 1 || p->rank < 0 || p->rank >= p->nranks) return false;
     if (p->nranks > 1 && p->nccl_unique_id == nullptr) return false;  // nranks == 1 + id: 1-rank NCCL comm
     if (p->local_slabs < 1 || (p->nranks > 1 && p->local_slabs != 1)) return false;
-    if (p->impl != SALE_IMPL_V0 && p->impl != SALE_IMPL_FUSED) return false;
-    if (p->impl == SALE_IMPL_FUSED && !sale::fused_available()) return false;
+    if (!(p->hg >= 0.0)) return false;
     int T = p->nranks * p->local_slabs;
     if (p->nz < T) return false;
     if (T > 1 && p->nz / T < ghost_depth(p)) return false;  // every slab owns >= g planes
@@ -170,10 +162,9 @@ size_t carve_slab(const sale_params* p, Slab& s, char* base)
     s.e[0] = take(nc);
     s.e[1] = take(nc);
     s.sig = take(nc);
-    s.rhoc = take(nc);
-    s.csc = take(nc);
+    s.hnu = take(nc);
     for (int a = 0; a < 3; ++a) {
-        s.x1[a] = euler ? take(nn) : nullptr;
+        s.x1[a] = nullptr;  // x' is formed from u' where needed (Euler)
         s.u1[a] = euler ? take(nn) : nullptr;
         s.dP[a] = euler ? take(nc) : nullptr;
     }
@@ -269,7 +260,9 @@ int nccl_check(sale_ctx* c, ncclResult_t r, const char* what)
 
 int launch_check(sale_ctx* c)
 {
-    return cuda_check(c, cudaGetLastError(), "kernel launch");
+    cudaError_t e = cudaGetLastError();
+    const cudaError_t noted = (cudaError_t)sale::take_launch_error();
+    return cuda_check(c, noted != cudaSuccess ? noted : e, "kernel launch");
 }
 
 cudaEvent_t take_event(sale_ctx* c)
@@ -496,75 +489,22 @@ int reduce_keys(sale_ctx* c)
                       "dt allreduce");
 }
 
-// Lagrange fused with more than one slab (ranks or emulated): boundary planes first,
-// the halo exchange on a side stream overlapping the interior.
-// Opt-in (SALE_OVERLAP=1): measured 1-6% slower with emulated slabs on one GPU, where
-// the device copies it hides are cheaper than the split's thin boundary grids
-// (DESIGN.md §8).
-bool overlap_enabled(const sale_ctx* c)
-{
-    static const int on = [] {
-        const char* v = getenv("SALE_OVERLAP");
-        return v ? atoi(v) : 0;
-    }();
-    return on && c->prm.rezone == SALE_LAGRANGE && c->prm.impl == SALE_IMPL_FUSED && c->prm.nmat == 0 &&
-           (c->prm.nranks > 1 || c->prm.local_slabs > 1);
-}
-
-int overlap_resources(sale_ctx* c)
-{
-    int rc = SALE_OK;
-    if (!c->side) rc = cuda_check(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
-    if (!rc && !c->evB) rc = cuda_check(c, cudaEventCreateWithFlags(&c->evB, cudaEventDisableTiming), "event");
-    if (!rc && !c->evX) rc = cuda_check(c, cudaEventCreateWithFlags(&c->evX, cudaEventDisableTiming), "event");
-    return rc;
-}
-
-// one Lagrange cycle, boundary first: part 0 of every slab (the planes the exchange
-// sends), then the exchange on the side stream while part 1 (the interior) runs on the
-// context's stream; the stream waits for the exchange before the dt allreduce.  The
-// interior reads buffer b and the owned planes of b^1 only; the exchange writes the
-// ghost planes of b^1 only.
-int enqueue_cycle_overlap(sale_ctx* c, int b)
+// one cycle reading buffers [b]; first = the first cycle of a sale_step call (Euler:
+// its ke_state runs ungated, DevState.active being still 0 then).
+//   Euler:    ke_state (cell state + dt candidate of the cycle-start state) -> dt /
+//             error allreduce -> k_begin -> kc_force -> kc_energy -> remap -> halo
+//   Lagrange: k_begin -> kc_force -> kc_energy (+ the new state's cell state and dt
+//             candidate) -> halo -> ghost cell state (more than one slab) -> allreduce
+int enqueue_one_cycle(sale_ctx* c, int b, bool first)
 {
     int rc;
-    if ((rc = overlap_resources(c))) return rc;
     sale::Stream st = (sale::Stream)c->stream;
-    int pr = prof_open(c, SALE_K_BEGIN);
-    c->launches += sale::launch_begin(c->dstate, c->phys, st);
-    prof_close(c, pr);
-    pr = prof_open(c, SALE_K_LAGRANGE);
-    for (auto& s : c->slabs) c->launches += sale::launch_lagrange_fused_part(s, c->phys, b, 0, st);
-    if ((rc = launch_check(c))) return rc;
-    if ((rc = cuda_check(c, cudaEventRecord(c->evB, c->stream), "event record"))) return rc;
-    if ((rc = cuda_check(c, cudaStreamWaitEvent(c->side, c->evB, 0), "stream wait"))) return rc;
-    if ((rc = exchange(c, b ^ 1, false, c->side))) return rc;
-    if ((rc = cuda_check(c, cudaEventRecord(c->evX, c->side), "event record"))) return rc;
-    for (auto& s : c->slabs) c->launches += sale::launch_lagrange_fused_part(s, c->phys, b, 1, st);
-    if ((rc = launch_check(c))) return rc;
-    if ((rc = cuda_check(c, cudaStreamWaitEvent(c->stream, c->evX, 0), "stream wait"))) return rc;
-    prof_close(c, pr);
-    pr = prof_open(c, SALE_K_HALO);
-    if ((rc = reduce_keys(c))) return rc;
-    prof_close(c, pr);
-    return SALE_OK;
-}
-
-// one cycle reading buffers [b]; first = the first cycle of a sale_step call (its
-// kf_sigma_e runs ungated: DevState.active is still 0 then)
-int enqueue_one_cycle(sale_ctx* c, int b, bool first, bool pre)
-{
-    if (overlap_enabled(c)) return enqueue_cycle_overlap(c, b);
-    int rc;
-    sale::Stream st = (sale::Stream)c->stream;
-    const bool mat = c->prm.nmat > 0;  // the material kernels (v0 schedule) whatever impl says
-    const bool v0 = c->prm.impl == SALE_IMPL_V0 || mat, euler = c->prm.rezone == SALE_EULER;
+    const bool euler = c->prm.rezone == SALE_EULER;
+    const bool multi = c->slabs.size() > 1 || c->prm.nranks > 1;
     int pr;
-    if (pre) {
+    if (euler) {
         pr = prof_open(c, SALE_K_LAGRANGE);
-        for (auto& s : c->slabs)
-            c->launches += c->prm.nmat ? sale::launch_mat_pre(s, c->phys, b, first ? 0 : 1, st)
-                                       : sale::launch_euler_pre(s, c->phys, b, first ? 0 : 1, st);
+        for (auto& s : c->slabs) c->launches += sale::launch_state_euler(s, c->phys, b, first ? 0 : 1, st);
         prof_close(c, pr);
         pr = prof_open(c, SALE_K_HALO);
         if ((rc = reduce_keys(c))) return rc;
@@ -575,40 +515,43 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first, bool pre)
     prof_close(c, pr);
     for (auto& s : c->slabs) {
         pr = prof_open(c, SALE_K_LAGRANGE);
-        c->launches += mat  ? sale::launch_lagrange_mat(s, c->phys, b, st)
-                       : v0 ? sale::launch_lagrange_v0(s, c->phys, b, st)
-                            : sale::launch_lagrange_fused(s, c->phys, b, st);
+        c->launches += sale::launch_force(s, c->phys, b, st);
+        c->launches += sale::launch_energy(s, c->phys, b, st);
         prof_close(c, pr);
         if (euler) {
             pr = prof_open(c, SALE_K_REMAP);
-            c->launches += mat  ? sale::launch_remap_mat(s, c->phys, b, st)
-                           : v0 ? sale::launch_remap_v0(s, c->phys, b, st)
-                                : sale::launch_remap_fused(s, c->phys, b, st);
+            c->launches += c->prm.nmat ? sale::launch_remap_mat(s, c->phys, b, st) : sale::launch_remap(s, c->phys, b, st);
             prof_close(c, pr);
         }
     }
     if ((rc = launch_check(c))) return rc;
     pr = prof_open(c, SALE_K_HALO);
     if ((rc = exchange(c, b ^ 1, false))) return rc;
-    if (!pre && (rc = reduce_keys(c))) return rc;
+    if (!euler && multi)  // the cell state of the ghost cell planes from the exchanged state
+        for (auto& s : c->slabs) {
+            c->launches += sale::launch_state_lag(s, c->phys, b ^ 1, s.k0 - 1, s.k0, 0, 1, st);
+            c->launches += sale::launch_state_lag(s, c->phys, b ^ 1, s.k1, s.k1 + 1, 0, 1, st);
+        }
+    if (!euler && (rc = reduce_keys(c))) return rc;
     prof_close(c, pr);
-    return SALE_OK;
+    return launch_check(c);
 }
 
 // CUDA graph of two consecutive cycles starting from buffer parity b (they return to
-// b), captured once per context and parity, then replayed: a cycle is 6-9 kernel
-// launches plus copies, which dominate small meshes.  Single-rank contexts only (the
-// NCCL calls of a multi-rank cycle stay on the plain path), never while profiling.
+// b), captured once per context and parity, then replayed: a cycle is 4-8 kernel
+// launches plus copies, which dominate small meshes.  The NCCL send/recv group and
+// the allreduce of a multi-rank cycle are captured with the kernels (NCCL >= 2.9
+// supports stream capture).  Never while profiling; SALE_GRAPHS=0 disables them.
 bool graphs_enabled(const sale_ctx* c)
 {
     static const int on = [] {
         const char* v = getenv("SALE_GRAPHS");
         return v ? atoi(v) : 1;
     }();
-    return on && !c->comm && !c->prof_on;
+    return on && !c->prof_on;
 }
 
-int graph_for(sale_ctx* c, int b, bool pre, cudaGraphExec_t* out)
+int graph_for(sale_ctx* c, int b, cudaGraphExec_t* out)
 {
     if (c->gexec[b]) {
         *out = c->gexec[b];
@@ -629,8 +572,8 @@ int graph_for(sale_ctx* c, int b, bool pre, cudaGraphExec_t* out)
         c->stream = user;
         return rc;
     }
-    int rc1 = enqueue_one_cycle(c, b, false, pre);
-    if (!rc1) rc1 = enqueue_one_cycle(c, b ^ 1, false, pre);
+    int rc1 = enqueue_one_cycle(c, b, false);
+    if (!rc1) rc1 = enqueue_one_cycle(c, b ^ 1, false);
     rc = cuda_check(c, cudaStreamEndCapture(c->stream, &g), "graph capture end");
     c->stream = user;
     if (rc1 || rc) {
@@ -652,37 +595,36 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
     int rc;
     int b = c->cur_enq;
     sale::Stream st = (sale::Stream)c->stream;
-    bool v0 = c->prm.impl == SALE_IMPL_V0 || c->prm.nmat > 0, euler = c->prm.rezone == SALE_EULER;
-    // Euler fused with the split force: each cycle's kf_sigma_e evaluates sigma and the
-    // dt candidate of its start state before k_begin (no separate dt pass)
-    const bool pre = euler && (c->prm.nmat ? true : !v0 && sale::euler_pre_sigma());
+    const bool euler = c->prm.rezone == SALE_EULER;
+    // prologue: ghost planes of the current state; Lagrange: the cell state of every
+    // local cell and the dt candidate of the owned ones (Euler: each cycle's ke_state)
     int pr = prof_open(c, SALE_K_PROLOGUE);
     c->launches += sale::launch_prep(c->dstate, st);
     if ((rc = exchange(c, b, true))) return rc;
-    if (!pre) {
-        for (auto& s : c->slabs) c->launches += sale::launch_dt_candidate(s, c->phys, b, st);
+    if (!euler) {
+        for (auto& s : c->slabs) c->launches += sale::launch_state_lag(s, c->phys, b, s.kb, s.kb + s.nzc, 1, 0, st);
         if ((rc = reduce_keys(c))) return rc;
     }
     prof_close(c, pr);
     int n = 0;
-    if (ncycles > 0) {  // the first cycle on the plain path (ungated sigma)
-        if ((rc = enqueue_one_cycle(c, b, true, pre))) return rc;
+    if (ncycles > 0) {  // the first cycle on the plain path (Euler: ungated ke_state)
+        if ((rc = enqueue_one_cycle(c, b, true))) return rc;
         b ^= 1;
         n = 1;
     }
     if (graphs_enabled(c) && ncycles - n >= 2) {
         cudaGraphExec_t ge = nullptr;
-        if ((rc = graph_for(c, b, pre, &ge))) return rc;
+        if ((rc = graph_for(c, b, &ge))) return rc;
         for (; n + 2 <= ncycles; n += 2) {
             if ((rc = cuda_check(c, cudaGraphLaunch(ge, c->stream), "graph launch"))) return rc;
             c->launches += c->glaunches[b];
         }
     }
     for (; n < ncycles; ++n) {
-        if ((rc = enqueue_one_cycle(c, b, false, pre))) return rc;
+        if ((rc = enqueue_one_cycle(c, b, false))) return rc;
         b ^= 1;
     }
-    if (pre && ncycles > 0 && (rc = reduce_keys(c))) return rc;  // the last cycle's error key
+    if (euler && ncycles > 0 && (rc = reduce_keys(c))) return rc;  // the last cycle's error key
     c->launches += sale::launch_commit(c->dstate, c->phys, (sale::Stream)c->stream);
     c->cur_enq = b;
     return launch_check(c);
@@ -859,6 +801,7 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
     ph.gamma = p->gamma; ph.c1 = p->q_lin; ph.c2 = p->q_quad; ph.cfl = p->cfl;
     ph.growth = p->dt_growth; ph.t_end = p->t_end;
     ph.rho0 = p->rho0; ph.e_bg = p->e_background; ph.e_dep = p->e_deposit;
+    ph.hg = p->hg;
     ph.nx = p->nx; ph.ny = p->ny; ph.nz = p->nz;
     ph.reflect = p->reflect_mask; ph.rezone = p->rezone;
     layout_slabs(p, c->slabs);
@@ -903,6 +846,10 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
     }
     if (!rc) rc = cuda_check(c, cudaStreamSynchronize(c->stream), "create sync");
     if (!rc && ph.rezone) rc = check_diag_areas(c);
+    // the Euler kernels form corner vectors and axis jumps from the diagonal table
+    // components (a tensor-product target mesh always has them)
+    if (!rc && ph.rezone && !(ph.diag_areas && ph.diag_jumps))
+        rc = set_err(c, SALE_EINVAL, "target mesh tables are not axis-aligned");
     if (rc) {
         if (c->comm) ncclCommDestroy(c->comm);
         cudaFreeHost(c->hstate);
@@ -1149,9 +1096,6 @@ void sale_destroy(sale_ctx* c)
     for (auto ge : c->gexec)
         if (ge) cudaGraphExecDestroy(ge);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-    if (c->side) cudaStreamDestroy(c->side);
-    if (c->evB) cudaEventDestroy(c->evB);
-    if (c->evX) cudaEventDestroy(c->evX);
     delete c;
 }
 

@@ -13,6 +13,7 @@ struct Phys {
     double lx, ly, lz;
     double gamma, c1, c2, cfl, growth, t_end;
     double rho0, e_bg, e_dep;
+    double hg;                // hourglass viscosity coefficient (reading HG)
     int nx, ny, nz;           // global cells
     unsigned reflect;         // bit f: face f of {-x,+x,-y,+y,-z,+z} reflects
     int rezone;               // 0 Lagrange, 1 Euler
@@ -49,10 +50,10 @@ struct Slab {
     double* u[2][3];          // node velocities (ping-pong)
     double* m[2];             // cell mass (Euler ping-pong; Lagrange uses m[0])
     double* e[2];             // specific internal energy (ping-pong)
-    double* sig;              // v0 scratch: sigma per cell
-    double* rhoc;             // Lagrange EoS cache: rho and sound speed c of every owned cell at the
-    double* csc;              // state the last dt-candidate pass saw (kf_energy / the prologue pass
-                              // evaluate them for c.5); the next kf_force reuses them (same bits)
+    double* sig;              // cell state of the cycle start: sigma = 0.25 (pf + q) (c.3 step 3) and
+    double* hnu;              // the uncapped hourglass coefficient nu_u (reading HG), written by the
+                              // state passes (Lagrange: the energy kernel of the previous cycle for
+                              // the new state, the prologue and the ghost pass; Euler: ke_state)
     double* x1[3];            // Euler scratch: x' (post-Lagrange positions)
     double* u1[3];            // Euler scratch: u'
     double* e1;               // Euler scratch: e'
@@ -92,7 +93,7 @@ struct Slab {
     double* mf[2];            // volume fraction f_k
     double* mm[2];            // material mass m_k (m above holds the sum over k)
     double* me[2];            // material specific energy e_k
-    double* sgm;              // scratch: each material's stress 0.25 (pf_k + q) at the cycle start (MM4)
+    double* sgm;              // each material's stress 0.25 (pf_k + q) at the cycle start (MM4; state passes)
     double* e1m;              // Euler scratch: e'_k
     double* rDm;              // Euler scratch: donor material density m_k / V' of each cell (k_mat_sweep)
     double mg[MAX_MAT];       // gamma of each material (here rather than in Phys: growing Phys
@@ -122,6 +123,12 @@ constexpr unsigned long long ERR_ORDER_TANGLED = 1, ERR_ORDER_NEGMASS = 2;
 // every launcher returns the number of kernels it launched
 typedef struct CUstream_st* Stream;
 
+// every launcher calls note_launch() right after each kernel launch: it keeps the
+// first launch error of this host thread (a later runtime call may clear the
+// runtime's own last-error slot); the host's launch check takes it
+void note_launch();
+int take_launch_error();  // a cudaError_t, 0 if none; resets
+
 int launch_init_tables(const Slab& s, const Phys& p, Stream st);
 int launch_sedov_init(const Slab& s, const Phys& p, Stream st);
 int launch_target_tables(const Slab& s, const Phys& p, Stream st);
@@ -129,40 +136,34 @@ int launch_prep(DevState* d, Stream st);
 int launch_begin(DevState* d, const Phys& p, Stream st);
 int launch_commit(DevState* d, const Phys& p, Stream st);
 int launch_reset_good(DevState* d, Stream st);
-int launch_dt_candidate(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st);
 // Steinberg shear / yield of the owned cells (include/sale.h); outputs at sh / y (device)
 int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& set, const double* eps, double* sh,
                      double* y, long long mstride, Stream st);
-// one cycle on one slab, reading buffers [cur], writing [cur^1]:
-// the Lagrangian phase (S1-S7; Lagrange mode also the next dt candidate), then
-// in Euler mode the remap (R1-R5 + next dt candidate)
-int launch_lagrange_v0(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_remap_v0(const Slab& s, const Phys& p, int cur, Stream st);
-// multi-material cells (kernels_mat.cu): the v0 schedule with the material axis
-int launch_lagrange_mat(const Slab& s, const Phys& p, int cur, Stream st);
+
+// ---- the cycle (kernels_lag.cu, kernels_remap.cu, kernels_mat.cu) ------------
+// Lagrange: the cell state (sigma, nu_u, material stresses) of buffer `cur` for cell
+// planes [kc0, kc1) (one thread per cell); key = 1 also forms the c.5 dt candidate of
+// the owned cells among them.  Used at the start of sale_step (all local cells) and,
+// with more than one slab, for the ghost cell planes after each cycle's exchange
+// (gate = 1: skipped unless a cycle is in flight).
+int launch_state_lag(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int key, int gate, Stream st);
+// Euler: the cell state and the dt candidate of the cycle-start state, before the
+// cycle's k_begin (gate = 0 for the first cycle of a sale_step call)
+int launch_state_euler(const Slab& s, const Phys& p, int cur, int gate, Stream st);
+// S5-S6: corner forces (pressure, viscosity, hourglass) gathered in the fixed order,
+// kinematics + BC.  Lagrange: x', u' into buffer cur^1; Euler: u' into Slab::u1.
+int launch_force(const Slab& s, const Phys& p, int cur, Stream st);
+// S7: V', tangle check, compatible energy with the hourglass work.  Lagrange: e' into
+// buffer cur^1 and the cell state + dt candidate of the new state; Euler: e' (e'_k), V',
+// and the moved-face s' the sweep reads.
+int launch_energy(const Slab& s, const Phys& p, int cur, Stream st);
+// R1-R4 (kernels_remap.cu; materials: kernels_mat.cu)
+int launch_remap(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_sweep(const Slab& s, const Phys& p, int cur, Stream st);
+int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st);
 int launch_mat_init(const Slab& s, const Phys& p, Stream st);
 int launch_mat_total(const Slab& s, const Phys& p, int cur, Stream st);
-// Euler: sigma + the cycle-start dt candidate, before the cycle's k_begin (gate as launch_euler_pre)
-int launch_mat_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st);
-int launch_kn_force_e(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_force_mat(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_sigma_e_mat(const Slab& s, const Phys& p, int cur, int gate, Stream st);
-int launch_energy_e_mat(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_sweep_mat(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_lagrange_fused(const Slab& s, const Phys& p, int cur, Stream st);
-// Lagrange fused in two parts: 0 = the planes the halo exchange sends, 1 = the interior
-int launch_lagrange_fused_part(const Slab& s, const Phys& p, int cur, int part, Stream st);
-int launch_remap_fused(const Slab& s, const Phys& p, int cur, Stream st);
-bool fused_available();
-// Euler fused, split force: kf_sigma_e (sigma + the dt candidate of the cycle-start
-// state) is launched before the cycle's k_begin; the remap then has no dt pass
-bool euler_pre_sigma();
-int launch_euler_pre(const Slab& s, const Phys& p, int cur, int gate, Stream st);
-// Euler fused: > 0 when the Lagrangian phase's energy kernel also does the remap's
-// swept volumes and donor data (kx_energy_sweep); the remap then starts at kr_flux
-int euler_esweep_variant();
 
 }  // namespace sale

@@ -20,7 +20,6 @@ OK, EINVAL, ENOMEM, ECUDA, ENCCL, ETANGLED, EDTCOLLAPSE, ENEGMASS, EPOISONED, ER
 CODE_NAMES = ["OK", "EINVAL", "ENOMEM", "ECUDA", "ENCCL", "ETANGLED", "EDTCOLLAPSE", "ENEGMASS",
               "EPOISONED", "EREPLICA"]
 LAGRANGE, EULER = 0, 1
-IMPL = {"fused": 0, "v0": 1}
 FIELDS = {"X": 0, "Y": 1, "Z": 2, "UX": 3, "UY": 4, "UZ": 5, "NODE_MASS": 6,
           "MASS": 7, "E": 8, "RHO": 9, "VOL": 10, "P": 11, "Q": 12, "CS": 13}
 MAX_MAT = 4
@@ -44,8 +43,8 @@ class SaleParams(C.Structure):
                 ("e_background", C.c_double), ("e_deposit", C.c_double), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
-                ("device", C.c_int32), ("impl", C.c_int32), ("local_slabs", C.c_int32),
-                ("nmat", C.c_int32), ("mat_gamma", C.c_double * MAX_MAT)]
+                ("device", C.c_int32), ("pad0", C.c_int32), ("local_slabs", C.c_int32),
+                ("nmat", C.c_int32), ("mat_gamma", C.c_double * MAX_MAT), ("hg", C.c_double)]
 
 
 class SaleSteinberg(C.Structure):
@@ -127,15 +126,15 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def make_params(cfg: dict, *, rank=0, nranks=1, device=0, impl="v0", local_slabs=1) -> SaleParams:
+def make_params(cfg: dict, *, rank=0, nranks=1, device=0, local_slabs=1) -> SaleParams:
     p = SaleParams()
-    p.abi_version = 2
+    p.abi_version = 3
     for k in ("nx", "ny", "nz", "lx", "ly", "lz", "gamma", "q_lin", "q_quad", "cfl", "dt_growth",
               "t_end", "rezone", "reflect_mask", "rho0", "e_background", "e_deposit"):
         setattr(p, k, cfg[k])
     p.rank, p.nranks, p.device = rank, nranks, device
-    p.impl = IMPL[impl] if isinstance(impl, str) else int(impl)
     p.local_slabs = local_slabs
+    p.hg = float(cfg.get("hg", 0.0))
     gam = list(cfg.get("mat_gamma", ()))[:MAX_MAT]  # nmat > MAX_MAT is rejected by libsale
     p.nmat = int(cfg.get("nmat", 0))
     p.mat_gamma = (C.c_double * MAX_MAT)(*(gam + [0.0] * (MAX_MAT - len(gam))))
@@ -176,19 +175,18 @@ class Sale:
 
     cfg: the sale_params values (configs.config / configs.sedov ...); optional
     cfg["nmat"] (1..4) and cfg["mat_gamma"] add the material axis (fields MAT_F<k>,
-    MAT_M<k>, MAT_E<k>; include/sale.h).  impl: "fused" (the z-marching kernels) or
-    "v0" (one kernel per step); local_slabs > 1 splits the mesh into emulated ranks."""
+    MAT_M<k>, MAT_E<k>; include/sale.h); cfg["hg"] the hourglass coefficient (0 if
+    absent).  local_slabs > 1 splits the mesh into emulated ranks on one GPU."""
 
     def __init__(self, cfg: dict, *, device: int = 0, stream=None, rank: int = 0, nranks: int = 1,
-                 nccl_id: bytes | None = None, impl: str = "v0", local_slabs: int = 1):
+                 nccl_id: bytes | None = None, local_slabs: int = 1):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("libsale needs a CUDA device (no CPU fallback)")
         L = lib()
         self.cfg = dict(cfg)
         self._L = L
-        p = make_params(cfg, rank=rank, nranks=nranks, device=device, impl=impl,
-                        local_slabs=local_slabs)
+        p = make_params(cfg, rank=rank, nranks=nranks, device=device, local_slabs=local_slabs)
         nbytes = L.sale_workspace_bytes(C.byref(p))
         if nbytes == 0:
             raise SaleError(EINVAL, "sale_workspace_bytes")

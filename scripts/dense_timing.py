@@ -10,7 +10,7 @@ from tests.helpers import apply_perturbation
 for name in ("C4", "C3"):
     for dense in (False, True):
         cfg, _ = config(name)
-        g = Sale(cfg, impl="fused")
+        g = Sale(cfg)
         if dense:
             apply_perturbation([g], cfg, 0, lagrange=(cfg["rezone"] == LAGRANGE))
         g.step(3)

@@ -29,7 +29,7 @@ for case in range(first, first + n):
     nmat = int(rng.integers(0, 5)) if rng.uniform() < 0.5 else 0
     extra = {"nmat": nmat, "mat_gamma": [float(x) for x in rng.uniform(1.1, 3.0, size=nmat)]} if nmat else {}
     cfg = sedov(shape, rezone, **extra)
-    g, o = Sale(cfg, impl="fused", local_slabs=slabs), O.Oracle(cfg)
+    g, o = Sale(cfg, local_slabs=slabs), O.Oracle(cfg)
     seed = int(rng.integers(0, 1000))
     if nmat:
         apply_perturbation_mm((g, o), cfg, seed)

@@ -8,7 +8,7 @@ from paper_2209_01983_b200.sale import Sale
 nmat = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 name = sys.argv[2] if len(sys.argv) > 2 else "C4"
 cfg, _ = config(name)
-g = Sale(dict(cfg, nmat=nmat, mat_gamma=[1.4, 5.0 / 3.0, 1.2, 2.0][:nmat]), impl="fused")
+g = Sale(dict(cfg, nmat=nmat, mat_gamma=[1.4, 5.0 / 3.0, 1.2, 2.0][:nmat]))
 m, e = g.get("MAT_M0"), g.get("MAT_E0")
 for k in range(nmat):
     g.set(f"MAT_F{k}", np.full(g.cell_shape, 1.0 / nmat))

@@ -56,7 +56,7 @@ def test_workspace_bytes_validates(L):
     assert sale.workspace_bytes(dict(cfg, gamma=1.0)) == 0
     assert sale.workspace_bytes(dict(cfg, nx=0)) == 0
     assert sale.workspace_bytes(dict(cfg, rezone=2)) == 0
-    assert sale.workspace_bytes(cfg, impl=7) == 0
+    assert sale.workspace_bytes(dict(cfg, hg=-1.0)) == 0
     # the material axis: 0..4 materials, every gamma > 1
     assert sale.workspace_bytes(dict(cfg, nmat=4, mat_gamma=[1.4, 1.5, 1.6, 1.7])) > sale.workspace_bytes(cfg)
     assert sale.workspace_bytes(dict(cfg, nmat=5, mat_gamma=[1.4] * 4)) == 0

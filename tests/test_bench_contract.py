@@ -37,4 +37,4 @@ def test_gpu_arm_line():
     assert r["bound"] == "alu" and 0 < r["frac"] < 1.2 and r["peak"] > 10
     assert d["gpu_launches"] >= 4 * 5
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
-    assert d["config"]["impl"] == "fused"
+    assert "workload" in d["config"]

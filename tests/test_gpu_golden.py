@@ -4,7 +4,7 @@ of SURVEY §8(f) NEXT-2) against golden oracle digests.
 tests/golden/<C>.json is written by scripts/oracle_digests.py, which calls only
 oracle/ (hours of single-core CPU for C3/C4, so it is not rerun at test time).
 The GPU runs the same config through the C ABI in the bench launch
-configuration (impl=fused) and must reproduce the oracle's status, cycle count
+configuration and must reproduce the oracle's status, cycle count
 and clock exactly, and every field's SHA-256 over its float64 bits; if a digest
 ever differs the strided samples are compared at the north-star bar (1e-9
 relative, reading Q19) to say how far apart they are.
@@ -39,7 +39,7 @@ def test_full_length_digest(name):
         g = json.load(f)
     cfg, _ = config(name)
     assert cfg == {k: g["params"][k] for k in cfg}
-    ctx = Sale(cfg, impl="fused")
+    ctx = Sale(cfg)
     if cfg.get("nmat"):  # the multi-material runs start from inputs.material_halves
         from paper_2209_01983_b200 import inputs
         for f, v in inputs.material_halves(cfg, ctx.get("MASS"), ctx.get("MAT_E0")).items():

@@ -24,7 +24,7 @@ def mat_fields(n):
 
 def _pair(cfg, seed, local_slabs=1):
     from paper_2209_01983_b200.sale import Sale
-    g, o = Sale(cfg, impl="fused", local_slabs=local_slabs), O.Oracle(cfg)
+    g, o = Sale(cfg, local_slabs=local_slabs), O.Oracle(cfg)
     apply_perturbation_mm((g, o), cfg, seed)
     return g, o
 
@@ -73,8 +73,8 @@ def test_one_material_equals_single_material_kernels(rezone):
     """nmat = 1 through the material kernels == nmat = 0 through the fused kernels."""
     from paper_2209_01983_b200.sale import Sale
     cfg = sedov((12, 10, 9), rezone)
-    a = Sale(cfg, impl="fused")
-    b = Sale(dict(cfg, nmat=1, mat_gamma=[cfg["gamma"]]), impl="fused")
+    a = Sale(cfg)
+    b = Sale(dict(cfg, nmat=1, mat_gamma=[cfg["gamma"]]))
     o = O.Oracle(cfg)
     apply_perturbation([o, a], cfg, seed=4, lagrange=rezone == LAGRANGE)
     for f in ("X", "Y", "Z") if rezone == LAGRANGE else ():
@@ -92,7 +92,7 @@ def test_one_material_equals_single_material_kernels(rezone):
 def test_two_gas_shock_tube_bitwise(rezone):
     from paper_2209_01983_b200.sale import Sale
     cfg = shock_tube(150, rezone, nmat=2, mat_gamma=[1.4, 5.0 / 3.0])
-    g, o = Sale(cfg, impl="fused"), O.Oracle(cfg)
+    g, o = Sale(cfg), O.Oracle(cfg)
     for f, v in inputs.two_material_tube_state(cfg, o.get("MASS")).items():
         g.set(f, v)
         o.set(f, v)
@@ -108,7 +108,7 @@ def test_material_argument_checks():
     assert workspace_bytes(dict(cfg, nmat=5, mat_gamma=[1.4] * 4)) == 0
     assert workspace_bytes(dict(cfg, nmat=2, mat_gamma=[1.4, 1.0])) == 0
     assert workspace_bytes(dict(cfg, nmat=2, mat_gamma=[1.4, 1.5])) > workspace_bytes(cfg)
-    g = Sale(dict(cfg, nmat=2, mat_gamma=[1.4, 1.5]), impl="fused")
+    g = Sale(dict(cfg, nmat=2, mat_gamma=[1.4, 1.5]))
     for f in ("MASS", "E"):
         with pytest.raises(SaleError):
             g.set(f, np.ones(g.cell_shape))
@@ -130,13 +130,13 @@ def test_full_size_material_properties(name):
     from paper_2209_01983_b200.sale import Sale
     cfg, _ = config(name)
     cycles = 6
-    a = Sale(cfg, impl="fused")
+    a = Sale(cfg)
     assert a.step(cycles) == (0, cycles)
     ref = {f: a.get(f) for f in ("UX", "MASS", "E", "P")}
     a.close()
     del a
     torch.cuda.empty_cache()
-    b = Sale(dict(cfg, nmat=1, mat_gamma=[cfg["gamma"]]), impl="fused")
+    b = Sale(dict(cfg, nmat=1, mat_gamma=[cfg["gamma"]]))
     assert b.step(cycles) == (0, cycles)
     for f in ("UX", "MASS", "P"):
         assert np.array_equal(b.get(f), ref[f]), f
@@ -144,7 +144,7 @@ def test_full_size_material_properties(name):
     b.close()
     del b
     torch.cuda.empty_cache()
-    c = Sale(dict(cfg, nmat=2, mat_gamma=[cfg["gamma"]] * 2), impl="fused")
+    c = Sale(dict(cfg, nmat=2, mat_gamma=[cfg["gamma"]] * 2))
     m, e = c.get("MAT_M0"), c.get("MAT_E0")
     c.set("MAT_F0", np.full(c.cell_shape, 0.25))
     c.set("MAT_F1", np.full(c.cell_shape, 0.75))
@@ -162,20 +162,26 @@ def test_full_size_material_properties(name):
 
 def test_material_error_paths_same_cycle_and_cell():
     """The material path reports the oracle's status, cycle and cell: a tangled cell in
-    Lagrange mode, and ENEGMASS in Euler mode when a CFL number far above 1 lets the
-    faces sweep more than a cell's volume out of it."""
+    Lagrange mode, and ENEGMASS in Euler mode when a CFL number above 1 lets the faces
+    sweep more than a cell's volume out of it."""
     from paper_2209_01983_b200.sale import Sale
     cfg = sedov((4, 4, 4), LAGRANGE, nmat=2, mat_gamma=[1.4, 1.6])
-    g, o = Sale(cfg, impl="fused"), O.Oracle(cfg)
+    g, o = Sale(cfg), O.Oracle(cfg)
     X = o.get("X")
     X[2, 2, 2] += 2.0
     for c in (g, o):
         c.set("X", X)
     assert g.step(3) == o.step(3) == (O.ETANGLED, 0)
     assert o.last_error().split()[-1] in g.last_error()
-    cfg = sedov((7, 6, 5), EULER, nmat=2, mat_gamma=[1.4, 1.6], cfl=1.5)
-    g, o = Sale(cfg, impl="fused"), O.Oracle(cfg)
-    apply_perturbation_mm((g, o), cfg, 2)
+    # a uniform translation at CFL 1.5 sweeps 1.5 cell volumes through every face
+    # (no deformation, so no tangle); alternating densities leave cells with m'' < 0
+    cfg = sedov((7, 6, 5), EULER, nmat=2, mat_gamma=[1.4, 1.6], cfl=1.5, reflect_mask=0, e_deposit=0.0,
+                e_background=1e-6)
+    g, o = Sale(cfg), O.Oracle(cfg)
+    m = o.get("MAT_M0") * np.where((np.arange(7) % 2) == 0, 1.0, 0.05)[None, None, :]
+    for c in (g, o):
+        c.set("UX", np.ones(o.node_shape))
+        c.set("MAT_M0", m)
     rg, ro = g.step(20), o.step(20)
     assert rg == ro == (O.ENEGMASS, 0), (rg, ro)
     assert o.last_error().split()[-1] in g.last_error()

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 def _pair(cfg, state):
     from paper_2209_01983_b200.sale import Sale
-    g, o = Sale(cfg, impl="fused"), O.Oracle(cfg)
+    g, o = Sale(cfg), O.Oracle(cfg)
     vol = o.get("MASS")
     for f, v in state(cfg, vol).items():
         g.set(f, v)

@@ -59,7 +59,7 @@ def test_gpu_steinberg_vs_oracle(rezone):
     from paper_2209_01983_b200.configs import sedov
     from paper_2209_01983_b200.sale import Sale
     cfg = sedov((37, 11, 14), rezone)
-    g, o = Sale(cfg, impl="fused", local_slabs=2), O.Oracle(cfg)
+    g, o = Sale(cfg, local_slabs=2), O.Oracle(cfg)
     assert g.step(12) == o.step(12)
     prm = P(G0=0.43, GP=1.7, GT=0.3, cv=0.8, rho0=1.1, T0=0.05, Y0=0.2, Ymax=0.9, beta=3.0, n=0.5)
     eps = np.random.Generator(np.random.PCG64(7)).uniform(0.0, 2.0, size=g.cell_shape)
@@ -111,7 +111,7 @@ def test_gpu_material_steinberg_vs_oracle(rezone):
     from paper_2209_01983_b200.configs import sedov
     from paper_2209_01983_b200.sale import Sale
     cfg = sedov((23, 9, 14), rezone, nmat=3, mat_gamma=[1.4, 5.0 / 3.0, 1.2])
-    g, o = Sale(cfg, impl="fused", local_slabs=2), O.Oracle(cfg)
+    g, o = Sale(cfg, local_slabs=2), O.Oracle(cfg)
     for f, v in inputs.material_mix(cfg, 8, o.get("MASS"), o.get("MAT_E0")).items():
         g.set(f, v)
         o.set(f, v)
