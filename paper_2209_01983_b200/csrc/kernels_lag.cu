@@ -2,18 +2,16 @@
 // §8(c) c.3 and c.5, with the readings HG and DT-Q of DESIGN.md §3) for both
 // rezoning modes, as z-marching kernels.
 //
-//   ke_state   (Euler, before k_begin): per cell of the cycle-start state the cell
-//              state -- sigma = 0.25 (pf + q), the uncapped hourglass coefficient nu_u,
-//              each material's stress -- and the c.5 dt candidate (DT-Q signal speed).
-//   k_state_lag (Lagrange, one thread per cell): the same from x, u of a buffer; run
-//              at the start of sale_step and for ghost cell planes after an exchange.
+//   kl_state / ke_state (before the cycle's k_begin): per cell of the cycle-start
+//              state the cell state -- sigma = 0.25 (pf + q), the uncapped hourglass
+//              coefficient nu_u, each material's stress -- and the c.5 dt candidate
+//              (DT-Q signal speed); Lagrange from x, Euler from the target tables.
 //   kc_force   : S1 face area vectors at t^n (Lagrange; Euler: target tables), the
 //              hourglass mode amplitudes of u^n, per cell the eight corner forces
 //              (sigma C_h + f_h) staged in shared memory, the nodal force and mass
 //              gather in the fixed order of c.2, kinematics + BC (S5, S6).
 //   kc_energy  : S7 geometry at t^{n+1} (V', tangle check), the compatible energy
-//              update with the hourglass work; Lagrange: also the cell state and the
-//              dt candidate of the new state (so the next cycle starts from them).
+//              update with the hourglass work.
 //
 // The node gather is split across z-steps: cell plane k contributes to node plane k
 // (its corners c = 0) and starts node plane k+1 (corners c = 1); the running sums
@@ -27,6 +25,17 @@
 #include <mutex>
 
 #include "sale_mesh.cuh"
+
+// resident CTAs per SM the register budgets are sized for (compile-time tuning knobs)
+#ifndef SALE_MB_ENERGY_L
+#define SALE_MB_ENERGY_L 1
+#endif
+#ifndef SALE_MB_FORCE
+#define SALE_MB_FORCE 2
+#endif
+#ifndef SALE_MB_STATE
+#define SALE_MB_STATE 2
+#endif
 
 namespace sale {
 
@@ -115,59 +124,201 @@ __device__ __forceinline__ void cell_state(const Slab& s, const Phys& p, double 
 }
 
 // ============================================================================
-// k_state_lag: one thread per cell of cell planes [kc0, kc1), buffer `cur`
+// kl_state (Lagrange): z-march over cell planes [kc0, kc1) of the state in buffer
+// `cur` (x, u, m, e).  Per column the x- and y-faces anchored there (centroid,
+// face-average velocity, s) and the z-face of the next node plane, the x' edge
+// lengths; per cell V (c.2), the EoS, the axis jumps (c.3 step 2), q, sigma, nu_u,
+// and for owned cells the c.5 dt candidate with the DT-Q signal speed.  A 32 x NW
+// tile yields 31 x (NW-1) cells.
 // ============================================================================
-template <int NM>
-__global__ void __launch_bounds__(128) k_state_lag(Slab s, Phys p, int cur, int kc0, int kc1, int key_on, int gate)
-{
-    if (gate && !s.st->active) return;
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long key = KEY_NONE;
-    if (t < s.pc * (long long)(kc1 - kc0)) {
-        const int k = kc0 + (int)(t / s.pc);
-        const long long r = t % s.pc;
-        const int j = (int)(r / p.nx), i = (int)(r % p.nx);
-        D3 N[8], U[8], A[6], Xb[6];
-        double sv[6];
-        load_hex_pos<false>(s, p, cur, i, j, k, N);
-        load_hex3(s, p, s.u[cur], i, j, k, U);
-        hex_faces(N, A, Xb, sv);
-        const double V = vol_from_s(sv);
-        double Lsum;
-        const double du = hex_du(Xb, U, Lsum);
-        const long long c = cidx(s, p, i, j, k);
-        const double m = s.m[0][c];
-        double fr[MAX_MAT], mr[MAX_MAT], er[MAX_MAT], sg[MAX_MAT];
+template <int NW, int NM>
+struct StateLagCTA {
+    static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
+    __host__ __device__ static constexpr int oN(int par, int c) { return (par * 7 + c) * PL; }  // x(3) u(3) |u|^2
+    static constexpr int OXB = 14 * PL;   // Xbar of the x-face (3), y-face (3)
+    static constexpr int OUB = 20 * PL;   // Ubar of the x-face (3), y-face (3)
+    static constexpr int OS = 26 * PL;    // s of the x-face, y-face
+    static constexpr int OED = 28 * PL;   // edge^2 minima: x-edges (2 planes), y-edges, z-edge
+    static constexpr int WORDS = 31 * PL + 2 * PAD;
+
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, za, zb;
+    long long nbc, cbc, cb;
+    bool out_cell;
+    D3 px, pu;
+    double pm, pe;
+    double pmf[NM > 0 ? NM : 1], pmm[NM > 0 ? NM : 1], pme[NM > 0 ? NM : 1];
+    D3 zXb, zUb;          // z-face at node plane kz: centroid, face-average u
+    double zs, zex, zey;  // its s and the x / y edges at (i, j) of that plane
+    unsigned long long key;
+
+    __device__ __forceinline__ StateLagCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kc0, int kc1,
+                                           int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + PAD + iy * FW + ix;
+        i = blockIdx.x * TX + ix;
+        j = blockIdx.y * TY + iy;
+        za = kc0 + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kc1 - 1 ? za + zchunk - 1 : kc1 - 1;
+        const int in = i < p.nx ? i : p.nx, jn = j < p.ny ? j : p.ny;
+        const int ic = i < p.nx ? i : p.nx - 1, jc = j < p.ny ? j : p.ny - 1;
+        nbc = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
+        cbc = (long long)ic + (long long)p.nx * (jc - (long long)p.ny * s.kb);
+        cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
+        out_cell = i < p.nx && j < p.ny && ix < TX && iy < TY;
+        key = KEY_NONE;
+    }
+    __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
+    {
+        const int kn = clampi(k, s.kb, s.kb + s.nzn - 1);
+        const long long n = nbc + (long long)kn * s.pn;
+        px = ld3(s.x[cur], n);
+        pu = ld3(s.u[cur], n);
+        const int kc = clampi(k - 1, s.kb, s.kb + s.nzc - 1);
+        const long long c = cbc + (long long)kc * s.pc;
+        pm = s.m[0][c];
+        pe = s.e[cur][c];
 #pragma unroll
         for (int a = 0; a < NM; ++a) {
-            fr[a] = s.mf[0][c + a * mat_stride(s)];
-            mr[a] = s.mm[0][c + a * mat_stride(s)];
-            er[a] = s.me[cur][c + a * mat_stride(s)];
+            pmf[a] = s.mf[0][c + a * mat_stride(s)];
+            pmm[a] = s.mm[0][c + a * mat_stride(s)];
+            pme[a] = s.me[cur][c + a * mat_stride(s)];
         }
-        double sig, nu_u, cs, cq;
-        cell_state<NM>(s, p, m, NM > 0 ? 0.0 : s.e[cur][c], fr, mr, er, V, du, Lsum, sig, nu_u, cs, cq, sg);
-        s.sig[c] = sig;
-        s.hnu[c] = nu_u;
-#pragma unroll
-        for (int a = 0; a < NM; ++a) s.sgm[c + a * mat_stride(s)] = sg[a];
-        if (key_on && k >= s.k0 && k < s.k1)
-            key = dt_key(dt_cell(p.cfl, hex_min_edge2(N), hex_max_speed2(U), cs, cq));
     }
-    if (key_on) block_min_atomic(key, &s.st->cand_key);
-}
+    template <int PAR>
+    __device__ __forceinline__ void put()
+    {
+        st3s(me, oN(PAR, 0), PL, px);
+        st3s(me, oN(PAR, 3), PL, pu);
+        me[oN(PAR, 6)] = speed2(pu);
+    }
+    template <int PAR>
+    __device__ __forceinline__ D3 X(int off) const { return ld3s(me + off, oN(PAR, 0), PL); }
+    template <int PAR>
+    __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oN(PAR, 3), PL); }
+    template <int PAR>
+    __device__ __forceinline__ double V2(int off) const { return me[off + oN(PAR, 6)]; }
+    // the z-face at this column of node plane B: (i,j) (i+1,j) (i+1,j+1) (i,j+1)
+    template <int B>
+    __device__ __forceinline__ void zface(D3& Xb, D3& Ub, double& sz, double& ex, double& ey) const
+    {
+        const D3 T0 = X<B>(0), T1 = X<B>(1), T2 = X<B>(FW + 1), T3 = X<B>(FW);
+        Xb = avg4(T0, T1, T2, T3);
+        sz = face_s(Xb, face_area(T0, T1, T2, T3));
+        Ub = avg4(U<B>(0), U<B>(1), U<B>(FW + 1), U<B>(FW));
+        ex = len2(T0, T1);
+        ey = len2(T0, T3);
+    }
 
-int launch_state_lag(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int key, int gate, Stream st)
+    template <int B0>
+    __device__ __forceinline__ void step(int kz)
+    {
+        constexpr int B1 = B0 ^ 1;
+        put<B1>();
+        const double m = pm, e = pe;
+        double cmf[NM > 0 ? NM : 1], cmm[NM > 0 ? NM : 1], cme[NM > 0 ? NM : 1];
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            cmf[a] = pmf[a];
+            cmm[a] = pmm[a];
+            cme[a] = pme[a];
+        }
+        if (kz < zb) fetch(kz + 2);
+        __syncthreads();
+        // ---- the faces anchored at this column
+        D3 zXbn, zUbn;
+        double zsn, zexn, zeyn;
+        zface<B1>(zXbn, zUbn, zsn, zexn, zeyn);
+        {
+            // x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
+            const D3 Q0 = X<B0>(0), Q1 = X<B0>(FW), Q2 = X<B1>(FW), Q3 = X<B1>(0);
+            const D3 Xbx = avg4(Q0, Q1, Q2, Q3);
+            me[OS] = face_s(Xbx, face_area(Q0, Q1, Q2, Q3));
+            st3s(me, OXB, PL, Xbx);
+            st3s(me, OUB, PL, avg4(U<B0>(0), U<B0>(FW), U<B1>(FW), U<B1>(0)));
+            // y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
+            const D3 R2 = X<B1>(1), R3 = X<B0>(1);
+            const D3 Xby = avg4(Q0, Q3, R2, R3);
+            me[OS + PL] = face_s(Xby, face_area(Q0, Q3, R2, R3));
+            st3s(me, OXB + 3 * PL, PL, Xby);
+            st3s(me, OUB + 3 * PL, PL, avg4(U<B0>(0), U<B1>(0), U<B1>(1), U<B0>(1)));
+            me[OED] = dmin(zex, zexn);        // x-edges (i,j) on planes kz, kz+1
+            me[OED + PL] = dmin(zey, zeyn);   // y-edges
+            me[OED + 2 * PL] = len2(Q0, Q3);  // z-edge (i,j): kz -> kz+1
+        }
+        double v2 = V2<B0>(0);  // max node speed^2 in corner order (before the barrier)
+        v2 = dmax(v2, V2<B0>(1));
+        v2 = dmax(v2, V2<B0>(FW));
+        v2 = dmax(v2, V2<B0>(FW + 1));
+        v2 = dmax(v2, V2<B1>(0));
+        v2 = dmax(v2, V2<B1>(1));
+        v2 = dmax(v2, V2<B1>(FW));
+        v2 = dmax(v2, V2<B1>(FW + 1));
+        __syncthreads();
+        // ---- cell (i,j,kz)
+        if (out_cell && kz >= 0 && kz < p.nz) {
+            double sv[6] = {me[OS], me[1 + OS], me[OS + PL], me[FW + OS + PL], zs, zsn};
+            const double V = vol_from_s(sv);
+            double Lx, Ly, Lz;
+            const double dx =
+                axis_jump_L(ld3s(me, OXB, PL), ld3s(me + 1, OXB, PL), ld3s(me, OUB, PL), ld3s(me + 1, OUB, PL), Lx);
+            const double dy = axis_jump_L(ld3s(me, OXB + 3 * PL, PL), ld3s(me + FW, OXB + 3 * PL, PL),
+                                          ld3s(me, OUB + 3 * PL, PL), ld3s(me + FW, OUB + 3 * PL, PL), Ly);
+            const double dz = axis_jump_L(zXb, zXbn, zUb, zUbn, Lz);
+            const double du = dmin(dmin(dx, dy), dz);
+            double sig, nu_u, cs, cq, sg[MAX_MAT];
+            cell_state<NM>(s, p, m, e, cmf, cmm, cme, V, du, (Lx + Ly) + Lz, sig, nu_u, cs, cq, sg);
+            const long long c = cb + (long long)kz * s.pc;
+            s.sig[c] = sig;
+            s.hnu[c] = nu_u;
+#pragma unroll
+            for (int a = 0; a < NM; ++a) s.sgm[c + a * mat_stride(s)] = sg[a];
+            if (kz >= s.k0 && kz < s.k1) {
+                double l2 = dmin(dmin(me[OED], me[FW + OED]), dmin(me[OED + PL], me[1 + OED + PL]));
+                l2 = dmin(l2, dmin(dmin(me[OED + 2 * PL], me[1 + OED + 2 * PL]),
+                                   dmin(me[FW + OED + 2 * PL], me[FW + 1 + OED + 2 * PL])));
+                const unsigned long long kk = dt_key(dt_cell(p.cfl, l2, v2, cs, cq));
+                key = kk < key ? kk : key;
+            }
+        }
+        zXb = zXbn;
+        zUb = zUbn;
+        zs = zsn;
+        zex = zexn;
+        zey = zeyn;
+        __syncthreads();
+    }
+
+    __device__ __forceinline__ void run()
+    {
+        fetch(za);
+        if (za & 1) put<1>();
+        else put<0>();
+        fetch(za + 1);
+        __syncthreads();
+        if (za & 1) zface<1>(zXb, zUb, zs, zex, zey);
+        else zface<0>(zXb, zUb, zs, zex, zey);
+        for (int kz = za; kz <= zb; ++kz) {
+            if (kz & 1) step<1>(kz);
+            else step<0>(kz);
+        }
+        block_min_atomic(key, &s.st->cand_key);
+    }
+};
+
+// gate = 0 for the first cycle of a sale_step call (DevState.active is still 0 there)
+template <int NW, int NM>
+__global__ void __launch_bounds__(FW * NW, SALE_MB_STATE) kl_state(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk, int gate)
 {
-    kc0 = imax_h(kc0, 0);
-    kc1 = imin_h(kc1, p.nz);
-    if (kc1 <= kc0) return 0;
-    const unsigned g = grid_for(s.pc * (long long)(kc1 - kc0), 128);
-    by_nmat(s.nmat, [&](auto nm) {
-        constexpr int NM = decltype(nm)::value;
-        k_state_lag<NM><<<g, 128, 0, (cudaStream_t)st>>>(s, p, cur, kc0, kc1, key, gate);
-        note_launch();
-    });
-    return 1;
+    if (gate && !s.st->active) return;
+    extern __shared__ double smem[];
+    StateLagCTA<NW, NM> c(s, p, cur, smem, kc0, kc1, zchunk);
+    c.run();
 }
 
 // ============================================================================
@@ -568,7 +719,7 @@ struct ForceCTA {
 };
 
 template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, 2) kc_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
+__global__ void __launch_bounds__(FW * NW, SALE_MB_FORCE) kc_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];
@@ -579,27 +730,20 @@ __global__ void __launch_bounds__(FW * NW, 2) kc_force(Slab s, Phys p, int cur, 
 // ============================================================================
 // kc_energy: cell planes [kc0, kc1) in z-chunks; thread (ix, iy) owns column
 // (i, j) = (bx*TX + ix, by*TY + iy) and its cell when ix < FW-1, iy < NW-1.
-//   Lagrange: stages x^n, x', u^n, u', |u'|^2; per column the t^n face areas, the
-//   moved faces (A', Xbar', s', Ubar'), the x' edge lengths; per cell W, the
-//   hourglass work, e', V', and the next state's EoS, jumps, sigma, nu_u and dt key.
-//   Euler: stages x' (formed from u'), u^n and ubar; areas from the tables.
+//   Lagrange: stages x^n, x', u^n, u'; per column the t^n face areas and the moved
+//   faces' s'; per cell W, the hourglass work, e', V' and the tangle check.
+//   Euler: stages x' (formed from u'), u^n and ubar; areas from the tables; also
+//   writes V' and the moved-face s' the sweep reads.
 // ============================================================================
 template <bool EULER, int NW, int NM>
 struct EnergyCTA {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
-    // node words: Lagrange x^n(3) x'(3) u^n(3) u'(3) |u'|^2; Euler x'(3) u^n(3) ubar(3)
-    static constexpr int NNW = EULER ? 9 : 13;
+    // node words: Lagrange x^n(3) x'(3) u^n(3) u'(3); Euler x'(3) u^n(3) ubar(3)
+    static constexpr int NNW = EULER ? 9 : 12;
     __host__ __device__ static constexpr int oN(int par, int c) { return (par * NNW + c) * PL; }
-    static constexpr int OF = 2 * NNW * PL;
-    // per-column face words: s' of the x/y face (2); Lagrange: A^n x/y (6), Xbar' x/y (6),
-    // Ubar' x/y (6), edge minima (3)
-    static constexpr int NFW = EULER ? 2 : 23;
-    static constexpr int OS = OF;                       // s'x, s'y
-    static constexpr int OAN = OF + 2 * PL;             // A^n x (3), y (3)
-    static constexpr int OXB = OAN + 6 * PL;            // Xbar' x (3), y (3)
-    static constexpr int OUB = OXB + 6 * PL;            // Ubar' x (3), y (3)
-    static constexpr int OED = OUB + 6 * PL;            // edge^2 minima: x, y, z
-    static constexpr int WORDS = OF + NFW * PL + 2 * PAD;
+    static constexpr int OS = 2 * NNW * PL;   // s' of the x-face, y-face
+    static constexpr int OAN = OS + 2 * PL;   // Lagrange: A^n of the x-face (3), y-face (3)
+    static constexpr int WORDS = OAN + (EULER ? 0 : 6) * PL + 2 * PAD;
 
     const Slab& s;
     const Phys& p;
@@ -614,10 +758,9 @@ struct EnergyCTA {
     double fm, fe, fsig, fnu, fz, fax, fay;
     double rf[NM > 0 ? NM : 1], rm[NM > 0 ? NM : 1], re[NM > 0 ? NM : 1], rs[NM > 0 ? NM : 1];
     double xcol, ycol, az;
-    // carried z-face state of node plane kz
-    D3 zA, zXb, zUb;
-    double zs, zex, zey;
-    unsigned long long key;
+    // carried z-face of node plane kz: t^n area (Lagrange), s' of the moved face
+    D3 zA;
+    double zs;
 
     __device__ __forceinline__ EnergyCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kc0, int kc1,
                                          int zchunk)
@@ -645,7 +788,6 @@ struct EnergyCTA {
             ycol = s.Yt[jn];
             az = s.TAz[2][(long long)jc * p.nx + ic];
         }
-        key = KEY_NONE;
     }
 
     __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
@@ -694,7 +836,6 @@ struct EnergyCTA {
             st3s(me, oN(PAR, 3), PL, fx1);
             st3s(me, oN(PAR, 6), PL, fu);
             st3s(me, oN(PAR, 9), PL, fu1);
-            me[oN(PAR, 12)] = speed2(fu1);
         }
     }
     template <int PAR>
@@ -704,30 +845,19 @@ struct EnergyCTA {
     template <int PAR>
     __device__ __forceinline__ D3 Un(int off) const { return ld3s(me + off, oN(PAR, EULER ? 3 : 6), PL); }
     template <int PAR>
-    __device__ __forceinline__ D3 U1(int off) const { return ld3s(me + off, oN(PAR, 9), PL); }
-    template <int PAR>
     __device__ __forceinline__ D3 Ub(int off) const  // ubar = 0.5 (u + u')
     {
         if constexpr (EULER) return ld3s(me + off, oN(PAR, 6), PL);
-        else return scl(0.5, add(Un<PAR>(off), U1<PAR>(off)));
+        else return scl(0.5, add(Un<PAR>(off), ld3s(me + off, oN(PAR, 9), PL)));
     }
-    template <int PAR>
-    __device__ __forceinline__ double V2(int off) const { return me[off + oN(PAR, 12)]; }
 
-    // the z-face at this column of node plane B: t^n area, and the moved face's s',
-    // centroid, face-average u' and the x' edges along x / y (Lagrange); Euler: s'
+    // the z-face at this column of node plane B: s' of the moved face, t^n area (Lagrange)
     template <int B>
-    __device__ __forceinline__ void zstate(D3& A, D3& Xb, D3& Ub1, double& sz, double& ex, double& ey) const
+    __device__ __forceinline__ void zstate(D3& A, double& sz) const
     {
         const D3 T0 = X1<B>(0), T1 = X1<B>(1), T2 = X1<B>(FW + 1), T3 = X1<B>(FW);
-        Xb = avg4(T0, T1, T2, T3);
-        sz = face_s(Xb, face_area(T0, T1, T2, T3));
-        if constexpr (!EULER) {
-            A = face_area(Xn<B>(0), Xn<B>(1), Xn<B>(FW + 1), Xn<B>(FW));
-            Ub1 = avg4(U1<B>(0), U1<B>(1), U1<B>(FW + 1), U1<B>(FW));
-            ex = len2(T0, T1);
-            ey = len2(T0, T3);
-        }
+        sz = face_s(avg4(T0, T1, T2, T3), face_area(T0, T1, T2, T3));
+        if constexpr (!EULER) A = face_area(Xn<B>(0), Xn<B>(1), Xn<B>(FW + 1), Xn<B>(FW));
     }
 
     template <int B0>
@@ -748,28 +878,19 @@ struct EnergyCTA {
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
         // ---- P2: faces anchored at this column
-        D3 zAn, zXbn, zUbn;
-        double zsn, zexn, zeyn;
-        zstate<B1>(zAn, zXbn, zUbn, zsn, zexn, zeyn);
+        D3 zAn;
+        double zsn;
+        zstate<B1>(zAn, zsn);
         {
             // moved x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
             const D3 Q0 = X1<B0>(0), Q1 = X1<B0>(FW), Q2 = X1<B1>(FW), Q3 = X1<B1>(0);
-            const D3 Xbx = avg4(Q0, Q1, Q2, Q3);
-            me[OS] = face_s(Xbx, face_area(Q0, Q1, Q2, Q3));
+            me[OS] = face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
             // moved y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
             const D3 R2 = X1<B1>(1), R3 = X1<B0>(1);
-            const D3 Xby = avg4(Q0, Q3, R2, R3);
-            me[OS + PL] = face_s(Xby, face_area(Q0, Q3, R2, R3));
+            me[OS + PL] = face_s(avg4(Q0, Q3, R2, R3), face_area(Q0, Q3, R2, R3));
             if constexpr (!EULER) {
                 st3s(me, OAN, PL, face_area(Xn<B0>(0), Xn<B0>(FW), Xn<B1>(FW), Xn<B1>(0)));
                 st3s(me, OAN + 3 * PL, PL, face_area(Xn<B0>(0), Xn<B1>(0), Xn<B1>(1), Xn<B0>(1)));
-                st3s(me, OXB, PL, Xbx);
-                st3s(me, OXB + 3 * PL, PL, Xby);
-                st3s(me, OUB, PL, avg4(U1<B0>(0), U1<B0>(FW), U1<B1>(FW), U1<B1>(0)));
-                st3s(me, OUB + 3 * PL, PL, avg4(U1<B0>(0), U1<B1>(0), U1<B1>(1), U1<B0>(1)));
-                me[OED] = dmin(zex, zexn);          // x-edges (i,j) on planes kz, kz+1
-                me[OED + PL] = dmin(zey, zeyn);     // y-edges
-                me[OED + 2 * PL] = len2(Q0, Q3);    // z-edge (i,j): kz -> kz+1
             } else if (own_col) {
                 // s' of the faces anchored at node (i,j,kz), for the sweep's swept volumes
                 const long long n = nb + (long long)kz * s.pn;
@@ -784,8 +905,7 @@ struct EnergyCTA {
             const long long cc = cb + (long long)kz * s.pc;
             double sv[6] = {me[OS], me[1 + OS], me[OS + PL], me[FW + OS + PL], zs, zsn};
             const double V1 = vol_from_s(sv);
-            const bool owned = kz >= s.k0 && kz < s.k1;
-            if (owned && !(V1 > 0.0))
+            if (kz >= s.k0 && kz < s.k1 && !(V1 > 0.0))
                 atomicMin(&s.st->err_key, (ERR_ORDER_TANGLED << 48) | (unsigned long long)gcell(p, i, j, kz));
             // hourglass modes of u^n and the capped coefficient
             D3 g[4];
@@ -818,59 +938,24 @@ struct EnergyCTA {
 #undef SALE_WH
             }
             // compatible energy with the hourglass work (HG); materials: MM4 share + HG heat
-            double e1 = 0.0, e1k[NM > 0 ? NM : 1];
             if constexpr (NM > 0) {
 #pragma unroll
                 for (int a = 0; a < NM; ++a) {
-                    e1k[a] = (cf[a] > 0.0 && cm[a] > 0.0) ? ce[a] - ddiv((((cs_[a] * W) + Wh) * dt) * cf[a], cm[a])
-                                                         : ce[a];
-                    if (EULER) s.e1m[cc + a * mat_stride(s)] = e1k[a];
-                    else s.me[cur ^ 1][cc + a * mat_stride(s)] = e1k[a];
+                    const double e1k = (cf[a] > 0.0 && cm[a] > 0.0)
+                                           ? ce[a] - ddiv((((cs_[a] * W) + Wh) * dt) * cf[a], cm[a])
+                                           : ce[a];
+                    if (EULER) s.e1m[cc + a * mat_stride(s)] = e1k;
+                    else s.me[cur ^ 1][cc + a * mat_stride(s)] = e1k;
                 }
             } else {
-                e1 = e - ddiv(((sig * W) + Wh) * dt, m);
+                const double e1 = e - ddiv(((sig * W) + Wh) * dt, m);
                 if (EULER) s.e1[cc] = e1;
                 else s.e[cur ^ 1][cc] = e1;
             }
-            if constexpr (EULER) {
-                s.V1[cc] = V1;
-            } else {
-                // the next cycle's cell state and the c.5 dt candidate of the new state
-                // (x', u', m, e'); every cell of the launch is owned
-                double Lx, Ly, Lz;
-                const double dx = axis_jump_L(ld3s(me, OXB, PL), ld3s(me + 1, OXB, PL), ld3s(me, OUB, PL),
-                                              ld3s(me + 1, OUB, PL), Lx);
-                const double dy = axis_jump_L(ld3s(me, OXB + 3 * PL, PL), ld3s(me + FW, OXB + 3 * PL, PL),
-                                              ld3s(me, OUB + 3 * PL, PL), ld3s(me + FW, OUB + 3 * PL, PL), Ly);
-                const double dz = axis_jump_L(zXb, zXbn, zUb, zUbn, Lz);
-                const double du = dmin(dmin(dx, dy), dz);
-                double sg2, nu2, cs2, cq2, sgk[MAX_MAT];
-                cell_state<NM>(s, p, m, e1, cf, cm, e1k, V1, du, (Lx + Ly) + Lz, sg2, nu2, cs2, cq2, sgk);
-                s.sig[cc] = sg2;
-                s.hnu[cc] = nu2;
-#pragma unroll
-                for (int a = 0; a < NM; ++a) s.sgm[cc + a * mat_stride(s)] = sgk[a];
-                double l2 = dmin(dmin(me[OED], me[FW + OED]), dmin(me[OED + PL], me[1 + OED + PL]));
-                l2 = dmin(l2, dmin(dmin(me[OED + 2 * PL], me[1 + OED + 2 * PL]),
-                                   dmin(me[FW + OED + 2 * PL], me[FW + 1 + OED + 2 * PL])));
-                double v2 = V2<B0>(0);
-                v2 = dmax(v2, V2<B0>(1));
-                v2 = dmax(v2, V2<B0>(FW));
-                v2 = dmax(v2, V2<B0>(FW + 1));
-                v2 = dmax(v2, V2<B1>(0));
-                v2 = dmax(v2, V2<B1>(1));
-                v2 = dmax(v2, V2<B1>(FW));
-                v2 = dmax(v2, V2<B1>(FW + 1));
-                const unsigned long long kk = dt_key(dt_cell(p.cfl, l2, v2, cs2, cq2));
-                key = kk < key ? kk : key;
-            }
+            if (EULER) s.V1[cc] = V1;
         }
         zA = zAn;
-        zXb = zXbn;
-        zUb = zUbn;
         zs = zsn;
-        zex = zexn;
-        zey = zeyn;
         __syncthreads();
     }
 
@@ -881,18 +966,17 @@ struct EnergyCTA {
         else put<0>();
         fetch(za + 1);
         __syncthreads();
-        if (za & 1) zstate<1>(zA, zXb, zUb, zs, zex, zey);
-        else zstate<0>(zA, zXb, zUb, zs, zex, zey);
+        if (za & 1) zstate<1>(zA, zs);
+        else zstate<0>(zA, zs);
         for (int kz = za; kz <= zb; ++kz) {
             if (kz & 1) step<1>(kz);
             else step<0>(kz);
         }
-        if (!EULER) block_min_atomic(key, &s.st->cand_key);
     }
 };
 
 template <bool EULER, int NW, int NM>
-__global__ void __launch_bounds__(FW * NW, 2) kc_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
+__global__ void __launch_bounds__(FW * NW, EULER ? 2 : SALE_MB_ENERGY_L) kc_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];
@@ -904,7 +988,17 @@ __global__ void __launch_bounds__(FW * NW, 2) kc_energy(Slab s, Phys p, int cur,
 // launchers
 // ============================================================================
 namespace {
-constexpr int NW_STATE = 8, NW_FORCE = 8, NW_ENERGY = 8;
+// warp rows per CTA (compile-time tuning knobs; scripts/build_probe.sh -D... for A/B runs)
+#ifndef SALE_NW_STATE
+#define SALE_NW_STATE 8
+#endif
+#ifndef SALE_NW_FORCE
+#define SALE_NW_FORCE 8
+#endif
+#ifndef SALE_NW_ENERGY
+#define SALE_NW_ENERGY 8
+#endif
+constexpr int NW_STATE = SALE_NW_STATE, NW_FORCE = SALE_NW_FORCE, NW_ENERGY = SALE_NW_ENERGY;
 
 // Euler: node planes the Lagrangian phase updates (owned + the ghost region the remap
 // reads), and the cell planes whose state the force gather needs
@@ -915,21 +1009,31 @@ inline void euler_ranges(const Slab& s, const Phys& p, int& kn0, int& kn1)
 }
 }  // namespace
 
-int launch_state_euler(const Slab& s, const Phys& p, int cur, int gate, Stream st)
+int launch_state(const Slab& s, const Phys& p, int cur, int gate, Stream st)
 {
-    int kn0, kn1;
-    euler_ranges(s, p, kn0, kn1);
-    const int kc0 = imax_h(kn0 - 1, 0), kc1 = imin_h(kn1 + 1, p.nz);
+    int kc0, kc1;
+    if (p.rezone) {
+        int kn0, kn1;
+        euler_ranges(s, p, kn0, kn1);
+        kc0 = imax_h(kn0 - 1, 0);
+        kc1 = imin_h(kn1 + 1, p.nz);
+    } else {  // the cells around the owned node planes [k0, k1]
+        kc0 = imax_h(s.k0 - 1, 0);
+        kc1 = imin_h(s.k1 + 1, p.nz);
+    }
     by_nmat(s.nmat, [&](auto nm) {
         constexpr int NM = decltype(nm)::value;
-        auto kern = ke_state<NW_STATE, NM>;
-        const size_t sm = sizeof(double) * StateEulerCTA<NW_STATE, NM>::WORDS;
-        set_smem(kern, sm);
-        const long long xy = (long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW_STATE - 1);
-        const int zc = zchunk_for(xy, kc1 - kc0, ZCHUNK);
-        dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW_STATE - 1), cdiv(kc1 - kc0, zc));
-        kern<<<grid, dim3(FW, NW_STATE), sm, (cudaStream_t)st>>>(s, p, cur, kc0, kc1, zc, gate);
-        note_launch();
+        auto go = [&](auto kern, size_t words) {
+            const size_t sm = sizeof(double) * words;
+            set_smem(kern, sm);
+            const long long xy = (long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW_STATE - 1);
+            const int zc = zchunk_for(xy, kc1 - kc0, ZCHUNK);
+            dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW_STATE - 1), cdiv(kc1 - kc0, zc));
+            kern<<<grid, dim3(FW, NW_STATE), sm, (cudaStream_t)st>>>(s, p, cur, kc0, kc1, zc, gate);
+            note_launch();
+        };
+        if (p.rezone) go(ke_state<NW_STATE, NM>, StateEulerCTA<NW_STATE, NM>::WORDS);
+        else go(kl_state<NW_STATE, NM>, StateLagCTA<NW_STATE, NM>::WORDS);
     });
     return 1;
 }

@@ -6,7 +6,7 @@
 // moves each material's mass, volume and energy from the donor cell.
 //
 // The cycle runs on the z-march kernels with a material axis (kernels_lag.cu
-// ke_state / k_state_lag / kc_energy and kernels_remap.cu kr_sweep, each with NM
+// kl_state / ke_state / kc_energy and kernels_remap.cu kr_sweep, each with NM
 // materials as a template parameter) and the single-material kernels that read
 // sigma and the cell totals only (kc_force, kn_update).  This file holds the remap
 // sequence, the per-material flux + cell update (k_mat_flux) and init / mass

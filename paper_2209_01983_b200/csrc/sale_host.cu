@@ -489,27 +489,22 @@ int reduce_keys(sale_ctx* c)
                       "dt allreduce");
 }
 
-// one cycle reading buffers [b]; first = the first cycle of a sale_step call (Euler:
-// its ke_state runs ungated, DevState.active being still 0 then).
-//   Euler:    ke_state (cell state + dt candidate of the cycle-start state) -> dt /
-//             error allreduce -> k_begin -> kc_force -> kc_energy -> remap -> halo
-//   Lagrange: k_begin -> kc_force -> kc_energy (+ the new state's cell state and dt
-//             candidate) -> halo -> ghost cell state (more than one slab) -> allreduce
+// one cycle reading buffers [b]; first = the first cycle of a sale_step call (its
+// state pass runs ungated, DevState.active being still 0 then).  Both modes:
+//   kl_state / ke_state (cell state + dt candidate of the cycle-start state) -> dt /
+//   error allreduce -> k_begin (commit the previous cycle, finalise dt) -> kc_force
+//   -> kc_energy -> [Euler: remap] -> halo exchange of the new state
 int enqueue_one_cycle(sale_ctx* c, int b, bool first)
 {
     int rc;
     sale::Stream st = (sale::Stream)c->stream;
     const bool euler = c->prm.rezone == SALE_EULER;
-    const bool multi = c->slabs.size() > 1 || c->prm.nranks > 1;
-    int pr;
-    if (euler) {
-        pr = prof_open(c, SALE_K_LAGRANGE);
-        for (auto& s : c->slabs) c->launches += sale::launch_state_euler(s, c->phys, b, first ? 0 : 1, st);
-        prof_close(c, pr);
-        pr = prof_open(c, SALE_K_HALO);
-        if ((rc = reduce_keys(c))) return rc;
-        prof_close(c, pr);
-    }
+    int pr = prof_open(c, SALE_K_LAGRANGE);
+    for (auto& s : c->slabs) c->launches += sale::launch_state(s, c->phys, b, first ? 0 : 1, st);
+    prof_close(c, pr);
+    pr = prof_open(c, SALE_K_HALO);
+    if ((rc = reduce_keys(c))) return rc;
+    prof_close(c, pr);
     pr = prof_open(c, SALE_K_BEGIN);
     c->launches += sale::launch_begin(c->dstate, c->phys, st);
     prof_close(c, pr);
@@ -527,12 +522,6 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first)
     if ((rc = launch_check(c))) return rc;
     pr = prof_open(c, SALE_K_HALO);
     if ((rc = exchange(c, b ^ 1, false))) return rc;
-    if (!euler && multi)  // the cell state of the ghost cell planes from the exchanged state
-        for (auto& s : c->slabs) {
-            c->launches += sale::launch_state_lag(s, c->phys, b ^ 1, s.k0 - 1, s.k0, 0, 1, st);
-            c->launches += sale::launch_state_lag(s, c->phys, b ^ 1, s.k1, s.k1 + 1, 0, 1, st);
-        }
-    if (!euler && (rc = reduce_keys(c))) return rc;
     prof_close(c, pr);
     return launch_check(c);
 }
@@ -595,19 +584,14 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
     int rc;
     int b = c->cur_enq;
     sale::Stream st = (sale::Stream)c->stream;
-    const bool euler = c->prm.rezone == SALE_EULER;
-    // prologue: ghost planes of the current state; Lagrange: the cell state of every
-    // local cell and the dt candidate of the owned ones (Euler: each cycle's ke_state)
+    // prologue: the ghost planes of the current state (set_field / resume honoured);
+    // each cycle's state pass then forms the cell state and the dt candidate
     int pr = prof_open(c, SALE_K_PROLOGUE);
     c->launches += sale::launch_prep(c->dstate, st);
     if ((rc = exchange(c, b, true))) return rc;
-    if (!euler) {
-        for (auto& s : c->slabs) c->launches += sale::launch_state_lag(s, c->phys, b, s.kb, s.kb + s.nzc, 1, 0, st);
-        if ((rc = reduce_keys(c))) return rc;
-    }
     prof_close(c, pr);
     int n = 0;
-    if (ncycles > 0) {  // the first cycle on the plain path (Euler: ungated ke_state)
+    if (ncycles > 0) {  // the first cycle on the plain path (ungated state pass)
         if ((rc = enqueue_one_cycle(c, b, true))) return rc;
         b ^= 1;
         n = 1;
@@ -624,7 +608,7 @@ int enqueue_cycles(sale_ctx* c, int ncycles)
         if ((rc = enqueue_one_cycle(c, b, false))) return rc;
         b ^= 1;
     }
-    if (euler && ncycles > 0 && (rc = reduce_keys(c))) return rc;  // the last cycle's error key
+    if (ncycles > 0 && (rc = reduce_keys(c))) return rc;  // the last cycle's error key
     c->launches += sale::launch_commit(c->dstate, c->phys, (sale::Stream)c->stream);
     c->cur_enq = b;
     return launch_check(c);

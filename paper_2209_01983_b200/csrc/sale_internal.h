@@ -142,21 +142,16 @@ int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& 
                      double* y, long long mstride, Stream st);
 
 // ---- the cycle (kernels_lag.cu, kernels_remap.cu, kernels_mat.cu) ------------
-// Lagrange: the cell state (sigma, nu_u, material stresses) of buffer `cur` for cell
-// planes [kc0, kc1) (one thread per cell); key = 1 also forms the c.5 dt candidate of
-// the owned cells among them.  Used at the start of sale_step (all local cells) and,
-// with more than one slab, for the ghost cell planes after each cycle's exchange
-// (gate = 1: skipped unless a cycle is in flight).
-int launch_state_lag(const Slab& s, const Phys& p, int cur, int kc0, int kc1, int key, int gate, Stream st);
-// Euler: the cell state and the dt candidate of the cycle-start state, before the
-// cycle's k_begin (gate = 0 for the first cycle of a sale_step call)
-int launch_state_euler(const Slab& s, const Phys& p, int cur, int gate, Stream st);
+// the cell state (sigma, nu_u, material stresses) and the c.5 dt candidate of the
+// cycle-start state in buffer `cur`, before the cycle's k_begin (gate = 0 for the
+// first cycle of a sale_step call, when DevState.active is still 0): every cell the
+// force gather reads (Lagrange: [k0-1, k1]; Euler: the remap's ghost region too)
+int launch_state(const Slab& s, const Phys& p, int cur, int gate, Stream st);
 // S5-S6: corner forces (pressure, viscosity, hourglass) gathered in the fixed order,
 // kinematics + BC.  Lagrange: x', u' into buffer cur^1; Euler: u' into Slab::u1.
 int launch_force(const Slab& s, const Phys& p, int cur, Stream st);
 // S7: V', tangle check, compatible energy with the hourglass work.  Lagrange: e' into
-// buffer cur^1 and the cell state + dt candidate of the new state; Euler: e' (e'_k), V',
-// and the moved-face s' the sweep reads.
+// buffer cur^1; Euler: e' (e'_k), V', and the moved-face s' the sweep reads.
 int launch_energy(const Slab& s, const Phys& p, int cur, Stream st);
 // R1-R4 (kernels_remap.cu; materials: kernels_mat.cu)
 int launch_remap(const Slab& s, const Phys& p, int cur, Stream st);

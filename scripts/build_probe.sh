@@ -1,11 +1,16 @@
 #!/bin/bash
-# build lib/libsale_probe.so with one source recompiled under extra -D flags (timing probes only)
-# usage: scripts/build_probe.sh kernels_fused.cu -DSALE_PROBE_NOLOAD
+# Build abtmp/libsale_<tag>.so with one source recompiled under extra -D flags, for
+# A/B timing runs only (SALE_LIB_PATH=abtmp/libsale_<tag>.so python bench.py ...).
+# usage: scripts/build_probe.sh <tag> kernels_lag.cu -DSALE_NW_FORCE=16 ...
 set -e
-R=/root/repo; SRC=$1; shift
-NCCL=$(python -c 'import nvidia,os;print(os.path.join(nvidia.__path__[0],"nccl"))')
+R=/root/repo; TAG=$1; SRC=$2; shift 2
+NCCL=$(cd $R/paper_2209_01983_b200 && python -c "import build,os; print(os.path.dirname(build.nccl_dirs()[0]))")
 OBJ=$R/paper_2209_01983_b200/lib/obj
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC -I $R/include -I $R/paper_2209_01983_b200/csrc -I $NCCL/include "$@" -c $R/paper_2209_01983_b200/csrc/$SRC -o /tmp/probe_${SRC%.cu}.o
-objs=""; for o in $OBJ/*.o; do b=$(basename $o); [ "$b" = "${SRC%.cu}.o" ] || objs="$objs $o"; done
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/paper_2209_01983_b200/lib/libsale_probe.so $objs /tmp/probe_${SRC%.cu}.o -L $NCCL/lib -l:libnccl.so.2 -Xlinker -rpath,$NCCL/lib
-echo built probe
+mkdir -p $R/abtmp
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 -Xcompiler -fPIC \
+    -I $R/include -I $R/paper_2209_01983_b200/csrc -I $NCCL/include "$@" \
+    -c $R/paper_2209_01983_b200/csrc/$SRC -o /tmp/probe_${TAG}.o
+objs=""; for c in $R/paper_2209_01983_b200/csrc/*.cu; do b=$(basename ${c%.cu}).o; [ "$b" = "${SRC%.cu}.o" ] || objs="$objs $OBJ/$b"; done
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/abtmp/libsale_${TAG}.so $objs /tmp/probe_${TAG}.o \
+    -L $NCCL/lib -l:libnccl.so.2 -Xlinker -rpath,$NCCL/lib
+echo built abtmp/libsale_${TAG}.so
