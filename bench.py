@@ -37,13 +37,14 @@ UNIT = "zone-cycles/s"
 # algorithmic bytes per zone-cycle (state read + written once, fp64)
 ALGO_BYTES = {configs.LAGRANGE: 120.0, configs.EULER: 80.0}
 # algorithmic FP64-pipe instructions per zone-cycle of each kernel
-# class (faces / edges / nodes computed once; an IEEE fp64 div or sqrt = 8 FP64
-# instructions, its fast-path SASS sequence)
-# (Lagrange: the t^n EoS and volume are the previous cycle's t^{n+1} values, evaluated
-# once; Euler: the t^n geometry of the fixed target mesh is loop-invariant and the
-# moved-face s' of S7 are shared with R1 -- DESIGN.md §7)
-ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 661.0, "remap": 0.0},
-             configs.EULER: {"lagrange": 362.0, "remap": 406.0}}
+# class (faces / edges / nodes computed once; a quantity two kernels both evaluate
+# -- the t^n areas, corner vectors, hourglass modes and corner forces the energy
+# kernel re-forms -- counted once; an IEEE fp64 div or sqrt = 8 FP64 instructions,
+# its fast-path SASS sequence).  Lagrange: state 390 + force 405 + energy 230;
+# Euler: state 138 + force 276 + energy 236 (the target geometry is tabled), remap
+# R1-R4 406.
+ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 1025.0, "remap": 0.0},
+             configs.EULER: {"lagrange": 650.0, "remap": 406.0}}
 # kernel name prefixes of each timing class (for the ncu traffic file)
 CLASS_KERNELS = {"lagrange": ("kc_", "ke_state", "k_state"), "remap": ("kr_", "kn_update", "k_mat_flux")}
 REASON_BITS = {"hw_slowdown": "hw_slowdown", "hw_thermal_slowdown": "hw_thermal_slowdown",
@@ -233,6 +234,91 @@ def workload_name(name):
             }.get(name, name)
 
 
+def time_cycles(ctx, cfg, steps, warmup, world, local, barrier, max_over_ranks, S):
+    """W untimed cycles, then K cycles bracketed by barrier + synchronize, CUDA events
+    on the context's stream, kernel-class timing and nvidia-smi clocks (max over ranks)."""
+    import torch
+    stream = ctx.stream
+    rc, done = ctx.step(warmup)
+    if rc or done != warmup:
+        raise RuntimeError(f"warmup failed rc={rc} done={done}: {ctx.last_error()}")
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.2)
+    launches0 = ctx.launches()
+    ctx.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.step_async(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    rc, done = ctx.sync()
+    barrier()
+    clocks = sampler.stop()
+    if rc or done != steps:
+        raise RuntimeError(f"timed run failed rc={rc} done={done}: {ctx.last_error()}")
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = ctx.launches() - launches0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    gcells = cfg["nx"] * cfg["ny"] * cfg["nz"]
+    return {"ms": ms, "launches": launches, "prof": prof, "clocks": clocks,
+            "value": gcells * steps / (ms * 1e-3)}
+
+
+def roofline_of(config_name, mode, prof, ms, steps, local_cells):
+    """The SALE kernels are bound by the FP64 pipe: the roofline ("alu")
+    of the dominant kernel class; the HBM view rides along."""
+    peak, peak_src = peaks()
+    fpk, fpk_src = fp64_peak()
+    dom = max(("lagrange", "remap"), key=lambda k: prof[k][0])
+    dom_ms, dom_n = prof[dom]
+    per_cycle_ms = dom_ms / steps                                  # the class may launch >1 group per cycle
+    fp64_per_cycle = ALGO_FP64[mode][dom] * local_cells            # FP64 instr of the class per cycle
+    achieved_t = fp64_per_cycle / (per_cycle_ms * 1e-3) / 1e12     # T instr/s
+    cyc_fp64 = sum(ALGO_FP64[mode].values()) * local_cells
+    cyc_t = cyc_fp64 / (ms / steps * 1e-3) / 1e12
+    cyc_bytes = ALGO_BYTES[mode] * local_cells
+    cycle_gbs = cyc_bytes / (ms / steps * 1e-3) / 1e9
+    tr_bytes, tr_src = traffic(config_name, dom)
+    return {"bound": "alu", "achieved": achieved_t, "peak": fpk, "unit": "T fp64-instr/s",
+            "frac": achieved_t / fpk, "traffic": tr_bytes, "traffic_unit": "DRAM bytes per cycle of the class",
+            "traffic_source": tr_src, "algo_bytes_per_cycle": ALGO_BYTES[mode] * local_cells,
+            "traffic_bytes_per_zone": (tr_bytes / local_cells) if tr_bytes else None,
+            "kernel": dom, "kernel_launch_groups_per_cycle": dom_n / steps,
+            "kernel_ms_per_cycle": per_cycle_ms, "kernel_share_of_step": dom_ms / ms,
+            "algo_fp64_instr_per_zone": ALGO_FP64[mode][dom], "peak_source": fpk_src,
+            "whole_cycle": {"achieved": cyc_t, "frac": cyc_t / fpk,
+                            "algo_fp64_instr_per_zone": sum(ALGO_FP64[mode].values())},
+            "hbm": {"achieved_gbs": cycle_gbs, "peak_gbs": peak, "frac": cycle_gbs / peak,
+                    "algo_bytes_per_zone_cycle": ALGO_BYTES[mode], "peak_source": peak_src}}
+
+
+def golden_check(name, S):
+    """Run the config's full golden length from the Sedov start (a fresh context) and
+    count the fields whose SHA-256 differs from the oracle's digest (tests/golden/,
+    written by scripts/oracle_digests.py from the oracle only).  None if absent."""
+    import hashlib
+    path = os.path.join(ROOT, "tests", "golden", f"{name}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        g = json.load(f)
+    cfg, _ = configs.config(name)
+    if g.get("params") != cfg:
+        return {"skipped": "golden parameters differ from the config"}
+    ctx = S.Sale(cfg)
+    rc, done = ctx.step(g["requested_cycles"])
+    bad = [f for f, ref in g["fields"].items()
+           if hashlib.sha256(ctx.get(f).ravel().tobytes()).hexdigest() != ref["sha256"]]
+    clk_ok = ctx.clock() == g["clock"]
+    ctx.close()
+    return {"cycles": done, "status": rc, "clock_equal": clk_ok, "fields": len(g["fields"]),
+            "fields_bit_mismatched": len(bad), "mismatched": bad}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -244,6 +330,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-allcore", type=int, default=1, help="also time one oracle per host core (0: off)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the P0-state, C3 and golden-check legs")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -269,7 +356,6 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     ctx = S.Sale(cfg, device=local, rank=rank, nranks=world, nccl_id=nid)
-    stream = ctx.stream
 
     def barrier():
         if world > 1:
@@ -282,62 +368,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    rc, done = ctx.step(args.warmup)
-    if rc or done != args.warmup:
-        raise RuntimeError(f"warmup failed rc={rc} done={done}: {ctx.last_error()}")
-
-    # ---- timed region ------------------------------------------------------
-    sampler = ClockSampler(local)
-    barrier()
-    torch.cuda.synchronize()
-    sampler.start()
-    time.sleep(0.2)
-    launches0 = ctx.launches()
-    ctx.profile(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    ctx.step_async(args.steps)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    rc, done = ctx.sync()
-    barrier()
-    clocks = sampler.stop()
-    if rc or done != args.steps:
-        raise RuntimeError(f"timed run failed rc={rc} done={done}: {ctx.last_error()}")
-    ms = max_over_ranks(e0.elapsed_time(e1))
-    launches = ctx.launches() - launches0
-    prof = ctx.profile_read()
-    ctx.profile(False)
+    res = time_cycles(ctx, cfg, args.steps, args.warmup, world, local, barrier, max_over_ranks, S)
+    ms, launches, prof, clocks, value = res["ms"], res["launches"], res["prof"], res["clocks"], res["value"]
     gcells = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    value = gcells * args.steps / (ms * 1e-3)
-
-    # ---- roofline of the dominant kernel class -------------------------------
-    # The SALE kernels are bound by the FP64 pipe: report that
-    # roofline ("alu") for the dominant kernel class; the HBM view rides along.
-    peak, peak_src = peaks()
-    fpk, fpk_src = fp64_peak()
     local_cells = cfg["nx"] * cfg["ny"] * (ctx.k1 - ctx.k0)
     mode = cfg["rezone"]
-    dom = max(("lagrange", "remap"), key=lambda k: prof[k][0])
-    dom_ms, dom_n = prof[dom]
-    per_cycle_ms = dom_ms / args.steps                             # the class may launch >1 group per cycle
-    fp64_per_cycle = ALGO_FP64[mode][dom] * local_cells           # FP64 instr of the class per cycle
-    achieved_t = fp64_per_cycle / (per_cycle_ms * 1e-3) / 1e12     # T instr/s
-    cyc_fp64 = sum(ALGO_FP64[mode].values()) * local_cells
-    cyc_t = cyc_fp64 / (ms / args.steps * 1e-3) / 1e12
-    cyc_bytes = ALGO_BYTES[mode] * local_cells
-    cycle_gbs = cyc_bytes / (ms / args.steps * 1e-3) / 1e9
-    tr_bytes, tr_src = traffic(args.config, dom)
-    roofline = {"bound": "alu", "achieved": achieved_t, "peak": fpk, "unit": "T fp64-instr/s",
-                "frac": achieved_t / fpk, "traffic": tr_bytes, "traffic_unit": "DRAM bytes per cycle of the class",
-                "traffic_source": tr_src, "algo_bytes_per_cycle": ALGO_BYTES[mode] * local_cells,
-                "kernel": dom, "kernel_launch_groups_per_cycle": dom_n / args.steps,
-                "kernel_ms_per_cycle": per_cycle_ms, "kernel_share_of_step": dom_ms / ms,
-                "algo_fp64_instr_per_zone": ALGO_FP64[mode][dom], "peak_source": fpk_src,
-                "whole_cycle": {"achieved": cyc_t, "frac": cyc_t / fpk,
-                                "algo_fp64_instr_per_zone": sum(ALGO_FP64[mode].values())},
-                "hbm": {"achieved_gbs": cycle_gbs, "peak_gbs": peak, "frac": cycle_gbs / peak,
-                        "algo_bytes_per_zone_cycle": ALGO_BYTES[mode], "peak_source": peak_src}}
+    roofline = roofline_of(args.config, mode, prof, ms, args.steps, local_cells)
 
     # ---- end to end through the public API with host buffers ------------------
     e2e = None
@@ -382,6 +418,43 @@ def main():
                                 "what": "one single-threaded oracle process per core on the same sample, "
                                         "concurrently; sum of their rates (replica throughput)"}
 
+    # ---- the same workload from the seeded perturbed state P0 (every node moving: no
+    # quiescent cells, so no zero-operand division shortcuts), the larger single-GPU
+    # config C3, and the golden-digest check of the kernels timed (N = 1 only)
+    extra = {}
+    if world == 1 and not args.no_extras:
+        from paper_2209_01983_b200 import inputs
+        pert = inputs.perturbation(cfg, 0)
+        for f in ("UX", "UY", "UZ"):
+            ctx.set(f, pert[f.lower()])
+        if mode == configs.LAGRANGE:
+            for f, d in (("X", "dx"), ("Y", "dy"), ("Z", "dz")):
+                ctx.set(f, ctx.get(f) + pert[d])
+        ctx.set("E", ctx.get("E") * pert["e_factor"])
+        del pert
+        rp = time_cycles(ctx, cfg, args.steps, 3, world, local, barrier, max_over_ranks, S)
+        extra["p0_state"] = {"value": rp["value"], "ms_per_step": rp["ms"] / args.steps,
+                             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in rp["prof"].items()},
+                             "what": "seeded perturbed state P0 (inputs.perturbation seed 0: node jitter, "
+                                     "u ~ U(-1e-3, 1e-3), e x U(0.5, 1.5)): every cell active"}
+    ctx.close()
+    if world == 1 and not args.no_extras:
+        import torch
+        torch.cuda.empty_cache()
+        if args.config == "C4":
+            c3, _ = configs.config("C3", 1)
+            c3ctx = S.Sale(c3, device=local)
+            r3 = time_cycles(c3ctx, c3, args.steps, args.warmup, world, local, barrier, max_over_ranks, S)
+            lc3 = c3["nx"] * c3["ny"] * c3["nz"]
+            extra["c3"] = {"workload": workload_name("C3"), "value": r3["value"], "unit": UNIT,
+                           "ms_per_step": r3["ms"] / args.steps,
+                           "roofline": roofline_of("C3", c3["rezone"], r3["prof"], r3["ms"], args.steps, lc3),
+                           "clocks": r3["clocks"], "gpu_launches": r3["launches"],
+                           "kernels_ms_per_step": {k: v[0] / args.steps for k, v in r3["prof"].items()}}
+            c3ctx.close()
+            torch.cuda.empty_cache()
+        extra["golden_check"] = golden_check(args.config, S)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -392,11 +465,15 @@ def main():
                        "cells_per_gpu": local_cells, "mesh": [cfg["nx"], cfg["ny"], cfg["nz"]],
                        "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
                        "step": "one SALE cycle",
+                       "state": f"Sedov initial state (c.6), cycles {args.warmup + 1}..{args.warmup + args.steps}"
+                                " (the shock near the origin; the bulk is quiescent -- p0_state times a "
+                                "fully active state)",
                        "l2": "inputs larger than L2 (state >= 1.1 GB per GPU), no flush"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
         }
+        line.update(extra)
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -9,3 +9,4 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run with -m gpu)")
     config.addinivalue_line("markers", "slow: long-running oracle physics check")
+    config.addinivalue_line("markers", "multigpu: torchrun over several GPUs (skipped when the box has fewer)")

@@ -55,14 +55,14 @@ def _worker(rank, world, port, cfg, full, q):
         for m in plan:
             flat = loc[m["field"]].view(-1)
             seg = flat[m["offset"]:m["offset"] + m["count"]]
-            # tag: field id x 2 + (0: message travels down to r-1, 1: up to r+1)
+            # one tag for every message, posted in plan order: a receive matches the
+            # peer's sends to this rank in posting order -- the pairing ncclSend /
+            # ncclRecv use inside one group (no tags there)
             if m["send"]:
-                tag = sale.FIELDS[m["field"]] * 2 + (0 if m["peer"] < rank else 1)
-                reqs.append(dist.isend(seg.clone(), m["peer"], tag=tag))
+                reqs.append(dist.isend(seg.clone(), m["peer"], tag=0))
             else:
-                tag = sale.FIELDS[m["field"]] * 2 + (1 if m["peer"] < rank else 0)
                 buf = torch.empty_like(seg)
-                reqs.append((dist.irecv(buf, m["peer"], tag=tag), seg, buf))
+                reqs.append((dist.irecv(buf, m["peer"], tag=0), seg, buf))
         for r in reqs:
             if isinstance(r, tuple):
                 r[0].wait()
@@ -110,11 +110,13 @@ def test_halo_plan_over_gloo(world, rezone, full, nmat):
         p.join(timeout=60)
     for r, (bad, _) in res.items():
         assert not bad, (r, bad[:5])
-    # every send has a matching receive of the same size on the peer
-    for r, (_, plan) in res.items():
-        for peer, send, field, count in plan:
-            mirror = [m for m in res[peer][1] if m[0] == r and m[1] != send and m[2] == field]
-            assert len(mirror) == 1 and mirror[0][3] == count
+    # NCCL pairing: the k-th send from a to b is the k-th receive at b from a, with the
+    # same field and count (the plans list the fields in the same order on every rank)
+    for a, (_, plan_a) in res.items():
+        for b in res:
+            sends = [(f, c) for peer, send, f, c in plan_a if peer == b and send]
+            recvs = [(f, c) for peer, send, f, c in res[b][1] if peer == a and not send]
+            assert sends == recvs, (a, b)
 
 
 def test_layout_remainder_to_lowest_ranks():
