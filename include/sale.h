@@ -149,7 +149,8 @@ typedef struct sale_ctx sale_ctx;
 uint64_t sale_workspace_bytes(const sale_params* p);
 
 /* Writes a fresh 128-byte NCCL unique id into id_out (call on rank 0, then
- * broadcast it).  SALE_ENCCL on failure. */
+ * broadcast it).  One id initialises one communicator: every context (every
+ * sale_create of a job) needs its own.  SALE_ENCCL on failure. */
 int32_t sale_nccl_unique_id(void* id_out_128);
 
 /* Validate; carve the workspace; NCCL init when nranks > 1; Sedov initial state

@@ -496,8 +496,7 @@ struct ForceCTA {
     static constexpr int PL = NW * FW, TX = FW - 2, TY = NW - 2;
     static constexpr int NNW = EULER ? 3 : 6;  // staged words per node: (x,) u
     __host__ __device__ static constexpr int oN(int par, int c) { return (par * NNW + c) * PL; }
-    static constexpr int OA = 2 * NNW * PL;                  // Lagrange: x-face A (3), y-face A (3)
-    static constexpr int OT = OA + (EULER ? 0 : 6) * PL;     // cell: corner forces t_h (24), m
+    static constexpr int OT = 2 * NNW * PL;                  // cell: corner forces t_h (24), m
     __host__ __device__ static constexpr int oT(int h, int c) { return OT + (h * 3 + c) * PL; }
     static constexpr int OM = OT + 24 * PL;
     static constexpr int WORDS = OM + PL + 2 * PAD;
@@ -591,6 +590,19 @@ struct ForceCTA {
     template <int CZ>
     __device__ __forceinline__ void gather4(D3& F, double& M, bool& hv, bool pz) const
     {
+        if (pz && pxm && pxp && pym && pyp) {  // all four present (interior): no selects
+            const D3 t0 = T<3 + 4 * CZ>(-1 - FW), t1 = T<2 + 4 * CZ>(-FW), t2 = T<1 + 4 * CZ>(-1), t3 = T<0 + 4 * CZ>(0);
+            const double m0 = me[-1 - FW + OM], m1 = me[-FW + OM], m2 = me[-1 + OM], m3 = me[OM];
+            if (hv) {
+                F = add(add(add(add(F, t0), t1), t2), t3);
+                M = (((M + m0) + m1) + m2) + m3;
+            } else {
+                F = add(add(add(t0, t1), t2), t3);
+                M = ((m0 + m1) + m2) + m3;
+            }
+            hv = true;
+            return;
+        }
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
             const int ap = g & 1, bp = g >> 1;
@@ -621,19 +633,12 @@ struct ForceCTA {
         const double sig = psig, nu_u = pnu, m = pm, ax = pax, ay = pay;
         if (kz < zb) fetch(kz + 2);
         __syncthreads();
-        // ---- P2 (Lagrange): the face area vectors anchored at this column (t^n)
-        D3 Ax, Ay, Azn;
-        if constexpr (!EULER) {
-            // x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
-            Ax = face_area(X<B0>(0), X<B0>(FW), X<B1>(FW), X<B1>(0));
-            // y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
-            Ay = face_area(X<B0>(0), X<B1>(0), X<B1>(1), X<B0>(1));
-            // z-face at node plane kz+1
-            Azn = zface<B1>();
-            st3s(me, OA, PL, Ax);
-            st3s(me, OA + 3 * PL, PL, Ay);
-            __syncthreads();
-        }
+        // ---- P2 (Lagrange): the z-face area of node plane kz+1 at this column (t^n);
+        // the cell's x- and y-faces are formed in P3 by the thread itself (its own and
+        // the +x / +y neighbours' anchored faces: two faces computed twice instead of a
+        // barrier and a shared-memory round trip)
+        D3 Azn;
+        if constexpr (!EULER) Azn = zface<B1>();
         // ---- P3: cell (i,j,kz): hourglass modes, the eight corner forces
         if (cell_thr && kz >= 0 && kz < p.nz) {
             D3 g[4];
@@ -656,7 +661,12 @@ struct ForceCTA {
                 SALE_TE(0) SALE_TE(1) SALE_TE(2) SALE_TE(3) SALE_TE(4) SALE_TE(5) SALE_TE(6) SALE_TE(7)
 #undef SALE_TE
             } else {
-                const D3 A[6] = {Ax, ld3s(me + 1, OA, PL), Ay, ld3s(me + FW, OA + 3 * PL, PL), zprevA, Azn};
+                // x-faces at node planes i, i+1: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1);
+                // y-faces at node planes j, j+1: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
+                const D3 A[6] = {face_area(X<B0>(0), X<B0>(FW), X<B1>(FW), X<B1>(0)),
+                                 face_area(X<B0>(1), X<B0>(FW + 1), X<B1>(FW + 1), X<B1>(1)),
+                                 face_area(X<B0>(0), X<B1>(0), X<B1>(1), X<B0>(1)),
+                                 face_area(X<B0>(FW), X<B1>(FW), X<B1>(FW + 1), X<B0>(FW + 1)), zprevA, Azn};
 #define SALE_TL(H)                                                                                  \
     {                                                                                               \
         const D3 C = corner_vec(A, (H)&1, ((H) >> 1) & 1, (H) >> 2);                                \

@@ -51,8 +51,16 @@ def assemble(ctx, cfg, field, rank, world):
     return out
 
 
-def run_case(name, cfg, cycles, world, rank, local, nid, mat_halves=False):
-    ctx = S.Sale(cfg, device=local, rank=rank, nranks=world, nccl_id=nid)
+def fresh_nccl_id(rank):
+    """A new NCCL unique id from rank 0 for every context (an id initialises one
+    communicator only)."""
+    obj = [S.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def run_case(name, cfg, cycles, world, rank, local, mat_halves=False):
+    ctx = S.Sale(cfg, device=local, rank=rank, nranks=world, nccl_id=fresh_nccl_id(rank))
     if mat_halves:  # C2M2's initial material layout, from the assembled Sedov state
         m = assemble(ctx, cfg, "MASS", rank, world)
         e0 = assemble(ctx, cfg, "MAT_E0", rank, world)
@@ -84,16 +92,13 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
-    obj = [S.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
-    nid = obj[0]
     failures = 0
 
     # small meshes against the CPU oracle (rank 0 computes it)
     small = [("C0", *config("C0")), ("E24", sedov((24, 20, 4 * world + 9), EULER), 40),
              ("L-warm", sedov((17, 13, 3 * world + 11), LAGRANGE, e_background=0.3), 25)]
     for name, cfg, cycles in small:
-        rc, done, clk, glob = run_case(name, cfg, cycles, world, rank, local, nid)
+        rc, done, clk, glob = run_case(name, cfg, cycles, world, rank, local)
         if rank == 0:
             import oracle as O
             o = O.Oracle(cfg)
@@ -113,7 +118,7 @@ def main():
                 continue
             g = json.load(open(path))
             cfg, _ = config(name)
-            rc, done, clk, glob = run_case(name, cfg, g["requested_cycles"], world, rank, local, nid,
+            rc, done, clk, glob = run_case(name, cfg, g["requested_cycles"], world, rank, local,
                                            mat_halves=bool(cfg.get("nmat")))
             if rank == 0:
                 bad = [f for f, v in glob.items()
