@@ -68,3 +68,26 @@ def noh_planar(n: int, **over) -> dict:
                t_end=0.6, reflect_mask=0x3D)
     cfg.update(over)
     return cfg
+
+
+def noh_spherical(n: int, **over) -> dict:
+    """Noh's spherical implosion in the octant [0,1]^3 ("spherical divergent shocks
+    (Noh)"): cold gas at u = -r_hat, gamma = 5/3, reflecting planes
+    x = y = z = 0, free outer faces, Lagrangian mode, run to t = 0.6 (the shock at
+    r = 0.2).  The state comes from inputs.noh_spherical_state."""
+    cfg = dict(_SEDOV, nx=n, ny=n, nz=n, rezone=LAGRANGE, gamma=5.0 / 3.0, t_end=0.6, e_deposit=0.0,
+               e_background=0.0)
+    cfg.update(over)
+    return cfg
+
+
+def sod_2d(n: int, rezone: int, **over) -> dict:
+    """Sod's problem in 2D (Fig. 2a "2D Lagrangian Sod simulation"): n x n x 1
+    cubic cells on [0,1]^2 (one cell across z), every face reflecting, gamma = 1.4, run
+    to t = 0.2.  The diaphragm runs along the diagonal x + y = 1, oblique to the mesh,
+    so the grid is tested off its axes (inputs.sod_oblique_state; SPEC S:526 reads the
+    paper's 2D Sod as planar)."""
+    cfg = dict(_SEDOV, nx=n, ny=n, nz=1, lz=1.0 / n, rezone=rezone, gamma=1.4, t_end=0.2, reflect_mask=0x3F,
+               e_deposit=0.0, e_background=0.0)
+    cfg.update(over)
+    return cfg

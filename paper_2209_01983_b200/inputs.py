@@ -133,3 +133,28 @@ def material_halves(cfg: dict, mass: np.ndarray, energy: np.ndarray, x0: float =
     return {"MAT_F0": np.where(right, 0.0, 1.0), "MAT_M0": np.where(right, 0.0, mass),
             "MAT_E0": np.where(right, 0.0, energy), "MAT_F1": np.where(right, 1.0, 0.0),
             "MAT_M1": np.where(right, mass, 0.0), "MAT_E1": np.where(right, energy, 0.0)}
+
+
+def noh_spherical_state(cfg: dict, X: np.ndarray, Y: np.ndarray, Z: np.ndarray, u0: float = -1.0,
+                        p0: float = 1e-6):
+    """Spherical Noh: node velocity u0 * (x, y, z) / r (zero at the origin) from the node
+    coordinates the context holds, and the pressure floor p0 of planar Noh (e = p0 u0^2 /
+    (gamma - 1) at rho = 1).  Returns {"UX", "UY", "UZ", "E"}."""
+    r = np.sqrt(X * X + Y * Y + Z * Z)
+    rs = np.where(r > 0.0, r, 1.0)
+    out = {f: np.where(r > 0.0, u0 * (A / rs), 0.0) for f, A in (("UX", X), ("UY", Y), ("UZ", Z))}
+    out["E"] = np.full((cfg["nz"], cfg["ny"], cfg["nx"]), p0 * u0 * u0 / (cfg["gamma"] - 1.0))
+    return out
+
+
+def sod_oblique_state(cfg: dict, volume: np.ndarray, left=(1.0, 1.0), right=(0.125, 0.1)):
+    """2D Sod with the diaphragm along x + y = 1: (rho, p) = left for cell centres with
+    x + y < 1, right beyond, at rest.  volume: the cells' V.  Returns {"MASS", "E"}."""
+    nx, ny = cfg["nx"], cfg["ny"]
+    xc = (np.arange(nx) + 0.5) * (cfg["lx"] / nx)
+    yc = (np.arange(ny) + 0.5) * (cfg["ly"] / ny)
+    lft = (yc[:, None] + xc[None, :] < 1.0)[None, :, :]
+    rho = np.where(lft, left[0], right[0])
+    p = np.where(lft, left[1], right[1])
+    g = cfg["gamma"]
+    return {"MASS": rho * volume, "E": np.broadcast_to(p / ((g - 1.0) * rho), volume.shape).copy()}

@@ -100,3 +100,17 @@ def noh_planar(t, g, u0=-1.0, rho0=1.0):
     rho2 = rho0 * (g + 1.0) / (g - 1.0)
     p2 = rho0 * (D + abs(u0)) * abs(u0)
     return D * t, rho2, p2, 0.5 * u0 * u0
+
+
+def noh_spherical(r, t, g, u0=-1.0, rho0=1.0):
+    """Noh's spherical problem (3D, cold gas at u0 r_hat): the shock at r_s = D t with
+    D = (g - 1) |u0| / 2; inside rho = rho0 ((g + 1)/(g - 1))^3, u = 0, p = (g - 1) rho e
+    with e = u0^2 / 2; outside the cold gas compressed by convergence, rho = rho0 (1 +
+    |u0| t / r)^2, u = u0, p = 0.  Returns (r_s, rho(r))."""
+    D = 0.5 * (g - 1.0) * abs(u0)
+    rs = D * t
+    r = np.asarray(r, dtype=float)
+    inside = rho0 * ((g + 1.0) / (g - 1.0)) ** 3
+    ahead = rho0 * (1.0 + abs(u0) * t / np.where(r < rs, 1.0, r)) ** 2
+    rho = np.where(r < rs, inside, ahead)
+    return rs, rho

@@ -1,12 +1,12 @@
 """GPU parity on the further workloads: Sod's shock tube in
-both rezone modes and the planar Noh implosion, loaded through set_field into the
-CUDA path and the oracle alike, run to t_end in several sale_step calls, compared
-bit for bit (same cycle count, same fields)."""
+both rezone modes, the 2D oblique Sod, the planar and the spherical Noh implosions,
+loaded through set_field into the CUDA path and the oracle alike, run to t_end in
+several sale_step calls, compared bit for bit (same cycle count, same fields)."""
 import pytest
 
 import oracle as O
 from paper_2209_01983_b200 import inputs
-from paper_2209_01983_b200.configs import EULER, LAGRANGE, noh_planar, shock_tube
+from paper_2209_01983_b200.configs import EULER, LAGRANGE, noh_planar, noh_spherical, shock_tube, sod_2d
 from tests.helpers import compare
 
 torch = pytest.importorskip("torch")
@@ -50,5 +50,25 @@ def test_sod_transverse_copies_bitwise():
     rows stay identical on the GPU as on the oracle."""
     cfg = shock_tube(64, LAGRANGE, ny=3, nz=2, ly=3.0 / 64, lz=2.0 / 64)
     g, o = _pair(cfg, lambda c, v: inputs.shock_tube_state(c, v))
+    _run(g, o)
+    compare(g, o)
+
+
+def test_noh_spherical_bitwise():
+    """Spherical Noh in the octant (24^3 to t = 0.6, 375 cycles): the state from
+    inputs.noh_spherical_state on both sides, bit for bit in several calls."""
+    from paper_2209_01983_b200.sale import Sale
+    cfg = noh_spherical(24)
+    g, o = Sale(cfg), O.Oracle(cfg)
+    for f, v in inputs.noh_spherical_state(cfg, o.get("X"), o.get("Y"), o.get("Z")).items():
+        g.set(f, v)
+        o.set(f, v)
+    _run(g, o)
+    compare(g, o)
+
+
+@pytest.mark.parametrize("rezone", [LAGRANGE, EULER])
+def test_sod_2d_oblique_bitwise(rezone):
+    g, o = _pair(sod_2d(64, rezone), lambda c, v: inputs.sod_oblique_state(c, v))
     _run(g, o)
     compare(g, o)
