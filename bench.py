@@ -46,7 +46,7 @@ ALGO_BYTES = {configs.LAGRANGE: 120.0, configs.EULER: 80.0}
 ALGO_FP64 = {configs.LAGRANGE: {"lagrange": 1025.0, "remap": 0.0},
              configs.EULER: {"lagrange": 650.0, "remap": 406.0}}
 # kernel name prefixes of each timing class (for the ncu traffic file)
-CLASS_KERNELS = {"lagrange": ("kc_", "ke_state", "k_state"), "remap": ("kr_", "kn_update", "k_mat_flux")}
+CLASS_KERNELS = {"lagrange": ("kc_", "ke_state", "kl_state"), "remap": ("kr_", "kn_update", "k_mat_flux")}
 REASON_BITS = {"hw_slowdown": "hw_slowdown", "hw_thermal_slowdown": "hw_thermal_slowdown",
                "sw_thermal_slowdown": "sw_thermal_slowdown", "sw_power_cap": "sw_power_cap"}
 

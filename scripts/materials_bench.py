@@ -1,8 +1,7 @@
 """Throughput of the multi-material cycle on the C4 and C3
 meshes: zone-cycles/s with nmat = 1, 2, 4 materials mixed in every cell (equal
 fractions 1/nmat, material densities and energies of the Sedov state, gammas
-1.4 / 5/3 / 1.2 / 2.0), beside the single-material fused and v0 kernels on the same
-mesh.  CUDA events on the context's stream, W warm-up cycles, K timed cycles, the
+1.4 / 5/3 / 1.2 / 2.0), beside the single-material kernels on the same mesh.  CUDA events on the context's stream, W warm-up cycles, K timed cycles, the
 per-class split from sale_profile.  python scripts/materials_bench.py [out.json]"""
 import json
 import sys
@@ -40,9 +39,9 @@ lines = []
 for name in ("C4", "C3"):
     cfg, _ = config(name)
     cells = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    for nmat, impl in ((0, "fused"), (0, "v0"), (1, "fused"), (2, "fused"), (4, "fused")):
+    for nmat in (0, 1, 2, 4):
         c = dict(cfg, nmat=nmat, mat_gamma=GAMMAS[:nmat]) if nmat else cfg
-        g = Sale(c, impl=impl)
+        g = Sale(c)
         if nmat > 1:
             m, e = g.get("MAT_M0"), g.get("MAT_E0")
             for k in range(nmat):
@@ -50,7 +49,7 @@ for name in ("C4", "C3"):
                 g.set(f"MAT_M{k}", m / nmat)
                 g.set(f"MAT_E{k}", e)
         ms, rate, prof = timed(g, cells)
-        line = {"workload": name, "nmat": nmat, "kernels": "material (kernels_mat.cu)" if nmat else impl,
+        line = {"workload": name, "nmat": nmat,
                 "cells": cells, "ms_per_cycle": ms, "zone_cycles_per_s": rate,
                 "class_ms_per_cycle": prof, "steps": K, "warmup": W}
         print(json.dumps(line), flush=True)

@@ -13,7 +13,7 @@ prm = dict(G0=0.43, GP=1.7, GT=0.3, Y0=0.2, Ymax=0.9, beta=3.0, n=0.5, cv=0.8, r
 lines = []
 for name, algo in (("C4", 48.0), ("C3", 64.0)):
     cfg, _ = config(name)
-    g = Sale(cfg, impl="fused")
+    g = Sale(cfg)
     g.step(3)
     cells = cfg["nx"] * cfg["ny"] * cfg["nz"]
     eps = torch.rand(g.cell_shape, dtype=torch.float64, device=g.torch_device)
