@@ -49,12 +49,25 @@ def _compile(src: str, obj: str, verbose: bool) -> str:
     return r.stderr if verbose else ""
 
 
+STAMP = os.path.join(LIBDIR, "libsale.stamp")
+
+
+def _stamp() -> str:
+    """The compile configuration the library was built with (nvcc, flags, sources): a
+    library built under other flags (e.g. SALE_FMAD=true, which breaks the bitwise
+    parity with the oracle) is rebuilt, never silently reused."""
+    srcs = sorted(os.path.basename(s) for s in glob.glob(os.path.join(CSRC, "*.cu")))
+    return "\n".join([NVCC, " ".join(flags()), " ".join(srcs)])
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     deps = srcs + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "sale.h"), __file__]
     newest = max(os.path.getmtime(d) for d in deps)
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+    stamp = _stamp()
+    same = os.path.exists(STAMP) and open(STAMP).read() == stamp
+    if not force and same and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
     os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
     objs = [os.path.join(LIBDIR, "obj", os.path.basename(s)[:-3] + ".o") for s in srcs]
@@ -71,6 +84,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(stamp)
     return LIB
 
 
