@@ -69,11 +69,12 @@ def main():
     ap.add_argument("--cycles", type=int, default=None)
     ap.add_argument("--chunk", type=int, default=10)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--gpus", type=int, default=1, help="C4 only: the n-GPU problem (lz = n), file C4n<n>.json")
     args = ap.parse_args()
     if args.threads > 0:
         os.environ["OMP_NUM_THREADS"] = str(args.threads)
         O.use_openmp()
-    cfg, cycles = config(args.name)
+    cfg, cycles = config(args.name, args.gpus)
     if args.cycles is not None:
         cycles = args.cycles
     o = O.Oracle(cfg)
@@ -101,7 +102,10 @@ def main():
         a = o.get(f).ravel()
         out["fields"][f] = {"sha256": digest(a), "n": int(a.size),
                             "sample": [float(v) for v in a[::STRIDE]]}
-    path = os.path.join(ROOT, "tests", "golden", f"{args.name}.json")
+    tag = args.name + (f"n{args.gpus}" if args.gpus > 1 else "")
+    out["config"] = tag
+    out["n_gpus"] = args.gpus
+    path = os.path.join(ROOT, "tests", "golden", f"{tag}.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)
     with open(path, "w") as fh:
         json.dump(out, fh)

@@ -6,7 +6,8 @@ Every rank runs its z-slab through the C ABI on its own GPU (NCCL halo exchange 
 dt allreduce); rank 0 assembles the owned slabs (the interface node
 plane is replicated: both owners' copies must be bit-equal) and compares:
   - small meshes with the CPU oracle, element by element, bitwise;
-  - with --full, BASELINE's C1 / C2 / C3 runs (and the two-material C2M2) with the
+  - with --full, BASELINE's C1 / C2 / C3 runs, the 2-GPU C4 problem (C4n2) and the
+    two-material C2M2 with the
     oracle's golden SHA-256 digests in tests/golden/ (the same files the 1-GPU
     test_gpu_golden.py reproduces), so the assembled multi-GPU fields must be the
     1-GPU bits.
@@ -112,12 +113,12 @@ def main():
 
     if full:  # BASELINE configs against the oracle's golden digests
         gold = os.path.join(ROOT, "tests", "golden")
-        for name in ("C1", "C2", "C2M2", "C3"):
+        for name in ("C1", "C2", "C2M2", "C3", "C4n2"):
             path = os.path.join(gold, f"{name}.json")
             if not os.path.exists(path):
                 continue
             g = json.load(open(path))
-            cfg, _ = config(name)
+            cfg, _ = config(name[:2], int(name[3:]) if "n" in name else 1)
             rc, done, clk, glob = run_case(name, cfg, g["requested_cycles"], world, rank, local,
                                            mat_halves=bool(cfg.get("nmat")))
             if rank == 0:
