@@ -118,7 +118,7 @@ def main():
             if not os.path.exists(path):
                 continue
             g = json.load(open(path))
-            cfg, _ = config(name[:2], int(name[3:]) if "n" in name else 1)
+            cfg, _ = config(name.split("n")[0], int(name.split("n")[1]) if "n" in name else 1)
             rc, done, clk, glob = run_case(name, cfg, g["requested_cycles"], world, rank, local,
                                            mat_halves=bool(cfg.get("nmat")))
             if rank == 0:

@@ -39,7 +39,7 @@ def test_full_length_digest(name):
         g = json.load(f)
     # C4n2: the 2-GPU weak-scaling problem (256 x 256 x 512, lz = 2) on one GPU, the same
     # digest tests/mgpu_worker.py checks the N-GPU runs against
-    cfg, _ = config(name[:2], int(name[3:]) if "n" in name else 1)
+    cfg, _ = config(name.split("n")[0], int(name.split("n")[1]) if "n" in name else 1)
     assert cfg == {k: g["params"][k] for k in cfg}
     ctx = Sale(cfg)
     if cfg.get("nmat"):  # the multi-material runs start from inputs.material_halves
