@@ -36,6 +36,15 @@
 #ifndef SALE_MB_STATE
 #define SALE_MB_STATE 2
 #endif
+#ifndef SALE_MB_STATE_E
+#define SALE_MB_STATE_E 4
+#endif
+#ifndef SALE_MB_FORCE_E
+#define SALE_MB_FORCE_E 2
+#endif
+#ifndef SALE_MB_ENERGY_E
+#define SALE_MB_ENERGY_E 2
+#endif
 
 namespace sale {
 
@@ -476,7 +485,7 @@ struct StateEulerCTA {
 
 // gate = 0 for the first cycle of a sale_step call (DevState.active is still 0 there)
 template <int NW, int NM>
-__global__ void __launch_bounds__(FW * NW, 2) ke_state(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk, int gate)
+__global__ void __launch_bounds__(FW * NW, SALE_MB_STATE_E) ke_state(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk, int gate)
 {
     if (gate && !s.st->active) return;
     extern __shared__ double smem[];
@@ -729,7 +738,7 @@ struct ForceCTA {
 };
 
 template <bool EULER, int NW>
-__global__ void __launch_bounds__(FW * NW, SALE_MB_FORCE) kc_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
+__global__ void __launch_bounds__(FW * NW, EULER ? SALE_MB_FORCE_E : SALE_MB_FORCE) kc_force(Slab s, Phys p, int cur, int kn0, int kn1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];
@@ -986,7 +995,7 @@ struct EnergyCTA {
 };
 
 template <bool EULER, int NW, int NM>
-__global__ void __launch_bounds__(FW * NW, EULER ? 2 : SALE_MB_ENERGY_L) kc_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
+__global__ void __launch_bounds__(FW * NW, EULER ? SALE_MB_ENERGY_E : SALE_MB_ENERGY_L) kc_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];

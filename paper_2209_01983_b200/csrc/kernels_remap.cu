@@ -18,6 +18,10 @@
 
 #include "sale_mesh.cuh"
 
+#ifndef SALE_MB_SWEEP
+#define SALE_MB_SWEEP 2
+#endif
+
 namespace sale {
 
 namespace {
@@ -390,7 +394,7 @@ constexpr int RZ = 32;
 template <int NW, int NM>
 static void sweep_launch(const Slab& s, const Phys& p, int cur, int kr0, int kr1, cudaStream_t cs)
 {
-    auto kern = kr_sweep<NW, 2, NM>;
+    auto kern = kr_sweep<NW, SALE_MB_SWEEP, NM>;
     const size_t sm = sizeof(double) * SweepCTA<NW, NM>::WORDS;
     static bool init = false;
     if (!init) {
