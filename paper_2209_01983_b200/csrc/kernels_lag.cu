@@ -28,7 +28,7 @@
 
 // resident CTAs per SM the register budgets are sized for (compile-time tuning knobs)
 #ifndef SALE_MB_ENERGY_L
-#define SALE_MB_ENERGY_L 1
+#define SALE_MB_ENERGY_L 2
 #endif
 #ifndef SALE_MB_FORCE
 #define SALE_MB_FORCE 2
@@ -926,6 +926,8 @@ struct EnergyCTA {
             const double V1 = vol_from_s(sv);
             if (kz >= s.k0 && kz < s.k1 && !(V1 > 0.0))
                 atomicMin(&s.st->err_key, (ERR_ORDER_TANGLED << 48) | (unsigned long long)gcell(p, i, j, kz));
+            double W = 0.0, Wh = 0.0;
+            if constexpr (EULER) {
             // hourglass modes of u^n and the capped coefficient
             D3 g[4];
             {
@@ -935,7 +937,6 @@ struct EnergyCTA {
             }
             const double nu = hg_cap(nu_u, m, dt);
             // W = sum_h C_h . ubar_h and W_hg = sum_h f_h . ubar_h in corner order
-            double W = 0.0, Wh = 0.0;
             {
                 D3 A[6];
                 if constexpr (!EULER)
@@ -955,6 +956,48 @@ struct EnergyCTA {
     }
                 SALE_WH(0) SALE_WH(1) SALE_WH(2) SALE_WH(3) SALE_WH(4) SALE_WH(5) SALE_WH(6) SALE_WH(7)
 #undef SALE_WH
+            }
+            } else {  // Lagrange: W first, then the modes (the face areas and the modes are
+                      // never live together: 2 CTAs per SM fit with a smaller spill)
+            // W = sum_h C_h . ubar_h in corner order (the face areas live only here) ...
+            {
+                D3 A[6];
+                if constexpr (!EULER)
+                    A[0] = ld3s(me, OAN, PL), A[1] = ld3s(me + 1, OAN, PL), A[2] = ld3s(me, OAN + 3 * PL, PL),
+                    A[3] = ld3s(me + FW, OAN + 3 * PL, PL), A[4] = zA, A[5] = zAn;
+#define SALE_W(H)                                                                                  \
+    {                                                                                              \
+        constexpr int a = (H)&1, b = ((H) >> 1) & 1, c = (H) >> 2;                                  \
+        const D3 ub = c ? Ub<B1>(a + b * FW) : Ub<B0>(a + b * FW);                                 \
+        D3 C;                                                                                      \
+        if constexpr (EULER) C = D3{a ? ax : -ax, b ? ay : -ay, c ? az : -az};                    \
+        else C = corner_vec(A, a, b, c);                                                           \
+        const double tw = dot(C, ub);                                                              \
+        W = (H) == 0 ? tw : W + tw;                                                                \
+    }
+                SALE_W(0) SALE_W(1) SALE_W(2) SALE_W(3) SALE_W(4) SALE_W(5) SALE_W(6) SALE_W(7)
+#undef SALE_W
+            }
+            // ... then the hourglass modes of u^n, the capped coefficient and W_hg =
+            // sum_h f_h . ubar_h (the modes live only here: fewer registers at the peak)
+            {
+                D3 g[4];
+                {
+                    const D3 Uc[8] = {Un<B0>(0), Un<B0>(1), Un<B0>(FW), Un<B0>(FW + 1),
+                                      Un<B1>(0), Un<B1>(1), Un<B1>(FW), Un<B1>(FW + 1)};
+                    hg_modes(Uc, g);
+                }
+                const double nu = hg_cap(nu_u, m, dt);
+#define SALE_WHG(H)                                                                                \
+    {                                                                                              \
+        constexpr int a = (H)&1, b = ((H) >> 1) & 1, c = (H) >> 2;                                  \
+        const D3 ub = c ? Ub<B1>(a + b * FW) : Ub<B0>(a + b * FW);                                 \
+        const double th = dot(hg_corner<H>(g, nu), ub);                                            \
+        Wh = (H) == 0 ? th : Wh + th;                                                              \
+    }
+                SALE_WHG(0) SALE_WHG(1) SALE_WHG(2) SALE_WHG(3) SALE_WHG(4) SALE_WHG(5) SALE_WHG(6) SALE_WHG(7)
+#undef SALE_WHG
+            }
             }
             // compatible energy with the hourglass work (HG); materials: MM4 share + HG heat
             if constexpr (NM > 0) {
