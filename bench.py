@@ -61,17 +61,24 @@ def peaks():
 
 
 def traffic(config_name: str, dom: str):
-    """DRAM bytes (read + write) per launch group of the dominant kernel class, from
-    the committed ncu --set full capture of this workload (profiles/traffic_<cfg>.json,
-    written by scripts/traffic_from_ncu.py); None if absent."""
+    """DRAM bytes (read + write) per launch group of the dominant kernel class, and the
+    class's time-weighted FP64-pipe utilisation, from the committed ncu --set full
+    capture of this workload (profiles/traffic_<cfg>.json, written by
+    scripts/traffic_from_ncu.py); Nones if absent."""
     try:
         with open(os.path.join(ROOT, "profiles", f"traffic_{config_name}.json")) as f:
             d = json.load(f)
         per = d["dram_bytes_per_launch"]
-        tot = sum(v for k, v in per.items() if k.startswith(CLASS_KERNELS[dom]))
-        return (tot if tot > 0 else None), d.get("source")
+        ks = [k for k in per if k.startswith(CLASS_KERNELS[dom])]
+        tot = sum(per[k] for k in ks)
+        fp = d.get("fp64_pipe_pct_of_active")
+        pipe = None
+        if fp:
+            t = d["gpu_time_ns_per_launch"]
+            pipe = sum(fp[k] * t[k] for k in ks) / sum(t[k] for k in ks)
+        return (tot if tot > 0 else None), d.get("source"), pipe
     except Exception:
-        return None, None
+        return None, None, None
 
 
 def fp64_peak():
@@ -234,14 +241,26 @@ def workload_name(name):
             }.get(name, name)
 
 
-def time_cycles(ctx, cfg, steps, warmup, world, local, barrier, max_over_ranks, S):
+def totals(ctx):
+    """Mass and total energy IE + KE (math.fsum, c.7) of the state, read back on the host."""
+    import math
+    M = ctx.get("NODE_MASS")
+    ke = math.fsum((0.5 * M * (ctx.get("UX") ** 2 + ctx.get("UY") ** 2 + ctx.get("UZ") ** 2)).ravel())
+    m = ctx.get("MASS")
+    return math.fsum(m.ravel()), math.fsum((m * ctx.get("E")).ravel()) + ke
+
+
+def time_cycles(ctx, cfg, steps, warmup, world, local, barrier, max_over_ranks, S, conservation=False):
     """W untimed cycles, then K cycles bracketed by barrier + synchronize, CUDA events
-    on the context's stream, kernel-class timing and nvidia-smi clocks (max over ranks)."""
+    on the context's stream, kernel-class timing and nvidia-smi clocks (max over ranks).
+    conservation: also the relative change of mass and of IE + KE over the K cycles
+    (read outside the timed region)."""
     import torch
     stream = ctx.stream
     rc, done = ctx.step(warmup)
     if rc or done != warmup:
         raise RuntimeError(f"warmup failed rc={rc} done={done}: {ctx.last_error()}")
+    before = totals(ctx) if conservation else None
     sampler = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -264,8 +283,16 @@ def time_cycles(ctx, cfg, steps, warmup, world, local, barrier, max_over_ranks, 
     prof = ctx.profile_read()
     ctx.profile(False)
     gcells = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    return {"ms": ms, "launches": launches, "prof": prof, "clocks": clocks,
-            "value": gcells * steps / (ms * 1e-3)}
+    out = {"ms": ms, "launches": launches, "prof": prof, "clocks": clocks, "value": gcells * steps / (ms * 1e-3)}
+    if conservation:
+        after = totals(ctx)
+        out["conservation"] = {
+            "mass_rel_change": abs(after[0] - before[0]) / before[0],
+            "energy_rel_change": abs(after[1] - before[1]) / before[1],
+            "what": "over the timed cycles; mass exact up to round-off in both modes; IE + KE conserved to "
+                    "round-off in Lagrange mode (compatible scheme with HG), not in Euler mode (the momentum "
+                    "remap dissipates kinetic energy, reading Q17)"}
+    return out
 
 
 def roofline_of(config_name, mode, prof, ms, steps, local_cells):
@@ -282,11 +309,12 @@ def roofline_of(config_name, mode, prof, ms, steps, local_cells):
     cyc_t = cyc_fp64 / (ms / steps * 1e-3) / 1e12
     cyc_bytes = ALGO_BYTES[mode] * local_cells
     cycle_gbs = cyc_bytes / (ms / steps * 1e-3) / 1e9
-    tr_bytes, tr_src = traffic(config_name, dom)
+    tr_bytes, tr_src, pipe = traffic(config_name, dom)
     return {"bound": "alu", "achieved": achieved_t, "peak": fpk, "unit": "T fp64-instr/s",
             "frac": achieved_t / fpk, "traffic": tr_bytes, "traffic_unit": "DRAM bytes per cycle of the class",
             "traffic_source": tr_src, "algo_bytes_per_cycle": ALGO_BYTES[mode] * local_cells,
             "traffic_bytes_per_zone": (tr_bytes / local_cells) if tr_bytes else None,
+            "ncu_fp64_pipe_pct": pipe,
             "kernel": dom, "kernel_launch_groups_per_cycle": dom_n / steps,
             "kernel_ms_per_cycle": per_cycle_ms, "kernel_share_of_step": dom_ms / ms,
             "algo_fp64_instr_per_zone": ALGO_FP64[mode][dom], "peak_source": fpk_src,
@@ -368,7 +396,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    res = time_cycles(ctx, cfg, args.steps, args.warmup, world, local, barrier, max_over_ranks, S)
+    res = time_cycles(ctx, cfg, args.steps, args.warmup, world, local, barrier, max_over_ranks, S,
+                      conservation=(world == 1))
     ms, launches, prof, clocks, value = res["ms"], res["launches"], res["prof"], res["clocks"], res["value"]
     gcells = cfg["nx"] * cfg["ny"] * cfg["nz"]
     local_cells = cfg["nx"] * cfg["ny"] * (ctx.k1 - ctx.k0)
@@ -444,12 +473,14 @@ def main():
         if args.config == "C4":
             c3, _ = configs.config("C3", 1)
             c3ctx = S.Sale(c3, device=local)
-            r3 = time_cycles(c3ctx, c3, args.steps, args.warmup, world, local, barrier, max_over_ranks, S)
+            r3 = time_cycles(c3ctx, c3, args.steps, args.warmup, world, local, barrier, max_over_ranks, S,
+                             conservation=True)
             lc3 = c3["nx"] * c3["ny"] * c3["nz"]
             extra["c3"] = {"workload": workload_name("C3"), "value": r3["value"], "unit": UNIT,
                            "ms_per_step": r3["ms"] / args.steps,
                            "roofline": roofline_of("C3", c3["rezone"], r3["prof"], r3["ms"], args.steps, lc3),
                            "clocks": r3["clocks"], "gpu_launches": r3["launches"],
+                           "conservation": r3.get("conservation"),
                            "kernels_ms_per_step": {k: v[0] / args.steps for k, v in r3["prof"].items()}}
             c3ctx.close()
             torch.cuda.empty_cache()
@@ -472,6 +503,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "conservation": res.get("conservation"),
         }
         line.update(extra)
         print(json.dumps(line), flush=True)
