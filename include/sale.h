@@ -110,7 +110,13 @@ typedef struct sale_params {
                                  aligned, owned by the caller, not freed by us     */
     uint64_t workspace_bytes;
     int32_t device;           /* CUDA device ordinal this context runs on          */
-    int32_t pad0;             /* zero                                              */
+    int32_t overlap;          /* boundary-first cycles (P:372-375
+                                 non-blocking exchange): the kernels that produce the
+                                 planes the halo exchange sends run first on those
+                                 planes, the exchange then runs on a side stream while
+                                 they finish the interior.  0 = automatic (on with more
+                                 than one rank), 1 = on (also for local_slabs > 1),
+                                 -1 = off.  Results are identical either way.        */
     int32_t local_slabs;      /* >= 1.  With nranks == 1, split the mesh into this
                                  many z-slabs on the same device exchanging halos
                                  by device copies (emulated ranks, used to prove

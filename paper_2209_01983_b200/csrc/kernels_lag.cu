@@ -1118,10 +1118,15 @@ int launch_force(const Slab& s, const Phys& p, int cur, Stream st)
     return 1;
 }
 
-int launch_energy(const Slab& s, const Phys& p, int cur, Stream st)
+int launch_energy(const Slab& s, const Phys& p, int cur, Stream st, int ka, int kb)
 {
     int kc0 = s.k0, kc1 = s.k1;
     if (p.rezone) euler_ranges(s, p, kc0, kc1);
+    if (ka >= 0) {  // a sub-range of the cell planes (boundary-first cycles)
+        kc0 = ka > kc0 ? ka : kc0;
+        kc1 = kb < kc1 ? kb : kc1;
+    }
+    if (kc1 <= kc0) return 0;
     auto go = [&](auto kern, size_t words) {
         const size_t sm = sizeof(double) * words;
         set_smem(kern, sm);

@@ -164,7 +164,7 @@ __global__ void k_mat_total(Slab s, Phys p, int cur)
 // R1-R4 with the material axis: the swept volumes and per-material donor data
 // (kr_sweep with NM materials), the material fluxes and cell update (k_mat_flux),
 // the node momentum update on the totals (kn_update)
-int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st)
+int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st, int nodes)
 {
     cudaStream_t cs = (cudaStream_t)st;
     const int bs = 128;
@@ -175,6 +175,7 @@ int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st)
         k_mat_flux<NM><<<grid_for(s.pc * (kr1 - kr0), bs), bs, 0, cs>>>(s, p, cur, kr0, kr1);
         note_launch();
     });
+    if (!nodes) return 2;
     launch_kn_update(s, p, cur, st);
     return 3;
 }

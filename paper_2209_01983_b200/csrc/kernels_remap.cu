@@ -52,7 +52,7 @@ struct Flux {
 template <bool TILE>  // TILE: 32 x 8 node tiles (grid x = x-tiles * y-tiles) instead of flattened rows
 // spd = 1: also store |u''|^2 per node (unused by the current schedule)
 // (8 CTAs per SM at 32 registers, as kn_force_e: more warps for the latency-bound gather)
-__global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int spd)
+__global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int spd, int kbase)
 {
     if (!s.st->active) return;
     int i, j, t;
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int
         i = t % (p.nx + 1);
         j = t / (p.nx + 1);
     }
-    const int k = s.k0 + blockIdx.y;
+    const int k = kbase + blockIdx.y;
     const bool pxm = i >= 1, pxp = i < p.nx, pym = j >= 1, pyp = j < p.ny, pzm = k >= 1, pzp = k < p.nz;
     const int c00 = i + p.nx * (j + p.ny * (k - s.kb));  // 32-bit: a slab holds < 2^31 cells
     const int sx = 1, sy = p.nx, sz = p.nx * p.ny;
@@ -425,23 +425,31 @@ int launch_sweep(const Slab& s, const Phys& p, int cur, Stream st)
 
 // R4 node momentum update on the cell totals (32 x 8 node tiles: the gathered cell
 // values are reused inside a block through L1)
-int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st)
+int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st, int ka, int kb)
 {
-    kn_update<true><<<dim3(cdivr(p.nx + 1, 32) * cdivr(p.ny + 1, 8), s.k1 - s.k0 + 1), 256, 0, (cudaStream_t)st>>>(
-        s, p, cur, 0);
+    int k0 = s.k0, k1 = s.k1;  // node planes [k0, k1]
+    if (ka >= 0) {             // a sub-range [ka, kb] (boundary-first cycles)
+        k0 = ka > k0 ? ka : k0;
+        k1 = kb < k1 ? kb : k1;
+    }
+    if (k1 < k0) return 0;
+    kn_update<true><<<dim3(cdivr(p.nx + 1, 32) * cdivr(p.ny + 1, 8), k1 - k0 + 1), 256, 0, (cudaStream_t)st>>>(
+        s, p, cur, 0, k0);
     note_launch();
     return 1;
 }
 
-// R1-R4 of the single-material scheme: kr_sweep, kr_flux, kn_update (the next cycle's
-// ke_state forms the dt candidate of the remapped state)
-int launch_remap(const Slab& s, const Phys& p, int cur, Stream st)
+// R1-R4 of the single-material scheme: kr_sweep, kr_flux and (nodes = 1) kn_update over
+// every owned node plane (the next cycle's ke_state forms the dt candidate of the
+// remapped state); nodes = 0 leaves R4 to the caller (boundary-first cycles)
+int launch_remap(const Slab& s, const Phys& p, int cur, Stream st, int nodes)
 {
     cudaStream_t cs = (cudaStream_t)st;
     const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     launch_sweep(s, p, cur, st);
     kr_flux<<<dim3(cdivr(p.nx, 32), cdivr(p.ny, 8), kr1 - kr0), dim3(32, 8), 0, cs>>>(s, p, cur, kr0);
     note_launch();
+    if (!nodes) return 2;
     launch_kn_update(s, p, cur, st);
     return 3;
 }

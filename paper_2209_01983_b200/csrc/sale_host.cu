@@ -61,6 +61,10 @@ struct sale_ctx {
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     long long glaunches[2] = {0, 0};
     cudaStream_t cap_stream = nullptr;  // private stream the graphs are captured on
+    // boundary-first cycles: the halo exchange runs on `side` while the interior
+    // finishes; evB = boundary planes done, evX = exchange done
+    cudaStream_t side = nullptr;
+    cudaEvent_t evB = nullptr, evX = nullptr;
 };
 
 namespace {
@@ -111,6 +115,7 @@ bool params_ok(const sale_params* p)
     if (p->nranks > 1 && p->nccl_unique_id == nullptr) return false;  // nranks == 1 + id: 1-rank NCCL comm
     if (p->local_slabs < 1 || (p->nranks > 1 && p->local_slabs != 1)) return false;
     if (!(p->hg >= 0.0)) return false;
+    if (p->overlap < -1 || p->overlap > 1) return false;
     int T = p->nranks * p->local_slabs;
     if (p->nz < T) return false;
     if (T > 1 && p->nz / T < ghost_depth(p)) return false;  // every slab owns >= g planes
@@ -489,16 +494,72 @@ int reduce_keys(sale_ctx* c)
                       "dt allreduce");
 }
 
+bool overlap_on(const sale_ctx* c)
+{
+    const int o = c->prm.overlap;
+    const bool multi = c->prm.nranks > 1 || c->prm.local_slabs > 1;
+    return multi && (o > 0 || (o == 0 && c->prm.nranks > 1));
+}
+
+int overlap_resources(sale_ctx* c)
+{
+    int rc = SALE_OK;
+    if (!c->side) rc = cuda_check(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+    if (!rc && !c->evB) rc = cuda_check(c, cudaEventCreateWithFlags(&c->evB, cudaEventDisableTiming), "event");
+    if (!rc && !c->evX) rc = cuda_check(c, cudaEventCreateWithFlags(&c->evX, cudaEventDisableTiming), "event");
+    return rc;
+}
+
+// The planes of a slab the exchange sends and the slab's last kernel writes:
+// Lagrange cell planes [k0, k0+g) and [k1-g, k1) (e'; x', u' come from kc_force, which
+// runs whole before); Euler node planes [k0, k0+g] and [k1-g, k1] (u''; m'', e'' come
+// from the flux kernel, which runs whole before).  part 0 = those, part 1 = the rest.
+// A slab too thin to have an interior runs whole as part 0.
+int launch_tail(sale_ctx* c, const Slab& s, int b, int part, sale::Stream st)
+{
+    const bool euler = c->prm.rezone == SALE_EULER;
+    const int g = s.g, k0 = s.k0, k1 = s.k1;
+    const bool thin = k1 - k0 < 2 * g + 2;
+    if (part == 1 && thin) return 0;
+    int n = 0;
+    if (euler) {
+        if (part == 0 && thin) return sale::launch_kn_update(s, c->phys, b, st);
+        if (part == 0) {
+            n += sale::launch_kn_update(s, c->phys, b, st, k0, k0 + g);
+            n += sale::launch_kn_update(s, c->phys, b, st, k1 - g, k1);
+        } else {
+            n += sale::launch_kn_update(s, c->phys, b, st, k0 + g + 1, k1 - g - 1);
+        }
+    } else {
+        if (part == 0 && thin) return sale::launch_energy(s, c->phys, b, st);
+        if (part == 0) {
+            n += sale::launch_energy(s, c->phys, b, st, k0, k0 + g);
+            n += sale::launch_energy(s, c->phys, b, st, k1 - g, k1);
+        } else {
+            n += sale::launch_energy(s, c->phys, b, st, k0 + g, k1 - g);
+        }
+    }
+    return n;
+}
+
 // one cycle reading buffers [b]; first = the first cycle of a sale_step call (its
 // state pass runs ungated, DevState.active being still 0 then).  Both modes:
 //   kl_state / ke_state (cell state + dt candidate of the cycle-start state) -> dt /
 //   error allreduce -> k_begin (commit the previous cycle, finalise dt) -> kc_force
 //   -> kc_energy -> [Euler: remap] -> halo exchange of the new state
+// Boundary-first (overlap_on): the last kernel of the cycle (Lagrange kc_energy, Euler
+// kn_update) runs first on the planes the exchange sends (launch_tail part 0 on every
+// slab), the exchange starts on the side stream, the interior (part 1) runs on the
+// context's stream meanwhile, and the stream joins the exchange before the next
+// cycle.  The interior writes owned planes of b^1 only, the exchange ghost planes of
+// b^1 only; it reads owned planes the boundary part finished.
 int enqueue_one_cycle(sale_ctx* c, int b, bool first)
 {
     int rc;
     sale::Stream st = (sale::Stream)c->stream;
     const bool euler = c->prm.rezone == SALE_EULER;
+    const bool ov = overlap_on(c);
+    if (ov && (rc = overlap_resources(c))) return rc;
     int pr = prof_open(c, SALE_K_LAGRANGE);
     for (auto& s : c->slabs) c->launches += sale::launch_state(s, c->phys, b, first ? 0 : 1, st);
     prof_close(c, pr);
@@ -511,19 +572,34 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first)
     for (auto& s : c->slabs) {
         pr = prof_open(c, SALE_K_LAGRANGE);
         c->launches += sale::launch_force(s, c->phys, b, st);
-        c->launches += sale::launch_energy(s, c->phys, b, st);
+        if (euler || !ov) c->launches += sale::launch_energy(s, c->phys, b, st);
+        else c->launches += launch_tail(c, s, b, 0, st);
         prof_close(c, pr);
         if (euler) {
             pr = prof_open(c, SALE_K_REMAP);
-            c->launches += c->prm.nmat ? sale::launch_remap_mat(s, c->phys, b, st) : sale::launch_remap(s, c->phys, b, st);
+            const int nodes = ov ? 0 : 1;
+            c->launches += c->prm.nmat ? sale::launch_remap_mat(s, c->phys, b, st, nodes)
+                                       : sale::launch_remap(s, c->phys, b, st, nodes);
+            if (ov) c->launches += launch_tail(c, s, b, 0, st);
             prof_close(c, pr);
         }
     }
     if ((rc = launch_check(c))) return rc;
-    pr = prof_open(c, SALE_K_HALO);
-    if ((rc = exchange(c, b ^ 1, false))) return rc;
+    if (!ov) {
+        pr = prof_open(c, SALE_K_HALO);
+        if ((rc = exchange(c, b ^ 1, false))) return rc;
+        prof_close(c, pr);
+        return launch_check(c);
+    }
+    if ((rc = cuda_check(c, cudaEventRecord(c->evB, c->stream), "event record"))) return rc;
+    if ((rc = cuda_check(c, cudaStreamWaitEvent(c->side, c->evB, 0), "stream wait"))) return rc;
+    if ((rc = exchange(c, b ^ 1, false, c->side))) return rc;
+    if ((rc = cuda_check(c, cudaEventRecord(c->evX, c->side), "event record"))) return rc;
+    pr = prof_open(c, euler ? SALE_K_REMAP : SALE_K_LAGRANGE);
+    for (auto& s : c->slabs) c->launches += launch_tail(c, s, b, 1, st);
     prof_close(c, pr);
-    return launch_check(c);
+    if ((rc = launch_check(c))) return rc;
+    return cuda_check(c, cudaStreamWaitEvent(c->stream, c->evX, 0), "stream wait");
 }
 
 // CUDA graph of two consecutive cycles starting from buffer parity b (they return to
@@ -1080,6 +1156,9 @@ void sale_destroy(sale_ctx* c)
     for (auto ge : c->gexec)
         if (ge) cudaGraphExecDestroy(ge);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->evB) cudaEventDestroy(c->evB);
+    if (c->evX) cudaEventDestroy(c->evX);
     delete c;
 }
 

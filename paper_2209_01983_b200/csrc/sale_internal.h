@@ -152,12 +152,15 @@ int launch_state(const Slab& s, const Phys& p, int cur, int gate, Stream st);
 int launch_force(const Slab& s, const Phys& p, int cur, Stream st);
 // S7: V', tangle check, compatible energy with the hourglass work.  Lagrange: e' into
 // buffer cur^1; Euler: e' (e'_k), V', and the moved-face s' the sweep reads.
-int launch_energy(const Slab& s, const Phys& p, int cur, Stream st);
-// R1-R4 (kernels_remap.cu; materials: kernels_mat.cu)
-int launch_remap(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st);
+// [ka, kb): a sub-range of the cell planes (boundary-first cycles); -1: all of them
+int launch_energy(const Slab& s, const Phys& p, int cur, Stream st, int ka = -1, int kb = -1);
+// R1-R4 (kernels_remap.cu; materials: kernels_mat.cu); nodes = 0: R1-R3 only (the caller
+// launches R4 by node-plane ranges, boundary first)
+int launch_remap(const Slab& s, const Phys& p, int cur, Stream st, int nodes = 1);
+int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st, int nodes = 1);
 int launch_sweep(const Slab& s, const Phys& p, int cur, Stream st);
-int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st);
+// R4 over the owned node planes, or the sub-range [ka, kb]
+int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st, int ka = -1, int kb = -1);
 int launch_mat_init(const Slab& s, const Phys& p, Stream st);
 int launch_mat_total(const Slab& s, const Phys& p, int cur, Stream st);
 

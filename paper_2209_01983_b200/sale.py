@@ -43,7 +43,7 @@ class SaleParams(C.Structure):
                 ("e_background", C.c_double), ("e_deposit", C.c_double), ("rank", C.c_int32),
                 ("nranks", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
-                ("device", C.c_int32), ("pad0", C.c_int32), ("local_slabs", C.c_int32),
+                ("device", C.c_int32), ("overlap", C.c_int32), ("local_slabs", C.c_int32),
                 ("nmat", C.c_int32), ("mat_gamma", C.c_double * MAX_MAT), ("hg", C.c_double)]
 
 
@@ -135,6 +135,7 @@ def make_params(cfg: dict, *, rank=0, nranks=1, device=0, local_slabs=1) -> Sale
     p.rank, p.nranks, p.device = rank, nranks, device
     p.local_slabs = local_slabs
     p.hg = float(cfg.get("hg", 0.0))
+    p.overlap = int(cfg.get("overlap", 0))
     gam = list(cfg.get("mat_gamma", ()))[:MAX_MAT]  # nmat > MAX_MAT is rejected by libsale
     p.nmat = int(cfg.get("nmat", 0))
     p.mat_gamma = (C.c_double * MAX_MAT)(*(gam + [0.0] * (MAX_MAT - len(gam))))
@@ -176,7 +177,7 @@ class Sale:
     cfg: the sale_params values (configs.config / configs.sedov ...); optional
     cfg["nmat"] (1..4) and cfg["mat_gamma"] add the material axis (fields MAT_F<k>,
     MAT_M<k>, MAT_E<k>; include/sale.h); cfg["hg"] the hourglass coefficient (0 if
-    absent).  local_slabs > 1 splits the mesh into emulated ranks on one GPU."""
+    absent); cfg["overlap"] the boundary-first mode (0 automatic, 1 on, -1 off).  local_slabs > 1 splits the mesh into emulated ranks on one GPU."""
 
     def __init__(self, cfg: dict, *, device: int = 0, stream=None, rank: int = 0, nranks: int = 1,
                  nccl_id: bytes | None = None, local_slabs: int = 1):
