@@ -57,11 +57,6 @@ constexpr int ZCHUNK = 32;   // z-planes per CTA on large meshes
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 inline int imin_h(int a, int b) { return a < b ? a : b; }
 inline int imax_h(int a, int b) { return a > b ? a : b; }
-inline unsigned grid_for(long long n, int bs)
-{
-    long long g = (n + bs - 1) / bs;
-    return (unsigned)(g > 0 ? g : 1);
-}
 
 __device__ __forceinline__ D3 ld3s(const double* b, int o0, int stride)
 {
