@@ -253,7 +253,8 @@ def test_sedov_similarity_law_lagrange_C1_trajectory():
 @pytest.mark.slow
 def test_sedov_similarity_law_lagrange_live():
     """The same law on a live 32^3 Lagrangian run (shell-averaged radius of the
-    density peak over cell centroids; window t in [0.010, 0.134])."""
+    density peak over cell centroids; window t in [0.010, 0.134]), and the octant
+    symmetry of its final state."""
     n = 32
     cfg = sedov((n, n, n), LAGRANGE)
     o = O.Oracle(cfg)
@@ -276,6 +277,10 @@ def test_sedov_similarity_law_lagrange_live():
         rs.append(bins[np.argmax(prof) - 1] + 0.5 * h)
     err, slope = _similarity(ts, rs)
     assert err <= 0.10 and abs(slope - 0.4) <= 0.05, (err, slope)
+    # octant permutation symmetry of the whole run (SURVEY c.9: <= 1e-10 relative)
+    e = o.get("E")
+    for perm in ((0, 2, 1), (2, 1, 0), (1, 0, 2)):
+        assert np.max(np.abs(e - e.transpose(perm))) <= 1e-10 * np.abs(e).max()
 
 
 # ------------------------------------------------------------------ errors
