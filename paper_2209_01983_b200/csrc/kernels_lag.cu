@@ -70,6 +70,22 @@ __device__ __forceinline__ void st3s(double* b, int o0, int stride, D3 v)
 }
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// asynchronous global -> shared copies (cp.async, 8 B): a node plane is staged
+// without passing through registers (no prefetch registers held across a step)
+__device__ __forceinline__ void cpa8(double* sdst, const double* gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa3(double* sdst, int stride, double* const a[3], long long n)
+{
+    cpa8(sdst, a[0] + n);
+    cpa8(sdst + stride, a[1] + n);
+    cpa8(sdst + 2 * stride, a[2] + n);
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // opt a kernel into `bytes` of dynamic shared memory, once per kernel (a process-wide
 // registry keyed by the kernel's address: instantiations of one launch lambda share
 // its function-local statics, so those cannot carry the flag)
@@ -337,9 +353,10 @@ __global__ void __launch_bounds__(FW * NW, SALE_MB_STATE) kl_state(Slab s, Phys 
 template <int NW, int NM>
 struct StateEulerCTA {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
+    // node u in a ring of 3 slots filled by cp.async two planes ahead
     __host__ __device__ static constexpr int oU(int par, int c) { return (par * 3 + c) * PL; }  // node u
-    __host__ __device__ static constexpr int oW(int xy) { return 6 * PL + xy * PL; }            // x/y face Ubar_a
-    static constexpr int WORDS = 8 * PL + 2 * PAD;
+    __host__ __device__ static constexpr int oW(int xy) { return 9 * PL + xy * PL; }            // x/y face Ubar_a
+    static constexpr int WORDS = 11 * PL + 2 * PAD;
 
     const Slab& s;
     const Phys& p;
@@ -348,7 +365,6 @@ struct StateEulerCTA {
     int i, j, za, zb, ic, jc;
     long long nbn, cb, cbc;
     bool out_cell;
-    D3 pu;
     double pm, pe, pv;
     double pmf[NM > 0 ? NM : 1], pmm[NM > 0 ? NM : 1], pme[NM > 0 ? NM : 1];
     double zprev;  // Ubar_z of the z-face at node plane kz (the -z face of cell kz)
@@ -374,10 +390,16 @@ struct StateEulerCTA {
         key = KEY_NONE;
     }
     __device__ __forceinline__ static int imin(int a, int b) { return a < b ? a : b; }
-    __device__ __forceinline__ void fetch(int k)  // node plane k (u), cell plane k-1 (m, e, V^T)
+    // node plane k (u of this column, clamped always-valid address) into slot SL
+    template <int SL>
+    __device__ __forceinline__ void stage(int k)
     {
         const int kn = clampi(k, s.kb, s.kb + s.nzn - 1);
-        pu = ld3(s.u[cur], nbn + (long long)kn * s.pn);
+        cpa3(me + oU(SL, 0), PL, s.u[cur], nbn + (long long)kn * s.pn);
+        cpa_commit();
+    }
+    __device__ __forceinline__ void fetch(int k)  // cell plane k-1 (m, e, V^T)
+    {
         const int kc = clampi(k - 1, s.kb, s.kb + s.nzc - 1);
         const long long c = cbc + (long long)kc * s.pc;
         pm = s.m[cur][c];
@@ -393,11 +415,12 @@ struct StateEulerCTA {
     template <int PAR>
     __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oU(PAR, 0), PL); }
 
-    template <int B0>
+    // B0, B1, B2: the slots of node planes kz, kz+1, kz+2
+    template <int B0, int B1, int B2>
     __device__ __forceinline__ void step(int kz)
     {
-        constexpr int B1 = B0 ^ 1;
-        st3s(me, oU(B1, 0), PL, pu);
+        cpa_wait_all();
+        __syncthreads();  // node plane kz+1 landed; slot B2 (plane kz-1) free
         const double m = pm, e = pe, V = pv;
         double cmf[NM > 0 ? NM : 1], cmm[NM > 0 ? NM : 1], cme[NM > 0 ? NM : 1];
 #pragma unroll
@@ -406,8 +429,10 @@ struct StateEulerCTA {
             cmm[a] = pmm[a];
             cme[a] = pme[a];
         }
-        if (kz < zb) fetch(kz + 2);
-        __syncthreads();
+        if (kz < zb) {
+            stage<B2>(kz + 2);
+            fetch(kz + 2);
+        }
         // the a-component of the face-average velocity of the faces anchored here
         const double* Ux0 = me + oU(B0, 0);
         const double* Ux1 = me + oU(B1, 0);
@@ -419,8 +444,7 @@ struct StateEulerCTA {
         const double uz = 0.25 * (((Uz1[0] + Uz1[1]) + Uz1[FW + 1]) + Uz1[FW]);  // z-face at node plane k+1
         me[oW(0)] = ux;
         me[oW(1)] = uy;
-        // max node speed^2 of the cell in corner order (read before the barrier: the
-        // next step overwrites the plane-kz slot)
+        // max node speed^2 of the cell in corner order
         double v2 = speed2(U<B0>(0));
         v2 = dmax(v2, speed2(U<B0>(1)));
         v2 = dmax(v2, speed2(U<B0>(FW)));
@@ -461,18 +485,22 @@ struct StateEulerCTA {
 
     __device__ __forceinline__ void run()
     {
-        fetch(za);
-        if (za & 1) st3s(me, oU(1, 0), PL, pu);
-        else st3s(me, oU(0, 0), PL, pu);
+        // slot of node plane k: (k - za) mod 3
+        stage<0>(za);
+        stage<1>(za + 1);
         fetch(za + 1);
+        cpa_wait_all();
         __syncthreads();
         {
-            const double* Uz = me + ((za & 1) ? oU(1, 2) : oU(0, 2));
+            const double* Uz = me + oU(0, 2);
             zprev = 0.25 * (((Uz[0] + Uz[1]) + Uz[FW + 1]) + Uz[FW]);
         }
         for (int kz = za; kz <= zb; ++kz) {
-            if (kz & 1) step<1>(kz);
-            else step<0>(kz);
+            switch ((kz - za) % 3) {
+            case 0: step<0, 1, 2>(kz); break;
+            case 1: step<1, 2, 0>(kz); break;
+            default: step<2, 0, 1>(kz); break;
+            }
         }
         block_min_atomic(key, &s.st->cand_key);
     }
@@ -499,8 +527,9 @@ template <bool EULER, int NW>
 struct ForceCTA {
     static constexpr int PL = NW * FW, TX = FW - 2, TY = NW - 2;
     static constexpr int NNW = EULER ? 3 : 6;  // staged words per node: (x,) u
+    // node planes in a ring of 3 slots filled by cp.async two planes ahead
     __host__ __device__ static constexpr int oN(int par, int c) { return (par * NNW + c) * PL; }
-    static constexpr int OT = 2 * NNW * PL;                  // cell: corner forces t_h (24), m
+    static constexpr int OT = 3 * NNW * PL;                  // cell: corner forces t_h (24), m
     __host__ __device__ static constexpr int oT(int h, int c) { return OT + (h * 3 + c) * PL; }
     static constexpr int OM = OT + 24 * PL;
     static constexpr int WORDS = OM + PL + 2 * PAD;
@@ -515,7 +544,6 @@ struct ForceCTA {
     bool node_thr, cell_thr, col_in, cellcol_in;
     bool pxm, pxp, pym, pyp;
     // prefetch registers (clamped, always-valid addresses)
-    D3 px, pu;
     double psig, pnu, pm, pax, pay;
     double az;    // Euler: z-face area (x-y cross-section) of this column, constant in z
     D3 zprevA;    // Lagrange: A of the z-face at node plane kz
@@ -551,13 +579,20 @@ struct ForceCTA {
         if (EULER) az = s.TAz[2][(long long)jc * p.nx + ic];
     }
 
-    // node plane k (x, u) and cell plane k-1 (sigma, nu_u, m; Euler: table areas)
-    __device__ __forceinline__ void fetch(int k)
+    // node plane k (x, u of this column, clamped always-valid addresses) into slot SL by
+    // cp.async
+    template <int SL>
+    __device__ __forceinline__ void stage(int k)
     {
         const int kn = clampi(k, s.kb, s.kb + s.nzn - 1);
         const long long n = nbc + (long long)kn * s.pn;
-        if (!EULER) px = ld3(s.x[cur], n);
-        pu = ld3(s.u[cur], n);
+        if (!EULER) cpa3(me + oN(SL, 0), PL, s.x[cur], n);
+        cpa3(me + oN(SL, EULER ? 0 : 3), PL, s.u[cur], n);
+        cpa_commit();
+    }
+    // cell plane k-1 (sigma, nu_u, m; Euler: table areas) into registers
+    __device__ __forceinline__ void fetch(int k)
+    {
         const int kc = clampi(k - 1, s.kb, s.kb + s.nzc - 1);
         const long long c = cbc + (long long)kc * s.pc;
         psig = s.sig[c];
@@ -568,12 +603,6 @@ struct ForceCTA {
             pax = s.TAx[0][(long long)kl * p.ny + jc];
             pay = s.TAy[1][(long long)kl * p.nx + ic];
         }
-    }
-    template <int PAR>
-    __device__ __forceinline__ void put()
-    {
-        if (!EULER) st3s(me, oN(PAR, 0), PL, px);
-        st3s(me, oN(PAR, EULER ? 0 : 3), PL, pu);
     }
     template <int PAR>
     __device__ __forceinline__ D3 X(int off) const { return ld3s(me + off, oN(PAR, 0), PL); }
@@ -628,15 +657,19 @@ struct ForceCTA {
         }
     }
 
-    template <int B0>
+    // B0, B1, B2: the slots of node planes kz, kz+1, kz+2
+    template <int B0, int B1, int B2>
     __device__ __forceinline__ void step(int kz)
     {
-        constexpr int B1 = B0 ^ 1;
-        // ---- P1: stage node plane kz+1; the cell operands of plane kz; prefetch
-        put<B1>();
-        const double sig = psig, nu_u = pnu, m = pm, ax = pax, ay = pay;
-        if (kz < zb) fetch(kz + 2);
+        // ---- P1: node plane kz+1 landed (its copies were issued a step ago); the cell
+        // operands of plane kz; node plane kz+2 into the slot plane kz-1 left
+        cpa_wait_all();
         __syncthreads();
+        const double sig = psig, nu_u = pnu, m = pm, ax = pax, ay = pay;
+        if (kz < zb) {
+            stage<B2>(kz + 2);
+            fetch(kz + 2);
+        }
         // ---- P2 (Lagrange): the z-face area of node plane kz+1 at this column (t^n);
         // the cell's x- and y-faces are formed in P3 by the thread itself (its own and
         // the +x / +y neighbours' anchored faces: two faces computed twice instead of a
@@ -715,19 +748,23 @@ struct ForceCTA {
 
     __device__ __forceinline__ void run()
     {
-        // prologue: node plane za-1 (and its z-face), prefetch node plane za + cell plane za-1
-        fetch(za - 1);
-        if ((za - 1) & 1) put<1>();
-        else put<0>();
+        // prologue: node planes za-1 (and its z-face) and za, the operands of cell plane
+        // za-1; slot of node plane k: (k - za + 1) mod 3
+        stage<0>(za - 1);
+        stage<1>(za);
         fetch(za);
         have = false;
         Fp = D3{0.0, 0.0, 0.0};
         Mp = 0.0;
+        cpa_wait_all();
         __syncthreads();
-        if constexpr (!EULER) zprevA = ((za - 1) & 1) ? zface<1>() : zface<0>();
+        if constexpr (!EULER) zprevA = zface<0>();
         for (int kz = za - 1; kz <= zb; ++kz) {
-            if (kz & 1) step<1>(kz);
-            else step<0>(kz);
+            switch ((kz - za + 1) % 3) {
+            case 0: step<0, 1, 2>(kz); break;
+            case 1: step<1, 2, 0>(kz); break;
+            default: step<2, 0, 1>(kz); break;
+            }
         }
     }
 };
@@ -754,8 +791,12 @@ struct EnergyCTA {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
     // node words: Lagrange x^n(3) x'(3) u^n(3) u'(3); Euler x'(3) u^n(3) ubar(3)
     static constexpr int NNW = EULER ? 9 : 12;
+    // node-plane slots: Euler 2 (register prefetch, staged one plane ahead: x' and ubar
+    // are formed when staged); Lagrange a ring of 3 filled by cp.async two planes ahead
+    // (the raw x^n, x', u^n, u' never pass through registers)
+    static constexpr int NSL = EULER ? 2 : 3;
     __host__ __device__ static constexpr int oN(int par, int c) { return (par * NNW + c) * PL; }
-    static constexpr int OS = 2 * NNW * PL;   // s' of the x-face, y-face
+    static constexpr int OS = NSL * NNW * PL;  // s' of the x-face, y-face
     static constexpr int OAN = OS + 2 * PL;   // Lagrange: A^n of the x-face (3), y-face (3)
     static constexpr int WORDS = OAN + (EULER ? 0 : 6) * PL + 2 * PAD;
 
@@ -804,18 +845,27 @@ struct EnergyCTA {
         }
     }
 
-    __device__ __forceinline__ void fetch(int k)  // node plane k, cell plane k-1
+    // Lagrange: cp.async of node plane k (x^n, x', u^n, u' of this column, clamped
+    // always-valid addresses) into slot SL
+    template <int SL>
+    __device__ __forceinline__ void stage(int k)
     {
         const int kn = clampi(k, s.kb, s.kb + s.nzn - 1);
         const long long n = nbc + (long long)kn * s.pn;
-        fu = ld3(s.u[cur], n);
+        cpa3(me + oN(SL, 0), PL, s.x[cur], n);
+        cpa3(me + oN(SL, 3), PL, s.x[cur ^ 1], n);
+        cpa3(me + oN(SL, 6), PL, s.u[cur], n);
+        cpa3(me + oN(SL, 9), PL, s.u[cur ^ 1], n);
+        cpa_commit();
+    }
+    __device__ __forceinline__ void fetch(int k)  // node plane k (Euler), cell plane k-1
+    {
+        const int kn = clampi(k, s.kb, s.kb + s.nzn - 1);
+        const long long n = nbc + (long long)kn * s.pn;
         if constexpr (EULER) {
+            fu = ld3(s.u[cur], n);
             fu1 = ld3(s.u1, n);
             fz = s.Zt[kn - s.kb];
-        } else {
-            fx = ld3(s.x[cur], n);
-            fx1 = ld3(s.x[cur ^ 1], n);
-            fu1 = ld3(s.u[cur ^ 1], n);
         }
         const int kc = clampi(k - 1, s.kb, s.kb + s.nzc - 1);
         const long long c = cbc + (long long)kc * s.pc;
@@ -874,12 +924,18 @@ struct EnergyCTA {
         if constexpr (!EULER) A = face_area(Xn<B>(0), Xn<B>(1), Xn<B>(FW + 1), Xn<B>(FW));
     }
 
-    template <int B0>
+    // B0, B1: the slots of node planes kz, kz+1; B2 (Lagrange): the slot plane kz+2 goes to
+    template <int B0, int B1, int B2>
     __device__ __forceinline__ void step(int kz)
     {
-        constexpr int B1 = B0 ^ 1;
-        // ---- P1: stage node plane kz+1; this cell's operands; prefetch
-        put<B1>();
+        // ---- P1: stage node plane kz+1 (Lagrange: wait for its copies); this cell's
+        // operands; prefetch
+        if constexpr (EULER) {
+            put<B1>();
+        } else {
+            cpa_wait_all();
+            __syncthreads();  // plane kz+1 visible; slot B2 (plane kz-1) free
+        }
         const double m = fm, e = fe, sig = fsig, nu_u = fnu, ax = fax, ay = fay;
         double cf[NM > 0 ? NM : 1], cm[NM > 0 ? NM : 1], ce[NM > 0 ? NM : 1], cs_[NM > 0 ? NM : 1];
 #pragma unroll
@@ -889,8 +945,11 @@ struct EnergyCTA {
             ce[a] = re[a];
             cs_[a] = rs[a];
         }
-        if (kz < zb) fetch(kz + 2);
-        __syncthreads();
+        if (kz < zb) {
+            if constexpr (!EULER) stage<B2>(kz + 2);
+            fetch(kz + 2);
+        }
+        if constexpr (EULER) __syncthreads();
         // ---- P2: faces anchored at this column
         D3 zAn;
         double zsn;
@@ -1013,21 +1072,38 @@ struct EnergyCTA {
         }
         zA = zAn;
         zs = zsn;
-        __syncthreads();
+        if constexpr (EULER) __syncthreads();
     }
 
     __device__ __forceinline__ void run()
     {
-        fetch(za);
-        if (za & 1) put<1>();
-        else put<0>();
-        fetch(za + 1);
-        __syncthreads();
-        if (za & 1) zstate<1>(zA, zs);
-        else zstate<0>(zA, zs);
-        for (int kz = za; kz <= zb; ++kz) {
-            if (kz & 1) step<1>(kz);
-            else step<0>(kz);
+        if constexpr (EULER) {
+            fetch(za);
+            if (za & 1) put<1>();
+            else put<0>();
+            fetch(za + 1);
+            __syncthreads();
+            if (za & 1) zstate<1>(zA, zs);
+            else zstate<0>(zA, zs);
+            for (int kz = za; kz <= zb; ++kz) {
+                if (kz & 1) step<1, 0, 0>(kz);
+                else step<0, 1, 0>(kz);
+            }
+        } else {
+            // slot of node plane k: (k - za) mod 3
+            stage<0>(za);
+            stage<1>(za + 1);
+            fetch(za + 1);
+            cpa_wait_all();
+            __syncthreads();
+            zstate<0>(zA, zs);
+            for (int kz = za; kz <= zb; ++kz) {
+                switch ((kz - za) % 3) {
+                case 0: step<0, 1, 2>(kz); break;
+                case 1: step<1, 2, 0>(kz); break;
+                default: step<2, 0, 1>(kz); break;
+                }
+            }
         }
     }
 };

@@ -4,11 +4,12 @@
 //               ribbons between the target and the moved faces shared between
 //               neighbouring faces; the moved faces' s' from kc_energy) and the
 //               R2 donor data m/V' (per material: m_k/V') and the 8-node mean u'.
-//   kr_flux   : one thread per cell: R2 donor-cell fluxes, R3 cell update
-//               (multi-material cells: k_mat_flux, kernels_mat.cu).
-//   kn_update : one thread per node: R4 node momentum from the gathered Delta m,
-//               Delta P, m'' (fixed gather order) + reflecting BC; R5 (x := x^T)
-//               is implicit.
+//   kr_tail   : z-march; R2 donor-cell fluxes and R3 cell update per cell, R4 node
+//               momentum from the gathered Delta m, Delta P, m'' (fixed gather order,
+//               through shared memory) + reflecting BC; R5 (x := x^T) is implicit.
+//   kn_update : one thread per node, R4 alone: the multi-material cycle's node update
+//               after k_mat_flux (kernels_mat.cu), which hands Delta m, Delta P, m''
+//               through HBM.
 //
 // Same expression trees and association as the oracle, so the results are
 // bit-identical.  Shared-memory access pattern: compile-time plane parity,
@@ -20,6 +21,15 @@
 
 #ifndef SALE_MB_SWEEP
 #define SALE_MB_SWEEP 2
+#endif
+#ifndef SALE_MB_TAIL
+#define SALE_MB_TAIL 2
+#endif
+#ifndef SALE_TAIL_PF  // kr_tail: L2 prefetch distance in planes (0: none)
+#define SALE_TAIL_PF 2
+#endif
+#ifndef SALE_NW_TAIL
+#define SALE_NW_TAIL 8
 #endif
 
 namespace sale {
@@ -37,11 +47,6 @@ __device__ __forceinline__ void st3r(double* b, int o0, int stride, D3 v)
     b[o0 + 2 * stride] = v.z;
 }
 
-struct Flux {
-    double mu, eps;
-    D3 pi;
-};
-
 }  // namespace
 
 // ============================================================================
@@ -51,7 +56,7 @@ struct Flux {
 // grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane: no idle lanes), y = planes
 template <bool TILE>  // TILE: 32 x 8 node tiles (grid x = x-tiles * y-tiles) instead of flattened rows
 // spd = 1: also store |u''|^2 per node (unused by the current schedule)
-// (8 CTAs per SM at 32 registers, as kn_force_e: more warps for the latency-bound gather)
+// (8 CTAs per SM at 32 registers: more warps for the latency-bound gather)
 __global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int spd, int kbase)
 {
     if (!s.st->active) return;
@@ -115,19 +120,13 @@ __global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int
 }
 
 // ============================================================================
-// kr_sweep + kr_flux: the remap as two lean kernels (the alternative to the
-// pipelined kr_cells_p, whose carried state spills).
-//
-//   kr_sweep : z-march over cell planes; stages x', u' node planes; per column
-//              and plane the six ribbons and three moved faces of c.4 step 1
-//              (ribbons shared with the neighbouring faces as in kr_cells), the
-//              swept volumes dV of the cell's -x/-y/-z faces, and the donor data
-//              r = m/V', Ubar = 8-node mean of u' (c.4 step 2).  Writes
-//              Slab::dV, rD, UD.  Dependencies reach only the +x / +y neighbours,
-//              so a 32 x NW tile yields 31 x (NW-1) columns.
-//   kr_flux  : one thread per cell: the six face fluxes from dV and the donor
-//              data (c.4 step 2), the cell update (c.4 step 3).
-// Same expressions, operands and association as kr_cells / the oracle.
+// kr_sweep: z-march over cell planes; stages x', u' node planes; per column and
+// plane the six ribbons and three moved faces of c.4 step 1 (ribbons shared with
+// the neighbouring faces), the swept volumes dV of the cell's -x/-y/-z faces, and
+// the donor data r = m/V', Ubar = 8-node mean of u' (c.4 step 2).  Writes Slab::dV,
+// rD, UD (read by kr_tail).  Dependencies reach only the +x / +y neighbours, so a
+// 32 x NW tile yields 31 x (NW-1) columns.  Same expressions, operands and
+// association as the oracle.
 // ============================================================================
 // NM > 0: multi-material cells: the donor data per material,
 // m_k / V' (Slab::rDm, MM5), instead of r = m / V'
@@ -332,12 +331,20 @@ __global__ void __launch_bounds__(RW * NW, MB) kr_sweep(Slab s, Phys p, int cur,
     c.run();
 }
 
-// grid: x = ceil(nx / 32), y = ceil(ny / 8), z = cell planes [kr0, kr1)
-// All loads are independent of the swept volumes' signs (both candidate donors of
-// every face are loaded, the donor is selected afterwards), so they overlap.
-#ifndef KR_FLUX_MB
-#define KR_FLUX_MB 3
-#endif
+// ============================================================================
+// kr_tail: R2 fluxes + R3 cell update and R4 node momentum in one z-march (the
+// round-2 kr_flux + kn_update pair, whose Delta m, Delta P and m'' went through HBM).
+// Thread (ix, iy) of a 32 x NW tile owns node (i, j) = (bx*TX + ix, by*TY + iy) and
+// the cell (i-1, j-1) below-left of it: per cell plane t it forms that cell's six face
+// fluxes from the swept volumes and the donor data of kr_sweep (c.4 step 2, every
+// operand loaded before the donor sign test, so the loads overlap), the cell update
+// (c.4 step 3) -- m'', e'' stored for the owned cells -- and puts Delta m, Delta P, m''
+// into shared memory (double-buffered by plane parity: one barrier per plane); then
+// node (i, j) of plane t is finished from the running sums (cells of plane t-1, c' = 0)
+// and the four cells of plane t (c' = 1), and node plane t+1 started from the same four
+// cells -- kn_update's fixed gather order, cells a' fastest, then b', then c'.  A tile
+// yields (32-1) x (NW-1) nodes; node planes [ka, kb] (cell planes [ka-1, kb]).
+// ============================================================================
 struct Donor {
     double r, e;
     D3 u;
@@ -346,15 +353,15 @@ __device__ __forceinline__ Donor donor_at(const Slab& s, long long d)
 {
     return Donor{s.rD[d], s.e1[d], ld3(s.UD, d)};
 }
-__global__ void __launch_bounds__(256, KR_FLUX_MB) kr_flux(Slab s, Phys p, int cur, int kr0)
+// c.4 steps 2-3 for cell (i, j, t): Delta m, Delta P and m''; stores m'', e'' (and the
+// ENEGMASS check) when `own`
+__device__ __forceinline__ void flux_cell(const Slab& s, const Phys& p, int cur, int i, int j, int t, bool own,
+                                          double& dm, D3& dP, double& m2)
 {
-    if (!s.st->active) return;
-    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 8 + threadIdx.y, t = kr0 + blockIdx.z;
-    if (i >= p.nx || j >= p.ny) return;
     const long long c = (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * (t - s.kb));
     const long long sa[3] = {1, p.nx, s.pc};
     const int ia[3] = {i, j, t}, na[3] = {p.nx, p.ny, p.nz};
-    const Donor own = donor_at(s, c);
+    const Donor own_d = donor_at(s, c);
     // faces in the order of c.4 step 3: -x +x -y +y -z +z; boundary faces carry no flux
     double mu[6], ep[6];
     D3 pi[6];
@@ -367,22 +374,164 @@ __global__ void __launch_bounds__(256, KR_FLUX_MB) kr_flux(Slab s, Phys p, int c
         const double dV = inner ? s.dV[a][plus ? nbr : c] : 0.0;  // the face is the -a face of the upper cell
         const Donor other = donor_at(s, nbr);
         // donor: the lower cell if the face moved toward +a (c.4 step 2)
-        const Donor& D = (dV > 0.0) == plus ? own : other;
+        const Donor& D = (dV > 0.0) == plus ? own_d : other;
         mu[f] = inner ? D.r * dV : 0.0;
         ep[f] = inner ? mu[f] * D.e : 0.0;
         pi[f] = inner ? scl(mu[f], D.u) : D3{0.0, 0.0, 0.0};
     }
-    const double dm = ((((mu[0] - mu[1]) + mu[2]) - mu[3]) + mu[4]) - mu[5];
+    dm = ((((mu[0] - mu[1]) + mu[2]) - mu[3]) + mu[4]) - mu[5];
     const double dE = ((((ep[0] - ep[1]) + ep[2]) - ep[3]) + ep[4]) - ep[5];
-    const D3 dP = sub(add(sub(add(sub(pi[0], pi[1]), pi[2]), pi[3]), pi[4]), pi[5]);
-    const double m = s.m[cur][c], e1 = own.e;
-    const double m2 = m + dm;
-    if (t >= s.k0 && t < s.k1 && !(m2 > 0.0))
-        atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, t));
-    s.e[cur ^ 1][c] = e1 + ddiv(dE - (e1 * dm), m2);
-    s.m[cur ^ 1][c] = m2;
-    s.dm[c] = dm;
-    st3(s.dP, c, dP);
+    dP = sub(add(sub(add(sub(pi[0], pi[1]), pi[2]), pi[3]), pi[4]), pi[5]);
+    const double m = s.m[cur][c], e1 = own_d.e;
+    m2 = m + dm;
+    if (own) {
+        if (t >= s.k0 && t < s.k1 && !(m2 > 0.0))
+            atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, t));
+        s.e[cur ^ 1][c] = e1 + ddiv(dE - (e1 * dm), m2);
+        s.m[cur ^ 1][c] = m2;
+    }
+}
+
+template <int NW>
+struct TailCTA {
+    static constexpr int PL = NW * RW, TX = RW - 1, TY = NW - 1;
+    __host__ __device__ static constexpr int oC(int par, int c) { return (par * 5 + c) * PL; }  // dm, dP(3), m''
+    static constexpr int WORDS = 10 * PL;
+
+    const Slab& s;
+    const Phys& p;
+    const int cur;
+    double* me;
+    int i, j, ka, kb, za, zb;
+    long long nb;
+    bool node_thr, cell_col, own_col;
+    bool pxm, pxp, pym, pyp;
+    D3 Fp;  // running sums of node plane t+1 (cells of plane t, c' = 0)
+    double Dp, Mp;
+    bool have;
+
+    __device__ __forceinline__ TailCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int ka_, int kb_,
+                                       int zchunk)
+        : s(s_), p(p_), cur(cur_)
+    {
+        const int ix = threadIdx.x, iy = threadIdx.y;
+        me = smem + iy * RW + ix;
+        i = blockIdx.x * TX + ix;
+        j = blockIdx.y * TY + iy;
+        ka = ka_;
+        kb = kb_;
+        za = ka + blockIdx.z * zchunk;
+        zb = za + zchunk - 1 < kb ? za + zchunk - 1 : kb;
+        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
+        node_thr = ix < TX && iy < TY && i <= p.nx && j <= p.ny;
+        cell_col = i >= 1 && i <= p.nx && j >= 1 && j <= p.ny;  // cell (i-1, j-1) exists
+        own_col = cell_col && ix >= 1 && iy >= 1;                // ... and this tile stores it
+        pxm = i >= 1;
+        pxp = i < p.nx;
+        pym = j >= 1;
+        pyp = j < p.ny;
+    }
+
+    // the four cells of the plane in buffer PAR at corners c' = CZ of node (i, j), in
+    // gather order a' fastest (cell (i-1+a', j-1+b') sits at me + a' + b' RW)
+    template <int PAR>
+    __device__ __forceinline__ void gather4(double& Dm, D3& DP, double& M2, bool& hv, bool pz) const
+    {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const int ap = g & 1, bp = g >> 1;
+            const int off = ap + bp * RW;
+            const bool pres = pz && (ap ? pxp : pxm) && (bp ? pyp : pym);
+            if (pres) {
+                const double d = me[off + oC(PAR, 0)], mm = me[off + oC(PAR, 4)];
+                const D3 dp = D3{me[off + oC(PAR, 1)], me[off + oC(PAR, 2)], me[off + oC(PAR, 3)]};
+                Dm = hv ? Dm + d : d;
+                DP = hv ? add(DP, dp) : dp;
+                M2 = hv ? M2 + mm : mm;
+                hv = true;
+            }
+        }
+    }
+
+    template <int PAR>
+    __device__ __forceinline__ void step(int t)
+    {
+        const bool fin = node_thr && t >= za;  // node plane t is finished in this step
+        const long long n = nb + (long long)t * s.pn;
+        D3 u1 = D3{0.0, 0.0, 0.0};
+        if (fin) u1 = ld3(s.u1, n);
+        const bool pz = t >= 0 && t < p.nz;  // cell plane t exists
+#if SALE_TAIL_PF
+        // the operands of plane t + PF into L2 (no registers held): the loads of a
+        // z-march step are exposed once per plane, an L2 hit shortens them
+        if (cell_col && t + SALE_TAIL_PF < p.nz && t + SALE_TAIL_PF <= zb) {
+            constexpr int PF = SALE_TAIL_PF;
+            const int tp = t + PF;
+            const long long c = (long long)(i - 1) + (long long)p.nx * ((long long)(j - 1) + (long long)p.ny * (tp - s.kb));
+            const double* a[9] = {s.rD, s.e1, s.UD[0], s.UD[1], s.UD[2], s.dV[0], s.dV[1], s.dV[2], s.m[cur]};
+#pragma unroll
+            for (int q = 0; q < 9; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(a[q] + c));
+            if (node_thr) {
+                const long long np = nb + (long long)tp * s.pn;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(s.u1[0] + np));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(s.u1[1] + np));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(s.u1[2] + np));
+            }
+        }
+#endif
+        if (cell_col && pz) {
+            double dm, m2;
+            D3 dP;
+            flux_cell(s, p, cur, i - 1, j - 1, t, own_col && t >= ka && t <= kb, dm, dP, m2);
+            me[oC(PAR, 0)] = dm;
+            me[oC(PAR, 1)] = dP.x;
+            me[oC(PAR, 2)] = dP.y;
+            me[oC(PAR, 3)] = dP.z;
+            me[oC(PAR, 4)] = m2;
+        }
+        __syncthreads();
+        if (!node_thr) return;
+        if (fin) {
+            double Dm = Dp, M2 = Mp;
+            D3 DP = Fp;
+            bool hv = have;
+            gather4<PAR>(Dm, DP, M2, hv, pz);
+            Dm = 0.125 * Dm;
+            DP = scl(0.125, DP);
+            M2 = 0.125 * M2;
+            D3 un = d3(u1.x + ddiv(DP.x - (u1.x * Dm), M2), u1.y + ddiv(DP.y - (u1.y * Dm), M2),
+                       u1.z + ddiv(DP.z - (u1.z * Dm), M2));
+            un = reflect(p, i, j, t, un);
+            st3(s.u[cur ^ 1], n, un);
+        }
+        have = false;
+        Dp = 0.0;
+        Mp = 0.0;
+        Fp = D3{0.0, 0.0, 0.0};
+        if (t < zb) gather4<PAR>(Dp, Fp, Mp, have, pz);
+    }
+
+    __device__ __forceinline__ void run()
+    {
+        have = false;
+        Dp = 0.0;
+        Mp = 0.0;
+        Fp = D3{0.0, 0.0, 0.0};
+        for (int t = za - 1; t <= zb; ++t) {
+            if (t & 1) step<1>(t);
+            else step<0>(t);
+        }
+    }
+};
+
+// grid: x = ceil((nx+1) / 31), y = ceil((ny+1) / (NW-1)), z = z-chunks of node planes [ka, kb]
+template <int NW>
+__global__ void __launch_bounds__(RW * NW, SALE_MB_TAIL) kr_tail(Slab s, Phys p, int cur, int ka, int kb, int zchunk)
+{
+    if (!s.st->active) return;
+    extern __shared__ double smem[];
+    TailCTA<NW> c(s, p, cur, smem, ka, kb, zchunk);
+    c.run();
 }
 
 // ============================================================================
@@ -439,19 +588,42 @@ int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st, int ka, i
     return 1;
 }
 
-// R1-R4 of the single-material scheme: kr_sweep, kr_flux and (nodes = 1) kn_update over
-// every owned node plane (the next cycle's ke_state forms the dt candidate of the
-// remapped state); nodes = 0 leaves R4 to the caller (boundary-first cycles)
+// R2-R4 of the single-material scheme over node planes [ka, kb] (default: the owned
+// planes [k0, k1]); the cells of planes [ka-1, kb] are formed, those in [ka, kb] n
+// [k0, k1) stored (so boundary-first sub-ranges split the owned cells disjointly)
+int launch_rtail(const Slab& s, const Phys& p, int cur, Stream st, int ka, int kb)
+{
+    int k0 = s.k0, k1 = s.k1;
+    if (ka >= 0) {
+        k0 = ka > k0 ? ka : k0;
+        k1 = kb < k1 ? kb : k1;
+    }
+    if (k1 < k0) return 0;
+    constexpr int NW = SALE_NW_TAIL;
+    auto kern = kr_tail<NW>;
+    const size_t sm = sizeof(double) * TailCTA<NW>::WORDS;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        init = true;
+    }
+    const long long xy = (long long)cdivr(p.nx + 1, RW - 1) * cdivr(p.ny + 1, NW - 1);
+    const int zc = zchunk_for(xy, k1 - k0 + 1, RZ);
+    dim3 grid(cdivr(p.nx + 1, RW - 1), cdivr(p.ny + 1, NW - 1), cdivr(k1 - k0 + 1, zc));
+    kern<<<grid, dim3(RW, NW), sm, (cudaStream_t)st>>>(s, p, cur, k0, k1, zc);
+    note_launch();
+    return 1;
+}
+
+// R1-R4 of the single-material scheme: kr_sweep and (nodes = 1) kr_tail over every
+// owned node plane (the next cycle's ke_state forms the dt candidate of the remapped
+// state); nodes = 0 leaves R2-R4 to the caller (boundary-first cycles: launch_rtail by
+// node-plane ranges)
 int launch_remap(const Slab& s, const Phys& p, int cur, Stream st, int nodes)
 {
-    cudaStream_t cs = (cudaStream_t)st;
-    const int kr0 = s.k0 - 1 > 0 ? s.k0 - 1 : 0, kr1 = s.k1 + 1 < p.nz ? s.k1 + 1 : p.nz;
     launch_sweep(s, p, cur, st);
-    kr_flux<<<dim3(cdivr(p.nx, 32), cdivr(p.ny, 8), kr1 - kr0), dim3(32, 8), 0, cs>>>(s, p, cur, kr0);
-    note_launch();
-    if (!nodes) return 2;
-    launch_kn_update(s, p, cur, st);
-    return 3;
+    if (!nodes) return 1;
+    return 1 + launch_rtail(s, p, cur, st);
 }
 
 }  // namespace sale

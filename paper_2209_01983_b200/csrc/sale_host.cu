@@ -512,8 +512,9 @@ int overlap_resources(sale_ctx* c)
 
 // The planes of a slab the exchange sends and the slab's last kernel writes:
 // Lagrange cell planes [k0, k0+g) and [k1-g, k1) (e'; x', u' come from kc_force, which
-// runs whole before); Euler node planes [k0, k0+g] and [k1-g, k1] (u''; m'', e'' come
-// from the flux kernel, which runs whole before).  part 0 = those, part 1 = the rest.
+// runs whole before); Euler node planes [k0, k0+g] and [k1-g, k1] (u''; single
+// material: kr_tail forms and stores m'', e'' of cell planes [k0, k0+g] and [k1-g, k1)
+// in the same launches; materials: k_mat_flux runs whole before).  part 0 = those, part 1 = the rest.
 // A slab too thin to have an interior runs whole as part 0.
 int launch_tail(sale_ctx* c, const Slab& s, int b, int part, sale::Stream st)
 {
@@ -523,12 +524,15 @@ int launch_tail(sale_ctx* c, const Slab& s, int b, int part, sale::Stream st)
     if (part == 1 && thin) return 0;
     int n = 0;
     if (euler) {
-        if (part == 0 && thin) return sale::launch_kn_update(s, c->phys, b, st);
+        // single material: kr_tail (R2-R4, the cells of the range stored by it);
+        // materials: kn_update (R4; k_mat_flux ran whole before)
+        auto nodes = c->prm.nmat ? sale::launch_kn_update : sale::launch_rtail;
+        if (part == 0 && thin) return nodes(s, c->phys, b, st, -1, -1);
         if (part == 0) {
-            n += sale::launch_kn_update(s, c->phys, b, st, k0, k0 + g);
-            n += sale::launch_kn_update(s, c->phys, b, st, k1 - g, k1);
+            n += nodes(s, c->phys, b, st, k0, k0 + g);
+            n += nodes(s, c->phys, b, st, k1 - g, k1);
         } else {
-            n += sale::launch_kn_update(s, c->phys, b, st, k0 + g + 1, k1 - g - 1);
+            n += nodes(s, c->phys, b, st, k0 + g + 1, k1 - g - 1);
         }
     } else {
         if (part == 0 && thin) return sale::launch_energy(s, c->phys, b, st);
