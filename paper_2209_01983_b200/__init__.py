@@ -2,7 +2,7 @@
 
     from paper_2209_01983_b200 import Sale, configs
     cfg, cycles = configs.config("C4")
-    ctx = Sale(cfg, impl="fused")
+    ctx = Sale(cfg)
     ctx.step(cycles)
 
 The compute path is libsale.so (hand-written sm_100a CUDA kernels behind the C

@@ -70,21 +70,6 @@ __device__ __forceinline__ void st3s(double* b, int o0, int stride, D3 v)
 }
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// asynchronous global -> shared copies (cp.async, 8 B): a node plane is staged
-// without passing through registers (no prefetch registers held across a step)
-__device__ __forceinline__ void cpa8(double* sdst, const double* gsrc)
-{
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cpa3(double* sdst, int stride, double* const a[3], long long n)
-{
-    cpa8(sdst, a[0] + n);
-    cpa8(sdst + stride, a[1] + n);
-    cpa8(sdst + 2 * stride, a[2] + n);
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // opt a kernel into `bytes` of dynamic shared memory, once per kernel (a process-wide
 // registry keyed by the kernel's address: instantiations of one launch lambda share

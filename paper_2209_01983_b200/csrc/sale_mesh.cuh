@@ -46,6 +46,22 @@ __device__ __forceinline__ void st3(double* const a[3], long long n, D3 v)
     a[2][n] = v.z;
 }
 
+// asynchronous global -> shared copies (cp.async, 8 B): a node plane is staged
+// without passing through registers (no prefetch registers held across a step)
+__device__ __forceinline__ void cpa8(double* sdst, const double* gsrc)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cpa3(double* sdst, int stride, double* const a[3], long long n)
+{
+    cpa8(sdst, a[0] + n);
+    cpa8(sdst + stride, a[1] + n);
+    cpa8(sdst + 2 * stride, a[2] + n);
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // the 8 nodes of cell (i,j,k) in hex order (c*2+b)*2+a
 template <bool EULER>
 __device__ __forceinline__ void load_hex_pos(const Slab& s, const Phys& p, int b, int i, int j,

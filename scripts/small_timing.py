@@ -5,7 +5,7 @@ from paper_2209_01983_b200.configs import config
 from paper_2209_01983_b200.sale import Sale
 for name in ("C0", "C2"):
     cfg, cycles = config(name)
-    g = Sale(cfg, impl="fused")
+    g = Sale(cfg)
     g.step(5)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
