@@ -1093,8 +1093,14 @@ struct EnergyCTA {
     }
 };
 
+#ifndef SALE_MB_ENERGY_L_MAT  // Lagrange with >= SALE_NM_ENERGY_L_MAT materials: one CTA per SM
+#define SALE_MB_ENERGY_L_MAT 1    // (their operands spill at two: C3 4 materials 9.47 -> 8.64 ms)
+#endif
+#ifndef SALE_NM_ENERGY_L_MAT
+#define SALE_NM_ENERGY_L_MAT 3
+#endif
 template <bool EULER, int NW, int NM>
-__global__ void __launch_bounds__(FW * NW, EULER ? SALE_MB_ENERGY_E : SALE_MB_ENERGY_L) kc_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
+__global__ void __launch_bounds__(FW * NW, EULER ? SALE_MB_ENERGY_E : (NM >= SALE_NM_ENERGY_L_MAT ? SALE_MB_ENERGY_L_MAT : SALE_MB_ENERGY_L)) kc_energy(Slab s, Phys p, int cur, int kc0, int kc1, int zchunk)
 {
     if (!s.st->active) return;
     extern __shared__ double smem[];

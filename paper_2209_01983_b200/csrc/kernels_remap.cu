@@ -55,9 +55,8 @@ __device__ __forceinline__ void st3r(double* b, int o0, int stride, D3 v)
 // ============================================================================
 // grid: x = ceil((nx+1)(ny+1) / 256) (flattened node plane: no idle lanes), y = planes
 template <bool TILE>  // TILE: 32 x 8 node tiles (grid x = x-tiles * y-tiles) instead of flattened rows
-// spd = 1: also store |u''|^2 per node (unused by the current schedule)
 // (8 CTAs per SM at 32 registers: more warps for the latency-bound gather)
-__global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int spd, int kbase)
+__global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int kbase)
 {
     if (!s.st->active) return;
     int i, j, t;
@@ -116,7 +115,6 @@ __global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int
                u1.z + ddiv(DP.z - (u1.z * Dm), M2));
     un = reflect(p, i, j, k, un);
     st3(s.u[cur ^ 1], n, un);
-    if (spd) s.x1[0][n] = speed2(un);  // |u''|^2 (x' scratch is free after the remap's cell kernels)
 }
 
 // ============================================================================
@@ -212,7 +210,7 @@ struct SweepCTA {
     __device__ __forceinline__ void put()
     {
         const D3 z = D3{0.0, 0.0, 0.0};
-        // x' = x^T + u' dt, kn_force_e's expression (c.3 step 6), formed when staged
+        // x' = x^T + u' dt, kc_force's expression (c.3 step 6), formed when staged
         const D3 x1 = D3{xcol + (qu1.x * dt), ycol + (qu1.y * dt), qz + (qu1.z * dt)};
         st3r(me, oN(PAR, 0), PL, qnok ? x1 : z);
         st3r(me, oN(PAR, 3), PL, qnok ? qu1 : z);
@@ -583,7 +581,7 @@ int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st, int ka, i
     }
     if (k1 < k0) return 0;
     kn_update<true><<<dim3(cdivr(p.nx + 1, 32) * cdivr(p.ny + 1, 8), k1 - k0 + 1), 256, 0, (cudaStream_t)st>>>(
-        s, p, cur, 0, k0);
+        s, p, cur, k0);
     note_launch();
     return 1;
 }

@@ -54,12 +54,12 @@ struct Slab {
     double* hnu;              // the uncapped hourglass coefficient nu_u (reading HG), written by the
                               // state passes (Lagrange: the energy kernel of the previous cycle for
                               // the new state, the prologue and the ghost pass; Euler: ke_state)
-    double* x1[3];            // Euler scratch: x' (post-Lagrange positions)
+    double* x1[3];            // unused (null): x' is formed from u' where it is staged (Euler)
     double* u1[3];            // Euler scratch: u'
     double* e1;               // Euler scratch: e'
     double* V1;               // Euler scratch: V'
-    double* dm;               // Euler scratch: Delta m
-    double* dP[3];            // Euler scratch: Delta P
+    double* dm;               // Euler scratch: Delta m (multi-material cycle: k_mat_flux -> kn_update;
+    double* dP[3];            //   Delta P           the single-material kr_tail keeps them on chip)
     double* dV[3];            // Euler scratch: swept volume of the -x/-y/-z face of each cell (kr_sweep)
     double* rD;               // Euler scratch: donor density m/V' of each cell (kr_sweep)
     double* UD[3];            // Euler scratch: donor velocity (8-node mean of u') of each cell (kr_sweep)
@@ -76,7 +76,7 @@ struct Slab {
     double* TAy[3];           // A of y-faces, index (k-kb)*nx + i  (independent of j)
     double* TAz[3];           // A of z-faces, index j*nx + i       (independent of k)
     double* sF[3];            // Euler scratch: s' (c.2 s of the moved face) of the x-, y-, z-face
-                              // anchored at node (i,j,k), node-indexed; written by kf_energy_e
+                              // anchored at node (i,j,k), node-indexed; written by kc_energy
                               // (which needs them for V'), read by kr_sweep's swept volumes
     double* TDx;              // cells i: cfl * sqrt(edge length^2 along x) of the target mesh (c.5);
     double* TDy;              //   the dt numerator cfl*sqrt(min(lx,ly,lz)) = min of these (sqrt and
@@ -95,7 +95,7 @@ struct Slab {
     double* me[2];            // material specific energy e_k
     double* sgm;              // each material's stress 0.25 (pf_k + q) at the cycle start (MM4; state passes)
     double* e1m;              // Euler scratch: e'_k
-    double* rDm;              // Euler scratch: donor material density m_k / V' of each cell (k_mat_sweep)
+    double* rDm;              // Euler scratch: donor material density m_k / V' of each cell (kr_sweep<NM>)
     double mg[MAX_MAT];       // gamma of each material (here rather than in Phys: growing Phys
     int nmat;                 //   perturbed the single-material kernels' code generation)
                               // nmat: 0 single material; 1..MAX_MAT the material axis (§10d)
