@@ -774,7 +774,8 @@ __global__ void __launch_bounds__(FW * NW, EULER ? SALE_MB_FORCE_E : SALE_MB_FOR
 template <bool EULER, int NW, int NM>
 struct EnergyCTA {
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
-    // node words: Lagrange x^n(3) x'(3) u^n(3) u'(3); Euler x'(3) u^n(3) ubar(3)
+    // node words: Lagrange x^n(3) x'(3) u^n(3) u'(3) (u' replaced by ubar once landed);
+    // Euler x'(3) u^n(3) ubar(3)
     static constexpr int NNW = EULER ? 9 : 12;
     // node-plane slots: Euler 2 (register prefetch, staged one plane ahead: x' and ubar
     // are formed when staged); Lagrange a ring of 3 filled by cp.async two planes ahead
@@ -896,8 +897,15 @@ struct EnergyCTA {
     template <int PAR>
     __device__ __forceinline__ D3 Ub(int off) const  // ubar = 0.5 (u + u')
     {
-        if constexpr (EULER) return ld3s(me + off, oN(PAR, 6), PL);
-        else return scl(0.5, add(Un<PAR>(off), ld3s(me + off, oN(PAR, 9), PL)));
+        return ld3s(me + off, oN(PAR, EULER ? 6 : 9), PL);
+    }
+    // Lagrange: once node plane PAR has landed, the column's own thread replaces u' by
+    // ubar = 0.5 (u + u') (the only use of u' here), once per node instead of once per
+    // cell corner
+    template <int PAR>
+    __device__ __forceinline__ void put_ubar()
+    {
+        st3s(me, oN(PAR, 9), PL, scl(0.5, add(Un<PAR>(0), ld3s(me, oN(PAR, 9), PL))));
     }
 
     // the z-face at this column of node plane B: s' of the moved face, t^n area (Lagrange)
@@ -920,6 +928,7 @@ struct EnergyCTA {
         } else {
             cpa_wait_all();
             __syncthreads();  // plane kz+1 visible; slot B2 (plane kz-1) free
+            put_ubar<B1>();   // read by the cells after the P2 / P3 barrier
         }
         const double m = fm, e = fe, sig = fsig, nu_u = fnu, ax = fax, ay = fay;
         double cf[NM > 0 ? NM : 1], cm[NM > 0 ? NM : 1], ce[NM > 0 ? NM : 1], cs_[NM > 0 ? NM : 1];
@@ -1081,6 +1090,7 @@ struct EnergyCTA {
             fetch(za + 1);
             cpa_wait_all();
             __syncthreads();
+            put_ubar<0>();
             zstate<0>(zA, zs);
             for (int kz = za; kz <= zb; ++kz) {
                 switch ((kz - za) % 3) {

@@ -187,4 +187,6 @@ inline int zchunk_for(long long ctas_xy, int planes, int zc0)
     return zc;
 }
 
+
+
 }  // namespace sale
