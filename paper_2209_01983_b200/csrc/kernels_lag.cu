@@ -39,6 +39,9 @@
 #ifndef SALE_MB_STATE_E
 #define SALE_MB_STATE_E 4
 #endif
+#ifndef SALE_FORCE_XROW  // kc_force: one node row staged beyond the thread rows
+#define SALE_FORCE_XROW 1
+#endif
 #ifndef SALE_MB_FORCE_E
 #define SALE_MB_FORCE_E 2
 #endif
@@ -510,11 +513,14 @@ __global__ void __launch_bounds__(FW * NW, SALE_MB_STATE_E) ke_state(Slab s, Phy
 // ============================================================================
 template <bool EULER, int NW>
 struct ForceCTA {
-    static constexpr int PL = NW * FW, TX = FW - 2, TY = NW - 2;
+    // XR: node rows staged beyond the NW thread rows (row NW, by the first warp row), so
+    // every warp row computes cells (NW rows) and NW-1 rows gather nodes
+    static constexpr int XR = SALE_FORCE_XROW;
+    static constexpr int PL = NW * FW, PLN = (NW + XR) * FW, TX = FW - 2, TY = NW - 2 + XR;
     static constexpr int NNW = EULER ? 3 : 6;  // staged words per node: (x,) u
     // node planes in a ring of 3 slots filled by cp.async two planes ahead
-    __host__ __device__ static constexpr int oN(int par, int c) { return (par * NNW + c) * PL; }
-    static constexpr int OT = 3 * NNW * PL;                  // cell: corner forces t_h (24), m
+    __host__ __device__ static constexpr int oN(int par, int c) { return (par * NNW + c) * PLN; }
+    static constexpr int OT = 3 * NNW * PLN;                 // cell: corner forces t_h (24), m
     __host__ __device__ static constexpr int oT(int h, int c) { return OT + (h * 3 + c) * PL; }
     static constexpr int OM = OT + 24 * PL;
     static constexpr int WORDS = OM + PL + 2 * PAD;
@@ -524,7 +530,7 @@ struct ForceCTA {
     const int cur;
     double* me;
     int i, j, za, zb, ic, jc;
-    long long nbc, cbc, nb;
+    long long nbc, cbc, nb, nbx;  // nbx: the extra staged row's node (i, j + NW), clamped
     double dt;
     bool node_thr, cell_thr, col_in, cellcol_in;
     bool pxm, pxp, pym, pyp;
@@ -556,7 +562,11 @@ struct ForceCTA {
         col_in = i >= 0 && i <= p.nx && j >= 0 && j <= p.ny;
         cellcol_in = i >= 0 && i < p.nx && j >= 0 && j < p.ny;
         node_thr = col_in && ix >= 1 && ix <= TX && iy >= 1 && iy <= TY;
-        cell_thr = cellcol_in && ix <= FW - 2 && iy <= NW - 2;
+        cell_thr = cellcol_in && ix <= FW - 2 && iy <= NW - 2 + XR;
+        {
+            const int jx = clampi(j + NW, 0, p.ny);
+            nbx = (long long)in + (long long)(p.nx + 1) * (jx - (long long)(p.ny + 1) * s.kb);
+        }
         pxm = i >= 1;    // cell i-1 exists (for a node column inside the mesh)
         pxp = i < p.nx;  // cell i exists
         pym = j >= 1;
@@ -571,8 +581,13 @@ struct ForceCTA {
     {
         const int kn = clampi(k, s.kb, s.kb + s.nzn - 1);
         const long long n = nbc + (long long)kn * s.pn;
-        if (!EULER) cpa3(me + oN(SL, 0), PL, s.x[cur], n);
-        cpa3(me + oN(SL, EULER ? 0 : 3), PL, s.u[cur], n);
+        if (!EULER) cpa3(me + oN(SL, 0), PLN, s.x[cur], n);
+        cpa3(me + oN(SL, EULER ? 0 : 3), PLN, s.u[cur], n);
+        if (XR && threadIdx.y == 0) {
+            const long long nx_ = nbx + (long long)kn * s.pn;
+            if (!EULER) cpa3(me + NW * FW + oN(SL, 0), PLN, s.x[cur], nx_);
+            cpa3(me + NW * FW + oN(SL, EULER ? 0 : 3), PLN, s.u[cur], nx_);
+        }
         cpa_commit();
     }
     // cell plane k-1 (sigma, nu_u, m; Euler: table areas) into registers
@@ -590,9 +605,9 @@ struct ForceCTA {
         }
     }
     template <int PAR>
-    __device__ __forceinline__ D3 X(int off) const { return ld3s(me + off, oN(PAR, 0), PL); }
+    __device__ __forceinline__ D3 X(int off) const { return ld3s(me + off, oN(PAR, 0), PLN); }
     template <int PAR>
-    __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oN(PAR, EULER ? 0 : 3), PL); }
+    __device__ __forceinline__ D3 U(int off) const { return ld3s(me + off, oN(PAR, EULER ? 0 : 3), PLN); }
     template <int PAR>
     __device__ __forceinline__ D3 zface() const
     {
@@ -1179,9 +1194,10 @@ int launch_force(const Slab& s, const Phys& p, int cur, Stream st)
     auto go = [&](auto kern, size_t words) {
         const size_t sm = sizeof(double) * words;
         set_smem(kern, sm);
-        const long long xy = (long long)cdiv(p.nx + 1, FW - 2) * cdiv(p.ny + 1, NW_FORCE - 2);
+        constexpr int TY = NW_FORCE - 2 + SALE_FORCE_XROW;
+        const long long xy = (long long)cdiv(p.nx + 1, FW - 2) * cdiv(p.ny + 1, TY);
         const int zc = zchunk_for(xy, kn1 - kn0 + 1, ZCHUNK);
-        dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, NW_FORCE - 2), cdiv(kn1 - kn0 + 1, zc));
+        dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, TY), cdiv(kn1 - kn0 + 1, zc));
         kern<<<grid, dim3(FW, NW_FORCE), sm, (cudaStream_t)st>>>(s, p, cur, kn0, kn1, zc);
         note_launch();
     };
