@@ -171,7 +171,7 @@ struct StateLagCTA {
         me = smem + PAD + iy * FW + ix;
         i = blockIdx.x * TX + ix;
         j = blockIdx.y * TY + iy;
-        za = kc0 + blockIdx.z * zchunk;
+        za = kc0 + zchunk_base(zchunk);
         zb = za + zchunk - 1 < kc1 - 1 ? za + zchunk - 1 : kc1 - 1;
         const int in = i < p.nx ? i : p.nx, jn = j < p.ny ? j : p.ny;
         const int ic = i < p.nx ? i : p.nx - 1, jc = j < p.ny ? j : p.ny - 1;
@@ -368,7 +368,7 @@ struct StateEulerCTA {
         j = blockIdx.y * TY + iy;
         ic = i < p.nx ? i : p.nx - 1;
         jc = j < p.ny ? j : p.ny - 1;
-        za = kc0 + blockIdx.z * zchunk;
+        za = kc0 + zchunk_base(zchunk);
         zb = imin(za + zchunk - 1, kc1 - 1);
         const int in = i < p.nx ? i : p.nx, jn = j < p.ny ? j : p.ny;
         nbn = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
@@ -550,7 +550,7 @@ struct ForceCTA {
         me = smem + PAD + iy * FW + ix;
         i = blockIdx.x * TX - 1 + ix;
         j = blockIdx.y * TY - 1 + iy;
-        za = kn0 + blockIdx.z * zchunk;
+        za = kn0 + zchunk_base(zchunk);
         zb = za + zchunk - 1 < kn1 ? za + zchunk - 1 : kn1;
         const int in = clampi(i, 0, p.nx), jn = clampi(j, 0, p.ny);
         ic = clampi(i, 0, p.nx - 1);
@@ -826,7 +826,7 @@ struct EnergyCTA {
         me = smem + PAD + iy * FW + ix;
         i = blockIdx.x * TX + ix;
         j = blockIdx.y * TY + iy;
-        za = kc0 + blockIdx.z * zchunk;
+        za = kc0 + zchunk_base(zchunk);
         zb = za + zchunk - 1 < kc1 - 1 ? za + zchunk - 1 : kc1 - 1;
         const int in = i < p.nx ? i : p.nx, jn = j < p.ny ? j : p.ny;
         ic = i < p.nx ? i : p.nx - 1;
@@ -1178,7 +1178,7 @@ int launch_state(const Slab& s, const Phys& p, int cur, int gate, Stream st)
             const long long xy = (long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW_STATE - 1);
             const int zc = zchunk_for(xy, kc1 - kc0, ZCHUNK);
             dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW_STATE - 1), cdiv(kc1 - kc0, zc));
-            kern<<<grid, dim3(FW, NW_STATE), sm, (cudaStream_t)st>>>(s, p, cur, kc0, kc1, zc, gate);
+            kern<<<grid, dim3(FW, NW_STATE), sm, (cudaStream_t)st>>>(s, p, cur, kc0, kc1, zorder(zc), gate);
             note_launch();
         };
         if (p.rezone) go(ke_state<NW_STATE, NM>, StateEulerCTA<NW_STATE, NM>::WORDS);
@@ -1198,7 +1198,7 @@ int launch_force(const Slab& s, const Phys& p, int cur, Stream st)
         const long long xy = (long long)cdiv(p.nx + 1, FW - 2) * cdiv(p.ny + 1, TY);
         const int zc = zchunk_for(xy, kn1 - kn0 + 1, ZCHUNK);
         dim3 grid(cdiv(p.nx + 1, FW - 2), cdiv(p.ny + 1, TY), cdiv(kn1 - kn0 + 1, zc));
-        kern<<<grid, dim3(FW, NW_FORCE), sm, (cudaStream_t)st>>>(s, p, cur, kn0, kn1, zc);
+        kern<<<grid, dim3(FW, NW_FORCE), sm, (cudaStream_t)st>>>(s, p, cur, kn0, kn1, zorder(zc));
         note_launch();
     };
     if (p.rezone) go(kc_force<true, NW_FORCE>, ForceCTA<true, NW_FORCE>::WORDS);
@@ -1221,7 +1221,7 @@ int launch_energy(const Slab& s, const Phys& p, int cur, Stream st, int ka, int 
         const long long xy = (long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW_ENERGY - 1);
         const int zc = zchunk_for(xy, kc1 - kc0, ZCHUNK);
         dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW_ENERGY - 1), cdiv(kc1 - kc0, zc));
-        kern<<<grid, dim3(FW, NW_ENERGY), sm, (cudaStream_t)st>>>(s, p, cur, kc0, kc1, zc);
+        kern<<<grid, dim3(FW, NW_ENERGY), sm, (cudaStream_t)st>>>(s, p, cur, kc0, kc1, zorder(zc));
         note_launch();
     };
     by_nmat(s.nmat, [&](auto nm) {

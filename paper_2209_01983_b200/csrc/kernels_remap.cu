@@ -165,7 +165,7 @@ struct SweepCTA {
         kr0 = kr0_;
         kr1 = kr1_;
         const int t0 = kr0 - 1 > 0 ? kr0 - 1 : 0, t1 = kr1 < p.nz - 1 ? kr1 : p.nz - 1;  // cell planes [t0, t1]
-        ta = t0 + blockIdx.z * zchunk;
+        ta = t0 + zchunk_base(zchunk);
         tb = ta + zchunk - 1 < t1 ? ta + zchunk - 1 : t1;
         nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
         cb = (long long)i + (long long)p.nx * (j - (long long)p.ny * s.kb);
@@ -418,7 +418,7 @@ struct TailCTA {
         j = blockIdx.y * TY + iy;
         ka = ka_;
         kb = kb_;
-        za = ka + blockIdx.z * zchunk;
+        za = ka + zchunk_base(zchunk);
         zb = za + zchunk - 1 < kb ? za + zchunk - 1 : kb;
         nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
         node_thr = ix < TX && iy < TY && i <= p.nx && j <= p.ny;
@@ -551,7 +551,7 @@ static void sweep_launch(const Slab& s, const Phys& p, int cur, int kr0, int kr1
     const int t0 = kr0 - 1 > 0 ? kr0 - 1 : 0, t1 = kr1 < p.nz - 1 ? kr1 : p.nz - 1;
     const int zc = zchunk_for((long long)cdivr(p.nx, RW - 1) * cdivr(p.ny, NW - 1), t1 - t0 + 1, RZ);
     dim3 grid(cdivr(p.nx, RW - 1), cdivr(p.ny, NW - 1), cdivr(t1 - t0 + 1, zc));
-    kern<<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zc);
+    kern<<<grid, dim3(RW, NW), sm, cs>>>(s, p, cur, kr0, kr1, zorder(zc));
     note_launch();
 }
 
@@ -608,7 +608,7 @@ int launch_rtail(const Slab& s, const Phys& p, int cur, Stream st, int ka, int k
     const long long xy = (long long)cdivr(p.nx + 1, RW - 1) * cdivr(p.ny + 1, NW - 1);
     const int zc = zchunk_for(xy, k1 - k0 + 1, RZ);
     dim3 grid(cdivr(p.nx + 1, RW - 1), cdivr(p.ny + 1, NW - 1), cdivr(k1 - k0 + 1, zc));
-    kern<<<grid, dim3(RW, NW), sm, (cudaStream_t)st>>>(s, p, cur, k0, k1, zc);
+    kern<<<grid, dim3(RW, NW), sm, (cudaStream_t)st>>>(s, p, cur, k0, k1, zorder(zc));
     note_launch();
     return 1;
 }

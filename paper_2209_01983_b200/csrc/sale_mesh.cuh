@@ -46,6 +46,17 @@ __device__ __forceinline__ void st3(double* const a[3], long long n, D3 v)
     a[2][n] = v.z;
 }
 
+// the first plane offset of this CTA's z-chunk.  A launch passes zchunk < 0 to run its
+// chunks in reverse order (consecutive kernels alternate, so each starts on the planes
+// the previous one finished last, whose data are still in L2); zchunk is made positive.
+// The order of the chunks never changes a result (each CTA's work is independent).
+__device__ __forceinline__ int zchunk_base(int& zchunk)
+{
+    const bool rev = zchunk < 0;
+    if (rev) zchunk = -zchunk;
+    return (int)(rev ? gridDim.z - 1 - blockIdx.z : blockIdx.z) * zchunk;
+}
+
 // asynchronous global -> shared copies (cp.async, 8 B): a node plane is staged
 // without passing through registers (no prefetch registers held across a step)
 __device__ __forceinline__ void cpa8(double* sdst, const double* gsrc)
@@ -180,6 +191,16 @@ __device__ __forceinline__ void mix_eos(const Slab& s, const double* f, const do
 // small ones shorter chunks (down to 4) so the grid still covers the 148 SMs twice
 // (a z-march is a chain of dependent plane steps; its length is the small-mesh time).
 // Chunking changes only which CTA computes a plane, never the arithmetic.
+#ifndef SALE_ZALT
+#define SALE_ZALT 1
+#endif
+// host: the zchunk argument of the next z-march launch, its chunk order alternating
+// from launch to launch (zchunk_base; performance only)
+inline int zorder(int zc)
+{
+    static thread_local unsigned n = 0;
+    return (SALE_ZALT && (n++ & 1u)) ? -zc : zc;
+}
 inline int zchunk_for(long long ctas_xy, int planes, int zc0)
 {
     int zc = zc0;
