@@ -359,6 +359,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-allcore", type=int, default=1, help="also time one oracle per host core (0: off)")
     ap.add_argument("--no-extras", action="store_true", help="skip the P0-state, C3 and golden-check legs")
+    ap.add_argument("--halo", default="copy", choices=["copy", "peer"],
+                    help="per-cycle halo exchange with N > 1: NCCL send/recv (copy) or the producing kernels "
+                         "storing into the neighbours' ghost planes over NVLink (peer)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -378,6 +381,7 @@ def main():
     if world > 1:
         dist.init_process_group("gloo")  # plumbing only: id broadcast, barrier, max
     cfg, _ = configs.config(args.config, world)
+    cfg["halo"] = S.HALO_PEER if args.halo == "peer" else S.HALO_COPY
     nid = None
     if world > 1:
         obj = [S.nccl_unique_id() if rank == 0 else None]
@@ -495,6 +499,7 @@ def main():
             "config": {"workload": workload_name(args.config), "global_cells": gcells,
                        "cells_per_gpu": local_cells, "mesh": [cfg["nx"], cfg["ny"], cfg["nz"]],
                        "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                       "halo": args.halo if world > 1 else "none (one slab)",
                        "step": "one SALE cycle",
                        "state": f"Sedov initial state (c.6), cycles {args.warmup + 1}..{args.warmup + args.steps}"
                                 " (the shock near the origin; the bulk is quiescent -- p0_state times a "

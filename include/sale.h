@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define SALE_ABI_VERSION 3
+#define SALE_ABI_VERSION 4
 #define SALE_MAX_MAT 4       /* materials per cell (multi-material mode)            */
 
 /* status codes */
@@ -58,6 +58,15 @@ extern "C" {
 #define SALE_ENEGMASS 7      /* remapped mass m'' not > 0 (c.4 step 3)              */
 #define SALE_EPOISONED 8     /* context unusable after an earlier error             */
 #define SALE_EREPLICA 9      /* replicated interface node planes differ (self-check) */
+
+/* halo exchange modes (sale_params.halo) */
+#define SALE_HALO_COPY 0     /* X1 as messages: grouped ncclSend/ncclRecv of whole ghost
+                                planes between ranks, device copies between emulated slabs */
+#define SALE_HALO_PEER 1     /* X1 fused into the kernels: the kernels that produce the planes
+                                a neighbour needs also store them straight into its ghost
+                                planes (the neighbour rank's workspace mapped over NVLink
+                                with CUDA IPC, or the neighbouring emulated slab), then
+                                signal it with one system-scope counter per cycle          */
 
 /* rezone modes */
 #define SALE_LAGRANGE 0
@@ -146,6 +155,16 @@ typedef struct sale_params {
                                  separations; the corner force -nu sum_m Gamma_m g_m
                                  damps the four hourglass modes g_m of u^n, its work
                                  heats the cell (total energy is conserved).       */
+    int32_t halo;             /* SALE_HALO_COPY (0) or SALE_HALO_PEER (1): how the ghost
+                                 planes of the new state reach the neighbours every
+                                 cycle (the paper's per-cycle
+                                 exchange).  PEER with nranks > 1
+                                 needs every rank's workspace in one cudaMalloc'd
+                                 allocation (CUDA IPC) and peer access between the
+                                 devices (NVLink / NVSwitch); the exchange at the start
+                                 of each sale_step call (and of the first cycle) stays
+                                 a copy exchange.  Results are identical either way.
+                                 Boundary-first cycles (overlap) apply to COPY only.  */
 } sale_params;
 
 typedef struct sale_ctx sale_ctx;

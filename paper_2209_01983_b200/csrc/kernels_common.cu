@@ -236,6 +236,67 @@ __global__ void k_commit(DevState* d, Phys p)
 
 __global__ void k_reset_good(DevState* d) { d->good = 0; }
 
+// ---------------------------------------------------------------- peer-store halo
+// (ranks).  After a cycle's producer kernels stored their planes into the
+// neighbours' ghost planes: one increment of each neighbour's arrival counter at system
+// scope (the producers are complete and their NVLink stores performed when this kernel
+// runs: stream order).  Before the next cycle's state pass reads the ghost planes:
+// wait until every neighbour's count reaches the cycles consumed + 1.  A cycle that is
+// not in flight (finished / failed: the same on every rank, dt and the error key being
+// all-reduced) neither signals nor waits.  The wait gives up after 60 s (a lost peer)
+// with SALE_ENCCL instead of hanging the device.
+__global__ void k_halo_signal(DevState* d, const HaloPeer* hp)
+{
+    if (!d->active) return;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        unsigned long long* f = hp->flag[side];
+        if (f) {
+            __threadfence_system();
+            atomicAdd_system(f, 1ull);
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long global_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void k_halo_wait(DevState* d, int first, int sides)
+{
+    if (first) {  // the copy exchange filled the ghost planes: absorb earlier arrivals
+        d->halo_seen[0] = ld_acquire_sys(&d->halo_in[0]);
+        d->halo_seen[1] = ld_acquire_sys(&d->halo_in[1]);
+        return;
+    }
+    if (!d->active) return;
+    const unsigned long long t0 = global_ns();
+    for (int side = 0; side < 2; ++side) {
+        if (!((sides >> side) & 1)) continue;  // no neighbour on this side
+        const unsigned long long want = d->halo_seen[side] + 1;
+        while (ld_acquire_sys(&d->halo_in[side]) < want) {
+            if (global_ns() - t0 > 60000000000ull) {
+                d->status = S_ENCCL;
+                d->err_cycle = d->cycle;
+                d->err_cell = -1;
+                d->active = 0;
+                return;
+            }
+            __nanosleep(200);
+        }
+        d->halo_seen[side] = want;
+    }
+}
+
 int launch_prep(DevState* d, Stream st)
 {
     k_prep<<<1, 1, 0, (cudaStream_t)st>>>(d);
@@ -251,6 +312,18 @@ int launch_begin(DevState* d, const Phys& p, Stream st)
 int launch_commit(DevState* d, const Phys& p, Stream st)
 {
     k_commit<<<1, 1, 0, (cudaStream_t)st>>>(d, p);
+    note_launch();
+    return 1;
+}
+int launch_halo_signal(DevState* d, const HaloPeer* hp_dev, Stream st)
+{
+    k_halo_signal<<<1, 1, 0, (cudaStream_t)st>>>(d, hp_dev);
+    note_launch();
+    return 1;
+}
+int launch_halo_wait(DevState* d, int first, int sides, Stream st)
+{
+    k_halo_wait<<<1, 1, 0, (cudaStream_t)st>>>(d, first, sides);
     note_launch();
     return 1;
 }

@@ -735,8 +735,14 @@ struct ForceCTA {
                     st3(s.u1, n, un);
                 } else {
                     const D3 x = X<B0>(0);
-                    st3(s.x[cur ^ 1], n, d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt)));
+                    const D3 xn = d3(x.x + (un.x * dt), x.y + (un.y * dt), x.z + (un.z * dt));
+                    st3(s.x[cur ^ 1], n, xn);
                     st3(s.u[cur ^ 1], n, un);
+                    if (s.hp) {  // peer-store halo: the neighbours' ghost node planes
+                        const long long q = (long long)i + (long long)(p.nx + 1) * j;
+                        halo_node3(s, s.hp->x, cur ^ 1, kz, q, xn);
+                        halo_node3(s, s.hp->u, cur ^ 1, kz, q, un);
+                    }
                 }
             }
             have = false;
@@ -1069,13 +1075,21 @@ struct EnergyCTA {
                     const double e1k = (cf[a] > 0.0 && cm[a] > 0.0)
                                            ? ce[a] - ddiv((((cs_[a] * W) + Wh) * dt) * cf[a], cm[a])
                                            : ce[a];
-                    if (EULER) s.e1m[cc + a * mat_stride(s)] = e1k;
-                    else s.me[cur ^ 1][cc + a * mat_stride(s)] = e1k;
+                    if (EULER) {
+                        s.e1m[cc + a * mat_stride(s)] = e1k;
+                    } else {
+                        s.me[cur ^ 1][cc + a * mat_stride(s)] = e1k;
+                        if (s.hp) halo_cell(s, s.hp->me, cur ^ 1, a, kz, (long long)i + (long long)p.nx * j, e1k);
+                    }
                 }
             } else {
                 const double e1 = e - ddiv(((sig * W) + Wh) * dt, m);
-                if (EULER) s.e1[cc] = e1;
-                else s.e[cur ^ 1][cc] = e1;
+                if (EULER) {
+                    s.e1[cc] = e1;
+                } else {
+                    s.e[cur ^ 1][cc] = e1;
+                    if (s.hp) halo_cell(s, s.hp->e, cur ^ 1, 0, kz, (long long)i + (long long)p.nx * j, e1);
+                }
             }
             if (EULER) s.V1[cc] = V1;
         }

@@ -118,16 +118,31 @@ __global__ void k_mat_flux(Slab s, Phys p, int cur, int kr0, int kr1)
     }
     if (k >= s.k0 && k < s.k1 && (bad || !(m2 > 0.0) || !(VV > 0.0)))
         atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, k));
+    // the material state of the owned cells (the ghost cells' come from the exchange);
+    // the cell total m'' of every cell (kn_update gathers the ghost cells' too)
+    const bool own = k >= s.k0 && k < s.k1;
+    const long long q = (long long)i + (long long)p.nx * j;
 #pragma unroll
     for (int a = 0; a < NM; ++a) {
+        if (!own) break;
         const long long ca = c + a * st;
         const double mm2 = s.mm[cur][ca] + dmk[a];
         const double e1 = s.e1m[ca];
-        s.me[cur ^ 1][ca] = (mm2 > 0.0) ? e1 + ddiv(dEk[a] - (e1 * dmk[a]), mm2) : 0.0;
-        s.mf[cur ^ 1][ca] = ddiv(vm2[a], VV);
+        const double me2 = (mm2 > 0.0) ? e1 + ddiv(dEk[a] - (e1 * dmk[a]), mm2) : 0.0;
+        const double mf2 = ddiv(vm2[a], VV);
+        s.me[cur ^ 1][ca] = me2;
+        s.mf[cur ^ 1][ca] = mf2;
         s.mm[cur ^ 1][ca] = mm2;
+        if (s.hp) {  // peer-store halo: the neighbours' ghost cell planes
+            halo_cell(s, s.hp->me, cur ^ 1, a, k, q, me2);
+            halo_cell(s, s.hp->mf, cur ^ 1, a, k, q, mf2);
+            halo_cell(s, s.hp->mm, cur ^ 1, a, k, q, mm2);
+        }
     }
     s.m[cur ^ 1][c] = m2;
+    // (an owned cell's m'' is also a neighbour's ghost cell: bit-identical to the value
+    // the neighbour forms for it itself, so the two stores never disagree)
+    if (s.hp && own) halo_cell(s, s.hp->m, cur ^ 1, 0, k, q, m2);
     s.dm[c] = dm;
     st3(s.dP, c, dP);
 }

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(256, 8) kn_update(Slab s, Phys p, int cur, int
                u1.z + ddiv(DP.z - (u1.z * Dm), M2));
     un = reflect(p, i, j, k, un);
     st3(s.u[cur ^ 1], n, un);
+    if (s.hp) halo_node3(s, s.hp->u, cur ^ 1, k, t, un);
 }
 
 // ============================================================================
@@ -385,8 +386,14 @@ __device__ __forceinline__ void flux_cell(const Slab& s, const Phys& p, int cur,
     if (own) {
         if (t >= s.k0 && t < s.k1 && !(m2 > 0.0))
             atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, i, j, t));
-        s.e[cur ^ 1][c] = e1 + ddiv(dE - (e1 * dm), m2);
+        const double e2 = e1 + ddiv(dE - (e1 * dm), m2);
+        s.e[cur ^ 1][c] = e2;
         s.m[cur ^ 1][c] = m2;
+        if (s.hp) {  // peer-store halo: the neighbours' ghost cell planes
+            const long long q = (long long)i + (long long)p.nx * j;
+            halo_cell(s, s.hp->e, cur ^ 1, 0, t, q, e2);
+            halo_cell(s, s.hp->m, cur ^ 1, 0, t, q, m2);
+        }
     }
 }
 
@@ -480,7 +487,7 @@ struct TailCTA {
         if (cell_col && pz) {
             double dm, m2;
             D3 dP;
-            flux_cell(s, p, cur, i - 1, j - 1, t, own_col && t >= ka && t <= kb, dm, dP, m2);
+            flux_cell(s, p, cur, i - 1, j - 1, t, own_col && t >= ka && t <= kb && t < s.k1, dm, dP, m2);
             me[oC(PAR, 0)] = dm;
             me[oC(PAR, 1)] = dP.x;
             me[oC(PAR, 2)] = dP.y;
@@ -501,6 +508,7 @@ struct TailCTA {
                        u1.z + ddiv(DP.z - (u1.z * Dm), M2));
             un = reflect(p, i, j, t, un);
             st3(s.u[cur ^ 1], n, un);
+            if (s.hp) halo_node3(s, s.hp->u, cur ^ 1, t, (long long)i + (long long)(p.nx + 1) * j, un);
         }
         have = false;
         Dp = 0.0;

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -65,6 +66,12 @@ struct sale_ctx {
     // finishes; evB = boundary planes done, evX = exchange done
     cudaStream_t side = nullptr;
     cudaEvent_t evB = nullptr, evX = nullptr;
+    // peer-store halo (sale_params.halo = SALE_HALO_PEER): per slab its device table of
+    // the neighbours' arrays; ranks: the neighbours' workspaces mapped by CUDA IPC, and
+    // which neighbours exist (bit 0 lower, bit 1 upper)
+    std::vector<sale::HaloPeer*> hp_dev;
+    void* ipc[2] = {nullptr, nullptr};
+    int peer_sides = 0;
 };
 
 namespace {
@@ -116,6 +123,7 @@ bool params_ok(const sale_params* p)
     if (p->local_slabs < 1 || (p->nranks > 1 && p->local_slabs != 1)) return false;
     if (!(p->hg >= 0.0)) return false;
     if (p->overlap < -1 || p->overlap > 1) return false;
+    if (p->halo != SALE_HALO_COPY && p->halo != SALE_HALO_PEER) return false;
     int T = p->nranks * p->local_slabs;
     if (p->nz < T) return false;
     if (T > 1 && p->nz / T < ghost_depth(p)) return false;  // every slab owns >= g planes
@@ -239,6 +247,7 @@ size_t total_bytes(const sale_params* p)
     layout_slabs(p, v);
     size_t total = align_up(sizeof(DevState));
     for (auto& s : v) total += carve_slab(p, s, nullptr);
+    if (p->halo == SALE_HALO_PEER) total += v.size() * align_up(sizeof(sale::HaloPeer));  // peer tables
     return total;
 }
 
@@ -496,6 +505,7 @@ int reduce_keys(sale_ctx* c)
 
 bool overlap_on(const sale_ctx* c)
 {
+    if (c->prm.halo == SALE_HALO_PEER) return false;  // no exchange to overlap
     const int o = c->prm.overlap;
     const bool multi = c->prm.nranks > 1 || c->prm.local_slabs > 1;
     return multi && (o > 0 || (o == 0 && c->prm.nranks > 1));
@@ -508,6 +518,112 @@ int overlap_resources(sale_ctx* c)
     if (!rc && !c->evB) rc = cuda_check(c, cudaEventCreateWithFlags(&c->evB, cudaEventDisableTiming), "event");
     if (!rc && !c->evX) rc = cuda_check(c, cudaEventCreateWithFlags(&c->evX, cudaEventDisableTiming), "event");
     return rc;
+}
+
+// ---- peer-store halo (SALE_HALO_PEER) ----------------------------------------
+// side 0 / 1 of table h: the arrays of neighbour slab P (in its owner's address space as
+// mapped here) that receive the planes of the per-cycle exchange (plan_fields, full = 0)
+void fill_side(const sale_ctx* c, const Slab& P, int side, sale::HaloPeer& h)
+{
+    const bool euler = c->prm.rezone == SALE_EULER;
+    const bool mat = c->prm.nmat > 0;
+    for (int b = 0; b < 2; ++b) {
+        for (int a = 0; a < 3; ++a) {
+            h.x[side][b][a] = euler ? nullptr : P.x[b][a];
+            h.u[side][b][a] = P.u[b][a];
+        }
+        h.m[side][b] = euler ? P.m[b] : nullptr;
+        h.e[side][b] = P.e[b];
+        h.mf[side][b] = mat && euler ? P.mf[b] : nullptr;
+        h.mm[side][b] = mat && euler ? P.mm[b] : nullptr;
+        h.me[side][b] = mat ? P.me[b] : nullptr;
+    }
+    h.mstride[side] = P.pc * (long long)P.nzc;
+    h.kb[side] = P.kb;
+}
+
+// ranks: map the neighbours' workspaces (CUDA IPC handles of the allocations holding
+// them, exchanged with one ncclAllGather) and fill the rank's table from their layout
+int ipc_neighbours(sale_ctx* c, sale::HaloPeer& h)
+{
+    typedef int (*RangeFn)(unsigned long long*, size_t*, unsigned long long);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess)
+        return set_err(c, SALE_ECUDA, "peer halo: cuMemGetAddressRange unavailable");
+    unsigned long long abase = 0;
+    size_t asz = 0;
+    if (((RangeFn)fn)(&abase, &asz, (unsigned long long)(uintptr_t)c->prm.workspace) != 0)
+        return set_err(c, SALE_ECUDA, "peer halo: workspace allocation range");
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        unsigned long long off;
+        char pad[128 - sizeof(cudaIpcMemHandle_t) - 8];
+    };
+    static_assert(sizeof(Rec) == 128, "IPC record");
+    Rec mine;
+    std::memset(&mine, 0, sizeof mine);
+    int rc = cuda_check(c, cudaIpcGetMemHandle(&mine.h, (void*)(uintptr_t)abase),
+                        "peer halo: cudaIpcGetMemHandle (the workspace must be cudaMalloc memory)");
+    if (rc) return rc;
+    mine.off = (unsigned long long)((uintptr_t)c->prm.workspace - abase);
+    const int n = c->prm.nranks, r = c->prm.rank;
+    char* dbuf = nullptr;
+    if ((rc = cuda_check(c, cudaMalloc((void**)&dbuf, sizeof(Rec) * (n + 1)), "peer halo: scratch"))) return rc;
+    std::vector<Rec> all(n);
+    rc = cuda_check(c, cudaMemcpy(dbuf, &mine, sizeof mine, cudaMemcpyHostToDevice), "peer halo: copy");
+    if (!rc)
+        rc = nccl_check(c, ncclAllGather(dbuf, dbuf + sizeof(Rec), sizeof(Rec), ncclUint8, c->comm, c->stream),
+                        "peer halo: handle allgather");
+    if (!rc) rc = cuda_check(c, cudaStreamSynchronize(c->stream), "peer halo: sync");
+    if (!rc)
+        rc = cuda_check(c, cudaMemcpy(all.data(), dbuf + sizeof(Rec), sizeof(Rec) * n, cudaMemcpyDeviceToHost),
+                        "peer halo: copy");
+    cudaFree(dbuf);
+    if (rc) return rc;
+    for (int side = 0; side < 2; ++side) {
+        const int peer = r + (side ? 1 : -1);
+        if (peer < 0 || peer >= n) continue;
+        void* mp = nullptr;
+        rc = cuda_check(c, cudaIpcOpenMemHandle(&mp, all[peer].h, cudaIpcMemLazyEnablePeerAccess),
+                        "peer halo: cudaIpcOpenMemHandle");
+        if (rc) return rc;
+        c->ipc[side] = mp;
+        char* pws = static_cast<char*>(mp) + all[peer].off;
+        sale_params qp = c->prm;
+        qp.rank = peer;
+        std::vector<Slab> v;
+        layout_slabs(&qp, v);
+        Slab P = v[0];
+        carve_slab(&qp, P, pws + align_up(sizeof(DevState)));
+        fill_side(c, P, side, h);
+        // we are our lower neighbour's upper neighbour: its halo_in[1], and vice versa
+        h.flag[side] = &reinterpret_cast<DevState*>(pws)->halo_in[1 - side];
+        c->peer_sides |= 1 << side;
+    }
+    return SALE_OK;
+}
+
+// build every slab's table (emulated slabs: the neighbouring slabs of this context;
+// ranks: the mapped neighbours) and point the slabs at them
+int peer_tables(sale_ctx* c)
+{
+    const size_t L = c->slabs.size();
+    std::vector<sale::HaloPeer> h(L);
+    for (auto& t : h) std::memset(&t, 0, sizeof t);
+    for (size_t l = 0; l < L; ++l) {
+        if (l > 0) fill_side(c, c->slabs[l - 1], 0, h[l]);
+        if (l + 1 < L) fill_side(c, c->slabs[l + 1], 1, h[l]);
+    }
+    int rc = SALE_OK;
+    if (c->prm.nranks > 1 && (rc = ipc_neighbours(c, h[0]))) return rc;
+    for (size_t l = 0; l < L; ++l) {
+        rc = cuda_check(c, cudaMemcpy(c->hp_dev[l], &h[l], sizeof h[l], cudaMemcpyHostToDevice), "peer table");
+        if (rc) return rc;
+        c->slabs[l].hp = c->hp_dev[l];
+    }
+    return SALE_OK;
 }
 
 // The planes of a slab the exchange sends and the slab's last kernel writes:
@@ -564,7 +680,14 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first)
     const bool euler = c->prm.rezone == SALE_EULER;
     const bool ov = overlap_on(c);
     if (ov && (rc = overlap_resources(c))) return rc;
-    int pr = prof_open(c, SALE_K_LAGRANGE);
+    const bool peer = c->prm.halo == SALE_HALO_PEER;
+    int pr;
+    if (peer && c->peer_sides) {  // ranks: the neighbours' planes of the previous cycle landed
+        pr = prof_open(c, SALE_K_HALO);
+        c->launches += sale::launch_halo_wait(c->dstate, first ? 1 : 0, c->peer_sides, st);
+        prof_close(c, pr);
+    }
+    pr = prof_open(c, SALE_K_LAGRANGE);
     for (auto& s : c->slabs) c->launches += sale::launch_state(s, c->phys, b, first ? 0 : 1, st);
     prof_close(c, pr);
     pr = prof_open(c, SALE_K_HALO);
@@ -589,6 +712,14 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first)
         }
     }
     if ((rc = launch_check(c))) return rc;
+    if (!ov && peer) {  // the producers stored the ghost planes; ranks: signal the neighbours
+        if (c->peer_sides) {
+            pr = prof_open(c, SALE_K_HALO);
+            c->launches += sale::launch_halo_signal(c->dstate, c->hp_dev[0], st);
+            prof_close(c, pr);
+        }
+        return launch_check(c);
+    }
     if (!ov) {
         pr = prof_open(c, SALE_K_HALO);
         if ((rc = exchange(c, b ^ 1, false))) return rc;
@@ -874,8 +1005,14 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
     size_t off = align_up(sizeof(DevState));
     for (auto& s : c->slabs) {
         s.st = c->dstate;
+        s.hp = nullptr;
         off += carve_slab(p, s, base + off);
     }
+    if (p->halo == SALE_HALO_PEER)
+        for (size_t l = 0; l < c->slabs.size(); ++l) {
+            c->hp_dev.push_back(reinterpret_cast<sale::HaloPeer*>(base + off));
+            off += align_up(sizeof(sale::HaloPeer));
+        }
     int rc = cuda_check(c, cudaHostAlloc((void**)&c->hstate, sizeof(DevState), cudaHostAllocDefault),
                         "cudaHostAlloc");
     if (rc) {
@@ -900,6 +1037,7 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
     }
     rc = cuda_check(c, cudaMemcpyAsync(c->dstate, c->hstate, sizeof(DevState), cudaMemcpyHostToDevice, c->stream),
                     "state init");
+    if (!rc && p->halo == SALE_HALO_PEER) rc = peer_tables(c);
     for (auto& s : c->slabs) {
         if (rc) break;
         c->launches += sale::launch_init_tables(s, ph, (sale::Stream)c->stream);
@@ -915,6 +1053,8 @@ int32_t sale_create(const sale_params* p, sale_ctx** out)
     if (!rc && ph.rezone && !(ph.diag_areas && ph.diag_jumps))
         rc = set_err(c, SALE_EINVAL, "target mesh tables are not axis-aligned");
     if (rc) {
+        for (auto m : c->ipc)
+            if (m) cudaIpcCloseMemHandle(m);
         if (c->comm) ncclCommDestroy(c->comm);
         cudaFreeHost(c->hstate);
         delete c;
@@ -1083,7 +1223,9 @@ int32_t sale_set_clock(sale_ctx* c, double t, double dt_last, int64_t cycle)
     c->hstate->dt_prev = dt_last;
     c->hstate->cycle = cycle;
     c->hstate->finished = (c->prm.t_end > 0.0 && t >= c->prm.t_end) ? 1 : 0;
-    rc = cuda_check(c, cudaMemcpyAsync(c->dstate, c->hstate, sizeof(DevState), cudaMemcpyHostToDevice, c->stream),
+    // (the clock and status only: the peer-store halo counters stay the device's)
+    rc = cuda_check(c, cudaMemcpyAsync(c->dstate, c->hstate, offsetof(DevState, halo_in), cudaMemcpyHostToDevice,
+                                       c->stream),
                     "set_clock");
     if (rc) return rc;
     return cuda_check(c, cudaStreamSynchronize(c->stream), "set_clock sync");
@@ -1150,6 +1292,8 @@ void sale_destroy(sale_ctx* c)
     if (!c) return;
     DeviceGuard guard(c->prm.device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto m : c->ipc)
+        if (m) cudaIpcCloseMemHandle(m);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->hstate) cudaFreeHost(c->hstate);
     for (auto& p : c->pending) {

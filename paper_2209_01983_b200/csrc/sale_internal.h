@@ -38,6 +38,34 @@ struct DevState {
     int good;                 // committed cycles since the last host read
     long long err_cycle;      // cycle in which status became non-zero
     long long err_cell;       // global linear cell index (-1 if none)
+    // peer-store halo between ranks (sale_params.halo = SALE_HALO_PEER): halo_in[side] counts
+    // the cycles whose planes the lower (0) / upper (1) neighbour has stored into this
+    // rank's ghost planes (the neighbour adds 1 at system scope after its producers);
+    // halo_seen[side] the ones this rank has consumed
+    unsigned long long halo_in[2];
+    unsigned long long halo_seen[2];
+};
+
+// Peer-store halo (sale_params.halo = SALE_HALO_PEER, the paper's
+// halo exchange P:372-375 fused into the kernels that produce the planes): the arrays
+// of the lower (side 0) and upper (side 1) neighbour slab -- another rank's workspace
+// mapped over NVLink (CUDA IPC), or the neighbouring emulated slab on this device --
+// into whose ghost planes the producer kernels store the planes the copy exchange
+// would send.  Null pointers: no neighbour on that side (or the field does not exist).
+// Device-resident (one per slab, in the workspace); Slab::hp points to it.
+struct HaloPeer {
+    double* x[2][2][3];       // [side][buffer][axis]: node positions (Lagrange)
+    double* u[2][2][3];       // node velocities
+    double* m[2][2];          // cell mass (Euler)
+    double* e[2][2];          // specific internal energy
+    double* mf[2][2];         // material fractions / masses (Euler) and energies, material k
+    double* mm[2][2];         //   at + k * mstride[side] (the neighbour's material stride)
+    double* me[2][2];
+    long long mstride[2];
+    int kb[2];                // the neighbour's local plane base (its global plane k is
+                              // local plane k - kb)
+    unsigned long long* flag[2];  // ranks: the neighbour's DevState::halo_in entry for this
+                                  // rank (lower neighbour: its [1], upper: its [0]); else null
 };
 
 // One z-slab of the mesh with its ghost planes, by value into kernels.
@@ -100,6 +128,7 @@ struct Slab {
     int nmat;                 //   perturbed the single-material kernels' code generation)
                               // nmat: 0 single material; 1..MAX_MAT the material axis (§10d)
     DevState* st;
+    const HaloPeer* hp;       // peer-store halo: the neighbours' arrays (null: copy exchange)
 };
 
 // Steinberg model parameters (copy of sale_steinberg_params, by value into the kernel)
@@ -166,6 +195,12 @@ int launch_rtail(const Slab& s, const Phys& p, int cur, Stream st, int ka = -1, 
 // R4 over the owned node planes, or the sub-range [ka, kb]
 int launch_kn_update(const Slab& s, const Phys& p, int cur, Stream st, int ka = -1, int kb = -1);
 int launch_mat_init(const Slab& s, const Phys& p, Stream st);
+// peer-store halo between ranks: signal the neighbours that this cycle's planes are
+// stored (after the cycle's producer kernels); wait for theirs before the next cycle
+// reads the ghost planes (first = 1: the first cycle of a sale_step call, whose ghost
+// planes come from the copy exchange: absorb, no wait)
+int launch_halo_signal(DevState* d, const HaloPeer* hp_dev, Stream st);
+int launch_halo_wait(DevState* d, int first, int sides, Stream st);  // sides: bit 0 lower, 1 upper
 int launch_mat_total(const Slab& s, const Phys& p, int cur, Stream st);
 
 }  // namespace sale

@@ -46,6 +46,50 @@ __device__ __forceinline__ void st3(double* const a[3], long long n, D3 v)
     a[2][n] = v.z;
 }
 
+// ---- peer-store halo (HaloPeer, sale_internal.h) --------------------------------
+// The neighbour sides that receive global node plane k (bit 0: lower, its ghost
+// planes [k0+1, k0+g]; bit 1: upper, [k1-g, k1-1]) and cell plane k ([k0, k0+g) /
+// [k1-g, k1)): the planes the copy exchange sends (build_plan).
+__device__ __forceinline__ int halo_sides_node(const Slab& s, int k)
+{
+    return ((k >= s.k0 + 1 && k <= s.k0 + s.g) ? 1 : 0) | ((k >= s.k1 - s.g && k <= s.k1 - 1) ? 2 : 0);
+}
+__device__ __forceinline__ int halo_sides_cell(const Slab& s, int k)
+{
+    return ((k >= s.k0 && k < s.k0 + s.g) ? 1 : 0) | ((k >= s.k1 - s.g && k < s.k1) ? 2 : 0);
+}
+// store node value v (three components of arrays a[side][b]) of global plane k,
+// in-plane index q, into the neighbours' ghost planes
+__device__ __forceinline__ void halo_node3(const Slab& s, double* const (*a)[2][3], int b, int k, long long q,
+                                           D3 v)
+{
+    const int sides = halo_sides_node(s, k);
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        if (!((sides >> side) & 1)) continue;
+        double* const* d = a[side][b];
+        double* const d0 = d[0];
+        if (!d0) continue;
+        const long long o = (long long)(k - s.hp->kb[side]) * s.pn + q;
+        d0[o] = v.x;
+        d[1][o] = v.y;
+        d[2][o] = v.z;
+    }
+}
+// cell value v of array a[side][b] (+ material k's offset), global plane k, in-plane q
+__device__ __forceinline__ void halo_cell(const Slab& s, double* const (*a)[2], int b, int mat, int k, long long q,
+                                          double v)
+{
+    const int sides = halo_sides_cell(s, k);
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        if (!((sides >> side) & 1)) continue;
+        double* const d = a[side][b];
+        if (!d) continue;
+        d[(long long)(k - s.hp->kb[side]) * s.pc + q + mat * s.hp->mstride[side]] = v;
+    }
+}
+
 // the first plane offset of this CTA's z-chunk.  A launch passes zchunk < 0 to run its
 // chunks in reverse order (consecutive kernels alternate, so each starts on the planes
 // the previous one finished last, whose data are still in L2); zchunk is made positive.

@@ -23,6 +23,7 @@ LAGRANGE, EULER = 0, 1
 FIELDS = {"X": 0, "Y": 1, "Z": 2, "UX": 3, "UY": 4, "UZ": 5, "NODE_MASS": 6,
           "MASS": 7, "E": 8, "RHO": 9, "VOL": 10, "P": 11, "Q": 12, "CS": 13}
 MAX_MAT = 4
+HALO_COPY, HALO_PEER = 0, 1  # sale_params.halo
 for _m in range(MAX_MAT):  # material fields (nmat >= 1): volume fraction, mass, specific energy
     FIELDS[f"MAT_F{_m}"], FIELDS[f"MAT_M{_m}"], FIELDS[f"MAT_E{_m}"] = 16 + _m, 20 + _m, 24 + _m
 NODE_FIELDS = ("X", "Y", "Z", "UX", "UY", "UZ", "NODE_MASS")
@@ -44,7 +45,8 @@ class SaleParams(C.Structure):
                 ("nranks", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
                 ("device", C.c_int32), ("overlap", C.c_int32), ("local_slabs", C.c_int32),
-                ("nmat", C.c_int32), ("mat_gamma", C.c_double * MAX_MAT), ("hg", C.c_double)]
+                ("nmat", C.c_int32), ("mat_gamma", C.c_double * MAX_MAT), ("hg", C.c_double),
+                ("halo", C.c_int32)]
 
 
 class SaleSteinberg(C.Structure):
@@ -128,7 +130,7 @@ def nccl_unique_id() -> bytes:
 
 def make_params(cfg: dict, *, rank=0, nranks=1, device=0, local_slabs=1) -> SaleParams:
     p = SaleParams()
-    p.abi_version = 3
+    p.abi_version = 4
     for k in ("nx", "ny", "nz", "lx", "ly", "lz", "gamma", "q_lin", "q_quad", "cfl", "dt_growth",
               "t_end", "rezone", "reflect_mask", "rho0", "e_background", "e_deposit"):
         setattr(p, k, cfg[k])
@@ -136,6 +138,7 @@ def make_params(cfg: dict, *, rank=0, nranks=1, device=0, local_slabs=1) -> Sale
     p.local_slabs = local_slabs
     p.hg = float(cfg.get("hg", 0.0))
     p.overlap = int(cfg.get("overlap", 0))
+    p.halo = int(cfg.get("halo", HALO_COPY))
     gam = list(cfg.get("mat_gamma", ()))[:MAX_MAT]  # nmat > MAX_MAT is rejected by libsale
     p.nmat = int(cfg.get("nmat", 0))
     p.mat_gamma = (C.c_double * MAX_MAT)(*(gam + [0.0] * (MAX_MAT - len(gam))))
@@ -177,7 +180,9 @@ class Sale:
     cfg: the sale_params values (configs.config / configs.sedov ...); optional
     cfg["nmat"] (1..4) and cfg["mat_gamma"] add the material axis (fields MAT_F<k>,
     MAT_M<k>, MAT_E<k>; include/sale.h); cfg["hg"] the hourglass coefficient (0 if
-    absent); cfg["overlap"] the boundary-first mode (0 automatic, 1 on, -1 off).  local_slabs > 1 splits the mesh into emulated ranks on one GPU."""
+    absent); cfg["overlap"] the boundary-first mode (0 automatic, 1 on, -1 off); cfg["halo"]
+    HALO_COPY (0, default) or HALO_PEER (1: the producing kernels store the ghost planes
+    straight into the neighbours').  local_slabs > 1 splits the mesh into emulated ranks on one GPU."""
 
     def __init__(self, cfg: dict, *, device: int = 0, stream=None, rank: int = 0, nranks: int = 1,
                  nccl_id: bytes | None = None, local_slabs: int = 1):

@@ -98,6 +98,9 @@ def main():
     # small meshes against the CPU oracle (rank 0 computes it)
     small = [("C0", *config("C0")), ("E24", sedov((24, 20, 4 * world + 9), EULER), 40),
              ("L-warm", sedov((17, 13, 3 * world + 11), LAGRANGE, e_background=0.3), 25)]
+    # and the same with the peer-store halo (kernels storing straight into the
+    # neighbours' ghost planes over NVLink; sale_params.halo = SALE_HALO_PEER)
+    small += [(name + "-peer", dict(cfg, halo=S.HALO_PEER), cycles) for name, cfg, cycles in small]
     for name, cfg, cycles in small:
         rc, done, clk, glob = run_case(name, cfg, cycles, world, rank, local)
         if rank == 0:

@@ -1,0 +1,85 @@
+"""GPU parity of the peer-store halo (sale_params.halo = SALE_HALO_PEER; SURVEY §8(f)
+NEXT-1, the paper's per-cycle exchange P:372-375 fused into the kernels that produce
+the planes): on emulated slabs the producer kernels (Lagrange kc_force / kc_energy,
+Euler kr_tail, materials k_mat_flux / kn_update) store the ghost planes straight into
+the neighbouring slab, no copy exchange runs -- bitwise against the copy exchange and
+the oracle, both modes, 0 / 2 mixed materials, thin slabs, CUDA-graph replay on and
+off, several sale_step calls.  The rank path (CUDA IPC mappings + the system-scope
+arrival counters) needs two GPUs: tests/test_multigpu.py runs it with halo = PEER."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+import oracle as O
+from paper_2209_01983_b200.configs import EULER, LAGRANGE, sedov
+from tests.helpers import ALL_FIELDS, apply_perturbation, compare
+from tests.test_gpu_materials import GAMMAS, apply_perturbation_mm, mat_fields
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _sale(cfg, **kw):
+    from paper_2209_01983_b200.sale import Sale
+    return Sale(cfg, **kw)
+
+
+@pytest.mark.parametrize("rezone", [LAGRANGE, EULER])
+@pytest.mark.parametrize("slabs,shape", [(2, (12, 10, 17)), (3, (9, 7, 26)), (4, (7, 6, 13))])
+@pytest.mark.parametrize("nmat", [0, 2])
+def test_peer_halo_bitwise(rezone, slabs, shape, nmat):
+    from paper_2209_01983_b200.sale import HALO_COPY, HALO_PEER
+    kw = dict(nmat=nmat, mat_gamma=GAMMAS[:nmat]) if nmat else {}
+    cfg = sedov(shape, rezone, e_background=0.3, **kw)
+    a = _sale(dict(cfg, halo=HALO_PEER), local_slabs=slabs)
+    b = _sale(dict(cfg, halo=HALO_COPY), local_slabs=slabs)
+    o = O.Oracle(cfg)
+    fields = ALL_FIELDS + (mat_fields(nmat) if nmat else ())
+    if nmat:
+        apply_perturbation_mm((a, o, b), cfg, 11)  # (the oracle, second, supplies the base state)
+    else:
+        apply_perturbation([o, a, b], cfg, 5, lagrange=(rezone == LAGRANGE))
+    for n in (1, 6, 11):
+        ra, rb, ro = a.step(n), b.step(n), o.step(n)
+        assert ra == rb == ro, (ra, rb, ro)
+    compare(a, b, fields)
+    compare(a, o, fields)
+    assert a.clock() == o.clock()
+
+
+@pytest.mark.parametrize("rezone", [LAGRANGE, EULER])
+def test_peer_halo_without_graphs(rezone):
+    """The same on the plain launch path (SALE_GRAPHS=0: every cycle enqueued
+    individually), in a child process (the switch is read once per process)."""
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import oracle as O\n"
+        "from paper_2209_01983_b200.configs import sedov\n"
+        "from paper_2209_01983_b200.sale import Sale, HALO_PEER\n"
+        "from tests.helpers import apply_perturbation, compare\n"
+        "cfg = sedov((11, 9, 20), %d, e_background=0.3)\n"
+        "g, o = Sale(dict(cfg, halo=HALO_PEER), local_slabs=3), O.Oracle(cfg)\n"
+        "apply_perturbation([o, g], cfg, 3, lagrange=(%d == 0))\n"
+        "for n in (2, 5, 7):\n"
+        "    assert g.step(n) == o.step(n) == (0, n)\n"
+        "compare(g, o)\n"
+        "print('ok')\n" % (ROOT, rezone, rezone))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, SALE_GRAPHS="0"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_peer_halo_single_slab_and_args():
+    """One slab: PEER has no neighbour (the copy path's results); an unknown mode is
+    rejected by sale_workspace_bytes / sale_create."""
+    from paper_2209_01983_b200 import sale
+    cfg = sedov((8, 8, 8), EULER)
+    a, b = _sale(dict(cfg, halo=sale.HALO_PEER)), _sale(cfg)
+    assert a.step(5) == b.step(5) == (0, 5)
+    compare(a, b)
+    assert sale.workspace_bytes(dict(cfg, halo=2)) == 0
+    assert sale.workspace_bytes(dict(cfg, halo=sale.HALO_PEER)) > sale.workspace_bytes(cfg) - 1
