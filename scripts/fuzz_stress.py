@@ -1,8 +1,8 @@
 """A longer randomised parity sweep than tests/test_gpu_fuzz.py (the race detector while
 compute-sanitizer is closed on the pool): N seeded random cases -- mesh shape 1..41 per
 axis, rezone mode, 1-3 emulated slabs, 0 or 1-4 materials, a perturbed / mixed state,
-hourglass coefficient 0 / 0.5 / 3, boundary-first cycles on or off, random sale_step
-chunkings -- each compared bit for bit with the oracle.
+hourglass coefficient 0 / 0.5 / 3, boundary-first cycles on or off, the copy or the
+peer-store halo, random sale_step chunkings -- each compared bit for bit with the oracle.
 python scripts/fuzz_stress.py N [first_seed] [out.json]"""
 import json
 import sys
@@ -32,7 +32,8 @@ for case in range(first, first + n):
     hg = (0.0, 0.5, 3.0)[int(rng.integers(0, 3))]
     ov = (-1, 1)[int(rng.integers(0, 2))]
     cfg = sedov(shape, rezone, hg=hg, **extra)
-    g, o = Sale(dict(cfg, overlap=ov), local_slabs=slabs), O.Oracle(cfg)
+    halo = int(np.random.Generator(np.random.PCG64(case + 7919)).integers(0, 2))  # copy / peer-store halo
+    g, o = Sale(dict(cfg, overlap=ov, halo=halo), local_slabs=slabs), O.Oracle(cfg)
     seed = int(rng.integers(0, 1000))
     if nmat:
         apply_perturbation_mm((g, o), cfg, seed)
@@ -50,7 +51,7 @@ for case in range(first, first + n):
     ok = ok and g.clock() == o.clock()
     if not ok:
         bad.append({"case": case, "shape": shape, "rezone": rezone, "slabs": slabs, "nmat": nmat, "hg": hg,
-                    "overlap": ov})
+                    "overlap": ov, "halo": halo})
     g.close()
 res = {"cases": n, "first_seed": first, "mismatches": bad, "final_status_counts": statuses,
        "seconds": time.time() - t0}

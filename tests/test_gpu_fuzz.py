@@ -24,7 +24,7 @@ def test_random_shapes_bitwise(case):
     g_depth = 1 if rezone == LAGRANGE else 3  # every slab must own >= g planes
     slabs = max(1, min(int(rng.integers(1, 4)), shape[2] // g_depth))
     cfg = sedov(shape, rezone)
-    g = Sale(cfg, local_slabs=slabs)
+    g = Sale(dict(cfg, halo=(case // 2) % 2), local_slabs=slabs)  # copy / peer-store halo
     o = O.Oracle(cfg)
     apply_perturbation([g, o], cfg, int(rng.integers(0, 1000)), lagrange=(rezone == LAGRANGE))
     for n in rng.integers(1, 9, size=3):
@@ -48,7 +48,7 @@ def test_random_shapes_materials_bitwise(case):
     slabs = max(1, min(int(rng.integers(1, 4)), shape[2] // g_depth))
     nmat = int(rng.integers(1, 5))
     cfg = sedov(shape, rezone, nmat=nmat, mat_gamma=[float(x) for x in rng.uniform(1.1, 3.0, size=nmat)])
-    g = Sale(cfg, local_slabs=slabs)
+    g = Sale(dict(cfg, halo=(case // 2) % 2), local_slabs=slabs)  # copy / peer-store halo
     o = O.Oracle(cfg)
     apply_perturbation_mm((g, o), cfg, int(rng.integers(0, 1000)))
     for n in rng.integers(1, 9, size=3):
