@@ -48,9 +48,6 @@
 #ifndef SALE_MB_ENERGY_E
 #define SALE_MB_ENERGY_E 2
 #endif
-#ifndef SALE_MB_ESWEEP
-#define SALE_MB_ESWEEP 2
-#endif
 
 namespace sale {
 
@@ -795,12 +792,8 @@ __global__ void __launch_bounds__(FW * NW, EULER ? SALE_MB_FORCE_E : SALE_MB_FOR
 //   Euler: stages x' (formed from u'), u^n and ubar; areas from the tables; also
 //   writes V' and the moved-face s' the sweep reads.
 // ============================================================================
-// SW (Euler, single material): the remap's R1 swept volumes and R2 donor data of
-// kernels_remap.cu's kr_sweep in the same z-march (kc_energy_sweep): the moved faces'
-// s' and V' never leave the SM, x' and u' are staged once.
-template <bool EULER, int NW, int NM, bool SW = false>
+template <bool EULER, int NW, int NM>
 struct EnergyCTA {
-    static_assert(!SW || (EULER && NM == 0), "the fused sweep is the single-material Euler path");
     static constexpr int PL = NW * FW, TX = FW - 1, TY = NW - 1;
     // node words: Lagrange x^n(3) x'(3) u^n(3) u'(3) (u' replaced by ubar once landed);
     // Euler x'(3) u^n(3) ubar(3)
@@ -812,12 +805,7 @@ struct EnergyCTA {
     __host__ __device__ static constexpr int oN(int par, int c) { return (par * NNW + c) * PL; }
     static constexpr int OS = NSL * NNW * PL;  // s' of the x-face, y-face
     static constexpr int OAN = OS + 2 * PL;   // Lagrange: A^n of the x-face (3), y-face (3)
-    // SW: u' of the two node-plane slots (donor velocity), the four vertical ribbons
-    static constexpr int OUP = OAN + (EULER ? 0 : 6) * PL;
-    __host__ __device__ static constexpr int oUP(int par, int c) { return OUP + (par * 3 + c) * PL; }
-    static constexpr int ORB = OUP + (SW ? 6 : 0) * PL;
-    __host__ __device__ static constexpr int oR(int c) { return ORB + c * PL; }  // Rxz Ryz Rzy Rzx
-    static constexpr int WORDS = ORB + (SW ? 4 : 0) * PL + 2 * PAD;
+    static constexpr int WORDS = OAN + (EULER ? 0 : 6) * PL + 2 * PAD;
 
     const Slab& s;
     const Phys& p;
@@ -835,11 +823,6 @@ struct EnergyCTA {
     // carried z-face of node plane kz: t^n area (Lagrange), s' of the moved face
     D3 zA;
     double zs;
-    // SW: target coordinates of the column, the carried ribbons Rxy, Ryx and Z of node
-    // plane kz, the prefetched target s of the cell's -x/-y/-z faces, the planes whose
-    // swept volumes are formed [kr0, kr1]
-    double tx0, tx1, ty0, ty1, rxy_t, ryx_t, zcur, fsT[3];
-    int kr0, kr1;
 
     __device__ __forceinline__ EnergyCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int kc0, int kc1,
                                          int zchunk)
@@ -866,12 +849,6 @@ struct EnergyCTA {
             xcol = s.Xt[in];
             ycol = s.Yt[jn];
             az = s.TAz[2][(long long)jc * p.nx + ic];
-        }
-        if constexpr (SW) {  // kr_sweep's column constants
-            tx0 = col_in ? s.Xt[i] : 0.0;
-            tx1 = (col_in && i + 1 <= p.nx) ? s.Xt[i + 1] : 0.0;
-            ty0 = col_in ? s.Yt[j] : 0.0;
-            ty1 = (col_in && j + 1 <= p.ny) ? s.Yt[j + 1] : 0.0;
         }
     }
 
@@ -916,11 +893,6 @@ struct EnergyCTA {
             fax = s.TAx[0][(long long)kl * p.ny + jc];
             fay = s.TAy[1][(long long)kl * p.nx + ic];
         }
-        if constexpr (SW) {
-            fsT[0] = s.sT[0][c];
-            fsT[1] = s.sT[1][c];
-            fsT[2] = s.sT[2][c];
-        }
     }
     template <int PAR>
     __device__ __forceinline__ void put()
@@ -930,7 +902,6 @@ struct EnergyCTA {
             st3s(me, oN(PAR, 0), PL, D3{xcol + (fu1.x * dt), ycol + (fu1.y * dt), fz + (fu1.z * dt)});
             st3s(me, oN(PAR, 3), PL, fu);
             st3s(me, oN(PAR, 6), PL, scl(0.5, add(fu, fu1)));
-            if constexpr (SW) st3s(me, oUP(PAR, 0), PL, fu1);
         } else {
             st3s(me, oN(PAR, 0), PL, fx);
             st3s(me, oN(PAR, 3), PL, fx1);
@@ -958,26 +929,6 @@ struct EnergyCTA {
         st3s(me, oN(PAR, 9), PL, scl(0.5, add(Un<PAR>(0), ld3s(me, oN(PAR, 9), PL))));
     }
 
-    template <int PAR>
-    __device__ __forceinline__ D3 U1(int off) const { return ld3s(me + off, oUP(PAR, 0), PL); }  // SW: u'
-    __device__ __forceinline__ static double fs(D3 Q0, D3 Q1, D3 Q2, D3 Q3)
-    {
-        return face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
-    }
-    // SW: the ribbons Rxy / Ryx of node plane k (slot PAR, Z = z) at this column, between
-    // the target and the moved x' (c.4 step 1; kr_sweep's rib_xy)
-    template <int PAR>
-    __device__ __forceinline__ void rib_xy(int k, double z, double& rxy, double& ryx) const
-    {
-        rxy = 0.0;
-        ryx = 0.0;
-        if (col_in && k >= 0 && k <= p.nz) {
-            const D3 T = D3{tx0, ty0, z}, L = X1<PAR>(0);
-            if (j + 1 <= p.ny) rxy = fs(T, L, X1<PAR>(FW), D3{tx0, ty1, z});
-            if (i + 1 <= p.nx) ryx = fs(T, D3{tx1, ty0, z}, X1<PAR>(1), L);
-        }
-    }
-
     // the z-face at this column of node plane B: s' of the moved face, t^n area (Lagrange)
     template <int B>
     __device__ __forceinline__ void zstate(D3& A, double& sz) const
@@ -993,13 +944,6 @@ struct EnergyCTA {
     {
         // ---- P1: stage node plane kz+1 (Lagrange: wait for its copies); this cell's
         // operands; prefetch
-        const double z1 = SW ? fz : 0.0;  // SW: Z of node plane kz+1
-        double cT[3] = {0.0, 0.0, 0.0};
-        if constexpr (SW) {
-            cT[0] = fsT[0];
-            cT[1] = fsT[1];
-            cT[2] = fsT[2];
-        }
         if constexpr (EULER) {
             put<B1>();
         } else {
@@ -1035,31 +979,13 @@ struct EnergyCTA {
             if constexpr (!EULER) {
                 st3s(me, OAN, PL, face_area(Xn<B0>(0), Xn<B0>(FW), Xn<B1>(FW), Xn<B1>(0)));
                 st3s(me, OAN + 3 * PL, PL, face_area(Xn<B0>(0), Xn<B1>(0), Xn<B1>(1), Xn<B0>(1)));
-            } else if (!SW && own_col) {
+            } else if (own_col) {
                 // s' of the faces anchored at node (i,j,kz), for the sweep's swept volumes
                 const long long n = nb + (long long)kz * s.pn;
                 s.sF[0][n] = me[OS];
                 s.sF[1][n] = me[OS + PL];
                 s.sF[2][n] = zs;
             }
-        }
-        // SW: kr_sweep's ribbons -- Rxy / Ryx of node plane kz+1 (this column, carried) and
-        // the vertical ribbons between node planes kz and kz+1 (shared with the neighbours)
-        double rxy_n = 0.0, ryx_n = 0.0;
-        if constexpr (SW) {
-            rib_xy<B1>(kz + 1, z1, rxy_n, ryx_n);
-            double rxz = 0.0, ryz = 0.0, rzy = 0.0, rzx = 0.0;
-            if (col_in) {
-                const D3 T0 = D3{tx0, ty0, zcur}, T1 = D3{tx0, ty0, z1}, L0 = X1<B0>(0), L1 = X1<B1>(0);
-                rxz = fs(T0, T1, L1, L0);
-                ryz = fs(T0, L0, L1, T1);
-                if (j + 1 <= p.ny) rzy = fs(T0, D3{tx0, ty1, zcur}, X1<B0>(FW), L0);
-                if (i + 1 <= p.nx) rzx = fs(T0, L0, X1<B0>(1), D3{tx1, ty0, zcur});
-            }
-            me[oR(0)] = rxz;
-            me[oR(1)] = ryz;
-            me[oR(2)] = rzy;
-            me[oR(3)] = rzx;
         }
         __syncthreads();
         // ---- P3: cell (i,j,kz)
@@ -1165,35 +1091,7 @@ struct EnergyCTA {
                     if (s.hp) halo_cell(s, s.hp->e, cur ^ 1, 0, kz, (long long)i + (long long)p.nx * j, e1);
                 }
             }
-            if constexpr (SW) {
-                // c.4 step 2 donor data: r = m / V', Ubar = 0.125 * (sum of u' in corner order)
-                D3 sum = U1<B0>(0);
-                sum = add(sum, U1<B0>(1));
-                sum = add(sum, U1<B0>(FW));
-                sum = add(sum, U1<B0>(FW + 1));
-                sum = add(sum, U1<B1>(0));
-                sum = add(sum, U1<B1>(1));
-                sum = add(sum, U1<B1>(FW));
-                sum = add(sum, U1<B1>(FW + 1));
-                st3(s.UD, cc, scl(0.125, sum));
-                s.rD[cc] = ddiv(m, V1);
-                // c.4 step 1: swept volumes of the cell's -x, -y, -z faces (interior faces)
-                if (kz >= kr0 && kz <= kr1) {
-                    if (kz < kr1 && i >= 1)
-                        s.dV[0][cc] = ddiv(((((me[FW + oR(0)] - me[oR(0)]) + rxy_n) - rxy_t) + me[OS]) - cT[0], 3.0);
-                    if (kz < kr1 && j >= 1)
-                        s.dV[1][cc] = ddiv(((((ryx_n - ryx_t) + me[1 + oR(1)]) - me[oR(1)]) + me[OS + PL]) - cT[1], 3.0);
-                    if (kz >= 1)
-                        s.dV[2][cc] = ddiv(((((me[1 + oR(2)] - me[oR(2)]) + me[FW + oR(3)]) - me[oR(3)]) + zs) - cT[2], 3.0);
-                }
-            } else if (EULER) {
-                s.V1[cc] = V1;
-            }
-        }
-        if constexpr (SW) {
-            rxy_t = rxy_n;
-            ryx_t = ryx_n;
-            zcur = z1;
+            if (EULER) s.V1[cc] = V1;
         }
         zA = zAn;
         zs = zsn;
@@ -1206,15 +1104,10 @@ struct EnergyCTA {
             fetch(za);
             if (za & 1) put<1>();
             else put<0>();
-            if constexpr (SW) zcur = fz;  // Z of node plane za
             fetch(za + 1);
             __syncthreads();
             if (za & 1) zstate<1>(zA, zs);
             else zstate<0>(zA, zs);
-            if constexpr (SW) {
-                if (za & 1) rib_xy<1>(za, zcur, rxy_t, ryx_t);
-                else rib_xy<0>(za, zcur, rxy_t, ryx_t);
-            }
             for (int kz = za; kz <= zb; ++kz) {
                 if (kz & 1) step<1, 0, 0>(kz);
                 else step<0, 1, 0>(kz);
@@ -1254,20 +1147,6 @@ __global__ void __launch_bounds__(FW * NW, EULER ? SALE_MB_ENERGY_E : (NM >= SAL
     c.run();
 }
 
-// Euler, single material: kc_energy and kr_sweep in one z-march (swept volumes of the
-// cell planes [kr0, kr1], donor data of every cell of the range)
-template <int NW>
-__global__ void __launch_bounds__(FW * NW, SALE_MB_ESWEEP) kc_energy_sweep(Slab s, Phys p, int cur, int kc0, int kc1,
-                                                                            int zchunk, int kr0, int kr1)
-{
-    if (!s.st->active) return;
-    extern __shared__ double smem[];
-    EnergyCTA<true, NW, 0, true> c(s, p, cur, smem, kc0, kc1, zchunk);
-    c.kr0 = kr0;
-    c.kr1 = kr1;
-    c.run();
-}
-
 // ============================================================================
 // launchers
 // ============================================================================
@@ -1282,11 +1161,7 @@ namespace {
 #ifndef SALE_NW_ENERGY
 #define SALE_NW_ENERGY 8
 #endif
-#ifndef SALE_NW_ESWEEP
-#define SALE_NW_ESWEEP 8
-#endif
 constexpr int NW_STATE = SALE_NW_STATE, NW_FORCE = SALE_NW_FORCE, NW_ENERGY = SALE_NW_ENERGY;
-constexpr int NW_ESWEEP = SALE_NW_ESWEEP;
 
 // Euler: node planes the Lagrangian phase updates (owned + the ghost region the remap
 // reads), and the cell planes whose state the force gather needs
@@ -1368,25 +1243,6 @@ int launch_energy(const Slab& s, const Phys& p, int cur, Stream st, int ka, int 
         if (p.rezone) go(kc_energy<true, NW_ENERGY, NM>, EnergyCTA<true, NW_ENERGY, NM>::WORDS);
         else go(kc_energy<false, NW_ENERGY, NM>, EnergyCTA<false, NW_ENERGY, NM>::WORDS);
     });
-    return 1;
-}
-
-// Euler, single material: the Lagrangian energy update fused with the remap's swept
-// volumes and donor data (kc_energy_sweep); the remap then runs kr_tail only
-int launch_energy_sweep(const Slab& s, const Phys& p, int cur, Stream st)
-{
-    int kc0, kc1;
-    euler_ranges(s, p, kc0, kc1);
-    if (kc1 <= kc0) return 0;
-    const int kr0 = imax_h(s.k0 - 1, 0), kr1 = imin_h(s.k1 + 1, p.nz);
-    auto kern = kc_energy_sweep<NW_ESWEEP>;
-    const size_t sm = sizeof(double) * EnergyCTA<true, NW_ESWEEP, 0, true>::WORDS;
-    set_smem(kern, sm);
-    const long long xy = (long long)cdiv(p.nx, FW - 1) * cdiv(p.ny, NW_ESWEEP - 1);
-    const int zc = zchunk_for(xy, kc1 - kc0, ZCHUNK);
-    dim3 grid(cdiv(p.nx, FW - 1), cdiv(p.ny, NW_ESWEEP - 1), cdiv(kc1 - kc0, zc));
-    kern<<<grid, dim3(FW, NW_ESWEEP), sm, (cudaStream_t)st>>>(s, p, cur, kc0, kc1, zorder(zc), kr0, kr1);
-    note_launch();
     return 1;
 }
 

@@ -625,11 +625,11 @@ int launch_rtail(const Slab& s, const Phys& p, int cur, Stream st, int ka, int k
 // owned node plane (the next cycle's ke_state forms the dt candidate of the remapped
 // state); nodes = 0 leaves R2-R4 to the caller (boundary-first cycles: launch_rtail by
 // node-plane ranges)
-int launch_remap(const Slab& s, const Phys& p, int cur, Stream st, int nodes, int sweep)
+int launch_remap(const Slab& s, const Phys& p, int cur, Stream st, int nodes)
 {
-    const int n = sweep ? launch_sweep(s, p, cur, st) : 0;  // sweep = 0: kc_energy_sweep formed R1-R2
-    if (!nodes) return n;
-    return n + launch_rtail(s, p, cur, st);
+    launch_sweep(s, p, cur, st);
+    if (!nodes) return 1;
+    return 1 + launch_rtail(s, p, cur, st);
 }
 
 }  // namespace sale

@@ -21,10 +21,6 @@
 #include "sale.h"
 #include "sale_internal.h"
 
-#ifndef SALE_FUSE_ES  // Euler: kc_energy + kr_sweep as one z-march (kc_energy_sweep)
-#define SALE_FUSE_ES 0
-#endif
-
 static_assert(SALE_OK == sale::S_OK && SALE_ETANGLED == sale::S_ETANGLED &&
                   SALE_EDTCOLLAPSE == sale::S_EDTCOLLAPSE && SALE_ENEGMASS == sale::S_ENEGMASS &&
                   SALE_EREPLICA == sale::S_EREPLICA,
@@ -685,8 +681,6 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first)
     const bool ov = overlap_on(c);
     if (ov && (rc = overlap_resources(c))) return rc;
     const bool peer = c->prm.halo == SALE_HALO_PEER;
-    // Euler, single material: the energy update and the remap's sweep in one kernel
-    const bool fused_es = SALE_FUSE_ES && euler && c->prm.nmat == 0;
     int pr;
     if (peer && c->peer_sides) {  // ranks: the neighbours' planes of the previous cycle landed
         pr = prof_open(c, SALE_K_HALO);
@@ -705,15 +699,14 @@ int enqueue_one_cycle(sale_ctx* c, int b, bool first)
     for (auto& s : c->slabs) {
         pr = prof_open(c, SALE_K_LAGRANGE);
         c->launches += sale::launch_force(s, c->phys, b, st);
-        if (fused_es) c->launches += sale::launch_energy_sweep(s, c->phys, b, st);
-        else if (euler || !ov) c->launches += sale::launch_energy(s, c->phys, b, st);
+        if (euler || !ov) c->launches += sale::launch_energy(s, c->phys, b, st);
         else c->launches += launch_tail(c, s, b, 0, st);
         prof_close(c, pr);
         if (euler) {
             pr = prof_open(c, SALE_K_REMAP);
             const int nodes = ov ? 0 : 1;
             c->launches += c->prm.nmat ? sale::launch_remap_mat(s, c->phys, b, st, nodes)
-                                       : sale::launch_remap(s, c->phys, b, st, nodes, fused_es ? 0 : 1);
+                                       : sale::launch_remap(s, c->phys, b, st, nodes);
             if (ov) c->launches += launch_tail(c, s, b, 0, st);
             prof_close(c, pr);
         }

@@ -183,13 +183,10 @@ int launch_force(const Slab& s, const Phys& p, int cur, Stream st);
 // buffer cur^1; Euler: e' (e'_k), V', and the moved-face s' the sweep reads.
 // [ka, kb): a sub-range of the cell planes (boundary-first cycles); -1: all of them
 int launch_energy(const Slab& s, const Phys& p, int cur, Stream st, int ka = -1, int kb = -1);
-// Euler, single material: S7 + the remap's R1 swept volumes and R2 donor data in one
-// z-march (then launch_remap with sweep = 0)
-int launch_energy_sweep(const Slab& s, const Phys& p, int cur, Stream st);
 // R1-R4 (kernels_remap.cu; materials: kernels_mat.cu); nodes = 0: the caller launches
 // the node part by node-plane ranges, boundary first (single material: R1 only, then
 // launch_rtail = R2-R4; materials: R1-R3, then launch_kn_update = R4)
-int launch_remap(const Slab& s, const Phys& p, int cur, Stream st, int nodes = 1, int sweep = 1);
+int launch_remap(const Slab& s, const Phys& p, int cur, Stream st, int nodes = 1);
 int launch_remap_mat(const Slab& s, const Phys& p, int cur, Stream st, int nodes = 1);
 int launch_sweep(const Slab& s, const Phys& p, int cur, Stream st);
 // single material: R2-R4 (fluxes, cell update, node momentum) over the owned node
