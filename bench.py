@@ -380,7 +380,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("gloo")  # plumbing only: id broadcast, barrier, max
-    cfg, _ = configs.config(args.config, world)
+    cfg, job_cycles = configs.config(args.config, world)
     cfg["halo"] = S.HALO_PEER if args.halo == "peer" else S.HALO_COPY
     nid = None
     if world > 1:
@@ -435,6 +435,24 @@ def main():
                "d2h_bytes_per_step": nbytes, "steps": args.e2e_steps,
                "what": "per step: set_field of the full state from pinned host, sale_step(1), "
                        "get_field of the full state to pinned host"}
+        # the whole BASELINE job through the same calls: the state from pinned host once,
+        # the config's cycles in one sale_step, the final state back to pinned host
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for f in fields:
+            ctx.set(f, host[f])
+        rc, done = ctx.step(job_cycles)
+        if rc or done != job_cycles:
+            raise RuntimeError(f"e2e job rc={rc} done={done}")
+        for f in fields:
+            ctx.get(f, out=host[f])
+        torch.cuda.synchronize()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        e2e["job"] = {"value": gcells * job_cycles / wall, "unit": UNIT, "cycles": job_cycles,
+                      "h2d_bytes": nbytes, "d2h_bytes": nbytes, "seconds": wall,
+                      "what": f"the {args.config} job end to end: set_field of the full state from pinned host, "
+                              f"sale_step({job_cycles}), get_field of the full state to pinned host"}
 
     # ---- CPU oracle baseline (rank 0, N=1 only) -------------------------------
     cpu = None
