@@ -28,9 +28,6 @@
 #ifndef SALE_TAIL_PF  // kr_tail: L2 prefetch distance in planes (0: none)
 #define SALE_TAIL_PF 2
 #endif
-#ifndef SALE_TAIL_BULK  // kr_tail with its operands staged by bulk copies (even nx)
-#define SALE_TAIL_BULK 0
-#endif
 #ifndef SALE_NW_TAIL
 #define SALE_NW_TAIL 8
 #endif
@@ -544,333 +541,6 @@ __global__ void __launch_bounds__(RW * NW, SALE_MB_TAIL) kr_tail(Slab s, Phys p,
 }
 
 // ============================================================================
-// kr_tail_bulk: kr_tail with its cell operands staged by the bulk-copy engine (TMA's
-// non-tensor form, cp.async.bulk global -> shared completing on an mbarrier).  Per cell
-// plane the lanes of warp 0 issue one 16-B-aligned row copy each of the plane's donor
-// data r, e', Ubar (rows Y0 .. Y0+NW+1 around the tile) and swept volumes dV_x, dV_y,
-// dV_z (the rows the flux reads), 36 doubles from the even column X0e <= X0 (clamped
-// to the mesh), into a ring of four plane slots; lane 0 then arms the slot's mbarrier
-// with the bytes in flight (expect_tx).  The threads wait on the mbarrier phase of the
-// plane they need instead of loading 40-odd operands per cell from L2.  Planes t-1, t,
-// t+1 are resident while plane t+2 lands; plane t+3 goes into the slot of plane t-1
-// right after the step's barrier (1.5 steps of latency cover).  Rows and columns outside
-// the mesh are not copied: their stale words sit only behind the boundary-face selects
-// (as kr_tail's clamped loads did).  The arithmetic, its association and the node
-// gather are kr_tail's (bit-identical).  Needs even nx (16-B aligned rows).
-// (Tensor-map TMA, cp.async.bulk.tensor, raised "illegal instruction" on this pool's
-// B200s even through libcu++ -- tools/tma_probe*.cu -- while the non-tensor bulk copy
-// works; hence row copies.)
-// ============================================================================
-namespace {
-constexpr int BP = 36;  // row pitch (doubles) of a staged box: 34 columns + the even start
-template <int NW>
-struct BulkLayout {
-    __host__ __device__ static constexpr int oDon(int k) { return k * BP * (NW + 2); }  // r, e', Ubar x, y, z: NW+2 rows
-    static constexpr int oDV0 = 5 * BP * (NW + 2);                 // NW rows (Y0+1 ..)
-    static constexpr int oDV1 = oDV0 + BP * NW;                    // NW+1 rows
-    static constexpr int oDV2 = oDV1 + BP * (NW + 1);              // NW rows
-    static constexpr int SLOT = oDV2 + BP * NW;                    // doubles per plane slot
-    static constexpr int NROW = 5 * (NW + 2) + NW + (NW + 1) + NW; // row copies per plane
-    static constexpr int NSLOT = 4;
-    static constexpr int OC = NSLOT * SLOT;                        // the Delta m, Delta P, m'' exchange (10 PL)
-    static constexpr int WORDS = OC + 10 * RW * NW + 4 + 2;        // + mbarriers + alignment slack
-};
-
-__device__ __forceinline__ unsigned smem_u32(const void* ptr) { return (unsigned)__cvta_generic_to_shared(ptr); }
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity)
-{
-    unsigned done = 0;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(bar)
-                 : "memory");
-}
-}  // namespace
-
-template <int NW>
-struct TailBulkCTA {
-    using LY = BulkLayout<NW>;
-    static constexpr int PL = NW * RW, TX = RW - 1, TY = NW - 1;
-    const Slab& s;
-    const Phys& p;
-    const int cur;
-    double* sl;      // plane slots (16-B aligned)
-    double* me;      // this thread in the exchange buffer
-    unsigned bar0;   // mbarrier of slot 0 (slot k at bar0 + 8k)
-    int i, j, ka, kb, za, zb, X0, Y0, X0e, sx, p0;
-    long long nb;
-    bool node_thr, cell_col, own_col;
-    bool pxm, pxp, pym, pyp;
-    D3 Fp;
-    double Dp, Mp;
-    bool have;
-
-    __device__ __forceinline__ TailBulkCTA(const Slab& s_, const Phys& p_, int cur_, double* smem, int ka_, int kb_,
-                                           int zchunk)
-        : s(s_), p(p_), cur(cur_)
-    {
-        const int ix = threadIdx.x, iy = threadIdx.y;
-        sl = smem + ((16u - (smem_u32(smem) & 15u)) & 15u) / 8u;  // 16-B aligned (stays a shared pointer)
-        me = sl + LY::OC + iy * RW + ix;
-        bar0 = smem_u32(sl + LY::OC + 10 * PL);
-        i = blockIdx.x * TX + ix;
-        j = blockIdx.y * TY + iy;
-        ka = ka_;
-        kb = kb_;
-        za = ka + zchunk_base(zchunk);
-        zb = za + zchunk - 1 < kb ? za + zchunk - 1 : kb;
-        X0 = blockIdx.x * TX - 2;  // the tile's cells and their x-neighbours: [X0, X0+33]
-        Y0 = blockIdx.y * TY - 2;
-        X0e = X0 & ~1;             // even start (16-B aligned rows: nx is even)
-        sx = X0 - X0e;
-        p0 = za - 2;  // the first cell plane staged (cells of plane za-1 and their -z donors)
-        nb = (long long)i + (long long)(p.nx + 1) * (j - (long long)(p.ny + 1) * s.kb);
-        node_thr = ix < TX && iy < TY && i <= p.nx && j <= p.ny;
-        cell_col = i >= 1 && i <= p.nx && j >= 1 && j <= p.ny;
-        own_col = cell_col && ix >= 1 && iy >= 1;
-        pxm = i >= 1;
-        pxp = i < p.nx;
-        pym = j >= 1;
-        pyp = j < p.ny;
-    }
-    __device__ __forceinline__ double* slot(int plane) const { return sl + ((plane - p0) & 3) * LY::SLOT; }
-    __device__ __forceinline__ unsigned bar(int plane) const { return bar0 + 8u * ((plane - p0) & 3); }
-    __device__ __forceinline__ unsigned parity(int plane) const { return ((plane - p0) >> 2) & 1; }
-    // warp 0: cell plane `plane` into its slot, one row copy per lane and round; lane 0
-    // arms the mbarrier with the bytes of the copies the warp issued
-    __device__ __forceinline__ void issue(int plane) const
-    {
-        const int lane = threadIdx.x;
-        double* d = slot(plane);
-        const unsigned b = bar(plane);
-        const int zl = plane - s.kb;  // local plane
-        const bool zin = plane >= 0 && plane < p.nz && zl >= 0 && zl < s.nzc;
-        const int xa = X0e > 0 ? X0e : 0, xb = X0e + BP < p.nx ? X0e + BP : p.nx;  // clamped, even
-        const unsigned rowbytes = xb > xa ? 8u * (xb - xa) : 0u;
-        unsigned bytes = 0;
-        for (int r = lane; r < LY::NROW; r += 32) {
-            const double* a;
-            int off, row;
-            if (r < 5 * (NW + 2)) {
-                const int k = r / (NW + 2);
-                row = r - k * (NW + 2);
-                a = k == 0 ? s.rD : k == 1 ? s.e1 : s.UD[k - 2];
-                off = LY::oDon(k) + row * BP;
-                row += Y0;
-            } else if (r < 5 * (NW + 2) + NW) {
-                row = r - 5 * (NW + 2);
-                a = s.dV[0];
-                off = LY::oDV0 + row * BP;
-                row += Y0 + 1;
-            } else if (r < 5 * (NW + 2) + 2 * NW + 1) {
-                row = r - 5 * (NW + 2) - NW;
-                a = s.dV[1];
-                off = LY::oDV1 + row * BP;
-                row += Y0 + 1;
-            } else {
-                row = r - 5 * (NW + 2) - 2 * NW - 1;
-                a = s.dV[2];
-                off = LY::oDV2 + row * BP;
-                row += Y0 + 1;
-            }
-            if (zin && row >= 0 && row < p.ny && rowbytes) {
-                const long long g = (long long)xa + (long long)p.nx * (row + (long long)p.ny * zl);
-                bulk_g2s(smem_u32(d + off + (xa - X0e)), a + g, rowbytes, b);
-                bytes += rowbytes;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-        if (lane == 0) mbar_expect_tx(b, bytes);
-    }
-
-    // c.4 steps 2-3 for this thread's cell (i-1, j-1, t) from the staged planes (kr_tail's
-    // flux_cell with its operands from shared memory; the same expressions)
-    __device__ __forceinline__ void flux(int t, bool own, double& dm, D3& dP, double& m2) const
-    {
-        const int ix = threadIdx.x, iy = threadIdx.y;
-        const double* S0 = slot(t);
-        const double* Sm = slot(t - 1);
-        const double* Sp = slot(t + 1);
-        const int od = (iy + 1) * BP + (ix + 1 + sx);  // donor box: cell (i-1, j-1)
-        const int ov = iy * BP + (ix + 1 + sx);        // dV boxes (rows from Y0+1)
-        auto don = [&](const double* S, int o) {
-            return Donor{S[LY::oDon(0) + o], S[LY::oDon(1) + o],
-                         D3{S[LY::oDon(2) + o], S[LY::oDon(3) + o], S[LY::oDon(4) + o]}};
-        };
-        const Donor own_d = don(S0, od);
-        const int ci = i - 1, cj = j - 1;
-        const long long c = (long long)ci + (long long)p.nx * ((long long)cj + (long long)p.ny * (t - s.kb));
-        const double m = s.m[cur][c];
-        double mu[6], ep[6];
-        D3 pi[6];
-#pragma unroll
-        for (int f = 0; f < 6; ++f) {
-            const int a = f >> 1;
-            const bool plus = f & 1;
-            const int ia = a == 0 ? ci : (a == 1 ? cj : t), na = a == 0 ? p.nx : (a == 1 ? p.ny : p.nz);
-            const bool inner = plus ? ia + 1 <= na - 1 : ia >= 1;  // a cell on both sides
-            // the neighbour across face f and the face's swept volume (the -a face of the upper cell)
-            const Donor o = f == 0 ? don(S0, od - 1) : f == 1 ? don(S0, od + 1) : f == 2 ? don(S0, od - BP)
-                          : f == 3 ? don(S0, od + BP) : f == 4 ? don(Sm, od) : don(Sp, od);
-            const double dvf = f == 0 ? S0[LY::oDV0 + ov] : f == 1 ? S0[LY::oDV0 + ov + 1]
-                             : f == 2 ? S0[LY::oDV1 + ov] : f == 3 ? S0[LY::oDV1 + ov + BP]
-                             : f == 4 ? S0[LY::oDV2 + ov] : Sp[LY::oDV2 + ov];
-            const double dV = inner ? dvf : 0.0;
-            const bool mine = (dV > 0.0) == plus;  // donor: the lower cell if the face moved toward +a
-            const double Dr = mine ? own_d.r : o.r, De = mine ? own_d.e : o.e;
-            const D3 Du = mine ? own_d.u : o.u;
-            mu[f] = inner ? Dr * dV : 0.0;
-            ep[f] = inner ? mu[f] * De : 0.0;
-            pi[f] = inner ? scl(mu[f], Du) : D3{0.0, 0.0, 0.0};
-        }
-        dm = ((((mu[0] - mu[1]) + mu[2]) - mu[3]) + mu[4]) - mu[5];
-        const double dE = ((((ep[0] - ep[1]) + ep[2]) - ep[3]) + ep[4]) - ep[5];
-        dP = sub(add(sub(add(sub(pi[0], pi[1]), pi[2]), pi[3]), pi[4]), pi[5]);
-        const double e1 = own_d.e;
-        m2 = m + dm;
-        if (own) {
-            if (t >= s.k0 && t < s.k1 && !(m2 > 0.0))
-                atomicMin(&s.st->err_key, (ERR_ORDER_NEGMASS << 48) | (unsigned long long)gcell(p, ci, cj, t));
-            const double e2 = e1 + ddiv(dE - (e1 * dm), m2);
-            s.e[cur ^ 1][c] = e2;
-            s.m[cur ^ 1][c] = m2;
-            if (s.hp) {
-                const long long q = (long long)ci + (long long)p.nx * cj;
-                halo_cell(s, s.hp->e, cur ^ 1, 0, t, q, e2);
-                halo_cell(s, s.hp->m, cur ^ 1, 0, t, q, m2);
-            }
-        }
-    }
-
-    template <int PAR>
-    __device__ __forceinline__ void gather4(double& Dm, D3& DP, double& M2, bool& hv, bool pz) const
-    {
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            const int ap = g & 1, bp = g >> 1;
-            const int off = ap + bp * RW;
-            const bool pres = pz && (ap ? pxp : pxm) && (bp ? pyp : pym);
-            if (pres) {
-                const double d = me[off + (PAR * 5 + 0) * PL], mm = me[off + (PAR * 5 + 4) * PL];
-                const D3 dp = D3{me[off + (PAR * 5 + 1) * PL], me[off + (PAR * 5 + 2) * PL], me[off + (PAR * 5 + 3) * PL]};
-                Dm = hv ? Dm + d : d;
-                DP = hv ? add(DP, dp) : dp;
-                M2 = hv ? M2 + mm : mm;
-                hv = true;
-            }
-        }
-    }
-
-    template <int PAR>
-    __device__ __forceinline__ void step(int t)
-    {
-        const bool fin = node_thr && t >= za;
-        const long long n = nb + (long long)t * s.pn;
-        D3 u1 = D3{0.0, 0.0, 0.0};
-        if (fin) u1 = ld3(s.u1, n);
-        if (t + 2 <= zb) {  // the node and mass operands two planes ahead into L2
-            if (node_thr) {
-                const long long np = nb + (long long)(t + 2) * s.pn;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(s.u1[0] + np));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(s.u1[1] + np));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(s.u1[2] + np));
-            }
-            if (cell_col && t + 2 < p.nz) {
-                const long long c = (long long)(i - 1) + (long long)p.nx * ((long long)(j - 1) + (long long)p.ny * (t + 2 - s.kb));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(s.m[cur] + c));
-            }
-        }
-        const bool pz = t >= 0 && t < p.nz;
-        mbar_wait(bar(t + 1), parity(t + 1));  // planes t-1 and t were waited for before
-        if (cell_col && pz) {
-            double dm, m2;
-            D3 dP;
-            flux(t, own_col && t >= ka && t <= kb && t < s.k1, dm, dP, m2);
-            me[(PAR * 5 + 0) * PL] = dm;
-            me[(PAR * 5 + 1) * PL] = dP.x;
-            me[(PAR * 5 + 2) * PL] = dP.y;
-            me[(PAR * 5 + 3) * PL] = dP.z;
-            me[(PAR * 5 + 4) * PL] = m2;
-        }
-        __syncthreads();
-        // every thread is past its reads of plane t-1: its slot takes plane t+3
-        if (threadIdx.y == 0 && t + 3 <= zb + 1) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(t + 3);
-        }
-        if (!node_thr) return;
-        if (fin) {
-            double Dm = Dp, M2 = Mp;
-            D3 DP = Fp;
-            bool hv = have;
-            gather4<PAR>(Dm, DP, M2, hv, pz);
-            Dm = 0.125 * Dm;
-            DP = scl(0.125, DP);
-            M2 = 0.125 * M2;
-            D3 un = d3(u1.x + ddiv(DP.x - (u1.x * Dm), M2), u1.y + ddiv(DP.y - (u1.y * Dm), M2),
-                       u1.z + ddiv(DP.z - (u1.z * Dm), M2));
-            un = reflect(p, i, j, t, un);
-            st3(s.u[cur ^ 1], n, un);
-            if (s.hp) halo_node3(s, s.hp->u, cur ^ 1, t, (long long)i + (long long)(p.nx + 1) * j, un);
-        }
-        have = false;
-        Dp = 0.0;
-        Mp = 0.0;
-        Fp = D3{0.0, 0.0, 0.0};
-        if (t < zb) gather4<PAR>(Dp, Fp, Mp, have, pz);
-    }
-
-    __device__ __forceinline__ void run()
-    {
-        if (threadIdx.x == 0 && threadIdx.y == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) mbar_init(bar0 + 8u * k, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-        if (threadIdx.y == 0)
-            for (int q = p0; q <= p0 + 3 && q <= zb + 1; ++q) issue(q);
-        have = false;
-        Dp = 0.0;
-        Mp = 0.0;
-        Fp = D3{0.0, 0.0, 0.0};
-        mbar_wait(bar(p0), parity(p0));  // the first step's planes t-1, t
-        mbar_wait(bar(p0 + 1), parity(p0 + 1));
-        for (int t = za - 1; t <= zb; ++t) {
-            if (t & 1) step<1>(t);
-            else step<0>(t);
-        }
-    }
-};
-
-template <int NW>
-__global__ void __launch_bounds__(RW * NW, 2) kr_tail_bulk(Slab s, Phys p, int cur, int ka, int kb, int zchunk)
-{
-    if (!s.st->active) return;
-    extern __shared__ double smem[];
-    TailBulkCTA<NW> c(s, p, cur, smem, ka, kb, zchunk);
-    c.run();
-}
-
-// ============================================================================
 namespace {
 inline int cdivr(int a, int b) { return (a + b - 1) / b; }
 constexpr int RZ = 32;
@@ -935,22 +605,6 @@ int launch_rtail(const Slab& s, const Phys& p, int cur, Stream st, int ka, int k
         k1 = kb < k1 ? kb : k1;
     }
     if (k1 < k0) return 0;
-    if (SALE_TAIL_BULK && p.nx % 2 == 0) {  // operands staged by bulk copies (16-B aligned rows)
-        constexpr int NW = 8;
-        auto kern = kr_tail_bulk<NW>;
-        const size_t sm = sizeof(double) * BulkLayout<NW>::WORDS;
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            init = true;
-        }
-        const long long xy = (long long)cdivr(p.nx + 1, RW - 1) * cdivr(p.ny + 1, NW - 1);
-        const int zc = zchunk_for(xy, k1 - k0 + 1, RZ);
-        dim3 grid(cdivr(p.nx + 1, RW - 1), cdivr(p.ny + 1, NW - 1), cdivr(k1 - k0 + 1, zc));
-        kern<<<grid, dim3(RW, NW), sm, (cudaStream_t)st>>>(s, p, cur, k0, k1, zorder(zc));
-        note_launch();
-        return 1;
-    }
     constexpr int NW = SALE_NW_TAIL;
     auto kern = kr_tail<NW>;
     const size_t sm = sizeof(double) * TailCTA<NW>::WORDS;
@@ -977,7 +631,5 @@ int launch_remap(const Slab& s, const Phys& p, int cur, Stream st, int nodes)
     if (!nodes) return 1;
     return 1 + launch_rtail(s, p, cur, st);
 }
-
-
 
 }  // namespace sale
