@@ -83,3 +83,36 @@ def test_peer_halo_single_slab_and_args():
     compare(a, b)
     assert sale.workspace_bytes(dict(cfg, halo=2)) == 0
     assert sale.workspace_bytes(dict(cfg, halo=sale.HALO_PEER)) > sale.workspace_bytes(cfg) - 1
+
+
+@pytest.mark.parametrize("name,slabs", [("C3", 4), ("C4n2", 2), ("C2M2", 3)])
+def test_peer_halo_full_length_digest(name, slabs):
+    """The BASELINE runs on emulated slabs with the peer-store halo reproduce the oracle's
+    golden digests (tests/golden/, written by scripts/oracle_digests.py from the oracle
+    only): C3 on 4 slabs (200 Lagrangian cycles), the 2-GPU weak-scaling problem C4n2 on
+    2 slabs (100 Eulerian cycles), and the two-material C2M2 on 3 slabs (300 cycles)."""
+    import hashlib
+    import json
+    from paper_2209_01983_b200 import inputs
+    from paper_2209_01983_b200.configs import config
+    from paper_2209_01983_b200.sale import HALO_PEER
+    path = os.path.join(ROOT, "tests", "golden", f"{name}.json")
+    if not os.path.exists(path):
+        pytest.skip("no golden")
+    g = json.load(open(path))
+    cfg, _ = config(name.split("n")[0], int(name.split("n")[1]) if "n" in name else 1)
+    ctx = _sale(dict(cfg, halo=HALO_PEER), local_slabs=slabs)
+    if cfg.get("nmat"):
+        for f, v in inputs.material_halves(cfg, ctx.get("MASS"), ctx.get("MAT_E0")).items():
+            ctx.set(f, v)
+    done, rc = 0, 0
+    while done < g["requested_cycles"]:
+        rc, d = ctx.step(min(1000, g["requested_cycles"] - done))
+        done += d
+        if rc or d == 0:
+            break
+    assert (rc, done) == (g["status"], g["cycles_done"])
+    assert ctx.clock() == g["clock"]
+    bad = [f for f, ref in g["fields"].items()
+           if hashlib.sha256(ctx.get(f).ravel().tobytes()).hexdigest() != ref["sha256"]]
+    assert not bad, bad
