@@ -2,7 +2,7 @@
 # per-kernel time / FP64 / issue / DRAM snapshot of a config (ncu, a few launches of each)
 CFG=${CFG:-C4}
 python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,dram__throughput.avg.pct_of_peak_sustained_elapsed,launch__registers_per_thread --clock-control none -k regex:"kf_|kr_|kn_" -s ${SKIP:-14} -c ${COUNT:-7} --csv python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ll_$CFG.csv 2>&1
+ncu --metrics gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pct_of_peak_sustained_active,dram__throughput.avg.pct_of_peak_sustained_elapsed,launch__registers_per_thread --clock-control none -k regex:"kc_|ke_|kl_|kr_|kn_" -s ${SKIP:-14} -c ${COUNT:-7} --csv python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ll_$CFG.csv 2>&1
 python - <<'PY'
 import csv, collections, os
 cfg = os.environ.get("CFG", "C4")
