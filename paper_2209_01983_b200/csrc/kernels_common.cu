@@ -442,6 +442,17 @@ __global__ void __launch_bounds__(256) k_steinberg(Slab s, Phys p, int cur, Stei
 {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long total = s.pc * (s.k1 - s.k0);
+    // without a plastic strain field the hardening factor Y0 (1 + beta 0)^n is the same for
+    // every cell: formed once per block (the same expression, the same bits) instead of one
+    // pow per cell
+    __shared__ double hconst[MAX_MAT];
+    if (!eps) {
+        if (threadIdx.x < (NM > 0 ? NM : 1)) {
+            const SteinbergP& sp = set.m[threadIdx.x];
+            hconst[threadIdx.x] = sp.Y0 * pow(1.0 + sp.beta * 0.0, sp.n);
+        }
+        __syncthreads();
+    }
     if (t >= total) return;
     const int k = s.k0 + (int)(t / s.pc);
     const long long r = t % s.pc;
@@ -482,7 +493,7 @@ __global__ void __launch_bounds__(256) k_steinberg(Slab s, Phys p, int cur, Stei
         const double T = e / sp.cv;
         // eta^(1/3): cbrt (within an ulp of the paper's pow(eta, 1/3), at a fraction of its cost)
         const double G = (sp.G0 + (sp.GP * pr) * cbrt(eta)) + sp.GT * (T - sp.T0);
-        const double h = sp.Y0 * pow(1.0 + sp.beta * ep, sp.n);
+        const double h = eps ? sp.Y0 * pow(1.0 + sp.beta * ep, sp.n) : hconst[a];
         sh[t + a * mstride] = G;
         y[t + a * mstride] = ((h < sp.Ymax) ? h : sp.Ymax) * (G / sp.G0);
     }

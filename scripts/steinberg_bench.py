@@ -16,26 +16,28 @@ for name, algo in (("C4", 48.0), ("C3", 64.0)):
     g = Sale(cfg)
     g.step(3)
     cells = cfg["nx"] * cfg["ny"] * cfg["nz"]
-    eps = torch.rand(g.cell_shape, dtype=torch.float64, device=g.torch_device)
-    out = g.steinberg(prm, eps)
-    for _ in range(3):
-        g.steinberg(prm, eps, out=out)
-    torch.cuda.synchronize()
-    n = 50
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(g.stream)
-    for _ in range(n):
-        g.steinberg(prm, eps, out=out)
-    b.record(g.stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / n
-    gbs = algo * cells / (ms * 1e-3) / 1e9
-    line = {"workload": name, "cells": cells, "ms_per_call": ms, "cells_per_s": cells / (ms * 1e-3),
-            "algo_bytes_per_cell": algo, "achieved_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
-            "bound": "hbm"}
-    print(json.dumps(line), flush=True)
-    lines.append(line)
-    del g, eps, out
+    eps_field = torch.rand(g.cell_shape, dtype=torch.float64, device=g.torch_device)
+    for eps, nbytes in ((eps_field, algo), (None, algo - 8.0)):  # with / without a plastic strain field
+        out = g.steinberg(prm, eps)
+        for _ in range(3):
+            g.steinberg(prm, eps, out=out)
+        torch.cuda.synchronize()
+        n = 50
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(g.stream)
+        for _ in range(n):
+            g.steinberg(prm, eps, out=out)
+        b.record(g.stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / n
+        gbs = nbytes * cells / (ms * 1e-3) / 1e9
+        line = {"workload": name, "eps": "field" if eps is not None else "none", "cells": cells, "ms_per_call": ms,
+                "cells_per_s": cells / (ms * 1e-3), "algo_bytes_per_cell": nbytes, "achieved_gbs": gbs,
+                "peak_gbs": peak, "frac": gbs / peak, "bound": "hbm"}
+        print(json.dumps(line), flush=True)
+        lines.append(line)
+        del out
+    del g, eps_field
     torch.cuda.empty_cache()
 if len(sys.argv) > 1:
     with open(sys.argv[1], "w") as f:
