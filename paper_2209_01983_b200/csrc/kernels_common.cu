@@ -436,9 +436,12 @@ int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st)
 // then the paper's shear / yield loop body (association as written there) once per
 // material with that material's constants (Fig. 6b's "do m=1, nmats"; one set when
 // the context has no material axis).  Material m's outputs at sh / y + m * mstride.
+#ifndef SALE_MB_STEIN_L  // Lagrange Steinberg kernel: resident 256-thread blocks per SM (64 registers)
+#define SALE_MB_STEIN_L 4
+#endif
 template <bool EULER, int NM>  // NM: materials (0: no material axis, one parameter set)
-__global__ void __launch_bounds__(256) k_steinberg(Slab s, Phys p, int cur, SteinbergSet set, const double* eps,
-                                                   double* sh, double* y, long long mstride)
+__device__ __forceinline__ void steinberg_cells(const Slab& s, const Phys& p, int cur, const SteinbergSet& set,
+                                                const double* eps, double* sh, double* y, long long mstride)
 {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long total = s.pc * (s.k1 - s.k0);
@@ -498,6 +501,21 @@ __global__ void __launch_bounds__(256) k_steinberg(Slab s, Phys p, int cur, Stei
         y[t + a * mstride] = ((h < sp.Ymax) ? h : sp.Ymax) * (G / sp.G0);
     }
 }
+// Euler: V from the target tables (light); Lagrange: V from the 8 moved nodes, sized for
+// four blocks per SM (C3 1.34 -> 1.21 ms per call with a strain field, scripts/ab_steinberg.py)
+template <int NM>
+__global__ void __launch_bounds__(256) k_steinberg_e(Slab s, Phys p, int cur, SteinbergSet set, const double* eps,
+                                                     double* sh, double* y, long long mstride)
+{
+    steinberg_cells<true, NM>(s, p, cur, set, eps, sh, y, mstride);
+}
+template <int NM>
+__global__ void __launch_bounds__(256, SALE_MB_STEIN_L) k_steinberg_l(Slab s, Phys p, int cur, SteinbergSet set,
+                                                                      const double* eps, double* sh, double* y,
+                                                                      long long mstride)
+{
+    steinberg_cells<false, NM>(s, p, cur, set, eps, sh, y, mstride);
+}
 
 int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& set, const double* eps, double* sh,
                      double* y, long long mstride, Stream st)
@@ -505,16 +523,16 @@ int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& 
     const long long n = s.pc * (s.k1 - s.k0);
     auto go = [&](auto kern) { kern<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, set, eps, sh, y, mstride); note_launch(); };
     switch (s.nmat * 2 + (p.rezone ? 1 : 0)) {
-    case 0: go(k_steinberg<false, 0>); break;
-    case 1: go(k_steinberg<true, 0>); break;
-    case 2: go(k_steinberg<false, 1>); break;
-    case 3: go(k_steinberg<true, 1>); break;
-    case 4: go(k_steinberg<false, 2>); break;
-    case 5: go(k_steinberg<true, 2>); break;
-    case 6: go(k_steinberg<false, 3>); break;
-    case 7: go(k_steinberg<true, 3>); break;
-    case 8: go(k_steinberg<false, 4>); break;
-    default: go(k_steinberg<true, 4>); break;
+    case 0: go(k_steinberg_l<0>); break;
+    case 1: go(k_steinberg_e<0>); break;
+    case 2: go(k_steinberg_l<1>); break;
+    case 3: go(k_steinberg_e<1>); break;
+    case 4: go(k_steinberg_l<2>); break;
+    case 5: go(k_steinberg_e<2>); break;
+    case 6: go(k_steinberg_l<3>); break;
+    case 7: go(k_steinberg_e<3>); break;
+    case 8: go(k_steinberg_l<4>); break;
+    default: go(k_steinberg_e<4>); break;
     }
     return 1;
 }
