@@ -9,9 +9,12 @@
  * below cites the §8(c) item it follows.  Loops are whole-mesh, one step at a
  * time, in the order c.3 / c.4 lists them; no blocking or fusion.
  *
- * Parity status of each part: see DESIGN.md §4 (pins) -- "parity unpinned"
- * items are listed there (absolute discretisation error beyond the Sedov
- * radius/symmetry checks; long-time C1 behaviour without hourglass control).
+ * Parity status of each part: see DESIGN.md §4 (pins).  "Parity unpinned" there:
+ * the absolute discretisation error beyond the Sedov radius / symmetry checks and
+ * the exact-solution comparisons of the Sod / Noh problems; the value hg = 0.5 of
+ * the hourglass coefficient (reading HG: any value in [0.2, 1] runs C1); the
+ * Lagrangian Sedov peak density (about 12 against the strong-shock bound 6).
+ * The readings of round 2 (HG, DT-Q, DT-C) are pinned by tests/test_oracle_readings_r2.py.
  *
  * Compile: gcc -O2 -ffp-contract=off (no FMA contraction, no fast-math).
  * The whole-mesh loops carry OpenMP work-sharing pragmas that only a -fopenmp
