@@ -116,12 +116,16 @@ def main():
 
     if full:  # BASELINE configs against the oracle's golden digests
         gold = os.path.join(ROOT, "tests", "golden")
-        for name in ("C1", "C2", "C2M2", "C3", "C4n2"):
-            path = os.path.join(gold, f"{name}.json")
+        # (and C3 / C4n2 once more with the peer-store halo)
+        for name in ("C1", "C2", "C2M2", "C3", "C4n2", "C3-peer", "C4n2-peer"):
+            base = name.split("-")[0]
+            path = os.path.join(gold, f"{base}.json")
             if not os.path.exists(path):
                 continue
             g = json.load(open(path))
-            cfg, _ = config(name.split("n")[0], int(name.split("n")[1]) if "n" in name else 1)
+            cfg, _ = config(base.split("n")[0], int(base.split("n")[1]) if "n" in base else 1)
+            if name.endswith("-peer"):
+                cfg = dict(cfg, halo=S.HALO_PEER)
             rc, done, clk, glob = run_case(name, cfg, g["requested_cycles"], world, rank, local,
                                            mat_halves=bool(cfg.get("nmat")))
             if rank == 0:
