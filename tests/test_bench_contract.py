@@ -37,4 +37,6 @@ def test_gpu_arm_line():
     assert r["bound"] == "alu" and 0 < r["frac"] < 1.2 and r["peak"] > 10
     assert d["gpu_launches"] >= 4 * 5
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    job = d["e2e"]["job"]  # the whole C4 job through the API, state from / to pinned host
+    assert job["cycles"] == 100 and job["value"] > 0 and job["h2d_bytes"] == d["e2e"]["h2d_bytes_per_step"]
     assert "workload" in d["config"]
