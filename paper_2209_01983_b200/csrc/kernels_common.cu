@@ -439,6 +439,45 @@ int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st)
 #ifndef SALE_MB_STEIN_L  // Lagrange Steinberg kernel: resident 256-thread blocks per SM (64 registers)
 #define SALE_MB_STEIN_L 4
 #endif
+#ifndef SALE_STEIN_ZMARCH  // Lagrange Steinberg as a z-march with shared faces (k_steinberg_zl)
+#define SALE_STEIN_ZMARCH 1
+#endif
+// the Steinberg formulas of owned cell t (local index c) with volume V
+template <int NM>
+__device__ __forceinline__ void steinberg_tail(const Slab& s, const Phys& p, int cur, const SteinbergSet& set,
+                                               const double* eps, double* sh, double* y, long long mstride,
+                                               long long t, long long c, double V, const double* hconst)
+{
+    const double m = mass_cur(s, p, cur)[c];
+    double rho = ddiv(m, V), pr, pf, cs, e;
+    if constexpr (NM > 0) {  // the mixed closure and the mixture's specific energy (as get_field P / E)
+        double pfk[MAX_MAT];
+        mix_eos_t<NM>(s, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, pf, cs, pfk);
+        const double* mk = mat_m(s, p, cur);
+        double sum = 0.0;
+#pragma unroll
+        for (int a = 0; a < NM; ++a) {
+            const double tt = mk[c + a * mat_stride(s)] * s.me[cur][c + a * mat_stride(s)];
+            sum = (a == 0) ? tt : sum + tt;
+        }
+        e = ddiv(sum, m);
+    } else {
+        e = s.e[cur][c];
+        eos(p.gamma, rho, e, pr, pf, cs);
+    }
+    const double ep = eps ? eps[t] : 0.0;
+#pragma unroll
+    for (int a = 0; a < (NM > 0 ? NM : 1); ++a) {
+        const SteinbergP& sp = set.m[a];
+        const double eta = sp.rho0 / rho;
+        const double T = e / sp.cv;
+        // eta^(1/3): cbrt (within an ulp of the paper's pow(eta, 1/3), at a fraction of its cost)
+        const double G = (sp.G0 + (sp.GP * pr) * cbrt(eta)) + sp.GT * (T - sp.T0);
+        const double h = eps ? sp.Y0 * pow(1.0 + sp.beta * ep, sp.n) : hconst[a];
+        sh[t + a * mstride] = G;
+        y[t + a * mstride] = ((h < sp.Ymax) ? h : sp.Ymax) * (G / sp.G0);
+    }
+}
 template <bool EULER, int NM>  // NM: materials (0: no material axis, one parameter set)
 __device__ __forceinline__ void steinberg_cells(const Slab& s, const Phys& p, int cur, const SteinbergSet& set,
                                                 const double* eps, double* sh, double* y, long long mstride)
@@ -471,36 +510,9 @@ __device__ __forceinline__ void steinberg_cells(const Slab& s, const Phys& p, in
         hex_faces(N, A, Xb, sv);
         V = vol_from_s(sv);
     }
-    const double m = mass_cur(s, p, cur)[c];
-    double rho = ddiv(m, V), pr, pf, cs, e;
-    if constexpr (NM > 0) {  // the mixed closure and the mixture's specific energy (as get_field P / E)
-        double pfk[MAX_MAT];
-        mix_eos_t<NM>(s, mat_f(s, p, cur), mat_m(s, p, cur), s.me[cur], c, mat_stride(s), V, rho, pr, pf, cs, pfk);
-        const double* mk = mat_m(s, p, cur);
-        double sum = 0.0;
-#pragma unroll
-        for (int a = 0; a < NM; ++a) {
-            const double tt = mk[c + a * mat_stride(s)] * s.me[cur][c + a * mat_stride(s)];
-            sum = (a == 0) ? tt : sum + tt;
-        }
-        e = ddiv(sum, m);
-    } else {
-        e = s.e[cur][c];
-        eos(p.gamma, rho, e, pr, pf, cs);
-    }
-    const double ep = eps ? eps[t] : 0.0;
-#pragma unroll
-    for (int a = 0; a < (NM > 0 ? NM : 1); ++a) {
-        const SteinbergP& sp = set.m[a];
-        const double eta = sp.rho0 / rho;
-        const double T = e / sp.cv;
-        // eta^(1/3): cbrt (within an ulp of the paper's pow(eta, 1/3), at a fraction of its cost)
-        const double G = (sp.G0 + (sp.GP * pr) * cbrt(eta)) + sp.GT * (T - sp.T0);
-        const double h = eps ? sp.Y0 * pow(1.0 + sp.beta * ep, sp.n) : hconst[a];
-        sh[t + a * mstride] = G;
-        y[t + a * mstride] = ((h < sp.Ymax) ? h : sp.Ymax) * (G / sp.G0);
-    }
+    steinberg_tail<NM>(s, p, cur, set, eps, sh, y, mstride, t, c, V, hconst);
 }
+
 // Euler: V from the target tables (light); Lagrange: V from the 8 moved nodes, sized for
 // four blocks per SM (C3 1.34 -> 1.21 ms per call with a strain field, scripts/ab_steinberg.py)
 template <int NM>
@@ -509,6 +521,79 @@ __global__ void __launch_bounds__(256) k_steinberg_e(Slab s, Phys p, int cur, St
 {
     steinberg_cells<true, NM>(s, p, cur, set, eps, sh, y, mstride);
 }
+// Lagrange as a z-march (kl_state's face sharing): a 32 x 8 CTA stages node planes of
+// x in shared memory and forms the s of the x- / y-face anchored at each column once per
+// plane (the z-face carried in a register), so a cell's V = vol_from_s of its six faces
+// costs three face evaluations instead of six, and its nodes are loaded once per column
+// instead of eight times per cell.  The faces' node order and expressions are
+// hex_faces' (c.2), so V is the same bits as the thread-per-cell kernel's.
+template <int NM>
+__global__ void __launch_bounds__(256) k_steinberg_zl(Slab s, Phys p, int cur, SteinbergSet set, const double* eps,
+                                                      double* sh, double* y, long long mstride, int zchunk)
+{
+    constexpr int FWS = 32, NWS = 8, PLS = NWS * FWS, PADS = FWS + 1, TXS = FWS - 1, TYS = NWS - 1;
+    constexpr int OSS = 6 * PLS;  // node slots: x (3) of 2 planes; then s of the x-face, y-face
+    __shared__ double sm[OSS + 2 * PLS + 2 * PADS];
+    __shared__ double hconst[MAX_MAT];
+    if (!eps) {
+        if (threadIdx.y == 0 && threadIdx.x < (NM > 0 ? NM : 1)) {
+            const SteinbergP& sp = set.m[threadIdx.x];
+            hconst[threadIdx.x] = sp.Y0 * pow(1.0 + sp.beta * 0.0, sp.n);
+        }
+    }
+    const int ix = threadIdx.x, iy = threadIdx.y;
+    double* me = sm + PADS + iy * FWS + ix;
+    const int i = blockIdx.x * TXS + ix, j = blockIdx.y * TYS + iy;
+    const int za = s.k0 + zchunk_base(zchunk);
+    const int zb = za + zchunk - 1 < s.k1 - 1 ? za + zchunk - 1 : s.k1 - 1;
+    const int in = i < p.nx ? i : p.nx, jn = j < p.ny ? j : p.ny;
+    const long long nbc = (long long)in + (long long)(p.nx + 1) * (jn - (long long)(p.ny + 1) * s.kb);
+    const bool out_cell = i < p.nx && j < p.ny && ix < TXS && iy < TYS;
+    auto fetch = [&](int k) { return ld3(s.x[cur], nbc + (long long)k * s.pn); };  // node planes [za, zb+1] exist
+    auto put = [&](int par, D3 v) {
+        double* q = me + par * 3 * PLS;
+        q[0] = v.x;
+        q[PLS] = v.y;
+        q[2 * PLS] = v.z;
+    };
+    auto X = [&](int par, int off) {
+        const double* q = me + off + par * 3 * PLS;
+        return D3{q[0], q[PLS], q[2 * PLS]};
+    };
+    auto zs_of = [&](int par) {  // s of the z-face at this column: (i,j) (i+1,j) (i+1,j+1) (i,j+1)
+        const D3 T0 = X(par, 0), T1 = X(par, 1), T2 = X(par, FWS + 1), T3 = X(par, FWS);
+        return face_s(avg4(T0, T1, T2, T3), face_area(T0, T1, T2, T3));
+    };
+    D3 px = fetch(za);
+    put(za & 1, px);
+    px = fetch(za + 1);
+    __syncthreads();
+    double zs = zs_of(za & 1);
+    for (int kz = za; kz <= zb; ++kz) {
+        const int b0 = kz & 1, b1 = b0 ^ 1;
+        put(b1, px);  // node plane kz+1
+        if (kz < zb) px = fetch(kz + 2);
+        __syncthreads();
+        const double zsn = zs_of(b1);
+        {
+            // x-face at node plane i: (i,j,kz) (i,j+1,kz) (i,j+1,kz+1) (i,j,kz+1)
+            const D3 Q0 = X(b0, 0), Q1 = X(b0, FWS), Q2 = X(b1, FWS), Q3 = X(b1, 0);
+            me[OSS] = face_s(avg4(Q0, Q1, Q2, Q3), face_area(Q0, Q1, Q2, Q3));
+            // y-face at node plane j: (i,j,kz) (i,j,kz+1) (i+1,j,kz+1) (i+1,j,kz)
+            const D3 R2 = X(b1, 1), R3 = X(b0, 1);
+            me[OSS + PLS] = face_s(avg4(Q0, Q3, R2, R3), face_area(Q0, Q3, R2, R3));
+        }
+        __syncthreads();
+        if (out_cell) {
+            const double sv[6] = {me[OSS], me[1 + OSS], me[OSS + PLS], me[FWS + OSS + PLS], zs, zsn};
+            const long long t = (long long)(kz - s.k0) * s.pc + (long long)j * p.nx + i;
+            steinberg_tail<NM>(s, p, cur, set, eps, sh, y, mstride, t, cidx(s, p, i, j, kz), vol_from_s(sv), hconst);
+        }
+        zs = zsn;
+        __syncthreads();
+    }
+}
+
 template <int NM>
 __global__ void __launch_bounds__(256, SALE_MB_STEIN_L) k_steinberg_l(Slab s, Phys p, int cur, SteinbergSet set,
                                                                       const double* eps, double* sh, double* y,
@@ -522,6 +607,24 @@ int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& 
 {
     const long long n = s.pc * (s.k1 - s.k0);
     auto go = [&](auto kern) { kern<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, set, eps, sh, y, mstride); note_launch(); };
+    if (SALE_STEIN_ZMARCH && !p.rezone) {  // Lagrange: the z-march kernel
+        const int planes = s.k1 - s.k0;
+        const long long xy = (long long)((p.nx + 30) / 31) * ((p.ny + 6) / 7);
+        const int zc = zchunk_for(xy, planes, 32);
+        const dim3 grid((p.nx + 30) / 31, (p.ny + 6) / 7, (planes + zc - 1) / zc);
+        auto gz = [&](auto kern) {
+            kern<<<grid, dim3(32, 8), 0, (cudaStream_t)st>>>(s, p, cur, set, eps, sh, y, mstride, zorder(zc));
+            note_launch();
+        };
+        switch (s.nmat) {
+        case 0: gz(k_steinberg_zl<0>); break;
+        case 1: gz(k_steinberg_zl<1>); break;
+        case 2: gz(k_steinberg_zl<2>); break;
+        case 3: gz(k_steinberg_zl<3>); break;
+        default: gz(k_steinberg_zl<4>); break;
+        }
+        return 1;
+    }
     switch (s.nmat * 2 + (p.rezone ? 1 : 0)) {
     case 0: go(k_steinberg_l<0>); break;
     case 1: go(k_steinberg_e<0>); break;
