@@ -436,12 +436,6 @@ int launch_derive(const Slab& s, const Phys& p, int cur, int field, Stream st)
 // then the paper's shear / yield loop body (association as written there) once per
 // material with that material's constants (Fig. 6b's "do m=1, nmats"; one set when
 // the context has no material axis).  Material m's outputs at sh / y + m * mstride.
-#ifndef SALE_MB_STEIN_L  // Lagrange Steinberg kernel: resident 256-thread blocks per SM (64 registers)
-#define SALE_MB_STEIN_L 4
-#endif
-#ifndef SALE_STEIN_ZMARCH  // Lagrange Steinberg as a z-march with shared faces (k_steinberg_zl)
-#define SALE_STEIN_ZMARCH 1
-#endif
 // the Steinberg formulas of owned cell t (local index c) with volume V
 template <int NM>
 __device__ __forceinline__ void steinberg_tail(const Slab& s, const Phys& p, int cur, const SteinbergSet& set,
@@ -500,21 +494,12 @@ __device__ __forceinline__ void steinberg_cells(const Slab& s, const Phys& p, in
     const long long r = t % s.pc;
     const int j = (int)(r / p.nx), i = (int)(r % p.nx);
     const long long c = cidx(s, p, i, j, k);
-    double V;
-    if (EULER) {
-        V = s.VT[c];  // the fixed mesh's volume (same formula, evaluated at create)
-    } else {
-        D3 N[8], A[6], Xb[6];
-        double sv[6];
-        load_hex_pos<EULER>(s, p, cur, i, j, k, N);
-        hex_faces(N, A, Xb, sv);
-        V = vol_from_s(sv);
-    }
+    static_assert(EULER, "Lagrange runs k_steinberg_zl");
+    const double V = s.VT[c];  // the fixed mesh's volume (same formula, evaluated at create)
     steinberg_tail<NM>(s, p, cur, set, eps, sh, y, mstride, t, c, V, hconst);
 }
 
-// Euler: V from the target tables (light); Lagrange: V from the 8 moved nodes, sized for
-// four blocks per SM (C3 1.34 -> 1.21 ms per call with a strain field, scripts/ab_steinberg.py)
+// Euler: V from the target tables (light)
 template <int NM>
 __global__ void __launch_bounds__(256) k_steinberg_e(Slab s, Phys p, int cur, SteinbergSet set, const double* eps,
                                                      double* sh, double* y, long long mstride)
@@ -594,20 +579,12 @@ __global__ void __launch_bounds__(256) k_steinberg_zl(Slab s, Phys p, int cur, S
     }
 }
 
-template <int NM>
-__global__ void __launch_bounds__(256, SALE_MB_STEIN_L) k_steinberg_l(Slab s, Phys p, int cur, SteinbergSet set,
-                                                                      const double* eps, double* sh, double* y,
-                                                                      long long mstride)
-{
-    steinberg_cells<false, NM>(s, p, cur, set, eps, sh, y, mstride);
-}
-
 int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& set, const double* eps, double* sh,
                      double* y, long long mstride, Stream st)
 {
     const long long n = s.pc * (s.k1 - s.k0);
     auto go = [&](auto kern) { kern<<<grid_for(n, 256), 256, 0, (cudaStream_t)st>>>(s, p, cur, set, eps, sh, y, mstride); note_launch(); };
-    if (SALE_STEIN_ZMARCH && !p.rezone) {  // Lagrange: the z-march kernel
+    if (!p.rezone) {  // Lagrange: the z-march kernel
         const int planes = s.k1 - s.k0;
         const long long xy = (long long)((p.nx + 30) / 31) * ((p.ny + 6) / 7);
         const int zc = zchunk_for(xy, planes, 32);
@@ -625,16 +602,11 @@ int launch_steinberg(const Slab& s, const Phys& p, int cur, const SteinbergSet& 
         }
         return 1;
     }
-    switch (s.nmat * 2 + (p.rezone ? 1 : 0)) {
-    case 0: go(k_steinberg_l<0>); break;
-    case 1: go(k_steinberg_e<0>); break;
-    case 2: go(k_steinberg_l<1>); break;
-    case 3: go(k_steinberg_e<1>); break;
-    case 4: go(k_steinberg_l<2>); break;
-    case 5: go(k_steinberg_e<2>); break;
-    case 6: go(k_steinberg_l<3>); break;
-    case 7: go(k_steinberg_e<3>); break;
-    case 8: go(k_steinberg_l<4>); break;
+    switch (s.nmat) {  // Euler: one thread per cell (V from the target tables)
+    case 0: go(k_steinberg_e<0>); break;
+    case 1: go(k_steinberg_e<1>); break;
+    case 2: go(k_steinberg_e<2>); break;
+    case 3: go(k_steinberg_e<3>); break;
     default: go(k_steinberg_e<4>); break;
     }
     return 1;

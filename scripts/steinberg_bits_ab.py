@@ -1,3 +1,7 @@
+"""Bitwise comparison of sale_steinberg's outputs between two library builds (experiments
+only; e.g. the thread-per-cell Lagrange kernel of commit 99c0249 vs k_steinberg_zl): C3 after 3
+cycles, a perturbed 2-slab Lagrangian mesh, a 2-material mesh; with and without a strain
+field.  usage: python scripts/steinberg_bits_ab.py lib_a.so lib_b.so"""
 import os, subprocess, sys, numpy as np
 CH = r'''
 import sys, numpy as np, torch
