@@ -123,6 +123,23 @@ def test_hourglass_corner_forces_conserve_momentum_and_dissipate():
         assert P <= 0.0
 
 
+def test_cell_energy_hourglass_heat_closed_form():
+    """Reading HG in the compatible energy (the per-cell entry point): on the unit cube
+    with a pure xi*eta*zeta mode u_h = Gamma_3(h) v (u' = u, dyadic values, so every
+    operation is exact), the pressure work W = sum_h C_h . ubar_h is 0 (C_h = (xi, eta,
+    zeta), orthogonal to the mode), g_3 = 8 v, f_h = -8 nu Gamma_3(h) v, and the
+    hourglass work W_hg = sum_h f_h . ubar_h = -64 nu |v|^2: the cell heats by
+    64 nu |v|^2 dt / m.  (scripts/oracle_mutations.py found the entry point's W_hg
+    otherwise unpinned.)"""
+    N0 = np.array([[float(a), float(b), float(c)] for (a, b, c) in CORNERS])
+    v = np.array([0.25, -0.5, 0.75])
+    U = np.array([gamma(3, h) * v for h in range(8)])
+    nu, sigma, m, e, dt = 0.375, 0.7, 2.0, 1.0, 0.125
+    e1 = O.cell_energy(N0, U, U, sigma, m, e, dt, nu=nu)
+    assert e1 == e + 64.0 * nu * float(v @ v) * dt / m == 2.3125
+    assert O.cell_energy(N0, U, U, sigma, m, e, dt, nu=0.0) == e  # no damping: W = 0, no heat
+
+
 def _box_cycle(hg, eps=1e-3, dims=(2.0, 1.0, 0.5), e0=2.5, gam=1.4):
     """One free box cell with pressure and an xi*eta*zeta hourglass mode of amplitude
     eps in u_z: returns (g3_z before, after, nu, dt, m, energies before/after)."""
