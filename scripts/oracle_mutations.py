@@ -91,9 +91,9 @@ def run(name, old, new):
                 return {"mutation": name, "error": "pattern not found"}
             open(src, "w").write(text.replace(old, new))
         t0 = time.time()
-        # (a test running past 300 s -- a mutated scheme gone unstable -- counts as a failure)
+        # (a test running past 300 s -- a mutated scheme gone unstable -- ends the run: killed)
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "not gpu", "-p", "no:cacheprovider",
-                            "--timeout", "300", *TESTS],
+                            "--timeout", "300", "--timeout-method", "thread", *TESTS],
                            cwd=d, capture_output=True, text=True, timeout=3600)
         tail = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-300:]
         failed = int(m.group(1)) if (m := re.search(r"(\d+) failed", tail)) else 0
@@ -101,9 +101,12 @@ def run(name, old, new):
         passed = int(m.group(1)) if (m := re.search(r"(\d+) passed", tail)) else 0
         killing = sorted({ln.split("::")[1].split(" ")[0].split("[")[0]
                           for ln in r.stdout.splitlines() if ln.startswith("FAILED ") and "::" in ln})
+        if r.returncode and not killing:  # timed out (the thread method ends the run) or crashed
+            killing = ["(a test ran past the 300-s limit: the mutated scheme does not finish)"
+                       if "Timeout" in r.stdout + r.stderr else "(the run crashed)"]
         return {"mutation": name, "sites": n, "failed": failed, "errors": errors, "passed": passed,
-                "killed": (failed + errors) > 0, "killing_tests": killing, "seconds": round(time.time() - t0, 1),
-                "summary": tail}
+                "killed": r.returncode != 0, "returncode": r.returncode, "killing_tests": killing,
+                "seconds": round(time.time() - t0, 1), "summary": tail[-300:]}
     finally:
         shutil.rmtree(d, ignore_errors=True)
 
