@@ -70,6 +70,19 @@ MUTATIONS = [
      "c->e[0] = p->e_deposit / c->m[0];", "c->e[0] = p->e_deposit;"),
     ("steinberg_eta_exponent", "Fig. 6b: eta^(1/3)",
      "pow(eta, 1.0 / 3.0)", "pow(eta, 1.0 / 2.0)"),
+    # multi-material cells (DESIGN.md §10d readings MM1-MM6)
+    ("mm_material_density", "MM1: rho_m = m_m / (f_m V)",
+     "double rk = mm[k] / (f[k] * V);", "double rk = mm[k] / V;"),
+    ("mm_sound_speed_gamma", "MM1: c = sqrt(sum f_m gamma_m pf_m / rho)",
+     "g = f[k] * (gam[k] * pfk);", "g = f[k] * pfk;"),
+    ("mm_volume_flux", "MM5: phi_m = f_m,D dV",
+     "o->phim[m] = c->mf[m][D] * dV;", "o->phim[m] = (c->mmat[m][D] / c->V1[D]) * dV;"),
+    ("mm_energy_remap", "MM6: e''_m = e'_m + (dE_m - e'_m dm_m) / m''_m",
+     "e1 + ((c->dEm[m][K] - (e1 * c->dmm[m][K])) / mm2)", "e1 + (c->dEm[m][K] / mm2)"),
+    ("mm_fraction_normalisation", "MM6: f''_m = V''_m / sum_k V''_k",
+     "c->mf[m][K] = c->vm2[m][K] / VV;", "c->mf[m][K] = c->vm2[m][K] / c->V1[K];"),
+    ("mm_energy_share", "MM4: each material does the work on its share f_m",
+     "c->e1m[m][K] = em - (((((sm * W) + Wh) * dt) * f) / mm);", "c->e1m[m][K] = em - ((((sm * W) + Wh) * dt) / mm);"),
 ]
 
 
