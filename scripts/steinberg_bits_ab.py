@@ -8,15 +8,19 @@ import sys, numpy as np, torch
 sys.path.insert(0, "/root/repo")
 from paper_2209_01983_b200.configs import config, sedov, LAGRANGE
 from paper_2209_01983_b200.sale import Sale
-from tests.helpers import apply_perturbation
-import oracle as O
+from paper_2209_01983_b200 import inputs
 prm = dict(G0=0.43, GP=1.7, GT=0.3, Y0=0.2, Ymax=0.9, beta=3.0, n=0.5, cv=0.8, rho0=1.1, T0=0.05)
 out = {}
 for name, cfg in (("C3", config("C3")[0]), ("P", sedov((37, 23, 29), LAGRANGE, e_background=0.3)),
                   ("M", sedov((21, 17, 19), LAGRANGE, nmat=2, mat_gamma=[1.4, 1.6]))):
     g = Sale(cfg, local_slabs=2 if name == "P" else 1)
-    if name == "P":
-        o = O.Oracle(cfg); apply_perturbation([o, g], cfg, 3, lagrange=True)
+    if name == "P":  # the seeded perturbed state P3 (inputs.perturbation), applied to the GPU state itself
+        pert = inputs.perturbation(cfg, 3)
+        for f, d in (("X", "dx"), ("Y", "dy"), ("Z", "dz")):
+            g.set(f, g.get(f) + pert[d])
+        for f in ("UX", "UY", "UZ"):
+            g.set(f, pert[f.lower()])
+        g.set("E", g.get("E") * pert["e_factor"])
     g.step(3)
     eps = torch.rand(g.cell_shape, dtype=torch.float64, device=g.torch_device, generator=torch.Generator(device="cuda").manual_seed(1))
     for tag, e in (("f", eps), ("n", None)):
