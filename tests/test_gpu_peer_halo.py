@@ -10,6 +10,7 @@ import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 import oracle as O
@@ -116,3 +117,28 @@ def test_peer_halo_full_length_digest(name, slabs):
     bad = [f for f, ref in g["fields"].items()
            if hashlib.sha256(ctx.get(f).ravel().tobytes()).hexdigest() != ref["sha256"]]
     assert not bad, bad
+
+
+def test_peer_halo_error_paths_same_cycle_and_cell():
+    """Errors with the peer-store halo on emulated slabs: a tangled cell in the upper slab
+    (Lagrange) and ENEGMASS from a CFL-1.5 uniform translation over alternating
+    densities (Euler) -- the oracle's status, good-cycle count, cell and clock."""
+    from paper_2209_01983_b200.sale import HALO_PEER
+    cfg = sedov((4, 4, 8), LAGRANGE)
+    g, o = _sale(dict(cfg, halo=HALO_PEER), local_slabs=2), O.Oracle(cfg)
+    X = o.get("X")
+    X[6, 2, 2] += 2.0  # a node of the upper slab
+    for c in (g, o):
+        c.set("X", X)
+    assert g.step(3) == o.step(3) == (O.ETANGLED, 0)
+    assert o.last_error().split()[-1] in g.last_error()
+    cfg = sedov((7, 6, 9), EULER, cfl=1.5, reflect_mask=0, e_deposit=0.0, e_background=1e-6)
+    g, o = _sale(dict(cfg, halo=HALO_PEER), local_slabs=3), O.Oracle(cfg)
+    m = o.get("MASS") * np.where((np.arange(7) % 2) == 0, 1.0, 0.05)[None, None, :]
+    for c in (g, o):
+        c.set("UX", np.ones(o.node_shape))
+        c.set("MASS", m)
+    rg, ro = g.step(20), o.step(20)
+    assert rg == ro and ro[0] == O.ENEGMASS, (rg, ro)
+    assert o.last_error().split()[-1] in g.last_error()
+    assert g.clock() == o.clock()
